@@ -1,0 +1,284 @@
+"""Pins of the oracle's environment dynamics, rewards and done rules (rows A3, A4).
+
+CartPole, Acrobot, Pendulum (BJ:9, Q24),
+Mueller-Brown / surface-D (Q23) and Tag (Q22) are
+checked against closed forms, Lagrangian mechanics derived independently in
+tests/mechanics.py, a library ODE solver, published stationary points and the SPEC rule
+examples -- never against a re-typed copy of the oracle's own formulas.
+"""
+import math
+from fractions import Fraction
+
+import numpy as np
+import pytest
+from scipy import integrate, optimize
+
+import mechanics as mech
+from conftest import golden_rows
+
+f32 = np.float32
+
+
+# ----------------------------------------------------------------------------- CartPole
+def test_cartpole_closed_form_from_rest(oracle):
+    for row in golden_rows("cartpole_closed_form.txt"):
+        a = int(row[0])
+        want = [float(Fraction(x)) for x in row[2:6]]
+        st, out, r, term = oracle.cartpole_step([0, 0, 0, 0], a, f64=True)
+        assert st == 0 and r == 1.0 and not term
+        np.testing.assert_allclose(out, want, rtol=0, atol=1e-15)
+        st, out32, r32, term32 = oracle.cartpole_step([0, 0, 0, 0], a)
+        # fp32 parity mode: every component within 2 ulp of the exact rational
+        for got, w in zip(out32, want):
+            assert abs(float(got) - w) <= 2 * np.spacing(f32(abs(w)) if w else f32(0))
+    # SPEC.md:233 signs
+    _, out, r, term = oracle.cartpole_step([0, 0, 0, 0], 1)
+    assert out[1] > 0 and out[3] < 0 and r == 1.0 and not term
+
+
+def test_cartpole_matches_lagrangian_mechanics(oracle):
+    """Explicit Euler of the cart-pole Euler-Lagrange equations."""
+    T, V = mech.cartpole_TV()
+    rng = np.random.default_rng(5)
+    tau = 0.02
+    for _ in range(60):
+        s = rng.uniform([-2, -2, -0.2, -2], [2, 2, 0.2, 2])
+        a = int(rng.integers(0, 2))
+        F = 10.0 if a == 1 else -10.0
+        xacc, thacc = mech.accelerations(T, V, [s[0], s[2]], [s[1], s[3]], [F, 0.0])
+        st, out, r, term = oracle.cartpole_step(s, a, f64=True)
+        assert st == 0
+        assert out[0] == s[0] + tau * s[1] and out[2] == s[2] + tau * s[3]
+        np.testing.assert_allclose((out[1] - s[1]) / tau, xacc, rtol=1e-7, atol=1e-7)
+        np.testing.assert_allclose((out[3] - s[3]) / tau, thacc, rtol=1e-7, atol=1e-7)
+        # fp32 parity mode is the same step up to fp32 rounding
+        _, o32, _, _ = oracle.cartpole_step(s.astype(f32), a)
+        np.testing.assert_allclose(o32, out, rtol=2e-5, atol=2e-6)
+
+
+def test_cartpole_thresholds_exact(oracle):
+    """Done exactly at the fp32 thresholds (reading Q6)."""
+    th = f32(12 * 2 * math.pi / 360)
+    xt = f32(2.4)
+    up = lambda v: np.nextafter(f32(v), f32(np.inf))
+    dn = lambda v: np.nextafter(f32(v), f32(-np.inf))
+    # velocities zero so that the post-step positions equal the pre-step ones
+    assert not oracle.cartpole_step([0, 0, th, 0], 0)[3]
+    assert oracle.cartpole_step([0, 0, up(th), 0], 0)[3]
+    assert not oracle.cartpole_step([0, 0, -th, 0], 0)[3]
+    assert oracle.cartpole_step([0, 0, dn(-th), 0], 0)[3]
+    assert not oracle.cartpole_step([xt, 0, 0, 0], 0)[3]
+    assert oracle.cartpole_step([up(xt), 0, 0, 0], 0)[3]
+    assert oracle.cartpole_step([dn(-xt), 0, 0, 0], 1)[3]
+    # theta = 0.22 -> done, reward 1.0 on the terminal step
+    st, out, r, term = oracle.cartpole_step([0, 0, 0.22, 0], 1)
+    assert term and r == 1.0
+    # S:231 invalid action
+    assert oracle.cartpole_step([0, 0, 0, 0], 2)[0] == 1
+    assert oracle.cartpole_step([0, 0, 0, 0], -1)[0] == 1
+
+
+# ----------------------------------------------------------------------------- Acrobot
+def test_acrobot_rest_equilibrium(oracle):
+    """hanging rest, zero torque -> unchanged (exactly, with the sin-form Q7)."""
+    for f64 in (False, True):
+        st, out, r, term = oracle.acrobot_step([0, 0, 0, 0], 1, f64=f64)
+        assert st == 0 and r == -1.0 and not term
+        assert np.all(out == 0)
+
+
+def test_acrobot_dsdt_matches_lagrangian(oracle):
+    rng = np.random.default_rng(7)
+    for _ in range(60):
+        s = rng.uniform([-3, -3, -4, -9], [3, 3, 4, 9])
+        tq = float(rng.choice([-1.0, 0.0, 1.0]))
+        d = oracle.acrobot_dsdt(s, tq)
+        ref = mech.acrobot_rhs(s, tq)
+        np.testing.assert_allclose(d, ref, rtol=1e-7, atol=1e-7)
+
+
+def test_acrobot_rk4_step(oracle):
+    """One step = classical RK4 over dt = 0.2 of the Lagrangian dynamics:
+    (a) equals textbook RK4 built on the independent right-hand side, (b) is within the
+    RK4 local-error bound of a tight library ODE solution."""
+    rng = np.random.default_rng(9)
+    dt = 0.2
+    for _ in range(25):
+        s = rng.uniform([-1, -1, -1, -1], [1, 1, 1, 1])
+        a = int(rng.integers(0, 3))
+        tq = [-1.0, 0.0, 1.0][a]
+        f = lambda y: mech.acrobot_rhs(y, tq)
+        k1 = f(s); k2 = f(s + dt / 2 * k1); k3 = f(s + dt / 2 * k2); k4 = f(s + dt * k3)
+        rk4 = s + dt / 6 * (k1 + 2 * k2 + 2 * k3 + k4)
+        st, out, r, term = oracle.acrobot_step(s, a, f64=True)
+        assert st == 0
+        np.testing.assert_allclose(out, rk4, rtol=1e-7, atol=1e-7)
+        sol = integrate.solve_ivp(lambda t, y: f(y), (0, dt), s, method="DOP853", rtol=1e-12, atol=1e-12)
+        assert np.max(np.abs(out - sol.y[:, -1])) < 5e-3  # O(dt^5) local error; Euler would be ~1e-1
+        # fp32 mode tracks the fp64 step
+        _, o32, _, _ = oracle.acrobot_step(s.astype(f32), a)
+        np.testing.assert_allclose(o32, out, rtol=1e-5, atol=1e-5)
+
+
+def test_acrobot_energy_conserved_without_torque(oracle):
+    rng = np.random.default_rng(3)
+    for _ in range(10):
+        s = rng.uniform([-0.5, -0.5, -0.5, -0.5], [0.5, 0.5, 0.5, 0.5])
+        H0 = mech.acrobot_energy(s)
+        for _ in range(5):
+            _, s, _, _ = oracle.acrobot_step(s, 1, f64=True)
+        assert abs(mech.acrobot_energy(s) - H0) < 1e-3 * (1 + abs(H0))
+
+
+def test_acrobot_terminal_wrap_bound(oracle):
+    # -cos(t1) - cos(t1 + t2) = 1.2 -> done ; 0.8 -> not done
+    for target, want in ((1.2, True), (0.8, False), (1.0 + 1e-3, True)):
+        # t2 = 0: -2 cos t1 = target
+        t1 = math.acos(-target / 2)
+        assert oracle.acrobot_terminal([t1, 0.0, 0.0, 0.0]) == want
+    # velocity bounds 4 pi, 9 pi; angles wrapped into [-pi, pi] (Q8)
+    st, out, r, term = oracle.acrobot_step([3.1, 3.1, 100.0, -100.0], 1)
+    assert out[2] == f32(4 * math.pi) and out[3] == f32(-9 * math.pi)
+    assert -f32(math.pi) <= out[0] <= f32(math.pi) and -f32(math.pi) <= out[1] <= f32(math.pi)
+    assert oracle.acrobot_step([0, 0, 0, 0], 3)[0] == 1
+
+
+# ----------------------------------------------------------------------------- Pendulum
+def _ev(expr):
+    return float(eval(expr, {"pi": math.pi}))
+
+
+def test_pendulum_closed_forms(oracle):
+    for row in golden_rows("pendulum_closed_form.txt"):
+        th, thd, u = _ev(row[0]), _ev(row[1]), _ev(row[2])
+        want_th, want_thd, want_r = _ev(row[4]), _ev(row[5]), _ev(row[6])
+        st, out, r = oracle.pendulum_step([th, thd], u, f64=True)
+        assert st == 0
+        np.testing.assert_allclose([out[0], out[1], r], [want_th, want_thd, want_r], rtol=1e-12, atol=1e-12)
+        st, o32, r32 = oracle.pendulum_step([th, thd], u)
+        np.testing.assert_allclose([o32[0], o32[1], r32], [want_th, want_thd, want_r], rtol=1e-6, atol=1e-6)
+    # (pi, 0, 0): cost pi^2
+    _, _, r = oracle.pendulum_step([math.pi, 0.0], 0.0, f64=True)
+    assert abs(r + math.pi**2) < 1e-12
+    assert oracle.pendulum_step([0.0, 0.0], float("nan"))[0] == 1
+
+
+# ----------------------------------------------------------------------------- Mueller-Brown
+def test_mueller_brown_stationary_points(oracle):
+    for name, kind, x, y, e in golden_rows("mueller_brown_stationary.txt"):
+        x, y, e = float(x), float(y), float(e)
+        grad = lambda v: np.array(oracle.mb_energy(v[0], v[1])[1:])
+        sol = optimize.root(grad, [x, y], method="lm", tol=1e-15)
+        xs, ys = sol.x
+        assert abs(xs - x) < 2e-3 and abs(ys - y) < 2e-3, name
+        E, gx, gy = oracle.mb_energy(xs, ys)
+        assert abs(E - e) < 0.01, name
+        assert math.hypot(gx, gy) < 1e-6
+        # classify by the Hessian (finite differences of the analytic gradient)
+        h = 1e-5
+        H = np.array([(grad([xs + h, ys]) - grad([xs - h, ys])) / (2 * h),
+                      (grad([xs, ys + h]) - grad([xs, ys - h])) / (2 * h)])
+        ev = np.linalg.eigvalsh(0.5 * (H + H.T))
+        assert (ev > 0).all() if kind == "minimum" else (ev[0] < 0 < ev[1]), name
+
+
+def test_mueller_brown_gradient_vs_finite_differences(oracle):
+    """analytic gradient vs central differences (h = 1e-5), rel. err < 1e-6."""
+    rng = np.random.default_rng(0)
+    h = 1e-5
+    for _ in range(20):
+        x, y = rng.uniform(-1.5, 1.0), rng.uniform(-0.3, 2.0)
+        E, gx, gy = oracle.mb_energy(x, y)
+        fx = (oracle.mb_energy(x + h, y)[0] - oracle.mb_energy(x - h, y)[0]) / (2 * h)
+        fy = (oracle.mb_energy(x, y + h)[0] - oracle.mb_energy(x, y - h)[0]) / (2 * h)
+        assert abs(fx - gx) <= 1e-6 * max(1.0, abs(gx))
+        assert abs(fy - gy) <= 1e-6 * max(1.0, abs(gy))
+
+
+# ----------------------------------------------------------------------------- surface-D
+def test_surface_energy_reduces_to_mueller_brown(oracle):
+    for D in (2, 5, 20):
+        q = np.zeros(D, f32); q[0], q[1] = 0.623499, 0.028038
+        assert oracle.surface_energy(q) == f32(oracle.mb_energy(float(q[0]), float(q[1]))[0])
+    q = np.zeros(20, f32); q[0], q[1] = 0.623499, 0.028038; q[5] = 0.1
+    E1 = oracle.mb_energy(float(q[0]), float(q[1]))[0] + 0.5 * 100 * float(q[5]) ** 2
+    assert oracle.surface_energy(q) == f32(E1)  # spring 1/2 kappa q^2 (Q23)
+
+
+def test_surface_rules(oracle):
+    D = 20
+    q = np.zeros(D, f32); q[0], q[1] = 0.3, 0.4; q[3] = -0.2
+    # zero action -> position unchanged, reward -c_step
+    st, out, r, term = oracle.surface_step(q, np.zeros(D, f32))
+    assert st == 0 and np.array_equal(out, q) and r == f32(-0.1) and not term
+    # action clipped to +-delta per dim, position clipped to the box
+    a = np.full(D, 5.0, f32)
+    st, out, r, term = oracle.surface_step(q, a)
+    np.testing.assert_array_equal(out, q + f32(0.05))
+    qb = q.copy(); qb[0] = 1.19
+    _, out, _, _ = oracle.surface_step(qb, a)
+    assert out[0] == f32(1.2)
+    # stepping into the goal radius -> done, +10 bonus
+    g = np.zeros(D, f32); g[0], g[1] = -0.558224, 1.441726
+    qs = g.copy(); qs[0] += f32(0.12)
+    a = np.zeros(D, f32); a[0] = -0.05
+    st, out, r, term = oracle.surface_step(qs, a)
+    assert term
+    e0, e1 = oracle.surface_energy(qs), oracle.surface_energy(out)
+    assert abs(r - (-(0.01 * (e1 - e0)) - 0.1 + 10.0)) < 1e-5
+    bad = np.zeros(D, f32); bad[4] = np.inf
+    assert oracle.surface_step(q, bad)[0] == 1
+
+
+def test_surface_energy_telescopes(oracle):
+    """sum of the per-step energy terms = w_E (E_start - E_end)."""
+    rng = np.random.default_rng(4)
+    D = 20
+    q = np.zeros(D, f32); q[0], q[1] = 0.623499, 0.028038
+    e_start = oracle.surface_energy(q)
+    acc = 0.0
+    for _ in range(200):
+        a = rng.normal(0, 0.03, D).astype(f32)
+        st, q2, r, term = oracle.surface_step(q, a)
+        acc += float(r) + 0.1 - (10.0 if term else 0.0)
+        q = q2
+    e_end = oracle.surface_energy(q)
+    assert abs(acc - 0.01 * (e_start - e_end)) <= 1e-5 * 200 + 1e-6 * abs(e_start - e_end)
+
+
+# ----------------------------------------------------------------------------- Tag
+def test_tag_spec_examples(oracle):
+    G = 20
+    # tagger at (0,0), runner at (0,1); tagger moves N, runner stays
+    st, x, y, act, rew, term = oracle.tag_step(G, 1, [0, 0], [0, 1], [1, 1], [1, 0])
+    assert st == 0 and (x[0], y[0]) == (0, 1)
+    assert rew[0] == 1.0 and rew[1] == -1.0 and act[1] == 0 and term
+    # two taggers land on one runner -> +0.5 each
+    st, x, y, act, rew, term = oracle.tag_step(G, 2, [0, 2, 1], [1, 1, 1], [1, 1, 1], [3, 4, 0])
+    assert list(rew) == [0.5, 0.5, -1.0] and term
+    # move W at x = 0 -> unchanged (clipped); S at y = 0 too
+    st, x, y, act, rew, term = oracle.tag_step(G, 1, [0, 5], [0, 5], [1, 1], [4, 2])
+    assert (x[0], y[0]) == (0, 0) and (x[1], y[1]) == (5, 4)
+    assert rew[1] == f32(0.01) and rew[0] == 0.0 and not term
+    # frozen inactive runner; invalid action
+    st, x, y, act, rew, term = oracle.tag_step(G, 1, [0, 5, 9], [0, 5, 9], [1, 0, 1], [0, 3, 0])
+    assert (x[1], y[1]) == (5, 5) and rew[1] == 0.0
+    assert oracle.tag_step(G, 1, [0, 1], [0, 1], [1, 1], [5, 0])[0] == 1
+
+
+def test_tag_conservation(oracle):
+    """total tagger reward from tags = -(total runner tag penalty) each step."""
+    rng = np.random.default_rng(2)
+    G, A, nt = 6, 30, 5
+    x = rng.integers(0, G, A); y = rng.integers(0, G, A); active = np.ones(A, np.uint8)
+    for _ in range(40):
+        act = rng.integers(0, 5, A)
+        prev_active = active.copy()
+        st, x, y, active, rew, term = oracle.tag_step(G, nt, x, y, active, act)
+        tagged = (prev_active[nt:] == 1) & (active[nt:] == 0)
+        assert np.all(rew[nt:][tagged] == -1.0)
+        assert abs(float(np.sum(rew[:nt], dtype=np.float64)) - tagged.sum()) <= 1e-6 * max(1, tagged.sum())
+        assert np.all(rew[nt:][(prev_active[nt:] == 1) & ~tagged] == f32(0.01))
+        assert np.all(rew[nt:][prev_active[nt:] == 0] == 0.0)
+        if term:
+            break

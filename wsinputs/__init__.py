@@ -1,0 +1,99 @@
+"""Seeded synthetic inputs shared by the oracle-side tests and the product-side tests and
+bench (the one module both sides may use).  It holds NONE of the method's arithmetic:
+no Philox, no sampling, no dynamics -- only the workload shapes of BASELINE.json's
+configs and numpy-generated policy inputs.
+
+Random numbers the METHOD draws (actions, resets, Gaussian noise) come from the
+counter-based Philox streams each side implements on its own (reading Q15); the numbers
+generated here are only the *given* inputs: probabilities, Gaussian head parameters and
+fixed-action tables.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass, field
+
+import numpy as np
+
+SEED = 0x24080930  # one seed for every config
+
+
+@dataclass(frozen=True)
+class Workload:
+    name: str
+    env: str
+    n_envs: int          # global env count (E_g)
+    n_agents: int
+    T: int
+    n_actions: int       # 0 for continuous
+    act_dim: int
+    params: dict = field(default_factory=dict)   # env params (tag grid/taggers, surface dim)
+    note: str = ""
+
+
+# BASELINE.json configs (BJ:7-11) made concrete
+CONFIGS = {
+    "C1": Workload("C1", "cartpole", 64, 1, 500, 2, 1, note="CartPole-v1 64 envs x 500 steps (BJ:7)"),
+    "C2": Workload("C2", "cartpole", 10000, 1, 1000, 2, 1, note="CartPole-v1 10K envs x 1000 steps (BJ:8)"),
+    "C3a": Workload("C3a", "acrobot", 100000, 1, 500, 3, 1, note="Acrobot-v1 100K envs x 500 (BJ:9)"),
+    "C3b": Workload("C3b", "pendulum", 100000, 1, 200, 0, 1, note="Pendulum-v1 100K envs x 200 (BJ:9)"),
+    "C4": Workload("C4", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10},
+                   note="tag 1K envs x 100 agents x 200 (BJ:10)"),
+    "C5": Workload("C5", "surface", 2000, 1, 200, 0, 20, {"dim": 20},
+                   note="surface-20 2K envs x 200 (BJ:11)"),
+    "D0": Workload("D0", "dummy", 1000000, 1, 100, 2, 1, note="store-write calibration"),
+}
+
+
+def uniform_probs(E: int, A: int, n: int) -> np.ndarray:
+    """Reading Q25: uniform 1/n probabilities, [E, A, n] float32."""
+    return np.full((E, A, n), 1.0 / n, dtype=np.float32)
+
+
+def random_probs(E: int, A: int, n: int, seed: int = SEED, zero_frac: float = 0.0,
+                 T: int | None = None) -> np.ndarray:
+    """Random unnormalised probability rows ([T,]E, A, n) with a fraction of exact zeros
+    (at least one nonzero per row) -- exercises Q13 (rows need not sum to 1, zeros are
+    never drawn)."""
+    rng = np.random.default_rng(seed)
+    shape = (E, A, n) if T is None else (T, E, A, n)
+    p = rng.gamma(0.7, 1.0, size=shape).astype(np.float32)
+    if zero_frac > 0:
+        z = rng.random(shape) < zero_frac
+        p[z] = 0.0
+        flat = p.reshape(-1, n)
+        dead = flat.sum(axis=1) == 0
+        flat[dead, rng.integers(0, n, dead.sum())] = 1.0
+    return p
+
+
+def gaussian_params(E: int, A: int, d: int, mean: float = 0.0, log_std: float = 0.0,
+                    jitter: float = 0.0, seed: int = SEED) -> np.ndarray:
+    """Continuous head input [E, A, 2d] = mean[d] | log_std[d] (reading Q25: Pendulum
+    mean 0, log_std 0; surface mean 0, log_std ln 0.025)."""
+    rng = np.random.default_rng(seed)
+    p = np.empty((E, A, 2 * d), np.float32)
+    p[..., :d] = mean + jitter * rng.standard_normal((E, A, d))
+    p[..., d:] = log_std + jitter * rng.standard_normal((E, A, d))
+    return p
+
+
+def action_table(T: int, E: int, A: int, n: int, seed: int = SEED, p1: float | None = None) -> np.ndarray:
+    """Fixed-action parity table [T, E, A] int32 (reading Q27)."""
+    rng = np.random.default_rng(seed)
+    if p1 is not None and n == 2:
+        return (rng.random((T, E, A)) < p1).astype(np.int32)
+    return rng.integers(0, n, size=(T, E, A), dtype=np.int32)
+
+
+def continuous_action_table(T: int, E: int, A: int, d: int, scale: float, seed: int = SEED) -> np.ndarray:
+    rng = np.random.default_rng(seed)
+    return (scale * rng.standard_normal((T, E, A, d))).astype(np.float32)
+
+
+def workload_probs(w: Workload) -> np.ndarray:
+    """The bench / parity input of a config: per-env given probabilities, step stride 0."""
+    if w.n_actions:
+        return uniform_probs(w.n_envs, w.n_agents, w.n_actions)
+    if w.env == "surface":
+        return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, float(np.log(0.025)))
+    return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, 0.0)
