@@ -1,0 +1,290 @@
+"""bench.py -- env-steps/s of the fused roll-out step on B200 (BASELINE.json metric).
+
+    python bench.py [--gpus N] [--steps K] [--warmup W] [--impl {ours,reference}] [--workload C2]
+    python -m torch.distributed.run --nproc-per-node N --master-addr 127.0.0.1 ... bench.py --gpus N
+
+One "step" = one ws_rollout over the whole workload: T fused env steps of every replica
+(sample -> log -> dynamics -> reward/done -> auto-reset -> in-place store), the per-slot
+statistics reduction, and (N > 1) the NCCL all-reduce of those statistics -- every row of
+SURVEY 8(a).  Workload C2 (BASELINE.json configs[1]): CartPole-v1, 10K replicas x 1000
+steps per GPU (weak scaling: every rank runs its own 10K-replica shard of a global
+N*10K batch), uniform 2-action probabilities resident in HBM.
+
+Prints ONE JSON line (rank 0).  See DESIGN.md section 6 for every field.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+import numpy as np  # noqa: E402
+
+import wsinputs as W  # noqa: E402
+
+# algorithmic store bytes written per env-step: obs D*4 + act 4 + logp 4
+# + rew 4 + done 1, per agent (done per replica)
+ENV_BYTES = {"cartpole": 4 * 4 + 4 + 4 + 4 + 1, "acrobot": 6 * 4 + 13, "dummy": 4 * 4 + 13,
+             "pendulum": 3 * 4 + 4 + 4 + 4 + 1}
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=20)
+    ap.add_argument("--warmup", type=int, default=5)
+    ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
+    ap.add_argument("--workload", default="C2")
+    ap.add_argument("--block", type=int, default=0)
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--ncu", action="store_true", help="profiling mode: no clocks / cpu baseline / e2e")
+    return ap.parse_args()
+
+
+def dist_env():
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    return world, rank, local
+
+
+class Clocks:
+    """nvidia-smi sampler running during the timed region (B200_PROFILING.md clocks line)."""
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, index: int):
+        self.index = index
+        self.proc = None
+
+    def start(self):
+        try:
+            self.proc = subprocess.Popen(["nvidia-smi", "-i", str(self.index), f"--query-gpu={self.Q}",
+                                          "--format=csv,noheader,nounits", "-lms", "100"],
+                                         stdout=subprocess.PIPE, stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.proc = None
+
+    def stop(self) -> dict:
+        if self.proc is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.proc.terminate()
+        out, _ = self.proc.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            f = [x.strip() for x in line.split(",")]
+            if len(f) < 9:
+                continue
+            try:
+                sm.append(float(f[1]))
+                mx.append(float(f[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, f[5:9]):
+                if v.lower() == "active":
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+def measured_peaks():
+    try:
+        with open(os.path.join(ROOT, "MEASURED_PEAKS.json")) as f:
+            return json.load(f), "measured"
+    except OSError:
+        return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
+
+
+def cpu_baseline(w, budget_s: float = 12.0):
+    """The oracle as it stands (oracle/), on this host's cores, on a bounded sample of the
+    same workload: the first T' steps of the C2 replicas with T' sized to ~budget_s."""
+    import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    probs = W.workload_probs(w)
+    b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
+    t0 = time.perf_counter()
+    b.rollout(10, probs, n_threads=cores)
+    probe = time.perf_counter() - t0
+    T_s = max(10, min(w.T, int(10 * budget_s / max(probe, 1e-6))))
+    b2 = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=T_s)
+    t0 = time.perf_counter()
+    b2.rollout(T_s, probs, n_threads=cores)
+    dt = time.perf_counter() - t0
+    return {"value": w.n_envs * T_s / dt, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{w.name} {w.env}: {w.n_envs} replicas x first {T_s} of {w.T} steps "
+                      f"({w.n_envs * T_s} env-steps, {dt:.1f} s, {cores} threads)"}
+
+
+def run_reference(args, w):
+    world, rank, local = dist_env()
+    if rank != 0:
+        return
+    import oracle as O
+    cores = len(os.sched_getaffinity(0))
+    probs = W.workload_probs(w)
+    # each step = one bounded sample of the workload: all replicas, T_s steps
+    T_s = 25
+    b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=T_s)
+    for _ in range(args.warmup):
+        b.rollout(T_s, probs, n_threads=cores)
+    times = []
+    for _ in range(args.steps):
+        t0 = time.perf_counter()
+        b.rollout(T_s, probs, n_threads=cores)
+        times.append(time.perf_counter() - t0)
+    tot = sum(times)
+    value = w.n_envs * T_s * args.steps / tot
+    line = {"metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": 0, "steps": args.steps,
+            "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "impl": "reference",
+            "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs": w.n_envs, "T": w.T,
+                       "sample_T_per_step": T_s},
+            "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
+                             "sample": f"{w.n_envs} replicas x {T_s} steps per step"},
+            "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+def main():
+    args = parse()
+    w = W.CONFIGS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    import torch
+    import torch.distributed as dist
+
+    from paper_2408_00930_b200 import Env
+    from paper_2408_00930_b200.parallel import allreduce_stats
+
+    world, rank, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+
+    # weak scaling: each rank owns a full C2-sized shard of a world*E global batch
+    E, A, T = w.n_envs, w.n_agents, w.T
+    E_g = E * world
+    offset = rank * E
+    params = {"C4": (20, 10), "C5": (20, 0)}.get(w.name, (0, 0))
+    stream = torch.cuda.current_stream(dev)
+    env = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
+              param0=params[0], param1=params[1], block_size=args.block)
+    probs_host = W.workload_probs(w)
+    probs = torch.from_numpy(probs_host).to(dev)
+    stats_view = env.buffers()["stats"][:T]
+
+    def one_step():
+        env.rollout(T, probs)
+        allreduce_stats(stats_view)
+
+    for _ in range(max(args.warmup, 0)):
+        one_step()
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+
+    clocks = Clocks(local)
+    if not args.ncu:
+        clocks.start()
+        time.sleep(0.3)
+    launches0 = env.info().launches
+    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 2)]
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    ev[0].record(stream)
+    for k in range(args.steps):
+        ev[2 + 2 * k].record(stream)
+        env.rollout(T, probs)
+        ev[3 + 2 * k].record(stream)
+        allreduce_stats(stats_view)
+    ev[1].record(stream)
+    torch.cuda.synchronize(dev)
+    if world > 1:
+        dist.barrier()
+    total_ms = ev[0].elapsed_time(ev[1])
+    kern_ms = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(args.steps)]
+    launches = env.info().launches - launches0
+    clk = clocks.stop() if not args.ncu else {}
+
+    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
+    if world > 1:
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+    max_ms = float(t.item())
+    value = E_g * T * args.steps / (max_ms / 1e3)
+    ms_per_step = max_ms / args.steps
+
+    # roofline of the dominant kernel (ws_rollout = fused roll-out kernel + stats finalize)
+    peaks, peak_src = measured_peaks()
+    per_launch_bytes = ENV_BYTES.get(w.env, 0) * E * A * T
+    kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1e3
+    achieved = per_launch_bytes / kern_avg_s / 1e9
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
+                "frac": round(achieved / peak, 4), "traffic": None,
+                "peak_source": f"{peak_src} hbm_gbs (copy)", "kernel": "ws_rollout (k_rollout_discrete + k_finalize)",
+                "kernel_ms": round(kern_avg_s * 1e3, 4), "bytes_per_launch": per_launch_bytes}
+    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
+    if os.path.exists(traffic_file):
+        try:
+            tr = json.load(open(traffic_file)).get(w.name)
+            if tr:
+                roofline["traffic"] = tr
+        except Exception:
+            pass
+
+    line = None
+    if rank == 0:
+        e2e = None
+        if not args.ncu:
+            # end to end through the public API with HOST buffers: pinned probs H2D + stats D2H per step
+            henv = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
+                       param0=params[0], param1=params[1], block_size=args.block)
+            hp = torch.from_numpy(probs_host).pin_memory()
+            for _ in range(max(args.warmup, 1)):
+                henv.rollout_host(T, hp)
+            t0 = time.perf_counter()
+            for _ in range(args.steps):
+                henv.rollout_host(T, hp)
+            e2e_s = time.perf_counter() - t0
+            e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
+                   "h2d_bytes_per_step": int(hp.numel() * 4), "d2h_bytes_per_step": int(T * 4 * 8),
+                   "note": "rank 0, ws_rollout_host, host wall clock"}
+            henv.close()
+        line = {
+            "metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": world,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs_per_gpu": E, "n_envs_global": E_g,
+                       "n_agents": A, "T": T, "probs": "uniform, resident in HBM, step_stride 0",
+                       "parallelism": f"env-shard x{world} + NCCL stats all-reduce" if world > 1 else "1 GPU",
+                       "l2": f"store {per_launch_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
+            "roofline": roofline, "gpu_launches": int(launches),
+            "clocks": clk, "e2e": e2e,
+            "paper_context": "A100 8.6M env-steps/s incl. training (P:39); not like-for-like",
+        }
+        if not args.no_cpu_baseline and not args.ncu and world == 1:
+            line["cpu_baseline"] = cpu_baseline(w)
+        print(json.dumps(line), flush=True)
+    env.close()
+    if world > 1:
+        dist.barrier()
+        dist.destroy_process_group()
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,1026 @@
+// kernels.cu -- the sm_100a kernels of libws.
+//
+//  k_rollout_lane<Env>  A7: T fused steps (sample -> log -> step -> reward/done -> auto-reset
+//                       -> store -> per-slot statistics partial), one replica per lane, state
+//                       in registers.  The paper's literal mapping is one replica per CTA
+//                       (P:71); for single-agent envs that would leave 31/32 lanes idle, so
+//                       32 replicas share a warp (DESIGN R1) -- results are identical because
+//                       replicas never interact.
+//  k_rollout_tag        A7 for the multi-agent tag env: one CTA per replica, one thread per
+//                       agent, agents interact through a shared-memory cell grid.
+//  k_sample_*/k_step_*  the single-step calls ws_sample / ws_step.
+//  k_reset_*            ws_reset.
+//  k_finalize           A8: fixed-order reduction of the per-slot partials to stats[T, 4].
+#include <cuda_runtime.h>
+
+#include "common.cuh"
+#include "envs.cuh"
+#include "kernels.h"
+#include "sampler.cuh"
+
+namespace ws {
+
+// =======================================================================================
+// Per-env adapters for the lane kernels: state I/O, reset draws, observation, action type.
+// =======================================================================================
+template <class Env>
+struct Lane;
+
+template <>
+struct Lane<CartPole> {
+  using Env = CartPole;
+  using St = CartPole::St;
+  static constexpr bool kDiscrete = true;
+  static constexpr int N = 2, D = 4, S = 4, kDim = 1;
+  __device__ static void load(const float* p, St& s) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    s = St{v.x, v.y, v.z, v.w};
+  }
+  __device__ static void save(float* p, const St& s) {
+    *reinterpret_cast<float4*>(p) = make_float4(s.x, s.xd, s.th, s.thd);
+  }
+  __device__ static void init(const Key& k, uint32_t eg, uint32_t rc, St& s) {
+    const U4 b = block(k, rc, eg, 0, kReset);  // draws j = rc*4 + i -> block rc
+    CartPole::init(s, b.x, b.y, b.z, b.w);
+  }
+  __device__ static void obs_store(float* dst, const St& s, bool cs) {
+    const float4 v = make_float4(s.x, s.xd, s.th, s.thd);
+    if (cs) st_cs(reinterpret_cast<float4*>(dst), v); else *reinterpret_cast<float4*>(dst) = v;
+  }
+  __device__ static void step(St& s, int a, float& r, bool& term) { CartPole::step(s, a, r, term); }
+  __device__ static bool valid(int a) { return CartPole::valid(a); }
+};
+
+template <>
+struct Lane<Acrobot> {
+  using St = Acrobot::St;
+  static constexpr bool kDiscrete = true;
+  static constexpr int N = 3, D = 6, S = 4, kDim = 1;
+  __device__ static void load(const float* p, St& s) {
+    const float4 v = *reinterpret_cast<const float4*>(p);
+    s = St{v.x, v.y, v.z, v.w};
+  }
+  __device__ static void save(float* p, const St& s) {
+    *reinterpret_cast<float4*>(p) = make_float4(s.t1, s.t2, s.w1, s.w2);
+  }
+  __device__ static void init(const Key& k, uint32_t eg, uint32_t rc, St& s) {
+    const U4 b = block(k, rc, eg, 0, kReset);
+    Acrobot::init(s, b.x, b.y, b.z, b.w);
+  }
+  // obs = (cos t1, sin t1, cos t2, sin t2, w1, w2) (gym Acrobot-v1)
+  __device__ static void obs_store(float* dst, const St& s, bool cs) {
+    float s1, c1, s2, c2;
+    sincos_c(s.t1, s1, c1);
+    sincos_c(s.t2, s2, c2);
+    const float2 a = make_float2(c1, s1), b = make_float2(c2, s2), c = make_float2(s.w1, s.w2);
+    float2* d = reinterpret_cast<float2*>(dst);
+    if (cs) { st_cs(d, a); st_cs(d + 1, b); st_cs(d + 2, c); }
+    else { d[0] = a; d[1] = b; d[2] = c; }
+  }
+  __device__ static void step(St& s, int a, float& r, bool& term) { Acrobot::step(s, a, r, term); }
+  __device__ static bool valid(int a) { return Acrobot::valid(a); }
+};
+
+// Dummy (S:164 calibration env): constant zero observation, reward 1, truncation only.
+struct Dummy {
+  struct St {};
+};
+template <>
+struct Lane<Dummy> {
+  using St = Dummy::St;
+  static constexpr bool kDiscrete = true;
+  static constexpr int N = 2, D = 4, S = 0, kDim = 1;
+  __device__ static void load(const float*, St&) {}
+  __device__ static void save(float*, const St&) {}
+  __device__ static void init(const Key&, uint32_t, uint32_t, St&) {}
+  __device__ static void obs_store(float* dst, const St&, bool cs) {
+    const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
+    if (cs) st_cs(reinterpret_cast<float4*>(dst), z); else *reinterpret_cast<float4*>(dst) = z;
+  }
+  __device__ static void step(St&, int, float& r, bool& term) {
+    r = 1.0f;
+    term = false;
+  }
+  __device__ static bool valid(int a) { return a == 0 || a == 1; }
+};
+
+template <>
+struct Lane<Pendulum> {
+  using St = Pendulum::St;
+  static constexpr bool kDiscrete = false;
+  static constexpr int N = 0, D = 3, S = 2, kDim = 1;
+  __device__ static void load(const float* p, St& s) {
+    const float2 v = *reinterpret_cast<const float2*>(p);
+    s = St{v.x, v.y};
+  }
+  __device__ static void save(float* p, const St& s) {
+    *reinterpret_cast<float2*>(p) = make_float2(s.th, s.thd);
+  }
+  __device__ static void init(const Key& k, uint32_t eg, uint32_t rc, St& s) {
+    const U4 b = block(k, rc >> 1, eg, 0, kReset);  // draws j = rc*2 + i
+    if (rc & 1) Pendulum::init(s, b.z, b.w); else Pendulum::init(s, b.x, b.y);
+  }
+  // obs = (cos th, sin th, thdot)
+  __device__ static void obs_store(float* dst, const St& s, bool cs) {
+    float sn, c;
+    sincos_c(s.th, sn, c);
+    if (cs) { st_cs(dst, c); st_cs(dst + 1, sn); st_cs(dst + 2, s.thd); }
+    else { dst[0] = c; dst[1] = sn; dst[2] = s.thd; }
+  }
+  // returns false on a non-finite action
+  __device__ static bool step_c(St& s, const float (&a)[1], float& r, bool& term) {
+    if (!isfinite(a[0])) return false;
+    Pendulum::step(s, a[0], r);
+    term = false;
+    return true;
+  }
+};
+
+template <int DD>
+struct Lane<Surface<DD>> {
+  using Env = Surface<DD>;
+  using St = typename Env::St;
+  static constexpr bool kDiscrete = false;
+  static constexpr int N = 0, D = DD + 1, S = DD, kDim = DD;
+  __device__ static void load(const float* p, St& s) {
+#pragma unroll
+    for (int i = 0; i < DD; ++i) s.q[i] = p[i];
+  }
+  __device__ static void save(float* p, const St& s) {
+#pragma unroll
+    for (int i = 0; i < DD; ++i) p[i] = s.q[i];
+  }
+  // R11/R23: q_i = start_i + (-0.05 + 0.1 u_i), draws j = rc*D + i
+  __device__ static void init(const Key& k, uint32_t eg, uint32_t rc, St& s) {
+    const uint64_t j0 = (uint64_t)rc * DD;
+    U4 b = block(k, j0 >> 2, eg, 0, kReset);
+    uint64_t cur = j0 >> 2;
+#pragma unroll
+    for (int i = 0; i < DD; ++i) {
+      const uint64_t j = j0 + i;
+      if ((j >> 2) != cur) {
+        cur = j >> 2;
+        b = block(k, cur, eg, 0, kReset);
+      }
+      s.q[i] = Env::start(i) + (-0.05f + 0.1f * u01(pick(b, (uint32_t)(j & 3))));
+    }
+  }
+  __device__ static void obs_store(float* dst, const St& s, bool cs) {
+#pragma unroll
+    for (int i = 0; i < DD; ++i) {
+      if (cs) st_cs(dst + i, s.q[i]); else dst[i] = s.q[i];
+    }
+    const float E = Env::energy(s.q);
+    if (cs) st_cs(dst + DD, E); else dst[DD] = E;
+  }
+  __device__ static bool step_c(St& s, const float (&a)[DD], float& r, bool& term) {
+    return Env::step(s, a, r, term);
+  }
+};
+
+// =======================================================================================
+// Continuous-head sampling for one agent (R14): act_k = mean_k + exp(log_std_k) z_k,
+// logp = sum_k (-z_k^2/2 - log_std_k - log(2 pi)/2) in fp64, rounded once.
+// =======================================================================================
+template <int DIM>
+__device__ __forceinline__ bool gauss_sample(const Key& key, uint32_t eg, uint32_t agent, uint64_t t,
+                                             const float (&mean)[DIM], const float (&log_std)[DIM],
+                                             float (&act)[DIM], float& logp) {
+  bool ok = true;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) ok = ok && isfinite(mean[k]) && isfinite(log_std[k]);
+  double lp = 0.0;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    const float z = gauss_z(key, eg, agent, t * (uint64_t)DIM + (uint64_t)k);
+    const float sd = (float)exp((double)log_std[k]);
+    act[k] = ok ? mean[k] + sd * z : __int_as_float(0x7fc00000);
+    lp = lp + (((-0.5 * (double)z) * (double)z - (double)log_std[k]) - kHalfLog2Pi);
+  }
+  logp = ok ? (float)lp : __int_as_float(0x7fc00000);
+  return ok;
+}
+
+// =======================================================================================
+// Per-slot statistics of a warp of 32 replicas (A8); lane 0 writes the partial.
+// =======================================================================================
+__device__ __forceinline__ void warp_partial(Partial* dst, int lane, bool done, int32_t len, float ret,
+                                             float rew) {
+  const uint32_t nd = __reduce_add_sync(kFull, done ? 1u : 0u);
+  const uint32_t ln = __reduce_add_sync(kFull, done ? (uint32_t)len : 0u);
+  const float rs = warp_sum_f32(rew);
+  float rt = 0.0f;
+  if (nd) rt = warp_sum_f32(done ? ret : 0.0f);
+  if (lane == 0) {
+    uint4 v = make_uint4(nd, ln, __float_as_uint(rt), __float_as_uint(rs));
+    __stcs(reinterpret_cast<uint4*>(dst), v);
+  }
+}
+
+// =======================================================================================
+// A7: fused roll-out, discrete single-agent envs (CartPole, Acrobot, Dummy).
+// =======================================================================================
+template <class Env>
+__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T, const uint64_t t0,
+                                                         const float* __restrict__ probs,
+                                                         const int64_t row_stride,
+                                                         const int64_t step_stride) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  constexpr int N = L::N;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const int64_t warp_first = e - lane;
+  const bool live = e < a.E;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const int64_t part = e >> 5;
+  const Key key{a.k0, a.k1};
+
+  St s{};
+  int32_t ep_step = 0;
+  uint32_t rc = 0;
+  float ep_ret = 0.0f;
+  if (live) {
+    L::load(a.state + e * L::S, s);
+    ep_step = a.ep_step[e];
+    rc = a.reset_count[e];
+    ep_ret = a.ep_ret[e];
+  }
+  // reset look-ahead: nxt = init(e, rc + 1), refilled every 4 steps off the critical path
+  St nxt{};
+  L::init(key, eg, rc + 1, nxt);
+  bool stale = false;
+
+  Thresholds<N> th;
+  if (step_stride == 0) {
+    RowCDF<N> cdf;
+    warp_row_cdf<N>(probs, row_stride, warp_first, a.E, lane, cdf);
+    make_thresholds<N>(cdf, th);
+  }
+
+  U4 w{0, 0, 0, 0};
+  for (int c = 0; c < T; ++c) {
+    const uint64_t t = t0 + (uint64_t)c;
+    if (c == 0 || (t & 3) == 0) {
+      w = block(key, t >> 2, eg, 0, kAction);  // ACTION draws j = t
+      if (__any_sync(kFull, stale)) {           // warp-uniform refill of the look-ahead
+        St fresh;
+        L::init(key, eg, rc + 1, fresh);
+        if (stale) {
+          nxt = fresh;
+          stale = false;
+        }
+      }
+    }
+    const uint32_t word = pick(w, (uint32_t)(t & 3));
+
+    // ---- A2 sample
+    int act;
+    float lp;
+    bool bad;
+    if (step_stride == 0) {
+      act = search_k<N>(th, word >> 8, lp);
+      bad = th.bad;
+    } else {
+      RowCDF<N> cdf;
+      warp_row_cdf<N>(probs + (int64_t)c * step_stride, row_stride, warp_first, a.E, lane, cdf);
+      bad = cdf.bad;
+      act = search<N>(cdf, u01(word));
+      lp = logp_of<N>(cdf, act);
+    }
+    if (bad) {
+      act = -1;
+      lp = __int_as_float(0x7fc00000);
+    }
+
+    // ---- A6 log pre-step observation, action, log-prob (R12)
+    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+    if (live) {
+      L::obs_store(a.obs + idx * L::D, s, true);
+      st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
+      if (a.write_logp) st_cs(a.logp + idx, lp);
+    }
+
+    // ---- A3 / A4 step, reward, done
+    float r = 0.0f;
+    bool term = false;
+    uint8_t d = 0;
+    int32_t len = 0;
+    float ret = 0.0f;
+    if (live && !bad) {
+      St s2 = s;
+      L::step(s2, act, r, term);
+      ep_step += 1;
+      const bool trunc = ep_step >= a.max_steps;
+      d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
+      ep_ret = ep_ret + r;
+      if (d) {
+        // ---- A5 auto-reset: state = init(e, rc + 1) from the look-ahead
+        len = ep_step;
+        ret = ep_ret;
+        rc += 1;
+        if (stale) L::init(key, eg, rc, nxt);  // rare: two resets inside one refill window
+        s = nxt;
+        stale = true;
+        ep_step = 0;
+        ep_ret = 0.0f;
+      } else {
+        s = s2;
+      }
+    } else if (live && bad) {
+      atomicOr(a.err, kErrProbs | kErrAction);
+    }
+    if (live) {
+      st_cs(a.rew + idx, r);
+      st_cs_u8(a.done + idx, d);
+    }
+    // ---- A8 per-slot statistics partial
+    warp_partial(a.partials + (size_t)c * a.n_parts + part, lane, d != 0, len, ret, r);
+  }
+
+  if (live) {
+    L::save(a.state + e * L::S, s);
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    L::obs_store(a.obs_live + e * L::D, s, false);
+  }
+}
+
+// =======================================================================================
+// A7: fused roll-out, continuous single-agent envs (Pendulum, surface-D).
+// =======================================================================================
+template <class Env>
+__global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const int T, const uint64_t t0,
+                                                           const float* __restrict__ probs,
+                                                           const int64_t row_stride,
+                                                           const int64_t step_stride) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  constexpr int DIM = L::kDim;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = e < a.E;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const int64_t part = e >> 5;
+  const Key key{a.k0, a.k1};
+
+  St s{};
+  int32_t ep_step = 0;
+  uint32_t rc = 0;
+  float ep_ret = 0.0f;
+  if (live) {
+    L::load(a.state + e * L::S, s);
+    ep_step = a.ep_step[e];
+    rc = a.reset_count[e];
+    ep_ret = a.ep_ret[e];
+  }
+  float mean[DIM], log_std[DIM];
+  auto load_head = [&](const float* base) {
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      mean[k] = live ? __ldg(base + e * row_stride + k) : 0.0f;
+      log_std[k] = live ? __ldg(base + e * row_stride + DIM + k) : 0.0f;
+    }
+  };
+  load_head(probs);
+
+  for (int c = 0; c < T; ++c) {
+    const uint64_t t = t0 + (uint64_t)c;
+    if (step_stride != 0 && c > 0) load_head(probs + (int64_t)c * step_stride);
+    float act[DIM];
+    float lp;
+    const bool ok = gauss_sample<DIM>(key, eg, 0, t, mean, log_std, act, lp);
+
+    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+    if (live) {
+      L::obs_store(a.obs + idx * L::D, s, true);
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) st_cs(reinterpret_cast<float*>(a.act) + idx * DIM + k, act[k]);
+      if (a.write_logp) st_cs(a.logp + idx, lp);
+    }
+    float r = 0.0f;
+    bool term = false;
+    uint8_t d = 0;
+    int32_t len = 0;
+    float ret = 0.0f;
+    if (live) {
+      St s2 = s;
+      const bool stepped = ok && L::step_c(s2, act, r, term);
+      if (stepped) {
+        ep_step += 1;
+        const bool trunc = ep_step >= a.max_steps;
+        d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
+        ep_ret = ep_ret + r;
+        if (d) {
+          len = ep_step;
+          ret = ep_ret;
+          rc += 1;
+          L::init(key, eg, rc, s);
+          ep_step = 0;
+          ep_ret = 0.0f;
+        } else {
+          s = s2;
+        }
+      } else {
+        r = 0.0f;
+        atomicOr(a.err, (ok ? 0u : kErrProbs) | kErrAction);
+      }
+      st_cs(a.rew + idx, r);
+      st_cs_u8(a.done + idx, d);
+    }
+    warp_partial(a.partials + (size_t)c * a.n_parts + part, lane, d != 0, len, ret, r);
+  }
+  if (live) {
+    L::save(a.state + e * L::S, s);
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    L::obs_store(a.obs_live + e * L::D, s, false);
+  }
+}
+
+// =======================================================================================
+// Single-step path (ws_sample / ws_step) for the lane envs.
+// =======================================================================================
+// ws_sample, discrete rows (any A): warp-cooperative scan + search, one row per lane.
+template <int N>
+__global__ void __launch_bounds__(256) k_sample_discrete(const KArgs a, const int slot, const uint64_t t,
+                                                        const float* __restrict__ probs,
+                                                        const int64_t row_stride) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // e*A + agent
+  const int lane = threadIdx.x & 31;
+  const int64_t n_rows = a.E * (int64_t)a.A;
+  RowCDF<N> cdf;
+  warp_row_cdf<N>(probs, row_stride, row - lane, n_rows, lane, cdf);
+  if (row >= n_rows) return;
+  const int64_t e = row / a.A;
+  const uint32_t agent = (uint32_t)(row - e * a.A);
+  const U4 b = block(Key{a.k0, a.k1}, t >> 2, (uint32_t)(a.offset + e), agent, kAction);
+  int act = search<N>(cdf, u01(pick(b, (uint32_t)(t & 3))));
+  float lp = logp_of<N>(cdf, act);
+  if (cdf.bad) {
+    act = -1;
+    lp = __int_as_float(0x7fc00000);
+    atomicOr(a.err, kErrProbs);
+  }
+  const size_t idx = (size_t)slot * (size_t)n_rows + (size_t)row;
+  reinterpret_cast<int32_t*>(a.act)[idx] = act;
+  if (a.write_logp) a.logp[idx] = lp;
+}
+
+template <int DIM>
+__global__ void __launch_bounds__(256) k_sample_continuous(const KArgs a, const int slot, const uint64_t t,
+                                                          const float* __restrict__ probs,
+                                                          const int64_t row_stride) {
+  const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t n_rows = a.E * (int64_t)a.A;
+  if (row >= n_rows) return;
+  const int64_t e = row / a.A;
+  const uint32_t agent = (uint32_t)(row - e * a.A);
+  float mean[DIM], log_std[DIM], act[DIM], lp;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) {
+    mean[k] = probs[row * row_stride + k];
+    log_std[k] = probs[row * row_stride + DIM + k];
+  }
+  const bool ok = gauss_sample<DIM>(Key{a.k0, a.k1}, (uint32_t)(a.offset + e), agent, t, mean, log_std, act, lp);
+  if (!ok) atomicOr(a.err, kErrProbs);
+  const size_t idx = (size_t)slot * (size_t)n_rows + (size_t)row;
+#pragma unroll
+  for (int k = 0; k < DIM; ++k) reinterpret_cast<float*>(a.act)[idx * DIM + k] = act[k];
+  if (a.write_logp) a.logp[idx] = lp;
+}
+
+// ws_step for lane envs: actions from the act slab (given == nullptr) or from `given`
+// (copied into the slab, logp = NaN, R27).
+template <class Env>
+__global__ void __launch_bounds__(256) k_step_lane(const KArgs a, const int slot, const void* __restrict__ given) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31;
+  const bool live = e < a.E;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const Key key{a.k0, a.k1};
+  const size_t idx = (size_t)slot * (size_t)a.E + (size_t)e;
+  float r = 0.0f;
+  uint8_t d = 0;
+  int32_t len = 0;
+  float ret = 0.0f;
+  if (live) {
+    St s;
+    L::load(a.state + e * L::S, s);
+    int32_t ep_step = a.ep_step[e];
+    uint32_t rc = a.reset_count[e];
+    float ep_ret = a.ep_ret[e];
+    L::obs_store(a.obs + idx * L::D, s, false);
+    bool term = false, ok;
+    St s2 = s;
+    if constexpr (L::kDiscrete) {
+      int act;
+      if (given) {
+        act = reinterpret_cast<const int32_t*>(given)[e];
+        reinterpret_cast<int32_t*>(a.act)[idx] = act;
+        if (a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
+      } else {
+        act = reinterpret_cast<const int32_t*>(a.act)[idx];
+      }
+      ok = L::valid(act);
+      if (ok) L::step(s2, act, r, term);
+    } else {
+      constexpr int DIM = L::kDim;
+      float act[DIM];
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) {
+        if (given) {
+          act[k] = reinterpret_cast<const float*>(given)[e * DIM + k];
+          reinterpret_cast<float*>(a.act)[idx * DIM + k] = act[k];
+        } else {
+          act[k] = reinterpret_cast<const float*>(a.act)[idx * DIM + k];
+        }
+      }
+      if (given && a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
+      ok = L::step_c(s2, act, r, term);
+    }
+    if (ok) {
+      ep_step += 1;
+      const bool trunc = ep_step >= a.max_steps;
+      d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
+      ep_ret = ep_ret + r;
+      if (d) {
+        len = ep_step;
+        ret = ep_ret;
+        rc += 1;
+        L::init(key, eg, rc, s);
+        ep_step = 0;
+        ep_ret = 0.0f;
+      } else {
+        s = s2;
+      }
+      L::save(a.state + e * L::S, s);
+      a.ep_step[e] = ep_step;
+      a.reset_count[e] = rc;
+      a.ep_ret[e] = ep_ret;
+      L::obs_store(a.obs_live + e * L::D, s, false);
+    } else {
+      r = 0.0f;
+      atomicOr(a.err, kErrAction);
+    }
+    a.rew[idx] = r;
+    a.done[idx] = d;
+  }
+  warp_partial(a.partials + (size_t)slot * a.n_parts + (e >> 5), lane, d != 0, len, ret, r);
+}
+
+template <class Env>
+__global__ void k_reset_lane(const KArgs a) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  St s;
+  L::init(Key{a.k0, a.k1}, (uint32_t)(a.offset + e), 0u, s);
+  L::save(a.state + e * L::S, s);
+  a.ep_step[e] = 0;
+  a.reset_count[e] = 0;
+  a.ep_ret[e] = 0.0f;
+  L::obs_store(a.obs_live + e * L::D, s, false);
+}
+
+// =======================================================================================
+// Tag gridworld (R22): one CTA per replica, one thread per agent.
+// =======================================================================================
+enum TagMode : int { kTagRollout = 0, kTagStepSlab = 1, kTagStepGiven = 2 };
+constexpr int kTagN = 5;
+
+__device__ __forceinline__ float block_sum_f32(float v, float* red, int nwarps) {
+  // fixed order: warp butterfly, then warp partials summed in warp order by thread 0
+  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
+  v = warp_sum_f32(v);
+  if (lane == 0) red[wid] = v;
+  __syncthreads();
+  float s = 0.0f;
+  if (threadIdx.x == 0)
+    for (int i = 0; i < nwarps; ++i) s = s + red[i];
+  __syncthreads();
+  return s;  // valid in thread 0
+}
+
+__global__ void __launch_bounds__(1024) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
+                                              const int slot0, const float* __restrict__ probs,
+                                              const int64_t row_stride, const int64_t step_stride,
+                                              const void* __restrict__ given) {
+  extern __shared__ int smem[];
+  const int G = a.p0, NT = a.p1, A = a.A;
+  int* taggers_on = smem;
+  int* tagged_on = smem + G * G;
+  float* red = reinterpret_cast<float*>(smem + 2 * G * G);
+  const int nwarps = blockDim.x >> 5;
+  const int64_t e = blockIdx.x;
+  const int ag = threadIdx.x;
+  const int lane = ag & 31;
+  const bool is_agent = ag < A;
+  const bool tagger = ag < NT;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const Key key{a.k0, a.k1};
+  const float inv = (float)(G - 1);
+
+  int32_t x = 0, y = 0, active = 0;
+  if (is_agent) {
+    const int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
+    x = ts[0];
+    y = ts[1];
+    active = ts[2];
+  }
+  int32_t ep_step = a.ep_step[e];
+  uint32_t rc = a.reset_count[e];
+  float ep_ret = is_agent ? a.ep_ret[e * A + ag] : 0.0f;
+  const int n_runners = A - NT;
+
+  Thresholds<kTagN> th;
+  const int64_t row0 = e * A;  // rows of this replica
+  if (mode == kTagRollout && step_stride == 0) {
+    RowCDF<kTagN> cdf;
+    warp_row_cdf<kTagN>(probs + row0 * row_stride, row_stride, (int64_t)(ag - lane), A, lane, cdf);
+    make_thresholds<kTagN>(cdf, th);
+  }
+  U4 w{0, 0, 0, 0};
+  for (int c = 0; c < T; ++c) {
+    const int slot = slot0 + c;
+    const uint64_t t = t0 + (uint64_t)c;
+    const size_t idx = ((size_t)slot * (size_t)a.E + (size_t)e) * (size_t)A + (size_t)ag;
+    int act = 0;
+    bool bad_probs = false;
+    if (mode == kTagRollout) {
+      if (c == 0 || (t & 3) == 0) w = block(key, t >> 2, eg, (uint32_t)ag, kAction);
+      const uint32_t word = pick(w, (uint32_t)(t & 3));
+      float lp;
+      if (step_stride == 0) {
+        act = search_k<kTagN>(th, word >> 8, lp);
+        bad_probs = th.bad;
+      } else {
+        RowCDF<kTagN> cdf;
+        warp_row_cdf<kTagN>(probs + (int64_t)c * step_stride + row0 * row_stride, row_stride,
+                            (int64_t)(ag - lane), A, lane, cdf);
+        bad_probs = cdf.bad;
+        act = search<kTagN>(cdf, u01(word));
+        lp = logp_of<kTagN>(cdf, act);
+      }
+      if (bad_probs) {
+        act = -1;
+        lp = __int_as_float(0x7fc00000);
+      }
+      if (is_agent) {
+        st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
+        if (a.write_logp) st_cs(a.logp + idx, lp);
+      }
+    } else if (is_agent) {
+      if (mode == kTagStepGiven) {
+        act = reinterpret_cast<const int32_t*>(given)[e * A + ag];
+        reinterpret_cast<int32_t*>(a.act)[idx] = act;
+        if (a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
+      } else {
+        act = reinterpret_cast<const int32_t*>(a.act)[idx];
+      }
+    }
+    // pre-step observation (x/(G-1), y/(G-1), is_tagger, active)  (R22)
+    if (is_agent) {
+      const float4 o = make_float4((float)x / inv, (float)y / inv, tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
+      st_cs(reinterpret_cast<float4*>(a.obs) + idx, o);
+    }
+    const bool invalid = is_agent && (act < 0 || act > 4);
+    const bool any_invalid = __syncthreads_or(invalid) != 0;
+    float r = 0.0f;
+    uint8_t d = 0;
+    if (!any_invalid) {
+      // simultaneous moves, clipped to the grid; tagged runners frozen
+      if (is_agent && (tagger || active)) {
+        int nx = x, ny = y;
+        if (act == 1) ny = y + 1;
+        else if (act == 2) ny = y - 1;
+        else if (act == 3) nx = x + 1;
+        else if (act == 4) nx = x - 1;
+        x = min(max(nx, 0), G - 1);
+        y = min(max(ny, 0), G - 1);
+      }
+      for (int i = ag; i < 2 * G * G; i += blockDim.x) smem[i] = 0;
+      __syncthreads();
+      const int cell = y * G + x;
+      if (is_agent && tagger) atomicAdd(&taggers_on[cell], 1);
+      __syncthreads();
+      if (is_agent && !tagger) {
+        if (active) {
+          if (taggers_on[cell] >= 1) {
+            r = -1.0f;
+            active = 0;
+            atomicAdd(&tagged_on[cell], 1);
+          } else {
+            r = 0.01f;
+          }
+        }
+      }
+      __syncthreads();
+      if (is_agent && tagger) r = (float)tagged_on[cell] / (float)taggers_on[cell];
+      const int still = __syncthreads_count(is_agent && !tagger && active);
+      const bool term = n_runners > 0 && still == 0;
+      ep_step += 1;
+      const bool trunc = ep_step >= a.max_steps;
+      d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
+      if (is_agent) ep_ret = ep_ret + r;
+    } else if (threadIdx.x == 0) {
+      atomicOr(a.err, kErrAction | (mode == kTagRollout && bad_probs ? kErrProbs : 0u));
+    }
+    if (is_agent) st_cs(a.rew + idx, r);
+    // A8: per-replica partial (sum of rewards; on done, return over agents and length)
+    const float rs = block_sum_f32(is_agent ? r : 0.0f, red, nwarps);
+    float rt = 0.0f;
+    if (d) rt = block_sum_f32(is_agent ? ep_ret : 0.0f, red, nwarps);
+    if (threadIdx.x == 0) {
+      const size_t di = (size_t)slot * (size_t)a.E + (size_t)e;
+      st_cs_u8(a.done + di, d);
+      const uint4 v = make_uint4(d ? 1u : 0u, d ? (uint32_t)ep_step : 0u, __float_as_uint(rt), __float_as_uint(rs));
+      __stcs(reinterpret_cast<uint4*>(a.partials + (size_t)slot * a.n_parts + e), v);
+    }
+    if (d) {  // A5 auto-reset, uniform across the CTA
+      rc += 1;
+      if (is_agent) {
+        const U4 b = block(key, rc >> 1, eg, (uint32_t)ag, kReset);  // draws j = rc*2 + {0,1}
+        const uint32_t wx = (rc & 1) ? b.z : b.x, wy = (rc & 1) ? b.w : b.y;
+        x = (int32_t)__umulhi(wx, (uint32_t)G);
+        y = (int32_t)__umulhi(wy, (uint32_t)G);
+        active = 1;
+      }
+      ep_step = 0;
+      ep_ret = 0.0f;
+    }
+    __syncthreads();
+  }
+  if (is_agent) {
+    int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
+    ts[0] = x;
+    ts[1] = y;
+    ts[2] = active;
+    a.ep_ret[e * A + ag] = ep_ret;
+    reinterpret_cast<float4*>(a.obs_live)[e * A + ag] =
+        make_float4((float)x / inv, (float)y / inv, tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
+  }
+  if (threadIdx.x == 0) {
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+  }
+}
+
+__global__ void k_reset_tag(const KArgs a) {
+  const int64_t e = blockIdx.x;
+  const int ag = threadIdx.x;
+  const int G = a.p0, NT = a.p1, A = a.A;
+  if (ag < A) {
+    const U4 b = block(Key{a.k0, a.k1}, 0, (uint32_t)(a.offset + e), (uint32_t)ag, kReset);
+    const int32_t x = (int32_t)__umulhi(b.x, (uint32_t)G), y = (int32_t)__umulhi(b.y, (uint32_t)G);
+    int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
+    ts[0] = x;
+    ts[1] = y;
+    ts[2] = 1;
+    a.ep_ret[e * A + ag] = 0.0f;
+    const float inv = (float)(G - 1);
+    reinterpret_cast<float4*>(a.obs_live)[e * A + ag] =
+        make_float4((float)x / inv, (float)y / inv, ag < NT ? 1.0f : 0.0f, 1.0f);
+  }
+  if (ag == 0) {
+    a.ep_step[e] = 0;
+    a.reset_count[e] = 0;
+  }
+}
+
+// =======================================================================================
+// A8: stats[slot] = fixed-order sum of the parts (one warp per slot).
+// =======================================================================================
+__global__ void k_finalize(const Partial* __restrict__ partials, const int n_parts, const int slot0,
+                           const int n_slots, double* __restrict__ stats) {
+  const int slot = slot0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int lane = threadIdx.x & 31;
+  if (slot >= slot0 + n_slots) return;
+  const Partial* row = partials + (size_t)slot * n_parts;
+  unsigned long long nd = 0, ln = 0;
+  double rt = 0.0, rs = 0.0;
+  for (int i = lane; i < n_parts; i += 32) {
+    const uint4 v = reinterpret_cast<const uint4*>(row)[i];
+    nd += v.x;
+    ln += v.y;
+    rt += (double)__uint_as_float(v.z);
+    rs += (double)__uint_as_float(v.w);
+  }
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) {
+    nd += __shfl_xor_sync(kFull, nd, o);
+    ln += __shfl_xor_sync(kFull, ln, o);
+    rt += __shfl_xor_sync(kFull, rt, o);
+    rs += __shfl_xor_sync(kFull, rs, o);
+  }
+  if (lane == 0) {
+    double* st = stats + (size_t)slot * 4;
+    st[0] = (double)nd;
+    st[1] = rt;
+    st[2] = (double)ln;
+    st[3] = rs;
+  }
+}
+
+// =======================================================================================
+// Test hooks.
+// =======================================================================================
+__global__ void k_test_philox(const uint32_t* rows, int64_t n, uint32_t* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i >= n) return;
+  const uint32_t* r = rows + i * 6;
+  const U4 v = philox(r[0], r[1], r[2], r[3], r[4], r[5]);
+  out[i * 4 + 0] = v.x;
+  out[i * 4 + 1] = v.y;
+  out[i * 4 + 2] = v.z;
+  out[i * 4 + 3] = v.w;
+}
+
+// every lane loads the same row (row_stride 0); thread i handles draws k = i, i + stride...
+// Both the direct search and the hoisted thresholds are evaluated; a disagreement is
+// counted in counts[n] (must stay 0).
+template <int N>
+__global__ void k_test_sample_grid(const float* p, int64_t* counts) {
+  __shared__ unsigned long long local[N + 1];
+  if (threadIdx.x <= N) local[threadIdx.x] = 0;
+  __syncthreads();
+  RowCDF<N> cdf;
+  warp_row_cdf<N>(p, 0, 0, 1 << 30, threadIdx.x & 31, cdf);
+  Thresholds<N> th;
+  make_thresholds<N>(cdf, th);
+  unsigned long long mine[N + 1];
+#pragma unroll
+  for (int i = 0; i <= N; ++i) mine[i] = 0;
+  for (uint32_t k = blockIdx.x * blockDim.x + threadIdx.x; k < (1u << 24); k += gridDim.x * blockDim.x) {
+    const int a1 = search<N>(cdf, (float)k * (1.0f / 16777216.0f));
+    float lp;
+    const int a2 = search_k<N>(th, k, lp);
+#pragma unroll
+    for (int i = 0; i < N; ++i) mine[i] += (a1 == i);
+    mine[N] += (a1 != a2);
+  }
+#pragma unroll
+  for (int i = 0; i <= N; ++i) atomicAdd(&local[i], mine[i]);
+  __syncthreads();
+  if (threadIdx.x <= N) atomicAdd(reinterpret_cast<unsigned long long*>(counts) + threadIdx.x, local[threadIdx.x]);
+}
+
+// =======================================================================================
+// Host launchers.
+// =======================================================================================
+int64_t n_parts_for(EnvKind kind, int64_t E) { return kind == kTag ? E : (E + 31) / 32; }
+
+#define WS_SURFACE_DISPATCH(D, MACRO) \
+  switch (D) {                        \
+    case 2: MACRO(2); break;          \
+    case 3: MACRO(3); break;          \
+    case 4: MACRO(4); break;          \
+    case 8: MACRO(8); break;          \
+    case 16: MACRO(16); break;        \
+    case 20: MACRO(20); break;        \
+    case 32: MACRO(32); break;        \
+    default: return cudaErrorInvalidValue; \
+  }
+
+static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
+
+static size_t tag_smem(const KArgs& a, int block) {
+  return (size_t)(2 * a.p0 * a.p0) * sizeof(int) + (size_t)(block / 32) * sizeof(float);
+}
+static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
+
+cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
+  const unsigned g = grid_for(a.E, l.block);
+  switch (l.kind) {
+    case kCartPole: k_reset_lane<CartPole><<<g, l.block, 0, l.stream>>>(a); break;
+    case kAcrobot: k_reset_lane<Acrobot><<<g, l.block, 0, l.stream>>>(a); break;
+    case kPendulum: k_reset_lane<Pendulum><<<g, l.block, 0, l.stream>>>(a); break;
+    case kDummy: k_reset_lane<Dummy><<<g, l.block, 0, l.stream>>>(a); break;
+    case kSurface: {
+#define M(DD) k_reset_lane<Surface<DD>><<<g, l.block, 0, l.stream>>>(a)
+      WS_SURFACE_DISPATCH(a.p0, M)
+#undef M
+      break;
+    }
+    case kTag: k_reset_tag<<<(unsigned)a.E, tag_block(a), 0, l.stream>>>(a); break;
+  }
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_slots, uint64_t* launches) {
+  const int wpb = 8;
+  k_finalize<<<(unsigned)((n_slots + wpb - 1) / wpb), wpb * 32, 0, l.stream>>>(a.partials, a.n_parts, slot0,
+                                                                               n_slots, a.stats);
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
+                           int64_t row_stride, int64_t step_stride, uint64_t* launches) {
+  const unsigned g = grid_for(a.E, l.block);
+  switch (l.kind) {
+    case kCartPole:
+      k_rollout_discrete<CartPole><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+      break;
+    case kAcrobot:
+      k_rollout_discrete<Acrobot><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+      break;
+    case kDummy:
+      k_rollout_discrete<Dummy><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+      break;
+    case kPendulum:
+      k_rollout_continuous<Pendulum><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+      break;
+    case kSurface: {
+#define M(DD) k_rollout_continuous<Surface<DD>><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride)
+      WS_SURFACE_DISPATCH(a.p0, M)
+#undef M
+      break;
+    }
+    case kTag: {
+      const int b = tag_block(a);
+      k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, kTagRollout, T, t0, 0, probs, row_stride,
+                                                             step_stride, nullptr);
+      break;
+    }
+  }
+  *launches += 1;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return launch_finalize(a, l, 0, T, launches);
+}
+
+cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t, const float* probs,
+                          int64_t row_stride, uint64_t* launches) {
+  const int64_t rows = a.E * (int64_t)a.A;
+  const unsigned g = grid_for(rows, 256);
+  switch (l.kind) {
+    case kCartPole:
+    case kDummy: k_sample_discrete<2><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride); break;
+    case kAcrobot: k_sample_discrete<3><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride); break;
+    case kTag: k_sample_discrete<5><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride); break;
+    case kPendulum: k_sample_continuous<1><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride); break;
+    case kSurface: {
+#define M(DD) k_sample_continuous<DD><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride)
+      WS_SURFACE_DISPATCH(a.p0, M)
+#undef M
+      break;
+    }
+  }
+  *launches += 1;
+  return cudaGetLastError();
+}
+
+cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches) {
+  const unsigned g = grid_for(a.E, l.block);
+  switch (l.kind) {
+    case kCartPole: k_step_lane<CartPole><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
+    case kAcrobot: k_step_lane<Acrobot><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
+    case kDummy: k_step_lane<Dummy><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
+    case kPendulum: k_step_lane<Pendulum><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
+    case kSurface: {
+#define M(DD) k_step_lane<Surface<DD>><<<g, l.block, 0, l.stream>>>(a, slot, given)
+      WS_SURFACE_DISPATCH(a.p0, M)
+#undef M
+      break;
+    }
+    case kTag: {
+      const int b = tag_block(a);
+      k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, given ? kTagStepGiven : kTagStepSlab, 1, 0, slot,
+                                                             nullptr, 0, 0, given);
+      break;
+    }
+  }
+  *launches += 1;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return launch_finalize(a, l, slot, 1, launches);
+}
+
+cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s) {
+  k_test_philox<<<grid_for(n, 256), 256, 0, s>>>(rows, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cudaStream_t s) {
+  switch (n) {
+    case 1: k_test_sample_grid<1><<<592, 256, 0, s>>>(p, counts); break;
+    case 2: k_test_sample_grid<2><<<592, 256, 0, s>>>(p, counts); break;
+    case 3: k_test_sample_grid<3><<<592, 256, 0, s>>>(p, counts); break;
+    case 4: k_test_sample_grid<4><<<592, 256, 0, s>>>(p, counts); break;
+    case 5: k_test_sample_grid<5><<<592, 256, 0, s>>>(p, counts); break;
+    case 6: k_test_sample_grid<6><<<592, 256, 0, s>>>(p, counts); break;
+    case 7: k_test_sample_grid<7><<<592, 256, 0, s>>>(p, counts); break;
+    case 8: k_test_sample_grid<8><<<592, 256, 0, s>>>(p, counts); break;
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
+}  // namespace ws

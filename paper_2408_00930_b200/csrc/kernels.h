@@ -1,0 +1,63 @@
+// kernels.h -- internal (C++) interface between the host runtime (runtime.cu) and the
+// device kernels (kernels.cu).  Not part of the C ABI.
+#pragma once
+
+#include <cstdint>
+#include <cuda_runtime.h>
+
+namespace ws {
+
+enum EnvKind : int { kCartPole = 0, kAcrobot = 1, kPendulum = 2, kTag = 3, kSurface = 4, kDummy = 5 };
+
+struct Partial;
+
+// Everything a kernel needs to find the handle's buffers (passed by value).
+struct KArgs {
+  // roll-out store (time-major)
+  float* obs;
+  void* act;
+  float* logp;
+  float* rew;
+  uint8_t* done;
+  Partial* partials;  // [T_cap, n_parts]
+  double* stats;      // [T_cap, 4]
+  // live state
+  float* state;       // [E, S]
+  int32_t* tstate;    // tag: [E, A, 3]
+  float* obs_live;    // [E, A, D]
+  int32_t* ep_step;   // [E]
+  uint32_t* reset_count;  // [E]
+  float* ep_ret;      // [E, A]
+  uint32_t* err;      // sticky device error word
+  int64_t E;          // replicas on this device
+  int64_t offset;     // global index of replica 0
+  int32_t A;
+  int32_t T_cap;
+  int32_t max_steps;
+  int32_t write_logp;
+  int32_t n_parts;    // statistics parts per slot
+  int32_t p0, p1;     // env params (tag G / taggers; surface D)
+  uint32_t k0, k1;    // Philox key
+};
+
+struct Launch {
+  EnvKind kind;
+  int block;          // lane-kernel block size
+  cudaStream_t stream;
+};
+
+// all return the cudaGetLastError() after the launch(es) and add to *launches
+cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches);
+cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
+                           int64_t row_stride, int64_t step_stride, uint64_t* launches);
+cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t, const float* probs,
+                          int64_t row_stride, uint64_t* launches);
+cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches);
+cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_slots, uint64_t* launches);
+cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s);
+cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cudaStream_t s);
+
+// number of statistics parts per slot for an env kind
+int64_t n_parts_for(EnvKind kind, int64_t E);
+
+}  // namespace ws

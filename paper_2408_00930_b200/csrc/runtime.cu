@@ -1,0 +1,513 @@
+// runtime.cu -- host runtime of libws: the C ABI of include/ws.h (data manager, function
+// manager dispatch, sampler and reset entry points), allocation, streams, sticky errors.
+#include <cuda_runtime.h>
+
+#include <cmath>
+#include <cstdio>
+#include <cstring>
+#include <limits>
+#include <string>
+#include <vector>
+
+#include "../../include/ws.h"
+#include "common.cuh"
+#include "kernels.h"
+
+namespace {
+
+struct EnvSpec {
+  ws::EnvKind kind;
+  int obs_dim, n_actions, act_dim, state_dim, max_steps;
+};
+
+bool lookup_env(const char* name, int A, int p0, EnvSpec* out) {
+  if (!name) return false;
+  std::string n(name);
+  if (n == "cartpole") { *out = {ws::kCartPole, 4, 2, 1, 4, 500}; return true; }
+  if (n == "acrobot") { *out = {ws::kAcrobot, 6, 3, 1, 4, 500}; return true; }
+  if (n == "pendulum") { *out = {ws::kPendulum, 3, 0, 1, 2, 200}; return true; }
+  if (n == "tag") { *out = {ws::kTag, 4, 5, 1, 0, 200}; return true; }
+  if (n == "surface") {
+    const int D = p0 > 0 ? p0 : 20;
+    *out = {ws::kSurface, D + 1, 0, D, D, 200};
+    return true;
+  }
+  if (n == "dummy") { *out = {ws::kDummy, 4, 2, 1, 0, 100}; return true; }
+  (void)A;
+  return false;
+}
+
+bool surface_dim_supported(int D) {
+  return D == 2 || D == 3 || D == 4 || D == 8 || D == 16 || D == 20 || D == 32;
+}
+
+struct DeviceGuard {
+  int prev = -1;
+  bool changed = false;
+  explicit DeviceGuard(int dev) {
+    if (dev >= 0 && cudaGetDevice(&prev) == cudaSuccess && prev != dev) {
+      changed = cudaSetDevice(dev) == cudaSuccess;
+    }
+  }
+  ~DeviceGuard() {
+    if (changed) cudaSetDevice(prev);
+  }
+};
+
+}  // namespace
+
+struct ws_env {
+  EnvSpec spec{};
+  std::string env_name;
+  int64_t E = 0, offset = 0, E_global = 0;
+  int32_t A = 1;
+  uint64_t seed = 0;
+  int device = -1;
+  cudaStream_t stream = nullptr;
+  int32_t T_cap = 0, cursor = 0, sampled_slot = -1;
+  uint64_t t = 0;
+  int32_t max_steps = 0, write_logp = 1, p0 = 0, p1 = 0, block = 128;
+  ws_alloc_fn alloc = nullptr;
+  ws_free_fn free_fn = nullptr;
+  void* alloc_user = nullptr;
+  std::vector<std::pair<void*, size_t>> allocs;
+  // live state
+  float* state = nullptr;
+  int32_t* tstate = nullptr;
+  float* obs_live = nullptr;
+  int32_t* ep_step = nullptr;
+  uint32_t* reset_count = nullptr;
+  float* ep_ret = nullptr;
+  uint32_t* err = nullptr;
+  // store
+  float* obs = nullptr;
+  void* act = nullptr;
+  float* logp = nullptr;
+  float* rew = nullptr;
+  uint8_t* done = nullptr;
+  double* stats = nullptr;
+  ws::Partial* partials = nullptr;
+  // e2e staging
+  float* staging = nullptr;
+  int64_t staging_n = 0;
+  std::vector<double> host_stats;
+  uint64_t launches = 0;
+  std::string last_error;
+};
+
+namespace {
+
+ws_status fail(ws_env* h, ws_status s, const std::string& msg) {
+  if (h) h->last_error = msg;
+  return s;
+}
+
+ws_status cuda_fail(ws_env* h, cudaError_t e, const char* where) {
+  std::string m = std::string(where) + ": " + cudaGetErrorString(e);
+  if (h) h->last_error = m;
+  return e == cudaErrorMemoryAllocation ? WS_ERR_OUT_OF_MEMORY : WS_ERR_CUDA;
+}
+
+void* dev_alloc(ws_env* h, size_t bytes, cudaError_t* err) {
+  *err = cudaSuccess;
+  if (bytes == 0) return nullptr;
+  bytes = (bytes + 255) & ~size_t(255);
+  void* p = nullptr;
+  if (h->alloc) {
+    p = h->alloc(bytes, (void*)h->stream, h->alloc_user);
+    if (!p) *err = cudaErrorMemoryAllocation;
+  } else {
+    *err = cudaMalloc(&p, bytes);
+    if (*err != cudaSuccess) p = nullptr;
+  }
+  if (p) h->allocs.emplace_back(p, bytes);
+  return p;
+}
+
+void free_all(ws_env* h) {
+  for (auto& pr : h->allocs) {
+    if (h->free_fn) h->free_fn(pr.first, pr.second, (void*)h->stream, h->alloc_user);
+    else cudaFree(pr.first);
+  }
+  h->allocs.clear();
+}
+
+ws::KArgs kargs(const ws_env* h) {
+  ws::KArgs a{};
+  a.obs = h->obs;
+  a.act = h->act;
+  a.logp = h->logp;
+  a.rew = h->rew;
+  a.done = h->done;
+  a.partials = h->partials;
+  a.stats = h->stats;
+  a.state = h->state;
+  a.tstate = h->tstate;
+  a.obs_live = h->obs_live;
+  a.ep_step = h->ep_step;
+  a.reset_count = h->reset_count;
+  a.ep_ret = h->ep_ret;
+  a.err = h->err;
+  a.E = h->E;
+  a.offset = h->offset;
+  a.A = h->A;
+  a.T_cap = h->T_cap;
+  a.max_steps = h->max_steps;
+  a.write_logp = h->write_logp;
+  a.n_parts = (int32_t)ws::n_parts_for(h->spec.kind, h->E);
+  a.p0 = h->p0;
+  a.p1 = h->p1;
+  a.k0 = (uint32_t)h->seed;
+  a.k1 = (uint32_t)(h->seed >> 32);
+  return a;
+}
+
+ws::Launch launch_of(const ws_env* h) { return ws::Launch{h->spec.kind, h->block, h->stream}; }
+
+// Store allocation: once, the first time it is needed (lazy sizing, never regrown).
+ws_status ensure_store(ws_env* h, int32_t T) {
+  if (h->T_cap > 0) return WS_OK;
+  if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "store capacity must be >= 1");
+  const size_t TEA = (size_t)T * (size_t)h->E * (size_t)h->A;
+  const size_t act_elems = TEA * (size_t)(h->spec.n_actions ? 1 : h->spec.act_dim);
+  cudaError_t e;
+  h->obs = (float*)dev_alloc(h, TEA * h->spec.obs_dim * sizeof(float), &e);
+  if (e) return cuda_fail(h, e, "alloc obs");
+  h->act = dev_alloc(h, act_elems * 4, &e);
+  if (e) return cuda_fail(h, e, "alloc act");
+  h->logp = (float*)dev_alloc(h, TEA * sizeof(float), &e);
+  if (e) return cuda_fail(h, e, "alloc logp");
+  h->rew = (float*)dev_alloc(h, TEA * sizeof(float), &e);
+  if (e) return cuda_fail(h, e, "alloc rew");
+  h->done = (uint8_t*)dev_alloc(h, (size_t)T * h->E, &e);
+  if (e) return cuda_fail(h, e, "alloc done");
+  h->stats = (double*)dev_alloc(h, (size_t)T * 4 * sizeof(double), &e);
+  if (e) return cuda_fail(h, e, "alloc stats");
+  h->partials = (ws::Partial*)dev_alloc(h, (size_t)T * ws::n_parts_for(h->spec.kind, h->E) * sizeof(ws::Partial), &e);
+  if (e) return cuda_fail(h, e, "alloc partials");
+  if ((e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(double), h->stream))) return cuda_fail(h, e, "memset stats");
+  h->T_cap = T;
+  return WS_OK;
+}
+
+ws_status check(ws_env* h) {
+  if (!h) return WS_ERR_INVALID_ARGUMENT;
+  h->last_error.clear();
+  return WS_OK;
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ws_abi_version(void) { return WS_ABI_VERSION; }
+
+const char* ws_status_string(ws_status s) {
+  switch (s) {
+    case WS_OK: return "ok";
+    case WS_ERR_INVALID_ARGUMENT: return "invalid argument";
+    case WS_ERR_UNKNOWN_ENV: return "unknown environment";
+    case WS_ERR_INVALID_ACTION: return "invalid action";
+    case WS_ERR_INVALID_PROBS: return "invalid probabilities";
+    case WS_ERR_OUT_OF_RANGE: return "slot out of range";
+    case WS_ERR_BAD_STATE: return "bad call order";
+    case WS_ERR_OUT_OF_MEMORY: return "out of memory";
+    case WS_ERR_CUDA: return "CUDA error";
+  }
+  return "unknown status";
+}
+
+const char* ws_last_error(const ws_env* h) { return h ? h->last_error.c_str() : ""; }
+
+ws_status ws_config_init(ws_config* cfg) {
+  if (!cfg) return WS_ERR_INVALID_ARGUMENT;
+  std::memset(cfg, 0, sizeof(*cfg));
+  cfg->n_agents = 1;
+  cfg->device = -1;
+  cfg->write_logp = 1;
+  return WS_OK;
+}
+
+ws_status ws_create(int64_t n_envs, int32_t n_agents, const char* env, uint64_t seed, ws_env** out) {
+  ws_config c;
+  ws_config_init(&c);
+  c.n_envs = n_envs;
+  c.n_agents = n_agents;
+  c.env = env;
+  c.seed = seed;
+  return ws_create_ex(&c, out);
+}
+
+ws_status ws_create_ex(const ws_config* cfg, ws_env** out) {
+  if (!out) return WS_ERR_INVALID_ARGUMENT;
+  *out = nullptr;
+  if (!cfg) return WS_ERR_INVALID_ARGUMENT;
+  // ---- synchronous validation; no CUDA call before this point
+  EnvSpec spec;
+  if (!lookup_env(cfg->env, cfg->n_agents, cfg->param0, &spec)) return WS_ERR_UNKNOWN_ENV;
+  if (cfg->n_envs < 1 || cfg->n_agents < 1 || cfg->env_offset < 0) return WS_ERR_INVALID_ARGUMENT;
+  const int64_t Eg = cfg->n_envs_global > 0 ? cfg->n_envs_global : cfg->env_offset + cfg->n_envs;
+  if (cfg->env_offset + cfg->n_envs > Eg || Eg > (int64_t)UINT32_MAX) return WS_ERR_INVALID_ARGUMENT;
+  if (spec.kind != ws::kTag && cfg->n_agents != 1) return WS_ERR_INVALID_ARGUMENT;
+  if (cfg->t_capacity < 0 || cfg->max_steps < 0) return WS_ERR_INVALID_ARGUMENT;
+  if (cfg->block_size != 0 && (cfg->block_size % 32 != 0 || cfg->block_size > 256 || cfg->block_size < 32))
+    return WS_ERR_INVALID_ARGUMENT;
+  int p0 = cfg->param0, p1 = cfg->param1;
+  if (spec.kind == ws::kTag) {
+    p0 = p0 > 0 ? p0 : 20;
+    p1 = p1 > 0 ? p1 : std::max(1, cfg->n_agents / 10);
+    if (p0 < 2 || p0 > 64 || p1 > cfg->n_agents || cfg->n_agents > 1024) return WS_ERR_INVALID_ARGUMENT;
+  } else if (spec.kind == ws::kSurface) {
+    p0 = p0 > 0 ? p0 : 20;
+    if (!surface_dim_supported(p0)) return WS_ERR_INVALID_ARGUMENT;
+  }
+  // ---- handle
+  ws_env* h = new ws_env();
+  h->spec = spec;
+  h->env_name = cfg->env;
+  h->E = cfg->n_envs;
+  h->offset = cfg->env_offset;
+  h->E_global = Eg;
+  h->A = cfg->n_agents;
+  h->seed = cfg->seed;
+  h->device = cfg->device;
+  h->stream = (cudaStream_t)cfg->stream;
+  h->max_steps = cfg->max_steps > 0 ? cfg->max_steps : spec.max_steps;
+  h->write_logp = cfg->write_logp ? 1 : 0;
+  h->p0 = p0;
+  h->p1 = p1;
+  h->block = cfg->block_size > 0 ? cfg->block_size : 128;
+  h->alloc = cfg->alloc;
+  h->free_fn = cfg->free;
+  h->alloc_user = cfg->alloc_user;
+  DeviceGuard g(h->device);
+  if (h->device < 0) cudaGetDevice(&h->device);
+  cudaError_t e;
+  const size_t EA = (size_t)h->E * h->A;
+  if (spec.state_dim) {
+    h->state = (float*)dev_alloc(h, (size_t)h->E * spec.state_dim * sizeof(float), &e);
+    if (e) { ws_status s = cuda_fail(h, e, "alloc state"); free_all(h); delete h; return s; }
+  }
+  if (spec.kind == ws::kTag) {
+    h->tstate = (int32_t*)dev_alloc(h, EA * 3 * sizeof(int32_t), &e);
+    if (e) { ws_status s = cuda_fail(h, e, "alloc tag state"); free_all(h); delete h; return s; }
+  }
+  h->obs_live = (float*)dev_alloc(h, EA * spec.obs_dim * sizeof(float), &e);
+  if (!e) h->ep_step = (int32_t*)dev_alloc(h, (size_t)h->E * sizeof(int32_t), &e);
+  if (!e) h->reset_count = (uint32_t*)dev_alloc(h, (size_t)h->E * sizeof(uint32_t), &e);
+  if (!e) h->ep_ret = (float*)dev_alloc(h, EA * sizeof(float), &e);
+  if (!e) h->err = (uint32_t*)dev_alloc(h, sizeof(uint32_t), &e);
+  if (e) { ws_status s = cuda_fail(h, e, "alloc live state"); free_all(h); delete h; return s; }
+  if (cfg->t_capacity > 0) {
+    ws_status s = ensure_store(h, cfg->t_capacity);
+    if (s != WS_OK) { free_all(h); delete h; return s; }
+  }
+  ws_status s = ws_reset(h);
+  if (s != WS_OK) { free_all(h); delete h; return s; }
+  *out = h;
+  return WS_OK;
+}
+
+ws_status ws_destroy(ws_env* h) {
+  if (!h) return WS_OK;
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  free_all(h);
+  delete h;
+  return WS_OK;
+}
+
+ws_status ws_reset(ws_env* h) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaMemsetAsync(h->err, 0, sizeof(uint32_t), h->stream);
+  if (e) return cuda_fail(h, e, "ws_reset memset");
+  if (h->stats && (e = cudaMemsetAsync(h->stats, 0, (size_t)h->T_cap * 4 * sizeof(double), h->stream)))
+    return cuda_fail(h, e, "ws_reset memset stats");
+  if ((e = ws::launch_reset(kargs(h), launch_of(h), &h->launches))) return cuda_fail(h, e, "reset kernel");
+  h->t = 0;
+  h->cursor = 0;
+  h->sampled_slot = -1;
+  return WS_OK;
+}
+
+ws_status ws_rewind(ws_env* h) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  h->cursor = 0;
+  h->sampled_slot = -1;
+  return WS_OK;
+}
+
+ws_status ws_sample(ws_env* h, const float* probs, int64_t row_stride) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (!probs || row_stride < 0) return fail(h, WS_ERR_INVALID_ARGUMENT, "probs must be a device pointer, row_stride >= 0");
+  DeviceGuard g(h->device);
+  ws_status s = ensure_store(h, 1000);
+  if (s) return s;
+  if (h->cursor >= h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "cursor at store capacity (ws_rewind)");
+  cudaError_t e = ws::launch_sample(kargs(h), launch_of(h), h->cursor, h->t, probs, row_stride, &h->launches);
+  if (e) return cuda_fail(h, e, "sample kernel");
+  h->sampled_slot = h->cursor;
+  return WS_OK;
+}
+
+ws_status ws_step(ws_env* h, const void* actions) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  ws_status s = ensure_store(h, 1000);
+  if (s) return s;
+  if (h->cursor >= h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "cursor at store capacity (ws_rewind)");
+  if (!actions && h->sampled_slot != h->cursor) return fail(h, WS_ERR_BAD_STATE, "ws_step(NULL) needs ws_sample first");
+  cudaError_t e = ws::launch_step(kargs(h), launch_of(h), h->cursor, actions, &h->launches);
+  if (e) return cuda_fail(h, e, "step kernel");
+  h->cursor += 1;
+  h->t += 1;
+  h->sampled_slot = -1;
+  return WS_OK;
+}
+
+ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_stride, int64_t step_stride) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
+  if (!probs || row_stride < 0 || step_stride < 0) return fail(h, WS_ERR_INVALID_ARGUMENT, "bad probs / strides");
+  DeviceGuard g(h->device);
+  ws_status s = ensure_store(h, T);
+  if (s) return s;
+  if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
+  cudaError_t e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
+  if (e) return cuda_fail(h, e, "rollout kernel");
+  h->t += (uint64_t)T;
+  h->cursor = T;
+  h->sampled_slot = -1;
+  return WS_OK;
+}
+
+static void sum_stats(const double* st, int n, ws_stats* out) {
+  ws_stats r{};
+  for (int i = 0; i < n; ++i) {
+    r.episodes += st[4 * i + 0];
+    r.sum_return += st[4 * i + 1];
+    r.sum_length += st[4 * i + 2];
+    r.sum_reward += st[4 * i + 3];
+  }
+  const double nan = std::numeric_limits<double>::quiet_NaN();
+  r.mean_return = r.episodes > 0 ? r.sum_return / r.episodes : nan;
+  r.mean_length = r.episodes > 0 ? r.sum_length / r.episodes : nan;
+  *out = r;
+}
+
+ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t n_probs, int64_t row_stride,
+                          int64_t step_stride, ws_stats* out) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (!host_probs || n_probs < 1 || !out) return fail(h, WS_ERR_INVALID_ARGUMENT, "host_probs / n_probs / out");
+  DeviceGuard g(h->device);
+  cudaError_t e;
+  if (h->staging_n < n_probs) {
+    if (h->staging) return fail(h, WS_ERR_INVALID_ARGUMENT, "n_probs grew beyond the first call's staging size");
+    h->staging = (float*)dev_alloc(h, (size_t)n_probs * sizeof(float), &e);
+    if (e) return cuda_fail(h, e, "alloc staging");
+    h->staging_n = n_probs;
+  }
+  if ((e = cudaMemcpyAsync(h->staging, host_probs, (size_t)n_probs * sizeof(float), cudaMemcpyHostToDevice, h->stream)))
+    return cuda_fail(h, e, "H2D probs");
+  ws_status s = ws_rollout(h, T, h->staging, row_stride, step_stride);
+  if (s) return s;
+  if ((int)h->host_stats.size() < 4 * T) h->host_stats.resize(4 * (size_t)T);
+  if ((e = cudaMemcpyAsync(h->host_stats.data(), h->stats, (size_t)T * 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream)))
+    return cuda_fail(h, e, "D2H stats");
+  if ((e = cudaStreamSynchronize(h->stream))) return cuda_fail(h, e, "sync");
+  sum_stats(h->host_stats.data(), T, out);
+  return WS_OK;
+}
+
+static ws_tensor tensor(void* p, ws_dtype dt, std::initializer_list<int64_t> shape) {
+  ws_tensor t{};
+  t.ptr = p;
+  t.dtype = dt;
+  t.ndim = (int32_t)shape.size();
+  int i = 0;
+  for (int64_t s : shape) t.shape[i++] = s;
+  return t;
+}
+
+ws_status ws_get_buffers(const ws_env* h, ws_buffers* out) {
+  if (!h || !out) return WS_ERR_INVALID_ARGUMENT;
+  const int64_t T = h->T_cap, E = h->E, A = h->A, D = h->spec.obs_dim;
+  std::memset(out, 0, sizeof(*out));
+  out->obs = tensor(h->obs, WS_F32, {T, E, A, D});
+  if (h->spec.n_actions) out->act = tensor(h->act, WS_I32, {T, E, A});
+  else out->act = tensor(h->act, WS_F32, {T, E, A, h->spec.act_dim});
+  out->logp = tensor(h->logp, WS_F32, {T, E, A});
+  out->rew = tensor(h->rew, WS_F32, {T, E, A});
+  out->done = tensor(h->done, WS_U8, {T, E});
+  out->stats = tensor(h->stats, WS_F64, {T, 4});
+  if (h->spec.kind == ws::kTag) out->state = tensor(h->tstate, WS_I32, {E, A, 3});
+  else out->state = tensor(h->state, WS_F32, {E, h->spec.state_dim});
+  out->obs_live = tensor(h->obs_live, WS_F32, {E, A, D});
+  out->ep_step = tensor(h->ep_step, WS_I32, {E});
+  out->reset_count = tensor(h->reset_count, WS_U32, {E});
+  out->ep_ret = tensor(h->ep_ret, WS_F32, {E, A});
+  return WS_OK;
+}
+
+ws_status ws_get_info(const ws_env* h, ws_info* out) {
+  if (!h || !out) return WS_ERR_INVALID_ARGUMENT;
+  std::memset(out, 0, sizeof(*out));
+  out->obs_dim = h->spec.obs_dim;
+  out->n_actions = h->spec.n_actions;
+  out->act_dim = h->spec.act_dim;
+  out->state_dim = h->spec.state_dim;
+  out->max_steps = h->max_steps;
+  out->n_agents = h->A;
+  out->t_capacity = h->T_cap;
+  out->cursor = h->cursor;
+  out->n_envs = h->E;
+  out->env_offset = h->offset;
+  out->n_envs_global = h->E_global;
+  out->t = h->t;
+  out->launches = h->launches;
+  out->probs_width = h->spec.n_actions ? h->spec.n_actions : 2 * h->spec.act_dim;
+  return WS_OK;
+}
+
+ws_status ws_synchronize(ws_env* h) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e) return cuda_fail(h, e, "ws_synchronize");
+  uint32_t word = 0;
+  if ((e = cudaMemcpy(&word, h->err, sizeof(word), cudaMemcpyDeviceToHost))) return cuda_fail(h, e, "read error word");
+  if (word & ws::kErrProbs) return fail(h, WS_ERR_INVALID_PROBS, "a probability row was invalid (sticky until ws_reset)");
+  if (word & ws::kErrAction) return fail(h, WS_ERR_INVALID_ACTION, "an action was invalid (sticky until ws_reset)");
+  return WS_OK;
+}
+
+ws_status ws_read_stats(ws_env* h, int32_t t0, int32_t t1, ws_stats* out) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (!out || t0 < 0 || t1 < t0 || t1 > h->T_cap) return fail(h, WS_ERR_INVALID_ARGUMENT, "bad slot range");
+  DeviceGuard g(h->device);
+  std::vector<double> st(4 * (size_t)(t1 - t0) + 4);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (!e && t1 > t0) e = cudaMemcpy(st.data(), h->stats + 4 * (size_t)t0, 4 * sizeof(double) * (t1 - t0), cudaMemcpyDeviceToHost);
+  if (e) return cuda_fail(h, e, "ws_read_stats");
+  sum_stats(st.data(), t1 - t0, out);
+  return WS_OK;
+}
+
+ws_status ws_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, void* stream) {
+  if (!rows || !out || n < 0) return WS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return WS_OK;
+  cudaError_t e = ws::launch_test_philox(rows, n, out, (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_test_sample_grid(const float* p, int32_t n, int64_t* counts, void* stream) {
+  if (!p || !counts || n < 1 || n > 8) return WS_ERR_INVALID_ARGUMENT;
+  cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(n + 1) * sizeof(int64_t), (cudaStream_t)stream);
+  if (!e) e = ws::launch_test_sample_grid(p, n, counts, (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,165 @@
+// sampler.cuh -- A2: action sampling from given policy probabilities ("operating an
+// agent that samples actions"; S:322-325 inverse CDF / mean + std * gaussian; BJ:5 "a
+// warp-level prefix sum and search over per-agent probabilities").
+//
+// Discrete rows: a warp loads the probability rows of its 32 owners coalesced (lanes walk
+// the flattened (row, action) index, floor(32/N) rows per 32-lane chunk), runs a segmented
+// Hillis-Steele inclusive scan in fp64 with __shfl_up_sync, and each owner lane gathers its
+// row's CDF with __shfl_sync.  The search then picks min{i : p_i > 0 and u*S < C_i}, with
+// the last nonzero action as fallback (R13).  For fp32 inputs whose magnitudes span less
+// than 2^29 the fp64 prefix sums are exact, so the result is independent of association
+// order and bit-identical to a sequential fp64 CDF (R16).
+//
+// When the probabilities are the same every step (step_stride 0) the search is hoisted:
+// per action i the integer threshold K_i = #{k in [0,2^24) : k 2^-24 S < C_i} is found once
+// by bisection on the same fp64 predicate, and each step compares the 24-bit draw k = w>>8
+// with K_i -- the identical decision for every k.
+#pragma once
+
+#include "common.cuh"
+
+namespace ws {
+
+template <int N>
+struct RowCDF {
+  double C[N];  // inclusive prefix sums (fp64)
+  float P[N];   // the row itself
+  bool bad;     // R13: p < 0, NaN / inf, or non-positive / non-finite sum
+};
+
+// Rows first_row + r (r = 0..31, row r owned by lane r); rows >= n_rows are absent.
+template <int N>
+__device__ __forceinline__ void warp_row_cdf(const float* __restrict__ probs, int64_t row_stride,
+                                             int64_t first_row, int64_t n_rows, int lane,
+                                             RowCDF<N>& out) {
+  static_assert(N >= 1 && N <= 32, "rows of 1..32 actions");
+  constexpr int RPC = 32 / N;                 // rows per 32-lane chunk
+  constexpr int NCH = (32 + RPC - 1) / RPC;   // chunks covering 32 rows
+  const int col = lane % N;
+  const int rl = lane / N;
+  const int src_base = (lane % RPC) * N;      // where this lane's own row sits in its chunk
+  const int my_chunk = lane / RPC;
+#pragma unroll
+  for (int j = 0; j < NCH; ++j) {
+    const int rr = j * RPC + rl;
+    const bool valid = (lane < RPC * N) && (rr < 32) && (first_row + rr < n_rows);
+    const float p = valid ? __ldg(probs + (first_row + rr) * row_stride + col) : 0.0f;
+    double v = (double)p;
+#pragma unroll
+    for (int off = 1; off < N; off <<= 1) {
+      const double t = __shfl_up_sync(kFull, v, off);
+      if (col >= off) v += t;
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const double c = __shfl_sync(kFull, v, src_base + i);
+      const float pi = __shfl_sync(kFull, p, src_base + i);
+      if (my_chunk == j) {
+        out.C[i] = c;
+        out.P[i] = pi;
+      }
+    }
+  }
+  bool bad = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) bad = bad || !(out.P[i] >= 0.0f) || !isfinite(out.P[i]);
+  const double S = out.C[N - 1];
+  out.bad = bad || !(S > 0.0) || !isfinite(S);
+}
+
+template <int N>
+__device__ __forceinline__ int last_nonzero(const RowCDF<N>& r) {
+  int last = 0;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (r.P[i] > 0.0f) last = i;
+  return last;
+}
+
+// Direct search for uniform u (fp32, exact multiple of 2^-24).
+template <int N>
+__device__ __forceinline__ int search(const RowCDF<N>& r, float u) {
+  const double target = (double)u * r.C[N - 1];
+  int a = -1;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (a < 0 && r.P[i] > 0.0f && target < r.C[i]) a = i;
+  return a < 0 ? last_nonzero(r) : a;
+}
+
+// R13 log-probability: (float)(log p_a - log S), both logs in fp64 (R3).
+template <int N>
+__device__ __forceinline__ float logp_of(const RowCDF<N>& r, int a) {
+  float pa = r.P[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    if (a == i) pa = r.P[i];
+  return (float)(log((double)pa) - log(r.C[N - 1]));
+}
+
+// Hoisted search for step_stride == 0.
+template <int N>
+struct Thresholds {
+  uint32_t K[N];     // draw k selects action i iff i is the first nonzero with k < K_i
+  float lp[N];       // log-probability of each action
+  uint32_t nzmask;
+  int fallback;
+  bool bad;
+};
+
+template <int N>
+__device__ __forceinline__ void make_thresholds(const RowCDF<N>& r, Thresholds<N>& th) {
+  th.bad = r.bad;
+  th.nzmask = 0;
+  th.fallback = last_nonzero(r);
+  const double S = r.C[N - 1];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    if (r.P[i] > 0.0f) th.nzmask |= 1u << i;
+    uint32_t lo = 0, hi = 1u << 24;  // smallest k with !(k 2^-24 S < C_i)
+    if (!r.bad) {
+      while (lo < hi) {
+        const uint32_t mid = (lo + hi) >> 1;
+        const double target = (double)((float)mid * (1.0f / 16777216.0f)) * S;
+        if (target < r.C[i]) lo = mid + 1; else hi = mid;
+      }
+    }
+    th.K[i] = lo;
+    th.lp[i] = (r.P[i] > 0.0f && !r.bad) ? (float)(log((double)r.P[i]) - log(S)) : 0.0f;
+  }
+}
+
+template <int N>
+__device__ __forceinline__ int search_k(const Thresholds<N>& th, uint32_t k, float& lp) {
+  int a = -1;
+#pragma unroll
+  for (int i = 0; i < N; ++i)
+    if (a < 0 && ((th.nzmask >> i) & 1u) && k < th.K[i]) a = i;
+  if (a < 0) a = th.fallback;
+  lp = th.lp[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    if (a == i) lp = th.lp[i];
+  return a;
+}
+
+// ---------------------------------------------------------------------------------------
+// Continuous head: z_k of agent a at step t is Gaussian draw j = t*d + k of the GAUSS
+// stream: Box-Muller on the word pair (2p, 2p+1), p = (j & 3) >> 1, u1 in (0, 1],
+// u2 in [0, 1); even j -> r cos, odd j -> r sin; fp64, one rounding (R14, R3).
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ float gauss_z(const Key& key, uint32_t eg, uint32_t agent, uint64_t j) {
+  const U4 b = block(key, j >> 2, eg, agent, kGauss);
+  const bool second = ((j & 3) >> 1) != 0;
+  const uint32_t w0 = second ? b.z : b.x, w1 = second ? b.w : b.y;
+  const double u1 = (double)((w0 >> 8) + 1) * (1.0 / 16777216.0);
+  const double u2 = (double)(w1 >> 8) * (1.0 / 16777216.0);
+  const double r = sqrt(-2.0 * log(u1));
+  const double ang = 2.0 * 3.14159265358979323846 * u2;
+  return (float)((j & 1) ? r * sin(ang) : r * cos(ang));
+}
+
+// R14 log-density constant 0.5 * log(fl64(2 pi)) (= 0.5 * log(6.283185307179586)).
+constexpr double kHalfLog2Pi = 0.9189385332046727;
+
+}  // namespace ws

@@ -1,0 +1,278 @@
+"""Thin Python binding of libws (include/ws.h): same call names, argument marshalling only.
+
+PyTorch provides device memory (libws's allocator hooks are routed to torch's caching
+allocator, so every byte is a torch tensor), the CUDA stream, and -- in parallel.py -- the
+process group; every step of the roll-out runs in libws's sm_100a kernels.
+
+    env = Env(10_000, 1, "cartpole", seed=0x24080930)
+    probs = torch.full((10_000, 1, 2), 0.5, device="cuda")
+    env.rollout(1000, probs)            # ws_rollout: one fused kernel + stats finalize
+    buf = env.buffers()                 # zero-copy torch views of the store (ws_get_buffers)
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+
+from . import _abi
+from ._abi import WSError, check, lib
+
+_TORCH_DTYPE = {_abi.F32: torch.float32, _abi.I32: torch.int32, _abi.U8: torch.uint8,
+                _abi.F64: torch.float64, _abi.U32: torch.uint32}
+
+
+class _TorchAllocator:
+    """libws allocation hooks backed by torch's caching allocator; counts calls so the
+    zero-steady-state-allocation invariant can be asserted."""
+
+    def __init__(self, device: torch.device):
+        self.device = device
+        self.live: dict[int, torch.Tensor] = {}
+        self.n_alloc = 0
+        self.n_free = 0
+        self.bytes = 0
+
+        def _alloc(nbytes, stream, user):
+            t = torch.empty(int(nbytes), dtype=torch.uint8, device=self.device)
+            p = t.data_ptr()
+            self.live[p] = t
+            self.n_alloc += 1
+            self.bytes += int(nbytes)
+            return p
+
+        def _free(ptr, nbytes, stream, user):
+            self.live.pop(int(ptr), None)
+            self.n_free += 1
+
+        self.c_alloc = _abi.ALLOC_FN(_alloc)
+        self.c_free = _abi.FREE_FN(_free)
+
+
+def _ptr(t: Optional[torch.Tensor]):
+    return None if t is None else C.c_void_p(t.data_ptr())
+
+
+class Env:
+    """A handle of libws (ws_env*): E replicas of `env` on one GPU."""
+
+    def __init__(self, n_envs: int, n_agents: int = 1, env: str = "cartpole", seed: int = 0, *,
+                 env_offset: int = 0, n_envs_global: int = 0, device=None, stream: Optional[torch.cuda.Stream] = None,
+                 t_capacity: int = 0, max_steps: int = 0, write_logp: bool = True, param0: int = 0,
+                 param1: int = 0, block_size: int = 0, torch_allocator: bool = True):
+        L = lib()
+        if not torch.cuda.is_available():
+            raise WSError(_abi.CUDA_ERROR, "no CUDA device: libws runs on the GPU only (no CPU fallback)")
+        self.device = torch.device("cuda", torch.cuda.current_device() if device is None else torch.device(device).index or 0)
+        self.stream = stream if stream is not None else torch.cuda.current_stream(self.device)
+        cfg = _abi.ws_config()
+        L.ws_config_init(C.byref(cfg))
+        cfg.n_envs = n_envs
+        cfg.env_offset = env_offset
+        cfg.n_envs_global = n_envs_global
+        cfg.n_agents = n_agents
+        self._env_name = env.encode()
+        cfg.env = self._env_name
+        cfg.seed = seed & 0xFFFFFFFFFFFFFFFF
+        cfg.device = self.device.index
+        cfg.stream = self.stream.cuda_stream
+        cfg.t_capacity = t_capacity
+        cfg.max_steps = max_steps
+        cfg.write_logp = 1 if write_logp else 0
+        cfg.param0 = param0
+        cfg.param1 = param1
+        cfg.block_size = block_size
+        self.allocator = _TorchAllocator(self.device) if torch_allocator else None
+        if self.allocator is not None:
+            cfg.alloc = self.allocator.c_alloc
+            cfg.free = self.allocator.c_free
+        h = C.c_void_p()
+        with torch.cuda.device(self.device):
+            st = L.ws_create_ex(C.byref(cfg), C.byref(h))
+        check(st)
+        self._h = h
+        self.env = env
+        self.n_envs, self.n_agents = n_envs, n_agents
+        self._views = None
+
+    # ------------------------------------------------------------------ lifetime
+    def close(self):
+        h = getattr(self, "_h", None)
+        if h:
+            lib().ws_destroy(h)
+            self._h = None
+            self._views = None
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:
+            pass
+
+    @property
+    def handle(self):
+        return self._h
+
+    # ------------------------------------------------------------------ calls
+    def _row_stride(self, probs: torch.Tensor, row_stride: Optional[int]) -> int:
+        if row_stride is not None:
+            return row_stride
+        return 0 if probs.dim() == 1 else probs.shape[-1]
+
+    def _check_probs(self, probs: torch.Tensor):
+        if probs.device != self.device or probs.dtype != torch.float32 or not probs.is_contiguous():
+            raise WSError(_abi.INVALID_ARGUMENT, "probs must be a contiguous float32 tensor on the handle's device")
+
+    def reset(self):
+        check(lib().ws_reset(self._h), self._h)
+
+    def rewind(self):
+        check(lib().ws_rewind(self._h), self._h)
+
+    def sample(self, probs: torch.Tensor, row_stride: Optional[int] = None):
+        self._check_probs(probs)
+        check(lib().ws_sample(self._h, _ptr(probs), self._row_stride(probs, row_stride)), self._h)
+
+    def step(self, actions: Optional[torch.Tensor] = None):
+        if actions is not None:
+            info = self.info()
+            want = torch.int32 if info.n_actions else torch.float32
+            if actions.device != self.device or actions.dtype != want or not actions.is_contiguous():
+                raise WSError(_abi.INVALID_ARGUMENT, f"actions must be contiguous {want} on the handle's device")
+        check(lib().ws_step(self._h, _ptr(actions)), self._h)
+
+    def rollout(self, T: int, probs: torch.Tensor, row_stride: Optional[int] = None, step_stride: int = 0):
+        self._check_probs(probs)
+        check(lib().ws_rollout(self._h, T, _ptr(probs), self._row_stride(probs, row_stride), step_stride), self._h)
+
+    def rollout_host(self, T: int, host_probs: torch.Tensor, row_stride: Optional[int] = None,
+                     step_stride: int = 0) -> _abi.ws_stats:
+        """ws_rollout_host: host (ideally pinned) probabilities in, statistics out."""
+        if host_probs.device.type != "cpu" or host_probs.dtype != torch.float32 or not host_probs.is_contiguous():
+            raise WSError(_abi.INVALID_ARGUMENT, "host_probs must be a contiguous float32 CPU tensor")
+        out = _abi.ws_stats()
+        check(lib().ws_rollout_host(self._h, T, _ptr(host_probs), host_probs.numel(),
+                                    self._row_stride(host_probs, row_stride), step_stride, C.byref(out)), self._h)
+        return out
+
+    def synchronize(self):
+        check(lib().ws_synchronize(self._h), self._h)
+
+    def status(self) -> int:
+        """ws_synchronize without raising: returns the ws_status."""
+        return lib().ws_synchronize(self._h)
+
+    def read_stats(self, t0: int = 0, t1: Optional[int] = None) -> _abi.ws_stats:
+        info = self.info()
+        out = _abi.ws_stats()
+        check(lib().ws_read_stats(self._h, t0, info.cursor if t1 is None else t1, C.byref(out)), self._h)
+        return out
+
+    def info(self) -> _abi.ws_info:
+        out = _abi.ws_info()
+        check(lib().ws_get_info(self._h, C.byref(out)))
+        return out
+
+    # ------------------------------------------------------------------ zero-copy views
+    def buffers(self) -> dict[str, torch.Tensor]:
+        """ws_get_buffers as torch tensors aliasing libws's device memory (no copy)."""
+        raw = _abi.ws_buffers()
+        check(lib().ws_get_buffers(self._h, C.byref(raw)))
+        out = {}
+        for name in _abi.BUFFER_NAMES:
+            t = getattr(raw, name)
+            shape = tuple(int(t.shape[i]) for i in range(t.ndim))
+            out[name] = self._view(t.ptr, _TORCH_DTYPE[t.dtype], shape)
+        return out
+
+    def _view(self, ptr, dtype, shape) -> Optional[torch.Tensor]:
+        if not ptr:
+            return None
+        n = 1
+        for s in shape:
+            n *= s
+        if self.allocator is not None and ptr in self.allocator.live:
+            owner = self.allocator.live[ptr]
+            nbytes = n * torch.empty((), dtype=dtype).element_size()
+            return owner[:nbytes].view(dtype).view(shape)
+
+        class _CAI:  # __cuda_array_interface__ for buffers libws allocated itself
+            pass
+        typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1", torch.float64: "<f8",
+                   torch.uint32: "<u4"}[dtype]
+        obj = _CAI()
+        obj.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr), False),
+                                        "version": 3, "strides": None}
+        return torch.as_tensor(obj, device=self.device)
+
+
+# ---------------------------------------------------------------------- C-ABI-named functions
+def ws_create(n_envs: int, n_agents: int, env: str, seed: int) -> Env:
+    return Env(n_envs, n_agents, env, seed)
+
+
+def ws_create_ex(**cfg) -> Env:
+    n_envs = cfg.pop("n_envs")
+    return Env(n_envs, cfg.pop("n_agents", 1), cfg.pop("env", "cartpole"), cfg.pop("seed", 0), **cfg)
+
+
+def ws_destroy(h: Env):
+    h.close()
+
+
+def ws_reset(h: Env):
+    h.reset()
+
+
+def ws_rewind(h: Env):
+    h.rewind()
+
+
+def ws_sample(h: Env, probs: torch.Tensor, row_stride: Optional[int] = None):
+    h.sample(probs, row_stride)
+
+
+def ws_step(h: Env, actions: Optional[torch.Tensor] = None):
+    h.step(actions)
+
+
+def ws_rollout(h: Env, T: int, probs: torch.Tensor, row_stride: Optional[int] = None, step_stride: int = 0):
+    h.rollout(T, probs, row_stride, step_stride)
+
+
+def ws_rollout_host(h: Env, T: int, host_probs: torch.Tensor, row_stride: Optional[int] = None, step_stride: int = 0):
+    return h.rollout_host(T, host_probs, row_stride, step_stride)
+
+
+def ws_get_buffers(h: Env) -> dict:
+    return h.buffers()
+
+
+def ws_get_info(h: Env):
+    return h.info()
+
+
+def ws_synchronize(h: Env):
+    h.synchronize()
+
+
+def ws_read_stats(h: Env, t0: int = 0, t1: Optional[int] = None):
+    return h.read_stats(t0, t1)
+
+
+def ws_test_philox(rows: torch.Tensor) -> torch.Tensor:
+    """rows: [n, 6] int32/uint32 device (c0..c3, k0, k1) -> [n, 4] Philox words (int32 view)."""
+    rows = rows.contiguous()
+    out = torch.empty((rows.shape[0], 4), dtype=torch.int32, device=rows.device)
+    check(lib().ws_test_philox(_ptr(rows), rows.shape[0], _ptr(out), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out
+
+
+def ws_test_sample_grid(p: torch.Tensor) -> torch.Tensor:
+    """Exhaustive 2^24-grid counts of the library sampler for one row p (n <= 8) -> [n + 1]
+    (the last entry counts direct-vs-hoisted search disagreements)."""
+    p = p.contiguous().float()
+    counts = torch.zeros(p.numel() + 1, dtype=torch.int64, device=p.device)
+    check(lib().ws_test_sample_grid(_ptr(p), p.numel(), _ptr(counts), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return counts

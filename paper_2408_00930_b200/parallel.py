@@ -1,0 +1,40 @@
+"""Multi-GPU plumbing: one process per GPU, replicas
+sharded contiguously across ranks, and the one real exchange of the path -- the sum
+all-reduce of the per-slot episode statistics (BJ:5 "NCCL over NVLink used only for the
+per-step episode-return and statistics all-reduce").
+
+Every Philox stream is keyed by the GLOBAL replica index (DESIGN R15), so each replica's
+trajectory is bit-identical whatever the number of ranks; only the statistics cross GPUs.
+"""
+from __future__ import annotations
+
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+
+def shard(n_envs_global: int, world: int, rank: int) -> tuple[int, int]:
+    """Contiguous balanced replica range of `rank` (S:167-175 partition_lanes): sizes differ
+    by at most 1; returns (env_offset, n_envs)."""
+    if world < 1 or not 0 <= rank < world:
+        raise ValueError("need world >= 1 and 0 <= rank < world")
+    lo = n_envs_global * rank // world
+    hi = n_envs_global * (rank + 1) // world
+    return lo, hi - lo
+
+
+def allreduce_stats(stats: torch.Tensor, group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
+    """In-place SUM all-reduce of a [T, 4] float64 statistics view across ranks (NCCL on the
+    GPU path; gloo in the CPU tests).  Counts are exact integers in fp64 (< 2^53)."""
+    if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
+        dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
+    return stats
+
+
+def summarize(stats: torch.Tensor) -> dict:
+    """Episode statistics over slots (P:93 average episodic reward, P:132 episodic step)."""
+    s = stats.double().sum(dim=0).tolist()
+    n = s[0]
+    return {"episodes": n, "mean_return": s[1] / n if n else float("nan"),
+            "mean_length": s[2] / n if n else float("nan"), "sum_reward": s[3]}

@@ -1,0 +1,103 @@
+"""CPU-only checks of the boundary: libws.so loads, exports every function include/ws.h
+declares, and its host-side argument validation answers without a GPU;
+sharding arithmetic and the statistics merge of the multi-GPU path."""
+import ctypes as C
+
+import numpy as np
+import pytest
+import torch
+
+import paper_2408_00930_b200 as P
+from paper_2408_00930_b200 import _abi
+from paper_2408_00930_b200.parallel import shard, summarize
+
+
+def test_library_exports_every_declared_symbol():
+    names = P.declared_functions()
+    assert len(names) >= 17
+    L = P.lib()
+    for n in names:
+        assert hasattr(L, n), n
+    assert L.ws_abi_version() == 1
+
+
+def test_config_init_defaults():
+    cfg = _abi.ws_config()
+    assert P.lib().ws_config_init(C.byref(cfg)) == 0
+    assert cfg.n_agents == 1 and cfg.device == -1 and cfg.write_logp == 1 and cfg.t_capacity == 0
+
+
+def test_struct_layouts_match_header():
+    # sizes the C compiler gives the ws.h structs on x86-64 (natural alignment)
+    assert C.sizeof(_abi.ws_tensor) == 8 + 4 + 4 + 5 * 8
+    assert C.sizeof(_abi.ws_buffers) == 11 * C.sizeof(_abi.ws_tensor)
+    assert C.sizeof(_abi.ws_stats) == 6 * 8
+    assert C.sizeof(_abi.ws_info) == 8 * 4 + 3 * 8 + 2 * 8 + 2 * 4
+    assert C.sizeof(_abi.ws_config) == 8 * 3 + 8 + 8 + 8 + 8 + 8 + 6 * 4 + 3 * 8
+
+
+def _create(**kw):
+    L = P.lib()
+    cfg = _abi.ws_config()
+    L.ws_config_init(C.byref(cfg))
+    cfg.n_envs = kw.get("n_envs", 4)
+    cfg.n_agents = kw.get("n_agents", 1)
+    name = kw.get("env", "cartpole").encode()
+    cfg.env = name
+    cfg.env_offset = kw.get("env_offset", 0)
+    cfg.n_envs_global = kw.get("n_envs_global", 0)
+    cfg.param0 = kw.get("param0", 0)
+    cfg.block_size = kw.get("block_size", 0)
+    h = C.c_void_p()
+    st = L.ws_create_ex(C.byref(cfg), C.byref(h))
+    return st, h
+
+
+@pytest.mark.parametrize("kw,status", [
+    (dict(n_envs=0), _abi.INVALID_ARGUMENT),                      # S:138 E = 0
+    (dict(env="nosuch"), _abi.UNKNOWN_ENV),
+    (dict(n_agents=2), _abi.INVALID_ARGUMENT),                    # single-agent env
+    (dict(env_offset=5, n_envs=4, n_envs_global=8), _abi.INVALID_ARGUMENT),  # shard past E_g
+    (dict(env="surface", param0=7), _abi.INVALID_ARGUMENT),       # unsupported surface dimension
+    (dict(block_size=48), _abi.INVALID_ARGUMENT),                 # launch shape must be k*32
+])
+def test_create_validates_before_touching_the_gpu(kw, status):
+    st, h = _create(**kw)
+    assert st == status and not h.value
+
+
+def test_null_handle_and_status_strings():
+    L = P.lib()
+    assert L.ws_reset(None) == _abi.INVALID_ARGUMENT
+    assert L.ws_destroy(None) == _abi.OK
+    for s in range(9):
+        assert L.ws_status_string(s)
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
+def test_product_path_fails_loudly_without_gpu():
+    with pytest.raises(P.WSError):
+        P.Env(4, 1, "cartpole", 0)
+    st, h = _create()
+    assert st == _abi.CUDA_ERROR and not h.value  # no silent CPU fallback
+
+
+def test_shard_balanced_contiguous():
+    """E=10, W=3 -> [0,4) [4,7) [7,10) (lane analog: sizes differ by <= 1)."""
+    assert [shard(10, 3, r) for r in range(3)] == [(0, 3), (3, 3), (6, 4)] or \
+        [shard(10, 3, r) for r in range(3)] == [(0, 4), (4, 3), (7, 3)]
+    for E in (1, 2, 10, 10000, 100003):
+        for W in (1, 2, 3, 4, 8):
+            parts = [shard(E, W, r) for r in range(W)]
+            assert parts[0][0] == 0
+            for (o1, n1), (o2, n2) in zip(parts, parts[1:]):
+                assert o1 + n1 == o2
+            assert sum(n for _, n in parts) == E
+            assert max(n for _, n in parts) - min(n for _, n in parts) <= 1
+    assert [n for _, n in (shard(2, 4, r) for r in range(4))].count(0) == 2
+
+
+def test_summarize():
+    st = torch.tensor([[2, 40, 30, 5], [0, 0, 0, 5], [1, 10, 10, 5]], dtype=torch.float64)
+    s = summarize(st)
+    assert s["episodes"] == 3 and s["mean_return"] == 50 / 3 and s["mean_length"] == 40 / 3
