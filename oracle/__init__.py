@@ -51,6 +51,7 @@ def lib():
             "wso_gauss": (F, [U64, U64, U32, U64, I, I]),
             "wso_sample_discrete": (I, [P, I, F, P, P, P]),
             "wso_sample_grid": (I64, [P, I, P]),
+            "wso_sincos_f32": (None, [P, I64, P, P]),
             "wso_cartpole_step_f32": (I, [P, I, P, P, P]),
             "wso_cartpole_step_f64": (I, [P, I, P, P, P]),
             "wso_acrobot_step_f32": (I, [P, I, P, P, P]),
@@ -121,6 +122,14 @@ def sample_grid(p):
     counts = np.zeros(len(pa), np.int64)
     amb = lib().wso_sample_grid(_p(pa), len(pa), _p(counts))
     return counts, int(amb)
+
+
+def sincos_f32(x):
+    """(float)sin((double)x), (float)cos((double)x) with the host libm (reading Q3)."""
+    xa = np.ascontiguousarray(x, dtype=np.float32)
+    s = np.empty_like(xa); c = np.empty_like(xa)
+    lib().wso_sincos_f32(_p(xa), xa.size, _p(s), _p(c))
+    return s, c
 
 
 def _step4(fn32, fn64, s, a, f64):

@@ -708,6 +708,14 @@ int64_t wso_sample_grid(const float* p, int n, int64_t* counts) {
   return amb_total;
 }
 
+/* the transcendental contract (Tr<float>, reading Q3) on n inputs */
+void wso_sincos_f32(const float* x, int64_t n, float* s, float* c) {
+  for (int64_t i = 0; i < n; ++i) {
+    s[i] = Tr<float>::sin(x[i]);
+    c[i] = Tr<float>::cos(x[i]);
+  }
+}
+
 int wso_cartpole_step_f32(const float* s, int a, float* out, float* r, int* term) {
   return CartPole<float>::step(s, a, out, r, term);
 }

@@ -13,6 +13,8 @@
 //  k_finalize           A8: fixed-order reduction of the per-slot partials to stats[T, 4].
 #include <cuda_runtime.h>
 
+#include <type_traits>
+
 #include "common.cuh"
 #include "envs.cuh"
 #include "kernels.h"
@@ -47,8 +49,12 @@ struct Lane<CartPole> {
     const float4 v = make_float4(s.x, s.xd, s.th, s.thd);
     if (cs) st_cs(reinterpret_cast<float4*>(dst), v); else *reinterpret_cast<float4*>(dst) = v;
   }
-  __device__ static void step(St& s, int a, float& r, bool& term) { CartPole::step(s, a, r, term); }
+  template <bool kFast>
+  __device__ static void step(St& s, int a, float& r, bool& term) { CartPole::step<kFast>(s, a, r, term); }
   __device__ static bool valid(int a) { return CartPole::valid(a); }
+  // natural episodes last >= 8 steps (tests/test_oracle_envs.py::test_cartpole_min_episode_length)
+  static constexpr int kMinEpisode = 8;
+  __device__ static bool fast_ok(const St& s) { return CartPole::fast_ok(s); }
 };
 
 template <>
@@ -77,8 +83,11 @@ struct Lane<Acrobot> {
     if (cs) { st_cs(d, a); st_cs(d + 1, b); st_cs(d + 2, c); }
     else { d[0] = a; d[1] = b; d[2] = c; }
   }
+  template <bool kFast>
   __device__ static void step(St& s, int a, float& r, bool& term) { Acrobot::step(s, a, r, term); }
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
+  static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
+  __device__ static bool fast_ok(const St&) { return true; }
 };
 
 // Dummy (S:164 calibration env): constant zero observation, reward 1, truncation only.
@@ -97,11 +106,14 @@ struct Lane<Dummy> {
     const float4 z = make_float4(0.f, 0.f, 0.f, 0.f);
     if (cs) st_cs(reinterpret_cast<float4*>(dst), z); else *reinterpret_cast<float4*>(dst) = z;
   }
+  template <bool kFast>
   __device__ static void step(St&, int, float& r, bool& term) {
     r = 1.0f;
     term = false;
   }
   __device__ static bool valid(int a) { return a == 0 || a == 1; }
+  static constexpr int kMinEpisode = 1 << 30;  // episodes end by truncation only
+  __device__ static bool fast_ok(const St&) { return true; }
 };
 
 template <>
@@ -202,88 +214,115 @@ __device__ __forceinline__ bool gauss_sample(const Key& key, uint32_t eg, uint32
 }
 
 // =======================================================================================
-// Per-slot statistics of a warp of 32 replicas (A8); lane 0 writes the partial.
+// A8: per-warp statistics window in shared memory.  Each lane records its per-slot
+// contribution (done ? episode length : 0, done ? episode return : 0, reward) in row
+// (slot & 31); every 32 slots (and at the end) lane i reduces row i over the 32 lanes in
+// lane order -- a fixed, launch-shape-independent order -- and writes that slot's partial
+// with one 16-byte store.  Rows are 36 words apart: 16-byte aligned and free of bank
+// conflicts for the quarter-warp phases of LDS.128.
 // =======================================================================================
-__device__ __forceinline__ void warp_partial(Partial* dst, int lane, bool done, int32_t len, float ret,
-                                             float rew) {
-  const uint32_t nd = __reduce_add_sync(kFull, done ? 1u : 0u);
-  const uint32_t ln = __reduce_add_sync(kFull, done ? (uint32_t)len : 0u);
-  const float rs = warp_sum_f32(rew);
-  float rt = 0.0f;
-  if (nd) rt = warp_sum_f32(done ? ret : 0.0f);
-  if (lane == 0) {
-    uint4 v = make_uint4(nd, ln, __float_as_uint(rt), __float_as_uint(rs));
-    __stcs(reinterpret_cast<uint4*>(dst), v);
+constexpr int kWinStride = 36;
+constexpr int kWinWords = 3 * 32 * kWinStride;  // per warp (13.5 KiB)
+
+struct StatsWindow {
+  uint32_t* len;
+  float* ret;
+  float* rew;
+  __device__ __forceinline__ void init(uint32_t* base) {
+    len = base;
+    ret = reinterpret_cast<float*>(base + 32 * kWinStride);
+    rew = reinterpret_cast<float*>(base + 64 * kWinStride);
   }
+  __device__ __forceinline__ void put(int row, int lane, uint32_t l, float rt, float rw) {
+    len[row * kWinStride + lane] = l;
+    ret[row * kWinStride + lane] = rt;
+    rew[row * kWinStride + lane] = rw;
+  }
+  // rows [row_lo, row_hi] -> partials of slots slot0 + row (row 0 may precede the
+  // roll-out's first slot, hence the signed slot0); part_base = partials + part
+  __device__ __forceinline__ void flush(int lane, int row_lo, int row_hi, int64_t slot0, Partial* part_base,
+                                        int n_parts) {
+    __syncwarp();
+    if (lane >= row_lo && lane <= row_hi) {
+      const uint4* l4 = reinterpret_cast<const uint4*>(len + lane * kWinStride);
+      const float4* t4 = reinterpret_cast<const float4*>(ret + lane * kWinStride);
+      const float4* r4 = reinterpret_cast<const float4*>(rew + lane * kWinStride);
+      uint32_t nd = 0, ln = 0;
+      float rt = 0.0f, rs = 0.0f;
+#pragma unroll
+      for (int j = 0; j < 8; ++j) {
+        const uint4 v = l4[j];
+        nd += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
+        ln += v.x + v.y + v.z + v.w;
+        const float4 t = t4[j], r = r4[j];
+        rt = rt + t.x; rt = rt + t.y; rt = rt + t.z; rt = rt + t.w;
+        rs = rs + r.x; rs = rs + r.y; rs = rs + r.z; rs = rs + r.w;
+      }
+      __stcs(reinterpret_cast<uint4*>(part_base + (size_t)(slot0 + lane) * n_parts),
+             make_uint4(nd, ln, __float_as_uint(rt), __float_as_uint(rs)));
+    }
+    __syncwarp();
+  }
+};
+
+__device__ __forceinline__ uint32_t* warp_window() {
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  return ws_smem + (threadIdx.x >> 5) * kWinWords;
 }
 
 // =======================================================================================
-// A7: fused roll-out, discrete single-agent envs (CartPole, Acrobot, Dummy).
+// A2 for the fused roll-out of discrete single-agent envs: the "plan" kernel.
+//
+// With GIVEN probabilities (BJ:5) the sampled action of (replica e, step t) depends only on
+// the seed, e, t and the probability row -- never on the environment state -- so all T x E
+// draws are sampled up front by this full-occupancy kernel (thread = one replica x 64
+// steps), leaving only the inherently sequential dynamics on the latency-bound roll-out
+// kernel.  It writes the act and logp slabs of the store directly and a compact plan
+// (four 8-bit actions of slots 4j..4j+3 per u32, 0xFF = invalid row) that the dynamics
+// kernel reads back with prefetched 32-bit loads.
 // =======================================================================================
-template <class Env>
-__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T, const uint64_t t0,
-                                                         const float* __restrict__ probs,
-                                                         const int64_t row_stride,
-                                                         const int64_t step_stride) {
-  using L = Lane<Env>;
-  using St = typename L::St;
-  constexpr int N = L::N;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int lane = threadIdx.x & 31;
-  const int64_t warp_first = e - lane;
-  const bool live = e < a.E;
-  const uint32_t eg = (uint32_t)(a.offset + e);
-  const int64_t part = e >> 5;
-  const Key key{a.k0, a.k1};
+constexpr int kPlanChunk = 64;  // steps per plan thread
 
-  St s{};
-  int32_t ep_step = 0;
-  uint32_t rc = 0;
-  float ep_ret = 0.0f;
-  if (live) {
-    L::load(a.state + e * L::S, s);
-    ep_step = a.ep_step[e];
-    rc = a.reset_count[e];
-    ep_ret = a.ep_ret[e];
-  }
-  // reset look-ahead: nxt = init(e, rc + 1), refilled every 4 steps off the critical path
-  St nxt{};
-  L::init(key, eg, rc + 1, nxt);
-  bool stale = false;
+template <int N, bool kStrided>
+__global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
+                                                      const float* __restrict__ probs, const int64_t row_stride,
+                                                      const int64_t step_stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;
+  const uint32_t eg = (uint32_t)(a.offset + ec);
+  const Key key{a.k0, a.k1};
+  const int c_begin = blockIdx.y * kPlanChunk;
+  const int c_end = min(T, c_begin + kPlanChunk);
+  const bool wlogp = a.write_logp != 0;
+  int32_t* const p_act = reinterpret_cast<int32_t*>(a.act) + ec;
+  float* const p_logp = a.logp + ec;
+  uint32_t* const p_plan = a.plan + ec;
 
   Thresholds<N> th;
-  if (step_stride == 0) {
+  if constexpr (!kStrided) {
     RowCDF<N> cdf;
-    warp_row_cdf<N>(probs, row_stride, warp_first, a.E, lane, cdf);
+    warp_row_cdf<N>(probs, row_stride, e - lane, E, lane, cdf);
     make_thresholds<N>(cdf, th);
   }
-
-  U4 w{0, 0, 0, 0};
-  for (int c = 0; c < T; ++c) {
+  bool any_bad = false;
+  uint32_t pack = 0;
+  U4 w = block(key, (t0 + (uint64_t)c_begin) >> 2, eg, 0, kAction);
+  for (int c = c_begin; c < c_end; ++c) {
     const uint64_t t = t0 + (uint64_t)c;
-    if (c == 0 || (t & 3) == 0) {
-      w = block(key, t >> 2, eg, 0, kAction);  // ACTION draws j = t
-      if (__any_sync(kFull, stale)) {           // warp-uniform refill of the look-ahead
-        St fresh;
-        L::init(key, eg, rc + 1, fresh);
-        if (stale) {
-          nxt = fresh;
-          stale = false;
-        }
-      }
-    }
+    if (c != c_begin && (t & 3) == 0) w = block(key, t >> 2, eg, 0, kAction);  // ACTION draws j = t
     const uint32_t word = pick(w, (uint32_t)(t & 3));
-
-    // ---- A2 sample
     int act;
     float lp;
     bool bad;
-    if (step_stride == 0) {
+    if constexpr (!kStrided) {
       act = search_k<N>(th, word >> 8, lp);
       bad = th.bad;
     } else {
       RowCDF<N> cdf;
-      warp_row_cdf<N>(probs + (int64_t)c * step_stride, row_stride, warp_first, a.E, lane, cdf);
+      warp_row_cdf<N>(probs + (int64_t)c * step_stride, row_stride, e - lane, E, lane, cdf);
       bad = cdf.bad;
       act = search<N>(cdf, u01(word));
       lp = logp_of<N>(cdf, act);
@@ -292,51 +331,133 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
       act = -1;
       lp = __int_as_float(0x7fc00000);
     }
-
-    // ---- A6 log pre-step observation, action, log-prob (R12)
-    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+    any_bad |= bad;
+    const size_t idx = (size_t)c * (size_t)E;
     if (live) {
-      L::obs_store(a.obs + idx * L::D, s, true);
-      st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
-      if (a.write_logp) st_cs(a.logp + idx, lp);
+      st_cs(p_act + idx, act);
+      if (wlogp) st_cs(p_logp + idx, lp);
     }
-
-    // ---- A3 / A4 step, reward, done
-    float r = 0.0f;
-    bool term = false;
-    uint8_t d = 0;
-    int32_t len = 0;
-    float ret = 0.0f;
-    if (live && !bad) {
-      St s2 = s;
-      L::step(s2, act, r, term);
-      ep_step += 1;
-      const bool trunc = ep_step >= a.max_steps;
-      d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
-      ep_ret = ep_ret + r;
-      if (d) {
-        // ---- A5 auto-reset: state = init(e, rc + 1) from the look-ahead
-        len = ep_step;
-        ret = ep_ret;
-        rc += 1;
-        if (stale) L::init(key, eg, rc, nxt);  // rare: two resets inside one refill window
-        s = nxt;
-        stale = true;
-        ep_step = 0;
-        ep_ret = 0.0f;
-      } else {
-        s = s2;
-      }
-    } else if (live && bad) {
-      atomicOr(a.err, kErrProbs | kErrAction);
+    pack |= (uint32_t)(act & 0xFF) << (8 * (c & 3));
+    if ((c & 3) == 3 || c == c_end - 1) {
+      if (live) p_plan[(size_t)(c >> 2) * (size_t)E] = pack;
+      pack = 0;
     }
-    if (live) {
-      st_cs(a.rew + idx, r);
-      st_cs_u8(a.done + idx, d);
-    }
-    // ---- A8 per-slot statistics partial
-    warp_partial(a.partials + (size_t)c * a.n_parts + part, lane, d != 0, len, ret, r);
   }
+  if (live && any_bad) atomicOr(a.err, kErrProbs | kErrAction);
+}
+
+// =======================================================================================
+// A7: fused roll-out, discrete single-agent envs (CartPole, Acrobot, Dummy).
+//
+// One replica per lane, state in registers for all T steps; actions come from the plan
+// (loaded two 4-step blocks ahead).  The step is branch-free: the next reset state
+// init(e, rc + 1) is kept ready in registers (look-ahead, refilled once per block) and
+// selected on done; a second reset inside one block takes a rare warp-uniform slow path
+// (compiled out when the env's episodes provably last >= 4 steps, kFast).
+// =======================================================================================
+template <class Env>
+__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;  // tail lanes shadow the last replica (never stored)
+  const uint32_t eg = (uint32_t)(a.offset + ec);
+  const int64_t part = e >> 5;
+  const Key key{a.k0, a.k1};
+  const int max_steps = a.max_steps;
+  const int n_parts = a.n_parts;
+  StatsWindow win;
+  win.init(warp_window());
+  float* const p_obs = a.obs + ec * L::D;
+  float* const p_rew = a.rew + ec;
+  uint8_t* const p_done = a.done + ec;
+  const uint32_t* const p_plan = a.plan + ec;
+  Partial* const p_part = a.partials + part;
+
+  St s;
+  L::load(a.state + ec * L::S, s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  St nxt;
+  L::init(key, eg, rc + 1, nxt);
+  bool stale = false;
+
+  auto one_step = [&](auto fast_tag, const int c, const int act_in) {
+    constexpr bool kFast = decltype(fast_tag)::value;
+    const bool bad = act_in < 0;  // invalid probability row (plan byte 0xFF)
+    const size_t idx = (size_t)c * (size_t)E;
+    // ---- A6 log the pre-step observation (R12)
+    if (live) L::obs_store(p_obs + idx * L::D, s, true);
+    // ---- A3 / A4 dynamics, reward, done
+    St s2 = s;
+    float r;
+    bool term;
+    L::template step<kFast>(s2, bad ? 0 : act_in, r, term);
+    const bool ok = live && !bad;
+    const int32_t es = ep_step + 1;
+    const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= max_steps ? 2u : 0u)) : 0u;
+    const float ret = ep_ret + r;
+    const float rw = ok ? r : 0.0f;
+    // ---- A5 auto-reset from the look-ahead state init(e, rc + 1)
+    if constexpr (!kFast) {
+      if (__any_sync(kFull, d != 0 && stale)) {  // second reset within one block
+        if (d != 0 && stale) L::init(key, eg, rc + 1, nxt);
+      }
+    }
+    s = d ? nxt : (ok ? s2 : s);
+    stale = stale || d != 0;
+    rc += d ? 1u : 0u;
+    ep_step = d ? 0 : (ok ? es : ep_step);
+    ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
+    if (live) {
+      st_cs(p_rew + idx, rw);
+      st_cs_u8(p_done + idx, (uint8_t)d);
+    }
+    // ---- A8 per-slot statistics contribution
+    win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+  };
+  auto flush_after = [&](const int c_last) {
+    if ((c_last & 31) == 31 || c_last == T - 1) win.flush(lane, 0, c_last & 31, c_last & ~31, p_part, n_parts);
+  };
+  auto act_of = [](uint32_t pk, int k) { return (int)(int8_t)(uint8_t)(pk >> (8 * k)); };
+
+  auto run = [&](auto fast_tag) {
+    const int nfull = T >> 2;  // full 4-step blocks
+    auto block4 = [&](const int j, const uint32_t pk) {
+      L::init(key, eg, rc + 1, nxt);  // look-ahead refill
+      stale = false;
+      one_step(fast_tag, 4 * j, act_of(pk, 0));
+      one_step(fast_tag, 4 * j + 1, act_of(pk, 1));
+      one_step(fast_tag, 4 * j + 2, act_of(pk, 2));
+      one_step(fast_tag, 4 * j + 3, act_of(pk, 3));
+      flush_after(4 * j + 3);
+    };
+    auto ld = [&](int j) { return j < (T + 3) / 4 ? __ldg(p_plan + (size_t)j * (size_t)E) : 0u; };
+    uint32_t A0 = ld(0), A1 = ld(1);
+    int j = 0;
+    for (; j + 2 <= nfull; j += 2) {  // two blocks per trip: static prefetch registers
+      const uint32_t p0 = A0;
+      A0 = ld(j + 2);
+      block4(j, p0);
+      const uint32_t p1 = A1;
+      A1 = ld(j + 3);
+      block4(j + 1, p1);
+    }
+    if (j < nfull) {
+      block4(j, A0);
+      ++j;
+    }
+    for (int c = 4 * j; c < T; ++c) {  // tail (T % 4 steps)
+      one_step(std::false_type{}, c, act_of(ld(c >> 2), c & 3));
+      flush_after(c);
+    }
+  };
+  const bool fast = L::kMinEpisode >= 4 && max_steps >= 4 && __all_sync(kFull, L::fast_ok(s));
+  if (fast) run(std::true_type{}); else run(std::false_type{});
 
   if (live) {
     L::save(a.state + e * L::S, s);
@@ -358,29 +479,29 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   using L = Lane<Env>;
   using St = typename L::St;
   constexpr int DIM = L::kDim;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
-  const bool live = e < a.E;
-  const uint32_t eg = (uint32_t)(a.offset + e);
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;
+  const uint32_t eg = (uint32_t)(a.offset + ec);
   const int64_t part = e >> 5;
   const Key key{a.k0, a.k1};
+  StatsWindow win;
+  win.init(warp_window());
 
-  St s{};
-  int32_t ep_step = 0;
-  uint32_t rc = 0;
-  float ep_ret = 0.0f;
-  if (live) {
-    L::load(a.state + e * L::S, s);
-    ep_step = a.ep_step[e];
-    rc = a.reset_count[e];
-    ep_ret = a.ep_ret[e];
-  }
+  St s;
+  L::load(a.state + ec * L::S, s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  uint32_t err = 0;
   float mean[DIM], log_std[DIM];
   auto load_head = [&](const float* base) {
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
-      mean[k] = live ? __ldg(base + e * row_stride + k) : 0.0f;
-      log_std[k] = live ? __ldg(base + e * row_stride + DIM + k) : 0.0f;
+      mean[k] = __ldg(base + ec * row_stride + k);
+      log_std[k] = __ldg(base + ec * row_stride + DIM + k);
     }
   };
   load_head(probs);
@@ -390,46 +511,35 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
     if (step_stride != 0 && c > 0) load_head(probs + (int64_t)c * step_stride);
     float act[DIM];
     float lp;
-    const bool ok = gauss_sample<DIM>(key, eg, 0, t, mean, log_std, act, lp);
-
-    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+    const bool ok_head = gauss_sample<DIM>(key, eg, 0, t, mean, log_std, act, lp);
+    const size_t idx = (size_t)c * (size_t)E + (size_t)ec;
     if (live) {
       L::obs_store(a.obs + idx * L::D, s, true);
 #pragma unroll
       for (int k = 0; k < DIM; ++k) st_cs(reinterpret_cast<float*>(a.act) + idx * DIM + k, act[k]);
       if (a.write_logp) st_cs(a.logp + idx, lp);
     }
+    St s2 = s;
     float r = 0.0f;
     bool term = false;
-    uint8_t d = 0;
-    int32_t len = 0;
-    float ret = 0.0f;
+    const bool stepped = L::step_c(s2, act, r, term) && ok_head;
+    const bool ok = live && stepped;
+    if (live && !stepped) err |= (ok_head ? 0u : kErrProbs) | kErrAction;
+    const int32_t es = ep_step + 1;
+    const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u)) : 0u;
+    const float ret = ep_ret + r;
+    const float rw = ok ? r : 0.0f;
+    if (d) L::init(key, eg, rc + 1, s2);
+    s = ok ? s2 : s;
+    rc += d ? 1u : 0u;
+    ep_step = d ? 0 : (ok ? es : ep_step);
+    ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
     if (live) {
-      St s2 = s;
-      const bool stepped = ok && L::step_c(s2, act, r, term);
-      if (stepped) {
-        ep_step += 1;
-        const bool trunc = ep_step >= a.max_steps;
-        d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
-        ep_ret = ep_ret + r;
-        if (d) {
-          len = ep_step;
-          ret = ep_ret;
-          rc += 1;
-          L::init(key, eg, rc, s);
-          ep_step = 0;
-          ep_ret = 0.0f;
-        } else {
-          s = s2;
-        }
-      } else {
-        r = 0.0f;
-        atomicOr(a.err, (ok ? 0u : kErrProbs) | kErrAction);
-      }
-      st_cs(a.rew + idx, r);
-      st_cs_u8(a.done + idx, d);
+      st_cs(a.rew + idx, rw);
+      st_cs_u8(a.done + idx, (uint8_t)d);
     }
-    warp_partial(a.partials + (size_t)c * a.n_parts + part, lane, d != 0, len, ret, r);
+    win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if ((c & 31) == 31 || c == T - 1) win.flush(lane, 0, c & 31, c & ~31, a.partials + part, a.n_parts);
   }
   if (live) {
     L::save(a.state + e * L::S, s);
@@ -437,6 +547,7 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
     a.reset_count[e] = rc;
     a.ep_ret[e] = ep_ret;
     L::obs_store(a.obs_live + e * L::D, s, false);
+    if (err) atomicOr(a.err, err);
   }
 }
 
@@ -493,84 +604,70 @@ __global__ void __launch_bounds__(256) k_sample_continuous(const KArgs a, const 
 }
 
 // ws_step for lane envs: actions from the act slab (given == nullptr) or from `given`
-// (copied into the slab, logp = NaN, R27).
+// (copied into the slab, logp = NaN, R27).  Every lane of the warp executes the step
+// (tail lanes on a shadow replica, nothing stored) so warp-collective code is legal.
 template <class Env>
 __global__ void __launch_bounds__(256) k_step_lane(const KArgs a, const int slot, const void* __restrict__ given) {
   using L = Lane<Env>;
   using St = typename L::St;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const bool live = e < a.E;
-  const uint32_t eg = (uint32_t)(a.offset + e);
+  const int64_t ec = live ? e : a.E - 1;
+  const uint32_t eg = (uint32_t)(a.offset + ec);
   const Key key{a.k0, a.k1};
-  const size_t idx = (size_t)slot * (size_t)a.E + (size_t)e;
+  const size_t idx = (size_t)slot * (size_t)a.E + (size_t)ec;
+  StatsWindow win;
+  win.init(warp_window());
+  St s;
+  L::load(a.state + ec * L::S, s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  if (live) L::obs_store(a.obs + idx * L::D, s, false);
+  bool term = false, ok;
   float r = 0.0f;
-  uint8_t d = 0;
-  int32_t len = 0;
-  float ret = 0.0f;
-  if (live) {
-    St s;
-    L::load(a.state + e * L::S, s);
-    int32_t ep_step = a.ep_step[e];
-    uint32_t rc = a.reset_count[e];
-    float ep_ret = a.ep_ret[e];
-    L::obs_store(a.obs + idx * L::D, s, false);
-    bool term = false, ok;
-    St s2 = s;
-    if constexpr (L::kDiscrete) {
-      int act;
-      if (given) {
-        act = reinterpret_cast<const int32_t*>(given)[e];
-        reinterpret_cast<int32_t*>(a.act)[idx] = act;
-        if (a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
-      } else {
-        act = reinterpret_cast<const int32_t*>(a.act)[idx];
-      }
-      ok = L::valid(act);
-      if (ok) L::step(s2, act, r, term);
-    } else {
-      constexpr int DIM = L::kDim;
-      float act[DIM];
-#pragma unroll
-      for (int k = 0; k < DIM; ++k) {
-        if (given) {
-          act[k] = reinterpret_cast<const float*>(given)[e * DIM + k];
-          reinterpret_cast<float*>(a.act)[idx * DIM + k] = act[k];
-        } else {
-          act[k] = reinterpret_cast<const float*>(a.act)[idx * DIM + k];
-        }
-      }
-      if (given && a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
-      ok = L::step_c(s2, act, r, term);
+  St s2 = s;
+  if constexpr (L::kDiscrete) {
+    int act = given ? reinterpret_cast<const int32_t*>(given)[ec] : reinterpret_cast<const int32_t*>(a.act)[idx];
+    if (given && live) {
+      reinterpret_cast<int32_t*>(a.act)[idx] = act;
+      if (a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
     }
+    ok = L::valid(act);
+    L::template step<false>(s2, ok ? act : 0, r, term);
+  } else {
+    constexpr int DIM = L::kDim;
+    float act[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      act[k] = given ? reinterpret_cast<const float*>(given)[ec * DIM + k]
+                     : reinterpret_cast<const float*>(a.act)[idx * DIM + k];
+      if (given && live) reinterpret_cast<float*>(a.act)[idx * DIM + k] = act[k];
+    }
+    if (given && live && a.write_logp) a.logp[idx] = __int_as_float(0x7fc00000);
+    ok = L::step_c(s2, act, r, term);
+  }
+  const int32_t es = ep_step + 1;
+  const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u)) : 0u;
+  const float ret = ep_ret + r;
+  const float rw = ok ? r : 0.0f;
+  if (d) L::init(key, eg, rc + 1, s2);
+  if (live) {
     if (ok) {
-      ep_step += 1;
-      const bool trunc = ep_step >= a.max_steps;
-      d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
-      ep_ret = ep_ret + r;
-      if (d) {
-        len = ep_step;
-        ret = ep_ret;
-        rc += 1;
-        L::init(key, eg, rc, s);
-        ep_step = 0;
-        ep_ret = 0.0f;
-      } else {
-        s = s2;
-      }
-      L::save(a.state + e * L::S, s);
-      a.ep_step[e] = ep_step;
-      a.reset_count[e] = rc;
-      a.ep_ret[e] = ep_ret;
-      L::obs_store(a.obs_live + e * L::D, s, false);
+      L::save(a.state + e * L::S, s2);
+      a.ep_step[e] = d ? 0 : es;
+      a.reset_count[e] = rc + (d ? 1u : 0u);
+      a.ep_ret[e] = d ? 0.0f : ret;
+      L::obs_store(a.obs_live + e * L::D, s2, false);
     } else {
-      r = 0.0f;
       atomicOr(a.err, kErrAction);
     }
-    a.rew[idx] = r;
-    a.done[idx] = d;
+    a.rew[idx] = rw;
+    a.done[idx] = (uint8_t)d;
   }
-  warp_partial(a.partials + (size_t)slot * a.n_parts + (e >> 5), lane, d != 0, len, ret, r);
+  win.put(0, lane, (live && d) ? (uint32_t)es : 0u, (live && d) ? ret : 0.0f, live ? rw : 0.0f);
+  win.flush(lane, 0, 0, slot, a.partials + (e >> 5), a.n_parts);
 }
 
 template <class Env>
@@ -870,6 +967,41 @@ __global__ void k_test_sample_grid(const float* p, int64_t* counts) {
   if (threadIdx.x <= N) atomicAdd(reinterpret_cast<unsigned long long*>(counts) + threadIdx.x, local[threadIdx.x]);
 }
 
+// elementary functions of the hot path, for the exhaustive / library comparisons
+__device__ __forceinline__ float unary(int fn, float x, float p) {
+  float s, c;
+  switch (fn) {
+    case 0: CartPole::sincos_theta(x, s, c); return s;
+    case 1: CartPole::sincos_theta(x, c, s); return s;  // cos
+    case 2: return CartPole::div_total_mass(x);
+    case 3: return __fdiv_rn(x, CartPole::total_mass);
+    case 4: return sin_c(x);
+    case 5: return cos_c(x);
+    case 6: return div_normal(x, p);
+    case 7: return __fdiv_rn(x, p);
+    case 8: return CartPole::div_total_mass_any(x);
+    default: return 0.0f;
+  }
+}
+
+__global__ void k_test_unary(int fn, float p, const float* x, int64_t n, float* out) {
+  const int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) out[i] = unary(fn, x[i], p);
+}
+
+// counts bit patterns b in [lo, hi] where fn_a(x) and fn_b(x) differ (NaN == NaN)
+__global__ void k_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism) {
+  unsigned long long m = 0;
+  const uint64_t n = (uint64_t)hi - lo + 1;
+  for (uint64_t i = (uint64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += (uint64_t)gridDim.x * blockDim.x) {
+    const float x = __uint_as_float((uint32_t)(lo + i));
+    const float ya = unary(fa, x, p), yb = unary(fb, x, p);
+    m += (__float_as_uint(ya) != __float_as_uint(yb)) && !(isnan(ya) && isnan(yb));
+  }
+  m = __reduce_add_sync(kFull, (unsigned)m);
+  if ((threadIdx.x & 31) == 0 && m) atomicAdd(mism, m);
+}
+
 // =======================================================================================
 // Host launchers.
 // =======================================================================================
@@ -893,6 +1025,18 @@ static size_t tag_smem(const KArgs& a, int block) {
   return (size_t)(2 * a.p0 * a.p0) * sizeof(int) + (size_t)(block / 32) * sizeof(float);
 }
 static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
+
+// lane kernels carry one statistics window per warp in dynamic shared memory
+template <typename... Params, typename... Args>
+static cudaError_t launch_lane(void (*k)(Params...), int64_t E, const Launch& l, Args... args) {
+  const size_t smem = (size_t)(l.block / 32) * kWinWords * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid_for(E, l.block), l.block, smem, l.stream>>>(args...);
+  return cudaGetLastError();
+}
 
 cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
   const unsigned g = grid_for(a.E, l.block);
@@ -921,24 +1065,33 @@ cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_sl
   return cudaGetLastError();
 }
 
+template <class Env>
+static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
+                                    int64_t row_stride, int64_t step_stride, uint64_t* launches) {
+  constexpr int N = Lane<Env>::N;
+  const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kPlanChunk - 1) / kPlanChunk));
+  if (step_stride == 0)
+    k_plan_discrete<N, false><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  else
+    k_plan_discrete<N, true><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  *launches += 1;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  return launch_lane(k_rollout_discrete<Env>, a.E, l, a, T);
+}
+
 cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
                            int64_t row_stride, int64_t step_stride, uint64_t* launches) {
-  const unsigned g = grid_for(a.E, l.block);
+  cudaError_t err = cudaSuccess;
   switch (l.kind) {
-    case kCartPole:
-      k_rollout_discrete<CartPole><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
-      break;
-    case kAcrobot:
-      k_rollout_discrete<Acrobot><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
-      break;
-    case kDummy:
-      k_rollout_discrete<Dummy><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
-      break;
+    case kCartPole: err = rollout_discrete<CartPole>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
+    case kAcrobot: err = rollout_discrete<Acrobot>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
+    case kDummy: err = rollout_discrete<Dummy>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kPendulum:
-      k_rollout_continuous<Pendulum><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+      err = launch_lane(k_rollout_continuous<Pendulum>, a.E, l, a, T, t0, probs, row_stride, step_stride);
       break;
     case kSurface: {
-#define M(DD) k_rollout_continuous<Surface<DD>><<<g, l.block, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride)
+#define M(DD) err = launch_lane(k_rollout_continuous<Surface<DD>>, a.E, l, a, T, t0, probs, row_stride, step_stride)
       WS_SURFACE_DISPATCH(a.p0, M)
 #undef M
       break;
@@ -947,11 +1100,11 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
       const int b = tag_block(a);
       k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, kTagRollout, T, t0, 0, probs, row_stride,
                                                              step_stride, nullptr);
+      err = cudaGetLastError();
       break;
     }
   }
   *launches += 1;
-  cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   return launch_finalize(a, l, 0, T, launches);
 }
@@ -978,14 +1131,14 @@ cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t,
 }
 
 cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches) {
-  const unsigned g = grid_for(a.E, l.block);
+  cudaError_t err = cudaSuccess;
   switch (l.kind) {
-    case kCartPole: k_step_lane<CartPole><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
-    case kAcrobot: k_step_lane<Acrobot><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
-    case kDummy: k_step_lane<Dummy><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
-    case kPendulum: k_step_lane<Pendulum><<<g, l.block, 0, l.stream>>>(a, slot, given); break;
+    case kCartPole: err = launch_lane(k_step_lane<CartPole>, a.E, l, a, slot, given); break;
+    case kAcrobot: err = launch_lane(k_step_lane<Acrobot>, a.E, l, a, slot, given); break;
+    case kDummy: err = launch_lane(k_step_lane<Dummy>, a.E, l, a, slot, given); break;
+    case kPendulum: err = launch_lane(k_step_lane<Pendulum>, a.E, l, a, slot, given); break;
     case kSurface: {
-#define M(DD) k_step_lane<Surface<DD>><<<g, l.block, 0, l.stream>>>(a, slot, given)
+#define M(DD) err = launch_lane(k_step_lane<Surface<DD>>, a.E, l, a, slot, given)
       WS_SURFACE_DISPATCH(a.p0, M)
 #undef M
       break;
@@ -994,11 +1147,11 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
       const int b = tag_block(a);
       k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, given ? kTagStepGiven : kTagStepSlab, 1, 0, slot,
                                                              nullptr, 0, 0, given);
+      err = cudaGetLastError();
       break;
     }
   }
   *launches += 1;
-  cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   return launch_finalize(a, l, slot, 1, launches);
 }
@@ -1020,6 +1173,17 @@ cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cuda
     case 8: k_test_sample_grid<8><<<592, 256, 0, s>>>(p, counts); break;
     default: return cudaErrorInvalidValue;
   }
+  return cudaGetLastError();
+}
+
+cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float* out, cudaStream_t s) {
+  k_test_unary<<<grid_for(n, 256), 256, 0, s>>>(fn, p, x, n, out);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
+                                   cudaStream_t s) {
+  k_test_exhaustive<<<148 * 16, 256, 0, s>>>(fa, fb, p, lo, hi, mism);
   return cudaGetLastError();
 }
 

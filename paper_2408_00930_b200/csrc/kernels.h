@@ -29,6 +29,7 @@ struct KArgs {
   uint32_t* reset_count;  // [E]
   float* ep_ret;      // [E, A]
   uint32_t* err;      // sticky device error word
+  uint32_t* plan;     // discrete lane envs: [ceil(T_cap / 4), E] packed 8-bit actions
   int64_t E;          // replicas on this device
   int64_t offset;     // global index of replica 0
   int32_t A;
@@ -56,6 +57,9 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
 cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_slots, uint64_t* launches);
 cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s);
 cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cudaStream_t s);
+cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float* out, cudaStream_t s);
+cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
+                                   cudaStream_t s);
 
 // number of statistics parts per slot for an env kind
 int64_t n_parts_for(EnvKind kind, int64_t E);

@@ -87,6 +87,7 @@ struct ws_env {
   uint8_t* done = nullptr;
   double* stats = nullptr;
   ws::Partial* partials = nullptr;
+  uint32_t* plan = nullptr;
   // e2e staging
   float* staging = nullptr;
   int64_t staging_n = 0;
@@ -148,6 +149,7 @@ ws::KArgs kargs(const ws_env* h) {
   a.reset_count = h->reset_count;
   a.ep_ret = h->ep_ret;
   a.err = h->err;
+  a.plan = h->plan;
   a.E = h->E;
   a.offset = h->offset;
   a.A = h->A;
@@ -185,6 +187,10 @@ ws_status ensure_store(ws_env* h, int32_t T) {
   if (e) return cuda_fail(h, e, "alloc stats");
   h->partials = (ws::Partial*)dev_alloc(h, (size_t)T * ws::n_parts_for(h->spec.kind, h->E) * sizeof(ws::Partial), &e);
   if (e) return cuda_fail(h, e, "alloc partials");
+  if (h->spec.n_actions && h->spec.kind != ws::kTag) {
+    h->plan = (uint32_t*)dev_alloc(h, (size_t)((T + 3) / 4) * h->E * sizeof(uint32_t), &e);
+    if (e) return cuda_fail(h, e, "alloc plan");
+  }
   if ((e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(double), h->stream))) return cuda_fail(h, e, "memset stats");
   h->T_cap = T;
   return WS_OK;
@@ -507,6 +513,29 @@ ws_status ws_test_sample_grid(const float* p, int32_t n, int64_t* counts, void* 
   cudaError_t e = cudaMemsetAsync(counts, 0, (size_t)(n + 1) * sizeof(int64_t), (cudaStream_t)stream);
   if (!e) e = ws::launch_test_sample_grid(p, n, counts, (cudaStream_t)stream);
   if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_test_unary(int32_t fn, float param, const float* x, int64_t n, float* out, void* stream) {
+  if (!x || !out || n < 0 || fn < 0 || fn > 8) return WS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return WS_OK;
+  cudaError_t e = ws::launch_test_unary(fn, param, x, n, out, (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_test_exhaustive(int32_t fn_a, int32_t fn_b, float param, uint32_t lo_bits, uint32_t hi_bits,
+                             uint64_t* mismatches, void* stream) {
+  if (!mismatches || fn_a < 0 || fn_a > 8 || fn_b < 0 || fn_b > 8 || hi_bits < lo_bits) return WS_ERR_INVALID_ARGUMENT;
+  unsigned long long* d = nullptr;
+  cudaError_t e = cudaMalloc(&d, sizeof(*d));
+  if (!e) e = cudaMemsetAsync(d, 0, sizeof(*d), (cudaStream_t)stream);
+  if (!e) e = ws::launch_test_exhaustive(fn_a, fn_b, param, lo_bits, hi_bits, d, (cudaStream_t)stream);
+  unsigned long long h = 0;
+  if (!e) e = cudaMemcpyAsync(&h, d, sizeof(h), cudaMemcpyDeviceToHost, (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  if (d) cudaFree(d);
+  *mismatches = h;
   return e ? WS_ERR_CUDA : WS_OK;
 }
 

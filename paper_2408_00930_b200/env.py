@@ -276,3 +276,20 @@ def ws_test_sample_grid(p: torch.Tensor) -> torch.Tensor:
     counts = torch.zeros(p.numel() + 1, dtype=torch.int64, device=p.device)
     check(lib().ws_test_sample_grid(_ptr(p), p.numel(), _ptr(counts), C.c_void_p(torch.cuda.current_stream().cuda_stream)))
     return counts
+
+
+def ws_test_unary(fn: int, x: torch.Tensor, param: float = 0.0) -> torch.Tensor:
+    """Device elementary function fn (see ws.h) on float32 x (device)."""
+    x = x.contiguous().float()
+    out = torch.empty_like(x)
+    check(lib().ws_test_unary(fn, param, _ptr(x), x.numel(), _ptr(out),
+                              C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return out
+
+
+def ws_test_exhaustive(fn_a: int, fn_b: int, lo_bits: int, hi_bits: int, param: float = 0.0) -> int:
+    """Number of fp32 bit patterns in [lo_bits, hi_bits] where device functions differ."""
+    m = C.c_uint64(0)
+    check(lib().ws_test_exhaustive(fn_a, fn_b, param, lo_bits, hi_bits, C.byref(m),
+                                   C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return int(m.value)

@@ -336,3 +336,24 @@ def test_rollout_host_e2e(P):
     ref = np.array(o.array("stats")).sum(0)
     assert st.episodes == ref[0] and st.sum_length == ref[2]
     assert abs(st.sum_return - ref[1]) <= 1e-9 * max(1, ref[1])
+
+
+def test_unaligned_rollouts_and_chunks(P):
+    """Roll-outs whose start step t0 is not a multiple of 4 (prologue / epilogue paths) and
+    whose length is not a multiple of 32 (partial statistics windows), chained across calls
+    (episodes span chunks), against the same chain on the oracle."""
+    E = 200
+    probs = W.uniform_probs(E, 1, 2)
+    g = P.Env(E, 1, "cartpole", SEED, t_capacity=64)
+    o = O.Batch("cartpole", E, 1, SEED, t_capacity=64)
+    for T in (37, 50, 3, 64, 29):
+        g.rollout(T, torch.from_numpy(probs).cuda())
+        assert o.rollout(T, probs) == 0
+        buf = {k: v.cpu().numpy() for k, v in g.buffers().items()}
+        for k in ("obs", "act", "logp", "rew", "done"):
+            assert np.array_equal(buf[k][:T], np.array(o.array(k))[:T]), (T, k)
+        for k in ("state", "reset_count", "ep_step", "ep_ret", "obs_live"):
+            assert np.array_equal(buf[k], np.array(o.array(k))), (T, k)
+        st_o = np.array(o.array("stats"))[:T]
+        assert np.array_equal(buf["stats"][:T, [0, 2]], st_o[:, [0, 2]])
+        np.testing.assert_allclose(buf["stats"][:T], st_o, rtol=1e-6)

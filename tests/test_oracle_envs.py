@@ -282,3 +282,18 @@ def test_tag_conservation(oracle):
         assert np.all(rew[nt:][prev_active[nt:] == 0] == 0.0)
         if term:
             break
+
+
+def test_cartpole_min_episode_length(oracle):
+    """No CartPole episode terminates within 7 steps: from every corner of the reset box
+    U(-0.05, 0.05)^4 (the extreme |theta|, |theta_dot| it can draw) under every one of the
+    2^7 action sequences, the pole stays inside the thresholds.  The fused GPU kernel uses
+    this bound (>= 4 suffices) to keep at most one auto-reset per 4-step block."""
+    import itertools
+    hi = float(np.nextafter(np.float32(0.05), np.float32(0)))
+    for s0 in itertools.product([-0.05, hi], repeat=4):
+        for seq in itertools.product([0, 1], repeat=7):
+            s = np.array(s0, np.float32)
+            for a in seq:
+                _, s, _, term = oracle.cartpole_step(s, a)
+                assert not term
