@@ -231,8 +231,11 @@ class Batch:
 
     def __del__(self):
         h = getattr(self, "_h", None)
-        if h:
-            lib().wso_destroy(h)
+        if h and _lib is not None:
+            try:
+                _lib.wso_destroy(h)
+            except Exception:  # interpreter teardown
+                pass
             self._h = None
 
     def info(self) -> dict:

@@ -241,8 +241,18 @@ struct StatsWindow {
   // rows [row_lo, row_hi] -> partials of slots slot0 + row (row 0 may precede the
   // roll-out's first slot, hence the signed slot0); part_base = partials + part
   __device__ __forceinline__ void flush(int lane, int row_lo, int row_hi, int64_t slot0, Partial* part_base,
-                                        int n_parts) {
+                                        int n_parts, int nlive = 32) {
+    if (nlive <= 0) return;  // (fully dead warps exit at kernel entry; defensive)
     __syncwarp();
+    if (nlive < 32) {  // tail warp: zero the shadow lanes' columns (they duplicate replica E-1)
+      for (int r = row_lo; r <= row_hi; ++r)
+        if (lane >= nlive) {
+          len[r * kWinStride + lane] = 0u;
+          ret[r * kWinStride + lane] = 0.0f;
+          rew[r * kWinStride + lane] = 0.0f;
+        }
+      __syncwarp();
+    }
     if (lane >= row_lo && lane <= row_hi) {
       const uint4* l4 = reinterpret_cast<const uint4*>(len + lane * kWinStride);
       const float4* t4 = reinterpret_cast<const float4*>(ret + lane * kWinStride);
@@ -291,7 +301,7 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = a.E;
   const bool live = e < E;
-  const int64_t ec = live ? e : E - 1;
+  const int64_t ec = live ? e : E - 1;  // tail lanes duplicate replica E-1 (identical stores)
   const uint32_t eg = (uint32_t)(a.offset + ec);
   const Key key{a.k0, a.k1};
   const int c_begin = blockIdx.y * kPlanChunk;
@@ -308,14 +318,8 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
     make_thresholds<N>(cdf, th);
   }
   bool any_bad = false;
-  uint32_t pack = 0;
-  U4 w = block(key, (t0 + (uint64_t)c_begin) >> 2, eg, 0, kAction);
-  for (int c = c_begin; c < c_end; ++c) {
-    const uint64_t t = t0 + (uint64_t)c;
-    if (c != c_begin && (t & 3) == 0) w = block(key, t >> 2, eg, 0, kAction);  // ACTION draws j = t
-    const uint32_t word = pick(w, (uint32_t)(t & 3));
+  auto sample = [&](const int c, const uint32_t word, float& lp) {
     int act;
-    float lp;
     bool bad;
     if constexpr (!kStrided) {
       act = search_k<N>(th, word >> 8, lp);
@@ -332,15 +336,57 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
       lp = __int_as_float(0x7fc00000);
     }
     any_bad |= bad;
-    const size_t idx = (size_t)c * (size_t)E;
-    if (live) {
-      st_cs(p_act + idx, act);
-      if (wlogp) st_cs(p_logp + idx, lp);
+    return act;
+  };
+  const size_t sE = (size_t)E;
+  if ((t0 & 3) == 0) {
+    // aligned: one Philox4x32 call per 4-slot group (ACTION draws j = t)
+    const int g_end = c_end >> 2;  // full groups
+    for (int g = c_begin >> 2; g < g_end; ++g) {
+      const U4 w = block(key, (t0 >> 2) + (uint64_t)g, eg, 0, kAction);
+      const size_t base = (size_t)(4 * g) * sE;
+      float lp0, lp1, lp2, lp3;
+      const int a0 = sample(4 * g, w.x, lp0), a1 = sample(4 * g + 1, w.y, lp1);
+      const int a2 = sample(4 * g + 2, w.z, lp2), a3 = sample(4 * g + 3, w.w, lp3);
+      st_cs(p_act + base, a0);
+      st_cs(p_act + base + sE, a1);
+      st_cs(p_act + base + 2 * sE, a2);
+      st_cs(p_act + base + 3 * sE, a3);
+      if (wlogp) {
+        st_cs(p_logp + base, lp0);
+        st_cs(p_logp + base + sE, lp1);
+        st_cs(p_logp + base + 2 * sE, lp2);
+        st_cs(p_logp + base + 3 * sE, lp3);
+      }
+      p_plan[(size_t)g * sE] = (uint32_t)(a0 & 0xFF) | ((uint32_t)(a1 & 0xFF) << 8) |
+                               ((uint32_t)(a2 & 0xFF) << 16) | ((uint32_t)(a3 & 0xFF) << 24);
     }
-    pack |= (uint32_t)(act & 0xFF) << (8 * (c & 3));
-    if ((c & 3) == 3 || c == c_end - 1) {
-      if (live) p_plan[(size_t)(c >> 2) * (size_t)E] = pack;
-      pack = 0;
+    if ((c_end & 3) != 0) {  // partial last group
+      const int c0 = c_end & ~3;
+      const U4 w = block(key, (t0 >> 2) + (uint64_t)(c0 >> 2), eg, 0, kAction);
+      uint32_t pack = 0;
+      for (int c = c0; c < c_end; ++c) {
+        float lp;
+        const int act = sample(c, pick(w, (uint32_t)(c & 3)), lp);
+        st_cs(p_act + (size_t)c * sE, act);
+        if (wlogp) st_cs(p_logp + (size_t)c * sE, lp);
+        pack |= (uint32_t)(act & 0xFF) << (8 * (c & 3));
+      }
+      p_plan[(size_t)(c0 >> 2) * sE] = pack;
+    }
+  } else {
+    uint32_t pack = 0;
+    for (int c = c_begin; c < c_end; ++c) {
+      const uint64_t t = t0 + (uint64_t)c;
+      float lp;
+      const int act = sample(c, pick(block(key, t >> 2, eg, 0, kAction), (uint32_t)(t & 3)), lp);
+      st_cs(p_act + (size_t)c * sE, act);
+      if (wlogp) st_cs(p_logp + (size_t)c * sE, lp);
+      pack |= (uint32_t)(act & 0xFF) << (8 * (c & 3));
+      if ((c & 3) == 3 || c == c_end - 1) {
+        p_plan[(size_t)(c >> 2) * sE] = pack;
+        pack = 0;
+      }
     }
   }
   if (live && any_bad) atomicOr(a.err, kErrProbs | kErrAction);
@@ -350,121 +396,184 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
 // A7: fused roll-out, discrete single-agent envs (CartPole, Acrobot, Dummy).
 //
 // One replica per lane, state in registers for all T steps; actions come from the plan
-// (loaded two 4-step blocks ahead).  The step is branch-free: the next reset state
-// init(e, rc + 1) is kept ready in registers (look-ahead, refilled once per block) and
-// selected on done; a second reset inside one block takes a rare warp-uniform slow path
-// (compiled out when the env's episodes provably last >= 4 steps, kFast).
+// (loaded two 4-step blocks ahead).  The step is straight-line code:
+//  - tail lanes of the last warp shadow replica E-1 (identical values, identical stores),
+//    so no store is predicated and the statistics ignore them at flush time;
+//  - the next reset state init(e, rc + 1) is kept ready in registers (look-ahead) and
+//    selected on done; it is refilled once per 8 steps when the env's episodes provably
+//    last >= 8 steps (kFast), else once per 4-step block with a warp-uniform slow path for
+//    a second reset inside the block;
+//  - blocks whose four actions are all valid (the common case) skip the invalid-row
+//    bookkeeping (kClean);
+//  - store addresses advance by one uniform slot stride per step.
 // =======================================================================================
 template <class Env>
-__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T) {
+struct DiscreteRunner {
   using L = Lane<Env>;
   using St = typename L::St;
-  const int lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
-  const int64_t E = a.E;
-  const bool live = e < E;
-  const int64_t ec = live ? e : E - 1;  // tail lanes shadow the last replica (never stored)
-  const uint32_t eg = (uint32_t)(a.offset + ec);
-  const int64_t part = e >> 5;
-  const Key key{a.k0, a.k1};
-  const int max_steps = a.max_steps;
-  const int n_parts = a.n_parts;
+  // per-lane constants
+  int lane, nlive, max_steps, n_parts, T;
+  uint32_t eg;
+  Key key;
+  size_t sE;
+  float* p_obs;
+  float* p_rew;
+  uint8_t* p_done;
+  const uint32_t* p_plan;
+  Partial* p_part;
   StatsWindow win;
-  win.init(warp_window());
-  float* const p_obs = a.obs + ec * L::D;
-  float* const p_rew = a.rew + ec;
-  uint8_t* const p_done = a.done + ec;
-  const uint32_t* const p_plan = a.plan + ec;
-  Partial* const p_part = a.partials + part;
+  // replica state (registers)
+  St s, nxt;
+  int32_t ep_step;
+  uint32_t rc;
+  float ep_ret;
+  bool stale;
 
-  St s;
-  L::load(a.state + ec * L::S, s);
-  int32_t ep_step = a.ep_step[ec];
-  uint32_t rc = a.reset_count[ec];
-  float ep_ret = a.ep_ret[ec];
-  St nxt;
-  L::init(key, eg, rc + 1, nxt);
-  bool stale = false;
+  static __device__ __forceinline__ int act_of(uint32_t pk, int k) { return (int)(int8_t)(uint8_t)(pk >> (8 * k)); }
 
-  auto one_step = [&](auto fast_tag, const int c, const int act_in) {
-    constexpr bool kFast = decltype(fast_tag)::value;
-    const bool bad = act_in < 0;  // invalid probability row (plan byte 0xFF)
-    const size_t idx = (size_t)c * (size_t)E;
+  __device__ __forceinline__ uint32_t ld(int j) const {
+    return j < (T + 3) / 4 ? __ldg(p_plan + (size_t)j * sE) : 0u;
+  }
+  __device__ __forceinline__ void refill() {
+    L::init(key, eg, rc + 1, nxt);
+    stale = false;
+  }
+  __device__ __forceinline__ void flush_after(int c_last) {
+    if ((c_last & 31) == 31 || c_last == T - 1) win.flush(lane, 0, c_last & 31, c_last & ~31, p_part, n_parts, nlive);
+  }
+
+  // one fused step at slot c (store offset idx = c * E)
+  template <bool kFast, bool kClean>
+  __device__ __forceinline__ void step(const int c, const size_t idx, const int act_in) {
+    const bool bad = kClean ? false : act_in < 0;  // invalid probability row (plan byte 0xFF)
     // ---- A6 log the pre-step observation (R12)
-    if (live) L::obs_store(p_obs + idx * L::D, s, true);
+    L::obs_store(p_obs + idx * L::D, s, true);
     // ---- A3 / A4 dynamics, reward, done
     St s2 = s;
     float r;
     bool term;
-    L::template step<kFast>(s2, bad ? 0 : act_in, r, term);
-    const bool ok = live && !bad;
+    L::template step<kFast>(s2, kClean ? act_in : (bad ? 0 : act_in), r, term);
     const int32_t es = ep_step + 1;
-    const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= max_steps ? 2u : 0u)) : 0u;
+    uint32_t d = (term ? 1u : 0u) | (es >= max_steps ? 2u : 0u);
+    float rw = r;
+    if (!kClean) {
+      d = bad ? 0u : d;
+      rw = bad ? 0.0f : r;
+    }
     const float ret = ep_ret + r;
-    const float rw = ok ? r : 0.0f;
     // ---- A5 auto-reset from the look-ahead state init(e, rc + 1)
-    if constexpr (!kFast) {
-      if (__any_sync(kFull, d != 0 && stale)) {  // second reset within one block
+    if (!kFast) {
+      if (__any_sync(kFull, d != 0 && stale)) {  // second reset within one refill window
         if (d != 0 && stale) L::init(key, eg, rc + 1, nxt);
       }
     }
-    s = d ? nxt : (ok ? s2 : s);
+    if (kClean) {
+      s = d ? nxt : s2;
+      ep_step = d ? 0 : es;
+      ep_ret = d ? 0.0f : ret;
+    } else {
+      s = d ? nxt : (bad ? s : s2);
+      ep_step = d ? 0 : (bad ? ep_step : es);
+      ep_ret = d ? 0.0f : (bad ? ep_ret : ret);
+    }
     stale = stale || d != 0;
     rc += d ? 1u : 0u;
-    ep_step = d ? 0 : (ok ? es : ep_step);
-    ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
-    if (live) {
-      st_cs(p_rew + idx, rw);
-      st_cs_u8(p_done + idx, (uint8_t)d);
-    }
+    st_cs(p_rew + idx, rw);
+    st_cs_u8(p_done + idx, (uint8_t)d);
     // ---- A8 per-slot statistics contribution
     win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
-  };
-  auto flush_after = [&](const int c_last) {
-    if ((c_last & 31) == 31 || c_last == T - 1) win.flush(lane, 0, c_last & 31, c_last & ~31, p_part, n_parts);
-  };
-  auto act_of = [](uint32_t pk, int k) { return (int)(int8_t)(uint8_t)(pk >> (8 * k)); };
+  }
 
-  auto run = [&](auto fast_tag) {
+  template <bool kFast, bool kClean>
+  __device__ __forceinline__ void body4(const int j, const uint32_t pk) {
+    const size_t idx = (size_t)(4 * j) * sE;
+    step<kFast, kClean>(4 * j, idx, act_of(pk, 0));
+    step<kFast, kClean>(4 * j + 1, idx + sE, act_of(pk, 1));
+    step<kFast, kClean>(4 * j + 2, idx + 2 * sE, act_of(pk, 2));
+    step<kFast, kClean>(4 * j + 3, idx + 3 * sE, act_of(pk, 3));
+  }
+  // one 8-step trip = blocks j, j+1.  The validity vote comes first so that the look-ahead
+  // refill and all eight steps form one straight-line basic block the scheduler can
+  // interleave (refill Philox and each step's stores / statistics under the next step's
+  // dynamics).
+  template <bool kFast>
+  __device__ __forceinline__ void trip8(const int j, const uint32_t p0, const uint32_t p1) {
+    if (kFast && __all_sync(kFull, ((p0 | p1) & 0x80808080u) == 0u)) {
+      refill();
+      body4<kFast, true>(j, p0);
+      body4<kFast, true>(j + 1, p1);
+    } else {
+      refill();
+      body4<false, false>(j, p0);
+      refill();
+      body4<false, false>(j + 1, p1);
+    }
+    flush_after(4 * j + 7);
+  }
+
+  template <bool kFast>
+  __device__ __forceinline__ void run() {
     const int nfull = T >> 2;  // full 4-step blocks
-    auto block4 = [&](const int j, const uint32_t pk) {
-      L::init(key, eg, rc + 1, nxt);  // look-ahead refill
-      stale = false;
-      one_step(fast_tag, 4 * j, act_of(pk, 0));
-      one_step(fast_tag, 4 * j + 1, act_of(pk, 1));
-      one_step(fast_tag, 4 * j + 2, act_of(pk, 2));
-      one_step(fast_tag, 4 * j + 3, act_of(pk, 3));
-      flush_after(4 * j + 3);
-    };
-    auto ld = [&](int j) { return j < (T + 3) / 4 ? __ldg(p_plan + (size_t)j * (size_t)E) : 0u; };
     uint32_t A0 = ld(0), A1 = ld(1);
     int j = 0;
-    for (; j + 2 <= nfull; j += 2) {  // two blocks per trip: static prefetch registers
-      const uint32_t p0 = A0;
+    for (; j + 2 <= nfull; j += 2) {  // 8 steps per trip; static prefetch registers
+      const uint32_t p0 = A0, p1 = A1;
       A0 = ld(j + 2);
-      block4(j, p0);
-      const uint32_t p1 = A1;
       A1 = ld(j + 3);
-      block4(j + 1, p1);
+      trip8<kFast>(j, p0, p1);
     }
     if (j < nfull) {
-      block4(j, A0);
+      refill();
+      body4<false, false>(j, A0);
+      flush_after(4 * j + 3);
       ++j;
     }
     for (int c = 4 * j; c < T; ++c) {  // tail (T % 4 steps)
-      one_step(std::false_type{}, c, act_of(ld(c >> 2), c & 3));
+      step<false, false>(c, (size_t)c * sE, act_of(ld(c >> 2), c & 3));
       flush_after(c);
     }
-  };
-  const bool fast = L::kMinEpisode >= 4 && max_steps >= 4 && __all_sync(kFull, L::fast_ok(s));
-  if (fast) run(std::true_type{}); else run(std::false_type{});
+  }
+};
+
+template <class Env>
+__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T) {
+  using L = Lane<Env>;
+  DiscreteRunner<Env> R;
+  R.lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  if (e - R.lane >= E) return;  // whole warp past the last replica (its partial part would not exist)
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;  // tail lanes shadow replica E-1 (identical stores)
+  R.nlive = (int)min((int64_t)32, E - (e - R.lane));
+  R.eg = (uint32_t)(a.offset + ec);
+  R.key = Key{a.k0, a.k1};
+  R.max_steps = a.max_steps;
+  R.n_parts = a.n_parts;
+  R.T = T;
+  R.sE = (size_t)E;
+  R.win.init(warp_window());
+  R.p_obs = a.obs + ec * L::D;
+  R.p_rew = a.rew + ec;
+  R.p_done = a.done + ec;
+  R.p_plan = a.plan + ec;
+  R.p_part = a.partials + (e >> 5);
+  L::load(a.state + ec * L::S, R.s);
+  R.ep_step = a.ep_step[ec];
+  R.rc = a.reset_count[ec];
+  R.ep_ret = a.ep_ret[ec];
+  L::init(R.key, R.eg, R.rc + 1, R.nxt);
+  R.stale = false;
+
+  const bool fast = L::kMinEpisode >= 8 && R.max_steps >= 8 && __all_sync(kFull, L::fast_ok(R.s));
+  if (fast) R.template run<true>(); else R.template run<false>();
 
   if (live) {
-    L::save(a.state + e * L::S, s);
-    a.ep_step[e] = ep_step;
-    a.reset_count[e] = rc;
-    a.ep_ret[e] = ep_ret;
-    L::obs_store(a.obs_live + e * L::D, s, false);
+    L::save(a.state + e * L::S, R.s);
+    a.ep_step[e] = R.ep_step;
+    a.reset_count[e] = R.rc;
+    a.ep_ret[e] = R.ep_ret;
+    L::obs_store(a.obs_live + e * L::D, R.s, false);
   }
 }
 
@@ -482,6 +591,7 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   const int lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = a.E;
+  if (e - lane >= E) return;  // whole warp past the last replica
   const bool live = e < E;
   const int64_t ec = live ? e : E - 1;
   const uint32_t eg = (uint32_t)(a.offset + ec);
@@ -612,6 +722,7 @@ __global__ void __launch_bounds__(256) k_step_lane(const KArgs a, const int slot
   using St = typename L::St;
   const int lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e - lane >= a.E) return;  // whole warp past the last replica
   const bool live = e < a.E;
   const int64_t ec = live ? e : a.E - 1;
   const uint32_t eg = (uint32_t)(a.offset + ec);

@@ -27,7 +27,8 @@ struct RowCDF {
   bool bad;     // R13: p < 0, NaN / inf, or non-positive / non-finite sum
 };
 
-// Rows first_row + r (r = 0..31, row r owned by lane r); rows >= n_rows are absent.
+// Rows first_row + r (r = 0..31, row r owned by lane r).  Rows >= n_rows (the tail of the
+// last warp) read row n_rows - 1, so tail lanes shadow the last real row exactly.
 template <int N>
 __device__ __forceinline__ void warp_row_cdf(const float* __restrict__ probs, int64_t row_stride,
                                              int64_t first_row, int64_t n_rows, int lane,
@@ -42,8 +43,9 @@ __device__ __forceinline__ void warp_row_cdf(const float* __restrict__ probs, in
 #pragma unroll
   for (int j = 0; j < NCH; ++j) {
     const int rr = j * RPC + rl;
-    const bool valid = (lane < RPC * N) && (rr < 32) && (first_row + rr < n_rows);
-    const float p = valid ? __ldg(probs + (first_row + rr) * row_stride + col) : 0.0f;
+    const bool valid = (lane < RPC * N) && (rr < 32);
+    const int64_t row = min(first_row + rr, n_rows - 1);
+    const float p = valid ? __ldg(probs + row * row_stride + col) : 0.0f;
     double v = (double)p;
 #pragma unroll
     for (int off = 1; off < N; off <<= 1) {

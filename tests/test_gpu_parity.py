@@ -104,7 +104,8 @@ def compare(buf, o, amb, env, T, exact_float=True):
     assert ulp_diff(lp_g[fin], lp_o[fin]).max(initial=0) <= 2, f"{env}: logp beyond 2 ulp"
     st_g, st_o = buf["stats"][:T], np.array(o.array("stats"))
     assert np.array_equal(st_g[:, [0, 2]], st_o[:, [0, 2]]), f"{env}: episode counts / lengths differ"
-    np.testing.assert_allclose(st_g[:, [1, 3]], st_o[:, [1, 3]], rtol=1e-6, atol=1e-6)
+    # fp32 partial sums over <= 128 terms per part (warp / CTA), then fp64: rel. error <= 128 u ~ 1e-5
+    np.testing.assert_allclose(st_g[:, [1, 3]], st_o[:, [1, 3]], rtol=1e-5, atol=1e-5)
     if exact_float:
         assert n_obs == 0 and n_rew == 0, f"{env}: {n_obs} obs / {n_rew} rew not bitwise equal (within R17)"
     return {"obs_bitwise_mismatch": n_obs, "rew_bitwise_mismatch": n_rew, "ambiguous": int(amb.sum())}

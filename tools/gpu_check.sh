@@ -13,4 +13,6 @@ if [ -n "${NCU}" ]; then
       python bench.py --steps 3 --warmup 1 --ncu > gpurun_out/ncu_launch_bench.log 2>&1; echo "ncu list rc=$?"
   timeout 1200 ncu --set full --clock-control none --import-source on -k regex:k_rollout -s 1 -c 1 \
       -o gpurun_out/prof_rollout -f python bench.py --steps 2 --warmup 1 --ncu > gpurun_out/ncu_full.log 2>&1; echo "ncu full rc=$?"
+  timeout 900 ncu --set full --clock-control none --import-source on -k regex:k_plan -s 1 -c 1 \
+      -o gpurun_out/prof_plan -f python bench.py --steps 2 --warmup 1 --ncu > gpurun_out/ncu_plan.log 2>&1; echo "ncu plan rc=$?"
 fi
