@@ -236,7 +236,7 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "peak_source": f"{peak_src} hbm_gbs (copy)", "kernel": "ws_rollout (k_rollout_discrete + k_finalize)",
+                "peak_source": f"{peak_src} hbm_gbs (copy)", "kernel": "ws_rollout = k_plan_discrete + k_rollout_discrete (CUDA events around the call)",
                 "kernel_ms": round(kern_avg_s * 1e3, 4), "bytes_per_launch": per_launch_bytes}
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):

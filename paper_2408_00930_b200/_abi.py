@@ -8,7 +8,7 @@ import os
 import re
 
 HERE = os.path.dirname(os.path.abspath(__file__))
-LIB_PATH = os.path.join(HERE, "lib", "libws.so")
+LIB_PATH = os.environ.get("WS_LIBWS") or os.path.join(HERE, "lib", "libws.so")  # override: profiling experiments
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ws.h")
 
 # ws_status
@@ -17,7 +17,8 @@ STATUS_NAMES = {0: "WS_OK", 1: "WS_ERR_INVALID_ARGUMENT", 2: "WS_ERR_UNKNOWN_ENV
                 4: "WS_ERR_INVALID_PROBS", 5: "WS_ERR_OUT_OF_RANGE", 6: "WS_ERR_BAD_STATE",
                 7: "WS_ERR_OUT_OF_MEMORY", 8: "WS_ERR_CUDA"}
 # ws_dtype
-F32, I32, U8, F64, U32 = range(5)
+F32, I32, U8, F64, U32, I64 = range(6)
+FX_SCALE = 2.0 ** -32  # fixed-point scale of stats[:, 1] and stats[:, 3]
 
 ALLOC_FN = C.CFUNCTYPE(C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)
 FREE_FN = C.CFUNCTYPE(None, C.c_void_p, C.c_size_t, C.c_void_p, C.c_void_p)

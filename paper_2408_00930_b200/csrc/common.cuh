@@ -103,13 +103,13 @@ __device__ __forceinline__ float warp_sum_f32(float v) {
   return v;
 }
 
-// Per-(slot, part) statistics partial: parts are warps of 32 consecutive replicas
-// (lane kernels) or single replicas (CTA kernels).  Reduced by k_finalize in fixed order.
-struct Partial {
-  uint32_t n_done;
-  uint32_t sum_len;
-  float sum_ret;
-  float sum_rew;
-};
+// A8 statistics are exact fixed-point integers: stats[slot] = {episodes, sum of returns
+// x 2^32, sum of lengths, sum of rewards x 2^32} as int64.  Every per-replica value is
+// converted once (an fp32 reward r is represented exactly whenever |r| >= 2^-8 and
+// |r| < 2^31; smaller values are rounded to a multiple of 2^-32), then summed with integer
+// adds / atomics, so the result is independent of summation order, launch shape and the
+// number of GPUs (DESIGN R20).
+enum StatField : int { kStEpisodes = 0, kStReturn = 1, kStLength = 2, kStReward = 3 };
+__device__ __forceinline__ long long to_fx(float v) { return __float2ll_rn(v * 4294967296.0f); }
 
 }  // namespace ws

@@ -10,7 +10,8 @@
 //                       agent, agents interact through a shared-memory cell grid.
 //  k_sample_*/k_step_*  the single-step calls ws_sample / ws_step.
 //  k_reset_*            ws_reset.
-//  k_finalize           A8: fixed-order reduction of the per-slot partials to stats[T, 4].
+//  statistics (A8)      exact fixed-point per-slot sums accumulated in place by integer
+//                       atomics (no separate reduction kernel).
 #include <cuda_runtime.h>
 
 #include <type_traits>
@@ -19,6 +20,10 @@
 #include "envs.cuh"
 #include "kernels.h"
 #include "sampler.cuh"
+
+#ifndef WS_EXP
+#define WS_EXP 0  // profiling experiment bits (compile-time; 0 in production)
+#endif
 
 namespace ws {
 
@@ -215,11 +220,11 @@ __device__ __forceinline__ bool gauss_sample(const Key& key, uint32_t eg, uint32
 
 // =======================================================================================
 // A8: per-warp statistics window in shared memory.  Each lane records its per-slot
-// contribution (done ? episode length : 0, done ? episode return : 0, reward) in row
-// (slot & 31); every 32 slots (and at the end) lane i reduces row i over the 32 lanes in
-// lane order -- a fixed, launch-shape-independent order -- and writes that slot's partial
-// with one 16-byte store.  Rows are 36 words apart: 16-byte aligned and free of bank
-// conflicts for the quarter-warp phases of LDS.128.
+// contribution (done ? episode length : 0, done ? episode return : 0, reward; the float
+// ones in 2^-32 fixed point) in row (slot & 31); every 32 slots (and at the end) lane i
+// reduces row i over the 32 lanes and adds the slot's four integers to stats[slot] with
+// integer atomics -- exact and order-independent.  Row strides (36 words, 34 int64) keep
+// rows 16-byte aligned and the quarter-warp phases of LDS.128 free of bank conflicts.
 // =======================================================================================
 constexpr int kWinStride = 36;
 constexpr int kWinWords = 3 * 32 * kWinStride;  // per warp (13.5 KiB)
@@ -238,46 +243,84 @@ struct StatsWindow {
     ret[row * kWinStride + lane] = rt;
     rew[row * kWinStride + lane] = rw;
   }
-  // rows [row_lo, row_hi] -> partials of slots slot0 + row (row 0 may precede the
-  // roll-out's first slot, hence the signed slot0); part_base = partials + part
-  __device__ __forceinline__ void flush(int lane, int row_lo, int row_hi, int64_t slot0, Partial* part_base,
-                                        int n_parts, int nlive = 32) {
+  // rows [row_lo, row_hi] -> stats of slots slot0 + row (row 0 may precede the roll-out's
+  // first slot, hence the signed slot0); lanes >= nlive are shadow lanes and are ignored.
+  // Each value is converted to 2^-32 fixed point before the integer sums (R20).
+  __device__ __forceinline__ void flush(int lane, int row_lo, int row_hi, int64_t slot0, unsigned long long* stats,
+                                        int nlive = 32) {
     if (nlive <= 0) return;  // (fully dead warps exit at kernel entry; defensive)
     __syncwarp();
     if (nlive < 32) {  // tail warp: zero the shadow lanes' columns (they duplicate replica E-1)
       for (int r = row_lo; r <= row_hi; ++r)
-        if (lane >= nlive) {
-          len[r * kWinStride + lane] = 0u;
-          ret[r * kWinStride + lane] = 0.0f;
-          rew[r * kWinStride + lane] = 0.0f;
-        }
+        if (lane >= nlive) put(r, lane, 0u, 0.0f, 0.0f);
       __syncwarp();
     }
     if (lane >= row_lo && lane <= row_hi) {
       const uint4* l4 = reinterpret_cast<const uint4*>(len + lane * kWinStride);
       const float4* t4 = reinterpret_cast<const float4*>(ret + lane * kWinStride);
       const float4* r4 = reinterpret_cast<const float4*>(rew + lane * kWinStride);
-      uint32_t nd = 0, ln = 0;
-      float rt = 0.0f, rs = 0.0f;
+      unsigned long long nd = 0, ln = 0;
+      long long rt = 0, rs = 0;
 #pragma unroll
       for (int j = 0; j < 8; ++j) {
         const uint4 v = l4[j];
         nd += (v.x != 0) + (v.y != 0) + (v.z != 0) + (v.w != 0);
-        ln += v.x + v.y + v.z + v.w;
+        ln += (unsigned long long)v.x + v.y + v.z + v.w;
         const float4 t = t4[j], r = r4[j];
-        rt = rt + t.x; rt = rt + t.y; rt = rt + t.z; rt = rt + t.w;
-        rs = rs + r.x; rs = rs + r.y; rs = rs + r.z; rs = rs + r.w;
+        rt += to_fx(t.x) + to_fx(t.y) + to_fx(t.z) + to_fx(t.w);
+        rs += to_fx(r.x) + to_fx(r.y) + to_fx(r.z) + to_fx(r.w);
       }
-      __stcs(reinterpret_cast<uint4*>(part_base + (size_t)(slot0 + lane) * n_parts),
-             make_uint4(nd, ln, __float_as_uint(rt), __float_as_uint(rs)));
+      if (cta_acc) {  // CTA-level aggregation in shared memory (pushed by CtaStats::push)
+        unsigned long long* acc = cta_acc + lane * 4;
+        if (nd) atomicAdd(acc + kStEpisodes, nd);
+        if (rt) atomicAdd(acc + kStReturn, (unsigned long long)rt);
+        if (ln) atomicAdd(acc + kStLength, ln);
+        if (rs) atomicAdd(acc + kStReward, (unsigned long long)rs);
+      } else {
+        unsigned long long* st = stats + (size_t)(slot0 + lane) * 4;
+        if (nd) atomicAdd(st + kStEpisodes, nd);
+        if (rt) atomicAdd(st + kStReturn, (unsigned long long)rt);
+        if (ln) atomicAdd(st + kStLength, ln);
+        if (rs) atomicAdd(st + kStReward, (unsigned long long)rs);
+      }
     }
     __syncwarp();
+  }
+  unsigned long long* cta_acc = nullptr;  // [32 rows][4] when aggregating per CTA
+};
+
+// Per-CTA statistics accumulator: the warps of a CTA add their window rows into a shared
+// [2][32][4] u64 buffer (double-buffered by window parity); after a named barrier over the
+// CTA's live warps, its first warp adds the 32 rows to the global stats with one atomic per
+// field and row, then clears the buffer -- 1/(warps per CTA) of the global atomics.
+struct CtaStats {
+  unsigned long long* buf;  // [2][32][4]
+  int n_live_threads;       // live warps x 32
+  bool leader;              // first warp of the CTA
+  __device__ __forceinline__ unsigned long long* acc(int window) { return buf + (window & 1) * 128; }
+  __device__ __forceinline__ void push(int lane, int window, int row_lo, int row_hi, int64_t slot0,
+                                       unsigned long long* stats) {
+    asm volatile("bar.sync 1, %0;" ::"r"(n_live_threads) : "memory");
+    if (leader && lane >= row_lo && lane <= row_hi) {
+      unsigned long long* a = acc(window) + lane * 4;
+      unsigned long long* st = stats + (size_t)(slot0 + lane) * 4;
+#pragma unroll
+      for (int f = 0; f < 4; ++f) {
+        if (a[f]) atomicAdd(st + f, a[f]);
+        a[f] = 0ull;
+      }
+    }
   }
 };
 
 __device__ __forceinline__ uint32_t* warp_window() {
   extern __shared__ __align__(16) uint32_t ws_smem[];
   return ws_smem + (threadIdx.x >> 5) * kWinWords;
+}
+// the [2][32][4] u64 CTA accumulator follows the per-warp windows
+__device__ __forceinline__ unsigned long long* cta_stats_buf() {
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  return reinterpret_cast<unsigned long long*>(ws_smem + (blockDim.x >> 5) * kWinWords);
 }
 
 // =======================================================================================
@@ -291,7 +334,7 @@ __device__ __forceinline__ uint32_t* warp_window() {
 // (four 8-bit actions of slots 4j..4j+3 per u32, 0xFF = invalid row) that the dynamics
 // kernel reads back with prefetched 32-bit loads.
 // =======================================================================================
-constexpr int kPlanChunk = 64;  // steps per plan thread
+constexpr int kPlanChunk = 128;  // steps per plan thread (thresholds amortised over 128 draws)
 
 template <int N, bool kStrided>
 __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
@@ -412,7 +455,7 @@ struct DiscreteRunner {
   using L = Lane<Env>;
   using St = typename L::St;
   // per-lane constants
-  int lane, nlive, max_steps, n_parts, T;
+  int lane, nlive, max_steps, T;
   uint32_t eg;
   Key key;
   size_t sE;
@@ -420,7 +463,8 @@ struct DiscreteRunner {
   float* p_rew;
   uint8_t* p_done;
   const uint32_t* p_plan;
-  Partial* p_part;
+  unsigned long long* p_stats;
+  CtaStats cta;
   StatsWindow win;
   // replica state (registers)
   St s, nxt;
@@ -435,11 +479,16 @@ struct DiscreteRunner {
     return j < (T + 3) / 4 ? __ldg(p_plan + (size_t)j * sE) : 0u;
   }
   __device__ __forceinline__ void refill() {
-    L::init(key, eg, rc + 1, nxt);
+    if (!(WS_EXP & 8)) L::init(key, eg, rc + 1, nxt);
     stale = false;
   }
   __device__ __forceinline__ void flush_after(int c_last) {
-    if ((c_last & 31) == 31 || c_last == T - 1) win.flush(lane, 0, c_last & 31, c_last & ~31, p_part, n_parts, nlive);
+    if ((c_last & 31) == 31 || c_last == T - 1) {
+      const int w = c_last >> 5;
+      win.cta_acc = cta.acc(w);
+      win.flush(lane, 0, c_last & 31, c_last & ~31, p_stats, nlive);
+      cta.push(lane, w, 0, c_last & 31, c_last & ~31, p_stats);
+    }
   }
 
   // one fused step at slot c (store offset idx = c * E)
@@ -447,12 +496,12 @@ struct DiscreteRunner {
   __device__ __forceinline__ void step(const int c, const size_t idx, const int act_in) {
     const bool bad = kClean ? false : act_in < 0;  // invalid probability row (plan byte 0xFF)
     // ---- A6 log the pre-step observation (R12)
-    L::obs_store(p_obs + idx * L::D, s, true);
+    if (!(WS_EXP & 4)) L::obs_store(p_obs + idx * L::D, s, true);
     // ---- A3 / A4 dynamics, reward, done
     St s2 = s;
     float r;
     bool term;
-    L::template step<kFast>(s2, kClean ? act_in : (bad ? 0 : act_in), r, term);
+    L::template step<kFast || (WS_EXP & 1)>(s2, kClean ? act_in : (bad ? 0 : act_in), r, term);
     const int32_t es = ep_step + 1;
     uint32_t d = (term ? 1u : 0u) | (es >= max_steps ? 2u : 0u);
     float rw = r;
@@ -478,10 +527,12 @@ struct DiscreteRunner {
     }
     stale = stale || d != 0;
     rc += d ? 1u : 0u;
-    st_cs(p_rew + idx, rw);
-    st_cs_u8(p_done + idx, (uint8_t)d);
+    if (!(WS_EXP & 4)) {
+      st_cs(p_rew + idx, rw);
+      st_cs_u8(p_done + idx, (uint8_t)d);
+    }
     // ---- A8 per-slot statistics contribution
-    win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if (!(WS_EXP & 2)) win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
   }
 
   template <bool kFast, bool kClean>
@@ -549,7 +600,6 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
   R.eg = (uint32_t)(a.offset + ec);
   R.key = Key{a.k0, a.k1};
   R.max_steps = a.max_steps;
-  R.n_parts = a.n_parts;
   R.T = T;
   R.sE = (size_t)E;
   R.win.init(warp_window());
@@ -557,7 +607,16 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
   R.p_rew = a.rew + ec;
   R.p_done = a.done + ec;
   R.p_plan = a.plan + ec;
-  R.p_part = a.partials + (e >> 5);
+  R.p_stats = a.stats;
+  {
+    const int64_t cta_first = (int64_t)blockIdx.x * blockDim.x;
+    const int64_t live_thr = min((int64_t)blockDim.x, ((E - cta_first + 31) / 32) * 32);
+    R.cta.buf = cta_stats_buf();
+    R.cta.n_live_threads = (int)live_thr;
+    R.cta.leader = (threadIdx.x >> 5) == 0;
+    for (int i = threadIdx.x; i < 256; i += (int)live_thr) R.cta.buf[i] = 0ull;  // live threads only
+    asm volatile("bar.sync 1, %0;" ::"r"(R.cta.n_live_threads) : "memory");
+  }
   L::load(a.state + ec * L::S, R.s);
   R.ep_step = a.ep_step[ec];
   R.rc = a.reset_count[ec];
@@ -595,7 +654,6 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   const bool live = e < E;
   const int64_t ec = live ? e : E - 1;
   const uint32_t eg = (uint32_t)(a.offset + ec);
-  const int64_t part = e >> 5;
   const Key key{a.k0, a.k1};
   StatsWindow win;
   win.init(warp_window());
@@ -649,7 +707,7 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
       st_cs_u8(a.done + idx, (uint8_t)d);
     }
     win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
-    if ((c & 31) == 31 || c == T - 1) win.flush(lane, 0, c & 31, c & ~31, a.partials + part, a.n_parts);
+    if ((c & 31) == 31 || c == T - 1) win.flush(lane, 0, c & 31, c & ~31, a.stats, (int)min((int64_t)32, E - (e - lane)));
   }
   if (live) {
     L::save(a.state + e * L::S, s);
@@ -778,7 +836,7 @@ __global__ void __launch_bounds__(256) k_step_lane(const KArgs a, const int slot
     a.done[idx] = (uint8_t)d;
   }
   win.put(0, lane, (live && d) ? (uint32_t)es : 0u, (live && d) ? ret : 0.0f, live ? rw : 0.0f);
-  win.flush(lane, 0, 0, slot, a.partials + (e >> 5), a.n_parts);
+  win.flush(lane, 0, 0, slot, a.stats);
 }
 
 template <class Env>
@@ -802,15 +860,16 @@ __global__ void k_reset_lane(const KArgs a) {
 enum TagMode : int { kTagRollout = 0, kTagStepSlab = 1, kTagStepGiven = 2 };
 constexpr int kTagN = 5;
 
-__device__ __forceinline__ float block_sum_f32(float v, float* red, int nwarps) {
-  // fixed order: warp butterfly, then warp partials summed in warp order by thread 0
+__device__ __forceinline__ long long block_sum_fx(long long v, long long* red, int nwarps) {
+  // exact integer sum over the CTA (order-independent)
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  v = warp_sum_f32(v);
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
   if (lane == 0) red[wid] = v;
   __syncthreads();
-  float s = 0.0f;
+  long long s = 0;
   if (threadIdx.x == 0)
-    for (int i = 0; i < nwarps; ++i) s = s + red[i];
+    for (int i = 0; i < nwarps; ++i) s += red[i];
   __syncthreads();
   return s;  // valid in thread 0
 }
@@ -823,7 +882,7 @@ __global__ void __launch_bounds__(1024) k_tag(const KArgs a, const int mode, con
   const int G = a.p0, NT = a.p1, A = a.A;
   int* taggers_on = smem;
   int* tagged_on = smem + G * G;
-  float* red = reinterpret_cast<float*>(smem + 2 * G * G);
+  long long* red = reinterpret_cast<long long*>(smem + 2 * G * G + ((2 * G * G) & 1));
   const int nwarps = blockDim.x >> 5;
   const int64_t e = blockIdx.x;
   const int ag = threadIdx.x;
@@ -941,14 +1000,19 @@ __global__ void __launch_bounds__(1024) k_tag(const KArgs a, const int mode, con
     }
     if (is_agent) st_cs(a.rew + idx, r);
     // A8: per-replica partial (sum of rewards; on done, return over agents and length)
-    const float rs = block_sum_f32(is_agent ? r : 0.0f, red, nwarps);
-    float rt = 0.0f;
-    if (d) rt = block_sum_f32(is_agent ? ep_ret : 0.0f, red, nwarps);
+    const long long rs = block_sum_fx(is_agent ? to_fx(r) : 0ll, red, nwarps);
+    long long rt = 0;
+    if (d) rt = block_sum_fx(is_agent ? to_fx(ep_ret) : 0ll, red, nwarps);
     if (threadIdx.x == 0) {
       const size_t di = (size_t)slot * (size_t)a.E + (size_t)e;
       st_cs_u8(a.done + di, d);
-      const uint4 v = make_uint4(d ? 1u : 0u, d ? (uint32_t)ep_step : 0u, __float_as_uint(rt), __float_as_uint(rs));
-      __stcs(reinterpret_cast<uint4*>(a.partials + (size_t)slot * a.n_parts + e), v);
+      unsigned long long* st = a.stats + (size_t)slot * 4;
+      if (d) {
+        atomicAdd(st + kStEpisodes, 1ull);
+        atomicAdd(st + kStLength, (unsigned long long)ep_step);
+        if (rt) atomicAdd(st + kStReturn, (unsigned long long)rt);
+      }
+      if (rs) atomicAdd(st + kStReward, (unsigned long long)rs);
     }
     if (d) {  // A5 auto-reset, uniform across the CTA
       rc += 1;
@@ -998,40 +1062,6 @@ __global__ void k_reset_tag(const KArgs a) {
   if (ag == 0) {
     a.ep_step[e] = 0;
     a.reset_count[e] = 0;
-  }
-}
-
-// =======================================================================================
-// A8: stats[slot] = fixed-order sum of the parts (one warp per slot).
-// =======================================================================================
-__global__ void k_finalize(const Partial* __restrict__ partials, const int n_parts, const int slot0,
-                           const int n_slots, double* __restrict__ stats) {
-  const int slot = slot0 + blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
-  const int lane = threadIdx.x & 31;
-  if (slot >= slot0 + n_slots) return;
-  const Partial* row = partials + (size_t)slot * n_parts;
-  unsigned long long nd = 0, ln = 0;
-  double rt = 0.0, rs = 0.0;
-  for (int i = lane; i < n_parts; i += 32) {
-    const uint4 v = reinterpret_cast<const uint4*>(row)[i];
-    nd += v.x;
-    ln += v.y;
-    rt += (double)__uint_as_float(v.z);
-    rs += (double)__uint_as_float(v.w);
-  }
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) {
-    nd += __shfl_xor_sync(kFull, nd, o);
-    ln += __shfl_xor_sync(kFull, ln, o);
-    rt += __shfl_xor_sync(kFull, rt, o);
-    rs += __shfl_xor_sync(kFull, rs, o);
-  }
-  if (lane == 0) {
-    double* st = stats + (size_t)slot * 4;
-    st[0] = (double)nd;
-    st[1] = rt;
-    st[2] = (double)ln;
-    st[3] = rs;
   }
 }
 
@@ -1116,8 +1146,6 @@ __global__ void k_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t
 // =======================================================================================
 // Host launchers.
 // =======================================================================================
-int64_t n_parts_for(EnvKind kind, int64_t E) { return kind == kTag ? E : (E + 31) / 32; }
-
 #define WS_SURFACE_DISPATCH(D, MACRO) \
   switch (D) {                        \
     case 2: MACRO(2); break;          \
@@ -1133,14 +1161,14 @@ int64_t n_parts_for(EnvKind kind, int64_t E) { return kind == kTag ? E : (E + 31
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 static size_t tag_smem(const KArgs& a, int block) {
-  return (size_t)(2 * a.p0 * a.p0) * sizeof(int) + (size_t)(block / 32) * sizeof(float);
+  return (size_t)(2 * a.p0 * a.p0 + 2) * sizeof(int) + (size_t)(block / 32) * sizeof(long long);
 }
 static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
 
 // lane kernels carry one statistics window per warp in dynamic shared memory
 template <typename... Params, typename... Args>
 static cudaError_t launch_lane(void (*k)(Params...), int64_t E, const Launch& l, Args... args) {
-  const size_t smem = (size_t)(l.block / 32) * kWinWords * sizeof(uint32_t);
+  const size_t smem = (size_t)(l.block / 32) * kWinWords * sizeof(uint32_t) + 256 * sizeof(unsigned long long);
   if (smem > 48 * 1024) {
     const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
     if (e != cudaSuccess) return e;
@@ -1164,14 +1192,6 @@ cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
     }
     case kTag: k_reset_tag<<<(unsigned)a.E, tag_block(a), 0, l.stream>>>(a); break;
   }
-  *launches += 1;
-  return cudaGetLastError();
-}
-
-cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_slots, uint64_t* launches) {
-  const int wpb = 8;
-  k_finalize<<<(unsigned)((n_slots + wpb - 1) / wpb), wpb * 32, 0, l.stream>>>(a.partials, a.n_parts, slot0,
-                                                                               n_slots, a.stats);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -1216,8 +1236,7 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
     }
   }
   *launches += 1;
-  if (err != cudaSuccess) return err;
-  return launch_finalize(a, l, 0, T, launches);
+  return err;
 }
 
 cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t, const float* probs,
@@ -1263,8 +1282,7 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
     }
   }
   *launches += 1;
-  if (err != cudaSuccess) return err;
-  return launch_finalize(a, l, slot, 1, launches);
+  return err;
 }
 
 cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s) {

@@ -9,8 +9,6 @@ namespace ws {
 
 enum EnvKind : int { kCartPole = 0, kAcrobot = 1, kPendulum = 2, kTag = 3, kSurface = 4, kDummy = 5 };
 
-struct Partial;
-
 // Everything a kernel needs to find the handle's buffers (passed by value).
 struct KArgs {
   // roll-out store (time-major)
@@ -19,8 +17,7 @@ struct KArgs {
   float* logp;
   float* rew;
   uint8_t* done;
-  Partial* partials;  // [T_cap, n_parts]
-  double* stats;      // [T_cap, 4]
+  unsigned long long* stats;  // [T_cap, 4] fixed-point int64 (common.cuh StatField)
   // live state
   float* state;       // [E, S]
   int32_t* tstate;    // tag: [E, A, 3]
@@ -36,7 +33,6 @@ struct KArgs {
   int32_t T_cap;
   int32_t max_steps;
   int32_t write_logp;
-  int32_t n_parts;    // statistics parts per slot
   int32_t p0, p1;     // env params (tag G / taggers; surface D)
   uint32_t k0, k1;    // Philox key
 };
@@ -54,14 +50,10 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t, const float* probs,
                           int64_t row_stride, uint64_t* launches);
 cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches);
-cudaError_t launch_finalize(const KArgs& a, const Launch& l, int slot0, int n_slots, uint64_t* launches);
 cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s);
 cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cudaStream_t s);
 cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float* out, cudaStream_t s);
 cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
                                    cudaStream_t s);
-
-// number of statistics parts per slot for an env kind
-int64_t n_parts_for(EnvKind kind, int64_t E);
 
 }  // namespace ws

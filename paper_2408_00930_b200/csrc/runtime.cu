@@ -85,13 +85,12 @@ struct ws_env {
   float* logp = nullptr;
   float* rew = nullptr;
   uint8_t* done = nullptr;
-  double* stats = nullptr;
-  ws::Partial* partials = nullptr;
+  unsigned long long* stats = nullptr;  // [T_cap, 4] fixed-point int64
   uint32_t* plan = nullptr;
   // e2e staging
   float* staging = nullptr;
   int64_t staging_n = 0;
-  std::vector<double> host_stats;
+  std::vector<long long> host_stats;
   uint64_t launches = 0;
   std::string last_error;
 };
@@ -140,7 +139,6 @@ ws::KArgs kargs(const ws_env* h) {
   a.logp = h->logp;
   a.rew = h->rew;
   a.done = h->done;
-  a.partials = h->partials;
   a.stats = h->stats;
   a.state = h->state;
   a.tstate = h->tstate;
@@ -156,7 +154,6 @@ ws::KArgs kargs(const ws_env* h) {
   a.T_cap = h->T_cap;
   a.max_steps = h->max_steps;
   a.write_logp = h->write_logp;
-  a.n_parts = (int32_t)ws::n_parts_for(h->spec.kind, h->E);
   a.p0 = h->p0;
   a.p1 = h->p1;
   a.k0 = (uint32_t)h->seed;
@@ -183,15 +180,14 @@ ws_status ensure_store(ws_env* h, int32_t T) {
   if (e) return cuda_fail(h, e, "alloc rew");
   h->done = (uint8_t*)dev_alloc(h, (size_t)T * h->E, &e);
   if (e) return cuda_fail(h, e, "alloc done");
-  h->stats = (double*)dev_alloc(h, (size_t)T * 4 * sizeof(double), &e);
+  h->stats = (unsigned long long*)dev_alloc(h, (size_t)T * 4 * sizeof(unsigned long long), &e);
   if (e) return cuda_fail(h, e, "alloc stats");
-  h->partials = (ws::Partial*)dev_alloc(h, (size_t)T * ws::n_parts_for(h->spec.kind, h->E) * sizeof(ws::Partial), &e);
-  if (e) return cuda_fail(h, e, "alloc partials");
   if (h->spec.n_actions && h->spec.kind != ws::kTag) {
     h->plan = (uint32_t*)dev_alloc(h, (size_t)((T + 3) / 4) * h->E * sizeof(uint32_t), &e);
     if (e) return cuda_fail(h, e, "alloc plan");
   }
-  if ((e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(double), h->stream))) return cuda_fail(h, e, "memset stats");
+  if ((e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream)))
+    return cuda_fail(h, e, "memset stats");
   h->T_cap = T;
   return WS_OK;
 }
@@ -328,7 +324,7 @@ ws_status ws_reset(ws_env* h) {
   DeviceGuard g(h->device);
   cudaError_t e = cudaMemsetAsync(h->err, 0, sizeof(uint32_t), h->stream);
   if (e) return cuda_fail(h, e, "ws_reset memset");
-  if (h->stats && (e = cudaMemsetAsync(h->stats, 0, (size_t)h->T_cap * 4 * sizeof(double), h->stream)))
+  if (h->stats && (e = cudaMemsetAsync(h->stats, 0, (size_t)h->T_cap * 4 * sizeof(unsigned long long), h->stream)))
     return cuda_fail(h, e, "ws_reset memset stats");
   if ((e = ws::launch_reset(kargs(h), launch_of(h), &h->launches))) return cuda_fail(h, e, "reset kernel");
   h->t = 0;
@@ -364,7 +360,8 @@ ws_status ws_step(ws_env* h, const void* actions) {
   if (s) return s;
   if (h->cursor >= h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "cursor at store capacity (ws_rewind)");
   if (!actions && h->sampled_slot != h->cursor) return fail(h, WS_ERR_BAD_STATE, "ws_step(NULL) needs ws_sample first");
-  cudaError_t e = ws::launch_step(kargs(h), launch_of(h), h->cursor, actions, &h->launches);
+  cudaError_t e = cudaMemsetAsync(h->stats + 4 * (size_t)h->cursor, 0, 4 * sizeof(unsigned long long), h->stream);
+  if (!e) e = ws::launch_step(kargs(h), launch_of(h), h->cursor, actions, &h->launches);
   if (e) return cuda_fail(h, e, "step kernel");
   h->cursor += 1;
   h->t += 1;
@@ -380,7 +377,8 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
   ws_status s = ensure_store(h, T);
   if (s) return s;
   if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
-  cudaError_t e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
+  cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
+  if (!e) e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
   if (e) return cuda_fail(h, e, "rollout kernel");
   h->t += (uint64_t)T;
   h->cursor = T;
@@ -388,14 +386,19 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
   return WS_OK;
 }
 
-static void sum_stats(const double* st, int n, ws_stats* out) {
-  ws_stats r{};
+static void sum_stats(const long long* st, int n, ws_stats* out) {
+  long long ep = 0, ln = 0, ret = 0, rew = 0;  // exact integer sums (fixed point, R20)
   for (int i = 0; i < n; ++i) {
-    r.episodes += st[4 * i + 0];
-    r.sum_return += st[4 * i + 1];
-    r.sum_length += st[4 * i + 2];
-    r.sum_reward += st[4 * i + 3];
+    ep += st[4 * i + 0];
+    ret += st[4 * i + 1];
+    ln += st[4 * i + 2];
+    rew += st[4 * i + 3];
   }
+  ws_stats r{};
+  r.episodes = (double)ep;
+  r.sum_return = (double)ret * 0x1.0p-32;
+  r.sum_length = (double)ln;
+  r.sum_reward = (double)rew * 0x1.0p-32;
   const double nan = std::numeric_limits<double>::quiet_NaN();
   r.mean_return = r.episodes > 0 ? r.sum_return / r.episodes : nan;
   r.mean_length = r.episodes > 0 ? r.sum_length / r.episodes : nan;
@@ -419,7 +422,8 @@ ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t
   ws_status s = ws_rollout(h, T, h->staging, row_stride, step_stride);
   if (s) return s;
   if ((int)h->host_stats.size() < 4 * T) h->host_stats.resize(4 * (size_t)T);
-  if ((e = cudaMemcpyAsync(h->host_stats.data(), h->stats, (size_t)T * 4 * sizeof(double), cudaMemcpyDeviceToHost, h->stream)))
+  if ((e = cudaMemcpyAsync(h->host_stats.data(), h->stats, (size_t)T * 4 * sizeof(long long), cudaMemcpyDeviceToHost,
+                           h->stream)))
     return cuda_fail(h, e, "D2H stats");
   if ((e = cudaStreamSynchronize(h->stream))) return cuda_fail(h, e, "sync");
   sum_stats(h->host_stats.data(), T, out);
@@ -446,7 +450,7 @@ ws_status ws_get_buffers(const ws_env* h, ws_buffers* out) {
   out->logp = tensor(h->logp, WS_F32, {T, E, A});
   out->rew = tensor(h->rew, WS_F32, {T, E, A});
   out->done = tensor(h->done, WS_U8, {T, E});
-  out->stats = tensor(h->stats, WS_F64, {T, 4});
+  out->stats = tensor(h->stats, WS_I64, {T, 4});
   if (h->spec.kind == ws::kTag) out->state = tensor(h->tstate, WS_I32, {E, A, 3});
   else out->state = tensor(h->state, WS_F32, {E, h->spec.state_dim});
   out->obs_live = tensor(h->obs_live, WS_F32, {E, A, D});
@@ -492,9 +496,10 @@ ws_status ws_read_stats(ws_env* h, int32_t t0, int32_t t1, ws_stats* out) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (!out || t0 < 0 || t1 < t0 || t1 > h->T_cap) return fail(h, WS_ERR_INVALID_ARGUMENT, "bad slot range");
   DeviceGuard g(h->device);
-  std::vector<double> st(4 * (size_t)(t1 - t0) + 4);
+  std::vector<long long> st(4 * (size_t)(t1 - t0) + 4);
   cudaError_t e = cudaStreamSynchronize(h->stream);
-  if (!e && t1 > t0) e = cudaMemcpy(st.data(), h->stats + 4 * (size_t)t0, 4 * sizeof(double) * (t1 - t0), cudaMemcpyDeviceToHost);
+  if (!e && t1 > t0)
+    e = cudaMemcpy(st.data(), h->stats + 4 * (size_t)t0, 4 * sizeof(long long) * (t1 - t0), cudaMemcpyDeviceToHost);
   if (e) return cuda_fail(h, e, "ws_read_stats");
   sum_stats(st.data(), t1 - t0, out);
   return WS_OK;

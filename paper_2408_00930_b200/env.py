@@ -20,7 +20,7 @@ from . import _abi
 from ._abi import WSError, check, lib
 
 _TORCH_DTYPE = {_abi.F32: torch.float32, _abi.I32: torch.int32, _abi.U8: torch.uint8,
-                _abi.F64: torch.float64, _abi.U32: torch.uint32}
+                _abi.F64: torch.float64, _abi.U32: torch.uint32, _abi.I64: torch.int64}
 
 
 class _TorchAllocator:
@@ -48,6 +48,14 @@ class _TorchAllocator:
 
         self.c_alloc = _abi.ALLOC_FN(_alloc)
         self.c_free = _abi.FREE_FN(_free)
+
+
+def decode_stats(st: torch.Tensor) -> torch.Tensor:
+    """Fixed-point int64 stats [T, 4] (include/ws.h, DESIGN R20) -> float64 [T, 4]."""
+    out = st.to(torch.float64)
+    out[:, 1] *= _abi.FX_SCALE
+    out[:, 3] *= _abi.FX_SCALE
+    return out
 
 
 def _ptr(t: Optional[torch.Tensor]):
@@ -174,6 +182,13 @@ class Env:
         check(lib().ws_get_info(self._h, C.byref(out)))
         return out
 
+    def stats_f64(self, t1: Optional[int] = None) -> torch.Tensor:
+        """Per-slot statistics [t1, 4] as float64 (episodes, sum of returns, sum of lengths,
+        sum of rewards), decoded from the exact fixed-point int64 slab."""
+        st = self.buffers()["stats"]
+        st = st[: (self.info().cursor if t1 is None else t1)]
+        return decode_stats(st)
+
     # ------------------------------------------------------------------ zero-copy views
     def buffers(self) -> dict[str, torch.Tensor]:
         """ws_get_buffers as torch tensors aliasing libws's device memory (no copy)."""
@@ -200,7 +215,7 @@ class Env:
         class _CAI:  # __cuda_array_interface__ for buffers libws allocated itself
             pass
         typestr = {torch.float32: "<f4", torch.int32: "<i4", torch.uint8: "|u1", torch.float64: "<f8",
-                   torch.uint32: "<u4"}[dtype]
+                   torch.uint32: "<u4", torch.int64: "<i8"}[dtype]
         obj = _CAI()
         obj.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr), False),
                                         "version": 3, "strides": None}

@@ -25,16 +25,22 @@ def shard(n_envs_global: int, world: int, rank: int) -> tuple[int, int]:
 
 
 def allreduce_stats(stats: torch.Tensor, group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
-    """In-place SUM all-reduce of a [T, 4] float64 statistics view across ranks (NCCL on the
-    GPU path; gloo in the CPU tests).  Counts are exact integers in fp64 (< 2^53)."""
+    """In-place SUM all-reduce of a [T, 4] statistics view across ranks (NCCL on the GPU
+    path; gloo in the CPU tests).  libws's slab is exact fixed-point int64 (DESIGN R20), so
+    the merged statistics are bit-identical for any number of ranks."""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
     return stats
 
 
 def summarize(stats: torch.Tensor) -> dict:
-    """Episode statistics over slots (P:93 average episodic reward, P:132 episodic step)."""
-    s = stats.double().sum(dim=0).tolist()
+    """Episode statistics over slots (P:93 average episodic reward, P:132 episodic step).
+    Accepts libws's fixed-point int64 slab or already-decoded float64 rows."""
+    if stats.dtype == torch.int64:
+        s = stats.sum(dim=0).tolist()
+        s = [s[0], s[1] * 2.0 ** -32, s[2], s[3] * 2.0 ** -32]
+    else:
+        s = stats.double().sum(dim=0).tolist()
     n = s[0]
     return {"episodes": n, "mean_return": s[1] / n if n else float("nan"),
             "mean_length": s[2] / n if n else float("nan"), "sum_reward": s[3]}
