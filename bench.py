@@ -29,10 +29,12 @@ import numpy as np  # noqa: E402
 
 import wsinputs as W  # noqa: E402
 
-# algorithmic store bytes written per env-step: obs D*4 + act 4 + logp 4
-# + rew 4 + done 1, per agent (done per replica)
-ENV_BYTES = {"cartpole": 4 * 4 + 4 + 4 + 4 + 1, "acrobot": 6 * 4 + 13, "dummy": 4 * 4 + 13,
-             "pendulum": 3 * 4 + 4 + 4 + 4 + 1}
+# Algorithmic store bytes written per env-step, split by the kernel
+# that writes them: the roll-out kernel writes obs (D_obs*4) + rew (4) + done (1); the plan
+# kernel writes act (4) + logp (4).  Per agent; done is per replica.
+OBS_DIM = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3, "tag": 4, "surface": 21}
+ROLLOUT_BYTES = {k: 4 * d + 4 + 1 for k, d in OBS_DIM.items()}
+PLAN_BYTES = {k: 8 for k in OBS_DIM}
 
 
 def parse():
@@ -104,24 +106,30 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
-def cpu_baseline(w, budget_s: float = 12.0):
-    """The oracle as it stands (oracle/), on this host's cores, on a bounded sample of the
-    same workload: the first T' steps of the C2 replicas with T' sized to ~budget_s."""
+def cpu_baseline(w, budget_s: float = 10.0):
+    """The oracle as it stands (oracle/, never tuned for this), on this host's cores, on a
+    bounded sample of the same workload: consecutive whole-workload roll-outs (the bench's
+    steps) until ~budget_s of CPU work, or a prefix of one roll-out if one is longer."""
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
     t0 = time.perf_counter()
-    b.rollout(10, probs, n_threads=cores)
+    b.rollout(min(10, w.T), probs, n_threads=cores)
     probe = time.perf_counter() - t0
-    T_s = max(10, min(w.T, int(10 * budget_s / max(probe, 1e-6))))
-    b2 = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=T_s)
+    T_s = max(10, min(w.T, int(min(10, w.T) * budget_s / max(probe, 1e-6))))
+    steps, dt, n = 0, 0.0, 0
     t0 = time.perf_counter()
-    b2.rollout(T_s, probs, n_threads=cores)
-    dt = time.perf_counter() - t0
-    return {"value": w.n_envs * T_s / dt, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
-            "sample": f"{w.name} {w.env}: {w.n_envs} replicas x first {T_s} of {w.T} steps "
-                      f"({w.n_envs * T_s} env-steps, {dt:.1f} s, {cores} threads)"}
+    while True:
+        b.rollout(T_s, probs, n_threads=cores)
+        steps += w.n_envs * T_s
+        n += 1
+        dt = time.perf_counter() - t0
+        if dt >= budget_s or n >= 1000:
+            break
+    return {"value": steps / dt, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{w.name} {w.env}: {n} x ({w.n_envs} replicas x {T_s} steps) = {steps} env-steps "
+                      f"in {dt:.1f} s on {cores} threads"}
 
 
 def run_reference(args, w):
@@ -201,6 +209,8 @@ def main():
     if not args.ncu:
         clocks.start()
         time.sleep(0.3)
+    env.enable_kernel_timing(True)  # CUDA events around every libws kernel, on its stream
+    env.kernel_times()
     launches0 = env.info().launches
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * args.steps + 2)]
     torch.cuda.synchronize(dev)
@@ -219,6 +229,8 @@ def main():
     total_ms = ev[0].elapsed_time(ev[1])
     kern_ms = [ev[2 + 2 * k].elapsed_time(ev[3 + 2 * k]) for k in range(args.steps)]
     launches = env.info().launches - launches0
+    ktimes = env.kernel_times()
+    env.enable_kernel_timing(False)
     clk = clocks.stop() if not args.ncu else {}
 
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
@@ -228,16 +240,27 @@ def main():
     value = E_g * T * args.steps / (max_ms / 1e3)
     ms_per_step = max_ms / args.steps
 
-    # roofline of the dominant kernel (ws_rollout = fused roll-out kernel + stats finalize)
+    # Roofline of the dominant kernel (the fused roll-out kernel), timed live with CUDA
+    # events on the handle's stream over the timed region (ws_kernel_times).
     peaks, peak_src = measured_peaks()
-    per_launch_bytes = ENV_BYTES.get(w.env, 0) * E * A * T
-    kern_avg_s = (sum(kern_ms) / len(kern_ms)) / 1e3
-    achieved = per_launch_bytes / kern_avg_s / 1e9
     peak = float(peaks.get("hbm_gbs", 6650.0))
+    n_roll, roll_ms = ktimes.get("rollout", (0, 0.0))
+    n_plan, plan_ms = ktimes.get("plan", (0, 0.0))
+    roll_bytes = ROLLOUT_BYTES.get(w.env, 0) * E * A * T if w.env != "tag" else (4 * 4 + 4) * E * A * T + E * T
+    achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
+    call_ms = sum(kern_ms) / len(kern_ms)
+    all_bytes = roll_bytes + PLAN_BYTES.get(w.env, 8) * E * A * T
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
-                "peak_source": f"{peak_src} hbm_gbs (copy)", "kernel": "ws_rollout = k_plan_discrete + k_rollout_discrete (CUDA events around the call)",
-                "kernel_ms": round(kern_avg_s * 1e3, 4), "bytes_per_launch": per_launch_bytes}
+                "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
+                "kernel": f"k_rollout_discrete<{w.env}>" if n_plan else "k_rollout",
+                "kernel_ms": round(roll_ms, 4), "launches_timed": n_roll,
+                "bytes_per_launch": roll_bytes, "bytes_per_env_step": roll_bytes / (E * A * T),
+                "other_kernels": {"plan": {"ms": round(plan_ms, 4), "launches": n_plan,
+                                           "achieved_GBps": round(PLAN_BYTES.get(w.env, 8) * E * A * T / (plan_ms / 1e3) / 1e9, 1) if plan_ms else None}},
+                "ws_rollout_call": {"ms": round(call_ms, 4), "bytes": all_bytes,
+                                    "achieved_GBps": round(all_bytes / (call_ms / 1e3) / 1e9, 1),
+                                    "frac": round(all_bytes / (call_ms / 1e3) / 1e9 / peak, 4)}}
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
@@ -272,7 +295,7 @@ def main():
             "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs_per_gpu": E, "n_envs_global": E_g,
                        "n_agents": A, "T": T, "probs": "uniform, resident in HBM, step_stride 0",
                        "parallelism": f"env-shard x{world} + NCCL stats all-reduce" if world > 1 else "1 GPU",
-                       "l2": f"store {per_launch_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
+                       "l2": f"store {all_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "gpu_launches": int(launches),
             "clocks": clk, "e2e": e2e,
             "paper_context": "A100 8.6M env-steps/s incl. training (P:39); not like-for-like",

@@ -60,6 +60,10 @@ class ws_stats(C.Structure):
                 ("episodes", "sum_return", "sum_length", "sum_reward", "mean_return", "mean_length")]
 
 
+class ws_kernel_time(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("launches", C.c_int32), ("mean_ms", C.c_float), ("total_ms", C.c_float)]
+
+
 _SIGS = {
     "ws_config_init": (C.c_int, [C.POINTER(ws_config)]),
     "ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -79,6 +83,8 @@ _SIGS = {
     "ws_status_string": (C.c_char_p, [C.c_int]),
     "ws_last_error": (C.c_char_p, [C.c_void_p]),
     "ws_abi_version": (C.c_int32, []),
+    "ws_enable_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ws_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(ws_kernel_time), C.c_int32, C.POINTER(C.c_int32)]),
     "ws_test_philox": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ws_test_sample_grid": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "ws_test_unary": (C.c_int, [C.c_int32, C.c_float, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),

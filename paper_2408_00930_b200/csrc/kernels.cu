@@ -1179,6 +1179,7 @@ static cudaError_t launch_lane(void (*k)(Params...), int64_t E, const Launch& l,
 
 cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
   const unsigned g = grid_for(a.E, l.block);
+  l.m(kKReset, 0);
   switch (l.kind) {
     case kCartPole: k_reset_lane<CartPole><<<g, l.block, 0, l.stream>>>(a); break;
     case kAcrobot: k_reset_lane<Acrobot><<<g, l.block, 0, l.stream>>>(a); break;
@@ -1192,6 +1193,7 @@ cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
     }
     case kTag: k_reset_tag<<<(unsigned)a.E, tag_block(a), 0, l.stream>>>(a); break;
   }
+  l.m(kKReset, 1);
   *launches += 1;
   return cudaGetLastError();
 }
@@ -1201,14 +1203,19 @@ static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint
                                     int64_t row_stride, int64_t step_stride, uint64_t* launches) {
   constexpr int N = Lane<Env>::N;
   const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kPlanChunk - 1) / kPlanChunk));
+  l.m(kKPlan, 0);
   if (step_stride == 0)
     k_plan_discrete<N, false><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
   else
     k_plan_discrete<N, true><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  l.m(kKPlan, 1);
   *launches += 1;
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  return launch_lane(k_rollout_discrete<Env>, a.E, l, a, T);
+  l.m(kKRollout, 0);
+  const cudaError_t e2 = launch_lane(k_rollout_discrete<Env>, a.E, l, a, T);
+  l.m(kKRollout, 1);
+  return e2;
 }
 
 cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
@@ -1219,18 +1226,24 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
     case kAcrobot: err = rollout_discrete<Acrobot>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kDummy: err = rollout_discrete<Dummy>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kPendulum:
+      l.m(kKRollout, 0);
       err = launch_lane(k_rollout_continuous<Pendulum>, a.E, l, a, T, t0, probs, row_stride, step_stride);
+      l.m(kKRollout, 1);
       break;
     case kSurface: {
+      l.m(kKRollout, 0);
 #define M(DD) err = launch_lane(k_rollout_continuous<Surface<DD>>, a.E, l, a, T, t0, probs, row_stride, step_stride)
       WS_SURFACE_DISPATCH(a.p0, M)
 #undef M
+      l.m(kKRollout, 1);
       break;
     }
     case kTag: {
       const int b = tag_block(a);
+      l.m(kKRollout, 0);
       k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, kTagRollout, T, t0, 0, probs, row_stride,
                                                              step_stride, nullptr);
+      l.m(kKRollout, 1);
       err = cudaGetLastError();
       break;
     }
@@ -1243,6 +1256,7 @@ cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t,
                           int64_t row_stride, uint64_t* launches) {
   const int64_t rows = a.E * (int64_t)a.A;
   const unsigned g = grid_for(rows, 256);
+  l.m(kKSample, 0);
   switch (l.kind) {
     case kCartPole:
     case kDummy: k_sample_discrete<2><<<g, 256, 0, l.stream>>>(a, slot, t, probs, row_stride); break;
@@ -1256,12 +1270,14 @@ cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t,
       break;
     }
   }
+  l.m(kKSample, 1);
   *launches += 1;
   return cudaGetLastError();
 }
 
 cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches) {
   cudaError_t err = cudaSuccess;
+  l.m(kKStep, 0);
   switch (l.kind) {
     case kCartPole: err = launch_lane(k_step_lane<CartPole>, a.E, l, a, slot, given); break;
     case kAcrobot: err = launch_lane(k_step_lane<Acrobot>, a.E, l, a, slot, given); break;
@@ -1281,6 +1297,7 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
       break;
     }
   }
+  l.m(kKStep, 1);
   *launches += 1;
   return err;
 }

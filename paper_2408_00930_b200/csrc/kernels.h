@@ -37,10 +37,18 @@ struct KArgs {
   uint32_t k0, k1;    // Philox key
 };
 
+// kernel classes for the optional per-kernel timing (ws_enable_kernel_timing)
+enum KernelId : int { kKPlan = 0, kKRollout = 1, kKSample = 2, kKStep = 3, kKReset = 4, kKCount = 5 };
+
 struct Launch {
   EnvKind kind;
   int block;          // lane-kernel block size
   cudaStream_t stream;
+  void (*mark)(void* ctx, int kernel, int phase) = nullptr;  // CUDA-event bracketing hook
+  void* mark_ctx = nullptr;
+  void m(int kernel, int phase) const {
+    if (mark) mark(mark_ctx, kernel, phase);
+  }
 };
 
 // all return the cudaGetLastError() after the launch(es) and add to *launches

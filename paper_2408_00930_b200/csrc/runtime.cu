@@ -4,6 +4,7 @@
 
 #include <cmath>
 #include <cstdio>
+#include <algorithm>
 #include <cstring>
 #include <limits>
 #include <string>
@@ -93,6 +94,13 @@ struct ws_env {
   std::vector<long long> host_stats;
   uint64_t launches = 0;
   std::string last_error;
+  // optional per-kernel CUDA-event timing (ws_enable_kernel_timing)
+  struct Ring {
+    std::vector<cudaEvent_t> b, e;
+    int n = 0, open = 0;
+  };
+  bool timing = false;
+  Ring rings[ws::kKCount];
 };
 
 namespace {
@@ -161,7 +169,28 @@ ws::KArgs kargs(const ws_env* h) {
   return a;
 }
 
-ws::Launch launch_of(const ws_env* h) { return ws::Launch{h->spec.kind, h->block, h->stream}; }
+constexpr int kTimingCap = 256;
+
+void mark_kernel(void* ctx, int kernel, int phase) {
+  ws_env* h = static_cast<ws_env*>(ctx);
+  ws_env::Ring& r = h->rings[kernel];
+  const int i = r.n % kTimingCap;
+  if (phase == 0) {
+    cudaEventRecord(r.b[i], h->stream);
+  } else {
+    cudaEventRecord(r.e[i], h->stream);
+    r.n += 1;
+  }
+}
+
+ws::Launch launch_of(ws_env* h) {
+  ws::Launch l{h->spec.kind, h->block, h->stream};
+  if (h->timing) {
+    l.mark = mark_kernel;
+    l.mark_ctx = h;
+  }
+  return l;
+}
 
 // Store allocation: once, the first time it is needed (lazy sizing, never regrown).
 ws_status ensure_store(ws_env* h, int32_t T) {
@@ -314,6 +343,10 @@ ws_status ws_destroy(ws_env* h) {
   if (!h) return WS_OK;
   DeviceGuard g(h->device);
   cudaStreamSynchronize(h->stream);
+  for (auto& r : h->rings) {
+    for (auto ev : r.b) cudaEventDestroy(ev);
+    for (auto ev : r.e) cudaEventDestroy(ev);
+  }
   free_all(h);
   delete h;
   return WS_OK;
@@ -542,6 +575,50 @@ ws_status ws_test_exhaustive(int32_t fn_a, int32_t fn_b, float param, uint32_t l
   if (d) cudaFree(d);
   *mismatches = h;
   return e ? WS_ERR_CUDA : WS_OK;
+}
+
+static const char* kKernelNames[ws::kKCount] = {"plan", "rollout", "sample", "step", "reset"};
+
+ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  if (enable && h->rings[0].b.empty()) {
+    for (auto& r : h->rings) {
+      r.b.resize(kTimingCap);
+      r.e.resize(kTimingCap);
+      for (int i = 0; i < kTimingCap; ++i) {
+        cudaError_t e = cudaEventCreate(&r.b[i]);
+        if (!e) e = cudaEventCreate(&r.e[i]);
+        if (e) return cuda_fail(h, e, "cudaEventCreate");
+      }
+    }
+  }
+  for (auto& r : h->rings) r.n = 0;
+  h->timing = enable != 0;
+  return WS_OK;
+}
+
+ws_status ws_kernel_times(ws_env* h, ws_kernel_time* out, int32_t capacity, int32_t* n_out) {
+  if (check(h) || !out || !n_out || capacity < ws::kKCount) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaStreamSynchronize(h->stream);
+  if (e) return cuda_fail(h, e, "ws_kernel_times");
+  for (int k = 0; k < ws::kKCount; ++k) {
+    ws_env::Ring& r = h->rings[k];
+    const int n = std::min(r.n, kTimingCap);
+    float tot = 0.0f;
+    for (int i = 0; i < n && h->timing; ++i) {
+      float ms = 0.0f;
+      if (cudaEventElapsedTime(&ms, r.b[i], r.e[i]) == cudaSuccess) tot += ms;
+    }
+    out[k].name = kKernelNames[k];
+    out[k].launches = n;
+    out[k].total_ms = tot;
+    out[k].mean_ms = n ? tot / (float)n : 0.0f;
+    r.n = 0;
+  }
+  *n_out = ws::kKCount;
+  return WS_OK;
 }
 
 }  // extern "C"

@@ -177,6 +177,16 @@ class Env:
         check(lib().ws_read_stats(self._h, t0, info.cursor if t1 is None else t1, C.byref(out)), self._h)
         return out
 
+    def enable_kernel_timing(self, enable: bool = True):
+        check(lib().ws_enable_kernel_timing(self._h, 1 if enable else 0), self._h)
+
+    def kernel_times(self) -> dict:
+        """{kernel class: (launches, mean_ms)} since the last call (ws_kernel_times)."""
+        arr = (_abi.ws_kernel_time * 8)()
+        n = C.c_int32(0)
+        check(lib().ws_kernel_times(self._h, arr, 8, C.byref(n)), self._h)
+        return {arr[i].name.decode(): (int(arr[i].launches), float(arr[i].mean_ms)) for i in range(n.value)}
+
     def info(self) -> _abi.ws_info:
         out = _abi.ws_info()
         check(lib().ws_get_info(self._h, C.byref(out)))
