@@ -139,8 +139,13 @@ def run_reference(args, w):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
-    # each step = one bounded sample of the workload: all replicas, T_s steps
-    T_s = 25
+    # each step = the workload's full roll-out (all replicas x T steps) unless one roll-out
+    # would take more than ~5 s on this host, then a prefix of T_s steps
+    b0 = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=min(10, w.T))
+    t0 = time.perf_counter()
+    b0.rollout(min(10, w.T), probs, n_threads=cores)
+    per_step = (time.perf_counter() - t0) / min(10, w.T)
+    T_s = max(1, min(w.T, int(5.0 / max(per_step, 1e-9))))
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=T_s)
     for _ in range(args.warmup):
         b.rollout(T_s, probs, n_threads=cores)
@@ -151,12 +156,12 @@ def run_reference(args, w):
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = w.n_envs * T_s * args.steps / tot
-    line = {"metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": 0, "steps": args.steps,
+    line = {"metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
             "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs": w.n_envs, "T": w.T,
-                       "sample_T_per_step": T_s},
+                       "sample_T_per_step": T_s, "device": f"host CPU, {cores} threads (oracle/)"},
             "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
                              "sample": f"{w.n_envs} replicas x {T_s} steps per step"},
             "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
