@@ -162,6 +162,7 @@ struct Lane<Surface<DD>> {
   __device__ static void load(const float* p, St& s) {
 #pragma unroll
     for (int i = 0; i < DD; ++i) s.q[i] = p[i];
+    s.E = Env::energy(s.q);
   }
   __device__ static void save(float* p, const St& s) {
 #pragma unroll
@@ -181,14 +182,14 @@ struct Lane<Surface<DD>> {
       }
       s.q[i] = Env::start(i) + (-0.05f + 0.1f * u01(pick(b, (uint32_t)(j & 3))));
     }
+    s.E = Env::energy(s.q);
   }
   __device__ static void obs_store(float* dst, const St& s, bool cs) {
 #pragma unroll
     for (int i = 0; i < DD; ++i) {
       if (cs) st_cs(dst + i, s.q[i]); else dst[i] = s.q[i];
     }
-    const float E = Env::energy(s.q);
-    if (cs) st_cs(dst + DD, E); else dst[DD] = E;
+    if (cs) st_cs(dst + DD, s.E); else dst[DD] = s.E;
   }
   __device__ static bool step_c(St& s, const float (&a)[DD], float& r, bool& term) {
     return Env::step(s, a, r, term);
@@ -637,13 +638,83 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
 }
 
 // =======================================================================================
-// A7: fused roll-out, continuous single-agent envs (Pendulum, surface-D).
+// A2 for the fused roll-out of continuous single-agent envs (Pendulum, surface-D): the
+// Gaussian plan kernel.  Like the discrete plan (R28), the draws z_k of (e, t) do not
+// depend on the state, so one thread per (replica, 32-step chunk) walks its contiguous
+// range of GAUSS draws j = t*d + k, one Philox4x32 call per 4 draws and one fp64
+// Box-Muller per pair, and writes act = mean + exp(log_std) z and logp (R14) into the store.
+// =======================================================================================
+constexpr int kGaussChunk = 32;  // steps per thread
+
+template <int DIM, bool kStrided>
+__global__ void __launch_bounds__(128) k_plan_gauss(const KArgs a, const int T, const uint64_t t0,
+                                                   const float* __restrict__ probs, const int64_t row_stride,
+                                                   const int64_t step_stride) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  if (e >= E) return;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const Key key{a.k0, a.k1};
+  const int c_begin = blockIdx.y * kGaussChunk;
+  const int c_end = min(T, c_begin + kGaussChunk);
+  float mean[DIM], sd[DIM], log_std[DIM];
+  bool ok = true;
+  auto load_head = [&](const float* base) {
+    ok = true;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      mean[k] = __ldg(base + e * row_stride + k);
+      log_std[k] = __ldg(base + e * row_stride + DIM + k);
+      ok = ok && isfinite(mean[k]) && isfinite(log_std[k]);
+      sd[k] = (float)exp((double)log_std[k]);
+    }
+  };
+  if (!kStrided) load_head(probs);
+  float* const p_act = reinterpret_cast<float*>(a.act);
+  bool any_bad = false;
+  for (int c = c_begin; c < c_end; ++c) {
+    if (kStrided) load_head(probs + (int64_t)c * step_stride);
+    const uint64_t j0 = (t0 + (uint64_t)c) * (uint64_t)DIM;
+    float z[DIM];
+    // draws j0 .. j0 + DIM - 1, pairs aligned at even j
+    uint64_t blk = ~0ull;
+    U4 w{0, 0, 0, 0};
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      const uint64_t j = j0 + (uint64_t)k;
+      if ((j & 1) == 0 || k == 0) {
+        if ((j >> 2) != blk) {
+          blk = j >> 2;
+          w = block(key, blk, eg, 0, kGauss);
+        }
+        float ze, zo;
+        gauss_pair(w, (int)((j & 3) >> 1), ze, zo);
+        z[k] = (j & 1) ? zo : ze;
+        if (k + 1 < DIM && (j & 1) == 0) z[k + 1] = zo;
+      }
+    }
+    double lp = 0.0;
+    float act[DIM];
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) {
+      act[k] = ok ? mean[k] + sd[k] * z[k] : __int_as_float(0x7fc00000);
+      lp = lp + (((-0.5 * (double)z[k]) * (double)z[k] - (double)log_std[k]) - kHalfLog2Pi);
+    }
+    const size_t idx = (size_t)c * (size_t)E + (size_t)e;
+#pragma unroll
+    for (int k = 0; k < DIM; ++k) st_cs(p_act + idx * DIM + k, act[k]);
+    if (a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : __int_as_float(0x7fc00000));
+    any_bad |= !ok;
+  }
+  if (any_bad) atomicOr(a.err, kErrProbs);
+}
+
+// =======================================================================================
+// A7: fused roll-out, continuous single-agent envs (Pendulum, surface-D): the dynamics
+// consume the planned actions from the act slab (prefetched one step ahead).
 // =======================================================================================
 template <class Env>
-__global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const int T, const uint64_t t0,
-                                                           const float* __restrict__ probs,
-                                                           const int64_t row_stride,
-                                                           const int64_t step_stride) {
+__global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const int T) {
   using L = Lane<Env>;
   using St = typename L::St;
   constexpr int DIM = L::kDim;
@@ -657,6 +728,8 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   const Key key{a.k0, a.k1};
   StatsWindow win;
   win.init(warp_window());
+  const float* const p_act = reinterpret_cast<const float*>(a.act) + ec * DIM;
+  const size_t sE = (size_t)E;
 
   St s;
   L::load(a.state + ec * L::S, s);
@@ -664,35 +737,25 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   uint32_t rc = a.reset_count[ec];
   float ep_ret = a.ep_ret[ec];
   uint32_t err = 0;
-  float mean[DIM], log_std[DIM];
-  auto load_head = [&](const float* base) {
+  float nxt[DIM];
 #pragma unroll
-    for (int k = 0; k < DIM; ++k) {
-      mean[k] = __ldg(base + ec * row_stride + k);
-      log_std[k] = __ldg(base + ec * row_stride + DIM + k);
-    }
-  };
-  load_head(probs);
+  for (int k = 0; k < DIM; ++k) nxt[k] = __ldcg(p_act + k);
 
   for (int c = 0; c < T; ++c) {
-    const uint64_t t = t0 + (uint64_t)c;
-    if (step_stride != 0 && c > 0) load_head(probs + (int64_t)c * step_stride);
     float act[DIM];
-    float lp;
-    const bool ok_head = gauss_sample<DIM>(key, eg, 0, t, mean, log_std, act, lp);
-    const size_t idx = (size_t)c * (size_t)E + (size_t)ec;
-    if (live) {
-      L::obs_store(a.obs + idx * L::D, s, true);
 #pragma unroll
-      for (int k = 0; k < DIM; ++k) st_cs(reinterpret_cast<float*>(a.act) + idx * DIM + k, act[k]);
-      if (a.write_logp) st_cs(a.logp + idx, lp);
+    for (int k = 0; k < DIM; ++k) act[k] = nxt[k];
+    if (c + 1 < T) {
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) nxt[k] = __ldcg(p_act + (size_t)(c + 1) * sE * DIM + k);
     }
+    const size_t idx = (size_t)c * sE + (size_t)ec;
+    L::obs_store(a.obs + idx * L::D, s, true);  // tail lanes store replica E-1's identical values
     St s2 = s;
     float r = 0.0f;
     bool term = false;
-    const bool stepped = L::step_c(s2, act, r, term) && ok_head;
-    const bool ok = live && stepped;
-    if (live && !stepped) err |= (ok_head ? 0u : kErrProbs) | kErrAction;
+    const bool ok = L::step_c(s2, act, r, term);
+    if (live && !ok) err |= kErrAction;
     const int32_t es = ep_step + 1;
     const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u)) : 0u;
     const float ret = ep_ret + r;
@@ -702,10 +765,8 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
     rc += d ? 1u : 0u;
     ep_step = d ? 0 : (ok ? es : ep_step);
     ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
-    if (live) {
-      st_cs(a.rew + idx, rw);
-      st_cs_u8(a.done + idx, (uint8_t)d);
-    }
+    st_cs(a.rew + idx, rw);
+    st_cs_u8(a.done + idx, (uint8_t)d);
     win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
     if ((c & 31) == 31 || c == T - 1) win.flush(lane, 0, c & 31, c & ~31, a.stats, (int)min((int64_t)32, E - (e - lane)));
   }
@@ -874,7 +935,8 @@ __device__ __forceinline__ long long block_sum_fx(long long v, long long* red, i
   return s;  // valid in thread 0
 }
 
-__global__ void __launch_bounds__(1024) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
+template <int kMaxThreads>
+__global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
                                               const int slot0, const float* __restrict__ probs,
                                               const int64_t row_stride, const int64_t step_stride,
                                               const void* __restrict__ given) {
@@ -1165,6 +1227,20 @@ static size_t tag_smem(const KArgs& a, int block) {
 }
 static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
 
+// CTA per replica (A threads rounded up to a warp multiple)
+static void tag_launch(const KArgs& a, const Launch& l, int b, int mode, int T, uint64_t t0, int slot0,
+                       const float* probs, int64_t row_stride, int64_t step_stride, const void* given) {
+  if (b <= 128)  // 64 registers: 8 CTAs per SM beat fewer, spill-free CTAs (measured, C4)
+    k_tag<1024><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
+                                                                  given);
+  else if (b <= 256)
+    k_tag<256><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
+                                                                 given);
+  else
+    k_tag<1024><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
+                                                                  given);
+}
+
 // lane kernels carry one statistics window per warp in dynamic shared memory
 template <typename... Params, typename... Args>
 static cudaError_t launch_lane(void (*k)(Params...), int64_t E, const Launch& l, Args... args) {
@@ -1218,6 +1294,26 @@ static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint
   return e2;
 }
 
+template <class Env>
+static cudaError_t rollout_continuous(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
+                                      int64_t row_stride, int64_t step_stride, uint64_t* launches) {
+  constexpr int DIM = Lane<Env>::kDim;
+  const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kGaussChunk - 1) / kGaussChunk));
+  l.m(kKPlan, 0);
+  if (step_stride == 0)
+    k_plan_gauss<DIM, false><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  else
+    k_plan_gauss<DIM, true><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  l.m(kKPlan, 1);
+  *launches += 1;
+  const cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  l.m(kKRollout, 0);
+  const cudaError_t e2 = launch_lane(k_rollout_continuous<Env>, a.E, l, a, T);
+  l.m(kKRollout, 1);
+  return e2;
+}
+
 cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
                            int64_t row_stride, int64_t step_stride, uint64_t* launches) {
   cudaError_t err = cudaSuccess;
@@ -1225,24 +1321,17 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
     case kCartPole: err = rollout_discrete<CartPole>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kAcrobot: err = rollout_discrete<Acrobot>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kDummy: err = rollout_discrete<Dummy>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
-    case kPendulum:
-      l.m(kKRollout, 0);
-      err = launch_lane(k_rollout_continuous<Pendulum>, a.E, l, a, T, t0, probs, row_stride, step_stride);
-      l.m(kKRollout, 1);
-      break;
+    case kPendulum: err = rollout_continuous<Pendulum>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kSurface: {
-      l.m(kKRollout, 0);
-#define M(DD) err = launch_lane(k_rollout_continuous<Surface<DD>>, a.E, l, a, T, t0, probs, row_stride, step_stride)
+#define M(DD) err = rollout_continuous<Surface<DD>>(a, l, T, t0, probs, row_stride, step_stride, launches)
       WS_SURFACE_DISPATCH(a.p0, M)
 #undef M
-      l.m(kKRollout, 1);
       break;
     }
     case kTag: {
       const int b = tag_block(a);
       l.m(kKRollout, 0);
-      k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, kTagRollout, T, t0, 0, probs, row_stride,
-                                                             step_stride, nullptr);
+      tag_launch(a, l, b, kTagRollout, T, t0, 0, probs, row_stride, step_stride, nullptr);
       l.m(kKRollout, 1);
       err = cudaGetLastError();
       break;
@@ -1291,8 +1380,7 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
     }
     case kTag: {
       const int b = tag_block(a);
-      k_tag<<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, given ? kTagStepGiven : kTagStepSlab, 1, 0, slot,
-                                                             nullptr, 0, 0, given);
+      tag_launch(a, l, b, given ? kTagStepGiven : kTagStepSlab, 1, 0, slot, nullptr, 0, 0, given);
       err = cudaGetLastError();
       break;
     }

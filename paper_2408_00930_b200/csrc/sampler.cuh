@@ -158,7 +158,22 @@ __device__ __forceinline__ float gauss_z(const Key& key, uint32_t eg, uint32_t a
   const double u2 = (double)(w1 >> 8) * (1.0 / 16777216.0);
   const double r = sqrt(-2.0 * log(u1));
   const double ang = 2.0 * 3.14159265358979323846 * u2;
-  return (float)((j & 1) ? r * sin(ang) : r * cos(ang));
+  double sn, cs;
+  sincos64(ang, sn, cs);
+  return (float)((j & 1) ? r * sn : r * cs);
+}
+
+// Both normals of the Box-Muller pair p of block b (draws 4 (b) + 2p and 4 (b) + 2p + 1).
+__device__ __forceinline__ void gauss_pair(const U4& b, int p, float& z_even, float& z_odd) {
+  const uint32_t w0 = p ? b.z : b.x, w1 = p ? b.w : b.y;
+  const double u1 = (double)((w0 >> 8) + 1) * (1.0 / 16777216.0);
+  const double u2 = (double)(w1 >> 8) * (1.0 / 16777216.0);
+  const double r = sqrt(-2.0 * log(u1));
+  const double ang = 2.0 * 3.14159265358979323846 * u2;
+  double sn, cs;
+  sincos64(ang, sn, cs);
+  z_even = (float)(r * cs);
+  z_odd = (float)(r * sn);
 }
 
 // R14 log-density constant 0.5 * log(fl64(2 pi)) (= 0.5 * log(6.283185307179586)).
