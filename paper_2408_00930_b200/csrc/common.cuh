@@ -71,86 +71,75 @@ __device__ __forceinline__ float u01(uint32_t w) { return (float)(w >> 8) * (1.0
 // < 1e-19) in Estrin form.  Larger |x| (never reached by the dynamics) use libdevice.
 // Pinned against the host libm by tests/test_gpu_kernels.py.
 // ---------------------------------------------------------------------------------------
+// fp64 constants in constant memory: DFMA / DMUL read them through the constant cache
+// instead of re-materialising each 64-bit immediate with two UMOVs per use
+__constant__ double kTrig[24] = {
+    6.36619772367581382433e-01,  // 0  2/pi
+    1.57079632673412561417e+00,  // 1  pi/2, three-part Cody-Waite split (fdlibm)
+    6.07710050630396597660e-11,  // 2
+    2.02226624871116645580e-21,  // 3
+    8.47842766036889956997e-32,  // 4
+    6755399441055744.0,          // 5  2^52 + 2^51
+    // sin: s3 .. s17
+    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, 1.0 / 362880.0, -1.0 / 39916800.0, 1.0 / 6227020800.0,
+    -1.0 / 1307674368000.0, 1.0 / 355687428096000.0,
+    // cos: c2 .. c18
+    -0.5, 1.0 / 24.0, -1.0 / 720.0, 1.0 / 40320.0, -1.0 / 3628800.0, 1.0 / 479001600.0,
+    -1.0 / 87178291200.0, 1.0 / 20922789888000.0, -1.0 / 6402373705728000.0,
+    0.0};
+
+// kChecked: |x| >= 2^20 (never reached by the environments' dynamics) falls back to
+// libdevice; callers whose arguments are provably bounded pass false.
+template <bool kChecked = true>
 __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
-  const double kInvPio2 = 6.36619772367581382433e-01;
-  const double kP1 = 1.57079632673412561417e+00, kP2 = 6.07710050630396597660e-11;
-  const double kP3 = 2.02226624871116645580e-21, kP3t = 8.47842766036889956997e-32;
-  const double kRound = 6755399441055744.0;  // 2^52 + 2^51
-  const double kd = fma(x, kInvPio2, kRound);
-  const double k = kd - kRound;
+  const double kd = fma(x, kTrig[0], kTrig[5]);
+  const double k = kd - kTrig[5];
   const int q = __double2loint(kd);
-  double r = fma(-k, kP1, x);
-  r = fma(-k, kP2, r);
-  r = fma(-k, kP3, r);
-  r = fma(-k, kP3t, r);
+  double r = fma(-k, kTrig[1], x);
+  r = fma(-k, kTrig[2], r);
+  r = fma(-k, kTrig[3], r);
+  r = fma(-k, kTrig[4], r);
   const double z = r * r, z2 = z * z, z4 = z2 * z2;
-  // sin r = r + r^3 (s3 + s5 z + ... + s17 z^7)
-  const double s_a = fma(z, 1.0 / 120.0, -1.0 / 6.0);
-  const double s_b = fma(z, 1.0 / 362880.0, -1.0 / 5040.0);
-  const double s_c = fma(z, 1.0 / 6227020800.0, -1.0 / 39916800.0);
-  const double s_d = fma(z, 1.0 / 355687428096000.0, -1.0 / 1307674368000.0);
+  // sin r = r + r^3 (s3 + s5 z + ... + s17 z^7), Estrin
+  const double s_a = fma(z, kTrig[7], kTrig[6]);
+  const double s_b = fma(z, kTrig[9], kTrig[8]);
+  const double s_c = fma(z, kTrig[11], kTrig[10]);
+  const double s_d = fma(z, kTrig[13], kTrig[12]);
   const double ps = fma(z4, fma(z2, s_d, s_c), fma(z2, s_b, s_a));
   // cos r = 1 + z (c2 + c4 z + ... + c18 z^8)
-  const double c_a = fma(z, 1.0 / 24.0, -0.5);
-  const double c_b = fma(z, 1.0 / 40320.0, -1.0 / 720.0);
-  const double c_c = fma(z, 1.0 / 479001600.0, -1.0 / 3628800.0);
-  const double c_d = fma(z, 1.0 / 20922789888000.0, -1.0 / 87178291200.0);
-  const double c_e = -1.0 / 6402373705728000.0;
-  const double pc = fma(z4, fma(z4, c_e, fma(z2, c_d, c_c)), fma(z2, c_b, c_a));
+  const double c_a = fma(z, kTrig[15], kTrig[14]);
+  const double c_b = fma(z, kTrig[17], kTrig[16]);
+  const double c_c = fma(z, kTrig[19], kTrig[18]);
+  const double c_d = fma(z, kTrig[21], kTrig[20]);
+  const double pc = fma(z4, fma(z4, kTrig[22], fma(z2, c_d, c_c)), fma(z2, c_b, c_a));
   const double sr = fma(r * z, ps, r);
   const double cr = fma(z, pc, 1.0);
   const double s0 = (q & 1) ? cr : sr;
   const double c0 = (q & 1) ? sr : cr;
   s = (q & 2) ? -s0 : s0;
   c = ((q + 1) & 2) ? -c0 : c0;
-  if (!(fabs(x) < 1048576.0)) sincos(x, &s, &c);
-}
-// Single-function variant: one polynomial instead of two -- the quadrant parity selects the
-// sin or cos coefficient set (read through the read-only cache), so sin64 / cos64 cost about
-// 60 % of sincos64.  Same reduction, same Taylor terms (r^17 / r^18).
-__device__ const double kTrigCoef[2][10] = {
-    // sin: r^3 .. r^17 coefficients (+ padding)
-    {-1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, 1.0 / 362880.0, -1.0 / 39916800.0, 1.0 / 6227020800.0,
-     -1.0 / 1307674368000.0, 1.0 / 355687428096000.0, 0.0, 0.0},
-    // cos: r^2 .. r^18 coefficients
-    {-0.5, 1.0 / 24.0, -1.0 / 720.0, 1.0 / 40320.0, -1.0 / 3628800.0, 1.0 / 479001600.0,
-     -1.0 / 87178291200.0, 1.0 / 20922789888000.0, -1.0 / 6402373705728000.0, 0.0}};
-
-// returns sin(x) if want_cos == 0 else cos(x)
-__device__ __forceinline__ double sin_or_cos64(double x, int want_cos) {
-  const double kInvPio2 = 6.36619772367581382433e-01;
-  const double kP1 = 1.57079632673412561417e+00, kP2 = 6.07710050630396597660e-11;
-  const double kP3 = 2.02226624871116645580e-21, kP3t = 8.47842766036889956997e-32;
-  const double kRound = 6755399441055744.0;
-  const double kd = fma(x, kInvPio2, kRound);
-  const double k = kd - kRound;
-  const int q = __double2loint(kd) + want_cos;  // cos(x) = sin(x + pi/2)
-  double r = fma(-k, kP1, x);
-  r = fma(-k, kP2, r);
-  r = fma(-k, kP3, r);
-  r = fma(-k, kP3t, r);
-  const int odd = q & 1;  // odd quadrant -> cos polynomial of r
-  const double* cf = kTrigCoef[odd];
-  const double z = r * r, z2 = z * z, z4 = z2 * z2;
-  const double a = fma(z, __ldg(cf + 1), __ldg(cf + 0));
-  const double b = fma(z, __ldg(cf + 3), __ldg(cf + 2));
-  const double cc = fma(z, __ldg(cf + 5), __ldg(cf + 4));
-  const double d = fma(z, __ldg(cf + 7), __ldg(cf + 6));
-  const double p = fma(z4, fma(z4, __ldg(cf + 8), fma(z2, d, cc)), fma(z2, b, a));
-  double v = odd ? fma(z, p, 1.0) : fma(r * z, p, r);
-  v = (q & 2) ? -v : v;
-  if (!(fabs(x) < 1048576.0)) v = want_cos ? cos(x) : sin(x);
-  return v;
+  if (kChecked && !(fabs(x) < 1048576.0)) sincos(x, &s, &c);
 }
 
+template <bool kChecked = true>
 __device__ __forceinline__ void sincos_c(float x, float& s, float& c) {
   double sd, cd;
-  sincos64((double)x, sd, cd);
+  sincos64<kChecked>((double)x, sd, cd);
   s = (float)sd;
   c = (float)cd;
 }
-__device__ __forceinline__ float sin_c(float x) { return (float)sin_or_cos64((double)x, 0); }
-__device__ __forceinline__ float cos_c(float x) { return (float)sin_or_cos64((double)x, 1); }
+template <bool kChecked = true>
+__device__ __forceinline__ float sin_c(float x) {
+  double sd, cd;
+  sincos64<kChecked>((double)x, sd, cd);
+  return (float)sd;
+}
+template <bool kChecked = true>
+__device__ __forceinline__ float cos_c(float x) {
+  double sd, cd;
+  sincos64<kChecked>((double)x, sd, cd);
+  return (float)cd;
+}
 
 // IEEE fp32 arithmetic without contraction: the library is built with --fmad=false, and
 // these make the intended rounding explicit where it matters.

@@ -81,8 +81,8 @@ struct Lane<Acrobot> {
   // obs = (cos t1, sin t1, cos t2, sin t2, w1, w2) (gym Acrobot-v1)
   __device__ static void obs_store(float* dst, const St& s, bool cs) {
     float s1, c1, s2, c2;
-    sincos_c(s.t1, s1, c1);
-    sincos_c(s.t2, s2, c2);
+    sincos_c<false>(s.t1, s1, c1);  // wrapped angles: |t| <= pi
+    sincos_c<false>(s.t2, s2, c2);
     const float2 a = make_float2(c1, s1), b = make_float2(c2, s2), c = make_float2(s.w1, s.w2);
     float2* d = reinterpret_cast<float2*>(dst);
     if (cs) { st_cs(d, a); st_cs(d + 1, b); st_cs(d + 2, c); }
@@ -317,6 +317,11 @@ struct CtaStats {
 __device__ __forceinline__ uint32_t* warp_window() {
   extern __shared__ __align__(16) uint32_t ws_smem[];
   return ws_smem + (threadIdx.x >> 5) * kWinWords;
+}
+// CTA accumulator at the start of dynamic shared memory (kernels without per-warp windows)
+__device__ __forceinline__ unsigned long long* cta_stats_buf_only() {
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  return reinterpret_cast<unsigned long long*>(ws_smem);
 }
 // the [2][32][4] u64 CTA accumulator follows the per-warp windows
 __device__ __forceinline__ unsigned long long* cta_stats_buf() {
@@ -778,6 +783,201 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
     L::obs_store(a.obs_live + e * L::D, s, false);
     if (err) atomicOr(a.err, err);
   }
+}
+
+// =======================================================================================
+// surface-D (R23) with one WARP per replica and one lane per coordinate (D <= 32): the
+// lane-per-replica kernel leaves C5's 2 000 replicas in 63 warps; this mapping gives 2 000.
+// Sums over coordinates (spring energy, goal distance, Gaussian log-density) are gathered
+// with shuffles: the spring energy in coordinate order (the oracle's sequential association,
+// bit-identical), the goal distance (only compared with r_goal^2) and the Gaussian
+// log-density (rounded to fp32, R18) by a fixed xor-butterfly; the four Mueller-Brown terms
+// run on lanes 0..3.
+// =======================================================================================
+__device__ const double kMB[6][4] = {{-200, -100, -170, 15}, {-1, -1, -6.5, 0.7}, {0, 0, 11, 0.6},
+                                      {-10, -10, -6.5, 0.7}, {1, 0, -0.5, -1}, {0, 0.5, 1.5, 1}};
+
+template <int D>
+struct SurfWarp {
+  using Env = Surface<D>;
+  // sequential fp64 sum of v over lanes [lo, hi) (all lanes get the result)
+  template <int LO, int HI>
+  __device__ static double ordered_sum(double v) {
+    double s = 0.0;
+#pragma unroll
+    for (int i = LO; i < HI; ++i) s += __shfl_sync(kFull, v, i);
+    return s;
+  }
+  // fixed-order xor-butterfly fp64 sum (all lanes get the same value): used where only a
+  // comparison (goal distance) or an fp32 rounding at <= 2 ulp tolerance (log-density)
+  // follows, so the association need not match the oracle's sequential loop
+  __device__ static double tree_sum(double v) {
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+    return v;
+  }
+  __device__ static float energy(float qk, int lane) {
+    const double x = (double)__shfl_sync(kFull, qk, 0), y = (double)__shfl_sync(kFull, qk, 1);
+    double ex = 0.0;
+    if (lane < 4) {
+      const double dx = x - __ldg(&kMB[4][lane]), dy = y - __ldg(&kMB[5][lane]);
+      ex = __ldg(&kMB[0][lane]) *
+           exp(__ldg(&kMB[1][lane]) * dx * dx + __ldg(&kMB[2][lane]) * dx * dy + __ldg(&kMB[3][lane]) * dy * dy);
+    }
+    const double E = ordered_sum<0, 4>(ex);
+    const double sq = (lane >= 2 && lane < D) ? (double)qk * (double)qk : 0.0;
+    const double spring = ordered_sum<2, D>(sq);
+    return (float)(E + 0.5 * Env::kappa * spring);
+  }
+  __device__ static float init(const Key& key, uint32_t eg, uint32_t rc, int lane) {
+    const uint64_t j = (uint64_t)rc * D + (uint64_t)(lane < D ? lane : 0);
+    const U4 b = block(key, j >> 2, eg, 0, kReset);
+    return Env::start(lane) + (-0.05f + 0.1f * u01(pick(b, (uint32_t)(j & 3))));
+  }
+};
+
+template <int D>
+__global__ void __launch_bounds__(256) k_rollout_surface_warp(const KArgs a, const int T) {
+  using SW = SurfWarp<D>;
+  using Env = Surface<D>;
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  const int64_t E = a.E;
+  if (e >= E) return;  // whole warp past the last replica
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const Key key{a.k0, a.k1};
+  const bool act_lane = lane < D;
+  const int kk = act_lane ? lane : 0;
+  const float lo = Env::lo(kk), hi = Env::hi(kk);
+  const double goal = Env::goal(kk);
+  const size_t sE = (size_t)E;
+  float* const p_obs = a.obs + e * (D + 1);
+  const float* const p_act = reinterpret_cast<const float*>(a.act) + e * D + kk;
+  CtaStats cta;
+  {
+    const int64_t first = (int64_t)blockIdx.x * (blockDim.x >> 5);
+    const int64_t live_warps = min((int64_t)(blockDim.x >> 5), E - first);
+    cta.buf = cta_stats_buf_only();
+    cta.n_live_threads = (int)live_warps * 32;
+    cta.leader = (threadIdx.x >> 5) == 0;
+    for (int i = threadIdx.x; i < 256; i += cta.n_live_threads) cta.buf[i] = 0ull;
+    asm volatile("bar.sync 1, %0;" ::"r"(cta.n_live_threads) : "memory");
+  }
+
+  float q = a.state[e * D + kk];
+  float Ecur = SW::energy(q, lane);
+  int32_t ep_step = a.ep_step[e];
+  uint32_t rc = a.reset_count[e];
+  float ep_ret = a.ep_ret[e];
+  uint32_t err = 0;
+  float an = __ldcg(p_act);
+  for (int c = 0; c < T; ++c) {
+    const float ak_in = an;
+    if (c + 1 < T) an = __ldcg(p_act + (size_t)(c + 1) * sE * D);
+    const size_t idx = (size_t)c * sE + (size_t)e;
+    // pre-step observation (q, E(q))
+    if (act_lane) st_cs(p_obs + (size_t)c * sE * (D + 1) + lane, q);
+    if (lane == (D < 32 ? D : 0)) st_cs(p_obs + (size_t)c * sE * (D + 1) + D, Ecur);
+    const bool ok = __all_sync(kFull, !act_lane || isfinite(ak_in));
+    float r = 0.0f;
+    uint32_t d = 0;
+    float qn = q, En = Ecur;
+    if (ok) {
+      const float ak = fminf(fmaxf(ak_in, -Env::delta), Env::delta);
+      const float qi = q + ak;
+      qn = act_lane ? fminf(fmaxf(qi, lo), hi) : 0.0f;
+      En = SW::energy(qn, lane);
+      const double di = act_lane ? (double)qn - goal : 0.0;
+      const double d2 = SW::tree_sum(di * di);
+      const bool term = d2 < Env::r_goal * Env::r_goal;
+      r = -(Env::w_E * (En - Ecur)) - Env::c_step;
+      if (term) r = r + Env::bonus;
+      const int32_t es = ep_step + 1;
+      d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
+      const float ret = ep_ret + r;
+      if (lane == 0) {
+        unsigned long long* acc = cta.acc(c >> 5) + (c & 31) * 4;
+        atomicAdd(acc + kStReward, (unsigned long long)to_fx(r));
+        if (d) {
+          atomicAdd(acc + kStEpisodes, 1ull);
+          atomicAdd(acc + kStLength, (unsigned long long)es);
+          atomicAdd(acc + kStReturn, (unsigned long long)to_fx(ret));
+        }
+      }
+      if (d) {  // auto-reset: every lane draws its own coordinate (warp-uniform branch)
+        rc += 1;
+        qn = SW::init(key, eg, rc, lane);
+        En = SW::energy(qn, lane);
+        ep_step = 0;
+        ep_ret = 0.0f;
+      } else {
+        ep_step = es;
+        ep_ret = ret;
+      }
+      q = qn;
+      Ecur = En;
+    } else if (lane == 0) {
+      err |= kErrAction;
+    }
+    if (lane == 0) {
+      st_cs(a.rew + idx, r);
+      st_cs_u8(a.done + idx, (uint8_t)d);
+    }
+    if ((c & 31) == 31 || c == T - 1) cta.push(lane, c >> 5, 0, c & 31, c & ~31, a.stats);
+  }
+  if (act_lane) a.state[e * D + lane] = q;
+  if (act_lane) a.obs_live[e * (D + 1) + lane] = q;
+  if (lane == (D < 32 ? D : 0)) a.obs_live[e * (D + 1) + D] = Ecur;
+  if (lane == 0) {
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    if (err) atomicOr(a.err, err);
+  }
+}
+
+// Gaussian plan with one warp per (replica, 32-step chunk), lane = action dimension; the
+// log-density terms are summed by a fixed xor-butterfly (<= 2 ulp from the oracle's
+// sequential sum after rounding, R18).
+template <int DIM, bool kStrided>
+__global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const int T, const uint64_t t0,
+                                                        const float* __restrict__ probs, const int64_t row_stride,
+                                                        const int64_t step_stride) {
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (e >= a.E) return;
+  const uint32_t eg = (uint32_t)(a.offset + e);
+  const Key key{a.k0, a.k1};
+  const int c_begin = blockIdx.y * kGaussChunk;
+  const int c_end = min(T, c_begin + kGaussChunk);
+  const bool act_lane = lane < DIM;
+  const int kk = act_lane ? lane : 0;
+  float mean = 0.0f, ls = 0.0f, sd = 1.0f;
+  bool ok = true;
+  auto load_head = [&](const float* base) {
+    mean = __ldg(base + e * row_stride + kk);
+    ls = __ldg(base + e * row_stride + DIM + kk);
+    ok = __all_sync(kFull, !act_lane || (isfinite(mean) && isfinite(ls)));
+    sd = (float)exp((double)ls);
+  };
+  if (!kStrided) load_head(probs);
+  float* const p_act = reinterpret_cast<float*>(a.act) + e * DIM + kk;
+  bool any_bad = false;
+  for (int c = c_begin; c < c_end; ++c) {
+    if (kStrided) load_head(probs + (int64_t)c * step_stride);
+    const uint64_t j = (t0 + (uint64_t)c) * (uint64_t)DIM + (uint64_t)kk;
+    const U4 w = block(key, j >> 2, eg, 0, kGauss);
+    float ze, zo;
+    gauss_pair(w, (int)((j & 3) >> 1), ze, zo);
+    const float z = (j & 1) ? zo : ze;
+    const double term = act_lane ? (((-0.5 * (double)z) * (double)z - (double)ls) - kHalfLog2Pi) : 0.0;
+    const double lp = SurfWarp<DIM>::tree_sum(term);
+    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+    if (act_lane) st_cs(p_act + (size_t)c * (size_t)a.E * DIM, ok ? mean + sd * z : __int_as_float(0x7fc00000));
+    if (lane == 0 && a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : __int_as_float(0x7fc00000));
+    any_bad |= !ok;
+  }
+  if (lane == 0 && any_bad) atomicOr(a.err, kErrProbs);
 }
 
 // =======================================================================================
@@ -1314,6 +1514,26 @@ static cudaError_t rollout_continuous(const KArgs& a, const Launch& l, int T, ui
   return e2;
 }
 
+template <int D>
+static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
+                                   int64_t row_stride, int64_t step_stride, uint64_t* launches) {
+  const dim3 pgrid(grid_for(a.E, 4), (unsigned)((T + kGaussChunk - 1) / kGaussChunk));
+  l.m(kKPlan, 0);
+  if (step_stride == 0)
+    k_plan_gauss_warp<D, false><<<pgrid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  else
+    k_plan_gauss_warp<D, true><<<pgrid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+  l.m(kKPlan, 1);
+  *launches += 1;
+  cudaError_t err = cudaGetLastError();
+  if (err != cudaSuccess) return err;
+  const int wpb = l.block / 32;  // replicas per CTA
+  l.m(kKRollout, 0);
+  k_rollout_surface_warp<D><<<grid_for(a.E, wpb), l.block, 256 * sizeof(unsigned long long), l.stream>>>(a, T);
+  l.m(kKRollout, 1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
                            int64_t row_stride, int64_t step_stride, uint64_t* launches) {
   cudaError_t err = cudaSuccess;
@@ -1323,7 +1543,7 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
     case kDummy: err = rollout_discrete<Dummy>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kPendulum: err = rollout_continuous<Pendulum>(a, l, T, t0, probs, row_stride, step_stride, launches); break;
     case kSurface: {
-#define M(DD) err = rollout_continuous<Surface<DD>>(a, l, T, t0, probs, row_stride, step_stride, launches)
+#define M(DD) err = rollout_surface<DD>(a, l, T, t0, probs, row_stride, step_stride, launches)
       WS_SURFACE_DISPATCH(a.p0, M)
 #undef M
       break;
