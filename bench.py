@@ -47,6 +47,8 @@ def parse():
     ap.add_argument("--block", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: no clocks / cpu baseline / e2e")
+    ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (gloo only for tests)")
+    ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (multi-rank test on one GPU)")
     return ap.parse_args()
 
 
@@ -183,10 +185,14 @@ def main():
     world, rank, local = dist_env()
     if world != args.gpus and rank == 0:
         print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    torch.cuda.set_device(local)
-    dev = torch.device("cuda", local)
+    local_dev = 0 if args.same_device else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
     if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
 
     # weak scaling: each rank owns a full C2-sized shard of a world*E global batch
     E, A, T = w.n_envs, w.n_agents, w.T
@@ -210,7 +216,7 @@ def main():
     if world > 1:
         dist.barrier()
 
-    clocks = Clocks(local)
+    clocks = Clocks(local_dev)
     if not args.ncu:
         clocks.start()
         time.sleep(0.3)
@@ -238,6 +244,9 @@ def main():
     env.enable_kernel_timing(False)
     clk = clocks.stop() if not args.ncu else {}
 
+    # merged per-slot statistics of the last roll-out (all ranks, exact int64; R20)
+    from paper_2408_00930_b200.parallel import summarize
+    merged = summarize(stats_view.cpu())
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
@@ -302,6 +311,7 @@ def main():
                        "parallelism": f"env-shard x{world} + NCCL stats all-reduce" if world > 1 else "1 GPU",
                        "l2": f"store {all_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "gpu_launches": int(launches),
+            "episode_stats_last_step": merged,
             "clocks": clk, "e2e": e2e,
             "paper_context": "A100 8.6M env-steps/s incl. training (P:39); not like-for-like",
         }
