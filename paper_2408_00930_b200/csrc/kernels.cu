@@ -340,7 +340,10 @@ __device__ __forceinline__ unsigned long long* cta_stats_buf() {
 // (four 8-bit actions of slots 4j..4j+3 per u32, 0xFF = invalid row) that the dynamics
 // kernel reads back with prefetched 32-bit loads.
 // =======================================================================================
-constexpr int kPlanChunk = 128;  // steps per plan thread (thresholds amortised over 128 draws)
+#ifndef WS_PLAN_CHUNK
+#define WS_PLAN_CHUNK 128
+#endif
+constexpr int kPlanChunk = WS_PLAN_CHUNK;  // steps per plan thread (thresholds amortised over the chunk)
 
 template <int N, bool kStrided>
 __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
@@ -677,26 +680,27 @@ __global__ void __launch_bounds__(128) k_plan_gauss(const KArgs a, const int T, 
   if (!kStrided) load_head(probs);
   float* const p_act = reinterpret_cast<float*>(a.act);
   bool any_bad = false;
+  uint64_t cur_blk = ~0ull, cur_pair = ~0ull;
+  U4 w{0, 0, 0, 0};
+  float ze = 0.0f, zo = 0.0f;
   for (int c = c_begin; c < c_end; ++c) {
     if (kStrided) load_head(probs + (int64_t)c * step_stride);
     const uint64_t j0 = (t0 + (uint64_t)c) * (uint64_t)DIM;
     float z[DIM];
-    // draws j0 .. j0 + DIM - 1, pairs aligned at even j
-    uint64_t blk = ~0ull;
-    U4 w{0, 0, 0, 0};
+    // draws j0 .. j0 + DIM - 1; one Box-Muller per aligned pair (2p, 2p+1) and one Philox
+    // call per block, both carried across steps (warp-uniform: every lane has the same j)
 #pragma unroll
     for (int k = 0; k < DIM; ++k) {
       const uint64_t j = j0 + (uint64_t)k;
-      if ((j & 1) == 0 || k == 0) {
-        if ((j >> 2) != blk) {
-          blk = j >> 2;
-          w = block(key, blk, eg, 0, kGauss);
+      if ((j >> 1) != cur_pair) {
+        if ((j >> 2) != cur_blk) {
+          cur_blk = j >> 2;
+          w = block(key, cur_blk, eg, 0, kGauss);
         }
-        float ze, zo;
-        gauss_pair(w, (int)((j & 3) >> 1), ze, zo);
-        z[k] = (j & 1) ? zo : ze;
-        if (k + 1 < DIM && (j & 1) == 0) z[k + 1] = zo;
+        cur_pair = j >> 1;
+        gauss_pair(w, (int)(cur_pair & 1), ze, zo);
       }
+      z[k] = (j & 1) ? zo : ze;
     }
     double lp = 0.0;
     float act[DIM];
@@ -961,15 +965,26 @@ __global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const in
     sd = (float)exp((double)ls);
   };
   if (!kStrided) load_head(probs);
+  // The chunk's GAUSS draws J0 .. J1-1 are Box-Muller pairs (2p, 2p+1): the warp's 32 lanes
+  // each take one pair at a time (one fp64 log / sqrt / sincos per pair, no lane computing a
+  // pair twice) and stage the normals in shared memory; the coordinate lanes then read them.
+  __shared__ float zbuf[4][kGaussChunk * DIM];
+  float* const zb = zbuf[(threadIdx.x >> 5) & 3];
+  const uint64_t J0 = (t0 + (uint64_t)c_begin) * (uint64_t)DIM, J1 = (t0 + (uint64_t)c_end) * (uint64_t)DIM;
+  for (uint64_t pr = (J0 >> 1) + (uint64_t)lane; pr < ((J1 + 1) >> 1); pr += 32) {
+    const U4 w = block(key, pr >> 1, eg, 0, kGauss);
+    float ze, zo;
+    gauss_pair(w, (int)(pr & 1), ze, zo);
+    const int64_t i0 = (int64_t)(2 * pr) - (int64_t)J0;
+    if (i0 >= 0) zb[i0] = ze;
+    if (i0 + 1 < (int64_t)(J1 - J0)) zb[i0 + 1] = zo;
+  }
+  __syncwarp();
   float* const p_act = reinterpret_cast<float*>(a.act) + e * DIM + kk;
   bool any_bad = false;
   for (int c = c_begin; c < c_end; ++c) {
     if (kStrided) load_head(probs + (int64_t)c * step_stride);
-    const uint64_t j = (t0 + (uint64_t)c) * (uint64_t)DIM + (uint64_t)kk;
-    const U4 w = block(key, j >> 2, eg, 0, kGauss);
-    float ze, zo;
-    gauss_pair(w, (int)((j & 3) >> 1), ze, zo);
-    const float z = (j & 1) ? zo : ze;
+    const float z = zb[(c - c_begin) * DIM + kk];
     const double term = act_lane ? (((-0.5 * (double)z) * (double)z - (double)ls) - kHalfLog2Pi) : 0.0;
     const double lp = SurfWarp<DIM>::tree_sum(term);
     const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
