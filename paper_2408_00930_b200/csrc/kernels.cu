@@ -1136,39 +1136,37 @@ __global__ void k_reset_lane(const KArgs a) {
 enum TagMode : int { kTagRollout = 0, kTagStepSlab = 1, kTagStepGiven = 2 };
 constexpr int kTagN = 5;
 
-__device__ __forceinline__ long long block_sum_fx(long long v, long long* red, int nwarps) {
-  // exact integer sum over the CTA (order-independent)
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-#pragma unroll
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-  if (lane == 0) red[wid] = v;
-  __syncthreads();
-  long long s = 0;
-  if (threadIdx.x == 0)
-    for (int i = 0; i < nwarps; ++i) s += red[i];
-  __syncthreads();
-  return s;  // valid in thread 0
-}
+// Shared memory of k_tag: occupancy grids taggers_on / tagged_on [G*G] ints, the reduction
+// buffer (2 int64 per warp) and the observation table x / (G - 1) for x in [0, G).
+__host__ __device__ inline int tag_red_offset(int G) { return 2 * G * G + ((2 * G * G) & 1); }  // in ints
+__host__ __device__ inline int tag_tab_offset(int G, int nwarps) { return tag_red_offset(G) + 4 * nwarps; }
 
-template <int kMaxThreads>
-__global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
+// kHoisted: roll-out with per-step-constant probabilities (thresholds hoisted, no per-step
+// CDF code in the kernel); otherwise the general kernel (per-step rows, ws_step modes).
+template <int kMaxThreads, int kMinBlocks, bool kHoisted>
+__global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
                                               const int slot0, const float* __restrict__ probs,
                                               const int64_t row_stride, const int64_t step_stride,
                                               const void* __restrict__ given) {
   extern __shared__ int smem[];
   const int G = a.p0, NT = a.p1, A = a.A;
+  const int nwarps = blockDim.x >> 5;
   int* taggers_on = smem;
   int* tagged_on = smem + G * G;
-  long long* red = reinterpret_cast<long long*>(smem + 2 * G * G + ((2 * G * G) & 1));
-  const int nwarps = blockDim.x >> 5;
+  long long* red = reinterpret_cast<long long*>(smem + tag_red_offset(G));
+  float* obs_tab = reinterpret_cast<float*>(smem + tag_tab_offset(G, nwarps));
   const int64_t e = blockIdx.x;
   const int ag = threadIdx.x;
-  const int lane = ag & 31;
+  const int lane = ag & 31, wid = ag >> 5;
   const bool is_agent = ag < A;
   const bool tagger = ag < NT;
   const uint32_t eg = (uint32_t)(a.offset + e);
   const Key key{a.k0, a.k1};
-  const float inv = (float)(G - 1);
+
+  // the grids start empty and every step removes its own marks (see below); the coordinate
+  // observations are the G values x / (G - 1) (IEEE division, R22), tabulated once
+  for (int i = ag; i < 2 * G * G; i += blockDim.x) smem[i] = 0;
+  for (int i = ag; i < G; i += blockDim.x) obs_tab[i] = (float)i / (float)(G - 1);
 
   int32_t x = 0, y = 0, active = 0;
   if (is_agent) {
@@ -1184,11 +1182,15 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
 
   Thresholds<kTagN> th;
   const int64_t row0 = e * A;  // rows of this replica
-  if (mode == kTagRollout && step_stride == 0) {
+  constexpr bool hoisted = kHoisted;  // == (mode == kTagRollout && step_stride == 0)
+  if (hoisted) {
     RowCDF<kTagN> cdf;
     warp_row_cdf<kTagN>(probs + row0 * row_stride, row_stride, (int64_t)(ag - lane), A, lane, cdf);
     make_thresholds<kTagN>(cdf, th);
   }
+  // with fixed probabilities an invalid row is invalid at every step: one vote up front
+  const bool any_bad_rows = hoisted ? (__syncthreads_or(is_agent && th.bad) != 0) : false;
+  __syncthreads();
   U4 w{0, 0, 0, 0};
   for (int c = 0; c < T; ++c) {
     const int slot = slot0 + c;
@@ -1196,11 +1198,11 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
     const size_t idx = ((size_t)slot * (size_t)a.E + (size_t)e) * (size_t)A + (size_t)ag;
     int act = 0;
     bool bad_probs = false;
-    if (mode == kTagRollout) {
+    if (kHoisted || mode == kTagRollout) {
       if (c == 0 || (t & 3) == 0) w = block(key, t >> 2, eg, (uint32_t)ag, kAction);
       const uint32_t word = pick(w, (uint32_t)(t & 3));
       float lp;
-      if (step_stride == 0) {
+      if (kHoisted) {
         act = search_k<kTagN>(th, word >> 8, lp);
         bad_probs = th.bad;
       } else {
@@ -1230,11 +1232,11 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
     }
     // pre-step observation (x/(G-1), y/(G-1), is_tagger, active)  (R22)
     if (is_agent) {
-      const float4 o = make_float4((float)x / inv, (float)y / inv, tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
+      const float4 o = make_float4(obs_tab[x], obs_tab[y], tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
       st_cs(reinterpret_cast<float4*>(a.obs) + idx, o);
     }
     const bool invalid = is_agent && (act < 0 || act > 4);
-    const bool any_invalid = __syncthreads_or(invalid) != 0;
+    const bool any_invalid = hoisted ? any_bad_rows : (__syncthreads_or(invalid) != 0);
     float r = 0.0f;
     uint8_t d = 0;
     if (!any_invalid) {
@@ -1248,16 +1250,16 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
         x = min(max(nx, 0), G - 1);
         y = min(max(ny, 0), G - 1);
       }
-      for (int i = ag; i < 2 * G * G; i += blockDim.x) smem[i] = 0;
-      __syncthreads();
       const int cell = y * G + x;
       if (is_agent && tagger) atomicAdd(&taggers_on[cell], 1);
       __syncthreads();
+      bool newly = false;
       if (is_agent && !tagger) {
         if (active) {
           if (taggers_on[cell] >= 1) {
             r = -1.0f;
             active = 0;
+            newly = true;
             atomicAdd(&tagged_on[cell], 1);
           } else {
             r = 0.01f;
@@ -1267,29 +1269,49 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
       __syncthreads();
       if (is_agent && tagger) r = (float)tagged_on[cell] / (float)taggers_on[cell];
       const int still = __syncthreads_count(is_agent && !tagger && active);
+      // every reader of the grids is past the count barrier: remove this step's marks, so the
+      // grids are empty again before the next step's first barrier (adds commute)
+      if (is_agent && tagger) atomicAdd(&taggers_on[cell], -1);
+      if (newly) atomicAdd(&tagged_on[cell], -1);
       const bool term = n_runners > 0 && still == 0;
       ep_step += 1;
       const bool trunc = ep_step >= a.max_steps;
       d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
       if (is_agent) ep_ret = ep_ret + r;
-    } else if (threadIdx.x == 0) {
-      atomicOr(a.err, kErrAction | (mode == kTagRollout && bad_probs ? kErrProbs : 0u));
+    } else {
+      if (threadIdx.x == 0) atomicOr(a.err, kErrAction | (mode == kTagRollout && bad_probs ? kErrProbs : 0u));
+      if (hoisted) __syncthreads();  // orders the previous step's reduction reads (no vote barrier here)
     }
     if (is_agent) st_cs(a.rew + idx, r);
-    // A8: per-replica partial (sum of rewards; on done, return over agents and length)
-    const long long rs = block_sum_fx(is_agent ? to_fx(r) : 0ll, red, nwarps);
-    long long rt = 0;
-    if (d) rt = block_sum_fx(is_agent ? to_fx(ep_ret) : 0ll, red, nwarps);
+    // A8: one exact CTA reduction of (sum of rewards, sum of episode returns) -- the latter
+    // is used only when the episode ended (d is CTA-uniform)
+    long long rs = is_agent ? to_fx(r) : 0ll;
+    long long rt = is_agent ? to_fx(ep_ret) : 0ll;
+#pragma unroll
+    for (int o = 16; o > 0; o >>= 1) {
+      rs += __shfl_xor_sync(kFull, rs, o);
+      rt += __shfl_xor_sync(kFull, rt, o);
+    }
+    if (lane == 0) {
+      red[2 * wid] = rs;
+      red[2 * wid + 1] = rt;
+    }
+    __syncthreads();
     if (threadIdx.x == 0) {
+      long long srs = 0, srt = 0;
+      for (int i = 0; i < nwarps; ++i) {
+        srs += red[2 * i];
+        srt += red[2 * i + 1];
+      }
       const size_t di = (size_t)slot * (size_t)a.E + (size_t)e;
       st_cs_u8(a.done + di, d);
       unsigned long long* st = a.stats + (size_t)slot * 4;
       if (d) {
         atomicAdd(st + kStEpisodes, 1ull);
         atomicAdd(st + kStLength, (unsigned long long)ep_step);
-        if (rt) atomicAdd(st + kStReturn, (unsigned long long)rt);
+        if (srt) atomicAdd(st + kStReturn, (unsigned long long)srt);
       }
-      if (rs) atomicAdd(st + kStReward, (unsigned long long)rs);
+      if (srs) atomicAdd(st + kStReward, (unsigned long long)srs);
     }
     if (d) {  // A5 auto-reset, uniform across the CTA
       rc += 1;
@@ -1303,7 +1325,8 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
       ep_step = 0;
       ep_ret = 0.0f;
     }
-    __syncthreads();
+    // (the reduction buffer is next written after at least one more CTA barrier, which
+    // thread 0 reaches only after reading it)
   }
   if (is_agent) {
     int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
@@ -1312,7 +1335,7 @@ __global__ void __launch_bounds__(kMaxThreads) k_tag(const KArgs a, const int mo
     ts[2] = active;
     a.ep_ret[e * A + ag] = ep_ret;
     reinterpret_cast<float4*>(a.obs_live)[e * A + ag] =
-        make_float4((float)x / inv, (float)y / inv, tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
+        make_float4(obs_tab[x], obs_tab[y], tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f);
   }
   if (threadIdx.x == 0) {
     a.ep_step[e] = ep_step;
@@ -1438,22 +1461,28 @@ __global__ void k_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
 static size_t tag_smem(const KArgs& a, int block) {
-  return (size_t)(2 * a.p0 * a.p0 + 2) * sizeof(int) + (size_t)(block / 32) * sizeof(long long);
+  return (size_t)(tag_tab_offset(a.p0, block / 32) + a.p0) * sizeof(int);
 }
 static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
 
 // CTA per replica (A threads rounded up to a warp multiple)
 static void tag_launch(const KArgs& a, const Launch& l, int b, int mode, int T, uint64_t t0, int slot0,
                        const float* probs, int64_t row_stride, int64_t step_stride, const void* given) {
-  if (b <= 128)  // 64 registers: 8 CTAs per SM beat fewer, spill-free CTAs (measured, C4)
-    k_tag<1024><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
-                                                                  given);
-  else if (b <= 256)
-    k_tag<256><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
-                                                                 given);
-  else
-    k_tag<1024><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, step_stride,
-                                                                  given);
+#ifndef WS_TAG_MINB
+#define WS_TAG_MINB 6
+#endif
+#define WS_TAG_LAUNCH(MT, MB, H)                                                                        \
+  k_tag<MT, MB, H><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, \
+                                                                  step_stride, given)
+  const bool h = mode == kTagRollout && step_stride == 0;
+  if (b <= 128) {  // 6 CTAs of 128 threads per SM (measured best for C4: 7 and 8 force spills / fewer registers)
+    if (h) WS_TAG_LAUNCH(128, WS_TAG_MINB, true); else WS_TAG_LAUNCH(128, WS_TAG_MINB, false);
+  } else if (b <= 256) {
+    if (h) WS_TAG_LAUNCH(256, 1, true); else WS_TAG_LAUNCH(256, 1, false);
+  } else {
+    if (h) WS_TAG_LAUNCH(1024, 1, true); else WS_TAG_LAUNCH(1024, 1, false);
+  }
+#undef WS_TAG_LAUNCH
 }
 
 // lane kernels carry one statistics window per warp in dynamic shared memory
