@@ -175,6 +175,53 @@ def test_cartpole_random_probs_per_step(P):
     compare(buf, o, amb, "cartpole", T)
 
 
+@pytest.mark.parametrize("env,A,n,params", [("acrobot", 1, 3, {}), ("dummy", 1, 2, {}), ("tag", 37, 5, {"p0": 9, "p1": 6})])
+def test_discrete_per_step_probs(P, env, A, n, params):
+    """Per-step probability rows (step_stride != 0) for the other discrete envs: the plan
+    kernel's strided path (lane envs) and the tag kernel's per-step CDF variant."""
+    E, T = 80, 96
+    probs = W.random_probs(E, A, n, seed=21, zero_frac=0.25, T=T)
+    g, o, buf, amb = run_pair(P, env, E, T, A=A, probs=probs, step_stride=E * A * n, params=params)
+    compare(buf, o, amb, env, T)
+
+
+@pytest.mark.parametrize("env,d,params", [("pendulum", 1, {}), ("surface", 20, {"p0": 20}), ("surface", 3, {"p0": 3})])
+def test_gaussian_per_step_params(P, env, d, params):
+    """Per-step Gaussian heads (step_stride != 0): both Gaussian plan kernels' strided paths."""
+    E, T = 64, 70
+    ls = float(np.log(0.025)) if env == "surface" else 0.0
+    probs = np.stack([W.gaussian_params(E, 1, d, 0.0, ls, jitter=0.3, seed=100 + t) for t in range(T)])
+    g, o, buf, amb = run_pair(P, env, E, T, probs=probs, step_stride=E * 2 * d, params=params)
+    compare(buf, o, amb, env, T)
+
+
+@pytest.mark.parametrize("env,A,n,step_stride", [("cartpole", 1, 2, False), ("acrobot", 1, 3, False),
+                                                 ("tag", 20, 5, False), ("cartpole", 1, 2, True),
+                                                 ("tag", 20, 5, True)])
+def test_invalid_probability_rows_in_rollout(P, env, A, n, step_stride):
+    """R13/R19 inside a fused roll-out: rows with p < 0, NaN or zero sum give act -1 and NaN
+    logp, the replica (tag: the whole replica step) does not advance, rew = done = 0, and the
+    status is WS_ERR_INVALID_PROBS -- element for element as the oracle."""
+    E, T = 96, 60
+    probs = W.random_probs(E, A, n, seed=13, zero_frac=0.2, T=T if step_stride else None)
+    bad = probs[7] if step_stride else probs
+    bad[5, 0, 0] = -1.0
+    bad[40, A - 1, 1] = np.nan
+    bad[77, 0, :] = 0.0
+    ss = E * A * n if step_stride else 0
+    g = P.Env(E, A, env, SEED, t_capacity=T)
+    g.rollout(T, torch.from_numpy(np.ascontiguousarray(probs)).cuda(), row_stride=n, step_stride=ss)
+    assert g.status() == P._abi.INVALID_PROBS
+    o = O.Batch(env, E, A, SEED, t_capacity=T)
+    amb = np.zeros((T, E, A), np.uint8)
+    assert o.rollout(T, probs, row_stride=n, step_stride=ss, ambiguous=amb, n_threads=4) == 0
+    assert o.synchronize() == P._abi.INVALID_PROBS
+    buf = {k: (v.cpu().numpy() if v is not None else None) for k, v in g.buffers().items()}
+    act = buf["act"][:T]
+    assert (act[:, [5, 40, 77]] == -1).any()
+    compare(buf, o, amb, env, T)
+
+
 def test_fixed_actions_64_steps(P):
     """BJ:5: fp32 states and rewards within 1e-5 relative per step for fixed action
     sequences over 64 steps (ws_step with given actions), E = 1024."""
