@@ -33,8 +33,15 @@ import wsinputs as W  # noqa: E402
 # that writes them: the roll-out kernel writes obs (D_obs*4) + rew (4) + done (1); the plan
 # kernel writes act (4) + logp (4).  Per agent; done is per replica.
 OBS_DIM = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3, "tag": 4, "surface": 21}
-ROLLOUT_BYTES = {k: 4 * d + 4 + 1 for k, d in OBS_DIM.items()}
-PLAN_BYTES = {k: 8 for k in OBS_DIM}
+# algorithmic bytes per env-step: the roll-out kernel writes obs + rew + done
+# and reads its actions (discrete: the packed plan, 1 byte; continuous: the act slab, 4 d);
+# the plan kernel writes act + logp (+ the packed plan for discrete envs)
+ACT_DIM = {"pendulum": 1, "surface": 20}
+ROLLOUT_BYTES = {k: 4 * d + 4 + 1 + (4 * ACT_DIM[k] if k in ACT_DIM else 0.25) for k, d in OBS_DIM.items()}
+PLAN_BYTES = {k: (4 * ACT_DIM[k] + 4 if k in ACT_DIM else 8.25) for k in OBS_DIM}
+KERNEL_NAME = {"cartpole": "k_rollout_discrete<CartPole>", "acrobot": "k_rollout_discrete<Acrobot>",
+               "dummy": "k_rollout_discrete<Dummy>", "pendulum": "k_rollout_continuous<Pendulum>",
+               "surface": "k_rollout_surface_seg<20>", "tag": "k_tag"}
 
 
 def parse():
@@ -260,14 +267,15 @@ def main():
     peak = float(peaks.get("hbm_gbs", 6650.0))
     n_roll, roll_ms = ktimes.get("rollout", (0, 0.0))
     n_plan, plan_ms = ktimes.get("plan", (0, 0.0))
-    roll_bytes = ROLLOUT_BYTES.get(w.env, 0) * E * A * T if w.env != "tag" else (4 * 4 + 4) * E * A * T + E * T
+    # tag samples inside its roll-out kernel: obs 16 + rew 4 + act 4 + logp 4 per agent-step, done 1 per env-step
+    roll_bytes = int(ROLLOUT_BYTES.get(w.env, 0) * E * A * T if w.env != "tag" else (16 + 4 + 4 + 4) * E * A * T + E * T)
     achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
     call_ms = sum(kern_ms) / len(kern_ms)
-    all_bytes = roll_bytes + PLAN_BYTES.get(w.env, 8) * E * A * T
+    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T if w.env != "tag" else 0))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
-                "kernel": f"k_rollout_discrete<{w.env}>" if n_plan else "k_rollout",
+                "kernel": KERNEL_NAME.get(w.env, "k_rollout"),
                 "kernel_ms": round(roll_ms, 4), "launches_timed": n_roll,
                 "bytes_per_launch": roll_bytes, "bytes_per_env_step": roll_bytes / (E * A * T),
                 "other_kernels": {"plan": {"ms": round(plan_ms, 4), "launches": n_plan,

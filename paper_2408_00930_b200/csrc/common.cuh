@@ -170,6 +170,18 @@ __device__ __forceinline__ float warp_sum_f32(float v) {
   return v;
 }
 
+// Exact warp sum of 64-bit integers (mod 2^64, i.e. exact for two's-complement values whose
+// sum fits): each value is split into four 16-bit chunks, each chunk column is summed with
+// one REDUX (32 x (2^16 - 1) < 2^32, no overflow) and the four sums are recombined.
+__device__ __forceinline__ unsigned long long warp_sum_u64(unsigned long long v) {
+  const unsigned c0 = __reduce_add_sync(kFull, (unsigned)(v & 0xFFFFu));
+  const unsigned c1 = __reduce_add_sync(kFull, (unsigned)((v >> 16) & 0xFFFFu));
+  const unsigned c2 = __reduce_add_sync(kFull, (unsigned)((v >> 32) & 0xFFFFu));
+  const unsigned c3 = __reduce_add_sync(kFull, (unsigned)(v >> 48));
+  return (unsigned long long)c0 + ((unsigned long long)c1 << 16) + ((unsigned long long)c2 << 32) +
+         ((unsigned long long)c3 << 48);
+}
+
 // A8 statistics are exact fixed-point integers: stats[slot] = {episodes, sum of returns
 // x 2^32, sum of lengths, sum of rewards x 2^32} as int64.  Every per-replica value is
 // converted once (an fp32 reward r is represented exactly whenever |r| >= 2^-8 and

@@ -801,142 +801,287 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
 __device__ const double kMB[6][4] = {{-200, -100, -170, 15}, {-1, -1, -6.5, 0.7}, {0, 0, 11, 0.6},
                                       {-10, -10, -6.5, 0.7}, {1, 0, -0.5, -1}, {0, 0.5, 1.5, 1}};
 
+// fixed-order xor-butterfly fp64 sum (all lanes get the same value): used where only an fp32
+// rounding at <= 2 ulp tolerance follows (the Gaussian log-density, R18), so the association
+// need not match the oracle's sequential loop
+__device__ __forceinline__ double warp_tree_sum(double v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
+  return v;
+}
+
+// =======================================================================================
+// A7 for surface-D, segmented: each replica is a segment of L = ceil(D/4) lanes holding four
+// coordinates each, so a warp advances R = 32 / L replicas at once (D = 20: 5 lanes, 6
+// replicas).  The coordinate-parallel work (action clip, update, observation stores, reset
+// draws, goal-distance partials) stays on the lanes; the two order-sensitive fp64 sums of
+// the energy -- the four Mueller-Brown terms and the spring term over coordinates 2..D-1 --
+// are gathered through shared memory and added sequentially in coordinate order, exactly
+// as Surface<D>::energy and the oracle do (R23).  The goal distance only feeds a comparison,
+// so its partials are added per lane, then over the segment.
+// =======================================================================================
 template <int D>
-struct SurfWarp {
+struct SurfSeg {
+  static constexpr int C = 4;                // coordinates per lane
+  static constexpr int L = (D + C - 1) / C;  // lanes per replica
+  static constexpr int R = 32 / L;           // replicas per warp
+};
+// per warp: qv [40][4] f32, sq [40][4] f64, mb [34][4] f64, gp [40] f64 -- lanes past the last
+// whole segment (D = 20: lanes 30, 31) work on a scratch segment R, so no branch diverges
+constexpr int kSegSlots = 40;
+constexpr int kSegWarpBytes = kSegSlots * 4 * 4 + kSegSlots * 4 * 8 + 34 * 4 * 8 + kSegSlots * 8;
+
+template <int D>
+struct SurfSegWarp {
   using Env = Surface<D>;
-  // sequential fp64 sum of v over lanes [lo, hi) (all lanes get the result)
-  template <int LO, int HI>
-  __device__ static double ordered_sum(double v) {
-    double s = 0.0;
+  using G = SurfSeg<D>;
+  static constexpr int C = G::C, L = G::L, R = G::R;
+  float* qv;   // [32][C] coordinates of the state being evaluated
+  double* sq;  // [32][C] squares (coordinates >= 2)
+  double* mb;  // [R][4] Mueller-Brown terms
+  double* gp;  // [32] goal-distance partials
+  int lane, seg, sl;
+  bool used;
+  double mc[6];  // Mueller-Brown coefficients (A, a, b, c, x0, y0) of term sl (L >= 4)
+
+  __device__ __forceinline__ void load_coefficients() {
 #pragma unroll
-    for (int i = LO; i < HI; ++i) s += __shfl_sync(kFull, v, i);
-    return s;
+    for (int i = 0; i < 6; ++i) mc[i] = __ldg(&kMB[i][sl < 4 ? sl : 0]);
   }
-  // fixed-order xor-butterfly fp64 sum (all lanes get the same value): used where only a
-  // comparison (goal distance) or an fp32 rounding at <= 2 ulp tolerance (log-density)
-  // follows, so the association need not match the oracle's sequential loop
-  __device__ static double tree_sum(double v) {
+  __device__ __forceinline__ bool valid(int i) const { return sl * C + i < D; }
+  // energy of the segment's state q (this lane's C coordinates); warp-collective
+  __device__ __forceinline__ float energy(const float (&q)[C]) {
+    __syncwarp();
 #pragma unroll
-    for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(kFull, v, o);
-    return v;
-  }
-  __device__ static float energy(float qk, int lane) {
-    const double x = (double)__shfl_sync(kFull, qk, 0), y = (double)__shfl_sync(kFull, qk, 1);
-    double ex = 0.0;
-    if (lane < 4) {
-      const double dx = x - __ldg(&kMB[4][lane]), dy = y - __ldg(&kMB[5][lane]);
-      ex = __ldg(&kMB[0][lane]) *
-           exp(__ldg(&kMB[1][lane]) * dx * dx + __ldg(&kMB[2][lane]) * dx * dy + __ldg(&kMB[3][lane]) * dy * dy);
+    for (int i = 0; i < C; ++i) {
+      const int k = sl * C + i;
+      qv[lane * C + i] = q[i];
+      sq[lane * C + i] = (k >= 2 && k < D) ? (double)q[i] * (double)q[i] : 0.0;
     }
-    const double E = ordered_sum<0, 4>(ex);
-    const double sq = (lane >= 2 && lane < D) ? (double)qk * (double)qk : 0.0;
-    const double spring = ordered_sum<2, D>(sq);
+    __syncwarp();
+    const int base = seg * L * C;
+    const double x = (double)qv[base], y = (double)qv[base + 1];
+    if constexpr (L >= 4) {  // one term per lane, coefficients in registers
+      if (sl < 4) {
+        const double dx = x - mc[4], dy = y - mc[5];
+        mb[seg * 4 + sl] = mc[0] * exp(mc[1] * dx * dx + mc[2] * dx * dy + mc[3] * dy * dy);
+      }
+    } else {
+#pragma unroll
+      for (int m0 = 0; m0 < 4; m0 += L) {
+        const int m = m0 + sl;
+        if (m < 4) {
+          const double dx = x - __ldg(&kMB[4][m]), dy = y - __ldg(&kMB[5][m]);
+          mb[seg * 4 + m] = __ldg(&kMB[0][m]) * exp(__ldg(&kMB[1][m]) * dx * dx + __ldg(&kMB[2][m]) * dx * dy +
+                                                    __ldg(&kMB[3][m]) * dy * dy);
+        }
+      }
+    }
+    __syncwarp();
+    const double2 m01 = reinterpret_cast<const double2*>(mb + seg * 4)[0];
+    const double2 m23 = reinterpret_cast<const double2*>(mb + seg * 4)[1];
+    const double E = (((0.0 + m01.x) + m01.y) + m23.x) + m23.y;
+    // all squares are fetched first (16-byte loads), then added in coordinate order
+    const double2* sp = reinterpret_cast<const double2*>(sq + base);
+    double v[((D + 1) / 2) * 2];
+#pragma unroll
+    for (int k = 0; k < (D + 1) / 2; ++k) {
+      const double2 t = sp[k];
+      v[2 * k] = t.x;
+      v[2 * k + 1] = t.y;
+    }
+    double spring = 0.0;
+#pragma unroll
+    for (int k = 2; k < D; ++k) spring += v[k];
     return (float)(E + 0.5 * Env::kappa * spring);
   }
-  __device__ static float init(const Key& key, uint32_t eg, uint32_t rc, int lane) {
-    const uint64_t j = (uint64_t)rc * D + (uint64_t)(lane < D ? lane : 0);
-    const U4 b = block(key, j >> 2, eg, 0, kReset);
-    return Env::start(lane) + (-0.05f + 0.1f * u01(pick(b, (uint32_t)(j & 3))));
+  // squared distance of the segment's state to the goal (fixed association; comparison only)
+  __device__ __forceinline__ double goal_d2(const float (&q)[C]) {
+    double p = 0.0;
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      if (valid(i)) {
+        const double di = (double)q[i] - Env::goal(sl * C + i);
+        p += di * di;
+      }
+    }
+    __syncwarp();
+    gp[lane] = p;
+    __syncwarp();
+    double g[L];
+#pragma unroll
+    for (int j = 0; j < L; ++j) g[j] = gp[seg * L + j];
+    double d2 = 0.0;
+#pragma unroll
+    for (int j = 0; j < L; ++j) d2 += g[j];
+    return d2;
   }
 };
 
 template <int D>
-__global__ void __launch_bounds__(256) k_rollout_surface_warp(const KArgs a, const int T) {
-  using SW = SurfWarp<D>;
+__global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, const int T) {
   using Env = Surface<D>;
-  const int lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  using SW = SurfSegWarp<D>;
+  constexpr int C = SW::C, L = SW::L, R = SW::R;
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  const int lane = threadIdx.x & 31, wib = threadIdx.x >> 5;
   const int64_t E = a.E;
-  if (e >= E) return;  // whole warp past the last replica
+  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // global warp index
+  if (wg * R >= E) return;  // whole warp past the last replica
+  SW w;
+  {
+    char* wb = reinterpret_cast<char*>(ws_smem) + 256 * sizeof(unsigned long long) + wib * kSegWarpBytes;
+    w.qv = reinterpret_cast<float*>(wb);
+    w.sq = reinterpret_cast<double*>(wb + kSegSlots * C * 4);
+    w.mb = reinterpret_cast<double*>(wb + kSegSlots * C * 4 + kSegSlots * C * 8);
+    w.gp = reinterpret_cast<double*>(wb + kSegSlots * C * 4 + kSegSlots * C * 8 + 34 * 4 * 8);
+  }
+  w.lane = lane;
+  w.seg = lane / L;
+  w.sl = lane % L;
+  w.used = w.seg < R;  // lanes of the scratch segment R (if any) compute but never store
+  w.load_coefficients();
+  const int seg = w.used ? w.seg : R - 1, sl = w.sl;
+  const int64_t e_raw = wg * R + seg;
+  const bool live = w.used && e_raw < E;      // this segment simulates a real replica
+  const int64_t e = e_raw < E ? e_raw : E - 1;  // else it shadows replica E-1 (identical stores)
+  const bool leader = live && sl == 0;
   const uint32_t eg = (uint32_t)(a.offset + e);
   const Key key{a.k0, a.k1};
-  const bool act_lane = lane < D;
-  const int kk = act_lane ? lane : 0;
-  const float lo = Env::lo(kk), hi = Env::hi(kk);
-  const double goal = Env::goal(kk);
   const size_t sE = (size_t)E;
-  float* const p_obs = a.obs + e * (D + 1);
-  const float* const p_act = reinterpret_cast<const float*>(a.act) + e * D + kk;
   CtaStats cta;
   {
-    const int64_t first = (int64_t)blockIdx.x * (blockDim.x >> 5);
-    const int64_t live_warps = min((int64_t)(blockDim.x >> 5), E - first);
-    cta.buf = cta_stats_buf_only();
-    cta.n_live_threads = (int)live_warps * 32;
-    cta.leader = (threadIdx.x >> 5) == 0;
+    const int64_t first_w = (int64_t)blockIdx.x * (blockDim.x >> 5);
+    int64_t live_w = 0;
+    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) live_w += ((first_w + i) * R < E) ? 1 : 0;
+    cta.buf = reinterpret_cast<unsigned long long*>(ws_smem);
+    cta.n_live_threads = (int)live_w * 32;
+    cta.leader = wib == 0;
     for (int i = threadIdx.x; i < 256; i += cta.n_live_threads) cta.buf[i] = 0ull;
     asm volatile("bar.sync 1, %0;" ::"r"(cta.n_live_threads) : "memory");
   }
-
-  float q = a.state[e * D + kk];
-  float Ecur = SW::energy(q, lane);
+  float lo[C], hi[C], q[C];
+#pragma unroll
+  for (int i = 0; i < C; ++i) {
+    const int k = sl * C + i;
+    lo[i] = Env::lo(k < D ? k : 0);
+    hi[i] = Env::hi(k < D ? k : 0);
+    q[i] = k < D ? a.state[e * D + k] : 0.0f;
+  }
+  float Ecur = w.energy(q);
   int32_t ep_step = a.ep_step[e];
   uint32_t rc = a.reset_count[e];
   float ep_ret = a.ep_ret[e];
   uint32_t err = 0;
-  float an = __ldcg(p_act);
+  const float* const p_act = reinterpret_cast<const float*>(a.act) + e * D + sl * C;
+  float* const p_obs = a.obs + e * (D + 1) + sl * C;
+  auto load_act = [&](int c, float (&v)[C]) {
+    const float* p = p_act + (size_t)c * sE * D;
+    if constexpr (D % 4 == 0) {
+      const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
+      v[0] = t.x; v[1] = t.y; v[2] = t.z; v[3] = t.w;
+    } else {
+#pragma unroll
+      for (int i = 0; i < C; ++i) v[i] = w.valid(i) ? __ldcg(p + i) : 0.0f;
+    }
+  };
+  float an[C];
+  load_act(0, an);
   for (int c = 0; c < T; ++c) {
-    const float ak_in = an;
-    if (c + 1 < T) an = __ldcg(p_act + (size_t)(c + 1) * sE * D);
+    float ak[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) ak[i] = an[i];
+    if (c + 1 < T) load_act(c + 1, an);
     const size_t idx = (size_t)c * sE + (size_t)e;
     // pre-step observation (q, E(q))
-    if (act_lane) st_cs(p_obs + (size_t)c * sE * (D + 1) + lane, q);
-    if (lane == (D < 32 ? D : 0)) st_cs(p_obs + (size_t)c * sE * (D + 1) + D, Ecur);
-    const bool ok = __all_sync(kFull, !act_lane || isfinite(ak_in));
+    if (w.used) {
+      float* po = p_obs + (size_t)c * sE * (D + 1);
+#pragma unroll
+      for (int i = 0; i < C; ++i)
+        if (w.valid(i)) st_cs(po + i, q[i]);
+      if (sl == L - 1) st_cs(po + (D - sl * C), Ecur);
+    }
+    // a replica step is valid iff all D action components are finite
+    bool bad_lane = false;
+#pragma unroll
+    for (int i = 0; i < C; ++i) bad_lane = bad_lane || (w.valid(i) && !isfinite(ak[i]));
+    const unsigned bm = __ballot_sync(kFull, w.used && bad_lane);
+    const bool ok = ((bm >> (seg * L)) & ((1u << L) - 1u)) == 0u;
+    float qn[C];
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const float ai = fminf(fmaxf(ak[i], -Env::delta), Env::delta);
+      qn[i] = w.valid(i) ? fminf(fmaxf(q[i] + ai, lo[i]), hi[i]) : 0.0f;
+      if (!ok) qn[i] = q[i];
+    }
+    const float En = w.energy(qn);
+    const double d2 = w.goal_d2(qn);
     float r = 0.0f;
     uint32_t d = 0;
-    float qn = q, En = Ecur;
     if (ok) {
-      const float ak = fminf(fmaxf(ak_in, -Env::delta), Env::delta);
-      const float qi = q + ak;
-      qn = act_lane ? fminf(fmaxf(qi, lo), hi) : 0.0f;
-      En = SW::energy(qn, lane);
-      const double di = act_lane ? (double)qn - goal : 0.0;
-      const double d2 = SW::tree_sum(di * di);
       const bool term = d2 < Env::r_goal * Env::r_goal;
       r = -(Env::w_E * (En - Ecur)) - Env::c_step;
       if (term) r = r + Env::bonus;
       const int32_t es = ep_step + 1;
       d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
       const float ret = ep_ret + r;
-      if (lane == 0) {
-        unsigned long long* acc = cta.acc(c >> 5) + (c & 31) * 4;
-        atomicAdd(acc + kStReward, (unsigned long long)to_fx(r));
-        if (d) {
-          atomicAdd(acc + kStEpisodes, 1ull);
-          atomicAdd(acc + kStLength, (unsigned long long)es);
-          atomicAdd(acc + kStReturn, (unsigned long long)to_fx(ret));
-        }
+      if (leader && d) {  // episode ends: rare except at the (synchronous) truncation step
+        unsigned long long* ac = cta.acc(c >> 5) + (c & 31) * 4;
+        atomicAdd(ac + kStEpisodes, 1ull);
+        atomicAdd(ac + kStLength, (unsigned long long)es);
+        atomicAdd(ac + kStReturn, (unsigned long long)to_fx(ret));
       }
-      if (d) {  // auto-reset: every lane draws its own coordinate (warp-uniform branch)
-        rc += 1;
-        qn = SW::init(key, eg, rc, lane);
-        En = SW::energy(qn, lane);
-        ep_step = 0;
-        ep_ret = 0.0f;
-      } else {
-        ep_step = es;
-        ep_ret = ret;
-      }
-      q = qn;
+      ep_step = d ? 0 : es;
+      ep_ret = d ? 0.0f : ret;
+#pragma unroll
+      for (int i = 0; i < C; ++i) q[i] = qn[i];
       Ecur = En;
-    } else if (lane == 0) {
+    } else if (leader) {
       err |= kErrAction;
     }
-    if (lane == 0) {
+    {  // slot reward sum over the warp's replicas: exact 64-bit sum by four 16-bit REDUXes
+      const unsigned long long sr = warp_sum_u64(leader ? (unsigned long long)to_fx(r) : 0ull);
+      if (lane == 0 && sr) atomicAdd(cta.acc(c >> 5) + (c & 31) * 4 + kStReward, sr);
+    }
+    if (leader) {
       st_cs(a.rew + idx, r);
       st_cs_u8(a.done + idx, (uint8_t)d);
     }
+    // A5 auto-reset: the segment's lanes draw their own coordinates (draws j = rc*D + k)
+    if (__any_sync(kFull, w.used && d != 0)) {
+      if (d) {
+        rc += 1;
+#pragma unroll
+        for (int i = 0; i < C; ++i) {
+          const int k = sl * C + i;
+          if (k < D) {
+            const uint64_t j = (uint64_t)rc * D + (uint64_t)k;
+            const U4 b = block(key, j >> 2, eg, 0, kReset);
+            q[i] = Env::start(k) + (-0.05f + 0.1f * u01(pick(b, (uint32_t)(j & 3))));
+          }
+        }
+      }
+      const float Er = w.energy(q);
+      if (d) Ecur = Er;
+    }
     if ((c & 31) == 31 || c == T - 1) cta.push(lane, c >> 5, 0, c & 31, c & ~31, a.stats);
   }
-  if (act_lane) a.state[e * D + lane] = q;
-  if (act_lane) a.obs_live[e * (D + 1) + lane] = q;
-  if (lane == (D < 32 ? D : 0)) a.obs_live[e * (D + 1) + D] = Ecur;
-  if (lane == 0) {
-    a.ep_step[e] = ep_step;
-    a.reset_count[e] = rc;
-    a.ep_ret[e] = ep_ret;
-    if (err) atomicOr(a.err, err);
+  if (live) {
+#pragma unroll
+    for (int i = 0; i < C; ++i) {
+      const int k = sl * C + i;
+      if (k < D) {
+        a.state[e * D + k] = q[i];
+        a.obs_live[e * (D + 1) + k] = q[i];
+      }
+    }
+    if (sl == L - 1) a.obs_live[e * (D + 1) + D] = Ecur;
+    if (sl == 0) {
+      a.ep_step[e] = ep_step;
+      a.reset_count[e] = rc;
+      a.ep_ret[e] = ep_ret;
+      if (err) atomicOr(a.err, err);
+    }
   }
 }
 
@@ -986,7 +1131,7 @@ __global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const in
     if (kStrided) load_head(probs + (int64_t)c * step_stride);
     const float z = zb[(c - c_begin) * DIM + kk];
     const double term = act_lane ? (((-0.5 * (double)z) * (double)z - (double)ls) - kHalfLog2Pi) : 0.0;
-    const double lp = SurfWarp<DIM>::tree_sum(term);
+    const double lp = warp_tree_sum(term);
     const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
     if (act_lane) st_cs(p_act + (size_t)c * (size_t)a.E * DIM, ok ? mean + sd * z : __int_as_float(0x7fc00000));
     if (lane == 0 && a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : __int_as_float(0x7fc00000));
@@ -1571,9 +1716,12 @@ static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint6
   *launches += 1;
   cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
-  const int wpb = l.block / 32;  // replicas per CTA
+  const int wpb = l.block / 32;  // warps per CTA
   l.m(kKRollout, 0);
-  k_rollout_surface_warp<D><<<grid_for(a.E, wpb), l.block, 256 * sizeof(unsigned long long), l.stream>>>(a, T);
+  {  // segments of ceil(D/4) lanes, 32 / ceil(D/4) replicas per warp
+    const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * kSegWarpBytes;
+    k_rollout_surface_seg<D><<<grid_for(a.E, (int64_t)wpb * SurfSeg<D>::R), l.block, smem, l.stream>>>(a, T);
+  }
   l.m(kKRollout, 1);
   return cudaGetLastError();
 }

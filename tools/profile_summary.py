@@ -32,7 +32,10 @@ def ncu(*args):
 
 
 def raw_metrics(rep):
-    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv"))))
+    return raw_rows(list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "raw", "--csv")))))
+
+
+def raw_rows(rows):
     if len(rows) < 3:
         return {}
     h, u = rows[0], rows[1]
@@ -48,7 +51,10 @@ def raw_metrics(rep):
 
 
 def source_mix(rep):
-    rows = list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass"))))
+    return source_rows(list(csv.reader(io.StringIO(ncu("-i", rep, "--page", "source", "--csv", "--print-source", "sass")))))
+
+
+def source_rows(rows):
     if len(rows) < 3:
         return {}
     h = rows[1]
@@ -72,11 +78,29 @@ def source_mix(rep):
             "op_mix_pct": {k: round(100 * v / to, 1) for k, v in ops.most_common(25)}}
 
 
+def to_bytes(m, key):
+    return float(m[key]["value"]) * {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9}[m[key]["unit"]]
+
+
 summary = {}
-for rep in sorted(glob.glob("gpurun_out/prof_*.ncu-rep")):
-    name = os.path.basename(rep)[len("prof_"):-len(".ncu-rep")]
-    m = raw_metrics(rep)
-    s = source_mix(rep)
+captures = [(os.path.basename(r)[len("prof_"):-len(".ncu-rep")], r, None) for r in sorted(glob.glob("gpurun_out/prof_*.ncu-rep"))]
+# captures exported to csv on the GPU box (tools/prof_one.sh, tools/prof_envs.sh)
+captures += [(os.path.basename(r)[len("prof_"):-len(".raw.csv")], None, r) for r in sorted(glob.glob("gpurun_out/prof_*.raw.csv"))]
+for name, rep, rawcsv in captures:
+    if rep:
+        m = raw_metrics(rep)
+        s = source_mix(rep)
+    else:
+        m = raw_rows(list(csv.reader(open(rawcsv))))
+        src = rawcsv[:-len(".raw.csv")] + ".src.csv"
+        s = source_rows(list(csv.reader(open(src)))) if os.path.exists(src) else {}
+        if name.startswith("env_") and m:  # per-workload roll-out capture: record its traffic
+            tf = "profiles/traffic.json"
+            t = json.load(open(tf)) if os.path.exists(tf) else {}
+            wl = name[len("env_"):]
+            t[wl] = to_bytes(m[0], "dram__bytes_read.sum") + to_bytes(m[0], "dram__bytes_write.sum")
+            t[wl + "_source"] = f"profiles/{tag}/{name}_metrics.json (ncu --set full, one launch)"
+            json.dump(t, open(tf, "w"), indent=1)
     json.dump(m, open(os.path.join(out, f"{name}_metrics.json"), "w"), indent=1)
     json.dump(s, open(os.path.join(out, f"{name}_stalls.json"), "w"), indent=1)
     summary[name] = {"metrics": m, "stalls": s}
