@@ -59,6 +59,10 @@ struct Lane<CartPole> {
   __device__ static bool valid(int a) { return CartPole::valid(a); }
   // natural episodes last >= 8 steps (tests/test_oracle_envs.py::test_cartpole_min_episode_length)
   static constexpr int kMinEpisode = 8;
+  // two builds of the fused roll-out (section 5): latency (few warps: unconstrained registers for
+  // the deepest schedule) and throughput (many warps: register budget for occupancy)
+  static constexpr int kMaxThreads = 256;
+  static constexpr int kWinRowsLat = 32, kWinRowsThr = 32, kMinBlocksThr = 0;  // 0: no register cap hint
   __device__ static bool fast_ok(const St& s) { return CartPole::fast_ok(s); }
 };
 
@@ -92,6 +96,10 @@ struct Lane<Acrobot> {
   __device__ static void step(St& s, int a, float& r, bool& term) { Acrobot::step(s, a, r, term); }
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
   static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
+  // throughput build: an 8-row statistics window and <= 80 registers give 6 resident CTAs of
+  // 128 threads per SM (C3a 100K: one wave); latency build: 32 rows, unconstrained registers
+  static constexpr int kMaxThreads = 128;
+  static constexpr int kWinRowsLat = 32, kWinRowsThr = 8, kMinBlocksThr = 6;
   __device__ static bool fast_ok(const St&) { return true; }
 };
 
@@ -118,6 +126,8 @@ struct Lane<Dummy> {
   }
   __device__ static bool valid(int a) { return a == 0 || a == 1; }
   static constexpr int kMinEpisode = 1 << 30;  // episodes end by truncation only
+  static constexpr int kMaxThreads = 256;
+  static constexpr int kWinRowsLat = 32, kWinRowsThr = 32, kMinBlocksThr = 0;  // 0: no register cap hint
   __device__ static bool fast_ok(const St&) { return true; }
 };
 
@@ -229,15 +239,20 @@ __device__ __forceinline__ bool gauss_sample(const Key& key, uint32_t eg, uint32
 // =======================================================================================
 constexpr int kWinStride = 36;
 constexpr int kWinWords = 3 * 32 * kWinStride;  // per warp (13.5 KiB)
+#ifndef WS_CONT_WIN_ROWS
+#define WS_CONT_WIN_ROWS 16
+#endif
+constexpr int kContWinRows = WS_CONT_WIN_ROWS;  // window depth of k_rollout_continuous
 
 struct StatsWindow {
   uint32_t* len;
   float* ret;
   float* rew;
-  __device__ __forceinline__ void init(uint32_t* base) {
+  // rows: the window depth (32, or fewer where the shared-memory footprint limits occupancy)
+  __device__ __forceinline__ void init(uint32_t* base, int rows = 32) {
     len = base;
-    ret = reinterpret_cast<float*>(base + 32 * kWinStride);
-    rew = reinterpret_cast<float*>(base + 64 * kWinStride);
+    ret = reinterpret_cast<float*>(base + rows * kWinStride);
+    rew = reinterpret_cast<float*>(base + 2 * rows * kWinStride);
   }
   __device__ __forceinline__ void put(int row, int lane, uint32_t l, float rt, float rw) {
     len[row * kWinStride + lane] = l;
@@ -459,10 +474,11 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
 //    bookkeeping (kClean);
 //  - store addresses advance by one uniform slot stride per step.
 // =======================================================================================
-template <class Env>
+template <class Env, bool kLat>
 struct DiscreteRunner {
   using L = Lane<Env>;
   using St = typename L::St;
+  static constexpr int kRows = kLat ? L::kWinRowsLat : L::kWinRowsThr;  // window depth (power of 2, <= 32)
   // per-lane constants
   int lane, nlive, max_steps, T;
   uint32_t eg;
@@ -492,11 +508,11 @@ struct DiscreteRunner {
     stale = false;
   }
   __device__ __forceinline__ void flush_after(int c_last) {
-    if ((c_last & 31) == 31 || c_last == T - 1) {
-      const int w = c_last >> 5;
+    if ((c_last & (kRows - 1)) == kRows - 1 || c_last == T - 1) {
+      const int w = c_last / kRows;
       win.cta_acc = cta.acc(w);
-      win.flush(lane, 0, c_last & 31, c_last & ~31, p_stats, nlive);
-      cta.push(lane, w, 0, c_last & 31, c_last & ~31, p_stats);
+      win.flush(lane, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats, nlive);
+      cta.push(lane, w, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats);
     }
   }
 
@@ -541,7 +557,7 @@ struct DiscreteRunner {
       st_cs_u8(p_done + idx, (uint8_t)d);
     }
     // ---- A8 per-slot statistics contribution
-    if (!(WS_EXP & 2)) win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if (!(WS_EXP & 2)) win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
   }
 
   template <bool kFast, bool kClean>
@@ -595,10 +611,16 @@ struct DiscreteRunner {
   }
 };
 
-template <class Env>
-__global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const int T) {
+template <class Env, bool kLat>
+// latency build: minBlocks 1 lets ptxas spend registers on a deeper schedule (C2 measured:
+// 174 registers, 0.180 ms vs 100 registers, 0.200 ms); throughput build: the env's budget
+__global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::kMinBlocksThr)
+    k_rollout_discrete(const KArgs a, const int T) {
   using L = Lane<Env>;
-  DiscreteRunner<Env> R;
+  using Run = DiscreteRunner<Env, kLat>;
+  constexpr int kWin = 3 * Run::kRows * kWinStride;  // window words per warp
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  Run R;
   R.lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = a.E;
@@ -611,7 +633,7 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
   R.max_steps = a.max_steps;
   R.T = T;
   R.sE = (size_t)E;
-  R.win.init(warp_window());
+  R.win.init(ws_smem + (threadIdx.x >> 5) * kWin, Run::kRows);
   R.p_obs = a.obs + ec * L::D;
   R.p_rew = a.rew + ec;
   R.p_done = a.done + ec;
@@ -620,7 +642,7 @@ __global__ void __launch_bounds__(256) k_rollout_discrete(const KArgs a, const i
   {
     const int64_t cta_first = (int64_t)blockIdx.x * blockDim.x;
     const int64_t live_thr = min((int64_t)blockDim.x, ((E - cta_first + 31) / 32) * 32);
-    R.cta.buf = cta_stats_buf();
+    R.cta.buf = reinterpret_cast<unsigned long long*>(ws_smem + (blockDim.x >> 5) * kWin);
     R.cta.n_live_threads = (int)live_thr;
     R.cta.leader = (threadIdx.x >> 5) == 0;
     for (int i = threadIdx.x; i < 256; i += (int)live_thr) R.cta.buf[i] = 0ull;  // live threads only
@@ -735,8 +757,13 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
   const int64_t ec = live ? e : E - 1;
   const uint32_t eg = (uint32_t)(a.offset + ec);
   const Key key{a.k0, a.k1};
+  // 16-row statistics window (6.9 KiB per warp instead of 13.5): this throughput-bound kernel
+  // is otherwise limited to 16 resident warps per SM by shared memory (measured: 8 rows flush
+  // too often, 32 rows cost occupancy)
+  constexpr int kRows = kContWinRows;
+  extern __shared__ __align__(16) uint32_t ws_smem[];
   StatsWindow win;
-  win.init(warp_window());
+  win.init(ws_smem + (threadIdx.x >> 5) * (3 * kRows * kWinStride), kRows);
   const float* const p_act = reinterpret_cast<const float*>(a.act) + ec * DIM;
   const size_t sE = (size_t)E;
 
@@ -776,8 +803,9 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
     ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
     st_cs(a.rew + idx, rw);
     st_cs_u8(a.done + idx, (uint8_t)d);
-    win.put(c & 31, lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
-    if ((c & 31) == 31 || c == T - 1) win.flush(lane, 0, c & 31, c & ~31, a.stats, (int)min((int64_t)32, E - (e - lane)));
+    win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
+      win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, (int)min((int64_t)32, E - (e - lane)));
   }
   if (live) {
     L::save(a.state + e * L::S, s);
@@ -1605,6 +1633,10 @@ __global__ void k_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t
 
 static inline unsigned grid_for(int64_t n, int block) { return (unsigned)((n + block - 1) / block); }
 
+// up to about one warp per SM sub-partition the fused roll-out is latency-bound and uses its
+// latency build; beyond, the throughput build
+constexpr int64_t kLatencyReplicas = 148 * 4 * 32;
+
 static size_t tag_smem(const KArgs& a, int block) {
   return (size_t)(tag_tab_offset(a.p0, block / 32) + a.p0) * sizeof(int);
 }
@@ -1678,9 +1710,19 @@ static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   l.m(kKRollout, 0);
-  const cudaError_t e2 = launch_lane(k_rollout_discrete<Env>, a.E, l, a, T);
+  // results do not depend on the CTA size or the build (launch-shape invariance tests)
+  const int block = l.block < Lane<Env>::kMaxThreads ? l.block : Lane<Env>::kMaxThreads;
+  const bool lat = a.E <= kLatencyReplicas;
+  const int rows = lat ? Lane<Env>::kWinRowsLat : Lane<Env>::kWinRowsThr;
+  void (*k)(const KArgs, const int) = lat ? k_rollout_discrete<Env, true> : k_rollout_discrete<Env, false>;
+  const size_t smem = (size_t)(block / 32) * 3 * rows * kWinStride * sizeof(uint32_t) + 256 * sizeof(unsigned long long);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k<<<grid_for(a.E, block), block, smem, l.stream>>>(a, T);
   l.m(kKRollout, 1);
-  return e2;
+  return cudaGetLastError();
 }
 
 template <class Env>
@@ -1698,9 +1740,15 @@ static cudaError_t rollout_continuous(const KArgs& a, const Launch& l, int T, ui
   const cudaError_t err = cudaGetLastError();
   if (err != cudaSuccess) return err;
   l.m(kKRollout, 0);
-  const cudaError_t e2 = launch_lane(k_rollout_continuous<Env>, a.E, l, a, T);
+  const size_t smem = (size_t)(l.block / 32) * 3 * kContWinRows * kWinStride * sizeof(uint32_t);
+  if (smem > 48 * 1024) {
+    const cudaError_t e = cudaFuncSetAttribute(k_rollout_continuous<Env>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                               (int)smem);
+    if (e != cudaSuccess) return e;
+  }
+  k_rollout_continuous<Env><<<grid_for(a.E, l.block), l.block, smem, l.stream>>>(a, T);
   l.m(kKRollout, 1);
-  return e2;
+  return cudaGetLastError();
 }
 
 template <int D>

@@ -292,6 +292,16 @@ def test_full_size_configs_sampled(P, cfg, windows):
         compare(sub, o, amb, w.env, w.T)
 
 
+@pytest.mark.parametrize("env,n", [("cartpole", 2), ("acrobot", 3), ("dummy", 2)])
+def test_throughput_build_parity(P, env, n):
+    """Above 148*4*32 replicas the fused discrete roll-out switches to its throughput build
+    (other register budget and statistics window depth): full element-wise parity there too."""
+    E, T = 20_000, 72
+    probs = W.random_probs(E, 1, n, seed=31, zero_frac=0.1)
+    g, o, buf, amb = run_pair(P, env, E, T, probs=probs)
+    compare(buf, o, amb, env, T)
+
+
 # ------------------------------------------------------------------------------ invariants
 def test_launch_shape_and_sharding_invariance(P):
     """S:148 / S:178 analog: per-replica outputs identical for every CTA size and for any
