@@ -100,6 +100,7 @@ struct ws_env {
     int n = 0, open = 0;
   };
   bool timing = false;
+  uint32_t timed_mask = 0;  // kernels (bit = KernelId) that get events
   Ring rings[ws::kKCount];
 };
 
@@ -173,6 +174,7 @@ constexpr int kTimingCap = 256;
 
 void mark_kernel(void* ctx, int kernel, int phase) {
   ws_env* h = static_cast<ws_env*>(ctx);
+  if (!((h->timed_mask >> kernel) & 1u)) return;
   ws_env::Ring& r = h->rings[kernel];
   const int i = r.n % kTimingCap;
   if (phase == 0) {
@@ -595,6 +597,7 @@ ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
   }
   for (auto& r : h->rings) r.n = 0;
   h->timing = enable != 0;
+  h->timed_mask = enable == 2 ? (1u << ws::kKRollout) : 0xFFFFFFFFu;
   return WS_OK;
 }
 

@@ -177,8 +177,11 @@ class Env:
         check(lib().ws_read_stats(self._h, t0, info.cursor if t1 is None else t1, C.byref(out)), self._h)
         return out
 
-    def enable_kernel_timing(self, enable: bool = True):
-        check(lib().ws_enable_kernel_timing(self._h, 1 if enable else 0), self._h)
+    def enable_kernel_timing(self, enable=True):
+        """True / 1: events around every kernel; 2: around the fused roll-out kernel only;
+        False / 0: off (ws.h ws_enable_kernel_timing)."""
+        mode = 0 if enable is False else (1 if enable is True else int(enable))
+        check(lib().ws_enable_kernel_timing(self._h, mode), self._h)
 
     def kernel_times(self) -> dict:
         """{kernel class: (launches, mean_ms)} since the last call (ws_kernel_times)."""
