@@ -55,6 +55,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: no clocks / cpu baseline / e2e")
     ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (gloo only for tests)")
+    ap.add_argument("--stats-reduce", default="p2p", choices=["p2p", "nccl"],
+                    help="N > 1: statistics all-reduce by libws's peer-memory kernel (default) or NCCL")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="diagnostic: no per-kernel CUDA events in the timed region (roofline unavailable)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (multi-rank test on one GPU)")
@@ -214,10 +216,18 @@ def main():
     probs_host = W.workload_probs(w)
     probs = torch.from_numpy(probs_host).to(dev)
     stats_view = env.buffers()["stats"][:T]
+    p2p = False
+    if world > 1 and args.stats_reduce == "p2p":
+        from paper_2408_00930_b200.parallel import attach_peer_stats
+        p2p = attach_peer_stats(env)  # falls back to NCCL if CUDA IPC is unavailable on any rank
+
+    def merge_stats():
+        if not p2p:
+            allreduce_stats(stats_view)
 
     def one_step():
         env.rollout(T, probs)
-        allreduce_stats(stats_view)
+        merge_stats()
 
     for _ in range(max(args.warmup, 0)):
         one_step()
@@ -241,12 +251,15 @@ def main():
     ev[0].record(stream)
     for k in range(args.steps):
         env.rollout(T, probs)
-        allreduce_stats(stats_view)
+        merge_stats()
     ev[1].record(stream)
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
     total_ms = ev[0].elapsed_time(ev[1])
+    st = env.status()  # sticky device errors (invalid rows, peer reduction timeout) fail the run
+    if st != 0:
+        raise RuntimeError(f"libws reported status {st} during the timed region")
     launches = env.info().launches - launches0
     ktimes = env.kernel_times()
     env.enable_kernel_timing(False)
@@ -334,7 +347,8 @@ def main():
             "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs_per_gpu": E, "n_envs_global": E_g,
                        "n_agents": A, "T": T, "probs": "uniform, resident in HBM, step_stride 0",
-                       "parallelism": f"env-shard x{world} + NCCL stats all-reduce" if world > 1 else "1 GPU",
+                       "parallelism": (f"env-shard x{world} + " + ("peer-memory (CUDA IPC, NVLink) stats all-reduce kernel"
+                                                                    if p2p else "NCCL stats all-reduce")) if world > 1 else "1 GPU",
                        "l2": f"store {all_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
             "roofline": roofline, "gpu_launches": int(launches),
             "episode_stats_last_step": merged,

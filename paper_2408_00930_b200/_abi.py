@@ -12,10 +12,11 @@ LIB_PATH = os.environ.get("WS_LIBWS") or os.path.join(HERE, "lib", "libws.so")  
 HEADER = os.path.join(os.path.dirname(HERE), "include", "ws.h")
 
 # ws_status
-OK, INVALID_ARGUMENT, UNKNOWN_ENV, INVALID_ACTION, INVALID_PROBS, OUT_OF_RANGE, BAD_STATE, OUT_OF_MEMORY, CUDA_ERROR = range(9)
+(OK, INVALID_ARGUMENT, UNKNOWN_ENV, INVALID_ACTION, INVALID_PROBS, OUT_OF_RANGE, BAD_STATE, OUT_OF_MEMORY, CUDA_ERROR,
+ PEER_ERROR) = range(10)
 STATUS_NAMES = {0: "WS_OK", 1: "WS_ERR_INVALID_ARGUMENT", 2: "WS_ERR_UNKNOWN_ENV", 3: "WS_ERR_INVALID_ACTION",
                 4: "WS_ERR_INVALID_PROBS", 5: "WS_ERR_OUT_OF_RANGE", 6: "WS_ERR_BAD_STATE",
-                7: "WS_ERR_OUT_OF_MEMORY", 8: "WS_ERR_CUDA"}
+                7: "WS_ERR_OUT_OF_MEMORY", 8: "WS_ERR_CUDA", 9: "WS_ERR_PEER"}
 # ws_dtype
 F32, I32, U8, F64, U32, I64 = range(6)
 FX_SCALE = 2.0 ** -32  # fixed-point scale of stats[:, 1] and stats[:, 3]
@@ -33,6 +34,10 @@ class ws_config(C.Structure):
         ("param0", C.c_int32), ("param1", C.c_int32), ("block_size", C.c_int32),
         ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
     ]
+
+
+class ws_ipc_handle(C.Structure):
+    _fields_ = [("bytes", C.c_ubyte * 64)]
 
 
 class ws_tensor(C.Structure):
@@ -84,6 +89,9 @@ _SIGS = {
     "ws_last_error": (C.c_char_p, [C.c_void_p]),
     "ws_abi_version": (C.c_int32, []),
     "ws_enable_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ws_peer_export": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),
+    "ws_peer_attach": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ws_ipc_handle)]),
+    "ws_peer_detach": (C.c_int, [C.c_void_p]),
     "ws_kernel_times": (C.c_int, [C.c_void_p, C.POINTER(ws_kernel_time), C.c_int32, C.POINTER(C.c_int32)]),
     "ws_test_philox": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ws_test_sample_grid": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),

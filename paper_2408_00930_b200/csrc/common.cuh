@@ -161,7 +161,7 @@ __device__ __forceinline__ void st_cs_u8(uint8_t* p, uint8_t v) {
 }
 
 // Device error word bits (sticky until ws_reset, R19).
-constexpr uint32_t kErrAction = 1u, kErrProbs = 2u;
+constexpr uint32_t kErrAction = 1u, kErrProbs = 2u, kErrPeer = 4u;
 
 __device__ __forceinline__ float warp_sum_f32(float v) {
   // xor butterfly; lane 0's value is the deterministic result used by the caller

@@ -1850,6 +1850,76 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
   return err;
 }
 
+// ---------------------------------------------------------------------------------------
+// A8 cross-GPU statistics all-reduce over peer memory (one CTA per rank, after the roll-out
+// on the same stream).  Buffer of rank r: gather_r[parity][src][t_cap][4] int64, then one
+// u64 arrival counter.  Epoch k uses parity k & 1: a rank can be at most one epoch ahead of
+// a peer's reader (it must first see that peer's arrival for epoch k-1), so two parities
+// suffice.  Sums are exact int64 (R20): the result is identical on every rank and equal to
+// the single-GPU statistics of the union of the shards.
+// ---------------------------------------------------------------------------------------
+__device__ __forceinline__ unsigned long long ld_acquire_sys(const unsigned long long* p) {
+  unsigned long long v;
+  asm volatile("ld.acquire.sys.global.u64 %0, [%1];" : "=l"(v) : "l"(p) : "memory");
+  return v;
+}
+__device__ __forceinline__ uint64_t global_ns() {
+  uint64_t t;
+  asm volatile("mov.u64 %0, %%globaltimer;" : "=l"(t));
+  return t;
+}
+
+__global__ void __launch_bounds__(256) k_peer_allreduce(const unsigned long long* local, const int T,
+                                                       const PeerArgs p, const uint64_t epoch,
+                                                       unsigned long long* out, uint32_t* err,
+                                                       const uint64_t timeout_ns) {
+  const int n = T * 4;
+  const size_t slice = (size_t)p.t_cap * 4;
+  const size_t par = (size_t)(epoch & 1) * (size_t)p.world * slice;
+  const size_t counter = 2 * (size_t)p.world * slice;  // arrival counter after both parities
+  // 1. publish this rank's slice to every rank (16-byte stores; slices are 32-byte aligned)
+  for (int r = 0; r < p.world; ++r) {
+    ulonglong2* dst = reinterpret_cast<ulonglong2*>(p.gather[r] + par + (size_t)p.rank * slice);
+    const ulonglong2* src = reinterpret_cast<const ulonglong2*>(local);
+    for (int i = threadIdx.x; i < n / 2; i += blockDim.x) dst[i] = src[i];
+  }
+  __threadfence_system();
+  __syncthreads();
+  // 2. signal every rank (release: the barrier orders all threads' fenced stores before it)
+  if ((int)threadIdx.x < p.world) atomicAdd_system(p.gather[threadIdx.x] + counter, 1ull);
+  // 3. wait until every rank has published epoch `epoch` into this rank's buffer
+  __shared__ int timed_out;
+  if (threadIdx.x == 0) {
+    timed_out = 0;
+    const unsigned long long target = (unsigned long long)p.world * (epoch + 1);
+    const unsigned long long* c = p.gather[p.rank] + counter;
+    const uint64_t t0 = global_ns();
+    while (ld_acquire_sys(c) < target) {
+      if (global_ns() - t0 > timeout_ns) {
+        timed_out = 1;
+        atomicOr(err, kErrPeer);
+        break;
+      }
+      __nanosleep(256);
+    }
+  }
+  __syncthreads();
+  if (timed_out) return;
+  // 4. merged statistics = sum of the slices (exact integers; rank order for definiteness)
+  const unsigned long long* g = p.gather[p.rank] + par;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    unsigned long long acc = 0;
+    for (int r = 0; r < p.world; ++r) acc += g[(size_t)r * slice + i];
+    out[i] = acc;
+  }
+}
+
+cudaError_t launch_peer_allreduce(const unsigned long long* local, int T, const PeerArgs& p, uint64_t epoch,
+                                  unsigned long long* out, uint32_t* err, double timeout_s, cudaStream_t s) {
+  k_peer_allreduce<<<1, 256, 0, s>>>(local, T, p, epoch, out, err, (uint64_t)(timeout_s * 1e9));
+  return cudaGetLastError();
+}
+
 cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s) {
   k_test_philox<<<grid_for(n, 256), 256, 0, s>>>(rows, n, out);
   return cudaGetLastError();

@@ -64,4 +64,15 @@ cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float*
 cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
                                    cudaStream_t s);
 
+// A8 across GPUs without NCCL (section 8e "v2"): every rank publishes its [T,4] statistics
+// into every peer's gather buffer through CUDA-IPC-mapped peer memory (NVLink / NVSwitch),
+// signals the peers' arrival counters, waits for all ranks and sums the slices.
+constexpr int kMaxPeers = 8;
+struct PeerArgs {
+  unsigned long long* gather[kMaxPeers];  // each rank's buffer [2][world][t_cap][4] + counter
+  int rank, world, t_cap;
+};
+cudaError_t launch_peer_allreduce(const unsigned long long* local, int T, const PeerArgs& p, uint64_t epoch,
+                                  unsigned long long* out, uint32_t* err, double timeout_s, cudaStream_t s);
+
 }  // namespace ws

@@ -101,6 +101,13 @@ struct ws_env {
   };
   bool timing = false;
   uint32_t timed_mask = 0;  // kernels (bit = KernelId) that get events
+  // cross-GPU statistics reduction over peer memory (ws_peer_export / ws_peer_attach)
+  unsigned long long* peer_own = nullptr;  // this rank's gather buffer (cudaMalloc, IPC-exported)
+  int32_t peer_world = 0, peer_rank = -1, peer_tcap = 0;
+  bool peer_attached = false;
+  void* peer_open[ws::kMaxPeers] = {};     // peers' buffers opened through CUDA IPC
+  uint64_t peer_epoch = 0;
+  double peer_timeout_s = 30.0;
   Ring rings[ws::kKCount];
 };
 
@@ -139,6 +146,19 @@ void free_all(ws_env* h) {
     else cudaFree(pr.first);
   }
   h->allocs.clear();
+}
+
+void peer_release(ws_env* h) {
+  for (int r = 0; r < ws::kMaxPeers; ++r)
+    if (h->peer_open[r]) {
+      cudaIpcCloseMemHandle(h->peer_open[r]);
+      h->peer_open[r] = nullptr;
+    }
+  if (h->peer_own) cudaFree(h->peer_own);
+  h->peer_own = nullptr;
+  h->peer_attached = false;
+  h->peer_world = 0;
+  h->peer_rank = -1;
 }
 
 ws::KArgs kargs(const ws_env* h) {
@@ -349,6 +369,7 @@ ws_status ws_destroy(ws_env* h) {
     for (auto ev : r.b) cudaEventDestroy(ev);
     for (auto ev : r.e) cudaEventDestroy(ev);
   }
+  peer_release(h);
   free_all(h);
   delete h;
   return WS_OK;
@@ -415,6 +436,18 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
   cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
   if (!e) e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
   if (e) return cuda_fail(h, e, "rollout kernel");
+  if (h->peer_attached) {  // A8 across GPUs: merged statistics in place, no NCCL call
+    ws::PeerArgs pa{};
+    for (int r = 0; r < h->peer_world; ++r)
+      pa.gather[r] = r == h->peer_rank ? h->peer_own : static_cast<unsigned long long*>(h->peer_open[r]);
+    pa.rank = h->peer_rank;
+    pa.world = h->peer_world;
+    pa.t_cap = h->peer_tcap;
+    e = ws::launch_peer_allreduce(h->stats, T, pa, h->peer_epoch, h->stats, h->err, h->peer_timeout_s, h->stream);
+    if (e) return cuda_fail(h, e, "peer statistics reduction");
+    h->peer_epoch += 1;
+    h->launches += 1;
+  }
   h->t += (uint64_t)T;
   h->cursor = T;
   h->sampled_slot = -1;
@@ -522,6 +555,7 @@ ws_status ws_synchronize(ws_env* h) {
   if (e) return cuda_fail(h, e, "ws_synchronize");
   uint32_t word = 0;
   if ((e = cudaMemcpy(&word, h->err, sizeof(word), cudaMemcpyDeviceToHost))) return cuda_fail(h, e, "read error word");
+  if (word & ws::kErrPeer) return fail(h, WS_ERR_PEER, "cross-GPU statistics reduction timed out waiting for a peer");
   if (word & ws::kErrProbs) return fail(h, WS_ERR_INVALID_PROBS, "a probability row was invalid (sticky until ws_reset)");
   if (word & ws::kErrAction) return fail(h, WS_ERR_INVALID_ACTION, "an action was invalid (sticky until ws_reset)");
   return WS_OK;
@@ -580,6 +614,58 @@ ws_status ws_test_exhaustive(int32_t fn_a, int32_t fn_b, float param, uint32_t l
 }
 
 static const char* kKernelNames[ws::kKCount] = {"plan", "rollout", "sample", "step", "reset"};
+
+ws_status ws_peer_export(ws_env* h, int32_t world, ws_ipc_handle* out) {
+  if (check(h) || !out || world < 1 || world > ws::kMaxPeers)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_peer_export: world must be in [1, 8]");
+  if (h->T_cap < 1) return fail(h, WS_ERR_BAD_STATE, "ws_peer_export needs the store (t_capacity or a first ws_rollout)");
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  peer_release(h);
+  const size_t words = 2 * (size_t)world * (size_t)h->T_cap * 4 + 4;  // + arrival counter (32-byte pad)
+  cudaError_t e = cudaMalloc(reinterpret_cast<void**>(&h->peer_own), words * sizeof(unsigned long long));
+  if (!e) e = cudaMemset(h->peer_own, 0, words * sizeof(unsigned long long));
+  cudaIpcMemHandle_t ih;
+  if (!e) e = cudaIpcGetMemHandle(&ih, h->peer_own);
+  if (e) {
+    peer_release(h);
+    return cuda_fail(h, e, "ws_peer_export");
+  }
+  static_assert(sizeof(cudaIpcMemHandle_t) <= sizeof(ws_ipc_handle), "IPC handle size");
+  std::memset(out, 0, sizeof(*out));
+  std::memcpy(out->bytes, &ih, sizeof(ih));
+  h->peer_world = world;
+  h->peer_tcap = h->T_cap;
+  return WS_OK;
+}
+
+ws_status ws_peer_attach(ws_env* h, int32_t rank, int32_t world, const ws_ipc_handle* handles) {
+  if (check(h) || !handles || world != h->peer_world || rank < 0 || rank >= world || !h->peer_own)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_peer_attach: call ws_peer_export(world) first; 0 <= rank < world");
+  DeviceGuard g(h->device);
+  for (int r = 0; r < world; ++r) {
+    if (r == rank) continue;
+    cudaIpcMemHandle_t ih;
+    std::memcpy(&ih, handles[r].bytes, sizeof(ih));
+    const cudaError_t e = cudaIpcOpenMemHandle(&h->peer_open[r], ih, cudaIpcMemLazyEnablePeerAccess);
+    if (e) {
+      peer_release(h);
+      return cuda_fail(h, e, "ws_peer_attach: cudaIpcOpenMemHandle");
+    }
+  }
+  h->peer_rank = rank;
+  h->peer_epoch = 0;
+  h->peer_attached = world > 1;
+  return WS_OK;
+}
+
+ws_status ws_peer_detach(ws_env* h) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaStreamSynchronize(h->stream);
+  peer_release(h);
+  return WS_OK;
+}
 
 ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;

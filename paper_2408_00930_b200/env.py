@@ -183,6 +183,25 @@ class Env:
         mode = 0 if enable is False else (1 if enable is True else int(enable))
         check(lib().ws_enable_kernel_timing(self._h, mode), self._h)
 
+    # ---- cross-GPU statistics over peer memory (ws.h "multi-GPU statistics")
+    def peer_export(self, world: int) -> bytes:
+        """Allocate this rank's IPC-exportable gather buffer; returns its 64-byte handle."""
+        hd = _abi.ws_ipc_handle()
+        check(lib().ws_peer_export(self._h, world, C.byref(hd)), self._h)
+        return bytes(hd.bytes)
+
+    def peer_attach(self, rank: int, handles) -> None:
+        """Open every other rank's buffer; each later rollout() merges the statistics."""
+        arr = (_abi.ws_ipc_handle * len(handles))()
+        for i, b in enumerate(handles):
+            C.memmove(arr[i].bytes, b, 64)
+        check(lib().ws_peer_attach(self._h, rank, len(handles), arr), self._h)
+        self.peers_attached = len(handles) > 1
+
+    def peer_detach(self) -> None:
+        check(lib().ws_peer_detach(self._h), self._h)
+        self.peers_attached = False
+
     def kernel_times(self) -> dict:
         """{kernel class: (launches, mean_ms)} since the last call (ws_kernel_times)."""
         arr = (_abi.ws_kernel_time * 8)()

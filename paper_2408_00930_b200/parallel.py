@@ -27,10 +27,45 @@ def shard(n_envs_global: int, world: int, rank: int) -> tuple[int, int]:
 def allreduce_stats(stats: torch.Tensor, group: Optional[dist.ProcessGroup] = None) -> torch.Tensor:
     """In-place SUM all-reduce of a [T, 4] statistics view across ranks (NCCL on the GPU
     path; gloo in the CPU tests).  libws's slab is exact fixed-point int64 (DESIGN R20), so
-    the merged statistics are bit-identical for any number of ranks."""
+    the merged statistics are bit-identical for any number of ranks.  (Handles attached with
+    attach_peer_stats already merge inside ws_rollout; their callers skip this.)"""
     if dist.is_available() and dist.is_initialized() and dist.get_world_size(group) > 1:
         dist.all_reduce(stats, op=dist.ReduceOp.SUM, group=group)
     return stats
+
+
+def attach_peer_stats(env, group: Optional[dist.ProcessGroup] = None) -> bool:
+    """Collective: switch `env` to the NCCL-free statistics all-reduce over CUDA-IPC peer
+    memory (libws ws_peer_export / ws_peer_attach): from now on every env.rollout() leaves
+    the merged [T,4] statistics of all ranks in its stats slab.  Returns False (and leaves
+    the NCCL path in place) when IPC is unavailable on any rank."""
+    if not (dist.is_available() and dist.is_initialized()):
+        return False
+    world, rank = dist.get_world_size(group), dist.get_rank(group)
+    if world < 2:
+        return False
+    try:
+        h = env.peer_export(world)
+        err = None
+    except Exception as ex:  # noqa: BLE001 -- reported collectively below
+        h, err = b"", repr(ex)
+    handles = [None] * world
+    dist.all_gather_object(handles, (h, err), group=group)
+    if any(e for _, e in handles):
+        return False
+    ok = True
+    try:
+        env.peer_attach(rank, [hh for hh, _ in handles])
+    except Exception:  # noqa: BLE001
+        ok = False
+    flags = [None] * world
+    dist.all_gather_object(flags, ok, group=group)
+    if not all(flags):
+        if ok:
+            env.peer_detach()
+        return False
+    dist.barrier(group)
+    return True
 
 
 def summarize(stats: torch.Tensor) -> dict:
