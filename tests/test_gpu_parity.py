@@ -302,6 +302,46 @@ def test_throughput_build_parity(P, env, n):
     compare(buf, o, amb, env, T)
 
 
+@pytest.mark.parametrize("env,n", [("cartpole", 2), ("acrobot", 3), ("dummy", 2)])
+@pytest.mark.parametrize("max_steps", [1, 3, 7, 8, 9])
+def test_short_truncation_limits(P, env, n, max_steps):
+    """Truncation every few steps (R10): below 8 the fused CartPole loop leaves its 8-step
+    refill window (fast path) for the per-step reset check; done bits, reset counters and
+    statistics as the oracle."""
+    E, T = 70, 45
+    probs = W.random_probs(E, 1, n, seed=51, zero_frac=0.1)
+    g, o, buf, amb = run_pair(P, env, E, T, probs=probs, max_steps=max_steps)
+    compare(buf, o, amb, env, T)
+
+
+@pytest.mark.parametrize("E,T", [(1, 1), (1, 37), (33, 1), (33, 9), (31, 64)])
+def test_tiny_shapes(P, E, T):
+    """Degenerate sizes: one replica, one step, a warp plus one replica, a partial warp."""
+    probs = W.random_probs(E, 1, 2, seed=52, zero_frac=0.1)
+    g, o, buf, amb = run_pair(P, "cartpole", E, T, probs=probs)
+    compare(buf, o, amb, "cartpole", T)
+
+
+def test_write_logp_off(P):
+    """write_logp = 0: the log-prob slab is never written; everything else is unchanged."""
+    E, T = 200, 50
+    probs = W.random_probs(E, 1, 2, seed=53, zero_frac=0.1)
+    g = P.Env(E, 1, "cartpole", SEED, t_capacity=T, write_logp=False)
+    lp = g.buffers()["logp"]
+    if lp is not None:
+        lp.fill_(7.0)
+    g.rollout(T, torch.from_numpy(probs).cuda())
+    assert g.status() == 0
+    o = O.Batch("cartpole", E, 1, SEED, t_capacity=T)
+    assert o.rollout(T, probs) == 0
+    buf = {k: (v.cpu().numpy() if v is not None else None) for k, v in g.buffers().items()}
+    for k in ("act", "obs", "rew", "done", "reset_count", "ep_step"):
+        assert np.array_equal(buf[k][:T] if buf[k].ndim > 1 else buf[k], np.array(o.array(k))[:T]
+                              if np.array(o.array(k)).ndim > 1 else np.array(o.array(k))), k
+    if buf["logp"] is not None:
+        assert (buf["logp"] == 7.0).all()
+
+
 # ------------------------------------------------------------------------------ invariants
 def test_launch_shape_and_sharding_invariance(P):
     """S:148 / S:178 analog: per-replica outputs identical for every CTA size and for any
