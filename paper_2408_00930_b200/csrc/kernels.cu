@@ -56,6 +56,13 @@ struct Lane<CartPole> {
   }
   template <bool kFast>
   __device__ static void step(St& s, int a, float& r, bool& term) { CartPole::step<kFast>(s, a, r, term); }
+  // per-state cached data carried by the fused loop (none for CartPole)
+  struct Aux {};
+  __device__ static Aux aux_of(const St&) { return Aux{}; }
+  template <bool kFast>
+  __device__ static void step_aux(St& s, Aux&, int a, float& r, bool& term) { step<kFast>(s, a, r, term); }
+  __device__ static void obs_store_aux(float* dst, const St& s, const Aux&, bool cs) { obs_store(dst, s, cs); }
+  __device__ static Aux select(bool p, const Aux& x, const Aux&) { return x; }
   __device__ static bool valid(int a) { return CartPole::valid(a); }
   // natural episodes last >= 8 steps (tests/test_oracle_envs.py::test_cartpole_min_episode_length)
   static constexpr int kMinEpisode = 8;
@@ -94,6 +101,22 @@ struct Lane<Acrobot> {
   }
   template <bool kFast>
   __device__ static void step(St& s, int a, float& r, bool& term) { Acrobot::step(s, a, r, term); }
+  // the fused loop carries each state's trigonometry: it serves the pre-step observation,
+  // the first RK4 stage and (computed for the new state) the terminal test -- 12 instead of
+  // 16 fp64 sincos evaluations per step
+  using Aux = Acrobot::Trig;
+  __device__ static Aux aux_of(const St& s) { return Acrobot::trig_of(s); }
+  template <bool kFast>
+  __device__ static void step_aux(St& s, Aux& tr, int a, float& r, bool& term) { Acrobot::step_trig(s, tr, a, r, term); }
+  __device__ static void obs_store_aux(float* dst, const St& s, const Aux& t, bool cs) {
+    const float2 a = make_float2(t.c1, t.s1), b = make_float2(t.c2, t.s2), c = make_float2(s.w1, s.w2);
+    float2* d = reinterpret_cast<float2*>(dst);
+    if (cs) { st_cs(d, a); st_cs(d + 1, b); st_cs(d + 2, c); }
+    else { d[0] = a; d[1] = b; d[2] = c; }
+  }
+  __device__ static Aux select(bool p, const Aux& x, const Aux& y) {
+    return Aux{p ? x.s1 : y.s1, p ? x.c1 : y.c1, p ? x.s2 : y.s2, p ? x.c2 : y.c2, p ? x.s12 : y.s12, p ? x.c12 : y.c12};
+  }
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
   static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
   // throughput build: an 8-row statistics window and <= 80 registers give 6 resident CTAs of
@@ -124,6 +147,12 @@ struct Lane<Dummy> {
     r = 1.0f;
     term = false;
   }
+  struct Aux {};
+  __device__ static Aux aux_of(const St&) { return Aux{}; }
+  template <bool kFast>
+  __device__ static void step_aux(St& s, Aux&, int a, float& r, bool& term) { step<kFast>(s, a, r, term); }
+  __device__ static void obs_store_aux(float* dst, const St& s, const Aux&, bool cs) { obs_store(dst, s, cs); }
+  __device__ static Aux select(bool p, const Aux& x, const Aux&) { return x; }
   __device__ static bool valid(int a) { return a == 0 || a == 1; }
   static constexpr int kMinEpisode = 1 << 30;  // episodes end by truncation only
   static constexpr int kMaxThreads = 256;
@@ -493,6 +522,7 @@ struct DiscreteRunner {
   StatsWindow win;
   // replica state (registers)
   St s, nxt;
+  typename L::Aux aux, aux_nxt;  // per-state cached data (Acrobot: trigonometry)
   int32_t ep_step;
   uint32_t rc;
   float ep_ret;
@@ -505,6 +535,7 @@ struct DiscreteRunner {
   }
   __device__ __forceinline__ void refill() {
     if (!(WS_EXP & 8)) L::init(key, eg, rc + 1, nxt);
+    aux_nxt = L::aux_of(nxt);
     stale = false;
   }
   __device__ __forceinline__ void flush_after(int c_last) {
@@ -521,12 +552,13 @@ struct DiscreteRunner {
   __device__ __forceinline__ void step(const int c, const size_t idx, const int act_in) {
     const bool bad = kClean ? false : act_in < 0;  // invalid probability row (plan byte 0xFF)
     // ---- A6 log the pre-step observation (R12)
-    if (!(WS_EXP & 4)) L::obs_store(p_obs + idx * L::D, s, true);
+    if (!(WS_EXP & 4)) L::obs_store_aux(p_obs + idx * L::D, s, aux, true);
     // ---- A3 / A4 dynamics, reward, done
     St s2 = s;
+    typename L::Aux aux2 = aux;
     float r;
     bool term;
-    L::template step<kFast || (WS_EXP & 1)>(s2, kClean ? act_in : (bad ? 0 : act_in), r, term);
+    L::template step_aux<kFast || (WS_EXP & 1)>(s2, aux2, kClean ? act_in : (bad ? 0 : act_in), r, term);
     const int32_t es = ep_step + 1;
     uint32_t d = (term ? 1u : 0u) | (es >= max_steps ? 2u : 0u);
     float rw = r;
@@ -538,14 +570,19 @@ struct DiscreteRunner {
     // ---- A5 auto-reset from the look-ahead state init(e, rc + 1)
     if (!kFast) {
       if (__any_sync(kFull, d != 0 && stale)) {  // second reset within one refill window
-        if (d != 0 && stale) L::init(key, eg, rc + 1, nxt);
+        if (d != 0 && stale) {
+          L::init(key, eg, rc + 1, nxt);
+          aux_nxt = L::aux_of(nxt);
+        }
       }
     }
     if (kClean) {
       s = d ? nxt : s2;
+      aux = L::select(d != 0, aux_nxt, aux2);
       ep_step = d ? 0 : es;
       ep_ret = d ? 0.0f : ret;
     } else {
+      aux = L::select(d != 0, aux_nxt, L::select(bad, aux, aux2));
       s = d ? nxt : (bad ? s : s2);
       ep_step = d ? 0 : (bad ? ep_step : es);
       ep_ret = d ? 0.0f : (bad ? ep_ret : ret);
@@ -653,6 +690,8 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
   R.rc = a.reset_count[ec];
   R.ep_ret = a.ep_ret[ec];
   L::init(R.key, R.eg, R.rc + 1, R.nxt);
+  R.aux = L::aux_of(R.s);
+  R.aux_nxt = L::aux_of(R.nxt);
   R.stale = false;
 
   const bool fast = L::kMinEpisode >= 8 && R.max_steps >= 8 && __all_sync(kFull, L::fast_ok(R.s));
