@@ -825,11 +825,23 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
       for (int k = 0; k < DIM; ++k) nxt[k] = __ldcg(p_act + (size_t)(c + 1) * sE * DIM + k);
     }
     const size_t idx = (size_t)c * sE + (size_t)ec;
-    L::obs_store(a.obs + idx * L::D, s, true);  // tail lanes store replica E-1's identical values
     St s2 = s;
     float r = 0.0f;
     bool term = false;
-    const bool ok = L::step_c(s2, act, r, term);
+    bool ok;
+    if constexpr (std::is_same<Env, Pendulum>::value) {  // one sincos serves the observation and the step
+      float sn, cs;
+      sincos_c(s.th, sn, cs);
+      float* dst = a.obs + idx * L::D;  // (cos th, sin th, thdot); tail lanes store replica E-1's values
+      st_cs(dst, cs);
+      st_cs(dst + 1, sn);
+      st_cs(dst + 2, s.thd);
+      ok = isfinite(act[0]);
+      if (ok) Pendulum::step_sin(s2, act[0], sn, r);
+    } else {
+      L::obs_store(a.obs + idx * L::D, s, true);  // tail lanes store replica E-1's identical values
+      ok = L::step_c(s2, act, r, term);
+    }
     if (live && !ok) err |= kErrAction;
     const int32_t es = ep_step + 1;
     const uint32_t d = ok ? ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u)) : 0u;
