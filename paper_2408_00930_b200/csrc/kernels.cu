@@ -1361,9 +1361,9 @@ enum TagMode : int { kTagRollout = 0, kTagStepSlab = 1, kTagStepGiven = 2 };
 constexpr int kTagN = 5;
 
 // Shared memory of k_tag: occupancy grids taggers_on / tagged_on [G*G] ints, the reduction
-// buffer (2 int64 per warp) and the observation table x / (G - 1) for x in [0, G).
+// buffer (3 int64 per warp) and the observation table x / (G - 1) for x in [0, G).
 __host__ __device__ inline int tag_red_offset(int G) { return 2 * G * G + ((2 * G * G) & 1); }  // in ints
-__host__ __device__ inline int tag_tab_offset(int G, int nwarps) { return tag_red_offset(G) + 4 * nwarps; }
+__host__ __device__ inline int tag_tab_offset(int G, int nwarps) { return tag_red_offset(G) + 6 * nwarps; }
 
 // kHoisted: roll-out with per-step-constant probabilities (thresholds hoisted, no per-step
 // CDF code in the kernel); otherwise the general kernel (per-step rows, ws_step modes).
@@ -1464,79 +1464,69 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
     float r = 0.0f;
     uint8_t d = 0;
     if (!any_invalid) {
-      // simultaneous moves, clipped to the grid; tagged runners frozen
-      if (is_agent && (tagger || active)) {
-        int nx = x, ny = y;
-        if (act == 1) ny = y + 1;
-        else if (act == 2) ny = y - 1;
-        else if (act == 3) nx = x + 1;
-        else if (act == 4) nx = x - 1;
-        x = min(max(nx, 0), G - 1);
-        y = min(max(ny, 0), G - 1);
-      }
+      // simultaneous moves, clipped to the grid; tagged runners frozen;
+      // branch-free: N (y+1), S (y-1), E (x+1), W (x-1), stay
+      const bool mv = is_agent && (tagger || active);
+      const int dxv = (act == 3 ? 1 : 0) - (act == 4 ? 1 : 0), dyv = (act == 1 ? 1 : 0) - (act == 2 ? 1 : 0);
+      x = mv ? min(max(x + dxv, 0), G - 1) : x;
+      y = mv ? min(max(y + dyv, 0), G - 1) : y;
       const int cell = y * G + x;
       if (is_agent && tagger) atomicAdd(&taggers_on[cell], 1);
       __syncthreads();
       bool newly = false;
-      if (is_agent && !tagger) {
-        if (active) {
-          if (taggers_on[cell] >= 1) {
-            r = -1.0f;
-            active = 0;
-            newly = true;
-            atomicAdd(&tagged_on[cell], 1);
-          } else {
-            r = 0.01f;
-          }
-        }
+      if (is_agent && !tagger && active) {
+        newly = taggers_on[cell] >= 1;
+        r = newly ? -1.0f : 0.01f;
+        active = newly ? 0 : active;
+        if (newly) atomicAdd(&tagged_on[cell], 1);
       }
       __syncthreads();
       if (is_agent && tagger) r = (float)tagged_on[cell] / (float)taggers_on[cell];
-      const int still = __syncthreads_count(is_agent && !tagger && active);
-      // every reader of the grids is past the count barrier: remove this step's marks, so the
-      // grids are empty again before the next step's first barrier (adds commute)
+      if (is_agent) ep_ret = ep_ret + r;
+      // A8 + termination in ONE CTA barrier: per warp the exact fixed-point reward sum (REDUX,
+      // warp_sum_u64) and the count of still-active runners; every thread adds the partials
+      const unsigned long long wrs = warp_sum_u64(is_agent ? (unsigned long long)to_fx(r) : 0ull);
+      const int wst = __popc(__ballot_sync(kFull, is_agent && !tagger && active));
+      if (lane == 0) {
+        red[3 * wid] = (long long)wrs;
+        red[3 * wid + 2] = wst;
+      }
+      __syncthreads();
+      long long srs = 0, still = 0;
+      for (int i = 0; i < nwarps; ++i) {
+        srs += red[3 * i];
+        still += red[3 * i + 2];
+      }
+      // every reader of the grids is past that barrier: remove this step's marks, so the grids
+      // are empty again before the next step's first barrier (adds commute)
       if (is_agent && tagger) atomicAdd(&taggers_on[cell], -1);
       if (newly) atomicAdd(&tagged_on[cell], -1);
       const bool term = n_runners > 0 && still == 0;
       ep_step += 1;
       const bool trunc = ep_step >= a.max_steps;
       d = (uint8_t)((term ? 1 : 0) | (trunc ? 2 : 0));
-      if (is_agent) ep_ret = ep_ret + r;
+      long long srt = 0;
+      if (d) {  // episode ended (CTA-uniform, once per episode): sum of the agents' returns
+        const unsigned long long wrt = warp_sum_u64(is_agent ? (unsigned long long)to_fx(ep_ret) : 0ull);
+        if (lane == 0) red[3 * wid + 1] = (long long)wrt;
+        __syncthreads();
+        if (threadIdx.x == 0)
+          for (int i = 0; i < nwarps; ++i) srt += red[3 * i + 1];
+      }
+      if (threadIdx.x == 0) {
+        unsigned long long* st = a.stats + (size_t)slot * 4;
+        if (d) {
+          atomicAdd(st + kStEpisodes, 1ull);
+          atomicAdd(st + kStLength, (unsigned long long)ep_step);
+          if (srt) atomicAdd(st + kStReturn, (unsigned long long)srt);
+        }
+        if (srs) atomicAdd(st + kStReward, (unsigned long long)srs);
+      }
     } else {
       if (threadIdx.x == 0) atomicOr(a.err, kErrAction | (mode == kTagRollout && bad_probs ? kErrProbs : 0u));
-      if (hoisted) __syncthreads();  // orders the previous step's reduction reads (no vote barrier here)
     }
     if (is_agent) st_cs(a.rew + idx, r);
-    // A8: one exact CTA reduction of (sum of rewards, sum of episode returns) -- the latter
-    // is used only when the episode ended (d is CTA-uniform)
-    long long rs = is_agent ? to_fx(r) : 0ll;
-    long long rt = is_agent ? to_fx(ep_ret) : 0ll;
-#pragma unroll
-    for (int o = 16; o > 0; o >>= 1) {
-      rs += __shfl_xor_sync(kFull, rs, o);
-      rt += __shfl_xor_sync(kFull, rt, o);
-    }
-    if (lane == 0) {
-      red[2 * wid] = rs;
-      red[2 * wid + 1] = rt;
-    }
-    __syncthreads();
-    if (threadIdx.x == 0) {
-      long long srs = 0, srt = 0;
-      for (int i = 0; i < nwarps; ++i) {
-        srs += red[2 * i];
-        srt += red[2 * i + 1];
-      }
-      const size_t di = (size_t)slot * (size_t)a.E + (size_t)e;
-      st_cs_u8(a.done + di, d);
-      unsigned long long* st = a.stats + (size_t)slot * 4;
-      if (d) {
-        atomicAdd(st + kStEpisodes, 1ull);
-        atomicAdd(st + kStLength, (unsigned long long)ep_step);
-        if (srt) atomicAdd(st + kStReturn, (unsigned long long)srt);
-      }
-      if (srs) atomicAdd(st + kStReward, (unsigned long long)srs);
-    }
+    if (threadIdx.x == 0) st_cs_u8(a.done + ((size_t)slot * (size_t)a.E + (size_t)e), d);
     if (d) {  // A5 auto-reset, uniform across the CTA
       rc += 1;
       if (is_agent) {
@@ -1549,8 +1539,8 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
       ep_step = 0;
       ep_ret = 0.0f;
     }
-    // (the reduction buffer is next written after at least one more CTA barrier, which
-    // thread 0 reaches only after reading it)
+    // (the reduction buffer is next written after the next valid step's first barrier, which
+    // every thread reaches only after reading it)
   }
   if (is_agent) {
     int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
@@ -1697,7 +1687,7 @@ static int tag_block(const KArgs& a) { return ((a.A + 31) / 32) * 32; }
 static void tag_launch(const KArgs& a, const Launch& l, int b, int mode, int T, uint64_t t0, int slot0,
                        const float* probs, int64_t row_stride, int64_t step_stride, const void* given) {
 #ifndef WS_TAG_MINB
-#define WS_TAG_MINB 6
+#define WS_TAG_MINB 7
 #endif
 #define WS_TAG_LAUNCH(MT, MB, H)                                                                        \
   k_tag<MT, MB, H><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, \
