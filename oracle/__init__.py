@@ -71,6 +71,8 @@ def lib():
             "wso_sample": (I, [P, P, I64, P, P]),
             "wso_step": (I, [P, P]),
             "wso_rollout": (I, [P, I, P, I64, I64, P, P, I]),
+            "wso_rollout_policy": (I, [P, I, P, I, I]),
+            "wso_policy_probs": (I, [P, I, I, I, P, I64, P]),
             "wso_synchronize": (I, [P]),
             "wso_info": (None, [P, P]),
             "wso_get": (P, [P, C.c_char_p]),
@@ -114,6 +116,15 @@ def sample_discrete(p, u: float):
     a = np.zeros(1, np.int32); lp = np.zeros(1, np.float32); amb = np.zeros(1, np.int32)
     st = lib().wso_sample_discrete(_p(pa), len(pa), np.float32(u), _p(a), _p(lp), _p(amb))
     return st, int(a[0]), float(lp[0]), bool(amb[0])
+
+
+def policy_probs(weights, D: int, H: int, N: int, obs) -> np.ndarray:
+    """MLP policy probabilities (R29) of observations [n, D] -> [n, N]."""
+    weights = np.ascontiguousarray(weights, dtype=np.float32)
+    obs = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1, D)
+    out = np.zeros((obs.shape[0], N), np.float32)
+    assert lib().wso_policy_probs(_p(weights), D, H, N, _p(obs), obs.shape[0], _p(out)) == 0
+    return out
 
 
 def sample_grid(p):
@@ -272,6 +283,11 @@ class Batch:
             override = np.ascontiguousarray(override, dtype=np.int32)
         return lib().wso_rollout(self._h, T, _p(probs), row_stride, step_stride, _p(override),
                                  _p(ambiguous), n_threads)
+
+    def rollout_policy(self, T: int, weights: np.ndarray, hidden: int, n_threads: int = 1) -> int:
+        """NEXT-N1: roll-out driven by the MLP policy (wso.cpp policy_probs, DESIGN R29)."""
+        weights = np.ascontiguousarray(weights, dtype=np.float32)
+        return lib().wso_rollout_policy(self._h, T, _p(weights), hidden, n_threads)
 
     def synchronize(self) -> int:
         return lib().wso_synchronize(self._h)

@@ -394,6 +394,42 @@ enum Err { E_OK = 0, E_INVALID_ARGUMENT = 1, E_UNKNOWN_ENV = 2, E_INVALID_ACTION
            E_INVALID_PROBS = 4, E_OUT_OF_RANGE = 5, E_BAD_STATE = 6 };
 const int ERRBIT_ACTION = 1, ERRBIT_PROBS = 2;
 
+/* ---------------------------------------------------------------------------------------
+ * NEXT-N1 ("action inference with deep policy models resident in global
+ * memory", "roll-outs, action inference, reset and training"): a two-layer MLP policy
+ * obs[D] -> ReLU(W1^T obs + b1)[H] -> logits W2^T h + b2 [N] -> softmax -> probabilities.
+ * Reading R29 (DESIGN): fp32 with fused multiply-adds in a fixed order -- h_j = b1_j, then
+ * h_j = fma(W1[k][j], obs_k, h_j) for k = 0..D-1, h_j = h_j > 0 ? h_j : 0; l_i = b2_i, then
+ * l_i = fma(W2[j][i], h_j, l_i) for j = 0..H-1; m = max_i l_i (first wins); e_i = (float)
+ * exp((double)(l_i - m)) (R3); S = e_0 + e_1 + ... in fp32; p_i = e_i / S.  Packed weights:
+ * W1 [D][H] | b1 [H] | W2 [H][N] | b2 [N], row-major fp32.
+ * ------------------------------------------------------------------------------------- */
+static void policy_probs(const float* w, int D, int H, int N, const float* obs, float* p) {
+  const float* W1 = w;
+  const float* b1 = W1 + (size_t)D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + (size_t)H * N;
+  std::vector<float> h((size_t)H), l((size_t)N);
+  for (int j = 0; j < H; ++j) {
+    float acc = b1[j];
+    for (int k = 0; k < D; ++k) acc = std::fma(W1[(size_t)k * H + j], obs[k], acc);
+    h[j] = acc > 0.0f ? acc : 0.0f;
+  }
+  for (int i = 0; i < N; ++i) {
+    float acc = b2[i];
+    for (int j = 0; j < H; ++j) acc = std::fma(W2[(size_t)j * N + i], h[j], acc);
+    l[i] = acc;
+  }
+  float m = l[0];
+  for (int i = 1; i < N; ++i) m = l[i] > m ? l[i] : m;
+  float S = 0.0f;
+  for (int i = 0; i < N; ++i) {
+    p[i] = (float)std::exp((double)(l[i] - m));
+    S = S + p[i];
+  }
+  for (int i = 0; i < N; ++i) p[i] = p[i] / S;
+}
+
 struct Batch {
   Kind kind;
   int64_t E, E_global, offset;
@@ -869,6 +905,55 @@ int wso_rollout(void* h, int T, const float* probs, int64_t row_stride, int64_t 
       const int32_t* ov = override_act ? override_act + (size_t)c * b->EA() : nullptr;
       uint8_t* amb = ambiguous_out ? ambiguous_out + (size_t)c * b->EA() : nullptr;
       b->sample_range(c, t0 + c, pr, row_stride, ov, amb, e0, e1, &errs[w]);
+      b->step_range(c, e0, e1, &st[w][(size_t)c * 4], &errs[w]);
+    }
+  };
+  if (n_threads == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 0; w < n_threads; ++w) th.emplace_back(worker, w);
+    for (auto& x : th) x.join();
+  }
+  for (int c = 0; c < T; ++c)
+    for (int i = 0; i < 4; ++i) {
+      double s = 0;
+      for (int w = 0; w < n_threads; ++w) s += st[w][(size_t)c * 4 + i];
+      b->stats[(size_t)c * 4 + i] = s;
+    }
+  for (int w = 0; w < n_threads; ++w) b->err |= errs[w];
+  b->t = t0 + T;
+  b->cursor = T;
+  b->sampled_slot = -1;
+  return E_OK;
+}
+
+/* NEXT-N1: probabilities of the MLP policy for n observations [n][D] -> out [n][N] */
+int wso_policy_probs(const float* weights, int D, int H, int N, const float* obs, int64_t n, float* out) {
+  if (!weights || !obs || !out || D < 1 || H < 1 || N < 1) return E_INVALID_ARGUMENT;
+  for (int64_t r = 0; r < n; ++r) policy_probs(weights, D, H, N, obs + r * D, out + r * N);
+  return E_OK;
+}
+
+/* NEXT-N1: roll-out whose probabilities come from the MLP policy applied to each replica's
+ * pre-step observation obs_live (single-agent discrete envs); otherwise as wso_rollout. */
+int wso_rollout_policy(void* h, int T, const float* weights, int H, int n_threads) {
+  Batch* b = (Batch*)h;
+  if (T < 1 || !weights || H < 1 || b->A != 1 || b->n_actions < 1) return E_INVALID_ARGUMENT;
+  if (T > b->T_cap) return E_OUT_OF_RANGE;
+  if (n_threads < 1) n_threads = 1;
+  if (n_threads > b->E) n_threads = (int)b->E;
+  const uint64_t t0 = b->t;
+  const int D = b->obs_dim, N = b->n_actions;
+  b->cursor = 0;
+  std::vector<float> probs((size_t)b->E * N);
+  std::vector<std::vector<double>> st(n_threads, std::vector<double>((size_t)T * 4, 0.0));
+  std::vector<int> errs(n_threads, 0);
+  auto worker = [&](int w) {
+    int64_t e0 = b->E * w / n_threads, e1 = b->E * (w + 1) / n_threads;
+    for (int c = 0; c < T; ++c) {
+      for (int64_t e = e0; e < e1; ++e) policy_probs(weights, D, H, N, &b->obs_live[(size_t)e * D], &probs[(size_t)e * N]);
+      b->sample_range(c, t0 + c, probs.data(), N, nullptr, nullptr, e0, e1, &errs[w]);
       b->step_range(c, e0, e1, &st[w][(size_t)c * 4], &errs[w]);
     }
   };

@@ -97,3 +97,14 @@ def workload_probs(w: Workload) -> np.ndarray:
     if w.env == "surface":
         return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, float(np.log(0.025)))
     return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, 0.0)
+
+
+def policy_weights(D: int, H: int, N: int, seed: int = SEED, scale: float = 1.0) -> np.ndarray:
+    """NEXT-N1 MLP policy weights, packed W1 [D][H] | b1 [H] | W2 [H][N] | b2 [N] (float32,
+    reading R29): Glorot-like normal draws times `scale`."""
+    rng = np.random.default_rng(seed)
+    W1 = rng.standard_normal((D, H)) * (scale / np.sqrt(D))
+    b1 = rng.standard_normal(H) * 0.1 * scale
+    W2 = rng.standard_normal((H, N)) * (scale / np.sqrt(H))
+    b2 = rng.standard_normal(N) * 0.1 * scale
+    return np.concatenate([W1.ravel(), b1, W2.ravel(), b2]).astype(np.float32)
