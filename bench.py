@@ -119,6 +119,14 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+def oracle_rollout(b, w, T, probs, cores):
+    """One oracle roll-out of workload w (policy-driven for NEXT-N1 workloads)."""
+    pol = W.workload_policy(w)
+    if pol:
+        return b.rollout_policy(T, pol[1], pol[0], n_threads=cores)
+    return b.rollout(T, probs, n_threads=cores)
+
+
 def cpu_baseline(w, budget_s: float = 10.0):
     """The oracle as it stands (oracle/, never tuned for this), on this host's cores, on a
     bounded sample of the same workload: consecutive whole-workload roll-outs (the bench's
@@ -128,13 +136,13 @@ def cpu_baseline(w, budget_s: float = 10.0):
     probs = W.workload_probs(w)
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
     t0 = time.perf_counter()
-    b.rollout(min(10, w.T), probs, n_threads=cores)
+    oracle_rollout(b, w, min(10, w.T), probs, cores)
     probe = time.perf_counter() - t0
     T_s = max(10, min(w.T, int(min(10, w.T) * budget_s / max(probe, 1e-6))))
     steps, dt, n = 0, 0.0, 0
     t0 = time.perf_counter()
     while True:
-        b.rollout(T_s, probs, n_threads=cores)
+        oracle_rollout(b, w, T_s, probs, cores)
         steps += w.n_envs * T_s
         n += 1
         dt = time.perf_counter() - t0
@@ -156,16 +164,16 @@ def run_reference(args, w):
     # would take more than ~5 s on this host, then a prefix of T_s steps
     b0 = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=min(10, w.T))
     t0 = time.perf_counter()
-    b0.rollout(min(10, w.T), probs, n_threads=cores)
+    oracle_rollout(b0, w, min(10, w.T), probs, cores)
     per_step = (time.perf_counter() - t0) / min(10, w.T)
     T_s = max(1, min(w.T, int(5.0 / max(per_step, 1e-9))))
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=T_s)
     for _ in range(args.warmup):
-        b.rollout(T_s, probs, n_threads=cores)
+        oracle_rollout(b, w, T_s, probs, cores)
     times = []
     for _ in range(args.steps):
         t0 = time.perf_counter()
-        b.rollout(T_s, probs, n_threads=cores)
+        oracle_rollout(b, w, T_s, probs, cores)
         times.append(time.perf_counter() - t0)
     tot = sum(times)
     value = w.n_envs * T_s * args.steps / tot
@@ -216,6 +224,15 @@ def main():
     probs_host = W.workload_probs(w)
     probs = torch.from_numpy(probs_host).to(dev)
     stats_view = env.buffers()["stats"][:T]
+    pol = W.workload_policy(w)  # NEXT-N1 workloads: actions from the in-kernel MLP policy
+    pol_w = torch.from_numpy(pol[1]).to(dev) if pol else None
+
+    def gpu_rollout(e_obj):
+        if pol:
+            e_obj.rollout_policy(T, pol_w, pol[0])
+        else:
+            e_obj.rollout(T, probs)
+
     p2p = False
     if world > 1 and args.stats_reduce == "p2p":
         from paper_2408_00930_b200.parallel import attach_peer_stats
@@ -226,7 +243,7 @@ def main():
             allreduce_stats(stats_view)
 
     def one_step():
-        env.rollout(T, probs)
+        gpu_rollout(env)
         merge_stats()
 
     for _ in range(max(args.warmup, 0)):
@@ -250,7 +267,7 @@ def main():
         dist.barrier()
     ev[0].record(stream)
     for k in range(args.steps):
-        env.rollout(T, probs)
+        gpu_rollout(env)
         merge_stats()
     ev[1].record(stream)
     torch.cuda.synchronize(dev)
@@ -277,7 +294,7 @@ def main():
     dev_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_diag)]
     for k in range(n_diag):
         dev_ev[2 * k].record(stream)
-        env.rollout(T, probs)
+        gpu_rollout(env)
         dev_ev[2 * k + 1].record(stream)
     torch.cuda.synchronize(dev)
     kern_ms = [dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)]
@@ -299,9 +316,11 @@ def main():
     n_plan, plan_ms = diag_times.get("plan", (0, 0.0))
     # tag samples inside its roll-out kernel: obs 16 + rew 4 + act 4 + logp 4 per agent-step, done 1 per env-step
     roll_bytes = int(ROLLOUT_BYTES.get(w.env, 0) * E * A * T if w.env != "tag" else (16 + 4 + 4 + 4) * E * A * T + E * T)
+    if pol:  # the policy kernel also writes act + logp and reads no plan
+        roll_bytes = int((4 * OBS_DIM[w.env] + 4 + 1 + 8) * E * A * T)
     achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
     call_ms = sum(kern_ms) / len(kern_ms)
-    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T if w.env != "tag" else 0))
+    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T if w.env not in ("tag",) and not pol else 0))
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
@@ -314,6 +333,22 @@ def main():
                 "ws_rollout_call": {"ms": round(call_ms, 4), "bytes": all_bytes,
                                     "achieved_GBps": round(all_bytes / (call_ms / 1e3) / 1e9, 1),
                                     "frac": round(all_bytes / (call_ms / 1e3) / 1e9 / peak, 4)}}
+    if pol:
+        # NEXT-N1: the MLP's fused multiply-adds per replica-step (D x H + H x n), against the
+        # fp32 FMA peak from unit counts and clock: 148 SMs x 128 lanes x 2 flop x 1.965 GHz
+        D_obs, Hh = OBS_DIM[w.env], pol[0]
+        flops = 2.0 * (D_obs * Hh + Hh * w.n_actions) * E * A * T
+        fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
+        tf = flops / (roll_ms / 1e3) / 1e12 if roll_ms > 0 else 0.0
+        roofline["kernel"] = f"k_rollout_policy<{w.env},{Hh}>"
+        roofline["other_kernels"] = {}
+        roofline["alu_view"] = {"achieved": round(tf, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
+                                "frac": round(tf / fp32_peak, 4), "flops_per_launch": flops,
+                                "peak_source": "derived: 148 SMs x 128 FP32 lanes x 2 x 1.965 GHz (B200_PROFILING.md)"}
+        if tf / fp32_peak > roofline["frac"]:  # report the binding one
+            hbm_view = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
+            roofline.update({"bound": "alu", "achieved": round(tf, 3), "peak": round(fp32_peak, 1),
+                             "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "hbm_view": hbm_view})
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
@@ -330,16 +365,33 @@ def main():
             # end to end through the public API with HOST buffers: pinned probs H2D + stats D2H per step
             henv = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
                        param0=params[0], param1=params[1], block_size=args.block)
-            hp = torch.from_numpy(probs_host).pin_memory()
+            if pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
+                hw = torch.from_numpy(pol[1]).pin_memory()
+                dw = torch.empty_like(hw, device=dev)
+                hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+
+                def host_step():
+                    dw.copy_(hw, non_blocking=True)
+                    henv.rollout_policy(T, dw, pol[0])
+                    hs.copy_(henv.buffers()["stats"][:T], non_blocking=True)
+                    torch.cuda.synchronize(dev)
+                h2d = int(hw.numel() * 4)
+            else:
+                hp = torch.from_numpy(probs_host).pin_memory()
+
+                def host_step():
+                    henv.rollout_host(T, hp)
+                h2d = int(hp.numel() * 4)
             for _ in range(max(args.warmup, 1)):
-                henv.rollout_host(T, hp)
+                host_step()
             t0 = time.perf_counter()
             for _ in range(args.steps):
-                henv.rollout_host(T, hp)
+                host_step()
             e2e_s = time.perf_counter() - t0
             e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
-                   "h2d_bytes_per_step": int(hp.numel() * 4), "d2h_bytes_per_step": int(T * 4 * 8),
-                   "note": "rank 0, ws_rollout_host, host wall clock"}
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(T * 4 * 8),
+                   "note": "rank 0, " + ("ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
+                           + ", host wall clock"}
             henv.close()
         line = {
             "metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": world,

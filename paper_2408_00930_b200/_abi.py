@@ -89,6 +89,7 @@ _SIGS = {
     "ws_last_error": (C.c_char_p, [C.c_void_p]),
     "ws_abi_version": (C.c_int32, []),
     "ws_enable_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
+    "ws_rollout_policy": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
     "ws_peer_export": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_attach": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_detach": (C.c_int, [C.c_void_p]),

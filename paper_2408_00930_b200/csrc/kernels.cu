@@ -63,6 +63,9 @@ struct Lane<CartPole> {
   __device__ static void step_aux(St& s, Aux&, int a, float& r, bool& term) { step<kFast>(s, a, r, term); }
   __device__ static void obs_store_aux(float* dst, const St& s, const Aux&, bool cs) { obs_store(dst, s, cs); }
   __device__ static Aux select(bool p, const Aux& x, const Aux&) { return x; }
+  __device__ static void obs_vals(const St& s, const Aux&, float (&o)[4]) {
+    o[0] = s.x; o[1] = s.xd; o[2] = s.th; o[3] = s.thd;
+  }
   __device__ static bool valid(int a) { return CartPole::valid(a); }
   // natural episodes last >= 8 steps (tests/test_oracle_envs.py::test_cartpole_min_episode_length)
   static constexpr int kMinEpisode = 8;
@@ -117,6 +120,9 @@ struct Lane<Acrobot> {
   __device__ static Aux select(bool p, const Aux& x, const Aux& y) {
     return Aux{p ? x.s1 : y.s1, p ? x.c1 : y.c1, p ? x.s2 : y.s2, p ? x.c2 : y.c2, p ? x.s12 : y.s12, p ? x.c12 : y.c12};
   }
+  __device__ static void obs_vals(const St& s, const Aux& t, float (&o)[6]) {
+    o[0] = t.c1; o[1] = t.s1; o[2] = t.c2; o[3] = t.s2; o[4] = s.w1; o[5] = s.w2;
+  }
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
   static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
   // throughput build: an 8-row statistics window and <= 80 registers give 6 resident CTAs of
@@ -153,6 +159,7 @@ struct Lane<Dummy> {
   __device__ static void step_aux(St& s, Aux&, int a, float& r, bool& term) { step<kFast>(s, a, r, term); }
   __device__ static void obs_store_aux(float* dst, const St& s, const Aux&, bool cs) { obs_store(dst, s, cs); }
   __device__ static Aux select(bool p, const Aux& x, const Aux&) { return x; }
+  __device__ static void obs_vals(const St&, const Aux&, float (&o)[4]) { o[0] = o[1] = o[2] = o[3] = 0.0f; }
   __device__ static bool valid(int a) { return a == 0 || a == 1; }
   static constexpr int kMinEpisode = 1 << 30;  // episodes end by truncation only
   static constexpr int kMaxThreads = 256;
@@ -703,6 +710,146 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
     a.reset_count[e] = R.rc;
     a.ep_ret[e] = R.ep_ret;
     L::obs_store(a.obs_live + e * L::D, R.s, false);
+  }
+}
+
+// =======================================================================================
+// NEXT-N1: fused roll-out with in-kernel policy inference ("operating an agent that
+// samples actions", "roll-outs, action inference, reset and training" on one GPU
+// store).  Each lane runs its replica's two-layer MLP on the pre-step observation
+// (weights in shared memory, fp32 FMAs in the fixed order of reading R29), softmax (R3
+// exponentials), the R13 inverse-CDF draw from the ACTION stream (R15), then the dynamics,
+// reward / done, auto-reset and all stores of k_rollout_discrete.  Actions now depend on
+// the state, so there is no plan kernel.  The network is tiny (D x H + H x N MACs per
+// replica-step) and per-replica, so it runs on the FMA pipe rather than the tensor cores.
+// =======================================================================================
+template <class Env, int H>
+__global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int T, const uint64_t t0,
+                                                       const float* __restrict__ weights) {
+  using L = Lane<Env>;
+  using St = typename L::St;
+  constexpr int D = L::D, N = L::N;
+  constexpr int NW = D * H + H + H * N + N;
+  constexpr int kRows = 16;
+  __shared__ __align__(16) float sw[NW];
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = weights[i];
+  __syncthreads();
+  const float* W1 = sw;
+  const float* b1 = W1 + D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + H * N;
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  if (e - lane >= E) return;  // whole warp past the last replica
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;  // tail lanes shadow replica E-1 (identical stores)
+  const int nlive = (int)min((int64_t)32, E - (e - lane));
+  const uint32_t eg = (uint32_t)(a.offset + ec);
+  const Key key{a.k0, a.k1};
+  const size_t sE = (size_t)E;
+  StatsWindow win;
+  win.init(ws_smem + (threadIdx.x >> 5) * (3 * kRows * kWinStride), kRows);
+  St s;
+  L::load(a.state + ec * L::S, s);
+  typename L::Aux aux = L::aux_of(s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  uint32_t err = 0;
+  U4 w4{0, 0, 0, 0};
+  for (int c = 0; c < T; ++c) {
+    const uint64_t t = t0 + (uint64_t)c;
+    if (c == 0 || (t & 3) == 0) w4 = block(key, t >> 2, eg, 0, kAction);
+    const size_t idx = (size_t)c * sE + (size_t)ec;
+    L::obs_store_aux(a.obs + idx * L::D, s, aux, true);
+    // ---- inference: h = relu(W1^T o + b1), l = W2^T h + b2, p = softmax(l)
+    float o[D];
+    L::obs_vals(s, aux, o);
+    float hid[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      float acc = b1[j];
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
+      hid[j] = acc > 0.0f ? acc : 0.0f;
+    }
+    float lg[N];
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      float acc = b2[i];
+#pragma unroll
+      for (int j = 0; j < H; ++j) acc = __fmaf_rn(W2[j * N + i], hid[j], acc);
+      lg[i] = acc;
+    }
+    float m = lg[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
+    RowCDF<N> cdf;
+    float S = 0.0f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      cdf.P[i] = (float)exp((double)fsub(lg[i], m));
+      S = fadd(S, cdf.P[i]);
+    }
+    double run = 0.0;
+    bool badp = false;
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      cdf.P[i] = fdiv(cdf.P[i], S);
+      run += (double)cdf.P[i];
+      cdf.C[i] = run;
+      badp = badp || !(cdf.P[i] >= 0.0f) || !isfinite(cdf.P[i]);
+    }
+    cdf.bad = badp || !(run > 0.0) || !isfinite(run);
+    // ---- A2 draw (R13) from the ACTION stream
+    int act = search<N>(cdf, u01(pick(w4, (uint32_t)(t & 3))));
+    float lp = logp_of<N>(cdf, act);
+    if (cdf.bad) {
+      act = -1;
+      lp = __int_as_float(0x7fc00000);
+      if (live) err |= kErrProbs | kErrAction;
+    }
+    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
+    if (a.write_logp) st_cs(a.logp + idx, lp);
+    // ---- A3-A5
+    const bool bad = act < 0;
+    St s2 = s;
+    typename L::Aux aux2 = aux;
+    float r;
+    bool term;
+    L::template step_aux<false>(s2, aux2, bad ? 0 : act, r, term);
+    const int32_t es = ep_step + 1;
+    const uint32_t d = bad ? 0u : ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u));
+    const float rw = bad ? 0.0f : r;
+    const float ret = ep_ret + r;
+    if (!bad) {
+      s = s2;
+      aux = aux2;
+      ep_step = es;
+      ep_ret = ret;
+    }
+    if (d) {  // auto-reset (R11)
+      rc += 1;
+      L::init(key, eg, rc, s);
+      aux = L::aux_of(s);
+      ep_step = 0;
+      ep_ret = 0.0f;
+    }
+    st_cs(a.rew + idx, rw);
+    st_cs_u8(a.done + idx, (uint8_t)d);
+    win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
+      win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, nlive);
+  }
+  if (live) {
+    L::save(a.state + e * L::S, s);
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    L::obs_store(a.obs_live + e * L::D, s, false);
+    if (err) atomicOr(a.err, err);
   }
 }
 
@@ -1837,6 +1984,33 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
       err = cudaGetLastError();
       break;
     }
+  }
+  *launches += 1;
+  return err;
+}
+
+template <class Env>
+static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
+                                  int hidden) {
+  const size_t smem = 4 * 3 * 16 * kWinStride * sizeof(uint32_t);  // 4 warps x 16-row windows
+  l.m(kKRollout, 0);
+  switch (hidden) {
+    case 32: k_rollout_policy<Env, 32><<<grid_for(a.E, 128), 128, smem, l.stream>>>(a, T, t0, weights); break;
+    case 64: k_rollout_policy<Env, 64><<<grid_for(a.E, 128), 128, smem, l.stream>>>(a, T, t0, weights); break;
+    default: return cudaErrorInvalidValue;
+  }
+  l.m(kKRollout, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
+                                  int hidden, uint64_t* launches) {
+  cudaError_t err = cudaErrorInvalidValue;
+  switch (l.kind) {
+    case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden); break;
+    case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden); break;
+    case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden); break;
+    default: break;
   }
   *launches += 1;
   return err;

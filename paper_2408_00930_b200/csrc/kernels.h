@@ -64,6 +64,10 @@ cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float*
 cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
                                    cudaStream_t s);
 
+// NEXT-N1: fused roll-out with in-kernel MLP policy inference (hidden 32 or 64)
+cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
+                                  int hidden, uint64_t* launches);
+
 // A8 across GPUs without NCCL (section 8e "v2"): every rank publishes its [T,4] statistics
 // into every peer's gather buffer through CUDA-IPC-mapped peer memory (NVLink / NVSwitch),
 // signals the peers' arrival counters, waits for all ranks and sums the slices.

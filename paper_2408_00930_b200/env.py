@@ -183,6 +183,15 @@ class Env:
         mode = 0 if enable is False else (1 if enable is True else int(enable))
         check(lib().ws_enable_kernel_timing(self._h, mode), self._h)
 
+    def rollout_policy(self, T: int, weights: torch.Tensor, hidden: int) -> None:
+        """NEXT-N1: T fused steps whose actions are drawn from an in-kernel MLP policy
+        (ws.h ws_rollout_policy); weights: packed fp32 device tensor."""
+        w = weights.contiguous()
+        if w.dtype != torch.float32 or w.device != self.device:
+            raise ValueError("weights: float32 on the handle's device")
+        check(lib().ws_rollout_policy(self._h, T, w.data_ptr(), hidden), self._h)
+        self._keep = w  # alive until the stream has consumed it
+
     # ---- cross-GPU statistics over peer memory (ws.h "multi-GPU statistics")
     def peer_export(self, world: int) -> bytes:
         """Allocate this rank's IPC-exportable gather buffer; returns its 64-byte handle."""

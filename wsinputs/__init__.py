@@ -41,6 +41,9 @@ CONFIGS = {
     "C5": Workload("C5", "surface", 2000, 1, 200, 0, 20, {"dim": 20},
                    note="surface-20 2K envs x 200 (BJ:11)"),
     "D0": Workload("D0", "dummy", 1000000, 1, 100, 2, 1, note="store-write calibration"),
+    # NEXT-N1: C2's shape with the actions drawn from an in-kernel MLP policy
+    "C2P": Workload("C2P", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64},
+                    note="CartPole-v1 10K envs x 1000 steps, in-kernel MLP policy 4-64-2 (NEXT-N1)"),
 }
 
 
@@ -88,6 +91,15 @@ def action_table(T: int, E: int, A: int, n: int, seed: int = SEED, p1: float | N
 def continuous_action_table(T: int, E: int, A: int, d: int, scale: float, seed: int = SEED) -> np.ndarray:
     rng = np.random.default_rng(seed)
     return (scale * rng.standard_normal((T, E, A, d))).astype(np.float32)
+
+
+def workload_policy(w: Workload):
+    """(hidden, packed weights) of a policy-driven workload, else None."""
+    H = w.params.get("policy_hidden")
+    if not H:
+        return None
+    D = {"cartpole": 4, "acrobot": 6, "dummy": 4}[w.env]
+    return H, policy_weights(D, H, w.n_actions, seed=SEED, scale=2.0)
 
 
 def workload_probs(w: Workload) -> np.ndarray:
