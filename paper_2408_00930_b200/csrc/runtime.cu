@@ -266,6 +266,7 @@ const char* ws_status_string(ws_status s) {
     case WS_ERR_BAD_STATE: return "bad call order";
     case WS_ERR_OUT_OF_MEMORY: return "out of memory";
     case WS_ERR_CUDA: return "CUDA error";
+    case WS_ERR_PEER: return "peer reduction timed out";
   }
   return "unknown status";
 }

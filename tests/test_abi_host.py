@@ -70,8 +70,13 @@ def test_null_handle_and_status_strings():
     L = P.lib()
     assert L.ws_reset(None) == _abi.INVALID_ARGUMENT
     assert L.ws_destroy(None) == _abi.OK
-    for s in range(9):
-        assert L.ws_status_string(s)
+    for s in range(10):
+        assert L.ws_status_string(s) and L.ws_status_string(s) != b"unknown status"
+    # the later entry points validate their handle before anything else
+    assert L.ws_rollout_policy(None, 10, None, 32) == _abi.INVALID_ARGUMENT
+    assert L.ws_peer_export(None, 2, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_peer_attach(None, 0, 2, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_peer_detach(None) == _abi.INVALID_ARGUMENT
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")

@@ -81,3 +81,18 @@ def test_policy_invalid_weights_are_sticky(P):
     assert g.status() == P._abi.INVALID_PROBS
     buf = g.buffers()
     assert (buf["act"][:T] == -1).all() and (buf["done"][:T] == 0).all() and (buf["rew"][:T] == 0).all()
+
+
+def test_policy_argument_validation(P):
+    g = P.Env(8, 1, "cartpole", SEED, t_capacity=4)
+    w = torch.zeros(4 * 32 + 32 + 32 * 2 + 2, device="cuda")
+    with pytest.raises(P.WSError):
+        g.rollout_policy(4, w, 48)  # hidden must be 32 or 64
+    with pytest.raises(P.WSError):
+        g.rollout_policy(5, w, 32)  # T beyond the store capacity
+    t = P.Env(2, 10, "tag", SEED, t_capacity=4)
+    with pytest.raises(P.WSError):
+        t.rollout_policy(4, w, 32)  # multi-agent env: not supported by the policy roll-out
+    p = P.Env(4, 1, "pendulum", SEED, t_capacity=4)
+    with pytest.raises(P.WSError):
+        p.rollout_policy(4, w, 32)  # continuous actions
