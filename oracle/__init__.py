@@ -73,6 +73,8 @@ def lib():
             "wso_rollout": (I, [P, I, P, I64, I64, P, P, I]),
             "wso_rollout_policy": (I, [P, I, P, I, I]),
             "wso_policy_probs": (I, [P, I, I, I, P, I64, P]),
+            "wso_gae_f32": (I, [I, I64, I, P, P, P, P, P, F, F, P, P]),
+            "wso_gae_f64": (I, [I, I64, I, P, P, P, P, P, D, D, P, P]),
             "wso_synchronize": (I, [P]),
             "wso_info": (None, [P, P]),
             "wso_get": (P, [P, C.c_char_p]),
@@ -125,6 +127,25 @@ def policy_probs(weights, D: int, H: int, N: int, obs) -> np.ndarray:
     out = np.zeros((obs.shape[0], N), np.float32)
     assert lib().wso_policy_probs(_p(weights), D, H, N, _p(obs), obs.shape[0], _p(out)) == 0
     return out
+
+
+def gae(rew, done, values, bootstrap, gamma, lam, v_trunc=None, f64=False):
+    """NEXT-N2 GAE (wso.cpp gae, DESIGN R30): rew / values / v_trunc [T, E, A] (or [T, E]),
+    done [T, E] u8, bootstrap [E, A] -> (advantages, returns), same shape as rew."""
+    dt = np.float64 if f64 else np.float32
+    rew = np.ascontiguousarray(rew, dtype=dt)
+    T, E = rew.shape[0], rew.shape[1]
+    A = int(np.prod(rew.shape[2:])) if rew.ndim > 2 else 1
+    done = np.ascontiguousarray(done, dtype=np.uint8).reshape(T, E)
+    values = np.ascontiguousarray(values, dtype=dt).reshape(rew.shape)
+    bootstrap = np.ascontiguousarray(bootstrap, dtype=dt).reshape(E * A)
+    vt = None if v_trunc is None else np.ascontiguousarray(v_trunc, dtype=dt).reshape(rew.shape)
+    adv = np.zeros(rew.shape, dt); ret = np.zeros(rew.shape, dt)
+    fn = lib().wso_gae_f64 if f64 else lib().wso_gae_f32
+    st = fn(T, E, A, _p(rew), _p(done), _p(values), _p(bootstrap), _p(vt), dt(gamma), dt(lam),
+            _p(adv), _p(ret))
+    assert st == 0, st
+    return adv, ret
 
 
 def sample_grid(p):

@@ -25,6 +25,9 @@
  * IEEE.  Each environment step is a template on the real type R so the same text also
  * runs in fp64 ("gym mode") for the closed-form and physics pins in tests/.
  *
+ * NEXT-N2 (first stage): generalised advantage estimation over the store (SPEC compute_gae
+ * S:389-397, reading R30), the step that consumes the roll-out store in place for training.
+ *
  * Pins: every exported function is pinned by tests/test_oracle_*.py against values the
  * mathematics fixes (Random123 known answers, exact rational steps, Lagrangian
  * mechanics, published Mueller-Brown stationary points, exhaustive multinomial counts,
@@ -691,6 +694,48 @@ struct Batch {
   }
 };
 
+/* ------------------------------------------------------------------------------------
+ * NEXT-N2 (first stage): generalised advantage estimation over the time-major store,
+ * SPEC compute_gae, "standard actor-critic machinery the paper presumes"
+ * ("supports actor-critic algorithms"), reading R30 of DESIGN.md:
+ *   columns c = e*A + a; d = done[t][e]; v_T = bootstrap[c]; A_T = 0; for t = T-1 .. 0:
+ *     terminated, or truncated without a terminal value:  delta = r_t - v_t;  A_t = delta
+ *     truncated with v_trunc given:       delta = (r_t + g*vtr_t) - v_t; A_t = delta
+ *     otherwise:  delta = (r_t + g*v_{t+1}) - v_t;  A_t = delta + (g*l)*A_{t+1}
+ *     returns_t = A_t + v_t
+ * The recursion of S:392 written out with the done mask applied by dropping the masked
+ * terms; every operation rounds to R (fp32 parity mode, fp64 for the brute-force pins).
+ * ---------------------------------------------------------------------------------- */
+template <class R>
+void gae(int T, int64_t E, int A, const R* rew, const uint8_t* done, const R* values,
+         const R* bootstrap, const R* v_trunc, R gamma, R lambda, R* adv, R* ret) {
+  const int64_t C = E * A;
+  const R gl = gamma * lambda;
+  for (int64_t c = 0; c < C; ++c) {
+    R a_next = (R)0;
+    for (int t = T - 1; t >= 0; --t) {
+      const size_t i = (size_t)t * C + c;
+      const uint8_t d = done[(size_t)t * E + c / A];
+      const R r = rew[i], v = values[i];
+      R delta, a;
+      if ((d & 1) || ((d & 2) && !v_trunc)) {
+        delta = r - v;
+        a = delta;
+      } else if (d & 2) {
+        delta = (r + gamma * v_trunc[i]) - v;
+        a = delta;
+      } else {
+        const R v_next = (t == T - 1) ? bootstrap[c] : values[i + C];
+        delta = (r + gamma * v_next) - v;
+        a = delta + gl * a_next;
+      }
+      adv[i] = a;
+      ret[i] = a + v;
+      a_next = a;
+    }
+  }
+}
+
 Kind parse_kind(const char* s, bool* ok) {
   *ok = true;
   std::string n(s ? s : "");
@@ -925,6 +970,24 @@ int wso_rollout(void* h, int T, const float* probs, int64_t row_stride, int64_t 
   b->t = t0 + T;
   b->cursor = T;
   b->sampled_slot = -1;
+  return E_OK;
+}
+
+/* NEXT-N2: GAE (R30) over time-major arrays; v_trunc may be NULL. */
+int wso_gae_f32(int T, int64_t E, int A, const float* rew, const uint8_t* done, const float* values,
+                const float* bootstrap, const float* v_trunc, float gamma, float lambda, float* adv,
+                float* ret) {
+  if (T < 1 || E < 1 || A < 1 || !rew || !done || !values || !bootstrap || !adv || !ret)
+    return E_INVALID_ARGUMENT;
+  gae<float>(T, E, A, rew, done, values, bootstrap, v_trunc, gamma, lambda, adv, ret);
+  return E_OK;
+}
+int wso_gae_f64(int T, int64_t E, int A, const double* rew, const uint8_t* done, const double* values,
+                const double* bootstrap, const double* v_trunc, double gamma, double lambda, double* adv,
+                double* ret) {
+  if (T < 1 || E < 1 || A < 1 || !rew || !done || !values || !bootstrap || !adv || !ret)
+    return E_INVALID_ARGUMENT;
+  gae<double>(T, E, A, rew, done, values, bootstrap, v_trunc, gamma, lambda, adv, ret);
   return E_OK;
 }
 
