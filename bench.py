@@ -119,12 +119,31 @@ def measured_peaks():
         return {"hbm_gbs": 6650.0, "bf16_tflops": 1590.0}, "fallback"
 
 
+_GAE_INPUTS = {}
+
+
+def oracle_gae_inputs(w):
+    """Given GAE inputs of a NEXT-N2 workload (generated once, outside any timing)."""
+    if w.name not in _GAE_INPUTS:
+        _GAE_INPUTS[w.name] = W.gae_inputs(w.T, w.n_envs, w.n_agents)
+    return _GAE_INPUTS[w.name]
+
+
 def oracle_rollout(b, w, T, probs, cores):
-    """One oracle roll-out of workload w (policy-driven for NEXT-N1 workloads)."""
+    """One oracle roll-out of workload w (policy-driven for NEXT-N1 workloads; followed by
+    GAE over the slots it wrote for NEXT-N2 workloads)."""
     pol = W.workload_policy(w)
     if pol:
-        return b.rollout_policy(T, pol[1], pol[0], n_threads=cores)
-    return b.rollout(T, probs, n_threads=cores)
+        st = b.rollout_policy(T, pol[1], pol[0], n_threads=cores)
+    else:
+        st = b.rollout(T, probs, n_threads=cores)
+    gae = w.params.get("gae")
+    if gae:
+        import oracle as O
+        values, boot, _ = oracle_gae_inputs(w)
+        O.gae(b.array("rew")[:T].reshape(T, w.n_envs, w.n_agents), b.array("done")[:T], values[:T], boot,
+              gae[0], gae[1])
+    return st
 
 
 def cpu_baseline(w, budget_s: float = 10.0):
@@ -134,6 +153,8 @@ def cpu_baseline(w, budget_s: float = 10.0):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
+    if w.params.get("gae"):
+        oracle_gae_inputs(w)
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
     t0 = time.perf_counter()
     oracle_rollout(b, w, min(10, w.T), probs, cores)
@@ -160,6 +181,8 @@ def run_reference(args, w):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
+    if w.params.get("gae"):
+        oracle_gae_inputs(w)
     # each step = the workload's full roll-out (all replicas x T steps) unless one roll-out
     # would take more than ~5 s on this host, then a prefix of T_s steps
     b0 = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=min(10, w.T))
@@ -217,7 +240,7 @@ def main():
     E, A, T = w.n_envs, w.n_agents, w.T
     E_g = E * world
     offset = rank * E
-    params = {"C4": (20, 10), "C5": (20, 0)}.get(w.name, (0, 0))
+    params = (w.params.get("grid", w.params.get("dim", 0)), w.params.get("taggers", 0))
     stream = torch.cuda.current_stream(dev)
     env = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
               param0=params[0], param1=params[1], block_size=args.block)
@@ -226,12 +249,20 @@ def main():
     stats_view = env.buffers()["stats"][:T]
     pol = W.workload_policy(w)  # NEXT-N1 workloads: actions from the in-kernel MLP policy
     pol_w = torch.from_numpy(pol[1]).to(dev) if pol else None
+    gae = w.params.get("gae")   # NEXT-N2 workloads: GAE over the store after every roll-out
+    if gae:
+        g_vals, g_boot, _ = (torch.from_numpy(x).to(dev) if x is not None else None
+                             for x in W.gae_inputs(T, E, A, seed=W.SEED + rank))
+        g_out = (torch.empty((T, E, A), dtype=torch.float32, device=dev),
+                 torch.empty((T, E, A), dtype=torch.float32, device=dev))
 
     def gpu_rollout(e_obj):
         if pol:
             e_obj.rollout_policy(T, pol_w, pol[0])
         else:
             e_obj.rollout(T, probs)
+        if gae:
+            e_obj.gae_store(T, g_vals, g_boot, gae[0], gae[1], out=g_out)
 
     p2p = False
     if world > 1 and args.stats_reduce == "p2p":
@@ -258,7 +289,7 @@ def main():
         time.sleep(0.3)
     # two CUDA events per step around the fused roll-out kernel only (libws ws_kernel_times):
     # the dominant kernel is timed live with the least perturbation of the timed loop
-    env.enable_kernel_timing(0 if args.no_kernel_timing else 2)
+    env.enable_kernel_timing(0 if args.no_kernel_timing else (3 if gae else 2))
     env.kernel_times()
     launches0 = env.info().launches
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -321,6 +352,10 @@ def main():
     achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
     call_ms = sum(kern_ms) / len(kern_ms)
     all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T if w.env not in ("tag",) and not pol else 0))
+    # NEXT-N2: GAE reads rew + values and writes adv + returns (16 B per agent-step), reads
+    # the replica's done byte (1 B per replica-step) and the bootstrap row once
+    gae_bytes = 16 * E * A * T + E * T + 4 * E * A if gae else 0
+    all_bytes += gae_bytes
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
@@ -349,6 +384,13 @@ def main():
             hbm_view = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
             roofline.update({"bound": "alu", "achieved": round(tf, 3), "peak": round(fp32_peak, 1),
                              "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "hbm_view": hbm_view})
+    if gae:
+        n_gae, gae_ms = ktimes.get("gae", (0, 0.0))
+        g_ach = gae_bytes / (gae_ms / 1e3) / 1e9 if gae_ms > 0 else 0.0
+        roofline["gae_kernel"] = {"kernel": "k_gae_tma", "bound": "hbm", "achieved": round(g_ach, 1), "peak": peak,
+                                  "unit": "GB/s", "frac": round(g_ach / peak, 4), "kernel_ms": round(gae_ms, 4),
+                                  "launches_timed": n_gae, "bytes_per_launch": gae_bytes,
+                                  "bytes_per_agent_step": gae_bytes / (E * A * T)}
     traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
     if os.path.exists(traffic_file):
         try:
@@ -381,6 +423,9 @@ def main():
 
                 def host_step():
                     henv.rollout_host(T, hp)
+                    if gae:
+                        henv.gae_store(T, g_vals, g_boot, gae[0], gae[1], out=g_out)
+                        torch.cuda.synchronize(dev)
                 h2d = int(hp.numel() * 4)
             for _ in range(max(args.warmup, 1)):
                 host_step()
@@ -391,6 +436,7 @@ def main():
             e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
                    "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(T * 4 * 8),
                    "note": "rank 0, " + ("ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
+                           + (" + ws_gae_store" if gae else "")
                            + ", host wall clock"}
             henv.close()
         line = {

@@ -69,6 +69,13 @@ class ws_kernel_time(C.Structure):
     _fields_ = [("name", C.c_char_p), ("launches", C.c_int32), ("mean_ms", C.c_float), ("total_ms", C.c_float)]
 
 
+class ws_gae_args(C.Structure):
+    _fields_ = [("T", C.c_int32), ("n_agents", C.c_int32), ("n_envs", C.c_int64),
+                ("rew", C.c_void_p), ("done", C.c_void_p), ("values", C.c_void_p), ("bootstrap", C.c_void_p),
+                ("v_trunc", C.c_void_p), ("gamma", C.c_float), ("lam", C.c_float),
+                ("adv", C.c_void_p), ("ret", C.c_void_p)]
+
+
 _SIGS = {
     "ws_config_init": (C.c_int, [C.POINTER(ws_config)]),
     "ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -90,6 +97,9 @@ _SIGS = {
     "ws_abi_version": (C.c_int32, []),
     "ws_enable_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "ws_rollout_policy": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
+    "ws_gae": (C.c_int, [C.POINTER(ws_gae_args), C.c_void_p]),
+    "ws_gae_store": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float,
+                               C.c_void_p, C.c_void_p]),
     "ws_peer_export": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_attach": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_detach": (C.c_int, [C.c_void_p]),

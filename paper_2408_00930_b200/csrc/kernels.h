@@ -38,7 +38,7 @@ struct KArgs {
 };
 
 // kernel classes for the optional per-kernel timing (ws_enable_kernel_timing)
-enum KernelId : int { kKPlan = 0, kKRollout = 1, kKSample = 2, kKStep = 3, kKReset = 4, kKCount = 5 };
+enum KernelId : int { kKPlan = 0, kKRollout = 1, kKSample = 2, kKStep = 3, kKReset = 4, kKGae = 5, kKCount = 6 };
 
 struct Launch {
   EnvKind kind;
@@ -67,6 +67,24 @@ cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_
 // NEXT-N1: fused roll-out with in-kernel MLP policy inference (hidden 32 or 64)
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, uint64_t* launches);
+
+// NEXT-N2: generalised advantage estimation over the time-major store (gae.cu, R30)
+struct GaeArgs {
+  const float* rew;        // [T, E, A]
+  const uint8_t* done;     // [T, E]
+  const float* values;     // [T, E, A]
+  const float* bootstrap;  // [E, A]
+  const float* v_trunc;    // [T, E, A] or null
+  float* adv;              // [T, E, A]
+  float* ret;              // [T, E, A]
+  int64_t E;
+  int32_t A, T;
+  float gamma, lambda;
+  int force_lane;          // 1 = per-thread-load kernel regardless of alignment (tests)
+};
+// 0 = per-thread loads, 1 = TMA tiles for r / v (done per thread), 2 = TMA tiles for r / v / done
+int gae_path(int64_t E, int32_t A, const void* rew, const void* values, const void* done);
+cudaError_t launch_gae(const GaeArgs& a, cudaStream_t s, uint64_t* launches);
 
 // A8 across GPUs without NCCL (section 8e "v2"): every rank publishes its [T,4] statistics
 // into every peer's gather buffer through CUDA-IPC-mapped peer memory (NVLink / NVSwitch),

@@ -493,6 +493,36 @@ ws_status ws_rollout_policy(ws_env* h, int32_t T, const float* weights, int32_t 
   return WS_OK;
 }
 
+static ws_status run_gae(ws_env* h, const ws_gae_args* a, cudaStream_t s, const ws::Launch* l) {
+  if (!a || a->T < 1 || a->n_envs < 1 || a->n_agents < 1 || !a->rew || !a->done || !a->values || !a->bootstrap ||
+      !a->adv || !a->ret || !(a->gamma >= 0.0f && a->gamma <= 1.0f) || !(a->lambda >= 0.0f && a->lambda <= 1.0f))
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_gae: T, E, A >= 1, non-NULL arrays, gamma and lambda in [0, 1]");
+  ws::GaeArgs g{a->rew, a->done, a->values, a->bootstrap, a->v_trunc, a->adv, a->ret, a->n_envs, a->n_agents,
+                a->T, a->gamma, a->lambda, 0};
+  uint64_t launches = 0;
+  if (l) l->m(ws::kKGae, 0);
+  cudaError_t e = ws::launch_gae(g, s, h ? &h->launches : &launches);
+  if (l) l->m(ws::kKGae, 1);
+  if (e) return cuda_fail(h, e, "gae kernel");
+  return WS_OK;
+}
+
+ws_status ws_gae(const ws_gae_args* args, void* stream) {
+  return run_gae(nullptr, args, static_cast<cudaStream_t>(stream), nullptr);
+}
+
+ws_status ws_gae_store(ws_env* h, int32_t T, const float* values, const float* bootstrap, const float* v_trunc,
+                       float gamma, float lambda, float* adv, float* ret) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1");
+  if (!h->rew) return fail(h, WS_ERR_BAD_STATE, "ws_gae_store needs the store (t_capacity or a first ws_rollout)");
+  if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity");
+  DeviceGuard g(h->device);
+  ws_gae_args a{T, h->A, h->E, h->rew, h->done, values, bootstrap, v_trunc, gamma, lambda, adv, ret};
+  const ws::Launch l = launch_of(h);
+  return run_gae(h, &a, h->stream, &l);
+}
+
 ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t n_probs, int64_t row_stride,
                           int64_t step_stride, ws_stats* out) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
@@ -633,7 +663,7 @@ ws_status ws_test_exhaustive(int32_t fn_a, int32_t fn_b, float param, uint32_t l
   return e ? WS_ERR_CUDA : WS_OK;
 }
 
-static const char* kKernelNames[ws::kKCount] = {"plan", "rollout", "sample", "step", "reset"};
+static const char* kKernelNames[ws::kKCount] = {"plan", "rollout", "sample", "step", "reset", "gae"};
 
 ws_status ws_peer_export(ws_env* h, int32_t world, ws_ipc_handle* out) {
   if (check(h) || !out || world < 1 || world > ws::kMaxPeers)
@@ -703,7 +733,9 @@ ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
   }
   for (auto& r : h->rings) r.n = 0;
   h->timing = enable != 0;
-  h->timed_mask = enable == 2 ? (1u << ws::kKRollout) : 0xFFFFFFFFu;
+  h->timed_mask = enable == 2   ? (1u << ws::kKRollout)
+                 : enable == 3 ? (1u << ws::kKRollout) | (1u << ws::kKGae)
+                               : 0xFFFFFFFFu;
   return WS_OK;
 }
 

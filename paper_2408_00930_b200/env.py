@@ -192,6 +192,24 @@ class Env:
         check(lib().ws_rollout_policy(self._h, T, w.data_ptr(), hidden), self._h)
         self._keep = w  # alive until the stream has consumed it
 
+    def gae_store(self, T: int, values: torch.Tensor, bootstrap: torch.Tensor, gamma: float, lam: float,
+                  v_trunc: Optional[torch.Tensor] = None, out: Optional[tuple] = None):
+        """NEXT-N2: advantages and returns of store slots [0, T) (ws.h ws_gae_store), reading
+        the handle's rew / done slabs in place.  values / v_trunc [T, E, A], bootstrap [E, A]
+        float32 on the handle's device.  -> (adv, ret) [T, E, A] float32."""
+        info = self.info()
+        shape = (T, int(info.n_envs), int(info.n_agents))
+        for name, t, shp in (("values", values, shape), ("bootstrap", bootstrap, shape[1:]),
+                             ("v_trunc", v_trunc, shape)):
+            if t is not None and (t.dtype != torch.float32 or t.device != self.device or not t.is_contiguous()
+                                  or t.numel() != _numel(shp)):
+                raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 {shp} on the handle's device")
+        adv, ret = out if out is not None else (torch.empty(shape, dtype=torch.float32, device=self.device),
+                                                torch.empty(shape, dtype=torch.float32, device=self.device))
+        check(lib().ws_gae_store(self._h, T, _ptr(values), _ptr(bootstrap), _ptr(v_trunc), gamma, lam,
+                                 _ptr(adv), _ptr(ret)), self._h)
+        return adv, ret
+
     # ---- cross-GPU statistics over peer memory (ws.h "multi-GPU statistics")
     def peer_export(self, world: int) -> bytes:
         """Allocate this rank's IPC-exportable gather buffer; returns its 64-byte handle."""
@@ -263,6 +281,13 @@ class Env:
         return torch.as_tensor(obj, device=self.device)
 
 
+def _numel(shape) -> int:
+    n = 1
+    for s in shape:
+        n *= int(s)
+    return n
+
+
 # ---------------------------------------------------------------------- C-ABI-named functions
 def ws_create(n_envs: int, n_agents: int, env: str, seed: int) -> Env:
     return Env(n_envs, n_agents, env, seed)
@@ -315,6 +340,26 @@ def ws_synchronize(h: Env):
 
 def ws_read_stats(h: Env, t0: int = 0, t1: Optional[int] = None):
     return h.read_stats(t0, t1)
+
+
+def ws_gae(rew: torch.Tensor, done: torch.Tensor, values: torch.Tensor, bootstrap: torch.Tensor, gamma: float,
+           lam: float, v_trunc: Optional[torch.Tensor] = None, out: Optional[tuple] = None):
+    """NEXT-N2 generalised advantage estimation (ws.h ws_gae, DESIGN R30) on device arrays:
+    rew / values / v_trunc [T, E, A] (or [T, E]) float32, done [T, E] uint8, bootstrap [E, A]
+    -> (adv, ret) shaped like rew, enqueued on torch's current stream."""
+    T, E = int(rew.shape[0]), int(rew.shape[1])
+    A = _numel(rew.shape[2:])
+    for name, t, dt, n in (("rew", rew, torch.float32, T * E * A), ("values", values, torch.float32, T * E * A),
+                           ("done", done, torch.uint8, T * E), ("bootstrap", bootstrap, torch.float32, E * A),
+                           ("v_trunc", v_trunc, torch.float32, T * E * A)):
+        if t is not None and (t.dtype != dt or not t.is_cuda or not t.is_contiguous() or t.numel() != n):
+            raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous {dt} device tensor with {n} elements")
+    adv, ret = out if out is not None else (torch.empty_like(rew), torch.empty_like(rew))
+    args = _abi.ws_gae_args(T, A, E, rew.data_ptr(), done.data_ptr(), values.data_ptr(), bootstrap.data_ptr(),
+                            v_trunc.data_ptr() if v_trunc is not None else None, gamma, lam,
+                            adv.data_ptr(), ret.data_ptr())
+    check(lib().ws_gae(C.byref(args), C.c_void_p(torch.cuda.current_stream(rew.device).cuda_stream)))
+    return adv, ret
 
 
 def ws_test_philox(rows: torch.Tensor) -> torch.Tensor:

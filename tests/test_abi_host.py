@@ -106,3 +106,19 @@ def test_summarize():
     st = torch.tensor([[2, 40, 30, 5], [0, 0, 0, 5], [1, 10, 10, 5]], dtype=torch.float64)
     s = summarize(st)
     assert s["episodes"] == 3 and s["mean_return"] == 50 / 3 and s["mean_length"] == 40 / 3
+
+
+def test_gae_argument_validation_without_gpu():
+    """ws_gae / ws_gae_store (NEXT-N2) reject bad arguments before any CUDA call."""
+    L = P.lib()
+    assert C.sizeof(_abi.ws_gae_args) == 4 + 4 + 8 + 5 * 8 + 4 + 4 + 2 * 8
+    assert L.ws_gae(None, None) == _abi.INVALID_ARGUMENT
+    fake = 256  # never dereferenced: validation fails first
+    good = dict(T=4, n_agents=1, n_envs=8, rew=fake, done=fake, values=fake, bootstrap=fake, v_trunc=None,
+                gamma=0.99, lam=0.95, adv=fake, ret=fake)
+    for bad in (dict(T=0), dict(n_envs=0), dict(n_agents=0), dict(rew=None), dict(done=None), dict(values=None),
+                dict(bootstrap=None), dict(adv=None), dict(ret=None), dict(gamma=1.5), dict(lam=-0.1),
+                dict(gamma=float("nan"))):
+        a = _abi.ws_gae_args(**{**good, **bad})
+        assert L.ws_gae(C.byref(a), None) == _abi.INVALID_ARGUMENT, bad
+    assert L.ws_gae_store(None, 4, None, None, None, 0.99, 0.95, None, None) == _abi.INVALID_ARGUMENT

@@ -44,6 +44,11 @@ CONFIGS = {
     # NEXT-N1: C2's shape with the actions drawn from an in-kernel MLP policy
     "C2P": Workload("C2P", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64},
                     note="CartPole-v1 10K envs x 1000 steps, in-kernel MLP policy 4-64-2 (NEXT-N1)"),
+    # NEXT-N2: C2's roll-out followed by GAE over the store it wrote
+    "C2G": Workload("C2G", "cartpole", 10000, 1, 1000, 2, 1, {"gae": (0.99, 0.95)},
+                    note="CartPole-v1 10K envs x 1000 steps + GAE(0.99, 0.95) over the store (NEXT-N2)"),
+    "C4G": Workload("C4G", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10, "gae": (0.99, 0.95)},
+                    note="tag 1K envs x 100 agents x 200 + GAE(0.99, 0.95) over the store (NEXT-N2)"),
 }
 
 
@@ -109,6 +114,17 @@ def workload_probs(w: Workload) -> np.ndarray:
     if w.env == "surface":
         return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, float(np.log(0.025)))
     return gaussian_params(w.n_envs, w.n_agents, w.act_dim, 0.0, 0.0)
+
+
+def gae_inputs(T: int, E: int, A: int, seed: int = SEED, with_trunc: bool = False):
+    """NEXT-N2 given inputs of GAE (reading R30): values [T, E, A], bootstrap [E, A] and,
+    optionally, terminal values v_trunc [T, E, A] (float32) -- value estimates of the scale
+    of CartPole returns (mean 10, std 5; SPEC S:433 defaults gamma 0.99 give returns <= 100)."""
+    rng = np.random.default_rng(seed)
+    values = (10.0 + 5.0 * rng.standard_normal((T, E, A))).astype(np.float32)
+    boot = (10.0 + 5.0 * rng.standard_normal((E, A))).astype(np.float32)
+    vtr = (10.0 + 5.0 * rng.standard_normal((T, E, A))).astype(np.float32) if with_trunc else None
+    return values, boot, vtr
 
 
 def policy_weights(D: int, H: int, N: int, seed: int = SEED, scale: float = 1.0) -> np.ndarray:
