@@ -76,6 +76,13 @@ class ws_gae_args(C.Structure):
                 ("adv", C.c_void_p), ("ret", C.c_void_p)]
 
 
+class ws_a2c_args(C.Structure):
+    _fields_ = [("obs_dim", C.c_int32), ("hidden", C.c_int32), ("n_actions", C.c_int32), ("rows", C.c_int64),
+                ("params", C.c_void_p), ("obs", C.c_void_p), ("act", C.c_void_p), ("adv", C.c_void_p),
+                ("ret", C.c_void_p), ("moments", C.c_void_p), ("batch", C.c_double), ("c_v", C.c_float),
+                ("c_e", C.c_float), ("workspace", C.c_void_p), ("grad", C.c_void_p), ("loss", C.c_void_p)]
+
+
 _SIGS = {
     "ws_config_init": (C.c_int, [C.POINTER(ws_config)]),
     "ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -100,6 +107,14 @@ _SIGS = {
     "ws_gae": (C.c_int, [C.POINTER(ws_gae_args), C.c_void_p]),
     "ws_gae_store": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float,
                                C.c_void_p, C.c_void_p]),
+    "ws_a2c_n_params": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32]),
+    "ws_a2c_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
+    "ws_ac_values": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
+                               C.c_void_p]),
+    "ws_a2c_moments": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ws_a2c_grad": (C.c_int, [C.POINTER(ws_a2c_args), C.c_void_p]),
+    "ws_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
+                          C.c_float, C.c_float, C.c_float, C.c_float, C.c_void_p, C.c_void_p]),
     "ws_peer_export": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_attach": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.POINTER(ws_ipc_handle)]),
     "ws_peer_detach": (C.c_int, [C.c_void_p]),

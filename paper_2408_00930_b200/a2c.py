@@ -1,0 +1,178 @@
+"""NEXT-N2: on-device A2C training over the GPU-resident roll-out store (include/ws.h
+"NEXT-N2: A2C update", DESIGN reading R31; SPEC a2c_update S:402-406, train S:419;
+P:41 "supports actor-critic algorithms", "roll-outs, action inference, reset and
+training" in one GPU-resident store, P:106 / P:122 "zero data transfer").
+
+Argument marshalling only: every arithmetic step runs in libws's kernels --
+ws_rollout_policy (roll-out with in-kernel policy inference), ws_ac_values (critic),
+ws_gae_store (advantages over the store, in place), ws_a2c_moments / ws_a2c_grad
+(normalised-advantage actor-critic gradient) and ws_adam (clip + Adam).  Data parallel:
+each rank trains on its replica shard; the two fp64 moments and the gradient are summed
+across ranks with torch.distributed (NCCL on GPUs), so every rank applies the same update.
+"""
+from __future__ import annotations
+
+import ctypes as C
+from typing import Optional
+
+import torch
+import torch.distributed as dist
+
+from . import _abi
+from ._abi import WSError, check, lib
+from .env import Env
+
+
+def n_params(obs_dim: int, hidden: int, n_actions: int) -> int:
+    return int(lib().ws_a2c_n_params(obs_dim, hidden, n_actions))
+
+
+def workspace(obs_dim: int, hidden: int, n_actions: int, device) -> torch.Tensor:
+    nbytes = int(lib().ws_a2c_workspace_bytes(obs_dim, hidden, n_actions))
+    if nbytes == 0:
+        raise WSError(_abi.INVALID_ARGUMENT, f"unsupported network shape D={obs_dim} H={hidden} n={n_actions}")
+    return torch.empty(nbytes, dtype=torch.uint8, device=device)
+
+
+def _s(stream: Optional[torch.cuda.Stream], t: torch.Tensor):
+    st = stream if stream is not None else torch.cuda.current_stream(t.device)
+    return C.c_void_p(st.cuda_stream)
+
+
+def _f32(name, t, n=None):
+    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous() or (n is not None and t.numel() != n):
+        raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 device tensor" +
+                      (f" with {n} elements" if n is not None else ""))
+
+
+def ac_values(params: torch.Tensor, obs: torch.Tensor, obs_dim: int, hidden: int, n_actions: int,
+              out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """V(o) of every row of obs (ws_ac_values) -> float32 [rows]."""
+    rows = obs.numel() // obs_dim
+    _f32("params", params, n_params(obs_dim, hidden, n_actions))
+    _f32("obs", obs, rows * obs_dim)
+    out = torch.empty(rows, dtype=torch.float32, device=obs.device) if out is None else out
+    check(lib().ws_ac_values(params.data_ptr(), obs_dim, hidden, n_actions, obs.data_ptr(), rows, out.data_ptr(),
+                             _s(stream, obs)))
+    return out
+
+
+def moments(x: torch.Tensor, ws: torch.Tensor, out: Optional[torch.Tensor] = None, stream=None) -> torch.Tensor:
+    """(sum x, sum x^2) in fp64 (ws_a2c_moments) -> float64 [2] device tensor."""
+    _f32("x", x)
+    out = torch.empty(2, dtype=torch.float64, device=x.device) if out is None else out
+    check(lib().ws_a2c_moments(x.data_ptr(), x.numel(), out.data_ptr(), ws.data_ptr(), _s(stream, x)))
+    return out
+
+
+def a2c_grad(params, obs, act, adv, ret, mom, batch: float, obs_dim: int, hidden: int, n_actions: int,
+             c_v: float, c_e: float, ws: torch.Tensor, grad: Optional[torch.Tensor] = None,
+             loss: Optional[torch.Tensor] = None, stream=None):
+    """This shard's gradient of the S:405 loss (ws_a2c_grad) -> (grad f32 [P], loss f64 [3])."""
+    rows = adv.numel()
+    P = n_params(obs_dim, hidden, n_actions)
+    _f32("params", params, P)
+    _f32("obs", obs, rows * obs_dim)
+    _f32("adv", adv, rows)
+    _f32("ret", ret, rows)
+    if act.dtype != torch.int32 or not act.is_contiguous() or act.numel() != rows:
+        raise WSError(_abi.INVALID_ARGUMENT, "act: contiguous int32 with one entry per row")
+    grad = torch.empty(P, dtype=torch.float32, device=adv.device) if grad is None else grad
+    loss = torch.empty(3, dtype=torch.float64, device=adv.device) if loss is None else loss
+    a = _abi.ws_a2c_args(obs_dim, hidden, n_actions, rows, params.data_ptr(), obs.data_ptr(), act.data_ptr(),
+                         adv.data_ptr(), ret.data_ptr(), mom.data_ptr(), float(batch), c_v, c_e, ws.data_ptr(),
+                         grad.data_ptr(), loss.data_ptr())
+    check(lib().ws_a2c_grad(C.byref(a), _s(stream, adv)))
+    return grad, loss
+
+
+def adam(params, grad, m, v, step: int, lr: float, beta1: float = 0.9, beta2: float = 0.999, eps: float = 1e-8,
+         max_norm: float = 0.0, grad_norm: Optional[torch.Tensor] = None, stream=None):
+    """Clip + one Adam step in place (ws_adam)."""
+    n = params.numel()
+    for name, t in (("params", params), ("grad", grad), ("m", m), ("v", v)):
+        _f32(name, t, n)
+    check(lib().ws_adam(params.data_ptr(), grad.data_ptr(), m.data_ptr(), v.data_ptr(), n, step, lr, beta1, beta2,
+                        eps, max_norm, None if grad_norm is None else grad_norm.data_ptr(), _s(stream, params)))
+
+
+def init_params(obs_dim: int, hidden: int, n_actions: int, seed: int = 0, device=None) -> torch.Tensor:
+    """Initial weights: W1 ~ N(0, 1/D), W2 ~ N(0, 0.01^2/H) (near-uniform policy), wv ~ N(0, 1/H),
+    zero biases; seeded on the host, copied once to the device."""
+    g = torch.Generator().manual_seed(seed)
+    D, H, N = obs_dim, hidden, n_actions
+    parts = [torch.randn(D * H, generator=g) / D ** 0.5, torch.zeros(H),
+             torch.randn(H * N, generator=g) * (0.01 / H ** 0.5), torch.zeros(N),
+             torch.randn(H, generator=g) / H ** 0.5, torch.zeros(1)]
+    return torch.cat(parts).float().to(device)
+
+
+class A2C:
+    """Synchronous advantage actor-critic on one Env (one rank's replica shard).
+
+    iteration(T): T fused roll-out steps with in-kernel policy inference, then one update
+    consuming the store in place (no copy of obs / act / rew / done anywhere)."""
+
+    def __init__(self, env: Env, hidden: int = 64, *, lr: float = 1e-3, gamma: float = 0.99, lam: float = 0.95,
+                 c_v: float = 0.5, c_e: float = 0.01, max_norm: float = 0.5, beta1: float = 0.9,
+                 beta2: float = 0.999, eps: float = 1e-8, seed: int = 0, params: Optional[torch.Tensor] = None,
+                 group: Optional[dist.ProcessGroup] = None):
+        info = env.info()
+        if int(info.n_agents) != 1 or int(info.n_actions) < 1:
+            raise WSError(_abi.INVALID_ARGUMENT, "A2C: single-agent discrete envs (cartpole, acrobot, dummy)")
+        self.env, self.H = env, hidden
+        self.D, self.N, self.E = int(info.obs_dim), int(info.n_actions), int(info.n_envs)
+        self.P = n_params(self.D, hidden, self.N)
+        dev = env.device
+        self.params = (init_params(self.D, hidden, self.N, seed, dev) if params is None
+                       else params.detach().to(dev, torch.float32).contiguous().clone())
+        if self.params.numel() != self.P:
+            raise WSError(_abi.INVALID_ARGUMENT, f"params: {self.P} floats")
+        self.m = torch.zeros_like(self.params)
+        self.v = torch.zeros_like(self.params)
+        self.ws = workspace(self.D, hidden, self.N, dev)
+        self.grad = torch.empty_like(self.params)
+        self.loss = torch.zeros(3, dtype=torch.float64, device=dev)
+        self.mom = torch.zeros(2, dtype=torch.float64, device=dev)
+        self.grad_norm = torch.zeros(1, dtype=torch.float32, device=dev)
+        self.bootstrap = torch.empty(self.E, dtype=torch.float32, device=dev)
+        self.hp = dict(lr=lr, gamma=gamma, lam=lam, c_v=c_v, c_e=c_e, max_norm=max_norm, beta1=beta1, beta2=beta2,
+                       eps=eps)
+        self.group = group
+        self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
+        self.step = 0
+        self._values = None
+
+    def _allreduce(self, t: torch.Tensor):
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
+
+    def update(self, T: int):
+        """One A2C update on store slots [0, T) (already rolled out with self.params)."""
+        env, D, H, N, hp = self.env, self.D, self.H, self.N, self.hp
+        s = env.stream
+        with torch.cuda.stream(s):
+            buf = env.buffers()
+            rows = T * self.E
+            obs = buf["obs"][:T].reshape(rows * D)
+            act = buf["act"][:T].reshape(rows)
+            if self._values is None or self._values.numel() != rows:
+                self._values = torch.empty(rows, dtype=torch.float32, device=env.device)
+            ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
+            ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
+            adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
+                                     hp["gamma"], hp["lam"])
+            moments(adv.view(-1), self.ws, out=self.mom, stream=s)
+            self._allreduce(self.mom)
+            a2c_grad(self.params, obs, act, adv.view(-1), ret.view(-1), self.mom, float(rows * self.world), D, H,
+                     N, hp["c_v"], hp["c_e"], self.ws, grad=self.grad, loss=self.loss, stream=s)
+            self._allreduce(self.grad)
+            self.step += 1
+            adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
+                 hp["max_norm"], grad_norm=self.grad_norm, stream=s)
+        self._adv = adv  # alive until the stream consumed it
+
+    def iteration(self, T: int):
+        """Roll out T steps with the current policy, then update (train)."""
+        self.env.rollout_policy(T, self.params, self.H)
+        self.update(T)

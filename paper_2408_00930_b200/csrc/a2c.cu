@@ -1,0 +1,498 @@
+// a2c.cu -- NEXT-N2: on-device actor-critic (A2C) update over the time-major roll-out
+// store, on sm_100a (include/ws.h "NEXT-N2: A2C update"; SPEC a2c_update S:402-406; P:41
+// "supports actor-critic algorithms"; DESIGN reading R31).
+//
+// Network (R29 policy + value head on the shared hidden layer):
+//   h = relu(W1^T o + b1), logits = W2^T h + b2, pi = softmax(logits), V = wv^T h + bv
+// Loss: -mean(log pi(a|o) A_hat) + c_v mean((V - R)^2) - c_e mean(Ent), with
+//   dL/dlogit_j = (A_hat/B)(pi_j - [j = a]) + (c_e/B) pi_j (log pi_j + Ent)
+//   dL/dV = 2 c_v (V - R) / B,  dL/dz_k = [z_k > 0] (sum_j W2[k][j] dL/dlogit_j + wv_k dL/dV)
+//
+// Kernels (all on the FMA pipe: the contractions here are [B x D] x [D x H] with D <= 6 and
+// [B x H] x [H x n] with n <= 5 -- K or N far below a tensor-core tile -- and the weight
+// gradients are reductions over B = T*E rows):
+//  - k_ac_values<D,H>: thread per row, weights broadcast from shared memory, H*(D+1) FMA.
+//  - k_moments / k_moments_final: fp64 sum and sum of squares, fixed grid -> deterministic.
+//  - k_a2c_grad<D,H,N>: persistent CTAs of 128 threads walk 128-row tiles.  Phase A: thread
+//    per row -- forward (h kept in shared memory, row stride H+1: conflict-free both ways),
+//    softmax / entropy / value, dL/dlogit and dL/dV, then dL/dz.  Phase B: the weight
+//    gradients are contractions over the tile's rows; warp w takes rows w, w+4, ..., lane l
+//    owns hidden units l (+32): per row it reads h and dz (2 x H/32 conflict-free loads) and
+//    the row's o / dlogit / dV (broadcast float4 loads) and accumulates D+1+N+1 FMA chains
+//    per unit in registers across all tiles.  The CTA reduces its 4 warps in a fixed order
+//    and writes one fp64 partial row; k_grad_final sums the rows in fixed order.
+//  - k_adam: one CTA: fp64 norm (fixed tree), clip, bias-corrected Adam in fp64, fp32 store.
+#include <cuda_runtime.h>
+
+#include <algorithm>
+#include <cmath>
+#include <cstdint>
+
+#include "../../include/ws.h"
+
+namespace {
+
+constexpr int kTile = 128;       // rows per tile == threads per CTA of k_a2c_grad
+constexpr int kWarps = kTile / 32;
+constexpr int kMaxGrid = 1184;   // 148 SMs x 8: bound of the partial-row workspace
+constexpr int kMomBlocks = 296;  // fixed grid of k_moments (order depends only on n)
+
+struct Layout {
+  int D, H, N, oW1, ob1, oW2, ob2, owv, obv, P;
+};
+
+__host__ __device__ inline Layout layout(int D, int H, int N) {
+  Layout L;
+  L.D = D; L.H = H; L.N = N;
+  L.oW1 = 0;
+  L.ob1 = D * H;
+  L.oW2 = L.ob1 + H;
+  L.ob2 = L.oW2 + H * N;
+  L.owv = L.ob2 + N;
+  L.obv = L.owv + H;
+  L.P = L.obv + 1;
+  return L;
+}
+
+bool supported(int D, int H, int N) {
+  return (D == 4 || D == 6) && (H == 32 || H == 64) && (N == 2 || N == 3 || N == 5);
+}
+
+__device__ __forceinline__ void load_params(float* sp, const float* params, int P) {
+  for (int i = threadIdx.x; i < P; i += blockDim.x) sp[i] = __ldg(params + i);
+}
+
+// ------------------------------------------------------------------------------ values
+template <int D, int H>
+__global__ void __launch_bounds__(256) k_ac_values(const float* __restrict__ params, int N,
+                                                   const float* __restrict__ obs, int64_t rows,
+                                                   float* __restrict__ values) {
+  extern __shared__ float sp[];
+  const Layout L = layout(D, H, N);
+  load_params(sp, params, L.P);
+  __syncthreads();
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
+    float o[D];
+#pragma unroll
+    for (int d = 0; d < D; ++d) o[d] = __ldg(obs + r * D + d);
+    float v = sp[L.obv];
+#pragma unroll 16
+    for (int k = 0; k < H; ++k) {
+      float z = sp[L.ob1 + k];
+#pragma unroll
+      for (int d = 0; d < D; ++d) z = fmaf(sp[L.oW1 + d * H + k], o[d], z);
+      v = fmaf(sp[L.owv + k], fmaxf(z, 0.0f), v);
+    }
+    __stcs(values + r, v);
+  }
+}
+
+// ------------------------------------------------------------------------------ moments
+__global__ void __launch_bounds__(256) k_moments(const float* __restrict__ x, int64_t n, double* __restrict__ part) {
+  __shared__ double s1[256], s2[256];
+  double a = 0.0, b = 0.0;
+  const int64_t stride = (int64_t)gridDim.x * blockDim.x;
+  for (int64_t i = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; i < n; i += stride) {
+    const double v = (double)__ldg(x + i);
+    a += v;
+    b = fma(v, v, b);
+  }
+  s1[threadIdx.x] = a;
+  s2[threadIdx.x] = b;
+  __syncthreads();
+  for (int w = 128; w > 0; w >>= 1) {
+    if (threadIdx.x < w) {
+      s1[threadIdx.x] += s1[threadIdx.x + w];
+      s2[threadIdx.x] += s2[threadIdx.x + w];
+    }
+    __syncthreads();
+  }
+  if (threadIdx.x == 0) {
+    part[2 * blockIdx.x] = s1[0];
+    part[2 * blockIdx.x + 1] = s2[0];
+  }
+}
+
+__global__ void k_moments_final(const double* __restrict__ part, int nb, double* __restrict__ out) {
+  if (threadIdx.x < 2) {
+    double s = 0.0;
+    for (int b = 0; b < nb; ++b) s += part[2 * b + threadIdx.x];
+    out[threadIdx.x] = s;
+  }
+}
+
+// ------------------------------------------------------------------------------ gradient
+struct GradDev {
+  const float* params;
+  const float* obs;
+  const int32_t* act;
+  const float* adv;
+  const float* ret;
+  const double* moments;
+  double batch;
+  float c_v, c_e;
+  int64_t rows;
+  double* partial;  // [gridDim.x][P + 3]
+};
+
+template <int D, int H, int N>
+struct GradSmem {
+  static constexpr int kP = D * H + H + H * N + N + H + 1;
+  static constexpr int kPpad = (kP + 3) & ~3;
+  static constexpr int kRow = H + 1;                // padded row of hs / dzs
+  static constexpr int kHs = kPpad;                 // offsets in floats
+  static constexpr int kDzs = kHs + kTile * kRow;
+  static constexpr int kOs = (kDzs + kTile * kRow + 3) & ~3;
+  static constexpr int kGs = kOs + kTile * 8;
+  static constexpr int kFloats = kGs + kTile * 8;
+  static constexpr size_t kBytes = (size_t)kFloats * sizeof(float);
+};
+
+template <int D, int H, int N>
+__global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
+  using S = GradSmem<D, H, N>;
+  constexpr Layout L{D, H, N, 0, D * H, D * H + H, D * H + H + H * N, D * H + H + H * N + N,
+                     D * H + H + H * N + N + H, S::kP};
+  constexpr int KP = H / 32;  // hidden units per lane in phase B
+  extern __shared__ __align__(16) float sm[];
+  float* sp = sm;
+  float* hs = sm + S::kHs;
+  float* dzs = sm + S::kDzs;
+  float* os = sm + S::kOs;
+  float* gs = sm + S::kGs;
+  load_params(sp, g.params, S::kP);
+
+  // normalisation (R31): mu, sigma over the global batch; skipped when sigma < 1e-8
+  const double mu = g.moments[0] / g.batch;
+  const double var = fmax(g.moments[1] / g.batch - mu * mu, 0.0);
+  const double sigma = sqrt(var);
+  const bool norm = sigma >= 1e-8;
+  const double inv_sigma = norm ? 1.0 / sigma : 1.0;
+  const float invB = (float)(1.0 / g.batch);
+  const float ce_b = g.c_e * invB;
+  const float cv2_b = 2.0f * g.c_v * invB;
+
+  const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
+  float aW1[KP][D], ab1[KP], aW2[KP][N], awv[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+#pragma unroll
+    for (int d = 0; d < D; ++d) aW1[q][d] = 0.0f;
+#pragma unroll
+    for (int j = 0; j < N; ++j) aW2[q][j] = 0.0f;
+    ab1[q] = 0.0f;
+    awv[q] = 0.0f;
+  }
+  float ab2[N], abv = 0.0f, lpol = 0.0f, lval = 0.0f, lent = 0.0f;
+#pragma unroll
+  for (int j = 0; j < N; ++j) ab2[j] = 0.0f;
+
+  const int64_t n_tiles = (g.rows + kTile - 1) / kTile;
+  for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
+    const int64_t base = tile * kTile;
+    const int nrow = (int)(g.rows - base < kTile ? g.rows - base : kTile);
+    __syncthreads();  // params loaded / previous tile's phase B done
+    // tile of observations: nrow * D contiguous floats -> os rows of 8
+    const float* ob = g.obs + base * D;
+    for (int i = tid; i < nrow * D; i += kTile) os[(i / D) * 8 + (i % D)] = __ldg(ob + i);
+    __syncthreads();
+
+    // ---- phase A: thread per row
+    const int s = tid;
+    float dl[N], dv = 0.0f;
+#pragma unroll
+    for (int j = 0; j < N; ++j) dl[j] = 0.0f;
+    float* hrow = hs + s * S::kRow;
+    if (s < nrow) {
+      const int64_t r = base + s;
+      const int a = __ldg(g.act + r);
+      const float A = __ldg(g.adv + r);
+      const float R = __ldg(g.ret + r);
+      float o[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) o[d] = os[s * 8 + d];
+      float l[N], v = sp[L.obv];
+#pragma unroll
+      for (int j = 0; j < N; ++j) l[j] = sp[L.ob2 + j];
+#pragma unroll 8
+      for (int k = 0; k < H; ++k) {
+        float z = sp[L.ob1 + k];
+#pragma unroll
+        for (int d = 0; d < D; ++d) z = fmaf(sp[L.oW1 + d * H + k], o[d], z);
+        const float h = fmaxf(z, 0.0f);
+        hrow[k] = h;
+#pragma unroll
+        for (int j = 0; j < N; ++j) l[j] = fmaf(sp[L.oW2 + k * N + j], h, l[j]);
+        v = fmaf(sp[L.owv + k], h, v);
+      }
+      if (a >= 0 && a < N) {
+        float m = l[0];
+#pragma unroll
+        for (int j = 1; j < N; ++j) m = fmaxf(m, l[j]);
+        float e[N], S = 0.0f;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          e[j] = expf(l[j] - m);
+          S += e[j];
+        }
+        const float lS = logf(S), invS = 1.0f / S;
+        float lp[N], p[N], ent = 0.0f, lpa = 0.0f;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          lp[j] = (l[j] - m) - lS;
+          p[j] = e[j] * invS;
+          ent -= p[j] * lp[j];
+          if (j == a) lpa = lp[j];
+        }
+        const float Ah = norm ? (float)(((double)A - mu) * inv_sigma) : A;
+        const float Ab = Ah * invB;
+#pragma unroll
+        for (int j = 0; j < N; ++j) dl[j] = Ab * (p[j] - (j == a ? 1.0f : 0.0f)) + ce_b * p[j] * (lp[j] + ent);
+        dv = cv2_b * (v - R);
+        lpol -= lpa * Ab;
+        lval += g.c_v * invB * (v - R) * (v - R);
+        lent -= ce_b * ent;
+#pragma unroll
+        for (int j = 0; j < N; ++j) ab2[j] += dl[j];
+        abv += dv;
+      }
+#pragma unroll 8
+      for (int k = 0; k < H; ++k) {
+        float dh = sp[L.owv + k] * dv;
+#pragma unroll
+        for (int j = 0; j < N; ++j) dh = fmaf(sp[L.oW2 + k * N + j], dl[j], dh);
+        dzs[s * S::kRow + k] = hrow[k] > 0.0f ? dh : 0.0f;
+      }
+    }
+    {
+      float4* g4 = reinterpret_cast<float4*>(gs + s * 8);
+      float t[8];
+#pragma unroll
+      for (int j = 0; j < 8; ++j) t[j] = 0.0f;
+#pragma unroll
+      for (int j = 0; j < N; ++j) t[j] = dl[j];
+      t[N] = dv;
+      g4[0] = make_float4(t[0], t[1], t[2], t[3]);
+      g4[1] = make_float4(t[4], t[5], t[6], t[7]);
+    }
+    __syncthreads();
+
+    // ---- phase B: contractions over the tile's rows; warp w takes rows w, w + 4, ...
+    for (int r = warp; r < nrow; r += kWarps) {
+      const float4 o0 = reinterpret_cast<const float4*>(os + r * 8)[0];
+      const float4 o1 = reinterpret_cast<const float4*>(os + r * 8)[1];
+      const float4 g0 = reinterpret_cast<const float4*>(gs + r * 8)[0];
+      const float4 g1 = reinterpret_cast<const float4*>(gs + r * 8)[1];
+      const float ov[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
+      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+#pragma unroll
+      for (int q = 0; q < KP; ++q) {
+        const int k = lane + 32 * q;
+        const float h = hs[r * S::kRow + k];
+        const float dz = dzs[r * S::kRow + k];
+#pragma unroll
+        for (int d = 0; d < D; ++d) aW1[q][d] = fmaf(ov[d], dz, aW1[q][d]);
+        ab1[q] += dz;
+#pragma unroll
+        for (int j = 0; j < N; ++j) aW2[q][j] = fmaf(h, gv[j], aW2[q][j]);
+        awv[q] = fmaf(h, gv[N], awv[q]);
+      }
+    }
+  }
+  __syncthreads();
+
+  // ---- CTA reduction in a fixed order: per-warp unit partials, per-thread bias / loss terms
+  double* out = g.partial + (size_t)blockIdx.x * (S::kP + 3);
+  float* red = hs;  // [kWarps][P] (P <= kTile * kRow)
+  for (int i = tid; i < kWarps * S::kP; i += kTile) red[i] = 0.0f;
+  __syncthreads();
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    const int k = lane + 32 * q;
+    float* rw = red + warp * S::kP;
+#pragma unroll
+    for (int d = 0; d < D; ++d) rw[L.oW1 + d * H + k] = aW1[q][d];
+    rw[L.ob1 + k] = ab1[q];
+#pragma unroll
+    for (int j = 0; j < N; ++j) rw[L.oW2 + k * N + j] = aW2[q][j];
+    rw[L.owv + k] = awv[q];
+  }
+  float* th = dzs;  // [kTile][N + 4]: per-thread b2, bv and loss terms
+  {
+    float* t = th + tid * (N + 4);
+#pragma unroll
+    for (int j = 0; j < N; ++j) t[j] = ab2[j];
+    t[N] = abv;
+    t[N + 1] = lpol;
+    t[N + 2] = lval;
+    t[N + 3] = lent;
+  }
+  __syncthreads();
+  for (int i = tid; i < S::kP; i += kTile) {
+    if (i >= L.ob2 && i < L.ob2 + N) continue;
+    if (i == L.obv) continue;
+    double s = 0.0;
+#pragma unroll
+    for (int w = 0; w < kWarps; ++w) s += (double)red[w * S::kP + i];
+    out[i] = s;
+  }
+  if (tid < N + 4) {
+    double s = 0.0;
+    for (int t = 0; t < kTile; ++t) s += (double)th[t * (N + 4) + tid];
+    const int dst = tid < N ? L.ob2 + tid : (tid == N ? L.obv : S::kP + (tid - N - 1));
+    out[dst] = s;
+  }
+}
+
+__global__ void __launch_bounds__(128) k_grad_final(const double* __restrict__ part, int nb, int P,
+                                                    float* __restrict__ grad, double* __restrict__ loss) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= P + 3) return;
+  double s = 0.0;
+  for (int b = 0; b < nb; ++b) s += part[(size_t)b * (P + 3) + c];
+  if (c < P) grad[c] = (float)s;
+  else if (loss) loss[c - P] = s;
+}
+
+// ------------------------------------------------------------------------------ Adam
+__global__ void __launch_bounds__(1024) k_adam(float* __restrict__ params, const float* __restrict__ grad,
+                                               float* __restrict__ m, float* __restrict__ v, int n, int step,
+                                               double lr, double b1, double b2, double eps, double max_norm,
+                                               float* __restrict__ grad_norm) {
+  __shared__ double red[1024];
+  double s = 0.0;
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double x = (double)grad[i];
+    s = fma(x, x, s);
+  }
+  red[threadIdx.x] = s;
+  __syncthreads();
+  for (int w = 512; w > 0; w >>= 1) {
+    if ((int)threadIdx.x < w) red[threadIdx.x] += red[threadIdx.x + w];
+    __syncthreads();
+  }
+  const double norm = sqrt(red[0]);
+  if (threadIdx.x == 0 && grad_norm) *grad_norm = (float)norm;
+  const double scale = (max_norm > 0.0 && norm > max_norm) ? max_norm / norm : 1.0;
+  const double c1 = 1.0 - pow(b1, (double)step), c2 = 1.0 - pow(b2, (double)step);
+  for (int i = threadIdx.x; i < n; i += blockDim.x) {
+    const double gi = (double)grad[i] * scale;
+    const double mi = b1 * (double)m[i] + (1.0 - b1) * gi;
+    const double vi = b2 * (double)v[i] + (1.0 - b2) * gi * gi;
+    const double upd = lr * (mi / c1) / (sqrt(vi / c2) + eps);
+    params[i] = (float)((double)params[i] - upd);
+    m[i] = (float)mi;
+    v[i] = (float)vi;
+  }
+}
+
+// ------------------------------------------------------------------------------ dispatch
+template <int D, int H, int N>
+cudaError_t launch_grad_t(const GradDev& g, cudaStream_t s, int* nb_out) {
+  using S = GradSmem<D, H, N>;
+  static int grid_cap = 0;  // CTAs per device at full residency (same for every B200)
+  cudaError_t e = cudaSuccess;
+  if (!grid_cap) {
+    e = cudaFuncSetAttribute(k_a2c_grad<D, H, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kBytes);
+    if (e) return e;
+    int dev = 0, sms = 0, per_sm = 0;
+    if ((e = cudaGetDevice(&dev))) return e;
+    if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_a2c_grad<D, H, N>, kTile, S::kBytes))) return e;
+    grid_cap = std::max(1, std::min(kMaxGrid, sms * std::max(per_sm, 1)));
+  }
+  const int64_t tiles = (g.rows + kTile - 1) / kTile;
+  const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, grid_cap));
+  k_a2c_grad<D, H, N><<<nb, kTile, S::kBytes, s>>>(g);
+  *nb_out = nb;
+  return cudaGetLastError();
+}
+
+template <int D, int H>
+cudaError_t launch_grad_dh(int N, const GradDev& g, cudaStream_t s, int* nb) {
+  switch (N) {
+    case 2: return launch_grad_t<D, H, 2>(g, s, nb);
+    case 3: return launch_grad_t<D, H, 3>(g, s, nb);
+    default: return launch_grad_t<D, H, 5>(g, s, nb);
+  }
+}
+
+cudaError_t launch_grad(int D, int H, int N, const GradDev& g, cudaStream_t s, int* nb) {
+  if (D == 4) return H == 32 ? launch_grad_dh<4, 32>(N, g, s, nb) : launch_grad_dh<4, 64>(N, g, s, nb);
+  return H == 32 ? launch_grad_dh<6, 32>(N, g, s, nb) : launch_grad_dh<6, 64>(N, g, s, nb);
+}
+
+template <int D, int H>
+cudaError_t launch_values_t(const float* params, int N, const float* obs, int64_t rows, float* values,
+                            cudaStream_t s) {
+  const Layout L = layout(D, H, N);
+  const int64_t blocks = std::min<int64_t>((rows + 255) / 256, 148 * 8);
+  k_ac_values<D, H><<<(int)blocks, 256, L.P * sizeof(float), s>>>(params, N, obs, rows, values);
+  return cudaGetLastError();
+}
+
+}  // namespace
+
+extern "C" {
+
+int32_t ws_a2c_n_params(int32_t D, int32_t H, int32_t N) {
+  if (D < 1 || H < 1 || N < 1) return 0;
+  return layout(D, H, N).P;
+}
+
+size_t ws_a2c_workspace_bytes(int32_t D, int32_t H, int32_t N) {
+  if (!supported(D, H, N)) return 0;
+  const size_t g = (size_t)kMaxGrid * (layout(D, H, N).P + 3) * sizeof(double);
+  const size_t m = (size_t)kMomBlocks * 2 * sizeof(double);
+  return std::max(g, m);
+}
+
+ws_status ws_ac_values(const float* params, int32_t D, int32_t H, int32_t N, const float* obs, int64_t rows,
+                       float* values, void* stream) {
+  if (!supported(D, H, N) || !params || rows < 0 || (rows > 0 && (!obs || !values))) return WS_ERR_INVALID_ARGUMENT;
+  if (rows == 0) return WS_OK;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  cudaError_t e;
+  if (D == 4) e = H == 32 ? launch_values_t<4, 32>(params, N, obs, rows, values, s)
+                          : launch_values_t<4, 64>(params, N, obs, rows, values, s);
+  else e = H == 32 ? launch_values_t<6, 32>(params, N, obs, rows, values, s)
+                   : launch_values_t<6, 64>(params, N, obs, rows, values, s);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_a2c_moments(const float* x, int64_t n, double* out, void* workspace, void* stream) {
+  if (!x || n < 1 || !out || !workspace) return WS_ERR_INVALID_ARGUMENT;
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  double* part = static_cast<double*>(workspace);
+  k_moments<<<kMomBlocks, 256, 0, s>>>(x, n, part);
+  k_moments_final<<<1, 32, 0, s>>>(part, kMomBlocks, out);
+  return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_a2c_grad(const ws_a2c_args* a, void* stream) {
+  if (!a || !supported(a->obs_dim, a->hidden, a->n_actions) || a->rows < 1 || !a->params || !a->obs || !a->act ||
+      !a->adv || !a->ret || !a->moments || !(a->batch > 0.0) || !a->workspace || !a->grad)
+    return WS_ERR_INVALID_ARGUMENT;
+  GradDev g{a->params, a->obs, a->act, a->adv, a->ret, a->moments, a->batch, a->c_v, a->c_e, a->rows,
+            static_cast<double*>(a->workspace)};
+  cudaStream_t s = static_cast<cudaStream_t>(stream);
+  int nb = 0;
+  cudaError_t e = launch_grad(a->obs_dim, a->hidden, a->n_actions, g, s, &nb);
+  if (e) return WS_ERR_CUDA;
+  const int P = layout(a->obs_dim, a->hidden, a->n_actions).P;
+  k_grad_final<<<(P + 3 + 127) / 128, 128, 0, s>>>(g.partial, nb, P, a->grad, a->loss);
+  return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
+}
+
+ws_status ws_adam(float* params, const float* grad, float* m, float* v, int32_t n, int32_t step, float lr,
+                  float beta1, float beta2, float eps, float max_norm, float* grad_norm, void* stream) {
+  if (!params || !grad || !m || !v || n < 1 || n > 65536 || step < 1 || !(lr >= 0.0f) || !(beta1 >= 0.0f && beta1 < 1.0f) ||
+      !(beta2 >= 0.0f && beta2 < 1.0f) || !(eps >= 0.0f))
+    return WS_ERR_INVALID_ARGUMENT;
+  k_adam<<<1, 1024, 0, static_cast<cudaStream_t>(stream)>>>(params, grad, m, v, n, step, lr, beta1, beta2, eps,
+                                                             max_norm, grad_norm);
+  return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
+}
+
+}  // extern "C"

@@ -122,3 +122,32 @@ def test_gae_argument_validation_without_gpu():
         a = _abi.ws_gae_args(**{**good, **bad})
         assert L.ws_gae(C.byref(a), None) == _abi.INVALID_ARGUMENT, bad
     assert L.ws_gae_store(None, 4, None, None, None, 0.99, 0.95, None, None) == _abi.INVALID_ARGUMENT
+
+
+def test_a2c_argument_validation_without_gpu():
+    """NEXT-N2 A2C entry points (ws.h, R31): sizes and argument checks before any CUDA call."""
+    L = P.lib()
+    assert L.ws_a2c_n_params(4, 64, 2) == 4 * 64 + 64 + 64 * 2 + 2 + 64 + 1
+    assert L.ws_a2c_n_params(6, 32, 3) == 6 * 32 + 32 + 32 * 3 + 3 + 32 + 1
+    assert L.ws_a2c_workspace_bytes(4, 64, 2) >= 8 * (L.ws_a2c_n_params(4, 64, 2) + 3)
+    for shape in ((5, 64, 2), (4, 48, 2), (4, 64, 4), (0, 64, 2)):
+        assert L.ws_a2c_workspace_bytes(*shape) == 0, shape
+    fake = 256
+    assert L.ws_ac_values(fake, 4, 48, 2, fake, 10, fake, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_ac_values(None, 4, 64, 2, fake, 10, fake, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_ac_values(fake, 4, 64, 2, None, 0, None, None) == _abi.OK  # empty batch: nothing to do
+    assert L.ws_a2c_moments(fake, 0, fake, fake, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_a2c_moments(None, 5, fake, fake, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_a2c_grad(None, None) == _abi.INVALID_ARGUMENT
+    good = dict(obs_dim=4, hidden=64, n_actions=2, rows=10, params=fake, obs=fake, act=fake, adv=fake, ret=fake,
+                moments=fake, batch=10.0, c_v=0.5, c_e=0.01, workspace=fake, grad=fake, loss=None)
+    for bad in (dict(rows=0), dict(hidden=16), dict(obs_dim=3), dict(n_actions=4), dict(params=None),
+                dict(obs=None), dict(act=None), dict(adv=None), dict(ret=None), dict(moments=None),
+                dict(batch=0.0), dict(batch=float("nan")), dict(workspace=None), dict(grad=None)):
+        a = _abi.ws_a2c_args(**{**good, **bad})
+        assert L.ws_a2c_grad(C.byref(a), None) == _abi.INVALID_ARGUMENT, bad
+    adam_ok = (fake, fake, fake, fake, 10, 1, 1e-3, 0.9, 0.999, 1e-8, 0.5, None, None)
+    for i, v in ((4, 0), (4, 70000), (5, 0), (6, -1.0), (7, 1.0), (8, 1.0), (9, -1e-8), (0, None), (1, None)):
+        args = list(adam_ok)
+        args[i] = v
+        assert L.ws_adam(*args) == _abi.INVALID_ARGUMENT, (i, v)

@@ -1,0 +1,238 @@
+"""NEXT-N2 on the GPU: the A2C update kernels (ws_ac_values, ws_a2c_moments, ws_a2c_grad,
+ws_adam; DESIGN R31) against the fp64 oracle (oracle/a2c.py), and one full training
+iteration (roll-out with in-kernel inference -> values -> GAE over the store -> gradient ->
+Adam) against the oracle's roll-out and update.
+
+Tolerances (derived in DESIGN section 4, R31): the GPU evaluates each row in fp32 (every
+product and sum rounded, u = 2^-24) and accumulates per lane in fp32; the oracle is exact
+fp64.  Each gradient component is compared against its own absolute-value scale
+S_i = sum over rows of |each factor| (the same chain rule with absolute values): a row's
+relative error is a few tens of u and the fp32 accumulation adds ~sqrt(rows per lane) u,
+so |g - g_oracle| <= 2e-5 S_i (1e-4 S_i at 10M rows) leaves a margin of > 10x over the
+observed error while a dropped term, wrong sign or transposed block fails by O(S_i)."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import wsinputs as W
+from oracle import a2c as OA
+
+pytestmark = pytest.mark.gpu
+SEED = W.SEED
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2408_00930_b200 as P
+    from paper_2408_00930_b200 import a2c
+    return a2c
+
+
+def grad_scale(params, obs, act, Ah, ret, D, H, N, c_v, c_e, B):
+    """Per-component absolute-value scale of the gradient sum (tolerance denominator)."""
+    W1, b1, W2, b2, wv, bv = OA.unpack(params, D, H, N)
+    z, h, logits, pi, V = OA.forward(params, obs, D, H, N)
+    o = np.abs(np.asarray(obs, np.float64).reshape(-1, D))
+    a = np.asarray(act).astype(np.int64)
+    ok = ((a >= 0) & (a < N)).astype(np.float64)
+    a = np.clip(a, 0, N - 1)
+    onehot = np.zeros_like(pi)
+    onehot[np.arange(len(a)), a] = 1.0
+    logpi = np.log(np.maximum(pi, 1e-300))
+    ent = -(pi * logpi).sum(axis=1)
+    dlog = (np.abs(Ah) / B)[:, None] * np.abs(pi - onehot) + (c_e / B) * pi * (np.abs(logpi) + ent[:, None])
+    dlog *= ok[:, None]
+    dV = 2 * c_v * np.abs(V - np.asarray(ret, np.float64)) / B * ok
+    dz = (dlog @ np.abs(W2).T + dV[:, None] * np.abs(wv)[None, :]) * (z > 0)
+    return np.concatenate([(o.T @ dz).ravel(), dz.sum(0), (h.T @ dlog).ravel(), dlog.sum(0), h.T @ dV, [dV.sum()]])
+
+
+def loss_scale(params, obs, act, Ah, ret, D, H, N, c_v, c_e):
+    """Absolute-value scales of the three loss terms: V - R cancels in fp32, so the value
+    term is compared against c_v mean((|V| + |R|)^2)."""
+    _, _, logits, pi, V = OA.forward(params, obs, D, H, N)
+    a = np.asarray(act).astype(np.int64)
+    ok = (a >= 0) & (a < N)
+    B = len(a)
+    lp = np.log(np.maximum(pi, 1e-300))
+    ent = -(pi * lp).sum(1)
+    pol = (np.abs(lp[np.arange(B), np.clip(a, 0, N - 1)]) * np.abs(Ah))[ok].sum() / B
+    val = c_v * ((np.abs(V) + np.abs(np.asarray(ret, np.float64))) ** 2)[ok].sum() / B
+    return np.array([pol, val, c_e * np.abs(ent[ok]).sum() / B + 1e-30])
+
+
+def oracle_grad_chunked(params, obs, act, Ah, ret, D, H, N, c_v, c_e, B, chunk=400_000):
+    g = 0.0
+    s = 0.0
+    L = np.zeros(3)
+    for i in range(0, len(act), chunk):
+        sl = slice(i, i + chunk)
+        g = g + OA.grad(params, obs[sl], act[sl], Ah[sl], ret[sl], D, H, N, c_v, c_e, batch=B)
+        s = s + grad_scale(params, obs[sl], act[sl], Ah[sl], ret[sl], D, H, N, c_v, c_e, B)
+        L += np.array(OA.loss(params, obs[sl], act[sl], Ah[sl], ret[sl], D, H, N, c_v, c_e, batch=B)[1:])
+    return g, s, L
+
+
+def cuda(x):
+    return torch.from_numpy(np.ascontiguousarray(x)).cuda()
+
+
+@pytest.mark.parametrize("D,H,N,rows", [(4, 64, 2, 3001), (6, 32, 3, 1000), (4, 32, 5, 129), (6, 64, 3, 77)])
+def test_values_match_oracle(P, D, H, N, rows):
+    params = W.a2c_params(D, H, N, seed=3)
+    obs, _, _, _ = W.a2c_batch(rows, D, N, seed=4)
+    v = P.ac_values(cuda(params), cuda(obs).view(-1), D, H, N).cpu().numpy()
+    ref = OA.values(params, obs, D, H, N)
+    W1, b1, W2, b2, wv, bv = OA.unpack(params, D, H, N)
+    h = OA.forward(params, obs, D, H, N)[1]
+    scale = np.abs(bv) + h @ np.abs(wv) + 1.0
+    assert np.all(np.abs(v - ref) <= 1e-5 * scale)
+
+
+def test_moments_exact_for_fp32_inputs(P):
+    x = (np.random.default_rng(5).standard_normal(1_000_003) * 3 + 1).astype(np.float32)
+    ws = P.workspace(4, 64, 2, "cuda")
+    m = P.moments(cuda(x), ws).cpu().numpy()
+    s1, s2 = OA.moments(x)
+    assert abs(m[0] - s1) <= 1e-12 * np.abs(x).sum()
+    assert abs(m[1] - s2) <= 1e-12 * s2
+
+
+@pytest.mark.parametrize("D,H,N,rows,inv", [(4, 64, 2, 5000, 0.0), (4, 64, 2, 1283, 0.1), (6, 32, 3, 2000, 0.05),
+                                            (6, 64, 3, 700, 0.0), (4, 32, 5, 300, 0.02), (4, 64, 5, 1, 0.0)])
+def test_grad_matches_oracle(P, D, H, N, rows, inv):
+    params = W.a2c_params(D, H, N, seed=11)
+    obs, act, adv, ret = W.a2c_batch(rows, D, N, seed=12, invalid_frac=inv)
+    c_v, c_e = 0.5, 0.02
+    ws = P.workspace(D, H, N, "cuda")
+    tadv = cuda(adv)
+    mom = P.moments(tadv, ws)
+    g, L = P.a2c_grad(cuda(params), cuda(obs).view(-1), cuda(act), tadv, cuda(ret), mom, float(rows), D, H, N,
+                      c_v, c_e, ws)
+    g = g.cpu().numpy().astype(np.float64)
+    L = L.cpu().numpy()
+    Ah = OA.normalize(adv)
+    ref = OA.grad(params, obs, act, Ah, ret, D, H, N, c_v, c_e)
+    scale = grad_scale(params, obs, act, Ah, ret, D, H, N, c_v, c_e, rows)
+    bad = np.abs(g - ref) > 2e-5 * scale + 1e-12
+    assert not bad.any(), (np.flatnonzero(bad)[:10], g[bad][:5], ref[bad][:5])
+    Lref = OA.loss(params, obs, act, Ah, ret, D, H, N, c_v, c_e)
+    assert np.all(np.abs(L - np.array(Lref[1:])) <= 2e-5 * loss_scale(params, obs, act, Ah, ret, D, H, N, c_v, c_e))
+
+
+def test_grad_sharded_batch_sums_to_global(P):
+    """DP: two shards with the global moments and batch size -> gradients that sum to the
+    single-shard gradient (up to fp32 accumulation)."""
+    D, H, N, rows = 4, 64, 2, 4000
+    params = cuda(W.a2c_params(D, H, N, seed=21))
+    obs, act, adv, ret = (cuda(x) for x in W.a2c_batch(rows, D, N, seed=22))
+    ws = P.workspace(D, H, N, "cuda")
+    mom = P.moments(adv, ws)
+    g_all, _ = P.a2c_grad(params, obs.view(-1), act, adv, ret, mom, float(rows), D, H, N, 0.5, 0.01, ws)
+    g_all = g_all.clone()
+    h = rows // 2
+    m1, m2 = P.moments(adv[:h].contiguous(), ws).clone(), P.moments(adv[h:].contiguous(), ws).clone()
+    mg = m1 + m2
+    g1, _ = P.a2c_grad(params, obs[:h].reshape(-1).contiguous(), act[:h].contiguous(), adv[:h].contiguous(),
+                       ret[:h].contiguous(), mg, float(rows), D, H, N, 0.5, 0.01, ws)
+    g1 = g1.clone()
+    g2, _ = P.a2c_grad(params, obs[h:].reshape(-1).contiguous(), act[h:].contiguous(), adv[h:].contiguous(),
+                       ret[h:].contiguous(), mg, float(rows), D, H, N, 0.5, 0.01, ws)
+    np.testing.assert_allclose((g1 + g2).cpu().numpy(), g_all.cpu().numpy(), rtol=1e-4, atol=1e-7)
+
+
+def test_grad_full_c2_batch(P):
+    """BASELINE configs[1] scale: 10K replicas x 1000 steps = 10M rows, H = 64, in the
+    launch configuration the bench uses; the oracle recomputes the whole sum in fp64 chunks."""
+    D, H, N, rows = 4, 64, 2, 10_000_000
+    params = W.a2c_params(D, H, N, seed=31)
+    obs, act, adv, ret = W.a2c_batch(rows, D, N, seed=32, invalid_frac=0.001)
+    ws = P.workspace(D, H, N, "cuda")
+    tadv = cuda(adv)
+    mom = P.moments(tadv, ws)
+    g, L = P.a2c_grad(cuda(params), cuda(obs).view(-1), cuda(act), tadv, cuda(ret), mom, float(rows), D, H, N,
+                      0.5, 0.01, ws)
+    g = g.cpu().numpy().astype(np.float64)
+    Ah = OA.normalize(adv)
+    ref, scale, Lref = oracle_grad_chunked(params, obs, act, Ah, ret, D, H, N, 0.5, 0.01, rows)
+    bad = np.abs(g - ref) > 1e-4 * scale + 1e-12
+    assert not bad.any(), (np.flatnonzero(bad)[:10], g[bad][:5], ref[bad][:5])
+    np.testing.assert_allclose(L.cpu().numpy(), Lref, rtol=1e-4)
+
+
+def test_adam_matches_oracle(P):
+    """Three clip + Adam steps on identical gradients: parameters within fp32 storage rounding
+    of the fp64 oracle; one step with a large gradient exercises the clip."""
+    n = 709
+    r = np.random.default_rng(41)
+    p = r.standard_normal(n).astype(np.float32)
+    tp, tm, tv = cuda(p), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda")
+    po, mo, vo = p.astype(np.float64), np.zeros(n), np.zeros(n)
+    gn = torch.zeros(1, device="cuda")
+    for k, sc in ((1, 5.0), (2, 0.01), (3, 0.2)):
+        g = (r.standard_normal(n) * sc).astype(np.float32)
+        P.adam(tp, cuda(g), tm, tv, k, 1e-3, 0.9, 0.999, 1e-8, 0.5, grad_norm=gn)
+        assert gn.item() == pytest.approx(np.linalg.norm(g.astype(np.float64)), rel=1e-6)
+        po, mo, vo = OA.adam(po, OA.clip(g, 0.5), mo, vo, k, 1e-3)
+        np.testing.assert_allclose(tp.cpu().numpy(), po, rtol=0, atol=1e-6 * (1 + np.abs(po)).max())
+    # zero gradient with zero moments: parameters unchanged
+    q = cuda(p)
+    P.adam(q, torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"), torch.zeros(n, device="cuda"), 1, 1e-3)
+    assert torch.equal(q, cuda(p))
+
+
+@pytest.mark.parametrize("env,H,E,T", [("cartpole", 64, 300, 128), ("acrobot", 32, 130, 64)])
+def test_training_iteration_matches_oracle(P, env, H, E, T):
+    """One A2C iteration: the store equals the oracle's policy roll-out bit for bit (R29), the
+    critic / GAE / gradient agree with the fp64 oracle on that store, and the parameters
+    after the step equal the oracle's Adam applied to the GPU's gradient."""
+    import paper_2408_00930_b200 as WS
+    D, N = {"cartpole": (4, 2), "acrobot": (6, 3)}[env]
+    params = W.a2c_params(D, H, N, seed=51, scale=1.0)
+    g = WS.Env(E, 1, env, SEED, t_capacity=T)
+    tr = P.A2C(g, H, params=torch.from_numpy(params), lr=1e-3, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01,
+               max_norm=0.5)
+    tr.iteration(T)
+    g.synchronize()
+    o = O.Batch(env, E, 1, SEED, t_capacity=T)
+    assert o.rollout_policy(T, params[:D * H + H + H * N + N], H, n_threads=8) == 0
+    buf = {k: (v.cpu().numpy() if v is not None else None) for k, v in g.buffers().items()}
+    for k in ("obs", "act", "rew", "done", "obs_live"):
+        assert np.array_equal(buf[k][:T] if k != "obs_live" else buf[k], o.array(k)[:T] if k != "obs_live"
+                              else o.array(k)), k
+    obs = o.array("obs")[:T].reshape(-1, D)
+    act = o.array("act")[:T].reshape(-1)
+    vals = OA.values(params, obs, D, H, N).reshape(T, E)
+    boot = OA.values(params, o.array("obs_live").reshape(-1, D), D, H, N)
+    adv, ret = O.gae(o.array("rew")[:T].reshape(T, E), o.array("done")[:T], vals, boot, 0.99, 0.95, f64=True)
+    Ah = OA.normalize(adv)
+    ref = OA.grad(params, obs, act, Ah, ret.ravel(), D, H, N, 0.5, 0.01)
+    scale = grad_scale(params, obs, act, Ah, ret.ravel(), D, H, N, 0.5, 0.01, T * E)
+    gg = tr.grad.cpu().numpy().astype(np.float64)
+    # advantages pass through an fp32 recursion of up to ~T terms: 1e-4 of the scale
+    bad = np.abs(gg - ref) > 1e-4 * scale + 1e-10
+    assert not bad.any(), (np.flatnonzero(bad)[:10], gg[bad][:5], ref[bad][:5])
+    p1, _, _ = OA.adam(params.astype(np.float64), OA.clip(gg, 0.5), np.zeros_like(gg), np.zeros_like(gg), 1, 1e-3)
+    np.testing.assert_allclose(tr.params.cpu().numpy(), p1, rtol=0, atol=2e-6 * (1 + np.abs(p1)).max())
+    assert tr.step == 1
+
+
+def test_cartpole_learns(P):
+    """The paper's convergence claim in miniature (Fig 2b): A2C on 2048 CartPole replicas
+    raises the mean episode length well above the random policy's ~22 steps."""
+    import paper_2408_00930_b200 as WS
+    E, T, H = 2048, 64, 64
+    g = WS.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    tr = P.A2C(g, H, lr=3e-3, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5, seed=1)
+    lengths = []
+    for it in range(300):
+        tr.iteration(T)
+        st = g.stats_f64(T).cpu().numpy().sum(0)
+        if st[0] > 0:
+            lengths.append(st[2] / st[0])
+    first, last = np.mean(lengths[:5]), np.mean(lengths[-20:])
+    print(f"cartpole A2C: mean episode length {first:.1f} -> {last:.1f}")
+    assert first < 40 and last > 3 * first

@@ -136,3 +136,25 @@ def policy_weights(D: int, H: int, N: int, seed: int = SEED, scale: float = 1.0)
     W2 = rng.standard_normal((H, N)) * (scale / np.sqrt(H))
     b2 = rng.standard_normal(N) * 0.1 * scale
     return np.concatenate([W1.ravel(), b1, W2.ravel(), b2]).astype(np.float32)
+
+
+def a2c_params(D: int, H: int, N: int, seed: int = SEED, scale: float = 1.0) -> np.ndarray:
+    """NEXT-N2 actor-critic parameters (reading R31): the R29 policy weights followed by a
+    value head wv [H] | bv [1] (float32)."""
+    rng = np.random.default_rng(seed + 1)
+    head = np.concatenate([rng.standard_normal(H) * (scale / np.sqrt(H)), [10.0 * scale]])
+    return np.concatenate([policy_weights(D, H, N, seed, scale), head]).astype(np.float32)
+
+
+def a2c_batch(rows: int, D: int, N: int, seed: int = SEED, invalid_frac: float = 0.0):
+    """NEXT-N2 given inputs of one update: obs [rows, D] (CartPole-scale N(0, 0.5^2)),
+    actions [rows] int32 (a fraction set to -1, the R13 invalid-row marker), advantages
+    (N(0.5, 2^2)) and returns (N(10, 5^2)) float32."""
+    rng = np.random.default_rng(seed + 2)
+    obs = (0.5 * rng.standard_normal((rows, D))).astype(np.float32)
+    act = rng.integers(0, N, rows).astype(np.int32)
+    if invalid_frac > 0:
+        act[rng.random(rows) < invalid_frac] = -1
+    adv = (0.5 + 2.0 * rng.standard_normal(rows)).astype(np.float32)
+    ret = (10.0 + 5.0 * rng.standard_normal(rows)).astype(np.float32)
+    return obs, act, adv, ret
