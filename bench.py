@@ -137,6 +137,19 @@ def oracle_rollout(b, w, T, probs, cores):
         st = b.rollout_policy(T, pol[1], pol[0], n_threads=cores)
     else:
         st = b.rollout(T, probs, n_threads=cores)
+    if w.params.get("a2c"):  # NEXT-N2: the oracle's A2C update on the slots just written
+        import oracle as O
+        from oracle import a2c as OA
+        H, params = pol
+        D = OBS_DIM[w.env]
+        N = w.n_actions
+        obs = b.array("obs")[:T].reshape(-1, D)
+        vals = OA.values(params, obs, D, H, N).reshape(T, w.n_envs)
+        boot = OA.values(params, b.array("obs_live").reshape(-1, D), D, H, N)
+        adv, ret = O.gae(b.array("rew")[:T].reshape(T, w.n_envs), b.array("done")[:T], vals, boot, 0.99, 0.95,
+                         f64=True)
+        z = np.zeros(params.size)
+        OA.update(params, z, z, 1, obs, b.array("act")[:T].reshape(-1), adv.ravel(), ret.ravel(), D, H, N, lr=1e-4)
     gae = w.params.get("gae")
     if gae:
         import oracle as O
@@ -256,8 +269,15 @@ def main():
         g_out = (torch.empty((T, E, A), dtype=torch.float32, device=dev),
                  torch.empty((T, E, A), dtype=torch.float32, device=dev))
 
+    trainer = None
+    if w.params.get("a2c"):  # NEXT-N2: every step is one A2C iteration (roll-out + update)
+        from paper_2408_00930_b200.a2c import A2C
+        trainer = A2C(env, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5)
+
     def gpu_rollout(e_obj):
-        if pol:
+        if trainer is not None and e_obj is env:
+            trainer.iteration(T)
+        elif pol:
             e_obj.rollout_policy(T, pol_w, pol[0])
         else:
             e_obj.rollout(T, probs)
@@ -309,6 +329,8 @@ def main():
     if st != 0:
         raise RuntimeError(f"libws reported status {st} during the timed region")
     launches = env.info().launches - launches0
+    if trainer is not None:  # handle-free A2C kernels per step: values x2, moments + final, grad + final, Adam
+        launches += 7 * args.steps
     ktimes = env.kernel_times()
     env.enable_kernel_timing(False)
     clk = clocks.stop() if not args.ncu else {}
@@ -331,6 +353,14 @@ def main():
     kern_ms = [dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)]
     diag_times = env.kernel_times()
     env.enable_kernel_timing(False)
+    upd_ms = None
+    if trainer is not None:  # the update alone (critic, GAE, moments, gradient, Adam)
+        for k in range(n_diag):
+            dev_ev[2 * k].record(stream)
+            trainer.update(T)
+            dev_ev[2 * k + 1].record(stream)
+        torch.cuda.synchronize(dev)
+        upd_ms = sum(dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)) / n_diag
 
     t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
     if world > 1:
@@ -384,6 +414,10 @@ def main():
             hbm_view = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
             roofline.update({"bound": "alu", "achieved": round(tf, 3), "peak": round(fp32_peak, 1),
                              "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "hbm_view": hbm_view})
+    if trainer is not None:
+        roofline["a2c_update"] = {"ms": round(upd_ms, 4), "rows": E * A * T,
+                                  "note": "ac_values x2 + gae + moments + gradient + clip/Adam, diagnostic pass",
+                                  "loss_last": [round(x, 6) for x in trainer.loss.cpu().tolist()]}
     if gae:
         n_gae, gae_ms = ktimes.get("gae", (0, 0.0))
         g_ach = gae_bytes / (gae_ms / 1e3) / 1e9 if gae_ms > 0 else 0.0
@@ -407,7 +441,20 @@ def main():
             # end to end through the public API with HOST buffers: pinned probs H2D + stats D2H per step
             henv = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
                        param0=params[0], param1=params[1], block_size=args.block)
-            if pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
+            if trainer is not None:  # NEXT-N2: one training iteration per step, loss + stats back to the host
+                from paper_2408_00930_b200.a2c import A2C
+                htr = A2C(henv, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01,
+                          max_norm=0.5)
+                hl = torch.empty(3, dtype=torch.float64).pin_memory()
+                hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+
+                def host_step():
+                    htr.iteration(T)
+                    hl.copy_(htr.loss, non_blocking=True)
+                    hs.copy_(henv.buffers()["stats"][:T], non_blocking=True)
+                    torch.cuda.synchronize(dev)
+                h2d = 0
+            elif pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
                 hw = torch.from_numpy(pol[1]).pin_memory()
                 dw = torch.empty_like(hw, device=dev)
                 hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
@@ -434,8 +481,9 @@ def main():
                 host_step()
             e2e_s = time.perf_counter() - t0
             e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
-                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(T * 4 * 8),
-                   "note": "rank 0, " + ("ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(T * 4 * 8) + (24 if trainer is not None else 0),
+                   "note": "rank 0, " + ("A2C iteration, loss + stats to pinned host memory" if trainer is not None
+                                         else "ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
                            + (" + ws_gae_store" if gae else "")
                            + ", host wall clock"}
             henv.close()

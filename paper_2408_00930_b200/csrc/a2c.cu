@@ -58,33 +58,62 @@ bool supported(int D, int H, int N) {
   return (D == 4 || D == 6) && (H == 32 || H == 64) && (N == 2 || N == 3 || N == 5);
 }
 
-__device__ __forceinline__ void load_params(float* sp, const float* params, int P) {
-  for (int i = threadIdx.x; i < P; i += blockDim.x) sp[i] = __ldg(params + i);
+// Per-hidden-unit weight record in shared memory: W1[0..D-1][k], b1[k], wv[k], W2[k][0..N-1],
+// padded to 16 B, so the thread-per-row loops fetch a unit's weights with 2-3 broadcast
+// LDS.128 instead of D+N+2 scalar loads.
+template <int D, int N>
+struct Rec {
+  static constexpr int kB1 = D, kWv = D + 1, kW2 = D + 2;
+  static constexpr int kLen = (D + 2 + N + 3) & ~3;
+};
+
+template <int D, int H, int N>
+__device__ __forceinline__ void load_records(float* wrec, const float* params) {
+  using RC = Rec<D, N>;
+  const Layout L = layout(D, H, N);
+  for (int i = threadIdx.x; i < H * RC::kLen; i += blockDim.x) {
+    const int k = i / RC::kLen, f = i % RC::kLen;
+    float x = 0.0f;
+    if (f < D) x = __ldg(params + L.oW1 + f * H + k);
+    else if (f == RC::kB1) x = __ldg(params + L.ob1 + k);
+    else if (f == RC::kWv) x = __ldg(params + L.owv + k);
+    else if (f < RC::kW2 + N) x = __ldg(params + L.oW2 + k * N + (f - RC::kW2));
+    wrec[i] = x;
+  }
 }
 
 // ------------------------------------------------------------------------------ values
-template <int D, int H>
-__global__ void __launch_bounds__(256) k_ac_values(const float* __restrict__ params, int N,
-                                                   const float* __restrict__ obs, int64_t rows,
-                                                   float* __restrict__ values) {
-  extern __shared__ float sp[];
-  const Layout L = layout(D, H, N);
-  load_params(sp, params, L.P);
+template <int D, int H, int N>
+__global__ void __launch_bounds__(256) k_ac_values(const float* __restrict__ params, const float* __restrict__ obs,
+                                                   int64_t rows, float* __restrict__ values) {
+  using RC = Rec<D, N>;
+  constexpr int kLoad = (D + 2 + 3) / 4;  // float4s holding W1[.][k], b1[k], wv[k]
+  extern __shared__ __align__(16) float wrec[];
+  load_records<D, H, N>(wrec, params);
+  const float bv = __ldg(params + layout(D, H, N).obv);
   __syncthreads();
   const int64_t stride = (int64_t)gridDim.x * blockDim.x;
   for (int64_t r = (int64_t)blockIdx.x * blockDim.x + threadIdx.x; r < rows; r += stride) {
     float o[D];
 #pragma unroll
     for (int d = 0; d < D; ++d) o[d] = __ldg(obs + r * D + d);
-    float v = sp[L.obv];
-#pragma unroll 16
-    for (int k = 0; k < H; ++k) {
-      float z = sp[L.ob1 + k];
+    float v0 = bv, v1 = 0.0f;
 #pragma unroll
-      for (int d = 0; d < D; ++d) z = fmaf(sp[L.oW1 + d * H + k], o[d], z);
-      v = fmaf(sp[L.owv + k], fmaxf(z, 0.0f), v);
+    for (int k = 0; k < H; ++k) {
+      float w[4 * kLoad];
+      const float4* rk = reinterpret_cast<const float4*>(wrec + k * RC::kLen);
+#pragma unroll
+      for (int c = 0; c < kLoad; ++c) {
+        const float4 t = rk[c];
+        w[4 * c] = t.x; w[4 * c + 1] = t.y; w[4 * c + 2] = t.z; w[4 * c + 3] = t.w;
+      }
+      float z = w[RC::kB1];
+#pragma unroll
+      for (int d = 0; d < D; ++d) z = fmaf(w[d], o[d], z);
+      if (k & 1) v1 = fmaf(w[RC::kWv], fmaxf(z, 0.0f), v1);
+      else v0 = fmaf(w[RC::kWv], fmaxf(z, 0.0f), v0);
     }
-    __stcs(values + r, v);
+    __stcs(values + r, v0 + v1);
   }
 }
 
@@ -139,29 +168,33 @@ struct GradDev {
 template <int D, int H, int N>
 struct GradSmem {
   static constexpr int kP = D * H + H + H * N + N + H + 1;
-  static constexpr int kPpad = (kP + 3) & ~3;
-  static constexpr int kRow = H + 1;                // padded row of hs / dzs
-  static constexpr int kHs = kPpad;                 // offsets in floats
-  static constexpr int kDzs = kHs + kTile * kRow;
-  static constexpr int kOs = (kDzs + kTile * kRow + 3) & ~3;
-  static constexpr int kGs = kOs + kTile * 8;
-  static constexpr int kFloats = kGs + kTile * 8;
+  static constexpr int kRec = Rec<D, N>::kLen;       // per-hidden-unit weight record
+  static constexpr int kOg = (D + N + 1 + 3) & ~3;   // per-row record: o, dL/dlogit, dL/dV
+  static constexpr int kHrow = H + 4;                // h row stride: 16-B rows, kHrow/4 odd
+  static constexpr int kW = 0;                       // [H][kRec]
+  static constexpr int kB2 = H * kRec;               // b2 [N], bv
+  static constexpr int kHs = kB2 + 8;                // [kTile][kHrow]
+  static constexpr int kOgs = kHs + kTile * kHrow;   // [kTile][kOg]
+  static constexpr int kFloats = kOgs + kTile * kOg;
   static constexpr size_t kBytes = (size_t)kFloats * sizeof(float);
+  static_assert((kHrow / 4) % 2 == 1, "conflict-free 16-B row stores");
+  static_assert(kTile * kHrow >= 4 * kP + kTile * (N + 4), "reduction scratch fits the h tile");
 };
 
 template <int D, int H, int N>
-__global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
+__global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
   using S = GradSmem<D, H, N>;
+  using RC = Rec<D, N>;
   constexpr Layout L{D, H, N, 0, D * H, D * H + H, D * H + H + H * N, D * H + H + H * N + N,
                      D * H + H + H * N + N + H, S::kP};
-  constexpr int KP = H / 32;  // hidden units per lane in phase B
+  constexpr int KP = H / 32;  // hidden units per lane in phase B (consecutive: k = KP*lane + q)
   extern __shared__ __align__(16) float sm[];
-  float* sp = sm;
+  float* wrec = sm + S::kW;
   float* hs = sm + S::kHs;
-  float* dzs = sm + S::kDzs;
-  float* os = sm + S::kOs;
-  float* gs = sm + S::kGs;
-  load_params(sp, g.params, S::kP);
+  float* ogs = sm + S::kOgs;
+  load_records<D, H, N>(wrec, g.params);
+  if (threadIdx.x < N) sm[S::kB2 + threadIdx.x] = __ldg(g.params + L.ob2 + threadIdx.x);
+  if (threadIdx.x == N) sm[S::kB2 + N] = __ldg(g.params + L.obv);
 
   // normalisation (R31): mu, sigma over the global batch; skipped when sigma < 1e-8
   const double mu = g.moments[0] / g.batch;
@@ -172,6 +205,7 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
   const float invB = (float)(1.0 / g.batch);
   const float ce_b = g.c_e * invB;
   const float cv2_b = 2.0f * g.c_v * invB;
+  const float cv_b = g.c_v * invB;
 
   const int tid = threadIdx.x, lane = tid & 31, warp = tid >> 5;
   float aW1[KP][D], ab1[KP], aW2[KP][N], awv[KP];
@@ -187,23 +221,29 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
   float ab2[N], abv = 0.0f, lpol = 0.0f, lval = 0.0f, lent = 0.0f;
 #pragma unroll
   for (int j = 0; j < N; ++j) ab2[j] = 0.0f;
+  __syncthreads();
+  // phase-B weights of this lane's hidden units, in registers for the whole kernel
+  float w2k[KP][N], wvk[KP];
+#pragma unroll
+  for (int q = 0; q < KP; ++q) {
+    const float* rk = wrec + (KP * lane + q) * S::kRec;
+    wvk[q] = rk[RC::kWv];
+#pragma unroll
+    for (int j = 0; j < N; ++j) w2k[q][j] = rk[RC::kW2 + j];
+  }
 
   const int64_t n_tiles = (g.rows + kTile - 1) / kTile;
   for (int64_t tile = blockIdx.x; tile < n_tiles; tile += gridDim.x) {
     const int64_t base = tile * kTile;
     const int nrow = (int)(g.rows - base < kTile ? g.rows - base : kTile);
-    __syncthreads();  // params loaded / previous tile's phase B done
-    // tile of observations: nrow * D contiguous floats -> os rows of 8
+    __syncthreads();  // previous tile's phase B done with hs / ogs
     const float* ob = g.obs + base * D;
-    for (int i = tid; i < nrow * D; i += kTile) os[(i / D) * 8 + (i % D)] = __ldg(ob + i);
+    for (int i = tid; i < nrow * D; i += kTile) ogs[(i / D) * S::kOg + (i % D)] = __ldg(ob + i);
     __syncthreads();
 
-    // ---- phase A: thread per row
+    // ---- phase A: thread per row: forward, softmax / entropy / value, dL/dlogit, dL/dV
     const int s = tid;
-    float dl[N], dv = 0.0f;
-#pragma unroll
-    for (int j = 0; j < N; ++j) dl[j] = 0.0f;
-    float* hrow = hs + s * S::kRow;
+    float* og = ogs + s * S::kOg;
     if (s < nrow) {
       const int64_t r = base + s;
       const int a = __ldg(g.act + r);
@@ -211,32 +251,61 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
       const float R = __ldg(g.ret + r);
       float o[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) o[d] = os[s * 8 + d];
-      float l[N], v = sp[L.obv];
+      for (int d = 0; d < D; ++d) o[d] = og[d];
+      float l0[N], l1[N], v0 = sm[S::kB2 + N], v1 = 0.0f;
 #pragma unroll
-      for (int j = 0; j < N; ++j) l[j] = sp[L.ob2 + j];
-#pragma unroll 8
-      for (int k = 0; k < H; ++k) {
-        float z = sp[L.ob1 + k];
-#pragma unroll
-        for (int d = 0; d < D; ++d) z = fmaf(sp[L.oW1 + d * H + k], o[d], z);
-        const float h = fmaxf(z, 0.0f);
-        hrow[k] = h;
-#pragma unroll
-        for (int j = 0; j < N; ++j) l[j] = fmaf(sp[L.oW2 + k * N + j], h, l[j]);
-        v = fmaf(sp[L.owv + k], h, v);
+      for (int j = 0; j < N; ++j) {
+        l0[j] = sm[S::kB2 + j];
+        l1[j] = 0.0f;
       }
+      float4* hrow = reinterpret_cast<float4*>(hs + s * S::kHrow);
+#pragma unroll 2
+      for (int kc = 0; kc < H; kc += 4) {
+        float h[4];
+#pragma unroll
+        for (int i = 0; i < 4; ++i) {
+          const int k = kc + i;
+          float w[RC::kLen];
+          const float4* rk = reinterpret_cast<const float4*>(wrec + k * S::kRec);
+#pragma unroll
+          for (int c = 0; c < RC::kLen / 4; ++c) {
+            const float4 t = rk[c];
+            w[4 * c] = t.x; w[4 * c + 1] = t.y; w[4 * c + 2] = t.z; w[4 * c + 3] = t.w;
+          }
+          float z = w[RC::kB1];
+#pragma unroll
+          for (int d = 0; d < D; ++d) z = fmaf(w[d], o[d], z);
+          h[i] = fmaxf(z, 0.0f);
+          if (i & 1) {
+#pragma unroll
+            for (int j = 0; j < N; ++j) l1[j] = fmaf(w[RC::kW2 + j], h[i], l1[j]);
+            v1 = fmaf(w[RC::kWv], h[i], v1);
+          } else {
+#pragma unroll
+            for (int j = 0; j < N; ++j) l0[j] = fmaf(w[RC::kW2 + j], h[i], l0[j]);
+            v0 = fmaf(w[RC::kWv], h[i], v0);
+          }
+        }
+        hrow[kc >> 2] = make_float4(h[0], h[1], h[2], h[3]);
+      }
+      float dl[N], dv = 0.0f;
+#pragma unroll
+      for (int j = 0; j < N; ++j) dl[j] = 0.0f;
       if (a >= 0 && a < N) {
+        float l[N];
+#pragma unroll
+        for (int j = 0; j < N; ++j) l[j] = l0[j] + l1[j];
+        const float v = v0 + v1;
         float m = l[0];
 #pragma unroll
         for (int j = 1; j < N; ++j) m = fmaxf(m, l[j]);
-        float e[N], S = 0.0f;
+        float e[N], Ssum = 0.0f;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
           e[j] = expf(l[j] - m);
-          S += e[j];
+          Ssum += e[j];
         }
-        const float lS = logf(S), invS = 1.0f / S;
+        const float lS = logf(Ssum), invS = 1.0f / Ssum;
         float lp[N], p[N], ent = 0.0f, lpa = 0.0f;
 #pragma unroll
         for (int j = 0; j < N; ++j) {
@@ -251,52 +320,50 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
         for (int j = 0; j < N; ++j) dl[j] = Ab * (p[j] - (j == a ? 1.0f : 0.0f)) + ce_b * p[j] * (lp[j] + ent);
         dv = cv2_b * (v - R);
         lpol -= lpa * Ab;
-        lval += g.c_v * invB * (v - R) * (v - R);
+        lval += cv_b * (v - R) * (v - R);
         lent -= ce_b * ent;
 #pragma unroll
         for (int j = 0; j < N; ++j) ab2[j] += dl[j];
         abv += dv;
       }
-#pragma unroll 8
-      for (int k = 0; k < H; ++k) {
-        float dh = sp[L.owv + k] * dv;
 #pragma unroll
-        for (int j = 0; j < N; ++j) dh = fmaf(sp[L.oW2 + k * N + j], dl[j], dh);
-        dzs[s * S::kRow + k] = hrow[k] > 0.0f ? dh : 0.0f;
-      }
-    }
-    {
-      float4* g4 = reinterpret_cast<float4*>(gs + s * 8);
-      float t[8];
-#pragma unroll
-      for (int j = 0; j < 8; ++j) t[j] = 0.0f;
-#pragma unroll
-      for (int j = 0; j < N; ++j) t[j] = dl[j];
-      t[N] = dv;
-      g4[0] = make_float4(t[0], t[1], t[2], t[3]);
-      g4[1] = make_float4(t[4], t[5], t[6], t[7]);
+      for (int j = 0; j < N; ++j) og[D + j] = dl[j];
+      og[D + N] = dv;
     }
     __syncthreads();
 
-    // ---- phase B: contractions over the tile's rows; warp w takes rows w, w + 4, ...
+    // ---- phase B: contractions over the tile's rows.  Warp w takes rows w, w + 4, ...; lane l
+    // owns hidden units KP*l .. KP*l+KP-1: dL/dz from its register weights, then D+1+N+1
+    // accumulations per unit.
     for (int r = warp; r < nrow; r += kWarps) {
-      const float4 o0 = reinterpret_cast<const float4*>(os + r * 8)[0];
-      const float4 o1 = reinterpret_cast<const float4*>(os + r * 8)[1];
-      const float4 g0 = reinterpret_cast<const float4*>(gs + r * 8)[0];
-      const float4 g1 = reinterpret_cast<const float4*>(gs + r * 8)[1];
-      const float ov[8] = {o0.x, o0.y, o0.z, o0.w, o1.x, o1.y, o1.z, o1.w};
-      const float gv[8] = {g0.x, g0.y, g0.z, g0.w, g1.x, g1.y, g1.z, g1.w};
+      float ogv[S::kOg];
+      const float4* og4 = reinterpret_cast<const float4*>(ogs + r * S::kOg);
+#pragma unroll
+      for (int c = 0; c < S::kOg / 4; ++c) {
+        const float4 t = og4[c];
+        ogv[4 * c] = t.x; ogv[4 * c + 1] = t.y; ogv[4 * c + 2] = t.z; ogv[4 * c + 3] = t.w;
+      }
+      float hv[KP];
+      if constexpr (KP == 2) {
+        const float2 t = reinterpret_cast<const float2*>(hs + r * S::kHrow)[lane];
+        hv[0] = t.x;
+        hv[1] = t.y;
+      } else {
+        hv[0] = hs[r * S::kHrow + lane];
+      }
+      const float dv = ogv[D + N];
 #pragma unroll
       for (int q = 0; q < KP; ++q) {
-        const int k = lane + 32 * q;
-        const float h = hs[r * S::kRow + k];
-        const float dz = dzs[r * S::kRow + k];
+        float dh = wvk[q] * dv;
 #pragma unroll
-        for (int d = 0; d < D; ++d) aW1[q][d] = fmaf(ov[d], dz, aW1[q][d]);
+        for (int j = 0; j < N; ++j) dh = fmaf(w2k[q][j], ogv[D + j], dh);
+        const float dz = hv[q] > 0.0f ? dh : 0.0f;
+#pragma unroll
+        for (int d = 0; d < D; ++d) aW1[q][d] = fmaf(ogv[d], dz, aW1[q][d]);
         ab1[q] += dz;
 #pragma unroll
-        for (int j = 0; j < N; ++j) aW2[q][j] = fmaf(h, gv[j], aW2[q][j]);
-        awv[q] = fmaf(h, gv[N], awv[q]);
+        for (int j = 0; j < N; ++j) aW2[q][j] = fmaf(hv[q], ogv[D + j], aW2[q][j]);
+        awv[q] = fmaf(hv[q], dv, awv[q]);
       }
     }
   }
@@ -304,12 +371,11 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
 
   // ---- CTA reduction in a fixed order: per-warp unit partials, per-thread bias / loss terms
   double* out = g.partial + (size_t)blockIdx.x * (S::kP + 3);
-  float* red = hs;  // [kWarps][P] (P <= kTile * kRow)
-  for (int i = tid; i < kWarps * S::kP; i += kTile) red[i] = 0.0f;
-  __syncthreads();
+  float* red = hs;                  // [kWarps][P]
+  float* th = hs + kWarps * S::kP;  // [kTile][N + 4]
 #pragma unroll
   for (int q = 0; q < KP; ++q) {
-    const int k = lane + 32 * q;
+    const int k = KP * lane + q;
     float* rw = red + warp * S::kP;
 #pragma unroll
     for (int d = 0; d < D; ++d) rw[L.oW1 + d * H + k] = aW1[q][d];
@@ -318,7 +384,6 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
     for (int j = 0; j < N; ++j) rw[L.oW2 + k * N + j] = aW2[q][j];
     rw[L.owv + k] = awv[q];
   }
-  float* th = dzs;  // [kTile][N + 4]: per-thread b2, bv and loss terms
   {
     float* t = th + tid * (N + 4);
 #pragma unroll
@@ -330,18 +395,17 @@ __global__ void __launch_bounds__(kTile) k_a2c_grad(const GradDev g) {
   }
   __syncthreads();
   for (int i = tid; i < S::kP; i += kTile) {
-    if (i >= L.ob2 && i < L.ob2 + N) continue;
-    if (i == L.obv) continue;
-    double s = 0.0;
+    if ((i >= L.ob2 && i < L.ob2 + N) || i == L.obv) continue;
+    double acc = 0.0;
 #pragma unroll
-    for (int w = 0; w < kWarps; ++w) s += (double)red[w * S::kP + i];
-    out[i] = s;
+    for (int w = 0; w < kWarps; ++w) acc += (double)red[w * S::kP + i];
+    out[i] = acc;
   }
   if (tid < N + 4) {
-    double s = 0.0;
-    for (int t = 0; t < kTile; ++t) s += (double)th[t * (N + 4) + tid];
+    double acc = 0.0;
+    for (int t = 0; t < kTile; ++t) acc += (double)th[t * (N + 4) + tid];
     const int dst = tid < N ? L.ob2 + tid : (tid == N ? L.obv : S::kP + (tid - N - 1));
-    out[dst] = s;
+    out[dst] = acc;
   }
 }
 
@@ -423,13 +487,21 @@ cudaError_t launch_grad(int D, int H, int N, const GradDev& g, cudaStream_t s, i
   return H == 32 ? launch_grad_dh<6, 32>(N, g, s, nb) : launch_grad_dh<6, 64>(N, g, s, nb);
 }
 
-template <int D, int H>
-cudaError_t launch_values_t(const float* params, int N, const float* obs, int64_t rows, float* values,
-                            cudaStream_t s) {
-  const Layout L = layout(D, H, N);
+template <int D, int H, int N>
+cudaError_t launch_values_t(const float* params, const float* obs, int64_t rows, float* values, cudaStream_t s) {
   const int64_t blocks = std::min<int64_t>((rows + 255) / 256, 148 * 8);
-  k_ac_values<D, H><<<(int)blocks, 256, L.P * sizeof(float), s>>>(params, N, obs, rows, values);
+  k_ac_values<D, H, N><<<(int)blocks, 256, H * Rec<D, N>::kLen * sizeof(float), s>>>(params, obs, rows, values);
   return cudaGetLastError();
+}
+
+template <int D, int H>
+cudaError_t launch_values_dh(int N, const float* params, const float* obs, int64_t rows, float* values,
+                             cudaStream_t s) {
+  switch (N) {
+    case 2: return launch_values_t<D, H, 2>(params, obs, rows, values, s);
+    case 3: return launch_values_t<D, H, 3>(params, obs, rows, values, s);
+    default: return launch_values_t<D, H, 5>(params, obs, rows, values, s);
+  }
 }
 
 }  // namespace
@@ -454,10 +526,10 @@ ws_status ws_ac_values(const float* params, int32_t D, int32_t H, int32_t N, con
   if (rows == 0) return WS_OK;
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   cudaError_t e;
-  if (D == 4) e = H == 32 ? launch_values_t<4, 32>(params, N, obs, rows, values, s)
-                          : launch_values_t<4, 64>(params, N, obs, rows, values, s);
-  else e = H == 32 ? launch_values_t<6, 32>(params, N, obs, rows, values, s)
-                   : launch_values_t<6, 64>(params, N, obs, rows, values, s);
+  if (D == 4) e = H == 32 ? launch_values_dh<4, 32>(N, params, obs, rows, values, s)
+                          : launch_values_dh<4, 64>(N, params, obs, rows, values, s);
+  else e = H == 32 ? launch_values_dh<6, 32>(N, params, obs, rows, values, s)
+                   : launch_values_dh<6, 64>(N, params, obs, rows, values, s);
   return e ? WS_ERR_CUDA : WS_OK;
 }
 

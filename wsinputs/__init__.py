@@ -47,6 +47,10 @@ CONFIGS = {
     # NEXT-N2: C2's roll-out followed by GAE over the store it wrote
     "C2G": Workload("C2G", "cartpole", 10000, 1, 1000, 2, 1, {"gae": (0.99, 0.95)},
                     note="CartPole-v1 10K envs x 1000 steps + GAE(0.99, 0.95) over the store (NEXT-N2)"),
+    # NEXT-N2: a full A2C iteration -- C2's roll-out with in-kernel inference of
+    # a 4-64-2 actor-critic, then critic values, GAE over the store, gradient, clip + Adam
+    "C2T": Workload("C2T", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64, "a2c": True},
+                    note="CartPole-v1 10K envs x 1000 steps + A2C update of a 4-64-2 actor-critic (NEXT-N2)"),
     "C4G": Workload("C4G", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10, "gae": (0.99, 0.95)},
                     note="tag 1K envs x 100 agents x 200 + GAE(0.99, 0.95) over the store (NEXT-N2)"),
 }
@@ -104,6 +108,8 @@ def workload_policy(w: Workload):
     if not H:
         return None
     D = {"cartpole": 4, "acrobot": 6, "dummy": 4}[w.env]
+    if w.params.get("a2c"):  # actor-critic: the policy prefix followed by the value head
+        return H, a2c_params(D, H, w.n_actions, seed=SEED, scale=1.0)
     return H, policy_weights(D, H, w.n_actions, seed=SEED, scale=2.0)
 
 
