@@ -274,8 +274,16 @@ def main():
         from paper_2408_00930_b200.a2c import A2C
         trainer = A2C(env, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5)
 
+    staged = w.params.get("staged")  # NEXT-N3: copy-based baseline pipeline
+    staged_rep = {}
+    if staged:
+        st_probs = torch.from_numpy(probs_host).pin_memory()
+        st_dst = env.host_store(T)
+
     def gpu_rollout(e_obj):
-        if trainer is not None and e_obj is env:
+        if staged and e_obj is env:
+            staged_rep.update(env.rollout_staged(T, st_probs, st_dst))
+        elif trainer is not None and e_obj is env:
             trainer.iteration(T)
         elif pol:
             e_obj.rollout_policy(T, pol_w, pol[0])
@@ -309,7 +317,7 @@ def main():
         time.sleep(0.3)
     # two CUDA events per step around the fused roll-out kernel only (libws ws_kernel_times):
     # the dominant kernel is timed live with the least perturbation of the timed loop
-    env.enable_kernel_timing(0 if args.no_kernel_timing else (3 if gae else 2))
+    env.enable_kernel_timing(0 if (args.no_kernel_timing or staged) else (3 if gae else 2))
     env.kernel_times()
     launches0 = env.info().launches
     ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
@@ -414,6 +422,17 @@ def main():
             hbm_view = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
             roofline.update({"bound": "alu", "achieved": round(tf, 3), "peak": round(fp32_peak, 1),
                              "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "hbm_view": hbm_view})
+    if staged:
+        # the same kernels one step at a time (diagnostic pass timing of the step kernel) and
+        # the transfer split of the last timed step
+        n_st, st_ms = diag_times.get("step", (0, 0.0))
+        sb = ROLLOUT_BYTES.get(w.env, 0) * E * A
+        ach = sb / (st_ms / 1e3) / 1e9 if st_ms > 0 else 0.0
+        roofline.update({"kernel": f"k_step_lane<{w.env}> (single step)", "kernel_ms": round(st_ms, 5),
+                         "launches_timed": n_st, "bytes_per_launch": sb, "achieved": round(ach, 1),
+                         "frac": round(ach / peak, 4), "other_kernels": {}})
+        roofline["staged_pipeline"] = {k: (round(v, 4) if "ms" in k else v) for k, v in staged_rep.items()}
+        roofline["staged_pipeline"]["transfer_share"] = round(staged_rep["transfer_ms"] / staged_rep["total_ms"], 4)
     if trainer is not None:
         roofline["a2c_update"] = {"ms": round(upd_ms, 4), "rows": E * A * T,
                                   "note": "ac_values x2 + gae + moments + gradient + clip/Adam, diagnostic pass",
@@ -454,6 +473,12 @@ def main():
                     hs.copy_(henv.buffers()["stats"][:T], non_blocking=True)
                     torch.cuda.synchronize(dev)
                 h2d = 0
+            elif staged:  # NEXT-N3: the staged pipeline is host-buffered by construction
+                hdst = henv.host_store(T)
+
+                def host_step():
+                    henv.rollout_staged(T, st_probs, hdst)
+                h2d = int(st_probs.numel() * 4 * T)
             elif pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
                 hw = torch.from_numpy(pol[1]).pin_memory()
                 dw = torch.empty_like(hw, device=dev)
@@ -480,9 +505,12 @@ def main():
             for _ in range(args.steps):
                 host_step()
             e2e_s = time.perf_counter() - t0
+            d2h = (int(sum(v.numel() * v.element_size() for v in hdst.values())) if staged
+                   else int(T * 4 * 8) + (24 if trainer is not None else 0))
             e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
-                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": int(T * 4 * 8) + (24 if trainer is not None else 0),
-                   "note": "rank 0, " + ("A2C iteration, loss + stats to pinned host memory" if trainer is not None
+                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+                   "note": "rank 0, " + ("ws_rollout_staged (per-step copies)" if staged else
+                                         "A2C iteration, loss + stats to pinned host memory" if trainer is not None
                                          else "ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
                            + (" + ws_gae_store" if gae else "")
                            + ", host wall clock"}

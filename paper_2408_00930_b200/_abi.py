@@ -83,6 +83,14 @@ class ws_a2c_args(C.Structure):
                 ("c_e", C.c_float), ("workspace", C.c_void_p), ("grad", C.c_void_p), ("loss", C.c_void_p)]
 
 
+class ws_host_store(C.Structure):
+    _fields_ = [(n, C.c_void_p) for n in ("obs", "act", "logp", "rew", "done")]
+
+
+class ws_staged_report(C.Structure):
+    _fields_ = [(n, C.c_double) for n in ("total_ms", "transfer_ms", "h2d_bytes", "d2h_bytes")]
+
+
 _SIGS = {
     "ws_config_init": (C.c_int, [C.POINTER(ws_config)]),
     "ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -95,6 +103,8 @@ _SIGS = {
     "ws_rollout": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64]),
     "ws_rollout_host": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                   C.POINTER(ws_stats)]),
+    "ws_rollout_staged": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
+                                    C.POINTER(ws_host_store), C.POINTER(ws_staged_report)]),
     "ws_get_buffers": (C.c_int, [C.c_void_p, C.POINTER(ws_buffers)]),
     "ws_get_info": (C.c_int, [C.c_void_p, C.POINTER(ws_info)]),
     "ws_synchronize": (C.c_int, [C.c_void_p]),

@@ -548,6 +548,86 @@ ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t
   return WS_OK;
 }
 
+ws_status ws_rollout_staged(ws_env* h, int32_t T, const float* host_probs, int64_t n_probs, int64_t row_stride,
+                            int64_t step_stride, const ws_host_store* dst, ws_staged_report* out) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1");
+  if (!host_probs || n_probs < 1 || row_stride < 0 || step_stride < 0 || !dst)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "host_probs / n_probs / strides / dst");
+  DeviceGuard g(h->device);
+  ws_status st = ensure_store(h, T);
+  if (st) return st;
+  if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity");
+  cudaError_t e = cudaSuccess;
+  if (h->staging_n < n_probs) {
+    if (h->staging) return fail(h, WS_ERR_INVALID_ARGUMENT, "n_probs grew beyond the first call's staging size");
+    h->staging = (float*)dev_alloc(h, (size_t)n_probs * sizeof(float), &e);
+    if (e) return cuda_fail(h, e, "alloc staging");
+    h->staging_n = n_probs;
+  }
+  const size_t EA = (size_t)h->E * h->A;
+  const size_t act_w = h->spec.n_actions ? 1 : (size_t)h->spec.act_dim;
+  struct Part { void* host; const void* dev; size_t bytes; };
+  const Part parts[5] = {
+      {dst->obs, h->obs, EA * h->spec.obs_dim * sizeof(float)},
+      {dst->act, h->act, EA * act_w * 4},
+      {dst->logp, h->logp, h->logp ? EA * sizeof(float) : 0},
+      {dst->rew, h->rew, EA * sizeof(float)},
+      {dst->done, h->done, (size_t)h->E},
+  };
+  cudaEvent_t ev[4];
+  for (int i = 0; i < 4; ++i)
+    if ((e = cudaEventCreate(&ev[i]))) return cuda_fail(h, e, "event");
+  cudaEvent_t first = nullptr;
+  if ((e = cudaEventCreate(&first))) return cuda_fail(h, e, "event");
+  double transfer = 0.0, h2d = 0.0, d2h = 0.0;
+  h->cursor = 0;
+  h->sampled_slot = -1;
+  for (int32_t t = 0; t < T && !e && st == WS_OK; ++t) {
+    const size_t n = (size_t)n_probs;  // the floats the trainer sends for this step
+    cudaEventRecord(ev[0], h->stream);
+    if (t == 0) cudaEventRecord(first, h->stream);
+    e = cudaMemcpyAsync(h->staging, host_probs + (size_t)t * step_stride, n * sizeof(float), cudaMemcpyHostToDevice,
+                        h->stream);
+    if (e) break;
+    h2d += (double)(n * sizeof(float));
+    cudaEventRecord(ev[1], h->stream);
+    st = ws_sample(h, h->staging, row_stride);
+    if (st) break;
+    st = ws_step(h, nullptr);
+    if (st) break;
+    cudaEventRecord(ev[2], h->stream);
+    for (const Part& p : parts) {
+      if (!p.host || !p.bytes) continue;
+      e = cudaMemcpyAsync(static_cast<char*>(p.host) + (size_t)t * p.bytes,
+                          static_cast<const char*>(p.dev) + (size_t)t * p.bytes, p.bytes, cudaMemcpyDeviceToHost,
+                          h->stream);
+      if (e) break;
+      d2h += (double)p.bytes;
+    }
+    if (e) break;
+    cudaEventRecord(ev[3], h->stream);
+    if ((e = cudaEventSynchronize(ev[3]))) break;  // the trainer waits for step t
+    float a = 0.0f, b = 0.0f;
+    cudaEventElapsedTime(&a, ev[0], ev[1]);
+    cudaEventElapsedTime(&b, ev[2], ev[3]);
+    transfer += (double)a + (double)b;
+  }
+  float total = 0.0f;
+  if (!e && st == WS_OK) cudaEventElapsedTime(&total, first, ev[3]);
+  for (int i = 0; i < 4; ++i) cudaEventDestroy(ev[i]);
+  cudaEventDestroy(first);
+  if (st) return st;
+  if (e) return cuda_fail(h, e, "staged roll-out copy");
+  if (out) {
+    out->total_ms = total;
+    out->transfer_ms = transfer;
+    out->h2d_bytes = h2d;
+    out->d2h_bytes = d2h;
+  }
+  return WS_OK;
+}
+
 static ws_tensor tensor(void* p, ws_dtype dt, std::initializer_list<int64_t> shape) {
   ws_tensor t{};
   t.ptr = p;

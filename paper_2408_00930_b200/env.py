@@ -164,6 +164,32 @@ class Env:
                                     self._row_stride(host_probs, row_stride), step_stride, C.byref(out)), self._h)
         return out
 
+    def rollout_staged(self, T: int, host_probs: torch.Tensor, dst: dict, row_stride: Optional[int] = None,
+                       step_stride: int = 0) -> dict:
+        """NEXT-N3 copy-based baseline (ws.h ws_rollout_staged): the same T steps as rollout(),
+        with the step's probabilities copied host -> device and the slot's obs / act / logp /
+        rew / done copied device -> host into `dst` (pinned CPU tensors shaped like the store
+        slabs' first T slots) every step.  Returns the transfer report."""
+        if host_probs.is_cuda or host_probs.dtype != torch.float32 or not host_probs.is_contiguous():
+            raise WSError(_abi.INVALID_ARGUMENT, "host_probs: contiguous float32 host tensor")
+        if step_stride:
+            per_step = host_probs.numel() - (T - 1) * step_stride
+        else:
+            per_step = host_probs.numel()
+        hs = _abi.ws_host_store(*[(dst[k].data_ptr() if dst.get(k) is not None else None)
+                                  for k in ("obs", "act", "logp", "rew", "done")])
+        rep = _abi.ws_staged_report()
+        check(lib().ws_rollout_staged(self._h, T, host_probs.data_ptr(), per_step,
+                                      self._row_stride(host_probs, row_stride), step_stride, C.byref(hs),
+                                      C.byref(rep)), self._h)
+        return {"total_ms": rep.total_ms, "transfer_ms": rep.transfer_ms, "h2d_bytes": rep.h2d_bytes,
+                "d2h_bytes": rep.d2h_bytes}
+
+    def host_store(self, T: int) -> dict:
+        """Pinned host tensors shaped like the first T slots of the store slabs (for rollout_staged)."""
+        return {k: torch.empty((T,) + tuple(v.shape[1:]), dtype=v.dtype).pin_memory()
+                for k, v in self.buffers().items() if k in ("obs", "act", "logp", "rew", "done") and v is not None}
+
     def synchronize(self):
         check(lib().ws_synchronize(self._h), self._h)
 

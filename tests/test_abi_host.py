@@ -151,3 +151,10 @@ def test_a2c_argument_validation_without_gpu():
         args = list(adam_ok)
         args[i] = v
         assert L.ws_adam(*args) == _abi.INVALID_ARGUMENT, (i, v)
+
+
+def test_staged_argument_validation_without_gpu():
+    """NEXT-N3 ws_rollout_staged rejects a NULL handle before any CUDA call."""
+    L = P.lib()
+    hs = _abi.ws_host_store()
+    assert L.ws_rollout_staged(None, 4, None, 0, 0, 0, C.byref(hs), None) == _abi.INVALID_ARGUMENT

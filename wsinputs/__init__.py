@@ -51,6 +51,11 @@ CONFIGS = {
     # a 4-64-2 actor-critic, then critic values, GAE over the store, gradient, clip + Adam
     "C2T": Workload("C2T", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64, "a2c": True},
                     note="CartPole-v1 10K envs x 1000 steps + A2C update of a 4-64-2 actor-critic (NEXT-N2)"),
+    # NEXT-N3: C2 through the copy-based baseline pipeline (per-step H2D of the
+    # probabilities and D2H of the slot, synchronised every step) -- the "data transfer"
+    # cost WarpSci removes
+    "C2X": Workload("C2X", "cartpole", 10000, 1, 1000, 2, 1, {"staged": True},
+                    note="CartPole-v1 10K envs x 1000 steps through the copy-based baseline pipeline (NEXT-N3)"),
     "C4G": Workload("C4G", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10, "gae": (0.99, 0.95)},
                     note="tag 1K envs x 100 agents x 200 + GAE(0.99, 0.95) over the store (NEXT-N2)"),
 }
