@@ -1,5 +1,5 @@
 #!/bin/bash
-for w in C1 C2 C3a C3b C4 C5 D0; do
+for w in ${WORKLOADS:-C1 C2 C3a C3b C4 C5 D0 C2P C2G C4G C2T C2X}; do
   timeout 600 python bench.py --workload $w --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$w.json 2> gpurun_out/bench_$w.err
   echo "$w rc=$?"; python -c "
 import json,sys
