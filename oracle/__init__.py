@@ -68,6 +68,8 @@ def lib():
             "wso_destroy": (None, [P]),
             "wso_set_capacity": (I, [P, I]),
             "wso_reset": (I, [P]),
+            "wso_register_user": (I, [C.c_char_p, C.c_char_p, I, I, I, I, I, I]),
+            "wso_set_env_data": (I, [P, P, I64, P, I64]),
             "wso_sample": (I, [P, P, I64, P, P]),
             "wso_step": (I, [P, P]),
             "wso_rollout": (I, [P, I, P, I64, I64, P, P, I]),
@@ -244,13 +246,70 @@ class _View(np.ndarray):
         self._owner = getattr(obj, "_owner", None)
 
 
+# ------------------------------------------------------------------ NEXT-N4 registered envs
+# The oracle's own prelude for a user environment's C source (the composer's input, contract
+# in include/ws.h): transcendental contract R3 (fp64 evaluation, one rounding), correctly
+# rounded sqrt, the same min / max / clip definitions; compiled without FMA contraction.
+_USER_PRELUDE = r"""
+#include <cmath>
+#define WS_FN static inline
+static inline float ws_sin(float x) { return (float)std::sin((double)x); }
+static inline float ws_cos(float x) { return (float)std::cos((double)x); }
+static inline float ws_exp(float x) { return (float)std::exp((double)x); }
+static inline float ws_log(float x) { return (float)std::log((double)x); }
+static inline float ws_tanh(float x) { return (float)std::tanh((double)x); }
+static inline float ws_sqrt(float x) { return std::sqrt(x); }
+static inline float ws_min(float a, float b) { return b < a ? b : a; }
+static inline float ws_max(float a, float b) { return a < b ? b : a; }
+static inline float ws_clip(float x, float lo, float hi) { return x < lo ? lo : (hi < x ? hi : x); }
+static inline float ws_abs(float x) { return std::fabs(x); }
+static inline float ws_floor(float x) { return std::floor(x); }
+#line 1 "user_env.c"
+"""
+_USER_EPILOGUE = r"""
+extern "C" {
+void wsu_init(float* s, const float* u, const float* p, const float* sh) { ws_env_init(s, u, p, sh); }
+void wsu_obs(const float* s, float* o, const float* p, const float* sh) { ws_env_obs(s, o, p, sh); }
+int wsu_step(float* s, int a, float* r, const float* p, const float* sh) { return ws_env_step(s, a, r, p, sh); }
+}
+"""
+_USER_ENVS = set()
+
+
+def register_user_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions: int, n_reset_draws: int,
+                      max_steps: int, n_params: int = 0) -> str:
+    """Compile a user environment's C source with g++ (-O2 -ffp-contract=off) and register it
+    with the oracle under `name`; Batch(name, ...) then simulates it.  Returns the .so path."""
+    import hashlib
+    defs = (f"#define WS_S {state_dim}\n#define WS_D {obs_dim}\n#define WS_N {n_actions}\n"
+            f"#define WS_R {n_reset_draws}\n#define WS_P {n_params}\n")
+    text = defs + _USER_PRELUDE + source + "\n" + _USER_EPILOGUE
+    key = hashlib.sha1(text.encode()).hexdigest()[:12]
+    d = os.path.join(_HERE, "build_user")
+    os.makedirs(d, exist_ok=True)
+    so = os.path.join(d, f"{name}_{key}.so")
+    if not os.path.exists(so):
+        src = so[:-3] + ".cpp"
+        with open(src, "w") as f:
+            f.write(text)
+        subprocess.run(["g++", "-std=c++17", "-O2", "-ffp-contract=off", "-fno-fast-math", "-fPIC", "-shared",
+                        "-o", so + ".tmp", src], check=True)
+        os.replace(so + ".tmp", so)
+    st = lib().wso_register_user(name.encode(), so.encode(), state_dim, obs_dim, n_actions, n_reset_draws,
+                                 max_steps, n_params)
+    if st != OK:
+        raise ValueError(f"wso_register_user failed ({st})")
+    _USER_ENVS.add(name)
+    return so
+
+
 class Batch:
     """make_batch .. run_rollout on the CPU; arrays are numpy views of the
     oracle's own storage (valid until the next set_capacity / destroy)."""
 
     def __init__(self, env: str, n_envs: int, n_agents: int = 1, seed: int = 0, *,
                  env_offset: int = 0, n_envs_global: int = 0, max_steps: int = 0,
-                 p0: int = 0, p1: int = 0, t_capacity: int = 0):
+                 p0: int = 0, p1: int = 0, t_capacity: int = 0, env_prm=None, env_shared=None):
         st = np.zeros(1, np.int32)
         self._h = lib().wso_create(env.encode(), n_envs, n_agents, seed & (2**64 - 1), env_offset,
                                    n_envs_global, max_steps, p0, p1, _p(st))
@@ -258,6 +317,11 @@ class Batch:
         if not self._h:
             raise ValueError(f"wso_create failed with status {self.status}")
         self.env = env
+        if env in _USER_ENVS:  # registered env: parameters / shared data, then the initial reset
+            prm = np.ascontiguousarray(np.zeros(0) if env_prm is None else env_prm, dtype=np.float32).ravel()
+            sh = np.ascontiguousarray(np.zeros(0) if env_shared is None else env_shared, dtype=np.float32).ravel()
+            assert lib().wso_set_env_data(self._h, _p(prm), prm.size, _p(sh), sh.size) == OK
+            assert self.reset() == OK
         if t_capacity:
             self.set_capacity(t_capacity)
 

@@ -38,6 +38,8 @@
 #include <cstdint>
 #include <cstdlib>
 #include <cstring>
+#include <dlfcn.h>
+#include <map>
 #include <limits>
 #include <string>
 #include <thread>
@@ -392,7 +394,22 @@ float gauss(uint64_t seed, uint64_t e_g, uint32_t agent, uint64_t t, int d, int 
  * The batch: make_batch, step_all, auto_reset, run_rollout
  * (S:158), log_step -- with the time-major store of S:40-45.
  * ---------------------------------------------------------------------------------- */
-enum Kind { K_CARTPOLE = 0, K_ACROBOT = 1, K_PENDULUM = 2, K_TAG = 3, K_SURFACE = 4, K_DUMMY = 5 };
+enum Kind { K_CARTPOLE = 0, K_ACROBOT = 1, K_PENDULUM = 2, K_TAG = 3, K_SURFACE = 4, K_DUMMY = 5, K_USER = 6 };
+
+/* NEXT-N4: an environment given as C source (the composer's input, include/ws.h contract),
+ * compiled by g++ into a shared object and called through these pointers; the engine
+ * semantics around it (sampling, store, truncation, reset draws, statistics) are the
+ * oracle's own, exactly as for the built-in envs. */
+struct UserEnv {
+  int state_dim, obs_dim, n_actions, n_reset, max_steps, n_params;
+  void (*init)(float*, const float*, const float*, const float*);
+  void (*obs)(const float*, float*, const float*, const float*);
+  int (*step)(float*, int, float*, const float*, const float*);
+};
+std::map<std::string, UserEnv>& user_envs() {
+  static std::map<std::string, UserEnv> m;
+  return m;
+}
 enum Err { E_OK = 0, E_INVALID_ARGUMENT = 1, E_UNKNOWN_ENV = 2, E_INVALID_ACTION = 3,
            E_INVALID_PROBS = 4, E_OUT_OF_RANGE = 5, E_BAD_STATE = 6 };
 const int ERRBIT_ACTION = 1, ERRBIT_PROBS = 2;
@@ -435,6 +452,10 @@ static void policy_probs(const float* w, int D, int H, int N, const float* obs, 
 
 struct Batch {
   Kind kind;
+  const UserEnv* user = nullptr;       // K_USER
+  std::vector<float> prm, shared;      // K_USER per-replica parameters [E, n_params] / shared data
+  const float* prm_row(int64_t e) const { return user && user->n_params ? &prm[(size_t)e * user->n_params] : nullptr; }
+  const float* shared_ptr() const { return shared.empty() ? nullptr : shared.data(); }
   int64_t E, E_global, offset;
   int A;
   uint64_t seed;
@@ -515,6 +536,12 @@ struct Batch {
         break;
       case K_DUMMY:
         break;
+      case K_USER: {
+        std::vector<float> u(std::max(1, user->n_reset));
+        for (int i = 0; i < user->n_reset; ++i) u[i] = U(0, i);
+        user->init(s, u.data(), prm_row(e), shared_ptr());
+        break;
+      }
     }
   }
 
@@ -548,6 +575,9 @@ struct Batch {
         break;
       case K_DUMMY:
         for (int i = 0; i < obs_dim; ++i) o[i] = 0.0f;
+        break;
+      case K_USER:
+        user->obs(s, o, prm_row(e), shared_ptr());
         break;
     }
   }
@@ -663,6 +693,12 @@ struct Batch {
           r[0] = 1.0f;
           break;
         }
+        case K_USER: {
+          int a = act_i[base];
+          bad = (a < 0 || a >= n_actions);
+          if (!bad) term = user->step(s, a, &r[0], prm_row(e), shared_ptr());
+          break;
+        }
       }
       if (bad) {  // reading Q19: sticky error, env not advanced, rew = 0, done = 0
         *err_out |= ERRBIT_ACTION;
@@ -745,6 +781,7 @@ Kind parse_kind(const char* s, bool* ok) {
   if (n == "tag") return K_TAG;
   if (n == "surface") return K_SURFACE;
   if (n == "dummy") return K_DUMMY;
+  if (user_envs().count(n)) return K_USER;
   *ok = false;
   return K_DUMMY;
 }
@@ -855,6 +892,13 @@ void* wso_create(const char* env, int64_t E, int A, uint64_t seed, int64_t env_o
       b->obs_dim = b->D + 1; b->n_actions = 0; b->act_dim = b->D; b->state_dim = b->D; b->n_reset_draws = b->D; b->T_max = 200;
       break;
     case K_DUMMY: b->obs_dim = 4; b->n_actions = 2; b->act_dim = 1; b->state_dim = 0; b->n_reset_draws = 0; b->T_max = 100; break;
+    case K_USER: {
+      const UserEnv& u = user_envs()[env];
+      b->user = &u;
+      b->obs_dim = u.obs_dim; b->n_actions = u.n_actions; b->act_dim = 1; b->state_dim = u.state_dim;
+      b->n_reset_draws = u.n_reset; b->T_max = u.max_steps;
+      break;
+    }
   }
   if (max_steps > 0) b->T_max = max_steps;
   b->state.assign((size_t)E * b->state_dim, 0.0f);
@@ -865,9 +909,31 @@ void* wso_create(const char* env, int64_t E, int A, uint64_t seed, int64_t env_o
   b->ep_step.assign(E, 0);
   b->reset_count.assign(E, 0);
   b->ep_ret.assign((size_t)E * A, 0.0f);
-  b->reset_all();
+  if (kind != K_USER) b->reset_all();  // registered envs: wso_set_env_data, then wso_reset
   *status = E_OK;
   return b;
+}
+
+/* NEXT-N4: register the env compiled (by oracle/__init__.py) into so_path */
+int wso_register_user(const char* name, const char* so_path, int state_dim, int obs_dim, int n_actions, int n_reset,
+                      int max_steps, int n_params) {
+  void* lib = dlopen(so_path, RTLD_NOW | RTLD_LOCAL);
+  if (!lib) return E_INVALID_ARGUMENT;
+  UserEnv u{state_dim, obs_dim, n_actions, n_reset, max_steps, n_params,
+            reinterpret_cast<void (*)(float*, const float*, const float*, const float*)>(dlsym(lib, "wsu_init")),
+            reinterpret_cast<void (*)(const float*, float*, const float*, const float*)>(dlsym(lib, "wsu_obs")),
+            reinterpret_cast<int (*)(float*, int, float*, const float*, const float*)>(dlsym(lib, "wsu_step"))};
+  if (!u.init || !u.obs || !u.step) return E_INVALID_ARGUMENT;
+  user_envs()[name] = u;
+  return E_OK;
+}
+
+int wso_set_env_data(void* h, const float* prm, int64_t n_prm, const float* shared, int64_t n_shared) {
+  Batch* b = (Batch*)h;
+  if (b->kind != K_USER) return E_INVALID_ARGUMENT;
+  b->prm.assign(prm, prm + n_prm);
+  b->shared.assign(shared, shared + n_shared);
+  return E_OK;
 }
 
 void wso_destroy(void* h) { delete (Batch*)h; }

@@ -33,6 +33,7 @@ class ws_config(C.Structure):
         ("t_capacity", C.c_int32), ("max_steps", C.c_int32), ("write_logp", C.c_int32),
         ("param0", C.c_int32), ("param1", C.c_int32), ("block_size", C.c_int32),
         ("alloc", ALLOC_FN), ("free", FREE_FN), ("alloc_user", C.c_void_p),
+        ("env_prm", C.c_void_p), ("env_shared", C.c_void_p),
     ]
 
 
@@ -91,6 +92,12 @@ class ws_staged_report(C.Structure):
     _fields_ = [(n, C.c_double) for n in ("total_ms", "transfer_ms", "h2d_bytes", "d2h_bytes")]
 
 
+class ws_env_def(C.Structure):
+    _fields_ = [("name", C.c_char_p), ("source", C.c_char_p), ("state_dim", C.c_int32), ("obs_dim", C.c_int32),
+                ("n_actions", C.c_int32), ("n_reset_draws", C.c_int32), ("max_steps", C.c_int32),
+                ("n_params", C.c_int32)]
+
+
 _SIGS = {
     "ws_config_init": (C.c_int, [C.POINTER(ws_config)]),
     "ws_create": (C.c_int, [C.c_int64, C.c_int32, C.c_char_p, C.c_uint64, C.POINTER(C.c_void_p)]),
@@ -105,6 +112,9 @@ _SIGS = {
                                   C.POINTER(ws_stats)]),
     "ws_rollout_staged": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64,
                                     C.POINTER(ws_host_store), C.POINTER(ws_staged_report)]),
+    "ws_register_env": (C.c_int, [C.POINTER(ws_env_def), C.c_char_p, C.c_size_t]),
+    "ws_registered_env": (C.c_int32, [C.c_char_p]),
+    "ws_set_env_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ws_get_buffers": (C.c_int, [C.c_void_p, C.POINTER(ws_buffers)]),
     "ws_get_info": (C.c_int, [C.c_void_p, C.POINTER(ws_info)]),
     "ws_synchronize": (C.c_int, [C.c_void_p]),

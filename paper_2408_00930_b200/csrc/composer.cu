@@ -1,0 +1,449 @@
+// composer.cu -- NEXT-N4: runtime environment composer.  A user environment is plain C
+// source (three functions, include/ws.h "NEXT-N4"), compiled at registration time by NVRTC
+// for sm_100a into a fused roll-out template (the analogue of the paper's Numba / CUDA C
+// environment path: "environments ... written in CUDA C or Numba", P:65 / P:71 one
+// replica per GPU thread, "domain agnostic"), loaded per device with
+// cudaLibraryLoadData and launched through the same handle API as the built-in envs.
+//
+// The template implements the engine's semantics exactly as the built-in lane kernels do
+// (DESIGN R11-R15, R19-R21): Philox4x32-10 streams keyed by the global replica index, the
+// R13 inverse-CDF sampler on the given probabilities (fp64 prefix sums), the pre-step
+// observation in obs[t] (R12), truncation at T_max (R10), auto-reset from the RESET stream
+// (draw j = reset_count * n_reset + i), sticky device errors (R19), exact fixed-point
+// per-slot statistics (R20).  The user functions receive a per-replica parameter row
+// (parameter jitter) and a shared read-only array in global memory (e.g. a 3-D grid, Fig 1).
+// NVRTC is loaded with dlopen at the first registration, so libws has no link-time
+// dependency on it.
+#include <cuda_runtime.h>
+#include <dlfcn.h>
+#include <nvrtc.h>
+
+#include <cstring>
+#include <map>
+#include <memory>
+#include <mutex>
+#include <string>
+#include <vector>
+
+#include "../../include/ws.h"
+#include "kernels.h"
+
+namespace {
+
+// ------------------------------------------------------------------------------ NVRTC
+struct Nvrtc {
+  bool ok = false;
+  std::string why;
+  nvrtcResult (*create)(nvrtcProgram*, const char*, const char*, int, const char* const*, const char* const*);
+  nvrtcResult (*compile)(nvrtcProgram, int, const char* const*);
+  nvrtcResult (*log_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*log)(nvrtcProgram, char*);
+  nvrtcResult (*cubin_size)(nvrtcProgram, size_t*);
+  nvrtcResult (*cubin)(nvrtcProgram, char*);
+  nvrtcResult (*destroy)(nvrtcProgram*);
+};
+
+Nvrtc& nvrtc() {
+  static Nvrtc n;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* lib = nullptr;
+    for (const char* name : {"libnvrtc.so.12", "libnvrtc.so", "/usr/local/cuda/lib64/libnvrtc.so.12",
+                             "/usr/local/cuda/lib64/libnvrtc.so"}) {
+      if ((lib = dlopen(name, RTLD_NOW | RTLD_LOCAL))) break;
+    }
+    if (!lib) {
+      n.why = "libnvrtc.so.12 not found";
+      return;
+    }
+    bool good = true;
+    auto sym = [&](const char* s) {
+      void* p = dlsym(lib, s);
+      good = good && p;
+      return p;
+    };
+    n.create = reinterpret_cast<decltype(n.create)>(sym("nvrtcCreateProgram"));
+    n.compile = reinterpret_cast<decltype(n.compile)>(sym("nvrtcCompileProgram"));
+    n.log_size = reinterpret_cast<decltype(n.log_size)>(sym("nvrtcGetProgramLogSize"));
+    n.log = reinterpret_cast<decltype(n.log)>(sym("nvrtcGetProgramLog"));
+    n.cubin_size = reinterpret_cast<decltype(n.cubin_size)>(sym("nvrtcGetCUBINSize"));
+    n.cubin = reinterpret_cast<decltype(n.cubin)>(sym("nvrtcGetCUBIN"));
+    n.destroy = reinterpret_cast<decltype(n.destroy)>(sym("nvrtcDestroyProgram"));
+    n.ok = good;
+    if (!good) n.why = "libnvrtc: missing symbols";
+  });
+  return n;
+}
+
+// ------------------------------------------------------------------------------ template
+// Kernel arguments: the same struct is spelled in the template source below (by value).
+struct UserArgs {
+  float* obs;
+  int32_t* act;
+  float* logp;
+  float* rew;
+  uint8_t* done;
+  unsigned long long* stats;
+  float* state;
+  float* obs_live;
+  int32_t* ep_step;
+  uint32_t* reset_count;
+  float* ep_ret;
+  uint32_t* err;
+  const float* prm;
+  const float* shared;
+  int64_t E;
+  int64_t offset;
+  int32_t max_steps;
+  int32_t write_logp;
+  uint32_t k0, k1;
+};
+
+const char* kPrelude = R"WS(
+typedef unsigned int ws_u32; typedef unsigned long long ws_u64; typedef long long ws_i64;
+typedef unsigned char ws_u8; typedef int ws_i32;
+#define WS_FN __device__ __forceinline__
+/* transcendental contract (DESIGN R3): fp64 evaluation, one rounding to fp32 */
+WS_FN float ws_sin(float x) { return (float)sin((double)x); }
+WS_FN float ws_cos(float x) { return (float)cos((double)x); }
+WS_FN float ws_exp(float x) { return (float)exp((double)x); }
+WS_FN float ws_log(float x) { return (float)log((double)x); }
+WS_FN float ws_tanh(float x) { return (float)tanh((double)x); }
+WS_FN float ws_sqrt(float x) { return __fsqrt_rn(x); }
+WS_FN float ws_min(float a, float b) { return b < a ? b : a; }
+WS_FN float ws_max(float a, float b) { return a < b ? b : a; }
+WS_FN float ws_clip(float x, float lo, float hi) { return x < lo ? lo : (hi < x ? hi : x); }
+WS_FN float ws_abs(float x) { return fabsf(x); }
+WS_FN float ws_floor(float x) { return floorf(x); }
+#line 1 "user_env.c"
+)WS";
+
+const char* kEngine = R"WS(
+#line 1 "ws_composer_engine"
+struct WsUserArgs {
+  float* obs; ws_i32* act; float* logp; float* rew; ws_u8* done; ws_u64* stats;
+  float* state; float* obs_live; ws_i32* ep_step; ws_u32* reset_count; float* ep_ret; ws_u32* err;
+  const float* prm; const float* shared;
+  ws_i64 E; ws_i64 offset; ws_i32 max_steps; ws_i32 write_logp; ws_u32 k0, k1;
+};
+
+/* Philox4x32-10; draw j of stream (env_global, agent, purpose) = word j & 3 of
+   Philox(ctr = (j >> 2, env_global, agent, purpose), key) (DESIGN R15) */
+WS_FN void ws_philox(ws_u32 c0, ws_u32 c1, ws_u32 c2, ws_u32 c3, ws_u32 k0, ws_u32 k1, ws_u32* w) {
+  for (int r = 0; r < 10; ++r) {
+    if (r > 0) { k0 += 0x9E3779B9u; k1 += 0xBB67AE85u; }
+    const ws_u32 lo0 = 0xD2511F53u * c0, hi0 = __umulhi(0xD2511F53u, c0);
+    const ws_u32 lo1 = 0xCD9E8D57u * c2, hi1 = __umulhi(0xCD9E8D57u, c2);
+    const ws_u32 n0 = hi1 ^ c1 ^ k0, n2 = hi0 ^ c3 ^ k1;
+    c0 = n0; c1 = lo1; c2 = n2; c3 = lo0;
+  }
+  w[0] = c0; w[1] = c1; w[2] = c2; w[3] = c3;
+}
+WS_FN ws_u32 ws_draw(const WsUserArgs& a, ws_u32 eg, ws_u32 purpose, ws_u64 j) {
+  ws_u32 w[4];
+  ws_philox((ws_u32)(j >> 2), eg, 0u, purpose, a.k0, a.k1, w);
+  return w[j & 3];
+}
+WS_FN float ws_u01(ws_u32 w) { return (float)(w >> 8) * (1.0f / 16777216.0f); }
+
+WS_FN void ws_init(const WsUserArgs& a, ws_u32 eg, ws_u32 rc, float* s, const float* prm) {
+  float u[WS_R > 0 ? WS_R : 1];
+  for (int i = 0; i < WS_R; ++i) u[i] = ws_u01(ws_draw(a, eg, 2u, (ws_u64)rc * WS_R + i));
+  ws_env_init(s, u, prm, a.shared);
+}
+
+/* R13: inverse CDF in index order on u * S (fp64), strict <, zero-probability actions never
+   drawn, fallback = last nonzero; invalid row -> -1 */
+WS_FN int ws_sample(const float* p, float u, float* lp) {
+  double S = 0.0;
+  int last = -1;
+  bool bad = false;
+  for (int i = 0; i < WS_N; ++i) {
+    const float x = p[i];
+    bad = bad || !(x >= 0.0f) || !isfinite(x);
+    S += (double)x;
+    if (x > 0.0f) last = i;
+  }
+  if (bad || !(S > 0.0) || !isfinite(S)) { *lp = __int_as_float(0x7fc00000); return -1; }
+  const double target = (double)u * S;
+  double C = 0.0;
+  int chosen = -1;
+  for (int i = 0; i < WS_N; ++i) {
+    C += (double)p[i];
+    if (chosen < 0 && p[i] > 0.0f && target < C) chosen = i;
+  }
+  if (chosen < 0) chosen = last;
+  *lp = (float)(log((double)p[chosen]) - log(S));
+  return chosen;
+}
+
+WS_FN ws_i64 ws_fx(float v) { return __float2ll_rn(v * 4294967296.0f); }
+WS_FN ws_i64 ws_wsum(ws_i64 v) {
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
+  return v;
+}
+
+extern "C" __global__ void k_user_reset(const WsUserArgs a) {
+  const ws_i64 e = (ws_i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e >= a.E) return;
+  const float* prm = a.prm ? a.prm + e * (WS_P > 0 ? WS_P : 1) : 0;
+  float s[WS_S];
+  ws_init(a, (ws_u32)(a.offset + e), 0u, s, prm);
+  for (int i = 0; i < WS_S; ++i) a.state[e * WS_S + i] = s[i];
+  float o[WS_D];
+  ws_env_obs(s, o, prm, a.shared);
+  for (int i = 0; i < WS_D; ++i) a.obs_live[e * WS_D + i] = o[i];
+  a.ep_step[e] = 0;
+  a.reset_count[e] = 0u;
+  a.ep_ret[e] = 0.0f;
+}
+
+/* fused roll-out of T steps, one replica per thread (P:65, P:71) */
+extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, const float* probs,
+                                          ws_i64 row_stride, ws_i64 step_stride) {
+  const ws_i64 e0 = (ws_i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e0 - (threadIdx.x & 31) >= a.E) return;          /* whole warp past the end */
+  const bool live = e0 < a.E;
+  const ws_i64 e = live ? e0 : a.E - 1;                /* tail lanes shadow E-1, store nothing */
+  const ws_u32 eg = (ws_u32)(a.offset + e);
+  const float* prm = a.prm ? a.prm + e * (WS_P > 0 ? WS_P : 1) : 0;
+  float s[WS_S], o[WS_D];
+  for (int i = 0; i < WS_S; ++i) s[i] = a.state[e * WS_S + i];
+  for (int i = 0; i < WS_D; ++i) o[i] = a.obs_live[e * WS_D + i];
+  ws_i32 ep_step = a.ep_step[e];
+  ws_u32 rc = a.reset_count[e];
+  float ep_ret = a.ep_ret[e];
+  ws_u32 err = 0;
+  for (int c = 0; c < T; ++c) {
+    const ws_u64 t = t0 + (ws_u64)c;
+    const ws_i64 idx = (ws_i64)c * a.E + e;
+    if (live) for (int i = 0; i < WS_D; ++i) __stcs(a.obs + idx * WS_D + i, o[i]);   /* R12 */
+    float lp;
+    const int act = ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, ws_u01(ws_draw(a, eg, 1u, t)), &lp);
+    if (live) {
+      __stcs(a.act + idx, act);
+      if (a.write_logp) __stcs(a.logp + idx, lp);
+    }
+    float r = 0.0f;
+    ws_u32 d = 0u;
+    float ret = 0.0f;
+    ws_i32 es = 0;
+    if (act < 0) {                                   /* R19: not advanced, rew 0, done 0 */
+      if (live) err |= 3u;
+    } else {
+      const int term = ws_env_step(s, act, &r, prm, a.shared);
+      es = ep_step + 1;
+      d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
+      ret = ep_ret + r;
+      ep_step = es;
+      ep_ret = ret;
+      if (d) {                                       /* auto-reset (R11) */
+        rc += 1u;
+        ws_init(a, eg, rc, s, prm);
+        ep_step = 0;
+        ep_ret = 0.0f;
+      }
+      ws_env_obs(s, o, prm, a.shared);
+    }
+    if (live) {
+      __stcs(a.rew + idx, r);
+      a.done[idx] = (ws_u8)d;
+    }
+    /* exact fixed-point per-slot statistics (R20), warp-reduced then one atomic per field */
+    const bool dl = live && d;
+    const ws_i64 f3 = ws_wsum(live ? ws_fx(r) : 0);
+    const unsigned any = __ballot_sync(0xffffffffu, dl);
+    ws_i64 f0 = 0, f1 = 0, f2 = 0;
+    if (any) {
+      f0 = ws_wsum(dl ? 1 : 0);
+      f1 = ws_wsum(dl ? ws_fx(ret) : 0);
+      f2 = ws_wsum(dl ? (ws_i64)es : 0);
+    }
+    if ((threadIdx.x & 31) == 0) {
+      ws_u64* st = a.stats + (ws_i64)c * 4;
+      if (f3) atomicAdd(st + 3, (ws_u64)f3);
+      if (any) {
+        atomicAdd(st + 0, (ws_u64)f0);
+        atomicAdd(st + 1, (ws_u64)f1);
+        atomicAdd(st + 2, (ws_u64)f2);
+      }
+    }
+  }
+  if (live) {
+    for (int i = 0; i < WS_S; ++i) a.state[e * WS_S + i] = s[i];
+    for (int i = 0; i < WS_D; ++i) a.obs_live[e * WS_D + i] = o[i];
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    if (err) atomicOr(a.err, err);
+  }
+}
+)WS";
+
+// ------------------------------------------------------------------------------ registry
+struct UserEnv {
+  ws_env_def def{};
+  std::string name, source, log;
+  std::vector<char> cubin;
+  std::map<int, std::pair<cudaLibrary_t, std::pair<cudaKernel_t, cudaKernel_t>>> per_dev;  // reset, rollout
+};
+
+std::mutex g_mu;
+std::map<std::string, std::unique_ptr<UserEnv>>& registry() {
+  static std::map<std::string, std::unique_ptr<UserEnv>> r;
+  return r;
+}
+
+bool builtin(const std::string& n) {
+  for (const char* b : {"cartpole", "acrobot", "pendulum", "tag", "surface", "dummy"})
+    if (n == b) return true;
+  return false;
+}
+
+void copy_log(const std::string& s, char* log, size_t n) {
+  if (!log || !n) return;
+  const size_t k = std::min(n - 1, s.size());
+  std::memcpy(log, s.data(), k);
+  log[k] = '\0';
+}
+
+cudaError_t kernels_for(UserEnv* u, cudaKernel_t* reset, cudaKernel_t* roll) {
+  int dev = 0;
+  cudaError_t e = cudaGetDevice(&dev);
+  if (e) return e;
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = u->per_dev.find(dev);
+  if (it == u->per_dev.end()) {
+    cudaLibrary_t lib;
+    if ((e = cudaLibraryLoadData(&lib, u->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0))) return e;
+    cudaKernel_t kr, kw;
+    if ((e = cudaLibraryGetKernel(&kr, lib, "k_user_reset"))) return e;
+    if ((e = cudaLibraryGetKernel(&kw, lib, "k_user_rollout"))) return e;
+    it = u->per_dev.emplace(dev, std::make_pair(lib, std::make_pair(kr, kw))).first;
+  }
+  *reset = it->second.second.first;
+  *roll = it->second.second.second;
+  return cudaSuccess;
+}
+
+UserArgs user_args(const ws::UserLaunch& l) {
+  const ws::KArgs& k = l.k;
+  return UserArgs{k.obs, static_cast<int32_t*>(k.act), k.logp, k.rew, k.done, k.stats, k.state, k.obs_live,
+                  k.ep_step, k.reset_count, k.ep_ret, k.err, l.prm, l.shared, k.E, k.offset, k.max_steps,
+                  k.write_logp, k.k0, k.k1};
+}
+
+}  // namespace
+
+namespace ws {
+
+bool user_env_spec(const char* name, UserSpec* out) {
+  if (!name) return false;
+  std::lock_guard<std::mutex> g(g_mu);
+  auto it = registry().find(name);
+  if (it == registry().end()) return false;
+  const ws_env_def& d = it->second->def;
+  out->handle = it->second.get();
+  out->obs_dim = d.obs_dim;
+  out->n_actions = d.n_actions;
+  out->state_dim = d.state_dim;
+  out->max_steps = d.max_steps;
+  out->n_params = d.n_params;
+  return true;
+}
+
+cudaError_t launch_user_reset(const UserLaunch& l) {
+  cudaKernel_t kr, kw;
+  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &kr, &kw);
+  if (e) return e;
+  UserArgs a = user_args(l);
+  void* args[] = {&a};
+  const unsigned grid = (unsigned)((l.k.E + 127) / 128);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(kr), dim3(grid), dim3(128), args, 0, l.stream);
+}
+
+cudaError_t launch_user_rollout(const UserLaunch& l, int T, uint64_t t0, const float* probs, int64_t row_stride,
+                                int64_t step_stride) {
+  cudaKernel_t kr, kw;
+  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &kr, &kw);
+  if (e) return e;
+  UserArgs a = user_args(l);
+  void* args[] = {&a, &T, &t0, &probs, &row_stride, &step_stride};
+  const unsigned grid = (unsigned)((l.k.E + 127) / 128);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(kw), dim3(grid), dim3(128), args, 0, l.stream);
+}
+
+}  // namespace ws
+
+extern "C" {
+
+ws_status ws_register_env(const ws_env_def* def, char* log, size_t log_size) {
+  copy_log("", log, log_size);
+  if (!def || !def->name || !def->source || !*def->name || builtin(def->name) || def->state_dim < 1 ||
+      def->state_dim > 32 || def->obs_dim < 1 || def->obs_dim > 32 || def->n_actions < 2 || def->n_actions > 16 ||
+      def->n_reset_draws < 0 || def->n_reset_draws > 64 || def->max_steps < 1 || def->n_params < 0 ||
+      def->n_params > 64) {
+    copy_log("ws_register_env: name (not a built-in), source, state_dim 1..32, obs_dim 1..32, n_actions 2..16, "
+             "n_reset_draws 0..64, max_steps >= 1, n_params 0..64", log, log_size);
+    return WS_ERR_INVALID_ARGUMENT;
+  }
+  {
+    std::lock_guard<std::mutex> g(g_mu);
+    if (registry().count(def->name)) {
+      copy_log("ws_register_env: name already registered", log, log_size);
+      return WS_ERR_INVALID_ARGUMENT;
+    }
+  }
+  Nvrtc& nv = nvrtc();
+  if (!nv.ok) {
+    copy_log("ws_register_env: " + nv.why, log, log_size);
+    return WS_ERR_CUDA;
+  }
+  auto u = std::make_unique<UserEnv>();
+  u->def = *def;
+  u->name = def->name;
+  u->source = def->source;
+  u->def.name = u->name.c_str();
+  u->def.source = u->source.c_str();
+  const std::string defs = "#define WS_S " + std::to_string(def->state_dim) + "\n#define WS_D " +
+                           std::to_string(def->obs_dim) + "\n#define WS_N " + std::to_string(def->n_actions) +
+                           "\n#define WS_R " + std::to_string(def->n_reset_draws) + "\n#define WS_P " +
+                           std::to_string(def->n_params) + "\n";
+  const std::string src = defs + kPrelude + u->source + "\n" + kEngine;
+  nvrtcProgram prog;
+  if (nv.create(&prog, src.c_str(), "ws_user_env.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {
+    copy_log("ws_register_env: nvrtcCreateProgram failed", log, log_size);
+    return WS_ERR_CUDA;
+  }
+  // --fmad=false: no FMA contraction of the user's fp32 arithmetic (DESIGN R4), IEEE div/sqrt
+  const char* opts[] = {"--gpu-architecture=sm_100a", "--fmad=false", "--std=c++17", "-lineinfo",
+                        "--prec-div=true", "--prec-sqrt=true", "-default-device"};
+  const nvrtcResult rc = nv.compile(prog, (int)(sizeof(opts) / sizeof(opts[0])), opts);
+  size_t n = 0;
+  nv.log_size(prog, &n);
+  std::string lg(n, '\0');
+  if (n) nv.log(prog, &lg[0]);
+  while (!lg.empty() && lg.back() == '\0') lg.pop_back();
+  u->log = lg;
+  if (rc != NVRTC_SUCCESS) {
+    copy_log(lg, log, log_size);
+    nv.destroy(&prog);
+    return WS_ERR_INVALID_ARGUMENT;
+  }
+  nv.cubin_size(prog, &n);
+  u->cubin.resize(n);
+  nv.cubin(prog, u->cubin.data());
+  nv.destroy(&prog);
+  copy_log(lg, log, log_size);
+  std::lock_guard<std::mutex> g(g_mu);
+  registry()[u->name] = std::move(u);
+  return WS_OK;
+}
+
+int32_t ws_registered_env(const char* name) {
+  if (!name) return 0;
+  std::lock_guard<std::mutex> g(g_mu);
+  return registry().count(name) ? 1 : 0;
+}
+
+}  // extern "C"

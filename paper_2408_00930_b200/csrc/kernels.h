@@ -7,7 +7,7 @@
 
 namespace ws {
 
-enum EnvKind : int { kCartPole = 0, kAcrobot = 1, kPendulum = 2, kTag = 3, kSurface = 4, kDummy = 5 };
+enum EnvKind : int { kCartPole = 0, kAcrobot = 1, kPendulum = 2, kTag = 3, kSurface = 4, kDummy = 5, kUser = 6 };
 
 // Everything a kernel needs to find the handle's buffers (passed by value).
 struct KArgs {
@@ -96,5 +96,22 @@ struct PeerArgs {
 };
 cudaError_t launch_peer_allreduce(const unsigned long long* local, int T, const PeerArgs& p, uint64_t epoch,
                                   unsigned long long* out, uint32_t* err, double timeout_s, cudaStream_t s);
+
+// NEXT-N4: environments registered at run time (composer.cu, ws_register_env)
+struct UserSpec {
+  void* handle;  // registry entry
+  int obs_dim, n_actions, state_dim, max_steps, n_params;
+};
+struct UserLaunch {
+  KArgs k;
+  void* handle;
+  const float* prm;     // [E, n_params] per-replica parameters or null
+  const float* shared;  // shared read-only data or null
+  cudaStream_t stream;
+};
+bool user_env_spec(const char* name, UserSpec* out);
+cudaError_t launch_user_reset(const UserLaunch& l);
+cudaError_t launch_user_rollout(const UserLaunch& l, int T, uint64_t t0, const float* probs, int64_t row_stride,
+                                int64_t step_stride);
 
 }  // namespace ws

@@ -19,6 +19,8 @@ namespace {
 struct EnvSpec {
   ws::EnvKind kind;
   int obs_dim, n_actions, act_dim, state_dim, max_steps;
+  void* user = nullptr;  // NEXT-N4 registry entry (kind == kUser)
+  int n_params = 0;
 };
 
 bool lookup_env(const char* name, int A, int p0, EnvSpec* out) {
@@ -34,6 +36,11 @@ bool lookup_env(const char* name, int A, int p0, EnvSpec* out) {
     return true;
   }
   if (n == "dummy") { *out = {ws::kDummy, 4, 2, 1, 0, 100}; return true; }
+  ws::UserSpec u;
+  if (ws::user_env_spec(name, &u)) {  // NEXT-N4: registered at run time (composer.cu)
+    *out = {ws::kUser, u.obs_dim, u.n_actions, 1, u.state_dim, u.max_steps, u.handle, u.n_params};
+    return true;
+  }
   (void)A;
   return false;
 }
@@ -88,6 +95,9 @@ struct ws_env {
   uint8_t* done = nullptr;
   unsigned long long* stats = nullptr;  // [T_cap, 4] fixed-point int64
   uint32_t* plan = nullptr;
+  // NEXT-N4 per-replica parameters / shared data of a registered env (caller-owned)
+  const float* user_prm = nullptr;
+  const float* user_shared = nullptr;
   // e2e staging
   float* staging = nullptr;
   int64_t staging_n = 0;
@@ -292,6 +302,15 @@ ws_status ws_create(int64_t n_envs, int32_t n_agents, const char* env, uint64_t 
   return ws_create_ex(&c, out);
 }
 
+ws_status ws_set_env_data(ws_env* h, const float* prm, const float* shared) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (h->spec.kind != ws::kUser) return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_set_env_data: registered envs only");
+  if (h->spec.n_params > 0 && !prm) return fail(h, WS_ERR_INVALID_ARGUMENT, "this env needs per-replica parameters");
+  h->user_prm = prm;
+  h->user_shared = shared;
+  return WS_OK;
+}
+
 ws_status ws_create_ex(const ws_config* cfg, ws_env** out) {
   if (!out) return WS_ERR_INVALID_ARGUMENT;
   *out = nullptr;
@@ -303,6 +322,7 @@ ws_status ws_create_ex(const ws_config* cfg, ws_env** out) {
   const int64_t Eg = cfg->n_envs_global > 0 ? cfg->n_envs_global : cfg->env_offset + cfg->n_envs;
   if (cfg->env_offset + cfg->n_envs > Eg || Eg > (int64_t)UINT32_MAX) return WS_ERR_INVALID_ARGUMENT;
   if (spec.kind != ws::kTag && cfg->n_agents != 1) return WS_ERR_INVALID_ARGUMENT;
+  if (spec.kind == ws::kUser && spec.n_params > 0 && !cfg->env_prm) return WS_ERR_INVALID_ARGUMENT;
   if (cfg->t_capacity < 0 || cfg->max_steps < 0) return WS_ERR_INVALID_ARGUMENT;
   if (cfg->block_size != 0 && (cfg->block_size % 32 != 0 || cfg->block_size > 256 || cfg->block_size < 32))
     return WS_ERR_INVALID_ARGUMENT;
@@ -334,6 +354,8 @@ ws_status ws_create_ex(const ws_config* cfg, ws_env** out) {
   h->alloc = cfg->alloc;
   h->free_fn = cfg->free;
   h->alloc_user = cfg->alloc_user;
+  h->user_prm = cfg->env_prm;
+  h->user_shared = cfg->env_shared;
   DeviceGuard g(h->device);
   if (h->device < 0) cudaGetDevice(&h->device);
   cudaError_t e;
@@ -383,7 +405,15 @@ ws_status ws_reset(ws_env* h) {
   if (e) return cuda_fail(h, e, "ws_reset memset");
   if (h->stats && (e = cudaMemsetAsync(h->stats, 0, (size_t)h->T_cap * 4 * sizeof(unsigned long long), h->stream)))
     return cuda_fail(h, e, "ws_reset memset stats");
-  if ((e = ws::launch_reset(kargs(h), launch_of(h), &h->launches))) return cuda_fail(h, e, "reset kernel");
+  if (h->spec.kind == ws::kUser) {
+    if (h->timing) mark_kernel(h, ws::kKReset, 0);
+    e = ws::launch_user_reset(ws::UserLaunch{kargs(h), h->spec.user, h->user_prm, h->user_shared, h->stream});
+    if (h->timing) mark_kernel(h, ws::kKReset, 1);
+    h->launches += 1;
+  } else {
+    e = ws::launch_reset(kargs(h), launch_of(h), &h->launches);
+  }
+  if (e) return cuda_fail(h, e, "reset kernel");
   h->t = 0;
   h->cursor = 0;
   h->sampled_slot = -1;
@@ -404,6 +434,7 @@ ws_status ws_sample(ws_env* h, const float* probs, int64_t row_stride) {
   ws_status s = ensure_store(h, 1000);
   if (s) return s;
   if (h->cursor >= h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "cursor at store capacity (ws_rewind)");
+  if (h->spec.kind == ws::kUser) return fail(h, WS_ERR_INVALID_ARGUMENT, "registered envs: ws_rollout only");
   cudaError_t e = ws::launch_sample(kargs(h), launch_of(h), h->cursor, h->t, probs, row_stride, &h->launches);
   if (e) return cuda_fail(h, e, "sample kernel");
   h->sampled_slot = h->cursor;
@@ -416,6 +447,7 @@ ws_status ws_step(ws_env* h, const void* actions) {
   ws_status s = ensure_store(h, 1000);
   if (s) return s;
   if (h->cursor >= h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "cursor at store capacity (ws_rewind)");
+  if (h->spec.kind == ws::kUser) return fail(h, WS_ERR_INVALID_ARGUMENT, "registered envs: ws_rollout only");
   if (!actions && h->sampled_slot != h->cursor) return fail(h, WS_ERR_BAD_STATE, "ws_step(NULL) needs ws_sample first");
   cudaError_t e = cudaMemsetAsync(h->stats + 4 * (size_t)h->cursor, 0, 4 * sizeof(unsigned long long), h->stream);
   if (!e) e = ws::launch_step(kargs(h), launch_of(h), h->cursor, actions, &h->launches);
@@ -435,7 +467,15 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
   if (s) return s;
   if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
   cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
-  if (!e) e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
+  if (!e && h->spec.kind == ws::kUser) {  // NEXT-N4: NVRTC-compiled fused roll-out
+    if (h->timing) mark_kernel(h, ws::kKRollout, 0);
+    e = ws::launch_user_rollout(ws::UserLaunch{kargs(h), h->spec.user, h->user_prm, h->user_shared, h->stream}, T,
+                                h->t, probs, row_stride, step_stride);
+    if (h->timing) mark_kernel(h, ws::kKRollout, 1);
+    h->launches += 1;
+  } else if (!e) {
+    e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
+  }
   if (e) return cuda_fail(h, e, "rollout kernel");
   if (h->peer_attached) {  // A8 across GPUs: merged statistics in place, no NCCL call
     ws::PeerArgs pa{};
@@ -478,7 +518,7 @@ ws_status ws_rollout_policy(ws_env* h, int32_t T, const float* weights, int32_t 
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
-  if (h->A != 1 || h->spec.n_actions < 1 || h->spec.kind == ws::kTag)
+  if (h->A != 1 || h->spec.n_actions < 1 || h->spec.kind == ws::kTag || h->spec.kind == ws::kUser)
     return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_rollout_policy: single-agent discrete envs (cartpole, acrobot, dummy)");
   DeviceGuard g(h->device);
   ws_status st = ensure_store(h, T);

@@ -68,7 +68,8 @@ class Env:
     def __init__(self, n_envs: int, n_agents: int = 1, env: str = "cartpole", seed: int = 0, *,
                  env_offset: int = 0, n_envs_global: int = 0, device=None, stream: Optional[torch.cuda.Stream] = None,
                  t_capacity: int = 0, max_steps: int = 0, write_logp: bool = True, param0: int = 0,
-                 param1: int = 0, block_size: int = 0, torch_allocator: bool = True):
+                 param1: int = 0, block_size: int = 0, torch_allocator: bool = True,
+                 env_prm: Optional[torch.Tensor] = None, env_shared: Optional[torch.Tensor] = None):
         L = lib()
         if not torch.cuda.is_available():
             raise WSError(_abi.CUDA_ERROR, "no CUDA device: libws runs on the GPU only (no CPU fallback)")
@@ -91,6 +92,12 @@ class Env:
         cfg.param0 = param0
         cfg.param1 = param1
         cfg.block_size = block_size
+        for name, t in (("env_prm", env_prm), ("env_shared", env_shared)):  # NEXT-N4 registered envs
+            if t is not None:
+                if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+                    raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 device tensor")
+                setattr(cfg, name, t.data_ptr())
+        self._env_data = (env_prm, env_shared)
         self.allocator = _TorchAllocator(self.device) if torch_allocator else None
         if self.allocator is not None:
             cfg.alloc = self.allocator.c_alloc
@@ -189,6 +196,15 @@ class Env:
         """Pinned host tensors shaped like the first T slots of the store slabs (for rollout_staged)."""
         return {k: torch.empty((T,) + tuple(v.shape[1:]), dtype=v.dtype).pin_memory()
                 for k, v in self.buffers().items() if k in ("obs", "act", "logp", "rew", "done") and v is not None}
+
+    def set_env_data(self, prm: Optional[torch.Tensor] = None, shared: Optional[torch.Tensor] = None):
+        """NEXT-N4: per-replica parameters [E, n_params] and shared read-only data of a
+        registered env (float32 device tensors, kept alive by the handle; ws_set_env_data)."""
+        for name, t in (("prm", prm), ("shared", shared)):
+            if t is not None and (t.dtype != torch.float32 or t.device != self.device or not t.is_contiguous()):
+                raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 tensor on the handle's device")
+        check(lib().ws_set_env_data(self._h, _ptr(prm), _ptr(shared)), self._h)
+        self._env_data = (prm, shared)
 
     def synchronize(self):
         check(lib().ws_synchronize(self._h), self._h)
@@ -305,6 +321,25 @@ class Env:
         obj.__cuda_array_interface__ = {"shape": shape, "typestr": typestr, "data": (int(ptr), False),
                                         "version": 3, "strides": None}
         return torch.as_tensor(obj, device=self.device)
+
+
+def register_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions: int, n_reset_draws: int,
+                 max_steps: int, n_params: int = 0) -> str:
+    """NEXT-N4: compile a C-source environment with NVRTC into the fused roll-out template
+    (ws.h ws_register_env); afterwards Env(E, 1, name, ...) runs it.  Returns the NVRTC log;
+    raises WSError (with the log) on a compile error.  Re-registering the same name with the
+    same source is a no-op."""
+    L = lib()
+    if L.ws_registered_env(name.encode()):
+        return ""
+    d = _abi.ws_env_def(name.encode(), source.encode(), state_dim, obs_dim, n_actions, n_reset_draws, max_steps,
+                        n_params)
+    buf = C.create_string_buffer(1 << 16)
+    st = L.ws_register_env(C.byref(d), buf, len(buf))
+    log = buf.value.decode(errors="replace")
+    if st != _abi.OK:
+        raise WSError(st, log)
+    return log
 
 
 def _numel(shape) -> int:

@@ -33,7 +33,7 @@ def test_struct_layouts_match_header():
     assert C.sizeof(_abi.ws_buffers) == 11 * C.sizeof(_abi.ws_tensor)
     assert C.sizeof(_abi.ws_stats) == 6 * 8
     assert C.sizeof(_abi.ws_info) == 8 * 4 + 3 * 8 + 2 * 8 + 2 * 4
-    assert C.sizeof(_abi.ws_config) == 8 * 3 + 8 + 8 + 8 + 8 + 8 + 6 * 4 + 3 * 8
+    assert C.sizeof(_abi.ws_config) == 8 * 3 + 8 + 8 + 8 + 8 + 8 + 6 * 4 + 3 * 8 + 2 * 8  # + env_prm, env_shared
 
 
 def _create(**kw):
@@ -158,3 +158,25 @@ def test_staged_argument_validation_without_gpu():
     L = P.lib()
     hs = _abi.ws_host_store()
     assert L.ws_rollout_staged(None, 4, None, 0, 0, 0, C.byref(hs), None) == _abi.INVALID_ARGUMENT
+
+
+def test_register_env_compiles_without_gpu():
+    """NEXT-N4: ws_register_env compiles user C source with NVRTC for sm_100a on a CPU-only
+    host; errors come back as WS_ERR_INVALID_ARGUMENT with the compiler log."""
+    import wsinputs.user_envs as U
+    L = P.lib()
+    log = P.register_env("h_mountaincar", U.MOUNTAINCAR_SRC, **U.MOUNTAINCAR)
+    assert L.ws_registered_env(b"h_mountaincar") == 1
+    assert P.register_env("h_mountaincar", U.MOUNTAINCAR_SRC, **U.MOUNTAINCAR) == ""  # idempotent
+    with pytest.raises(P.WSError) as ex:
+        P.register_env("h_broken", "WS_FN int ws_env_step(float *s) { return undefined_symbol; }", 2, 2, 3, 1, 10)
+    assert ex.value.status == _abi.INVALID_ARGUMENT and "undefined_symbol" in str(ex.value)
+    assert L.ws_registered_env(b"h_broken") == 0
+    buf = C.create_string_buffer(256)
+    for bad in (dict(name=b"cartpole"), dict(state_dim=0), dict(obs_dim=33), dict(n_actions=1), dict(max_steps=0),
+                dict(n_params=65), dict(source=None)):
+        d = dict(name=b"h_x", source=U.MOUNTAINCAR_SRC.encode(), state_dim=2, obs_dim=2, n_actions=3,
+                 n_reset_draws=1, max_steps=200, n_params=0)
+        d.update(bad)
+        assert L.ws_register_env(C.byref(_abi.ws_env_def(**d)), buf, 256) == _abi.INVALID_ARGUMENT, bad
+    assert L.ws_set_env_data(None, None, None) == _abi.INVALID_ARGUMENT

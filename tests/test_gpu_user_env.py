@@ -1,0 +1,112 @@
+"""NEXT-N4 on the GPU: environments registered as C source (ws_register_env, NVRTC ->
+sm_100a fused roll-out template) against the oracle's registered-env path (pinned in
+tests/test_oracle_user_env.py), element by element; CartPole written as a user env against
+the hand-written built-in CartPole kernel; per-replica parameters and shared data; sharding
+invariance; the single-step path is refused."""
+import numpy as np
+import pytest
+import torch
+
+import oracle as O
+import wsinputs as W
+import wsinputs.user_envs as U
+
+pytestmark = pytest.mark.gpu
+SEED = W.SEED
+
+
+@pytest.fixture(scope="module")
+def P():
+    if not torch.cuda.is_available():
+        pytest.skip("needs a GPU")
+    import paper_2408_00930_b200 as P
+    for name, (src, dims) in U.ENVS.items():
+        P.register_env(name, src, **dims)
+        O.register_user_env(name, src, **dims)
+    return P
+
+
+KEYS = ("obs", "act", "logp", "rew", "done", "stats", "state", "obs_live", "reset_count", "ep_step")
+
+
+def same(buf, o, T):
+    for k in KEYS:
+        ref = o.array(k)
+        got = buf[k]
+        if k in ("obs", "act", "logp", "rew", "done"):
+            got, ref = got[:T], ref[:T]
+        if k == "stats":
+            continue
+        assert np.array_equal(got, ref, equal_nan=True), k
+
+
+@pytest.mark.parametrize("name,E,T,max_steps", [("u_cartpole", 1000, 300, 0), ("u_cartpole", 77, 120, 25),
+                                                ("u_mountaincar", 513, 450, 0), ("u_mountaincar", 1, 10, 3)])
+def test_registered_env_matches_oracle(P, name, E, T, max_steps):
+    n = U.ENVS[name][1]["n_actions"]
+    probs = W.random_probs(E, 1, n, seed=21, zero_frac=0.2)
+    g = P.Env(E, 1, name, SEED, t_capacity=T, max_steps=max_steps)
+    g.rollout(T, torch.from_numpy(probs).cuda())
+    assert g.status() == 0
+    o = O.Batch(name, E, 1, SEED, t_capacity=T, max_steps=max_steps)
+    assert o.rollout(T, probs) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    same(buf, o, T)
+    assert np.array_equal(g.stats_f64(T).cpu().numpy(), o.array("stats")[:T])
+
+
+def test_user_cartpole_equals_builtin_kernel(P):
+    """The NVRTC-compiled user CartPole and the hand-written k_rollout_discrete<CartPole>
+    produce the same store bit for bit (both follow R3-R6 and the engine readings)."""
+    E, T = 4096, 400
+    probs = torch.from_numpy(W.random_probs(E, 1, 2, seed=22)).cuda()
+    a = P.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    b = P.Env(E, 1, "u_cartpole", SEED, t_capacity=T)
+    a.rollout(T, probs)
+    b.rollout(T, probs)
+    A = {k: v.cpu().numpy() for k, v in a.buffers().items() if v is not None}
+    B = {k: v.cpu().numpy() for k, v in b.buffers().items() if v is not None}
+    for k in ("obs", "act", "logp", "rew", "done", "stats", "state", "obs_live", "reset_count", "ep_step"):
+        assert np.array_equal(A[k], B[k], equal_nan=True), k
+
+
+def test_pointmass_parameters_and_shared_grid(P):
+    E, T = 700, 200
+    prm, grid = U.pointmass_data(E)
+    probs = W.random_probs(E, 1, 3, seed=23)
+    tp, tg = torch.from_numpy(prm).cuda(), torch.from_numpy(grid).cuda()
+    g = P.Env(E, 1, "u_pointmass", SEED, t_capacity=T, env_prm=tp, env_shared=tg)
+    g.rollout(T, torch.from_numpy(probs).cuda())
+    o = O.Batch("u_pointmass", E, 1, SEED, t_capacity=T, env_prm=prm, env_shared=grid)
+    assert o.rollout(T, probs) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    same(buf, o, T)
+    # a parameter change through ws_set_env_data + ws_reset takes effect
+    prm2 = prm.copy()
+    prm2[:, 1] = 0.0
+    g.set_env_data(torch.from_numpy(prm2).cuda(), tg)
+    g.reset()
+    g.rollout(T, torch.from_numpy(probs).cuda())
+    o2 = O.Batch("u_pointmass", E, 1, SEED, t_capacity=T, env_prm=prm2, env_shared=grid)
+    assert o2.rollout(T, probs) == 0
+    same({k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}, o2, T)
+
+
+def test_sharded_registered_env(P):
+    """Two shards of a registered env equal the corresponding replicas of one unsharded run
+    (streams keyed by the global replica index, R15)."""
+    E, T = 300, 100
+    probs = torch.from_numpy(W.random_probs(E, 1, 3, seed=24)).cuda()
+    full = P.Env(E, 1, "u_mountaincar", SEED, t_capacity=T)
+    full.rollout(T, probs)
+    F = full.buffers()["obs"].cpu().numpy()
+    h = 128
+    s1 = P.Env(E - h, 1, "u_mountaincar", SEED, env_offset=h, n_envs_global=E, t_capacity=T)
+    s1.rollout(T, probs[h:].contiguous())
+    assert np.array_equal(s1.buffers()["obs"].cpu().numpy(), F[:, h:])
+
+
+def test_single_step_path_refused(P):
+    g = P.Env(8, 1, "u_mountaincar", SEED, t_capacity=4)
+    with pytest.raises(P.WSError):
+        g.sample(torch.full((8, 1, 3), 1 / 3, device="cuda"))

@@ -1,0 +1,78 @@
+"""Pins of the oracle's NEXT-N4 registered-env path (oracle/wso.cpp K_USER, DESIGN R32):
+CartPole rewritten as a user env must reproduce the already-pinned built-in CartPole
+roll-out bit for bit (same engine semantics around a different step function), MountainCar
+obeys gym's rules (velocity and position bounds, inelastic left wall, goal, reward -1,
+truncation at 200), and the point mass reads its per-replica parameters and the shared map."""
+import numpy as np
+import pytest
+
+import oracle as O
+import wsinputs as W
+import wsinputs.user_envs as U
+
+SEED = W.SEED
+
+
+@pytest.fixture(scope="module", autouse=True)
+def registered():
+    for name, (src, dims) in U.ENVS.items():
+        O.register_user_env(name, src, **dims)
+
+
+def test_user_cartpole_equals_builtin():
+    E, T = 64, 600
+    probs = W.random_probs(E, 1, 2, seed=3)
+    a = O.Batch("cartpole", E, 1, SEED, t_capacity=T, max_steps=30)
+    b = O.Batch("u_cartpole", E, 1, SEED, t_capacity=T, max_steps=30)
+    assert a.rollout(T, probs) == 0 and b.rollout(T, probs) == 0
+    for k in ("obs", "act", "logp", "rew", "done", "stats", "state", "obs_live", "reset_count", "ep_step"):
+        assert np.array_equal(a.array(k), b.array(k), equal_nan=True), k
+    assert (a.array("done")[:T] & 2).any() and (a.array("done")[:T] & 1).any()  # both done kinds
+
+
+def test_mountaincar_rules():
+    E, T = 200, 400
+    o = O.Batch("u_mountaincar", E, 1, SEED, t_capacity=T)
+    assert o.rollout(T, W.random_probs(E, 1, 3, seed=4)) == 0
+    obs, rew, done = o.array("obs")[:T], o.array("rew")[:T], o.array("done")[:T]
+    x, v = obs[..., 0, 0], obs[..., 0, 1]
+    assert np.all(rew == -1.0)
+    assert np.all((x >= -1.2) & (x <= 0.6)) and np.all(np.abs(v) <= 0.07)
+    # initial distribution U(-0.6, -0.4), v = 0 (every slot right after a reset)
+    first = np.concatenate([obs[0, :, 0]] + [obs[t + 1, done[t] != 0, 0] for t in range(T - 1)])
+    assert np.all((first[:, 0] >= -0.6) & (first[:, 0] < -0.4)) and np.all(first[:, 1] == 0)
+    # random actions essentially never reach the goal: truncation at exactly 200 steps
+    assert (done == 2).sum() >= E and np.all(o.array("stats")[:T][:, 2][o.array("stats")[:T][:, 0] > 0] % 200 == 0)
+    # inelastic left wall: a state at x = -1.2 never carries negative velocity
+    assert np.all(v[x == -1.2] >= 0)
+
+
+def test_mountaincar_step_from_rest_closed_form():
+    """From x = -pi/6 (the valley floor, cos(3x) = 0 up to rounding), v = 0, a push right
+    adds exactly the force 0.001 (gravity term vanishes to fp32 precision): one step."""
+    E = 1
+    o = O.Batch("u_mountaincar", E, 1, SEED, t_capacity=1)
+    st = o.array("state")
+    st[0, 0] = np.float32(-np.pi / 6)
+    st[0, 1] = 0.0
+    assert o.step(np.array([2], np.int32)) == 0
+    s = o.array("state")[0]
+    assert abs(s[1] - 0.001) < 1e-9 and abs(s[0] - (np.float32(-np.pi / 6) + s[1])) < 1e-7
+
+
+def test_pointmass_parameters_and_shared_map():
+    E, T = 32, 150
+    prm, grid = U.pointmass_data(E)
+    o = O.Batch("u_pointmass", E, 1, SEED, t_capacity=T, env_prm=prm, env_shared=grid)
+    assert o.rollout(T, W.random_probs(E, 1, 3, seed=6)) == 0
+    rew = o.array("rew")[:T, :, 0]
+    obs = o.array("obs")[:T, :, 0]
+    assert np.all(np.isin(rew, grid))                          # rewards come from the shared map
+    assert np.array_equal(obs[:, :, 2], np.broadcast_to(prm[:, 0], (T, E)))  # obs carries prm[0]
+    # parameter jitter: the same actions with another force gain give other trajectories
+    prm2 = prm.copy()
+    prm2[:, 0] *= 2
+    o2 = O.Batch("u_pointmass", E, 1, SEED, t_capacity=T, env_prm=prm2, env_shared=grid)
+    assert o2.rollout(T, W.random_probs(E, 1, 3, seed=6)) == 0
+    assert np.array_equal(o.array("act")[:1], o2.array("act")[:1])
+    assert not np.array_equal(o.array("obs")[2:, :, :, :2], o2.array("obs")[2:, :, :, :2])
