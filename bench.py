@@ -33,6 +33,23 @@ import wsinputs as W  # noqa: E402
 # that writes them: the roll-out kernel writes obs (D_obs*4) + rew (4) + done (1); the plan
 # kernel writes act (4) + logp (4).  Per agent; done is per replica.
 OBS_DIM = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3, "tag": 4, "surface": 21}
+# NEXT-N4 registered env (k_user_rollout samples in-loop: it writes obs + act + logp + rew + done)
+USER_BYTES = {"u_cartpole": 4 * 4 + 4 + 4 + 4 + 1}
+
+
+def register_user(w, oracle_side: bool):
+    """Register a NEXT-N4 workload's C-source env (product: NVRTC; oracle: g++)."""
+    name = w.params.get("user")
+    if not name:
+        return
+    import wsinputs.user_envs as U
+    src, dims = U.ENVS[name]
+    if oracle_side:
+        import oracle as O
+        O.register_user_env(name, src, **dims)
+    else:
+        from paper_2408_00930_b200 import register_env
+        register_env(name, src, **dims)
 # algorithmic bytes per env-step (DESIGN section 5): the roll-out kernel writes obs + rew + done
 # and reads its actions (discrete: the packed plan, 1 byte; continuous: the act slab, 4 d);
 # the plan kernel writes act + logp (+ the packed plan for discrete envs)
@@ -166,6 +183,7 @@ def cpu_baseline(w, budget_s: float = 10.0):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
+    register_user(w, oracle_side=True)
     if w.params.get("gae"):
         oracle_gae_inputs(w)
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
@@ -194,6 +212,7 @@ def run_reference(args, w):
     import oracle as O
     cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
+    register_user(w, oracle_side=True)
     if w.params.get("gae"):
         oracle_gae_inputs(w)
     # each step = the workload's full roll-out (all replicas x T steps) unless one roll-out
@@ -255,6 +274,7 @@ def main():
     offset = rank * E
     params = (w.params.get("grid", w.params.get("dim", 0)), w.params.get("taggers", 0))
     stream = torch.cuda.current_stream(dev)
+    register_user(w, oracle_side=False)
     env = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
               param0=params[0], param1=params[1], block_size=args.block)
     probs_host = W.workload_probs(w)
@@ -385,11 +405,14 @@ def main():
     n_plan, plan_ms = diag_times.get("plan", (0, 0.0))
     # tag samples inside its roll-out kernel: obs 16 + rew 4 + act 4 + logp 4 per agent-step, done 1 per env-step
     roll_bytes = int(ROLLOUT_BYTES.get(w.env, 0) * E * A * T if w.env != "tag" else (16 + 4 + 4 + 4) * E * A * T + E * T)
+    if w.env in USER_BYTES:
+        roll_bytes = int(USER_BYTES[w.env] * E * A * T)
     if pol:  # the policy kernel also writes act + logp and reads no plan
         roll_bytes = int((4 * OBS_DIM[w.env] + 4 + 1 + 8) * E * A * T)
     achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
     call_ms = sum(kern_ms) / len(kern_ms)
-    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T if w.env not in ("tag",) and not pol else 0))
+    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T
+                                  if w.env not in ("tag",) and w.env not in USER_BYTES and not pol else 0))
     # NEXT-N2: GAE reads rew + values and writes adv + returns (16 B per agent-step), reads
     # the replica's done byte (1 B per replica-step) and the bootstrap row once
     gae_bytes = 16 * E * A * T + E * T + 4 * E * A if gae else 0
@@ -397,7 +420,8 @@ def main():
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
-                "kernel": KERNEL_NAME.get(w.env, "k_rollout"),
+                "kernel": KERNEL_NAME.get(w.env, "k_user_rollout (NVRTC, registered env)" if w.env in USER_BYTES
+                                          else "k_rollout"),
                 "kernel_ms": round(roll_ms, 4), "launches_timed": n_roll,
                 "bytes_per_launch": roll_bytes, "bytes_per_env_step": roll_bytes / (E * A * T),
                 "other_kernels": {"note": f"diagnostic pass of {n_diag} steps after the timed region",

@@ -178,9 +178,46 @@ WS_FN int ws_sample(const float* p, float u, float* lp) {
 }
 
 WS_FN ws_i64 ws_fx(float v) { return __float2ll_rn(v * 4294967296.0f); }
+/* exact warp sum of 64-bit values (two's complement, mod 2^64): four 16-bit chunks, one
+   REDUX each (32 x (2^16 - 1) < 2^32), recombined */
 WS_FN ws_i64 ws_wsum(ws_i64 v) {
-  for (int o = 16; o > 0; o >>= 1) v += __shfl_down_sync(0xffffffffu, v, o);
-  return v;
+  const ws_u64 u = (ws_u64)v;
+  ws_u64 t = 0;
+  for (int k = 0; k < 4; ++k) t += (ws_u64)__reduce_add_sync(0xffffffffu, (ws_u32)((u >> (16 * k)) & 0xffffu)) << (16 * k);
+  return (ws_i64)t;
+}
+
+/* R13 sampler state for a probability row that is constant over the roll-out (step_stride
+   0): prefix sums, total and log-probabilities computed once per replica */
+struct WsRow {
+  double C[WS_N];
+  double S;
+  float lp[WS_N];
+  int last;
+  bool bad;
+};
+WS_FN void ws_row_init(const float* p, WsRow& r) {
+  r.S = 0.0; r.last = -1; r.bad = false;
+  for (int i = 0; i < WS_N; ++i) {
+    const float x = p[i];
+    r.bad = r.bad || !(x >= 0.0f) || !isfinite(x);
+    r.S += (double)x;
+    r.C[i] = r.S;
+    if (x > 0.0f) r.last = i;
+  }
+  r.bad = r.bad || !(r.S > 0.0) || !isfinite(r.S);
+  const double lS = r.bad ? 0.0 : log(r.S);
+  for (int i = 0; i < WS_N; ++i) r.lp[i] = (!r.bad && p[i] > 0.0f) ? (float)(log((double)p[i]) - lS) : 0.0f;
+}
+WS_FN int ws_row_draw(const WsRow& r, const float* p, float u, float* lp) {
+  if (r.bad) { *lp = __int_as_float(0x7fc00000); return -1; }
+  const double target = (double)u * r.S;
+  int chosen = -1;
+  for (int i = 0; i < WS_N; ++i)
+    if (chosen < 0 && p[i] > 0.0f && target < r.C[i]) chosen = i;
+  if (chosen < 0) chosen = r.last;
+  *lp = r.lp[chosen];
+  return chosen;
 }
 
 extern "C" __global__ void k_user_reset(const WsUserArgs a) {
@@ -214,12 +251,24 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
   ws_u32 rc = a.reset_count[e];
   float ep_ret = a.ep_ret[e];
   ws_u32 err = 0;
+  const bool hoist = step_stride == 0;    /* same row every step: CDF and logs once */
+  float p0[WS_N];
+  WsRow row;
+  if (hoist) {
+    for (int i = 0; i < WS_N; ++i) p0[i] = probs[e * row_stride + i];
+    ws_row_init(p0, row);
+  }
+  ws_u32 w4[4] = {0u, 0u, 0u, 0u};
   for (int c = 0; c < T; ++c) {
     const ws_u64 t = t0 + (ws_u64)c;
     const ws_i64 idx = (ws_i64)c * a.E + e;
     if (live) for (int i = 0; i < WS_D; ++i) __stcs(a.obs + idx * WS_D + i, o[i]);   /* R12 */
+    /* ACTION stream: one Philox block serves 4 consecutive steps (draw j = t, R15) */
+    if (c == 0 || (t & 3) == 0) ws_philox((ws_u32)(t >> 2), eg, 0u, 1u, a.k0, a.k1, w4);
+    const float u = ws_u01(w4[t & 3]);
     float lp;
-    const int act = ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, ws_u01(ws_draw(a, eg, 1u, t)), &lp);
+    const int act = hoist ? ws_row_draw(row, p0, u, &lp)
+                          : ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, u, &lp);
     if (live) {
       __stcs(a.act + idx, act);
       if (a.write_logp) __stcs(a.logp + idx, lp);

@@ -56,6 +56,10 @@ CONFIGS = {
     # cost WarpSci removes
     "C2X": Workload("C2X", "cartpole", 10000, 1, 1000, 2, 1, {"staged": True},
                     note="CartPole-v1 10K envs x 1000 steps through the copy-based baseline pipeline (NEXT-N3)"),
+    # NEXT-N4: C2 with CartPole supplied as user C source through the runtime
+    # env composer (NVRTC-compiled generic template) instead of the hand-written kernel
+    "C2U": Workload("C2U", "u_cartpole", 10000, 1, 1000, 2, 1, {"user": "u_cartpole"},
+                    note="CartPole-v1 10K envs x 1000 steps, env registered as C source (NVRTC composer, NEXT-N4)"),
     "C4G": Workload("C4G", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10, "gae": (0.99, 0.95)},
                     note="tag 1K envs x 100 agents x 200 + GAE(0.99, 0.95) over the store (NEXT-N2)"),
 }
