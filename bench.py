@@ -357,8 +357,8 @@ def main():
     if st != 0:
         raise RuntimeError(f"libws reported status {st} during the timed region")
     launches = env.info().launches - launches0
-    if trainer is not None:  # handle-free A2C kernels per step: values x2, moments + final, grad + final, Adam
-        launches += 7 * args.steps
+    if trainer is not None:  # handle-free A2C kernels per step: moments + final, grad + final, Adam
+        launches += 5 * args.steps
     ktimes = env.kernel_times()
     env.enable_kernel_timing(False)
     clk = clocks.stop() if not args.ncu else {}
@@ -385,7 +385,7 @@ def main():
     if trainer is not None:  # the update alone (critic, GAE, moments, gradient, Adam)
         for k in range(n_diag):
             dev_ev[2 * k].record(stream)
-            trainer.update(T)
+            trainer.update(T, values_ready=True)
             dev_ev[2 * k + 1].record(stream)
         torch.cuda.synchronize(dev)
         upd_ms = sum(dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)) / n_diag
@@ -459,7 +459,7 @@ def main():
         roofline["staged_pipeline"]["transfer_share"] = round(staged_rep["transfer_ms"] / staged_rep["total_ms"], 4)
     if trainer is not None:
         roofline["a2c_update"] = {"ms": round(upd_ms, 4), "rows": E * A * T,
-                                  "note": "ac_values x2 + gae + moments + gradient + clip/Adam, diagnostic pass",
+                                  "note": "gae + moments + gradient + clip/Adam (the critic comes from the roll-out kernel), diagnostic pass",
                                   "loss_last": [round(x, 6) for x in trainer.loss.cpu().tolist()]}
     if gae:
         n_gae, gae_ms = ktimes.get("gae", (0, 0.0))

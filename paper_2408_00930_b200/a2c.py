@@ -4,7 +4,8 @@ P:41 "supports actor-critic algorithms", "roll-outs, action inference, rese
 training" in one GPU-resident store, P:106 / P:122 "zero data transfer").
 
 Argument marshalling only: every arithmetic step runs in libws's kernels --
-ws_rollout_policy (roll-out with in-kernel policy inference), ws_ac_values (critic),
+ws_rollout_actor_critic (roll-out with in-kernel policy inference that also writes the
+critic's values from the same hidden layer), ws_ac_values (stand-alone critic),
 ws_gae_store (advantages over the store, in place), ws_a2c_moments / ws_a2c_grad
 (normalised-advantage actor-critic gradient) and ws_adam (clip + Adam).  Data parallel:
 each rank trains on its replica shard; the two fp64 moments and the gradient are summed
@@ -147,8 +148,14 @@ class A2C:
         if self.world > 1:
             dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
 
-    def update(self, T: int):
-        """One A2C update on store slots [0, T) (already rolled out with self.params)."""
+    def _value_buf(self, rows: int) -> torch.Tensor:
+        if self._values is None or self._values.numel() != rows:
+            self._values = torch.empty(rows, dtype=torch.float32, device=self.env.device)
+        return self._values
+
+    def update(self, T: int, values_ready: bool = False):
+        """One A2C update on store slots [0, T) (already rolled out with self.params).
+        values_ready: the roll-out already wrote the critic (ws_rollout_actor_critic)."""
         env, D, H, N, hp = self.env, self.D, self.H, self.N, self.hp
         s = env.stream
         with torch.cuda.stream(s):
@@ -156,10 +163,10 @@ class A2C:
             rows = T * self.E
             obs = buf["obs"][:T].reshape(rows * D)
             act = buf["act"][:T].reshape(rows)
-            if self._values is None or self._values.numel() != rows:
-                self._values = torch.empty(rows, dtype=torch.float32, device=env.device)
-            ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
-            ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
+            self._value_buf(rows)
+            if not values_ready:
+                ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
+                ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
             adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
                                      hp["gamma"], hp["lam"])
             moments(adv.view(-1), self.ws, out=self.mom, stream=s)
@@ -173,6 +180,8 @@ class A2C:
         self._adv = adv  # alive until the stream consumed it
 
     def iteration(self, T: int):
-        """Roll out T steps with the current policy, then update (train)."""
-        self.env.rollout_policy(T, self.params, self.H)
-        self.update(T)
+        """Roll out T steps with the current policy (the kernel also writes the critic's values
+        from the hidden layer it already computes), then update (train)."""
+        vals = self._value_buf(T * self.E)
+        self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap)
+        self.update(T, values_ready=True)

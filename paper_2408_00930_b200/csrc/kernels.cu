@@ -723,13 +723,18 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
 // the state, so there is no plan kernel.  The network is tiny (D x H + H x N MACs per
 // replica-step) and per-replica, so it runs on the FMA pipe rather than the tensor cores.
 // =======================================================================================
-template <class Env, int H>
+// kCritic (NEXT-N2, R31): the weights carry a value head wv [H] | bv after b2 and the kernel
+// also writes values[t][e] = V(obs[t]) (the pre-step observation of slot t) and, after the
+// last step, bootstrap[e] = V(obs_live): v = bv, then v = fma(wv_j, h_j, v) for j = 0..H-1,
+// from the hidden layer the policy already computed (no second pass over the store).
+template <class Env, int H, bool kCritic>
 __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int T, const uint64_t t0,
-                                                       const float* __restrict__ weights) {
+                                                       const float* __restrict__ weights,
+                                                       float* __restrict__ values, float* __restrict__ bootstrap) {
   using L = Lane<Env>;
   using St = typename L::St;
   constexpr int D = L::D, N = L::N;
-  constexpr int NW = D * H + H + H * N + N;
+  constexpr int NW = D * H + H + H * N + N + (kCritic ? H + 1 : 0);
   constexpr int kRows = 16;
   __shared__ __align__(16) float sw[NW];
   extern __shared__ __align__(16) uint32_t ws_smem[];
@@ -739,6 +744,7 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
   const float* b1 = W1 + D * H;
   const float* W2 = b1 + H;
   const float* b2 = W2 + H * N;
+  const float* wv = b2 + N;  // kCritic only
   const int lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = a.E;
@@ -774,6 +780,12 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
 #pragma unroll
       for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
       hid[j] = acc > 0.0f ? acc : 0.0f;
+    }
+    if constexpr (kCritic) {
+      float v = wv[H];
+#pragma unroll
+      for (int j = 0; j < H; ++j) v = __fmaf_rn(wv[j], hid[j], v);
+      if (live) st_cs(values + idx, v);
     }
     float lg[N];
 #pragma unroll
@@ -842,6 +854,19 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
     if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
       win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, nlive);
+  }
+  if constexpr (kCritic) {  // bootstrap value of the observation after the last step
+    float o[D];
+    L::obs_vals(s, aux, o);
+    float v = wv[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      float acc = b1[j];
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
+      v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
+    }
+    if (live) bootstrap[e] = v;
   }
   if (live) {
     L::save(a.state + e * L::S, s);
@@ -1991,25 +2016,34 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                  int hidden) {
+                                  int hidden, float* values, float* bootstrap) {
   const size_t smem = 4 * 3 * 16 * kWinStride * sizeof(uint32_t);  // 4 warps x 16-row windows
+  const unsigned g = grid_for(a.E, 128);
   l.m(kKRollout, 0);
-  switch (hidden) {
-    case 32: k_rollout_policy<Env, 32><<<grid_for(a.E, 128), 128, smem, l.stream>>>(a, T, t0, weights); break;
-    case 64: k_rollout_policy<Env, 64><<<grid_for(a.E, 128), 128, smem, l.stream>>>(a, T, t0, weights); break;
-    default: return cudaErrorInvalidValue;
+  if (values) {
+    switch (hidden) {
+      case 32: k_rollout_policy<Env, 32, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 64: k_rollout_policy<Env, 64, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (hidden) {
+      case 32: k_rollout_policy<Env, 32, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 64: k_rollout_policy<Env, 64, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      default: return cudaErrorInvalidValue;
+    }
   }
   l.m(kKRollout, 1);
   return cudaGetLastError();
 }
 
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                  int hidden, uint64_t* launches) {
+                                  int hidden, uint64_t* launches, float* values, float* bootstrap) {
   cudaError_t err = cudaErrorInvalidValue;
   switch (l.kind) {
-    case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden); break;
-    case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden); break;
-    case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden); break;
+    case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden, values, bootstrap); break;
+    case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden, values, bootstrap); break;
+    case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden, values, bootstrap); break;
     default: break;
   }
   *launches += 1;

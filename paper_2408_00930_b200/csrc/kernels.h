@@ -65,8 +65,11 @@ cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_
                                    cudaStream_t s);
 
 // NEXT-N1: fused roll-out with in-kernel MLP policy inference (hidden 32 or 64)
+// values / bootstrap non-null: the weights carry the R31 value head and the kernel also writes
+// the critic's values [T, E] and bootstrap [E] (NEXT-N2)
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                  int hidden, uint64_t* launches);
+                                  int hidden, uint64_t* launches, float* values = nullptr,
+                                  float* bootstrap = nullptr);
 
 // NEXT-N2: generalised advantage estimation over the time-major store (gae.cu, R30)
 struct GaeArgs {

@@ -514,23 +514,36 @@ static void sum_stats(const long long* st, int n, ws_stats* out) {
   *out = r;
 }
 
-ws_status ws_rollout_policy(ws_env* h, int32_t T, const float* weights, int32_t hidden) {
+static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t hidden, float* values,
+                            float* bootstrap) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
   if (h->A != 1 || h->spec.n_actions < 1 || h->spec.kind == ws::kTag || h->spec.kind == ws::kUser)
-    return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_rollout_policy: single-agent discrete envs (cartpole, acrobot, dummy)");
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "policy roll-out: single-agent discrete envs (cartpole, acrobot, dummy)");
   DeviceGuard g(h->device);
   ws_status st = ensure_store(h, T);
   if (st) return st;
   if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
   cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
-  if (!e) e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches);
+  if (!e) e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches, values,
+                                        bootstrap);
   if (e) return cuda_fail(h, e, "policy roll-out kernel");
   h->t += (uint64_t)T;
   h->cursor = T;
   h->sampled_slot = -1;
   return WS_OK;
+}
+
+ws_status ws_rollout_policy(ws_env* h, int32_t T, const float* weights, int32_t hidden) {
+  return run_policy(h, T, weights, hidden, nullptr, nullptr);
+}
+
+ws_status ws_rollout_actor_critic(ws_env* h, int32_t T, const float* params, int32_t hidden, float* values,
+                                  float* bootstrap) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (!values || !bootstrap) return fail(h, WS_ERR_INVALID_ARGUMENT, "values and bootstrap are required");
+  return run_policy(h, T, params, hidden, values, bootstrap);
 }
 
 static ws_status run_gae(ws_env* h, const ws_gae_args* a, cudaStream_t s, const ws::Launch* l) {

@@ -234,6 +234,20 @@ class Env:
         check(lib().ws_rollout_policy(self._h, T, w.data_ptr(), hidden), self._h)
         self._keep = w  # alive until the stream has consumed it
 
+    def rollout_actor_critic(self, T: int, params: torch.Tensor, hidden: int, values: torch.Tensor,
+                             bootstrap: torch.Tensor) -> None:
+        """NEXT-N2: the policy roll-out that also writes the critic's values [T, E] and the
+        bootstrap values [E] (ws.h ws_rollout_actor_critic); params: R31 packed float32."""
+        w = params.contiguous()
+        for name, t in (("params", w), ("values", values), ("bootstrap", bootstrap)):
+            if t.dtype != torch.float32 or t.device != self.device or not t.is_contiguous():
+                raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 on the handle's device")
+        if values.numel() < T * self.n_envs or bootstrap.numel() < self.n_envs:
+            raise WSError(_abi.INVALID_ARGUMENT, "values [T, E] / bootstrap [E]")
+        check(lib().ws_rollout_actor_critic(self._h, T, w.data_ptr(), hidden, values.data_ptr(),
+                                            bootstrap.data_ptr()), self._h)
+        self._keep = w
+
     def gae_store(self, T: int, values: torch.Tensor, bootstrap: torch.Tensor, gamma: float, lam: float,
                   v_trunc: Optional[torch.Tensor] = None, out: Optional[tuple] = None):
         """NEXT-N2: advantages and returns of store slots [0, T) (ws.h ws_gae_store), reading

@@ -236,3 +236,30 @@ def test_cartpole_learns(P):
     first, last = np.mean(lengths[:5]), np.mean(lengths[-20:])
     print(f"cartpole A2C: mean episode length {first:.1f} -> {last:.1f}")
     assert first < 40 and last > 3 * first
+
+
+@pytest.mark.parametrize("env,H,E,T", [("cartpole", 64, 1000, 200), ("acrobot", 32, 257, 64)])
+def test_actor_critic_rollout_writes_critic(P, env, H, E, T):
+    """ws_rollout_actor_critic: the store is bit-identical to ws_rollout_policy's (the value
+    head only adds outputs), values[t] = V(obs[t]) and bootstrap = V(obs_live) within the
+    critic tolerance of the fp64 oracle."""
+    import paper_2408_00930_b200 as WS
+    D, N = {"cartpole": (4, 2), "acrobot": (6, 3)}[env]
+    params = W.a2c_params(D, H, N, seed=81)
+    tp = torch.from_numpy(params).cuda()
+    a = WS.Env(E, 1, env, SEED, t_capacity=T)
+    b = WS.Env(E, 1, env, SEED, t_capacity=T)
+    vals = torch.empty(T * E, device="cuda")
+    boot = torch.empty(E, device="cuda")
+    a.rollout_policy(T, tp, H)
+    b.rollout_actor_critic(T, tp, H, vals, boot)
+    A = {k: v.cpu().numpy() for k, v in a.buffers().items() if v is not None}
+    B = {k: v.cpu().numpy() for k, v in b.buffers().items() if v is not None}
+    for k in ("obs", "act", "logp", "rew", "done", "stats", "state", "obs_live"):
+        assert np.array_equal(A[k], B[k], equal_nan=True), k
+    obs = B["obs"][:T].reshape(-1, D)
+    _, _, _, _, wv, bv = OA.unpack(params, D, H, N)
+    for o, v in ((obs, vals.cpu().numpy()), (B["obs_live"].reshape(-1, D), boot.cpu().numpy())):
+        ref = OA.values(params, o, D, H, N)
+        h = OA.forward(params, o, D, H, N)[1]
+        assert np.all(np.abs(v - ref) <= 1e-5 * (np.abs(bv) + h @ np.abs(wv) + 1.0))
