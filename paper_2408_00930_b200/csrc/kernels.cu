@@ -2017,19 +2017,20 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, float* values, float* bootstrap) {
-  const size_t smem = 4 * 3 * 16 * kWinStride * sizeof(uint32_t);  // 4 warps x 16-row windows
-  const unsigned g = grid_for(a.E, 128);
+  const int b = l.block < 128 ? l.block : 128;                              // launch bounds 128
+  const size_t smem = (size_t)(b / 32) * 3 * 16 * kWinStride * sizeof(uint32_t);  // per-warp 16-row windows
+  const unsigned g = grid_for(a.E, b);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
-      case 64: k_rollout_policy<Env, 64, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 32: k_rollout_policy<Env, 32, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 64: k_rollout_policy<Env, 64, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
-      case 64: k_rollout_policy<Env, 64, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 32: k_rollout_policy<Env, 32, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 64: k_rollout_policy<Env, 64, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
       default: return cudaErrorInvalidValue;
     }
   }
