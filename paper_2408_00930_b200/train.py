@@ -77,6 +77,7 @@ def main(argv=None):
     ap.add_argument("--target", type=float, default=None)
     ap.add_argument("--log-every", type=int, default=10)
     ap.add_argument("--csv", default="-")
+    ap.add_argument("--seed", type=lambda x: int(x, 0), default=0x24080930)
     a = ap.parse_args(argv)
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
         local = int(os.environ.get("LOCAL_RANK", 0))
@@ -84,7 +85,7 @@ def main(argv=None):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     out = sys.stdout if a.csv == "-" else open(a.csv, "w", newline="")
     train(a.env, a.envs, a.T, a.iters, a.hidden, a.lr, a.gamma, a.lam, c_e=a.entropy, target=a.target,
-          log_every=a.log_every, out=out)
+          log_every=a.log_every, seed=a.seed, out=out)
     if out is not sys.stdout:
         out.close()
     if dist.is_initialized():
