@@ -800,10 +800,21 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
     RowCDF<N> cdf;
     float S = 0.0f;
+    if constexpr (N == 2) {
+      // exp(l_max - m) = exp(0) = 1 exactly: one fp64 exponential per step instead of two
+      // (bit-identical to the loop below, including non-finite logits -> NaN -> invalid row)
+      const bool k0 = !(lg[1] > lg[0]);  // m == lg[0]
+      const float eo = (float)exp((double)fsub(k0 ? lg[1] : lg[0], m));
+      const float em = isfinite(m) ? 1.0f : __int_as_float(0x7fc00000);
+      cdf.P[0] = k0 ? em : eo;
+      cdf.P[1] = k0 ? eo : em;
+      S = fadd(fadd(S, cdf.P[0]), cdf.P[1]);
+    } else {
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      cdf.P[i] = (float)exp((double)fsub(lg[i], m));
-      S = fadd(S, cdf.P[i]);
+      for (int i = 0; i < N; ++i) {
+        cdf.P[i] = (float)exp((double)fsub(lg[i], m));
+        S = fadd(S, cdf.P[i]);
+      }
     }
     double run = 0.0;
     bool badp = false;
@@ -817,7 +828,7 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     cdf.bad = badp || !(run > 0.0) || !isfinite(run);
     // ---- A2 draw (R13) from the ACTION stream
     int act = search<N>(cdf, u01(pick(w4, (uint32_t)(t & 3))));
-    float lp = logp_of<N>(cdf, act);
+    float lp = logp_of_normalised<N>(cdf, act);
     if (cdf.bad) {
       act = -1;
       lp = __int_as_float(0x7fc00000);

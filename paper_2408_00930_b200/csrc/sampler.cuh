@@ -99,6 +99,21 @@ __device__ __forceinline__ float logp_of(const RowCDF<N>& r, int a) {
   return (float)(log((double)pa) - log(r.C[N - 1]));
 }
 
+// logp_of for a row normalised in fp32 (the policy softmax): the fp64 row sum C = 1 + d with
+// |d| ~ 1e-7, so log C = d - d^2/2 + d^3/3 (truncation ~d^4/4, far below an fp64 ulp of
+// the result) replaces the second fp64 log; log-probabilities are compared within 2 ulp
+// (R18), actions are unaffected.
+template <int N>
+__device__ __forceinline__ float logp_of_normalised(const RowCDF<N>& r, int a) {
+  float pa = r.P[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i)
+    if (a == i) pa = r.P[i];
+  const double d = r.C[N - 1] - 1.0;
+  const double lC = fabs(d) < 1e-6 ? d * (1.0 - d * (0.5 - d * (1.0 / 3.0))) : log(r.C[N - 1]);
+  return (float)(log((double)pa) - lC);
+}
+
 // Hoisted search for step_stride == 0.
 template <int N>
 struct Thresholds {
