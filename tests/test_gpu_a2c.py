@@ -275,3 +275,13 @@ def test_cartpole_solved_by_training_loop(P):
     secs, steps, ret, length = curve[-1]
     print(f"cartpole solved: mean return {ret:.1f} after {steps:.3g} env steps, {secs:.2f} s wall-clock")
     assert ret >= 475.0 and curve[0][2] < 100.0
+
+
+def test_acrobot_solved_by_training_loop(P):
+    """Acrobot-v1 ("the Acrobot ... converges"): 10K replicas, T = 128, lr 1e-3 reach a
+    mean episodic return >= -100 (gym's solve threshold; a random policy scores ~ -499)."""
+    from paper_2408_00930_b200.train import train
+    curve = train("acrobot", 10000, 128, 1500, lr=1e-3, c_e=0.01, target=-100.0, log_every=50)
+    secs, steps, ret, length = curve[-1]
+    print(f"acrobot solved: mean return {ret:.1f} after {steps:.3g} env steps, {secs:.2f} s wall-clock")
+    assert ret >= -100.0 and curve[0][2] < -400.0
