@@ -330,6 +330,18 @@ def main():
     torch.cuda.synchronize(dev)
     if world > 1:
         dist.barrier()
+    if p2p:  # the peer-memory reduction must have worked on every rank, else fall back to NCCL
+        ok = torch.tensor([1 if env.status() == 0 else 0], dtype=torch.int32, device=dev)
+        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+        if int(ok.item()) == 0:
+            print("warning: peer-memory statistics reduction failed during warm-up; using NCCL", file=sys.stderr)
+            env.peer_detach()
+            env.reset()
+            p2p = False
+            for _ in range(max(args.warmup, 1)):
+                one_step()
+            torch.cuda.synchronize(dev)
+            dist.barrier()
 
     clocks = Clocks(local_dev)
     if not args.ncu:
