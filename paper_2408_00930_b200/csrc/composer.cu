@@ -236,8 +236,12 @@ extern "C" __global__ void k_user_reset(const WsUserArgs a) {
 }
 
 /* fused roll-out of T steps, one replica per thread (P:65, P:71) */
-extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, const float* probs,
-                                          ws_i64 row_stride, ws_i64 step_stride) {
+/* The fused loop.  kH == 0: actions from the given probabilities (R13); kH > 0: from the
+   R29 MLP policy (hidden kH, weights in shared memory `sw`) on the pre-step observation,
+   evaluated in R29's order, with the R31 critic written to values / bootstrap if kCritic. */
+template <int kH, bool kCritic>
+WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_i64 row_stride,
+                  ws_i64 step_stride, const float* sw, float* values, float* bootstrap) {
   const ws_i64 e0 = (ws_i64)blockIdx.x * blockDim.x + threadIdx.x;
   if (e0 - (threadIdx.x & 31) >= a.E) return;          /* whole warp past the end */
   const bool live = e0 < a.E;
@@ -251,13 +255,19 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
   ws_u32 rc = a.reset_count[e];
   float ep_ret = a.ep_ret[e];
   ws_u32 err = 0;
-  const bool hoist = step_stride == 0;    /* same row every step: CDF and logs once */
+  const bool hoist = kH == 0 && step_stride == 0;    /* same row every step: CDF and logs once */
   float p0[WS_N];
   WsRow row;
   if (hoist) {
     for (int i = 0; i < WS_N; ++i) p0[i] = probs[e * row_stride + i];
     ws_row_init(p0, row);
   }
+  const int kHH = kH > 0 ? kH : 1;
+  const float* W1 = sw;                       /* [D][H] */
+  const float* b1 = W1 + WS_D * kHH;          /* [H] */
+  const float* W2 = b1 + kHH;                 /* [H][N] */
+  const float* b2 = W2 + kHH * WS_N;          /* [N] */
+  const float* wv = b2 + WS_N;                /* [H] | bv (critic) */
   ws_u32 w4[4] = {0u, 0u, 0u, 0u};
   for (int c = 0; c < T; ++c) {
     const ws_u64 t = t0 + (ws_u64)c;
@@ -267,8 +277,32 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
     if (c == 0 || (t & 3) == 0) ws_philox((ws_u32)(t >> 2), eg, 0u, 1u, a.k0, a.k1, w4);
     const float u = ws_u01(w4[t & 3]);
     float lp;
-    const int act = hoist ? ws_row_draw(row, p0, u, &lp)
-                          : ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, u, &lp);
+    int act;
+    if (kH > 0) {
+      float lg[WS_N];
+      for (int i = 0; i < WS_N; ++i) lg[i] = b2[i];
+      float v = kCritic ? wv[kHH] : 0.0f;
+      for (int j = 0; j < kHH; ++j) {
+        float acc = b1[j];
+        for (int k = 0; k < WS_D; ++k) acc = __fmaf_rn(W1[k * kHH + j], o[k], acc);
+        const float hj = acc > 0.0f ? acc : 0.0f;
+        for (int i = 0; i < WS_N; ++i) lg[i] = __fmaf_rn(W2[j * WS_N + i], hj, lg[i]);
+        if (kCritic) v = __fmaf_rn(wv[j], hj, v);
+      }
+      if (kCritic && live) __stcs(values + idx, v);
+      float m = lg[0];
+      for (int i = 1; i < WS_N; ++i) m = lg[i] > m ? lg[i] : m;
+      float p[WS_N], S = 0.0f;
+      for (int i = 0; i < WS_N; ++i) {
+        p[i] = (float)exp((double)__fsub_rn(lg[i], m));
+        S = __fadd_rn(S, p[i]);
+      }
+      for (int i = 0; i < WS_N; ++i) p[i] = __fdiv_rn(p[i], S);
+      act = ws_sample(p, u, &lp);
+    } else {
+      act = hoist ? ws_row_draw(row, p0, u, &lp)
+                  : ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, u, &lp);
+    }
     if (live) {
       __stcs(a.act + idx, act);
       if (a.write_logp) __stcs(a.logp + idx, lp);
@@ -318,6 +352,15 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
       }
     }
   }
+  if (kCritic) {  /* bootstrap value of the observation after the last step */
+    float v = wv[kHH];
+    for (int j = 0; j < kHH; ++j) {
+      float acc = b1[j];
+      for (int k = 0; k < WS_D; ++k) acc = __fmaf_rn(W1[k * kHH + j], o[k], acc);
+      v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
+    }
+    if (live) bootstrap[e] = v;
+  }
   if (live) {
     for (int i = 0; i < WS_S; ++i) a.state[e * WS_S + i] = s[i];
     for (int i = 0; i < WS_D; ++i) a.obs_live[e * WS_D + i] = o[i];
@@ -327,6 +370,34 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
     if (err) atomicOr(a.err, err);
   }
 }
+
+extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, const float* probs,
+                                          ws_i64 row_stride, ws_i64 step_stride) {
+  ws_run<0, false>(a, T, t0, probs, row_stride, step_stride, 0, 0, 0);
+}
+
+/* policy roll-outs: weights (R29, + R31 value head for the critic variants) staged in shared
+   memory once per CTA */
+template <int kH, bool kCritic>
+WS_FN void ws_policy(const WsUserArgs& a, int T, ws_u64 t0, const float* w, float* values, float* bootstrap) {
+  __shared__ float sw[WS_D * kH + kH + kH * WS_N + WS_N + kH + 1];
+  const int nw = WS_D * kH + kH + kH * WS_N + WS_N + (kCritic ? kH + 1 : 0);
+  for (int i = threadIdx.x; i < nw; i += blockDim.x) sw[i] = w[i];
+  __syncthreads();
+  ws_run<kH, kCritic>(a, T, t0, 0, 0, 0, sw, values, bootstrap);
+}
+extern "C" __global__ void k_user_policy_32(const WsUserArgs a, int T, ws_u64 t0, const float* w) {
+  ws_policy<32, false>(a, T, t0, w, 0, 0);
+}
+extern "C" __global__ void k_user_policy_64(const WsUserArgs a, int T, ws_u64 t0, const float* w) {
+  ws_policy<64, false>(a, T, t0, w, 0, 0);
+}
+extern "C" __global__ void k_user_ac_32(const WsUserArgs a, int T, ws_u64 t0, const float* w, float* v, float* b) {
+  ws_policy<32, true>(a, T, t0, w, v, b);
+}
+extern "C" __global__ void k_user_ac_64(const WsUserArgs a, int T, ws_u64 t0, const float* w, float* v, float* b) {
+  ws_policy<64, true>(a, T, t0, w, v, b);
+}
 )WS";
 
 // ------------------------------------------------------------------------------ registry
@@ -334,7 +405,11 @@ struct UserEnv {
   ws_env_def def{};
   std::string name, source, log;
   std::vector<char> cubin;
-  std::map<int, std::pair<cudaLibrary_t, std::pair<cudaKernel_t, cudaKernel_t>>> per_dev;  // reset, rollout
+  struct Kernels {
+    cudaLibrary_t lib;
+    cudaKernel_t reset, rollout, policy32, policy64, ac32, ac64;
+  };
+  std::map<int, Kernels> per_dev;
 };
 
 std::mutex g_mu;
@@ -356,22 +431,23 @@ void copy_log(const std::string& s, char* log, size_t n) {
   log[k] = '\0';
 }
 
-cudaError_t kernels_for(UserEnv* u, cudaKernel_t* reset, cudaKernel_t* roll) {
+cudaError_t kernels_for(UserEnv* u, const UserEnv::Kernels** out) {
   int dev = 0;
   cudaError_t e = cudaGetDevice(&dev);
   if (e) return e;
   std::lock_guard<std::mutex> g(g_mu);
   auto it = u->per_dev.find(dev);
   if (it == u->per_dev.end()) {
-    cudaLibrary_t lib;
-    if ((e = cudaLibraryLoadData(&lib, u->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0))) return e;
-    cudaKernel_t kr, kw;
-    if ((e = cudaLibraryGetKernel(&kr, lib, "k_user_reset"))) return e;
-    if ((e = cudaLibraryGetKernel(&kw, lib, "k_user_rollout"))) return e;
-    it = u->per_dev.emplace(dev, std::make_pair(lib, std::make_pair(kr, kw))).first;
+    UserEnv::Kernels k{};
+    if ((e = cudaLibraryLoadData(&k.lib, u->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0))) return e;
+    const std::pair<cudaKernel_t*, const char*> names[] = {
+        {&k.reset, "k_user_reset"},       {&k.rollout, "k_user_rollout"}, {&k.policy32, "k_user_policy_32"},
+        {&k.policy64, "k_user_policy_64"}, {&k.ac32, "k_user_ac_32"},      {&k.ac64, "k_user_ac_64"}};
+    for (const auto& n : names)
+      if ((e = cudaLibraryGetKernel(n.first, k.lib, n.second))) return e;
+    it = u->per_dev.emplace(dev, k).first;
   }
-  *reset = it->second.second.first;
-  *roll = it->second.second.second;
+  *out = &it->second;
   return cudaSuccess;
 }
 
@@ -402,24 +478,40 @@ bool user_env_spec(const char* name, UserSpec* out) {
 }
 
 cudaError_t launch_user_reset(const UserLaunch& l) {
-  cudaKernel_t kr, kw;
-  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &kr, &kw);
+  const UserEnv::Kernels* k = nullptr;
+  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &k);
   if (e) return e;
   UserArgs a = user_args(l);
   void* args[] = {&a};
   const unsigned grid = (unsigned)((l.k.E + 127) / 128);
-  return cudaLaunchKernel(reinterpret_cast<const void*>(kr), dim3(grid), dim3(128), args, 0, l.stream);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(k->reset), dim3(grid), dim3(128), args, 0, l.stream);
 }
 
 cudaError_t launch_user_rollout(const UserLaunch& l, int T, uint64_t t0, const float* probs, int64_t row_stride,
                                 int64_t step_stride) {
-  cudaKernel_t kr, kw;
-  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &kr, &kw);
+  const UserEnv::Kernels* k = nullptr;
+  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &k);
   if (e) return e;
   UserArgs a = user_args(l);
   void* args[] = {&a, &T, &t0, &probs, &row_stride, &step_stride};
   const unsigned grid = (unsigned)((l.k.E + 127) / 128);
-  return cudaLaunchKernel(reinterpret_cast<const void*>(kw), dim3(grid), dim3(128), args, 0, l.stream);
+  return cudaLaunchKernel(reinterpret_cast<const void*>(k->rollout), dim3(grid), dim3(128), args, 0, l.stream);
+}
+
+cudaError_t launch_user_policy(const UserLaunch& l, int T, uint64_t t0, const float* weights, int hidden,
+                               float* values, float* bootstrap) {
+  const UserEnv::Kernels* k = nullptr;
+  cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &k);
+  if (e) return e;
+  UserArgs a = user_args(l);
+  const unsigned grid = (unsigned)((l.k.E + 127) / 128);
+  cudaKernel_t f = values ? (hidden == 32 ? k->ac32 : k->ac64) : (hidden == 32 ? k->policy32 : k->policy64);
+  if (values) {
+    void* args[] = {&a, &T, &t0, &weights, &values, &bootstrap};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(f), dim3(grid), dim3(128), args, 0, l.stream);
+  }
+  void* args[] = {&a, &T, &t0, &weights};
+  return cudaLaunchKernel(reinterpret_cast<const void*>(f), dim3(grid), dim3(128), args, 0, l.stream);
 }
 
 }  // namespace ws

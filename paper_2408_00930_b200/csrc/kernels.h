@@ -116,5 +116,9 @@ bool user_env_spec(const char* name, UserSpec* out);
 cudaError_t launch_user_reset(const UserLaunch& l);
 cudaError_t launch_user_rollout(const UserLaunch& l, int T, uint64_t t0, const float* probs, int64_t row_stride,
                                 int64_t step_stride);
+// the R29 policy (hidden 32 / 64) inside the registered env's loop; values / bootstrap
+// non-null: also the R31 critic
+cudaError_t launch_user_policy(const UserLaunch& l, int T, uint64_t t0, const float* weights, int hidden,
+                               float* values, float* bootstrap);
 
 }  // namespace ws

@@ -519,15 +519,22 @@ static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t 
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
-  if (h->A != 1 || h->spec.n_actions < 1 || h->spec.kind == ws::kTag || h->spec.kind == ws::kUser)
-    return fail(h, WS_ERR_INVALID_ARGUMENT, "policy roll-out: single-agent discrete envs (cartpole, acrobot, dummy)");
+  if (h->A != 1 || h->spec.n_actions < 1 || h->spec.kind == ws::kTag)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "policy roll-out: single-agent discrete envs");
   DeviceGuard g(h->device);
   ws_status st = ensure_store(h, T);
   if (st) return st;
   if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
   cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
-  if (!e) e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches, values,
-                                        bootstrap);
+  if (!e && h->spec.kind == ws::kUser) {  // NEXT-N4 registered env: the template's policy loop
+    if (h->timing) mark_kernel(h, ws::kKRollout, 0);
+    e = ws::launch_user_policy(ws::UserLaunch{kargs(h), h->spec.user, h->user_prm, h->user_shared, h->stream}, T,
+                               h->t, weights, hidden, values, bootstrap);
+    if (h->timing) mark_kernel(h, ws::kKRollout, 1);
+    h->launches += 1;
+  } else if (!e) {
+    e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches, values, bootstrap);
+  }
   if (e) return cuda_fail(h, e, "policy roll-out kernel");
   h->t += (uint64_t)T;
   h->cursor = T;

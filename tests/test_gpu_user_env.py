@@ -110,3 +110,47 @@ def test_single_step_path_refused(P):
     g = P.Env(8, 1, "u_mountaincar", SEED, t_capacity=4)
     with pytest.raises(P.WSError):
         g.sample(torch.full((8, 1, 3), 1 / 3, device="cuda"))
+
+
+@pytest.mark.parametrize("H", [32, 64])
+def test_registered_env_policy_rollout(P, H):
+    """The R29 policy inside the registered env's loop (ws_rollout_policy on a C-source env)
+    equals the oracle's policy roll-out, and the user CartPole with the critic equals the
+    hand-written policy kernel on the built-in CartPole bit for bit (values included)."""
+    E, T = 300, 150
+    w = W.policy_weights(4, H, 2, seed=91, scale=2.0)
+    g = P.Env(E, 1, "u_cartpole", SEED, t_capacity=T)
+    g.rollout_policy(T, torch.from_numpy(w).cuda(), H)
+    assert g.status() == 0
+    o = O.Batch("u_cartpole", E, 1, SEED, t_capacity=T)
+    assert o.rollout_policy(T, w, H, n_threads=4) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done", "obs_live", "reset_count"):
+        ref = o.array(k)[:T] if k in ("obs", "act", "rew", "done") else o.array(k)
+        got = buf[k][:T] if k in ("obs", "act", "rew", "done") else buf[k]
+        assert np.array_equal(got, ref), k
+    lg, lo = buf["logp"][:T], o.array("logp")[:T]
+    assert np.all(np.abs(lg.view(np.int32).astype(np.int64) - lo.view(np.int32).astype(np.int64)) <= 2)
+    # critic variant against the built-in kernel
+    params = torch.from_numpy(W.a2c_params(4, H, 2, seed=92)).cuda()
+    a = P.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    b = P.Env(E, 1, "u_cartpole", SEED, t_capacity=T)
+    va, ba = torch.empty(T * E, device="cuda"), torch.empty(E, device="cuda")
+    vb, bb = torch.empty(T * E, device="cuda"), torch.empty(E, device="cuda")
+    a.rollout_actor_critic(T, params, H, va, ba)
+    b.rollout_actor_critic(T, params, H, vb, bb)
+    A = {k: v.cpu().numpy() for k, v in a.buffers().items() if v is not None}
+    B = {k: v.cpu().numpy() for k, v in b.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done", "state", "obs_live", "stats"):
+        assert np.array_equal(A[k], B[k]), k
+    assert torch.equal(va, vb) and torch.equal(ba, bb)
+
+
+def test_registered_env_trains(P):
+    """The training loop on an environment supplied as C source (CartPole through the
+    composer) solves it like the built-in env."""
+    from paper_2408_00930_b200.train import train
+    curve = train("u_cartpole", 10000, 32, 3000, lr=3e-3, target=475.0, log_every=50)
+    print(f"u_cartpole solved: mean return {curve[-1][2]:.1f} after {curve[-1][1]:.3g} env steps, "
+          f"{curve[-1][0]:.2f} s")
+    assert curve[-1][2] >= 475.0
