@@ -26,7 +26,9 @@ Plain fp64 evaluation in the order the definitions are written; the backward pas
 hand-derived chain rule of the loss above.  Pins (tests/test_oracle_a2c.py): central finite
 differences of ``loss``, torch autograd (fp64) of an independently written network,
 torch.optim.Adam + clip_grad_norm_, closed forms (uniform policy entropy = log n, zero
-advantages and V == returns -> only the entropy term), the SPEC S:404-406 examples.
+advantages and V == returns -> only the entropy term), the SPEC S:404-406 examples; PPO
+(R33) against torch autograd of an independent clipped-surrogate loss and the
+SPEC identity / clip-rule examples.
 """
 from __future__ import annotations
 
@@ -171,3 +173,41 @@ def update(params, m, v, k, obs, act, adv, ret, D, H, n, *, c_v=0.5, c_e=0.01, l
     L = loss(params, obs, act, Ah, ret, D, H, n, c_v, c_e)
     p2, m2, v2 = adam(params, clip(g, max_norm), m, v, k, lr, beta1, beta2, eps)
     return p2, m2, v2, g, L
+
+
+# ------------------------------------------------------------------------------ PPO (R33)
+# SPEC ppo_update: "K epochs x M minibatches of the clipped surrogate
+# mean(min(rho A_hat, clip(rho, 1 +- eps) A_hat)) with rho = exp(log pi_new - log pi_old);
+# value and entropy terms as in A2C".  Reading R33: the loss minimised is
+#   -mean(min(rho A_hat, clip(rho, 1-eps, 1+eps) A_hat)) + c_v mean((V-R)^2) - c_e mean(Ent)
+# with log pi_old the behaviour log-probabilities logged by the roll-out (constants).
+
+def ppo_loss(params, obs, act, adv_hat, ret, logp_old, D, H, n, c_v, c_e, eps, batch=None):
+    """(total, surrogate term, value term, entropy term)."""
+    _, _, logits, pi, V = forward(params, obs, D, H, n)
+    ok, a = _valid(act, n)
+    B = len(a) if batch is None else batch
+    lse = logits.max(axis=1) + np.log(np.exp(logits - logits.max(axis=1, keepdims=True)).sum(axis=1))
+    logp = logits[np.arange(len(a)), a] - lse
+    rho = np.exp(logp - np.asarray(logp_old, dtype=np.float64).ravel())
+    Ah = np.asarray(adv_hat, dtype=np.float64).ravel()
+    surr = np.minimum(rho * Ah, np.clip(rho, 1 - eps, 1 + eps) * Ah)
+    ent = -(pi * np.log(np.maximum(pi, 1e-300))).sum(axis=1)
+    R = np.asarray(ret, dtype=np.float64).ravel()
+    pol = -surr[ok].sum() / B
+    val = c_v * ((V - R) ** 2)[ok].sum() / B
+    entt = -c_e * ent[ok].sum() / B
+    return pol + val + entt, pol, val, entt
+
+
+def ppo_grad(params, obs, act, adv_hat, ret, logp_old, D, H, n, c_v, c_e, eps, batch=None) -> np.ndarray:
+    """d ppo_loss / d params: the A2C chain rule with A_hat replaced by rho A_hat on rows
+    where the unclipped term is the minimum (rho A_hat <= clip(rho) A_hat), 0 elsewhere."""
+    _, _, logits, pi, _ = forward(params, obs, D, H, n)
+    ok, a = _valid(act, n)
+    lse = logits.max(axis=1) + np.log(np.exp(logits - logits.max(axis=1, keepdims=True)).sum(axis=1))
+    logp = logits[np.arange(len(a)), a] - lse
+    rho = np.exp(logp - np.asarray(logp_old, dtype=np.float64).ravel())
+    Ah = np.asarray(adv_hat, dtype=np.float64).ravel()
+    active = rho * Ah <= np.clip(rho, 1 - eps, 1 + eps) * Ah
+    return grad(params, obs, act, np.where(active, rho * Ah, 0.0), ret, D, H, n, c_v, c_e, batch)

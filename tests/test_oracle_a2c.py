@@ -167,3 +167,56 @@ def test_update_decreases_loss_on_frozen_batch():
         L1 = OA.loss(p2, obs, act, OA.normalize(adv), ret, D, H, n, 0.5, 0.01)
         wins += L1[0] < L0[0]
     assert wins >= 9
+
+
+# ---------------------------------------------------------------- PPO (R33)
+def torch_ppo_loss(params, obs, act, adv_hat, ret, logp_old, D, H, n, c_v, c_e, eps):
+    p = torch.tensor(params, dtype=torch.float64, requires_grad=True)
+    W1, b1, W2, b2, wv, bv = torch.split(p, [D * H, H, H * n, n, H, 1])
+    o = torch.tensor(obs, dtype=torch.float64)
+    h = torch.relu(o @ W1.view(D, H) + b1)
+    dist = torch.distributions.Categorical(logits=h @ W2.view(H, n) + b2)
+    V = h @ wv + bv
+    a = torch.tensor(act, dtype=torch.int64)
+    rho = torch.exp(dist.log_prob(a) - torch.tensor(logp_old, dtype=torch.float64))
+    A = torch.tensor(adv_hat, dtype=torch.float64)
+    surr = torch.min(rho * A, torch.clamp(rho, 1 - eps, 1 + eps) * A)
+    R = torch.tensor(ret, dtype=torch.float64)
+    L = -surr.mean() + c_v * ((V - R) ** 2).mean() - c_e * dist.entropy().mean()
+    L.backward()
+    return L.item(), p.grad.numpy()
+
+
+@pytest.mark.parametrize("D,H,n", SHAPES)
+def test_ppo_grad_matches_torch_and_differences(D, H, n):
+    params, obs, act, adv, ret = batch(D, H, n, 200, seed=31 + H)
+    # behaviour log-probs of a perturbed policy: ratios spread over both clip edges
+    old = OA.forward(params + np.random.default_rng(2).standard_normal(params.size) * 0.3, obs, D, H, n)[3]
+    logp_old = np.log(old[np.arange(200), act])
+    L_t, g_t = torch_ppo_loss(params, obs, act, adv, ret, logp_old, D, H, n, 0.5, 0.01, 0.2)
+    L = OA.ppo_loss(params, obs, act, adv, ret, logp_old, D, H, n, 0.5, 0.01, 0.2)[0]
+    g = OA.ppo_grad(params, obs, act, adv, ret, logp_old, D, H, n, 0.5, 0.01, 0.2)
+    assert abs(L - L_t) < 1e-12 * max(1, abs(L))
+    np.testing.assert_allclose(g, g_t, rtol=1e-9, atol=1e-12)
+    rho = OA.forward(params, obs, D, H, n)[3][np.arange(200), act] / old[np.arange(200), act]
+    assert (rho < 0.8).any() and (rho > 1.2).any()  # both clip edges exercised
+
+
+def test_ppo_identity_and_clip_rule():
+    """S:410: new params = old params -> rho = 1, surrogate = mean(A_hat), gradient = A2C's;
+    S:411: rho = 1.5, A_hat > 0, eps = 0.2 -> the clipped term 1.2 A_hat is used (zero
+    surrogate gradient on that row)."""
+    D, H, n = 4, 8, 2
+    params, obs, act, adv, ret = batch(D, H, n, 64, seed=41)
+    pi = OA.forward(params, obs, D, H, n)[3]
+    logp_now = np.log(pi[np.arange(64), act])
+    L = OA.ppo_loss(params, obs, act, adv, ret, logp_now, D, H, n, 0.5, 0.01, 0.2)
+    assert L[1] == pytest.approx(-adv.mean(), rel=1e-12)
+    np.testing.assert_allclose(OA.ppo_grad(params, obs, act, adv, ret, logp_now, D, H, n, 0.5, 0.01, 0.2),
+                               OA.grad(params, obs, act, adv, ret, D, H, n, 0.5, 0.01), rtol=1e-10, atol=1e-14)
+    one = np.array([1.0])
+    lo = logp_now[:1] - np.log(1.5)  # rho = 1.5 on row 0
+    Lr = OA.ppo_loss(params, obs[:1], act[:1], one, ret[:1], lo, D, H, n, 0.0, 0.0, 0.2)
+    assert Lr[1] == pytest.approx(-1.2, rel=1e-12)
+    g = OA.ppo_grad(params, obs[:1], act[:1], one, ret[:1], lo, D, H, n, 0.0, 0.0, 0.2)
+    assert np.abs(g).max() == 0.0
