@@ -81,7 +81,8 @@ class ws_a2c_args(C.Structure):
     _fields_ = [("obs_dim", C.c_int32), ("hidden", C.c_int32), ("n_actions", C.c_int32), ("rows", C.c_int64),
                 ("params", C.c_void_p), ("obs", C.c_void_p), ("act", C.c_void_p), ("adv", C.c_void_p),
                 ("ret", C.c_void_p), ("moments", C.c_void_p), ("batch", C.c_double), ("c_v", C.c_float),
-                ("c_e", C.c_float), ("workspace", C.c_void_p), ("grad", C.c_void_p), ("loss", C.c_void_p)]
+                ("c_e", C.c_float), ("workspace", C.c_void_p), ("grad", C.c_void_p), ("loss", C.c_void_p),
+                ("logp_old", C.c_void_p), ("clip_eps", C.c_float), ("norm_batch", C.c_double)]
 
 
 class ws_host_store(C.Structure):

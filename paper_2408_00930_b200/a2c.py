@@ -68,8 +68,10 @@ def moments(x: torch.Tensor, ws: torch.Tensor, out: Optional[torch.Tensor] = Non
 
 def a2c_grad(params, obs, act, adv, ret, mom, batch: float, obs_dim: int, hidden: int, n_actions: int,
              c_v: float, c_e: float, ws: torch.Tensor, grad: Optional[torch.Tensor] = None,
-             loss: Optional[torch.Tensor] = None, stream=None):
-    """This shard's gradient of the S:405 loss (ws_a2c_grad) -> (grad f32 [P], loss f64 [3])."""
+             loss: Optional[torch.Tensor] = None, stream=None, logp_old: Optional[torch.Tensor] = None,
+             clip_eps: float = 0.2, norm_batch: float = 0.0):
+    """This shard's gradient of the S:405 loss (ws_a2c_grad) -> (grad f32 [P], loss f64 [3]).
+    logp_old given: the PPO clipped surrogate (R33) instead of the A2C policy term."""
     rows = adv.numel()
     P = n_params(obs_dim, hidden, n_actions)
     _f32("params", params, P)
@@ -80,9 +82,12 @@ def a2c_grad(params, obs, act, adv, ret, mom, batch: float, obs_dim: int, hidden
         raise WSError(_abi.INVALID_ARGUMENT, "act: contiguous int32 with one entry per row")
     grad = torch.empty(P, dtype=torch.float32, device=adv.device) if grad is None else grad
     loss = torch.empty(3, dtype=torch.float64, device=adv.device) if loss is None else loss
+    if logp_old is not None:
+        _f32("logp_old", logp_old, rows)
     a = _abi.ws_a2c_args(obs_dim, hidden, n_actions, rows, params.data_ptr(), obs.data_ptr(), act.data_ptr(),
                          adv.data_ptr(), ret.data_ptr(), mom.data_ptr(), float(batch), c_v, c_e, ws.data_ptr(),
-                         grad.data_ptr(), loss.data_ptr())
+                         grad.data_ptr(), loss.data_ptr(),
+                         None if logp_old is None else logp_old.data_ptr(), clip_eps, float(norm_batch))
     check(lib().ws_a2c_grad(C.byref(a), _s(stream, adv)))
     return grad, loss
 
@@ -153,31 +158,43 @@ class A2C:
             self._values = torch.empty(rows, dtype=torch.float32, device=self.env.device)
         return self._values
 
+    def _advantages(self, T: int, values_ready: bool):
+        """Critic values (unless the roll-out wrote them), GAE over the store in place, and the
+        global-batch moments of the advantages.  Returns (obs, act, adv, ret, rows)."""
+        env, D, H, N, hp = self.env, self.D, self.H, self.N, self.hp
+        s = env.stream
+        buf = env.buffers()
+        rows = T * self.E
+        obs = buf["obs"][:T].reshape(rows * D)
+        act = buf["act"][:T].reshape(rows)
+        self._value_buf(rows)
+        if not values_ready:
+            ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
+            ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
+        adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
+                                 hp["gamma"], hp["lam"])
+        moments(adv.view(-1), self.ws, out=self.mom, stream=s)
+        self._allreduce(self.mom)
+        self._adv = adv  # alive until the stream consumed it
+        return obs, act, adv.view(-1), ret.view(-1), rows
+
+    def _step(self, obs, act, adv, ret, rows, norm_rows, logp_old=None, clip_eps=0.2):
+        """One gradient (this shard's rows) -> all-reduce -> clip + Adam."""
+        hp, s = self.hp, self.env.stream
+        a2c_grad(self.params, obs, act, adv, ret, self.mom, float(rows * self.world), self.D, self.H, self.N,
+                 hp["c_v"], hp["c_e"], self.ws, grad=self.grad, loss=self.loss, stream=s, logp_old=logp_old,
+                 clip_eps=clip_eps, norm_batch=float(norm_rows * self.world))
+        self._allreduce(self.grad)
+        self.step += 1
+        adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
+             hp["max_norm"], grad_norm=self.grad_norm, stream=s)
+
     def update(self, T: int, values_ready: bool = False):
         """One A2C update on store slots [0, T) (already rolled out with self.params).
         values_ready: the roll-out already wrote the critic (ws_rollout_actor_critic)."""
-        env, D, H, N, hp = self.env, self.D, self.H, self.N, self.hp
-        s = env.stream
-        with torch.cuda.stream(s):
-            buf = env.buffers()
-            rows = T * self.E
-            obs = buf["obs"][:T].reshape(rows * D)
-            act = buf["act"][:T].reshape(rows)
-            self._value_buf(rows)
-            if not values_ready:
-                ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
-                ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
-            adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
-                                     hp["gamma"], hp["lam"])
-            moments(adv.view(-1), self.ws, out=self.mom, stream=s)
-            self._allreduce(self.mom)
-            a2c_grad(self.params, obs, act, adv.view(-1), ret.view(-1), self.mom, float(rows * self.world), D, H,
-                     N, hp["c_v"], hp["c_e"], self.ws, grad=self.grad, loss=self.loss, stream=s)
-            self._allreduce(self.grad)
-            self.step += 1
-            adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
-                 hp["max_norm"], grad_norm=self.grad_norm, stream=s)
-        self._adv = adv  # alive until the stream consumed it
+        with torch.cuda.stream(self.env.stream):
+            obs, act, adv, ret, rows = self._advantages(T, values_ready)
+            self._step(obs, act, adv, ret, rows, rows)
 
     def iteration(self, T: int):
         """Roll out T steps with the current policy (the kernel also writes the critic's values
@@ -185,3 +202,33 @@ class A2C:
         vals = self._value_buf(T * self.E)
         self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap)
         self.update(T, values_ready=True)
+
+
+class PPO(A2C):
+    """SPEC ppo_update (DESIGN R33): after each roll-out, `epochs` passes of
+    `minibatches` clipped-surrogate steps.  Minibatch m is the contiguous slot range
+    [m T / M, (m + 1) T / M) of the time-major store (every replica's rows of those slots; no
+    copy, pointer offsets into the store), in a fixed order; the behaviour log-probabilities
+    are the store's logp slab written by the roll-out; advantages are normalised once with the
+    whole (global) batch's moments; one all-reduce + clip + Adam step per minibatch."""
+
+    def __init__(self, env: Env, hidden: int = 64, *, epochs: int = 4, minibatches: int = 4, clip_eps: float = 0.2,
+                 **kw):
+        super().__init__(env, hidden, **kw)
+        if epochs < 1 or minibatches < 1:
+            raise WSError(_abi.INVALID_ARGUMENT, "epochs, minibatches >= 1")
+        self.epochs, self.minibatches, self.clip_eps = epochs, minibatches, clip_eps
+
+    def update(self, T: int, values_ready: bool = False):
+        if T < self.minibatches:
+            raise WSError(_abi.INVALID_ARGUMENT, "T must be >= minibatches")
+        with torch.cuda.stream(self.env.stream):
+            obs, act, adv, ret, rows = self._advantages(T, values_ready)
+            logp = self.env.buffers()["logp"][:T].reshape(rows)
+            E, D, M = self.E, self.D, self.minibatches
+            for _ in range(self.epochs):
+                for m in range(M):
+                    t0, t1 = T * m // M, T * (m + 1) // M
+                    r0, r1 = t0 * E, t1 * E
+                    self._step(obs[r0 * D:r1 * D], act[r0:r1], adv[r0:r1], ret[r0:r1], r1 - r0, rows,
+                               logp_old=logp[r0:r1], clip_eps=self.clip_eps)

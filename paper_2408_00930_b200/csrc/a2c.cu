@@ -163,6 +163,9 @@ struct GradDev {
   float c_v, c_e;
   int64_t rows;
   double* partial;  // [gridDim.x][P + 3]
+  const float* logp_old;  // PPO (R33): behaviour log-probs [rows]; null = A2C
+  float clip_eps;
+  double norm_batch;      // rows the moments were summed over (minibatches: the whole batch)
 };
 
 template <int D, int H, int N>
@@ -197,8 +200,8 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
   if (threadIdx.x == N) sm[S::kB2 + N] = __ldg(g.params + L.obv);
 
   // normalisation (R31): mu, sigma over the global batch; skipped when sigma < 1e-8
-  const double mu = g.moments[0] / g.batch;
-  const double var = fmax(g.moments[1] / g.batch - mu * mu, 0.0);
+  const double mu = g.moments[0] / g.norm_batch;
+  const double var = fmax(g.moments[1] / g.norm_batch - mu * mu, 0.0);
   const double sigma = sqrt(var);
   const bool norm = sigma >= 1e-8;
   const double inv_sigma = norm ? 1.0 / sigma : 1.0;
@@ -314,12 +317,20 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
           ent -= p[j] * lp[j];
           if (j == a) lpa = lp[j];
         }
-        const float Ah = norm ? (float)(((double)A - mu) * inv_sigma) : A;
+        float Ah = norm ? (float)(((double)A - mu) * inv_sigma) : A;
+        float surr = lpa * Ah;  // A2C: the policy term is -log pi(a) A_hat
+        if (g.logp_old) {       // PPO (R33): clipped surrogate; gradient rho A_hat where unclipped wins
+          const float rho = expf(lpa - __ldg(g.logp_old + r));
+          const float rc = fminf(fmaxf(rho, 1.0f - g.clip_eps), 1.0f + g.clip_eps);
+          const float s1 = rho * Ah, s2 = rc * Ah;
+          surr = fminf(s1, s2);
+          Ah = s1 <= s2 ? s1 : 0.0f;
+        }
         const float Ab = Ah * invB;
 #pragma unroll
         for (int j = 0; j < N; ++j) dl[j] = Ab * (p[j] - (j == a ? 1.0f : 0.0f)) + ce_b * p[j] * (lp[j] + ent);
         dv = cv2_b * (v - R);
-        lpol -= lpa * Ab;
+        lpol -= surr * invB;
         lval += cv_b * (v - R) * (v - R);
         lent -= ce_b * ent;
 #pragma unroll
@@ -546,8 +557,10 @@ ws_status ws_a2c_grad(const ws_a2c_args* a, void* stream) {
   if (!a || !supported(a->obs_dim, a->hidden, a->n_actions) || a->rows < 1 || !a->params || !a->obs || !a->act ||
       !a->adv || !a->ret || !a->moments || !(a->batch > 0.0) || !a->workspace || !a->grad)
     return WS_ERR_INVALID_ARGUMENT;
+  if (a->logp_old && !(a->clip_eps >= 0.0f && a->clip_eps < 1.0f)) return WS_ERR_INVALID_ARGUMENT;
   GradDev g{a->params, a->obs, a->act, a->adv, a->ret, a->moments, a->batch, a->c_v, a->c_e, a->rows,
-            static_cast<double*>(a->workspace)};
+            static_cast<double*>(a->workspace), a->logp_old, a->clip_eps,
+            a->norm_batch > 0.0 ? a->norm_batch : a->batch};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int nb = 0;
   cudaError_t e = launch_grad(a->obs_dim, a->hidden, a->n_actions, g, s, &nb);

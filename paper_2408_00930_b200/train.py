@@ -1,4 +1,4 @@
-"""NEXT-N2: the training loop (SPEC train S:418-421; P:86 / P:95 convergence claims, Fig 2(b)):
+"""NEXT-N2: the training loop (SPEC train S:418-421; A2C or PPO; P:86 / P:95 convergence claims, Fig 2(b)):
 alternate fused roll-outs with in-kernel inference and on-device A2C updates until a budget
 of iterations or a target mean episodic return, emitting the learning curve
 (wall-clock seconds, env steps, mean episodic return, mean episode length) as CSV.  No data
@@ -19,7 +19,7 @@ import time
 import torch
 import torch.distributed as dist
 
-from .a2c import A2C
+from .a2c import A2C, PPO
 from .env import Env
 from .parallel import shard
 
@@ -27,13 +27,17 @@ from .parallel import shard
 def train(env_name: str = "cartpole", n_envs: int = 10000, T: int = 32, iters: int = 1000, hidden: int = 64,
           lr: float = 3e-3, gamma: float = 0.99, lam: float = 0.95, c_v: float = 0.5, c_e: float = 0.01,
           max_norm: float = 0.5, seed: int = 0x24080930, target: float | None = None, log_every: int = 10,
-          out=None) -> list[tuple]:
+          out=None, algo: str = "a2c", epochs: int = 4, minibatches: int = 4, clip_eps: float = 0.2) -> list[tuple]:
     """Returns the learning curve [(seconds, env_steps, mean_return, mean_length)]."""
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
     off, n = shard(n_envs, world, rank)
     env = Env(n, 1, env_name, seed, env_offset=off, n_envs_global=n_envs, t_capacity=T)
-    tr = A2C(env, hidden, lr=lr, gamma=gamma, lam=lam, c_v=c_v, c_e=c_e, max_norm=max_norm, seed=seed & 0xFFFF)
+    kw = dict(lr=lr, gamma=gamma, lam=lam, c_v=c_v, c_e=c_e, max_norm=max_norm, seed=seed & 0xFFFF)
+    if algo == "ppo":
+        tr = PPO(env, hidden, epochs=epochs, minibatches=minibatches, clip_eps=clip_eps, **kw)
+    else:
+        tr = A2C(env, hidden, **kw)
     stats = torch.zeros((log_every, 4), dtype=torch.int64, device=env.device)
     curve = []
     writer = csv.writer(out) if out is not None and rank == 0 else None
@@ -78,6 +82,10 @@ def main(argv=None):
     ap.add_argument("--log-every", type=int, default=10)
     ap.add_argument("--csv", default="-")
     ap.add_argument("--seed", type=lambda x: int(x, 0), default=0x24080930)
+    ap.add_argument("--algo", choices=["a2c", "ppo"], default="a2c")
+    ap.add_argument("--epochs", type=int, default=4)
+    ap.add_argument("--minibatches", type=int, default=4)
+    ap.add_argument("--clip", type=float, default=0.2)
     a = ap.parse_args(argv)
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
         local = int(os.environ.get("LOCAL_RANK", 0))
@@ -85,7 +93,8 @@ def main(argv=None):
         dist.init_process_group("nccl", device_id=torch.device("cuda", local))
     out = sys.stdout if a.csv == "-" else open(a.csv, "w", newline="")
     train(a.env, a.envs, a.T, a.iters, a.hidden, a.lr, a.gamma, a.lam, c_e=a.entropy, target=a.target,
-          log_every=a.log_every, seed=a.seed, out=out)
+          log_every=a.log_every, seed=a.seed, out=out, algo=a.algo, epochs=a.epochs, minibatches=a.minibatches,
+          clip_eps=a.clip)
     if out is not sys.stdout:
         out.close()
     if dist.is_initialized():

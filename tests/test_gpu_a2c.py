@@ -285,3 +285,62 @@ def test_acrobot_solved_by_training_loop(P):
     secs, steps, ret, length = curve[-1]
     print(f"acrobot solved: mean return {ret:.1f} after {steps:.3g} env steps, {secs:.2f} s wall-clock")
     assert ret >= -100.0 and curve[0][2] < -400.0
+
+
+@pytest.mark.parametrize("D,H,N,rows", [(4, 64, 2, 3000), (6, 32, 3, 1000)])
+def test_ppo_grad_matches_oracle(P, D, H, N, rows):
+    """ws_a2c_grad with behaviour log-probs (PPO, R33) against oracle/a2c.py ppo_grad; the
+    behaviour policy is a perturbed copy so that ratios fall on both sides of the clip range
+    (rows within 1e-3 of an edge are moved away: fp32 vs fp64 may pick different branches)."""
+    params = W.a2c_params(D, H, N, seed=101)
+    obs, act, adv, ret = W.a2c_batch(rows, D, N, seed=102)
+    pert = params + np.random.default_rng(103).standard_normal(params.size).astype(np.float32) * 0.3
+    p_new = OA.forward(params, obs, D, H, N)[3][np.arange(rows), act]
+    p_old = OA.forward(pert, obs, D, H, N)[3][np.arange(rows), act]
+    rho = p_new / p_old
+    for edge in (0.8, 1.2):
+        near = np.abs(rho - edge) < 1e-3
+        p_old[near] = p_new[near] / (edge + 2e-3)
+    logp_old = np.log(p_old).astype(np.float32)
+    assert ((p_new / p_old) < 0.8).any() and ((p_new / p_old) > 1.2).any()
+    ws = P.workspace(D, H, N, "cuda")
+    tadv = cuda(adv)
+    mom = P.moments(tadv, ws)
+    g, L = P.a2c_grad(cuda(params), cuda(obs).view(-1), cuda(act), tadv, cuda(ret), mom, float(rows), D, H, N,
+                      0.5, 0.01, ws, logp_old=cuda(logp_old), clip_eps=0.2)
+    g = g.cpu().numpy().astype(np.float64)
+    Ah = OA.normalize(adv)
+    ref = OA.ppo_grad(params, obs, act, Ah, ret, logp_old, D, H, N, 0.5, 0.01, 0.2)
+    rho64 = np.exp(np.log(p_new) - logp_old)
+    scale = grad_scale(params, obs, act, Ah * np.maximum(rho64, 1.0), ret, D, H, N, 0.5, 0.01, rows)
+    bad = np.abs(g - ref) > 2e-5 * scale + 1e-12
+    assert not bad.any(), (np.flatnonzero(bad)[:10], g[bad][:5], ref[bad][:5])
+    Lref = OA.ppo_loss(params, obs, act, Ah, ret, logp_old, D, H, N, 0.5, 0.01, 0.2)
+    assert abs(L.cpu().numpy()[0] - Lref[1]) <= 2e-5 * (np.abs(Ah) * np.maximum(rho64, 1.2)).mean()
+
+
+def test_minibatch_normalisation_uses_whole_batch(P):
+    """norm_batch: a minibatch normalises with the whole batch's moments and count while its
+    means divide by its own size."""
+    D, H, N, rows, r0, r1 = 4, 64, 2, 4000, 1000, 2500
+    params = W.a2c_params(D, H, N, seed=111)
+    obs, act, adv, ret = W.a2c_batch(rows, D, N, seed=112)
+    ws = P.workspace(D, H, N, "cuda")
+    mom = P.moments(cuda(adv), ws)
+    g, _ = P.a2c_grad(cuda(params), cuda(obs[r0:r1]).view(-1), cuda(act[r0:r1]), cuda(adv[r0:r1]),
+                      cuda(ret[r0:r1]), mom, float(r1 - r0), D, H, N, 0.5, 0.01, ws, norm_batch=float(rows))
+    Ah = OA.normalize(adv)[r0:r1]
+    ref = OA.grad(params, obs[r0:r1], act[r0:r1], Ah, ret[r0:r1], D, H, N, 0.5, 0.01)
+    scale = grad_scale(params, obs[r0:r1], act[r0:r1], Ah, ret[r0:r1], D, H, N, 0.5, 0.01, r1 - r0)
+    assert np.all(np.abs(g.cpu().numpy() - ref) <= 2e-5 * scale + 1e-12)
+
+
+def test_cartpole_solved_by_ppo(P):
+    """PPO (SPEC ppo_update, R33): 4 epochs x 4 minibatches per 32-step roll-out of 10K
+    replicas solve CartPole (mean return >= 475) within 1000 iterations."""
+    from paper_2408_00930_b200.train import train
+    curve = train("cartpole", 10000, 32, 1000, lr=1e-3, target=475.0, log_every=50, algo="ppo", epochs=4,
+                  minibatches=4)
+    print(f"cartpole PPO solved: mean return {curve[-1][2]:.1f} after {curve[-1][1]:.3g} env steps, "
+          f"{curve[-1][0]:.2f} s")
+    assert curve[-1][2] >= 475.0
