@@ -166,7 +166,20 @@ def oracle_rollout(b, w, T, probs, cores):
         adv, ret = O.gae(b.array("rew")[:T].reshape(T, w.n_envs), b.array("done")[:T], vals, boot, 0.99, 0.95,
                          f64=True)
         z = np.zeros(params.size)
-        OA.update(params, z, z, 1, obs, b.array("act")[:T].reshape(-1), adv.ravel(), ret.ravel(), D, H, N, lr=1e-4)
+        act = b.array("act")[:T].reshape(-1)
+        ppo = w.params.get("ppo")
+        if ppo:  # K epochs x M minibatches of the clipped surrogate (R33), whole-batch normalisation
+            Ah, logp_old, p, m, v, k = OA.normalize(adv), b.array("logp")[:T].reshape(-1), params, z, z, 0
+            E = w.n_envs
+            for _ in range(ppo[0]):
+                for mb in range(ppo[1]):
+                    r0, r1 = T * mb // ppo[1] * E, T * (mb + 1) // ppo[1] * E
+                    g = OA.ppo_grad(p, obs[r0:r1], act[r0:r1], Ah[r0:r1], ret.ravel()[r0:r1], logp_old[r0:r1],
+                                    D, H, N, 0.5, 0.01, 0.2)
+                    k += 1
+                    p, m, v = OA.adam(p, OA.clip(g, 0.5), m, v, k, 1e-4)
+        else:
+            OA.update(params, z, z, 1, obs, act, adv.ravel(), ret.ravel(), D, H, N, lr=1e-4)
     gae = w.params.get("gae")
     if gae:
         import oracle as O
@@ -291,8 +304,10 @@ def main():
 
     trainer = None
     if w.params.get("a2c"):  # NEXT-N2: every step is one A2C iteration (roll-out + update)
-        from paper_2408_00930_b200.a2c import A2C
-        trainer = A2C(env, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5)
+        from paper_2408_00930_b200.a2c import A2C, PPO
+        ppo = w.params.get("ppo")
+        trainer = (PPO(env, pol[0], params=pol_w, epochs=ppo[0], minibatches=ppo[1], lr=1e-4) if ppo else
+                   A2C(env, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5))
 
     staged = w.params.get("staged")  # NEXT-N3: copy-based baseline pipeline
     staged_rep = {}
@@ -369,8 +384,9 @@ def main():
     if st != 0:
         raise RuntimeError(f"libws reported status {st} during the timed region")
     launches = env.info().launches - launches0
-    if trainer is not None:  # handle-free A2C kernels per step: moments + final, grad + final, Adam
-        launches += 5 * args.steps
+    if trainer is not None:  # handle-free kernels per step: moments + final, then (grad + final, Adam) per update
+        n_upd = (w.params["ppo"][0] * w.params["ppo"][1]) if w.params.get("ppo") else 1
+        launches += (2 + 3 * n_upd) * args.steps
     ktimes = env.kernel_times()
     env.enable_kernel_timing(False)
     clk = clocks.stop() if not args.ncu else {}
@@ -497,9 +513,11 @@ def main():
             henv = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
                        param0=params[0], param1=params[1], block_size=args.block)
             if trainer is not None:  # NEXT-N2: one training iteration per step, loss + stats back to the host
-                from paper_2408_00930_b200.a2c import A2C
-                htr = A2C(henv, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01,
-                          max_norm=0.5)
+                from paper_2408_00930_b200.a2c import A2C, PPO
+                ppo = w.params.get("ppo")
+                htr = (PPO(henv, pol[0], params=pol_w, epochs=ppo[0], minibatches=ppo[1], lr=1e-4) if ppo else
+                       A2C(henv, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01,
+                           max_norm=0.5))
                 hl = torch.empty(3, dtype=torch.float64).pin_memory()
                 hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
 

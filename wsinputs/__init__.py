@@ -51,6 +51,9 @@ CONFIGS = {
     # a 4-64-2 actor-critic, then critic values, GAE over the store, gradient, clip + Adam
     "C2T": Workload("C2T", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64, "a2c": True},
                     note="CartPole-v1 10K envs x 1000 steps + A2C update of a 4-64-2 actor-critic (NEXT-N2)"),
+    "C2O": Workload("C2O", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64, "a2c": True, "ppo": (4, 4)},
+                    note="CartPole-v1 10K envs x 1000 steps + PPO update (4 epochs x 4 minibatches) of a 4-64-2 "
+                         "actor-critic (NEXT-N2)"),
     # NEXT-N3: C2 through the copy-based baseline pipeline (per-step H2D of the
     # probabilities and D2H of the slot, synchronised every step) -- the "data transfer"
     # cost WarpSci removes
