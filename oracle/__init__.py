@@ -69,6 +69,8 @@ def lib():
             "wso_set_capacity": (I, [P, I]),
             "wso_reset": (I, [P]),
             "wso_register_user": (I, [C.c_char_p, C.c_char_p, I, I, I, I, I, I]),
+            "wso_policy_gauss_rows": (I, [P, I, I, I, P, I64, P]),
+            "wso_rollout_policy_gauss": (I, [P, I, P, I, I]),
             "wso_set_env_data": (I, [P, P, I64, P, I64]),
             "wso_sample": (I, [P, P, I64, P, P]),
             "wso_step": (I, [P, P]),
@@ -128,6 +130,15 @@ def policy_probs(weights, D: int, H: int, N: int, obs) -> np.ndarray:
     obs = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1, D)
     out = np.zeros((obs.shape[0], N), np.float32)
     assert lib().wso_policy_probs(_p(weights), D, H, N, _p(obs), obs.shape[0], _p(out)) == 0
+    return out
+
+
+def policy_gauss_rows(weights, D: int, H: int, d: int, obs) -> np.ndarray:
+    """Gaussian policy head rows (mean | log_std, R34) of observations [n, D] -> [n, 2d]."""
+    weights = np.ascontiguousarray(weights, dtype=np.float32)
+    obs = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1, D)
+    out = np.zeros((obs.shape[0], 2 * d), np.float32)
+    assert lib().wso_policy_gauss_rows(_p(weights), D, H, d, _p(obs), obs.shape[0], _p(out)) == 0
     return out
 
 
@@ -373,6 +384,11 @@ class Batch:
         """NEXT-N1: roll-out driven by the MLP policy (wso.cpp policy_probs, DESIGN R29)."""
         weights = np.ascontiguousarray(weights, dtype=np.float32)
         return lib().wso_rollout_policy(self._h, T, _p(weights), hidden, n_threads)
+
+    def rollout_policy_gauss(self, T: int, weights: np.ndarray, hidden: int, n_threads: int = 1) -> int:
+        """NEXT-N1 continuous (R34): roll-out whose Gaussian head rows come from the policy."""
+        w = np.ascontiguousarray(weights, dtype=np.float32)
+        return lib().wso_rollout_policy_gauss(self._h, T, _p(w), hidden, n_threads)
 
     def synchronize(self) -> int:
         return lib().wso_synchronize(self._h)

@@ -1106,6 +1106,77 @@ int wso_rollout_policy(void* h, int T, const float* weights, int H, int n_thread
   return E_OK;
 }
 
+/* NEXT-N1 for continuous actions (reading R34): a Gaussian policy -- the R29 network with d
+ * linear outputs as the mean (mean_i = b2_i, then fma(W2[j][i], h_j, mean_i) for j = 0..H-1)
+ * and a learned, state-independent log standard deviation vector; packed weights
+ * W1 [D][H] | b1 [H] | W2 [H][d] | b2 [d] | log_std [d].  Each step the replica's head row
+ * (mean | log_std) is sampled by the R14 Gaussian head exactly as a given row would be. */
+static void policy_gauss_row(const float* w, int D, int H, int d, const float* obs, float* row) {
+  const float* W1 = w;
+  const float* b1 = W1 + (size_t)D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + (size_t)H * d;
+  const float* log_std = b2 + d;
+  std::vector<float> h((size_t)H);
+  for (int j = 0; j < H; ++j) {
+    float acc = b1[j];
+    for (int k = 0; k < D; ++k) acc = std::fma(W1[(size_t)k * H + j], obs[k], acc);
+    h[j] = acc > 0.0f ? acc : 0.0f;
+  }
+  for (int i = 0; i < d; ++i) {
+    float acc = b2[i];
+    for (int j = 0; j < H; ++j) acc = std::fma(W2[(size_t)j * d + i], h[j], acc);
+    row[i] = acc;
+    row[d + i] = log_std[i];
+  }
+}
+
+int wso_policy_gauss_rows(const float* weights, int D, int H, int d, const float* obs, int64_t n, float* out) {
+  for (int64_t r = 0; r < n; ++r) policy_gauss_row(weights, D, H, d, obs + r * D, out + r * 2 * d);
+  return E_OK;
+}
+
+int wso_rollout_policy_gauss(void* h, int T, const float* weights, int H, int n_threads) {
+  Batch* b = (Batch*)h;
+  if (T < 1 || !weights || H < 1 || b->A != 1 || b->n_actions != 0) return E_INVALID_ARGUMENT;
+  if (T > b->T_cap) return E_OUT_OF_RANGE;
+  if (n_threads < 1) n_threads = 1;
+  if (n_threads > b->E) n_threads = (int)b->E;
+  const uint64_t t0 = b->t;
+  const int D = b->obs_dim, d = b->act_dim;
+  b->cursor = 0;
+  std::vector<float> rows((size_t)b->E * 2 * d);
+  std::vector<std::vector<double>> st(n_threads, std::vector<double>((size_t)T * 4, 0.0));
+  std::vector<int> errs(n_threads, 0);
+  auto worker = [&](int w) {
+    int64_t e0 = b->E * w / n_threads, e1 = b->E * (w + 1) / n_threads;
+    for (int c = 0; c < T; ++c) {
+      for (int64_t e = e0; e < e1; ++e)
+        policy_gauss_row(weights, D, H, d, &b->obs_live[(size_t)e * D], &rows[(size_t)e * 2 * d]);
+      b->sample_range(c, t0 + c, rows.data(), 2 * d, nullptr, nullptr, e0, e1, &errs[w]);
+      b->step_range(c, e0, e1, &st[w][(size_t)c * 4], &errs[w]);
+    }
+  };
+  if (n_threads == 1) {
+    worker(0);
+  } else {
+    std::vector<std::thread> th;
+    for (int w = 0; w < n_threads; ++w) th.emplace_back(worker, w);
+    for (auto& x : th) x.join();
+  }
+  for (int c = 0; c < T; ++c)
+    for (int i = 0; i < 4; ++i) {
+      double s = 0;
+      for (int w = 0; w < n_threads; ++w) s += st[w][(size_t)c * 4 + i];
+      b->stats[(size_t)c * 4 + i] = s;
+    }
+  for (int w = 0; w < n_threads; ++w) b->err |= errs[w];
+  b->t = t0 + T;
+  b->cursor = T;
+  b->sampled_slot = -1;
+  return E_OK;
+}
+
 int wso_synchronize(void* h) { return status_from_err(((Batch*)h)->err); }
 
 /* introspection: info[0..9] = obs_dim, n_actions, act_dim, state_dim, T_max, T_cap,

@@ -99,3 +99,53 @@ def test_policy_rollout_uses_the_pre_step_observation():
     np.testing.assert_allclose(lp, np.log(pa.astype(np.float64)), rtol=1e-6, atol=1e-6)
     # the sampled actions follow the probabilities (frequency vs mean probability, 2400 draws)
     assert abs((act == 0).mean() - p[..., 0].mean()) < 0.03
+
+
+# ---------------------------------------------------------------- Gaussian policy (R34)
+def gauss_params(D, H, d, seed, log_std=-0.5):
+    r = np.random.default_rng(seed)
+    return np.concatenate([r.standard_normal(D * H) / np.sqrt(D), r.standard_normal(H) * 0.1,
+                           r.standard_normal(H * d) / np.sqrt(H), r.standard_normal(d) * 0.1,
+                           np.full(d, log_std)]).astype(np.float32)
+
+
+def test_gauss_policy_rows_match_fp64_network():
+    D, H, d = 3, 32, 1
+    w = gauss_params(D, H, d, seed=3)
+    obs = np.random.default_rng(4).standard_normal((400, D)).astype(np.float32)
+    rows = O.policy_gauss_rows(w, D, H, d, obs)
+    W1 = w[:D * H].reshape(D, H).astype(np.float64)
+    b1 = w[D * H:D * H + H].astype(np.float64)
+    W2 = w[D * H + H:D * H + H + H * d].reshape(H, d).astype(np.float64)
+    b2 = w[D * H + H + H * d:D * H + H + H * d + d].astype(np.float64)
+    mean = np.maximum(obs @ W1 + b1, 0) @ W2 + b2
+    np.testing.assert_allclose(rows[:, :d], mean, rtol=2e-5, atol=2e-6)
+    assert np.all(rows[:, d:] == np.float32(-0.5))
+
+
+def test_constant_gauss_policy_equals_given_rows():
+    """W2 = 0: the mean is b2 exactly, so the policy roll-out must reproduce the (pinned)
+    given-row Gaussian roll-out with rows (b2 | log_std) element by element."""
+    D, H, d, E, T = 3, 32, 1, 64, 120
+    w = gauss_params(D, H, d, seed=5, log_std=0.3)
+    w[D * H + H:D * H + H + H * d] = 0.0
+    a = O.Batch("pendulum", E, 1, W.SEED, t_capacity=T)
+    assert a.rollout_policy_gauss(T, w, H) == 0
+    rows = np.tile(np.concatenate([w[D * H + H + H * d:D * H + H + H * d + d], w[-d:]]), (E, 1, 1)).astype(np.float32)
+    b = O.Batch("pendulum", E, 1, W.SEED, t_capacity=T)
+    assert b.rollout(T, rows) == 0
+    for k in ("obs", "act", "logp", "rew", "done", "stats", "state"):
+        assert np.array_equal(a.array(k), b.array(k)), k
+
+
+def test_gauss_policy_logp_is_density_at_logged_observation():
+    from scipy.stats import norm
+    D, H, d, E, T = 3, 32, 1, 16, 40
+    w = gauss_params(D, H, d, seed=6, log_std=-0.2)
+    o = O.Batch("pendulum", E, 1, W.SEED, t_capacity=T)
+    assert o.rollout_policy_gauss(T, w, H) == 0
+    obs = o.array("obs")[:T].reshape(-1, D)
+    rows = O.policy_gauss_rows(w, D, H, d, obs)
+    act = o.array("act")[:T].reshape(-1)
+    ref = norm.logpdf(act.astype(np.float64), rows[:, 0].astype(np.float64), np.exp(np.float64(-0.2)))
+    np.testing.assert_allclose(o.array("logp")[:T].reshape(-1), ref, rtol=1e-5, atol=1e-5)
