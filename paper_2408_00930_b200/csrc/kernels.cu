@@ -1052,6 +1052,120 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
 }
 
 // =======================================================================================
+// NEXT-N1 for continuous actions (R34): Pendulum with a Gaussian MLP policy inside the fused
+// loop -- the R29 network (fp32 FMAs in R29's order) with one linear output as the mean and a
+// learned log_std, sampled by the R14 Gaussian head (gauss_sample: the GAUSS draw j = t of
+// the replica's stream, act = mean + exp(log_std) z, fp64 log-density); kCritic adds the R31
+// value head (values[t] = V(obs[t]), bootstrap = V(obs_live)).  Weights W1 [3][H] | b1 [H] |
+// W2 [H][1] | b2 [1] | log_std [1] (| wv [H] | bv) staged in shared memory.
+// =======================================================================================
+template <int H, bool kCritic>
+__global__ void __launch_bounds__(128) k_rollout_gpolicy(const KArgs a, const int T, const uint64_t t0,
+                                                        const float* __restrict__ weights,
+                                                        float* __restrict__ values, float* __restrict__ bootstrap) {
+  using L = Lane<Pendulum>;
+  using St = Pendulum::St;
+  constexpr int D = 3;
+  constexpr int NW = D * H + H + H + 1 + 1 + (kCritic ? H + 1 : 0);
+  __shared__ float sw[NW];
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = weights[i];
+  __syncthreads();
+  const float* W1 = sw;
+  const float* b1 = W1 + D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + H;
+  const float* ls = b2 + 1;
+  const float* wv = ls + 1;  // kCritic only
+  const int lane = threadIdx.x & 31;
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int64_t E = a.E;
+  if (e - lane >= E) return;
+  const bool live = e < E;
+  const int64_t ec = live ? e : E - 1;
+  const uint32_t eg = (uint32_t)(a.offset + ec);
+  const Key key{a.k0, a.k1};
+  constexpr int kRows = kContWinRows;
+  extern __shared__ __align__(16) uint32_t ws_smem[];
+  StatsWindow win;
+  win.init(ws_smem + (threadIdx.x >> 5) * (3 * kRows * kWinStride), kRows);
+  const size_t sE = (size_t)E;
+  St s;
+  L::load(a.state + ec * L::S, s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  uint32_t err = 0;
+  auto head = [&](const float (&o)[3], float& mean, float& v) {
+    mean = b2[0];
+    v = kCritic ? wv[H] : 0.0f;
+#pragma unroll
+    for (int j = 0; j < H; ++j) {
+      float acc = b1[j];
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
+      const float hj = acc > 0.0f ? acc : 0.0f;
+      mean = __fmaf_rn(W2[j], hj, mean);
+      if (kCritic) v = __fmaf_rn(wv[j], hj, v);
+    }
+  };
+  for (int c = 0; c < T; ++c) {
+    const uint64_t t = t0 + (uint64_t)c;
+    const size_t idx = (size_t)c * sE + (size_t)ec;
+    float sn, cs;
+    sincos_c(s.th, sn, cs);
+    float* dst = a.obs + idx * L::D;  // (cos th, sin th, thdot)
+    st_cs(dst, cs);
+    st_cs(dst + 1, sn);
+    st_cs(dst + 2, s.thd);
+    const float o[3] = {cs, sn, s.thd};
+    float mean1, v;
+    head(o, mean1, v);
+    if (kCritic) st_cs(values + idx, v);
+    const float mean[1] = {mean1}, lstd[1] = {ls[0]};
+    float act[1], lp;
+    const bool okp = gauss_sample<1>(key, eg, 0, t, mean, lstd, act, lp);
+    st_cs(reinterpret_cast<float*>(a.act) + idx, act[0]);
+    if (a.write_logp) st_cs(a.logp + idx, lp);
+    St s2 = s;
+    float r = 0.0f;
+    const bool ok = isfinite(act[0]);
+    if (live && !okp) err |= kErrProbs;
+    if (live && !ok) err |= kErrAction;
+    if (ok) Pendulum::step_sin(s2, act[0], sn, r);
+    const int32_t es = ep_step + 1;
+    const uint32_t d = ok ? (es >= a.max_steps ? 2u : 0u) : 0u;
+    const float ret = ep_ret + r;
+    const float rw = ok ? r : 0.0f;
+    if (d) L::init(key, eg, rc + 1, s2);
+    s = ok ? s2 : s;
+    rc += d ? 1u : 0u;
+    ep_step = d ? 0 : (ok ? es : ep_step);
+    ep_ret = d ? 0.0f : (ok ? ret : ep_ret);
+    st_cs(a.rew + idx, rw);
+    st_cs_u8(a.done + idx, (uint8_t)d);
+    win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
+      win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, (int)min((int64_t)32, E - (e - lane)));
+  }
+  if (kCritic) {
+    float sn, cs;
+    sincos_c(s.th, sn, cs);
+    const float o[3] = {cs, sn, s.thd};
+    float m_unused, v;
+    head(o, m_unused, v);
+    if (live) bootstrap[e] = v;
+  }
+  if (live) {
+    L::save(a.state + e * L::S, s);
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    L::obs_store(a.obs_live + e * L::D, s, false);
+    if (err) atomicOr(a.err, err);
+  }
+}
+
+// =======================================================================================
 // surface-D (R23) with one WARP per replica and one lane per coordinate (D <= 32): the
 // lane-per-replica kernel leaves C5's 2 000 replicas in 63 warps; this mapping gives 2 000.
 // Sums over coordinates (spring energy, goal distance, Gaussian log-density) are gathered
@@ -2049,10 +2163,33 @@ static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64
   return cudaGetLastError();
 }
 
+static cudaError_t rollout_gpolicy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
+                                   int hidden, float* values, float* bootstrap) {
+  const size_t smem = (size_t)4 * 3 * kContWinRows * kWinStride * sizeof(uint32_t);  // 4 warps' windows
+  const unsigned g = grid_for(a.E, 128);
+  l.m(kKRollout, 0);
+  if (values) {
+    switch (hidden) {
+      case 32: k_rollout_gpolicy<32, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 64: k_rollout_gpolicy<64, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      default: return cudaErrorInvalidValue;
+    }
+  } else {
+    switch (hidden) {
+      case 32: k_rollout_gpolicy<32, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 64: k_rollout_gpolicy<64, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      default: return cudaErrorInvalidValue;
+    }
+  }
+  l.m(kKRollout, 1);
+  return cudaGetLastError();
+}
+
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, uint64_t* launches, float* values, float* bootstrap) {
   cudaError_t err = cudaErrorInvalidValue;
   switch (l.kind) {
+    case kPendulum: err = rollout_gpolicy(a, l, T, t0, weights, hidden, values, bootstrap); break;
     case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden, values, bootstrap); break;
     case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden, values, bootstrap); break;
     case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden, values, bootstrap); break;

@@ -93,6 +93,46 @@ def test_policy_argument_validation(P):
     t = P.Env(2, 10, "tag", SEED, t_capacity=4)
     with pytest.raises(P.WSError):
         t.rollout_policy(4, w, 32)  # multi-agent env: not supported by the policy roll-out
-    p = P.Env(4, 1, "pendulum", SEED, t_capacity=4)
+    p = P.Env(4, 1, "surface", SEED, t_capacity=4, param0=20)
     with pytest.raises(P.WSError):
-        p.rollout_policy(4, w, 32)  # continuous actions
+        p.rollout_policy(4, w, 32)  # continuous actions beyond Pendulum (R34): not supported
+
+
+@pytest.mark.parametrize("H,E,T", [(32, 300, 200), (64, 129, 150)])
+def test_gaussian_policy_rollout_parity(P, H, E, T):
+    """NEXT-N1 continuous (R34): Pendulum with the Gaussian MLP policy in the fused loop
+    against the oracle's policy roll-out: obs / act / rew / done / state bit-identical,
+    log-probs within 2 ulp (R18); with the critic, values within the critic tolerance."""
+    from test_oracle_policy import gauss_params
+    D, d = 3, 1
+    w = gauss_params(D, H, d, seed=17, log_std=-0.3)
+    g = P.Env(E, 1, "pendulum", SEED, t_capacity=T)
+    g.rollout_policy(T, torch.from_numpy(w).cuda(), H)
+    assert g.status() == 0
+    o = O.Batch("pendulum", E, 1, SEED, t_capacity=T)
+    assert o.rollout_policy_gauss(T, w, H, n_threads=8) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done", "state", "obs_live", "reset_count"):
+        ref = o.array(k)[:T] if k in ("obs", "act", "rew", "done") else o.array(k)
+        got = buf[k][:T] if k in ("obs", "act", "rew", "done") else buf[k]
+        assert np.array_equal(got, ref), k
+    lg, lo = buf["logp"][:T].ravel(), o.array("logp")[:T].ravel()
+    assert np.all(np.abs(lg.view(np.int32).astype(np.int64) - lo.view(np.int32).astype(np.int64)) <= 2)
+    st_g, st_o = g.stats_f64(T).cpu().numpy(), np.array(o.array("stats"))[:T]
+    assert np.array_equal(st_g[:, [0, 2]], st_o[:, [0, 2]])
+    # R20: per-replica rewards rounded to multiples of 2^-32 (Pendulum rewards can be < 2^-8)
+    np.testing.assert_allclose(st_g[:, [1, 3]], st_o[:, [1, 3]], rtol=1e-12, atol=E * 2.0 ** -32)
+    # critic variant: same store, values = wv^T h + bv of the logged observations
+    r = np.random.default_rng(18)
+    head = np.concatenate([r.standard_normal(H) / np.sqrt(H), [-3.0]]).astype(np.float32)
+    wc = np.concatenate([w, head])
+    gc = P.Env(E, 1, "pendulum", SEED, t_capacity=T)
+    vals, boot = torch.empty(T * E, device="cuda"), torch.empty(E, device="cuda")
+    gc.rollout_actor_critic(T, torch.from_numpy(wc).cuda(), H, vals, boot)
+    assert np.array_equal(gc.buffers()["act"].cpu().numpy(), buf["act"])
+    obs = buf["obs"][:T].reshape(-1, D).astype(np.float64)
+    W1 = w[:D * H].reshape(D, H).astype(np.float64)
+    b1 = w[D * H:D * H + H].astype(np.float64)
+    h = np.maximum(obs @ W1 + b1, 0.0)
+    ref = h @ head[:H].astype(np.float64) + head[H]
+    assert np.all(np.abs(vals.cpu().numpy() - ref) <= 1e-5 * (3.0 + h @ np.abs(head[:H])))
