@@ -211,3 +211,76 @@ def ppo_grad(params, obs, act, adv_hat, ret, logp_old, D, H, n, c_v, c_e, eps, b
     Ah = np.asarray(adv_hat, dtype=np.float64).ravel()
     active = rho * Ah <= np.clip(rho, 1 - eps, 1 + eps) * Ah
     return grad(params, obs, act, np.where(active, rho * Ah, 0.0), ret, D, H, n, c_v, c_e, batch)
+
+
+# ------------------------------------------------------------------------------ Gaussian (R35)
+# Continuous actions ("both discrete and continuous actions"): the R34 Gaussian policy
+# with the R31 value head.  Packed params  W1 [D][H] | b1 [H] | W2 [H][d] | b2 [d] |
+# log_std [d] | wv [H] | bv.  log pi(a|o) = sum_k -(a_k - mu_k)^2 / (2 sigma_k^2) - log sigma_k
+# - log(2 pi)/2, entropy = sum_k log sigma_k + log(2 pi e)/2 (state independent); the loss
+# is R31's with these.
+
+def n_params_gauss(D: int, H: int, d: int) -> int:
+    return D * H + H + H * d + d + d + H + 1
+
+
+def unpack_gauss(params, D: int, H: int, d: int):
+    p = np.asarray(params, dtype=np.float64)
+    assert p.size == n_params_gauss(D, H, d)
+    o = 0
+    W1 = p[o:o + D * H].reshape(D, H); o += D * H
+    b1 = p[o:o + H]; o += H
+    W2 = p[o:o + H * d].reshape(H, d); o += H * d
+    b2 = p[o:o + d]; o += d
+    log_std = p[o:o + d]; o += d
+    wv = p[o:o + H]; o += H
+    return W1, b1, W2, b2, log_std, wv, p[o]
+
+
+def forward_gauss(params, obs, D, H, d):
+    W1, b1, W2, b2, log_std, wv, bv = unpack_gauss(params, D, H, d)
+    o = np.asarray(obs, dtype=np.float64).reshape(-1, D)
+    z = o @ W1 + b1
+    h = np.maximum(z, 0.0)
+    return z, h, h @ W2 + b2, log_std, h @ wv + bv
+
+
+def loss_gauss(params, obs, act, adv_hat, ret, D, H, d, c_v, c_e, batch=None):
+    _, _, mu, log_std, V = forward_gauss(params, obs, D, H, d)
+    a = np.asarray(act, dtype=np.float64).reshape(-1, d)
+    ok = np.isfinite(a).all(axis=1)
+    a = np.where(np.isfinite(a), a, 0.0)
+    B = len(a) if batch is None else batch
+    sig2 = np.exp(2 * log_std)
+    logp = (-(a - mu) ** 2 / (2 * sig2) - log_std - 0.5 * np.log(2 * np.pi)).sum(axis=1)
+    ent = (log_std + 0.5 * np.log(2 * np.pi * np.e)).sum()
+    Ah = np.asarray(adv_hat, dtype=np.float64).ravel()
+    R = np.asarray(ret, dtype=np.float64).ravel()
+    pol = -(logp * Ah)[ok].sum() / B
+    val = c_v * ((V - R) ** 2)[ok].sum() / B
+    entt = -c_e * ent * ok.sum() / B
+    return pol + val + entt, pol, val, entt
+
+
+def grad_gauss(params, obs, act, adv_hat, ret, D, H, d, c_v, c_e, batch=None) -> np.ndarray:
+    """Chain rule: dL/dmu_k = -(A_hat/B)(a_k - mu_k)/sigma_k^2;
+    dL/dlog_sigma_k = sum_rows -(A_hat/B)((a_k - mu_k)^2/sigma_k^2 - 1) - c_e n_valid / B;
+    the rest as in `grad` with dL/dlogit replaced by dL/dmu.  Rows with a non-finite action
+    contribute nothing."""
+    W1, b1, W2, b2, log_std, wv, bv = unpack_gauss(params, D, H, d)
+    z, h, mu, _, V = forward_gauss(params, obs, D, H, d)
+    o = np.asarray(obs, dtype=np.float64).reshape(-1, D)
+    a = np.asarray(act, dtype=np.float64).reshape(-1, d)
+    ok = np.isfinite(a).all(axis=1)
+    a = np.where(np.isfinite(a), a, 0.0)
+    w = ok.astype(np.float64)
+    B = len(a) if batch is None else batch
+    Ah = np.asarray(adv_hat, dtype=np.float64).ravel()
+    R = np.asarray(ret, dtype=np.float64).ravel()
+    sig2 = np.exp(2 * log_std)
+    dmu = -(Ah / B)[:, None] * (a - mu) / sig2 * w[:, None]
+    dls = (-(Ah / B)[:, None] * ((a - mu) ** 2 / sig2 - 1.0) * w[:, None]).sum(axis=0) - c_e * w.sum() / B
+    dV = 2.0 * c_v * (V - R) / B * w
+    dz = (dmu @ W2.T + dV[:, None] * wv[None, :]) * (z > 0)
+    return np.concatenate([(o.T @ dz).ravel(), dz.sum(axis=0), (h.T @ dmu).ravel(), dmu.sum(axis=0), dls,
+                           h.T @ dV, [dV.sum()]])

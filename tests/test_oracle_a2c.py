@@ -220,3 +220,39 @@ def test_ppo_identity_and_clip_rule():
     assert Lr[1] == pytest.approx(-1.2, rel=1e-12)
     g = OA.ppo_grad(params, obs[:1], act[:1], one, ret[:1], lo, D, H, n, 0.0, 0.0, 0.2)
     assert np.abs(g).max() == 0.0
+
+
+# ---------------------------------------------------------------- Gaussian actor-critic (R35)
+@pytest.mark.parametrize("D,H,d", [(3, 8, 1), (3, 32, 1), (5, 16, 2)])
+def test_gauss_grad_matches_torch_and_differences(D, H, d):
+    r = np.random.default_rng(D * 10 + d)
+    params = r.standard_normal(OA.n_params_gauss(D, H, d)) * 0.5
+    B = 150
+    obs = r.standard_normal((B, D))
+    act = r.standard_normal((B, d)) * 1.5
+    act[::23] = np.nan  # rows with a non-finite action contribute nothing
+    adv, ret = r.standard_normal(B), r.standard_normal(B)
+    g = OA.grad_gauss(params, obs, act, adv, ret, D, H, d, 0.5, 0.03, batch=200)
+    # torch autograd of an independent formulation (torch.distributions.Normal)
+    p = torch.tensor(params, requires_grad=True)
+    W1, b1, W2, b2, ls, wv, bv = torch.split(p, [D * H, H, H * d, d, d, H, 1])
+    o = torch.tensor(obs)
+    h = torch.relu(o @ W1.view(D, H) + b1)
+    dist = torch.distributions.Normal(h @ W2.view(H, d) + b2, torch.exp(ls))
+    ok = torch.tensor(np.isfinite(act).all(axis=1)).double()
+    a = torch.tensor(np.nan_to_num(act))
+    V = (h @ wv + bv)
+    L = (-(dist.log_prob(a).sum(1) * torch.tensor(adv) * ok).sum() + 0.5 * (((V - torch.tensor(ret)) ** 2) * ok).sum()
+         - 0.03 * (dist.entropy().sum(1) * ok).sum()) / 200
+    L.backward()
+    np.testing.assert_allclose(g, p.grad.numpy(), rtol=1e-9, atol=1e-12)
+    assert OA.loss_gauss(params, obs, act, adv, ret, D, H, d, 0.5, 0.03, batch=200)[0] == pytest.approx(L.item(), rel=1e-12)
+    # central differences of the oracle's own loss (fp64)
+    fd = np.zeros_like(g)
+    for i in range(0, params.size, max(1, params.size // 40)):
+        pp, pm = params.copy(), params.copy()
+        pp[i] += 1e-6
+        pm[i] -= 1e-6
+        fd[i] = (OA.loss_gauss(pp, obs, act, adv, ret, D, H, d, 0.5, 0.03, batch=200)[0] -
+                 OA.loss_gauss(pm, obs, act, adv, ret, D, H, d, 0.5, 0.03, batch=200)[0]) / 2e-6
+        assert abs(fd[i] - g[i]) <= 1e-5 * max(1e-3, abs(g[i])), i
