@@ -82,7 +82,8 @@ class ws_a2c_args(C.Structure):
                 ("params", C.c_void_p), ("obs", C.c_void_p), ("act", C.c_void_p), ("adv", C.c_void_p),
                 ("ret", C.c_void_p), ("moments", C.c_void_p), ("batch", C.c_double), ("c_v", C.c_float),
                 ("c_e", C.c_float), ("workspace", C.c_void_p), ("grad", C.c_void_p), ("loss", C.c_void_p),
-                ("logp_old", C.c_void_p), ("clip_eps", C.c_float), ("norm_batch", C.c_double)]
+                ("logp_old", C.c_void_p), ("clip_eps", C.c_float), ("norm_batch", C.c_double),
+                ("gaussian", C.c_int32), ("act_f", C.c_void_p)]
 
 
 class ws_host_store(C.Structure):
@@ -130,6 +131,7 @@ _SIGS = {
     "ws_gae_store": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float,
                                C.c_void_p, C.c_void_p]),
     "ws_a2c_n_params": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32]),
+    "ws_a2c_n_params_ex": (C.c_int32, [C.c_int32, C.c_int32, C.c_int32, C.c_int32]),
     "ws_a2c_workspace_bytes": (C.c_size_t, [C.c_int32, C.c_int32, C.c_int32]),
     "ws_ac_values": (C.c_int, [C.c_void_p, C.c_int32, C.c_int32, C.c_int32, C.c_void_p, C.c_int64, C.c_void_p,
                                C.c_void_p]),

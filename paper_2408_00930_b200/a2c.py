@@ -24,8 +24,9 @@ from ._abi import WSError, check, lib
 from .env import Env
 
 
-def n_params(obs_dim: int, hidden: int, n_actions: int) -> int:
-    return int(lib().ws_a2c_n_params(obs_dim, hidden, n_actions))
+def n_params(obs_dim: int, hidden: int, n_actions: int, gaussian: bool = False) -> int:
+    """Packed parameter count (R31; gaussian: the R35 layout with log_std after b2)."""
+    return int(lib().ws_a2c_n_params_ex(obs_dim, hidden, n_actions, 1 if gaussian else 0))
 
 
 def workspace(obs_dim: int, hidden: int, n_actions: int, device) -> torch.Tensor:
@@ -71,23 +72,29 @@ def a2c_grad(params, obs, act, adv, ret, mom, batch: float, obs_dim: int, hidden
              loss: Optional[torch.Tensor] = None, stream=None, logp_old: Optional[torch.Tensor] = None,
              clip_eps: float = 0.2, norm_batch: float = 0.0):
     """This shard's gradient of the S:405 loss (ws_a2c_grad) -> (grad f32 [P], loss f64 [3]).
-    logp_old given: the PPO clipped surrogate (R33) instead of the A2C policy term."""
+    logp_old given: the PPO clipped surrogate (R33) instead of the A2C policy term.  act float32
+    [rows, n_actions]: continuous actions, Gaussian head (R35)."""
     rows = adv.numel()
-    P = n_params(obs_dim, hidden, n_actions)
+    gaussian = act.dtype == torch.float32
+    P = n_params(obs_dim, hidden, n_actions, gaussian)
     _f32("params", params, P)
     _f32("obs", obs, rows * obs_dim)
     _f32("adv", adv, rows)
     _f32("ret", ret, rows)
-    if act.dtype != torch.int32 or not act.is_contiguous() or act.numel() != rows:
+    if gaussian:
+        _f32("act", act, rows * n_actions)
+    elif act.dtype != torch.int32 or not act.is_contiguous() or act.numel() != rows:
         raise WSError(_abi.INVALID_ARGUMENT, "act: contiguous int32 with one entry per row")
     grad = torch.empty(P, dtype=torch.float32, device=adv.device) if grad is None else grad
     loss = torch.empty(3, dtype=torch.float64, device=adv.device) if loss is None else loss
     if logp_old is not None:
         _f32("logp_old", logp_old, rows)
-    a = _abi.ws_a2c_args(obs_dim, hidden, n_actions, rows, params.data_ptr(), obs.data_ptr(), act.data_ptr(),
+    a = _abi.ws_a2c_args(obs_dim, hidden, n_actions, rows, params.data_ptr(), obs.data_ptr(),
+                         None if gaussian else act.data_ptr(),
                          adv.data_ptr(), ret.data_ptr(), mom.data_ptr(), float(batch), c_v, c_e, ws.data_ptr(),
                          grad.data_ptr(), loss.data_ptr(),
-                         None if logp_old is None else logp_old.data_ptr(), clip_eps, float(norm_batch))
+                         None if logp_old is None else logp_old.data_ptr(), clip_eps, float(norm_batch),
+                         1 if gaussian else 0, act.data_ptr() if gaussian else None)
     check(lib().ws_a2c_grad(C.byref(a), _s(stream, adv)))
     return grad, loss
 
@@ -102,14 +109,18 @@ def adam(params, grad, m, v, step: int, lr: float, beta1: float = 0.9, beta2: fl
                         eps, max_norm, None if grad_norm is None else grad_norm.data_ptr(), _s(stream, params)))
 
 
-def init_params(obs_dim: int, hidden: int, n_actions: int, seed: int = 0, device=None) -> torch.Tensor:
-    """Initial weights: W1 ~ N(0, 1/D), W2 ~ N(0, 0.01^2/H) (near-uniform policy), wv ~ N(0, 1/H),
-    zero biases; seeded on the host, copied once to the device."""
+def init_params(obs_dim: int, hidden: int, n_actions: int, seed: int = 0, device=None,
+                gaussian: bool = False) -> torch.Tensor:
+    """Initial weights: W1 ~ N(0, 1/D), W2 ~ N(0, 0.01^2/H) (near-uniform policy / near-zero
+    mean), log_std = 0 (Gaussian head), wv ~ N(0, 1/H), zero biases; seeded on the host,
+    copied once to the device."""
     g = torch.Generator().manual_seed(seed)
     D, H, N = obs_dim, hidden, n_actions
     parts = [torch.randn(D * H, generator=g) / D ** 0.5, torch.zeros(H),
-             torch.randn(H * N, generator=g) * (0.01 / H ** 0.5), torch.zeros(N),
-             torch.randn(H, generator=g) / H ** 0.5, torch.zeros(1)]
+             torch.randn(H * N, generator=g) * (0.01 / H ** 0.5), torch.zeros(N)]
+    if gaussian:
+        parts.append(torch.zeros(N))
+    parts += [torch.randn(H, generator=g) / H ** 0.5, torch.zeros(1)]
     return torch.cat(parts).float().to(device)
 
 
@@ -124,13 +135,17 @@ class A2C:
                  beta2: float = 0.999, eps: float = 1e-8, seed: int = 0, params: Optional[torch.Tensor] = None,
                  group: Optional[dist.ProcessGroup] = None):
         info = env.info()
-        if int(info.n_agents) != 1 or int(info.n_actions) < 1:
-            raise WSError(_abi.INVALID_ARGUMENT, "A2C: single-agent discrete envs (cartpole, acrobot, dummy)")
+        self.gaussian = int(info.n_actions) == 0  # continuous actions: Gaussian head (R34 / R35)
+        if int(info.n_agents) != 1:
+            raise WSError(_abi.INVALID_ARGUMENT, "A2C: single-agent envs")
         self.env, self.H = env, hidden
-        self.D, self.N, self.E = int(info.obs_dim), int(info.n_actions), int(info.n_envs)
-        self.P = n_params(self.D, hidden, self.N)
+        self.D, self.E = int(info.obs_dim), int(info.n_envs)
+        self.N = int(info.act_dim) if self.gaussian else int(info.n_actions)
+        self.P = n_params(self.D, hidden, self.N, self.gaussian)
+        if self.P == 0 or int(lib().ws_a2c_workspace_bytes(self.D, hidden, self.N)) == 0:
+            raise WSError(_abi.INVALID_ARGUMENT, f"A2C: unsupported network shape D={self.D} H={hidden} n={self.N}")
         dev = env.device
-        self.params = (init_params(self.D, hidden, self.N, seed, dev) if params is None
+        self.params = (init_params(self.D, hidden, self.N, seed, dev, self.gaussian) if params is None
                        else params.detach().to(dev, torch.float32).contiguous().clone())
         if self.params.numel() != self.P:
             raise WSError(_abi.INVALID_ARGUMENT, f"params: {self.P} floats")
@@ -166,9 +181,11 @@ class A2C:
         buf = env.buffers()
         rows = T * self.E
         obs = buf["obs"][:T].reshape(rows * D)
-        act = buf["act"][:T].reshape(rows)
+        act = buf["act"][:T].reshape(rows * N if self.gaussian else rows)
         self._value_buf(rows)
         if not values_ready:
+            if self.gaussian:
+                raise WSError(_abi.INVALID_ARGUMENT, "Gaussian A2C: the critic comes from the roll-out kernel")
             ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
             ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
         adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
@@ -230,5 +247,6 @@ class PPO(A2C):
                 for m in range(M):
                     t0, t1 = T * m // M, T * (m + 1) // M
                     r0, r1 = t0 * E, t1 * E
-                    self._step(obs[r0 * D:r1 * D], act[r0:r1], adv[r0:r1], ret[r0:r1], r1 - r0, rows,
+                    na = self.N if self.gaussian else 1
+                    self._step(obs[r0 * D:r1 * D], act[r0 * na:r1 * na], adv[r0:r1], ret[r0:r1], r1 - r0, rows,
                                logp_old=logp[r0:r1], clip_eps=self.clip_eps)

@@ -39,22 +39,26 @@ constexpr int kMomBlocks = 296;  // fixed grid of k_moments (order depends only 
 
 struct Layout {
   int D, H, N, oW1, ob1, oW2, ob2, owv, obv, P;
+  int ols;  // Gaussian (R35): log_std [N] after b2; == ob2 + N for the discrete layout too (empty)
 };
 
-__host__ __device__ inline Layout layout(int D, int H, int N) {
+// G = 1: Gaussian head (R35) -- N mean outputs, then log_std [N] before the value head
+__host__ __device__ inline Layout layout(int D, int H, int N, int G = 0) {
   Layout L;
   L.D = D; L.H = H; L.N = N;
   L.oW1 = 0;
   L.ob1 = D * H;
   L.oW2 = L.ob1 + H;
   L.ob2 = L.oW2 + H * N;
-  L.owv = L.ob2 + N;
+  L.ols = L.ob2 + N;
+  L.owv = L.ols + G * N;
   L.obv = L.owv + H;
   L.P = L.obv + 1;
   return L;
 }
 
-bool supported(int D, int H, int N) {
+bool supported(int D, int H, int N, int G = 0) {
+  if (G) return D == 3 && (H == 32 || H == 64) && N == 1;  // Pendulum (R34 / R35)
   return (D == 4 || D == 6) && (H == 32 || H == 64) && (N == 2 || N == 3 || N == 5);
 }
 
@@ -67,10 +71,10 @@ struct Rec {
   static constexpr int kLen = (D + 2 + N + 3) & ~3;
 };
 
-template <int D, int H, int N>
+template <int D, int H, int N, int G = 0>
 __device__ __forceinline__ void load_records(float* wrec, const float* params) {
   using RC = Rec<D, N>;
-  const Layout L = layout(D, H, N);
+  const Layout L = layout(D, H, N, G);
   for (int i = threadIdx.x; i < H * RC::kLen; i += blockDim.x) {
     const int k = i / RC::kLen, f = i % RC::kLen;
     float x = 0.0f;
@@ -163,14 +167,15 @@ struct GradDev {
   float c_v, c_e;
   int64_t rows;
   double* partial;  // [gridDim.x][P + 3]
+  const float* act_f;     // Gaussian (R35): actions [rows][N] f32
   const float* logp_old;  // PPO (R33): behaviour log-probs [rows]; null = A2C
   float clip_eps;
   double norm_batch;      // rows the moments were summed over (minibatches: the whole batch)
 };
 
-template <int D, int H, int N>
+template <int D, int H, int N, int G = 0>
 struct GradSmem {
-  static constexpr int kP = D * H + H + H * N + N + H + 1;
+  static constexpr int kP = D * H + H + H * N + N + G * N + H + 1;
   static constexpr int kRec = Rec<D, N>::kLen;       // per-hidden-unit weight record
   static constexpr int kOg = (D + N + 1 + 3) & ~3;   // per-row record: o, dL/dlogit, dL/dV
   static constexpr int kHrow = H + 4;                // h row stride: 16-B rows, kHrow/4 odd
@@ -181,23 +186,26 @@ struct GradSmem {
   static constexpr int kFloats = kOgs + kTile * kOg;
   static constexpr size_t kBytes = (size_t)kFloats * sizeof(float);
   static_assert((kHrow / 4) % 2 == 1, "conflict-free 16-B row stores");
-  static_assert(kTile * kHrow >= 4 * kP + kTile * (N + 4), "reduction scratch fits the h tile");
+  static constexpr int kTh = N + 4 + G * N;          // per-thread scalars: b2, bv, 3 loss terms (+ log_std)
+  static_assert(kTile * kHrow >= 4 * kP + kTile * kTh, "reduction scratch fits the h tile");
+  static_assert(!G || N <= 3, "Gaussian head: b2 | bv | log_std fit the 8-float slot");
 };
 
-template <int D, int H, int N>
+template <int D, int H, int N, int G = 0>
 __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
-  using S = GradSmem<D, H, N>;
+  using S = GradSmem<D, H, N, G>;
   using RC = Rec<D, N>;
-  constexpr Layout L{D, H, N, 0, D * H, D * H + H, D * H + H + H * N, D * H + H + H * N + N,
-                     D * H + H + H * N + N + H, S::kP};
+  constexpr Layout L{D, H, N, 0, D * H, D * H + H, D * H + H + H * N, D * H + H + H * N + N + G * N,
+                     D * H + H + H * N + N + G * N + H, S::kP, D * H + H + H * N + N};
   constexpr int KP = H / 32;  // hidden units per lane in phase B (consecutive: k = KP*lane + q)
   extern __shared__ __align__(16) float sm[];
   float* wrec = sm + S::kW;
   float* hs = sm + S::kHs;
   float* ogs = sm + S::kOgs;
-  load_records<D, H, N>(wrec, g.params);
+  load_records<D, H, N, G>(wrec, g.params);
   if (threadIdx.x < N) sm[S::kB2 + threadIdx.x] = __ldg(g.params + L.ob2 + threadIdx.x);
   if (threadIdx.x == N) sm[S::kB2 + N] = __ldg(g.params + L.obv);
+  if (G && threadIdx.x < N) sm[S::kB2 + 4 + threadIdx.x] = __ldg(g.params + L.ols + threadIdx.x);
 
   // normalisation (R31): mu, sigma over the global batch; skipped when sigma < 1e-8
   const double mu = g.moments[0] / g.norm_batch;
@@ -221,9 +229,9 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
     ab1[q] = 0.0f;
     awv[q] = 0.0f;
   }
-  float ab2[N], abv = 0.0f, lpol = 0.0f, lval = 0.0f, lent = 0.0f;
+  float ab2[N], abv = 0.0f, lpol = 0.0f, lval = 0.0f, lent = 0.0f, als[N];
 #pragma unroll
-  for (int j = 0; j < N; ++j) ab2[j] = 0.0f;
+  for (int j = 0; j < N; ++j) ab2[j] = 0.0f, als[j] = 0.0f;
   __syncthreads();
   // phase-B weights of this lane's hidden units, in registers for the whole kernel
   float w2k[KP][N], wvk[KP];
@@ -249,7 +257,7 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
     float* og = ogs + s * S::kOg;
     if (s < nrow) {
       const int64_t r = base + s;
-      const int a = __ldg(g.act + r);
+      const int a = G ? 0 : __ldg(g.act + r);
       const float A = __ldg(g.adv + r);
       const float R = __ldg(g.ret + r);
       float o[D];
@@ -294,7 +302,51 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
       float dl[N], dv = 0.0f;
 #pragma unroll
       for (int j = 0; j < N; ++j) dl[j] = 0.0f;
-      if (a >= 0 && a < N) {
+      if constexpr (G) {
+        // Gaussian head (R35): mean = the linear outputs, log pi = sum_j -(a-mu)^2/(2 s^2)
+        // - log s - log(2 pi)/2; rows with a non-finite action contribute nothing
+        float act[N];
+        bool okr = true;
+#pragma unroll
+        for (int j = 0; j < N; ++j) {
+          act[j] = __ldg(g.act_f + r * N + j);
+          okr = okr && isfinite(act[j]);
+        }
+        if (okr) {
+          const float v = v0 + v1;
+          float diff[N], iv[N], lpa = 0.0f, ent = 0.0f;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            const float ls = sm[S::kB2 + 4 + j];
+            diff[j] = act[j] - (l0[j] + l1[j]);
+            iv[j] = expf(-2.0f * ls);
+            lpa += -0.5f * diff[j] * diff[j] * iv[j] - ls - 0.91893853320467274f;
+            ent += ls + 1.41893853320467274f;  // log(2 pi e) / 2
+          }
+          float Ah = norm ? (float)(((double)A - mu) * inv_sigma) : A;
+          float surr = lpa * Ah;
+          if (g.logp_old) {
+            const float rho = expf(lpa - __ldg(g.logp_old + r));
+            const float rc = fminf(fmaxf(rho, 1.0f - g.clip_eps), 1.0f + g.clip_eps);
+            const float s1 = rho * Ah, s2 = rc * Ah;
+            surr = fminf(s1, s2);
+            Ah = s1 <= s2 ? s1 : 0.0f;
+          }
+          const float Ab = Ah * invB;
+#pragma unroll
+          for (int j = 0; j < N; ++j) {
+            dl[j] = -Ab * diff[j] * iv[j];
+            als[j] += -Ab * (diff[j] * diff[j] * iv[j] - 1.0f) - ce_b;
+          }
+          dv = cv2_b * (v - R);
+          lpol -= surr * invB;
+          lval += cv_b * (v - R) * (v - R);
+          lent -= ce_b * ent;
+#pragma unroll
+          for (int j = 0; j < N; ++j) ab2[j] += dl[j];
+          abv += dv;
+        }
+      } else if (a >= 0 && a < N) {
         float l[N];
 #pragma unroll
         for (int j = 0; j < N; ++j) l[j] = l0[j] + l1[j];
@@ -383,7 +435,7 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
   // ---- CTA reduction in a fixed order: per-warp unit partials, per-thread bias / loss terms
   double* out = g.partial + (size_t)blockIdx.x * (S::kP + 3);
   float* red = hs;                  // [kWarps][P]
-  float* th = hs + kWarps * S::kP;  // [kTile][N + 4]
+  float* th = hs + kWarps * S::kP;  // [kTile][kTh]
 #pragma unroll
   for (int q = 0; q < KP; ++q) {
     const int k = KP * lane + q;
@@ -396,26 +448,33 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
     rw[L.owv + k] = awv[q];
   }
   {
-    float* t = th + tid * (N + 4);
+    float* t = th + tid * S::kTh;
 #pragma unroll
     for (int j = 0; j < N; ++j) t[j] = ab2[j];
     t[N] = abv;
     t[N + 1] = lpol;
     t[N + 2] = lval;
     t[N + 3] = lent;
+    if (G) {
+#pragma unroll
+      for (int j = 0; j < N; ++j) t[N + 4 + j] = als[j];
+    }
   }
   __syncthreads();
   for (int i = tid; i < S::kP; i += kTile) {
-    if ((i >= L.ob2 && i < L.ob2 + N) || i == L.obv) continue;
+    if ((i >= L.ob2 && i < L.ob2 + N + G * N) || i == L.obv) continue;
     double acc = 0.0;
 #pragma unroll
     for (int w = 0; w < kWarps; ++w) acc += (double)red[w * S::kP + i];
     out[i] = acc;
   }
-  if (tid < N + 4) {
+  if (tid < S::kTh) {
     double acc = 0.0;
-    for (int t = 0; t < kTile; ++t) acc += (double)th[t * (N + 4) + tid];
-    const int dst = tid < N ? L.ob2 + tid : (tid == N ? L.obv : S::kP + (tid - N - 1));
+    for (int t = 0; t < kTile; ++t) acc += (double)th[t * S::kTh + tid];
+    const int dst = tid < N ? L.ob2 + tid
+                  : tid == N ? L.obv
+                  : tid < N + 4 ? S::kP + (tid - N - 1)
+                  : L.ols + (tid - N - 4);
     out[dst] = acc;
   }
 }
@@ -463,23 +522,23 @@ __global__ void __launch_bounds__(1024) k_adam(float* __restrict__ params, const
 }
 
 // ------------------------------------------------------------------------------ dispatch
-template <int D, int H, int N>
+template <int D, int H, int N, int G = 0>
 cudaError_t launch_grad_t(const GradDev& g, cudaStream_t s, int* nb_out) {
-  using S = GradSmem<D, H, N>;
+  using S = GradSmem<D, H, N, G>;
   static int grid_cap = 0;  // CTAs per device at full residency (same for every B200)
   cudaError_t e = cudaSuccess;
   if (!grid_cap) {
-    e = cudaFuncSetAttribute(k_a2c_grad<D, H, N>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kBytes);
+    e = cudaFuncSetAttribute(k_a2c_grad<D, H, N, G>, cudaFuncAttributeMaxDynamicSharedMemorySize, (int)S::kBytes);
     if (e) return e;
     int dev = 0, sms = 0, per_sm = 0;
     if ((e = cudaGetDevice(&dev))) return e;
     if ((e = cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev))) return e;
-    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_a2c_grad<D, H, N>, kTile, S::kBytes))) return e;
+    if ((e = cudaOccupancyMaxActiveBlocksPerMultiprocessor(&per_sm, k_a2c_grad<D, H, N, G>, kTile, S::kBytes))) return e;
     grid_cap = std::max(1, std::min(kMaxGrid, sms * std::max(per_sm, 1)));
   }
   const int64_t tiles = (g.rows + kTile - 1) / kTile;
   const int nb = (int)std::max<int64_t>(1, std::min<int64_t>(tiles, grid_cap));
-  k_a2c_grad<D, H, N><<<nb, kTile, S::kBytes, s>>>(g);
+  k_a2c_grad<D, H, N, G><<<nb, kTile, S::kBytes, s>>>(g);
   *nb_out = nb;
   return cudaGetLastError();
 }
@@ -493,7 +552,8 @@ cudaError_t launch_grad_dh(int N, const GradDev& g, cudaStream_t s, int* nb) {
   }
 }
 
-cudaError_t launch_grad(int D, int H, int N, const GradDev& g, cudaStream_t s, int* nb) {
+cudaError_t launch_grad(int D, int H, int N, const GradDev& g, cudaStream_t s, int* nb, int G = 0) {
+  if (G) return H == 32 ? launch_grad_t<3, 32, 1, 1>(g, s, nb) : launch_grad_t<3, 64, 1, 1>(g, s, nb);
   if (D == 4) return H == 32 ? launch_grad_dh<4, 32>(N, g, s, nb) : launch_grad_dh<4, 64>(N, g, s, nb);
   return H == 32 ? launch_grad_dh<6, 32>(N, g, s, nb) : launch_grad_dh<6, 64>(N, g, s, nb);
 }
@@ -524,9 +584,14 @@ int32_t ws_a2c_n_params(int32_t D, int32_t H, int32_t N) {
   return layout(D, H, N).P;
 }
 
+int32_t ws_a2c_n_params_ex(int32_t D, int32_t H, int32_t N, int32_t gaussian) {
+  if (D < 1 || H < 1 || N < 1) return 0;
+  return layout(D, H, N, gaussian ? 1 : 0).P;
+}
+
 size_t ws_a2c_workspace_bytes(int32_t D, int32_t H, int32_t N) {
-  if (!supported(D, H, N)) return 0;
-  const size_t g = (size_t)kMaxGrid * (layout(D, H, N).P + 3) * sizeof(double);
+  if (!supported(D, H, N) && !supported(D, H, N, 1)) return 0;
+  const size_t g = (size_t)kMaxGrid * (layout(D, H, N, 1).P + 3) * sizeof(double);
   const size_t m = (size_t)kMomBlocks * 2 * sizeof(double);
   return std::max(g, m);
 }
@@ -554,18 +619,19 @@ ws_status ws_a2c_moments(const float* x, int64_t n, double* out, void* workspace
 }
 
 ws_status ws_a2c_grad(const ws_a2c_args* a, void* stream) {
-  if (!a || !supported(a->obs_dim, a->hidden, a->n_actions) || a->rows < 1 || !a->params || !a->obs || !a->act ||
-      !a->adv || !a->ret || !a->moments || !(a->batch > 0.0) || !a->workspace || !a->grad)
+  if (!a || !supported(a->obs_dim, a->hidden, a->n_actions, a->gaussian ? 1 : 0) || a->rows < 1 || !a->params ||
+      !a->obs || !(a->gaussian ? a->act_f != nullptr : a->act != nullptr) || !a->adv || !a->ret || !a->moments ||
+      !(a->batch > 0.0) || !a->workspace || !a->grad)
     return WS_ERR_INVALID_ARGUMENT;
   if (a->logp_old && !(a->clip_eps >= 0.0f && a->clip_eps < 1.0f)) return WS_ERR_INVALID_ARGUMENT;
   GradDev g{a->params, a->obs, a->act, a->adv, a->ret, a->moments, a->batch, a->c_v, a->c_e, a->rows,
-            static_cast<double*>(a->workspace), a->logp_old, a->clip_eps,
+            static_cast<double*>(a->workspace), a->act_f, a->logp_old, a->clip_eps,
             a->norm_batch > 0.0 ? a->norm_batch : a->batch};
   cudaStream_t s = static_cast<cudaStream_t>(stream);
   int nb = 0;
-  cudaError_t e = launch_grad(a->obs_dim, a->hidden, a->n_actions, g, s, &nb);
+  cudaError_t e = launch_grad(a->obs_dim, a->hidden, a->n_actions, g, s, &nb, a->gaussian ? 1 : 0);
   if (e) return WS_ERR_CUDA;
-  const int P = layout(a->obs_dim, a->hidden, a->n_actions).P;
+  const int P = layout(a->obs_dim, a->hidden, a->n_actions, a->gaussian ? 1 : 0).P;
   k_grad_final<<<(P + 3 + 127) / 128, 128, 0, s>>>(g.partial, nb, P, a->grad, a->loss);
   return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
 }

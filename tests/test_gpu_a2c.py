@@ -344,3 +344,86 @@ def test_cartpole_solved_by_ppo(P):
     print(f"cartpole PPO solved: mean return {curve[-1][2]:.1f} after {curve[-1][1]:.3g} env steps, "
           f"{curve[-1][0]:.2f} s")
     assert curve[-1][2] >= 475.0
+
+
+def gauss_grad_scale(params, obs, act, Ah, ret, D, H, d, c_v, c_e, B):
+    W1, b1, W2, b2, ls, wv, bv = OA.unpack_gauss(params, D, H, d)
+    z, h, mu, _, V = OA.forward_gauss(params, obs, D, H, d)
+    o = np.abs(np.asarray(obs, np.float64).reshape(-1, D))
+    a = np.asarray(act, np.float64).reshape(-1, d)
+    iv = np.exp(-2 * ls)
+    dmu = (np.abs(Ah) / B)[:, None] * np.abs(a - mu) * iv
+    dls = ((np.abs(Ah) / B)[:, None] * ((a - mu) ** 2 * iv + 1)).sum(0) + c_e * len(a) / B
+    dV = 2 * c_v * np.abs(V - np.asarray(ret, np.float64)) / B
+    dz = (dmu @ np.abs(W2).T + dV[:, None] * np.abs(wv)[None, :]) * (z > 0)
+    return np.concatenate([(o.T @ dz).ravel(), dz.sum(0), (h.T @ dmu).ravel(), dmu.sum(0), dls, h.T @ dV,
+                           [dV.sum()]])
+
+
+@pytest.mark.parametrize("H,rows", [(64, 5000), (32, 777)])
+def test_gaussian_grad_matches_oracle(P, H, rows):
+    """Continuous actor-critic (R35): ws_a2c_grad with the Gaussian head against
+    oracle/a2c.py grad_gauss."""
+    D, d = 3, 1
+    r = np.random.default_rng(121)
+    params = (r.standard_normal(OA.n_params_gauss(D, H, d)) * 0.5).astype(np.float32)
+    obs = r.standard_normal((rows, D)).astype(np.float32)
+    act = (r.standard_normal((rows, d)) * 1.5).astype(np.float32)
+    adv = r.standard_normal(rows).astype(np.float32)
+    ret = (r.standard_normal(rows) * 5).astype(np.float32)
+    ws = P.workspace(D, H, d, "cuda")
+    tadv = cuda(adv)
+    mom = P.moments(tadv, ws)
+    g, L = P.a2c_grad(cuda(params), cuda(obs).view(-1), cuda(act).view(-1), tadv, cuda(ret), mom, float(rows),
+                      D, H, d, 0.5, 0.02, ws)
+    Ah = OA.normalize(adv)
+    ref = OA.grad_gauss(params, obs, act, Ah, ret, D, H, d, 0.5, 0.02)
+    scale = gauss_grad_scale(params, obs, act, Ah, ret, D, H, d, 0.5, 0.02, rows)
+    got = g.cpu().numpy().astype(np.float64)
+    bad = np.abs(got - ref) > 2e-5 * scale + 1e-12
+    assert not bad.any(), (np.flatnonzero(bad)[:10], got[bad][:5], ref[bad][:5])
+    Lref = OA.loss_gauss(params, obs, act, Ah, ret, D, H, d, 0.5, 0.02)
+    np.testing.assert_allclose(L.cpu().numpy(), Lref[1:], rtol=1e-4, atol=1e-5)
+
+
+def test_gaussian_training_iteration_matches_oracle(P):
+    """One A2C iteration on Pendulum: Gaussian policy roll-out with the fused critic, GAE,
+    gradient -- the store equals the oracle's Gaussian policy roll-out and the gradient the
+    oracle's on that store."""
+    import paper_2408_00930_b200 as WS
+    D, d, H, E, T = 3, 1, 32, 256, 100
+    r = np.random.default_rng(131)
+    params = (r.standard_normal(OA.n_params_gauss(D, H, d)) * 0.4).astype(np.float32)
+    params[D * H + H + H * d + d] = -0.5  # log_std
+    g = WS.Env(E, 1, "pendulum", SEED, t_capacity=T)
+    tr = P.A2C(g, H, params=torch.from_numpy(params), lr=1e-3)
+    assert tr.gaussian
+    tr.iteration(T)
+    g.synchronize()
+    o = O.Batch("pendulum", E, 1, SEED, t_capacity=T)
+    assert o.rollout_policy_gauss(T, params[:D * H + H + H * d + 2 * d], H, n_threads=8) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done"):
+        assert np.array_equal(buf[k][:T], o.array(k)[:T]), k
+    obs = o.array("obs")[:T].reshape(-1, D)
+    act = o.array("act")[:T].reshape(-1, d)
+    vals = OA.forward_gauss(params, obs, D, H, d)[4].reshape(T, E)
+    boot = OA.forward_gauss(params, o.array("obs_live").reshape(-1, D), D, H, d)[4]
+    adv, ret = O.gae(o.array("rew")[:T].reshape(T, E), o.array("done")[:T], vals, boot, 0.99, 0.95, f64=True)
+    Ah = OA.normalize(adv)
+    ref = OA.grad_gauss(params, obs, act, Ah, ret.ravel(), D, H, d, 0.5, 0.01)
+    scale = gauss_grad_scale(params, obs, act, Ah, ret.ravel(), D, H, d, 0.5, 0.01, T * E)
+    got = tr.grad.cpu().numpy().astype(np.float64)
+    bad = np.abs(got - ref) > 1e-4 * scale + 1e-10
+    assert not bad.any(), (np.flatnonzero(bad)[:10], got[bad][:5], ref[bad][:5])
+
+
+def test_pendulum_learns_with_gaussian_a2c(P):
+    """Continuous control ("both discrete and continuous actions"): the Gaussian
+    actor-critic on 10K Pendulum replicas lifts the mean episodic return from the random
+    policy's ~ -1100 to above -600 within 600 iterations of 64 steps."""
+    from paper_2408_00930_b200.train import train
+    curve = train("pendulum", 10000, 64, 600, lr=1e-3, c_e=0.0, log_every=50)
+    first, best = curve[0][2], max(c[2] for c in curve)
+    print(f"pendulum A2C: mean return {first:.1f} -> best {best:.1f}")
+    assert first < -900.0 and best > -600.0
