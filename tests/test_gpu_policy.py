@@ -136,3 +136,34 @@ def test_gaussian_policy_rollout_parity(P, H, E, T):
     h = np.maximum(obs @ W1 + b1, 0.0)
     ref = h @ head[:H].astype(np.float64) + head[H]
     assert np.all(np.abs(vals.cpu().numpy() - ref) <= 1e-5 * (3.0 + h @ np.abs(head[:H])))
+
+
+def test_torch_policy_rollout(P):
+    """paper_2408_00930_b200.policy.rollout_with: (1) a torch policy returning fixed rows
+    reproduces the fused ws_rollout on those rows bit for bit (single-step sample + step ==
+    fused roll-out, R28); (2) an observation-dependent torch network drives the roll-out:
+    every logged log-prob is the log of the policy's probability of the logged action at the
+    logged (pre-step) observation."""
+    from paper_2408_00930_b200.policy import rollout_with
+    E, T = 300, 64
+    probs = torch.from_numpy(W.random_probs(E, 1, 3, seed=141, zero_frac=0.2)).cuda()
+    a = P.Env(E, 1, "acrobot", SEED, t_capacity=T)
+    rollout_with(a, lambda obs: probs, T)
+    b = P.Env(E, 1, "acrobot", SEED, t_capacity=T)
+    b.rollout(T, probs)
+    A = {k: v.cpu().numpy() for k, v in a.buffers().items() if v is not None}
+    B = {k: v.cpu().numpy() for k, v in b.buffers().items() if v is not None}
+    for k in ("obs", "act", "logp", "rew", "done", "state", "obs_live", "reset_count", "stats"):
+        assert np.array_equal(A[k], B[k], equal_nan=True), k
+    torch.manual_seed(0)
+    net = torch.nn.Sequential(torch.nn.Linear(4, 32), torch.nn.Tanh(), torch.nn.Linear(32, 2)).cuda()
+    pol = lambda obs: torch.softmax(net(obs), dim=-1)  # noqa: E731
+    c = P.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    with torch.no_grad():
+        rollout_with(c, pol, T)
+        C_ = c.buffers()
+        p_all = pol(C_["obs"][:T])                       # [T, E, 1, 2] at the logged observations
+        act = C_["act"][:T].long()
+        lp_ref = torch.log(torch.gather(p_all, -1, act.unsqueeze(-1)).squeeze(-1))
+    assert torch.allclose(C_["logp"][:T], lp_ref, atol=1e-5)
+    assert 0.05 < (act == 0).float().mean().item() < 0.95
