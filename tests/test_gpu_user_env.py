@@ -154,3 +154,22 @@ def test_registered_env_trains(P):
     print(f"u_cartpole solved: mean return {curve[-1][2]:.1f} after {curve[-1][1]:.3g} env steps, "
           f"{curve[-1][0]:.2f} s")
     assert curve[-1][2] >= 475.0
+
+
+def test_noisy_pes_env_matches_oracle(P):
+    """u_mbgrid: a discrete walker on a noisy Mueller-Brown PES (fp32 terms with ws_exp, a
+    shared 32 x 32 noise grid, per-replica step sizes) -- GPU store vs the oracle."""
+    E, T = 1000, 200
+    prm, grid = U.mbgrid_data(E)
+    probs = W.random_probs(E, 1, 5, seed=151)
+    g = P.Env(E, 1, "u_mbgrid", SEED, t_capacity=T, env_prm=torch.from_numpy(prm).cuda(),
+              env_shared=torch.from_numpy(grid).cuda())
+    g.rollout(T, torch.from_numpy(probs).cuda())
+    assert g.status() == 0
+    o = O.Batch("u_mbgrid", E, 1, SEED, t_capacity=T, env_prm=prm, env_shared=grid)
+    assert o.rollout(T, probs) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    same(buf, o, T)
+    st_g, st_o = g.stats_f64(T).cpu().numpy(), np.array(o.array("stats"))[:T]
+    assert np.array_equal(st_g[:, [0, 2]], st_o[:, [0, 2]])
+    np.testing.assert_allclose(st_g[:, [1, 3]], st_o[:, [1, 3]], rtol=1e-12, atol=E * 2.0 ** -32)

@@ -76,3 +76,31 @@ def test_pointmass_parameters_and_shared_map():
     assert o2.rollout(T, W.random_probs(E, 1, 3, seed=6)) == 0
     assert np.array_equal(o.array("act")[:1], o2.array("act")[:1])
     assert not np.array_equal(o.array("obs")[2:, :, :, :2], o2.array("obs")[2:, :, :, :2])
+
+
+def test_noisy_mueller_brown_surface():
+    """u_mbgrid (noisy PES): with a zero noise grid the observed energy is the Mueller-Brown
+    energy of the pinned oracle function (fp32 terms, within fp32 rounding), the start lies
+    near minimum B (E ~ -108, tests/golden/mueller_brown_stationary.txt); with noise the
+    energy moves by exactly the grid cell's value; steps move by the replica's step size."""
+    E, T = 64, 60
+    prm, grid0 = U.mbgrid_data(E, noise=0.0)
+    o = O.Batch("u_mbgrid", E, 1, SEED, t_capacity=T, env_prm=prm, env_shared=grid0)
+    assert o.rollout(T, W.random_probs(E, 1, 5, seed=9)) == 0
+    obs = o.array("obs")[:T, :, 0]
+    ref = np.array([[O.mb_energy(float(x), float(y))[0] for x, y in row[:, :2]] for row in obs])
+    np.testing.assert_allclose(obs[..., 2], ref, rtol=2e-5, atol=2e-4)
+    assert np.all(np.abs(obs[0, :, 2] + 108.17) < 6.0)  # near minimum B at the start
+    step = np.abs(np.diff(obs[:, :, :2], axis=0)).sum(-1)
+    nxt = obs[1:, :, :2]
+    inside = (nxt[..., 0] > -1.5) & (nxt[..., 0] < 1.2) & (nxt[..., 1] > -0.5) & (nxt[..., 1] < 2.0)
+    moved = (step > 0) & (o.array("done")[:T - 1] == 0) & inside  # box clipping excluded
+    np.testing.assert_allclose(step[moved], np.broadcast_to(prm[:, 0], step.shape)[moved], rtol=1e-5, atol=1e-6)
+    _, grid = U.mbgrid_data(E)
+    o2 = O.Batch("u_mbgrid", E, 1, SEED, t_capacity=T, env_prm=prm, env_shared=grid)
+    assert o2.rollout(T, W.random_probs(E, 1, 5, seed=9)) == 0
+    x, y = o2.array("obs")[0, :, 0, 0], o2.array("obs")[0, :, 0, 1]
+    ix = np.clip(np.floor((x + np.float32(1.5)) * np.float32(32 / 2.7)).astype(int), 0, 31)
+    iy = np.clip(np.floor((y + np.float32(0.5)) * np.float32(32 / 2.5)).astype(int), 0, 31)
+    np.testing.assert_allclose(o2.array("obs")[0, :, 0, 2] - o.array("obs")[0, :, 0, 2], grid[iy * 32 + ix],
+                               rtol=1e-5, atol=1e-4)

@@ -11,6 +11,11 @@ implemented separately on each side.
 * POINTMASS_SRC  a damped point mass with per-replica parameters (prm[0] force gain, prm[1]
                  damping: parameter jitter) and a shared read-only reward map of 64 cells over
                  [-1, 1] (a grid in global memory, Fig 1).
+* MBGRID_SRC     a discrete walker on a NOISY Mueller-Brown potential-energy surface (the
+                 catalysis-style PES of the paper's reaction env, SURVEY 8(f) N4 "noisy PES"):
+                 the MB energy (fp32 terms, exponentials via ws_exp) plus a shared 32 x 32 noise
+                 grid over the box; per-replica step size prm[0]; start near minimum B, goal =
+                 within 0.1 of minimum A; reward -0.01 dE - 0.1.
 """
 
 CARTPOLE = dict(state_dim=4, obs_dim=4, n_actions=2, n_reset_draws=4, max_steps=500, n_params=0)
@@ -97,5 +102,59 @@ def pointmass_data(E: int, seed: int = 0x24080930):
     return prm, grid
 
 
+MBGRID = dict(state_dim=2, obs_dim=3, n_actions=5, n_reset_draws=2, max_steps=200, n_params=1)
+MBGRID_SRC = r"""
+WS_FN float mb_energy(float x, float y, const float *shared) {
+  const float A[4] = {-200.0f, -100.0f, -170.0f, 15.0f};
+  const float a[4] = {-1.0f, -1.0f, -6.5f, 0.7f};
+  const float b[4] = {0.0f, 0.0f, 11.0f, 0.6f};
+  const float c[4] = {-10.0f, -10.0f, -6.5f, 0.7f};
+  const float x0[4] = {1.0f, 0.0f, -0.5f, -1.0f};
+  const float y0[4] = {0.0f, 0.5f, 1.5f, 1.0f};
+  float E = 0.0f;
+  for (int k = 0; k < 4; ++k) {
+    const float dx = x - x0[k], dy = y - y0[k];
+    E = E + A[k] * ws_exp(a[k] * dx * dx + b[k] * dx * dy + c[k] * dy * dy);
+  }
+  int ix = (int)ws_floor((x + 1.5f) * (32.0f / 2.7f));
+  int iy = (int)ws_floor((y + 0.5f) * (32.0f / 2.5f));
+  ix = ix < 0 ? 0 : (ix > 31 ? 31 : ix);
+  iy = iy < 0 ? 0 : (iy > 31 ? 31 : iy);
+  return E + shared[iy * 32 + ix];
+}
+WS_FN void ws_env_init(float *s, const float *u, const float *prm, const float *shared) {
+  s[0] = 0.623f + 0.1f * (u[0] - 0.5f);
+  s[1] = 0.028f + 0.1f * (u[1] - 0.5f);
+}
+WS_FN void ws_env_obs(const float *s, float *o, const float *prm, const float *shared) {
+  o[0] = s[0];
+  o[1] = s[1];
+  o[2] = mb_energy(s[0], s[1], shared);
+}
+WS_FN int ws_env_step(float *s, int a, float *r, const float *prm, const float *shared) {
+  const float e0 = mb_energy(s[0], s[1], shared);
+  const float h = prm[0];
+  float x = s[0] + (a == 1 ? h : (a == 2 ? -h : 0.0f));
+  float y = s[1] + (a == 3 ? h : (a == 4 ? -h : 0.0f));
+  x = ws_clip(x, -1.5f, 1.2f);
+  y = ws_clip(y, -0.5f, 2.0f);
+  s[0] = x;
+  s[1] = y;
+  *r = -0.01f * (mb_energy(x, y, shared) - e0) - 0.1f;
+  return (ws_abs(x + 0.558f) < 0.1f && ws_abs(y - 1.442f) < 0.1f) ? 1 : 0;
+}
+"""
+
+
+def mbgrid_data(E: int, seed: int = 0x24080930, noise: float = 5.0):
+    """Per-replica step sizes U(0.02, 0.06) (jitter) and the shared 32 x 32 noise grid
+    N(0, noise^2) (0 = the clean surface), float32."""
+    import numpy as np
+    rng = np.random.default_rng(seed + 11)
+    prm = rng.uniform(0.02, 0.06, (E, 1)).astype(np.float32)
+    grid = (noise * rng.standard_normal(32 * 32)).astype(np.float32)
+    return prm, grid
+
+
 ENVS = {"u_cartpole": (CARTPOLE_SRC, CARTPOLE), "u_mountaincar": (MOUNTAINCAR_SRC, MOUNTAINCAR),
-        "u_pointmass": (POINTMASS_SRC, POINTMASS)}
+        "u_pointmass": (POINTMASS_SRC, POINTMASS), "u_mbgrid": (MBGRID_SRC, MBGRID)}
