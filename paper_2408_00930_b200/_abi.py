@@ -126,7 +126,8 @@ _SIGS = {
     "ws_abi_version": (C.c_int32, []),
     "ws_enable_kernel_timing": (C.c_int, [C.c_void_p, C.c_int32]),
     "ws_rollout_policy": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32]),
-    "ws_rollout_actor_critic": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ws_rollout_actor_critic": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p,
+                                          C.c_void_p]),
     "ws_gae": (C.c_int, [C.POINTER(ws_gae_args), C.c_void_p]),
     "ws_gae_store": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p, C.c_void_p, C.c_float, C.c_float,
                                C.c_void_p, C.c_void_p]),

@@ -133,7 +133,7 @@ class A2C:
     def __init__(self, env: Env, hidden: int = 64, *, lr: float = 1e-3, gamma: float = 0.99, lam: float = 0.95,
                  c_v: float = 0.5, c_e: float = 0.01, max_norm: float = 0.5, beta1: float = 0.9,
                  beta2: float = 0.999, eps: float = 1e-8, seed: int = 0, params: Optional[torch.Tensor] = None,
-                 group: Optional[dist.ProcessGroup] = None):
+                 group: Optional[dist.ProcessGroup] = None, bootstrap_truncation: bool = True):
         info = env.info()
         self.gaussian = int(info.n_actions) == 0  # continuous actions: Gaussian head (R34 / R35)
         if int(info.n_agents) != 1:
@@ -163,6 +163,11 @@ class A2C:
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.step = 0
         self._values = None
+        # truncated episodes bootstrap from V(post-step state) written by the roll-out kernel
+        # (GAE's v_trunc, R30); registered envs treat truncation as termination (R31)
+        self.bootstrap_truncation = bootstrap_truncation and env.env in ("cartpole", "acrobot", "dummy",
+                                                                         "pendulum")
+        self._vtrunc = None
 
     def _allreduce(self, t: torch.Tensor):
         if self.world > 1:
@@ -171,6 +176,7 @@ class A2C:
     def _value_buf(self, rows: int) -> torch.Tensor:
         if self._values is None or self._values.numel() != rows:
             self._values = torch.empty(rows, dtype=torch.float32, device=self.env.device)
+            self._vtrunc = torch.zeros(rows, dtype=torch.float32, device=self.env.device)
         return self._values
 
     def _advantages(self, T: int, values_ready: bool):
@@ -188,8 +194,9 @@ class A2C:
                 raise WSError(_abi.INVALID_ARGUMENT, "Gaussian A2C: the critic comes from the roll-out kernel")
             ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
             ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
+        vtr = self._vtrunc.view(T, self.E, 1) if (values_ready and self.bootstrap_truncation) else None
         adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
-                                 hp["gamma"], hp["lam"])
+                                 hp["gamma"], hp["lam"], v_trunc=vtr)
         moments(adv.view(-1), self.ws, out=self.mom, stream=s)
         self._allreduce(self.mom)
         self._adv = adv  # alive until the stream consumed it
@@ -217,7 +224,8 @@ class A2C:
         """Roll out T steps with the current policy (the kernel also writes the critic's values
         from the hidden layer it already computes), then update (train)."""
         vals = self._value_buf(T * self.E)
-        self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap)
+        self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap,
+                                      self._vtrunc if self.bootstrap_truncation else None)
         self.update(T, values_ready=True)
 
 

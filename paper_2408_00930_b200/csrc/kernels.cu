@@ -730,7 +730,8 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
 template <class Env, int H, bool kCritic>
 __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int T, const uint64_t t0,
                                                        const float* __restrict__ weights,
-                                                       float* __restrict__ values, float* __restrict__ bootstrap) {
+                                                       float* __restrict__ values, float* __restrict__ bootstrap,
+                                                       float* __restrict__ values_trunc) {
   using L = Lane<Env>;
   using St = typename L::St;
   constexpr int D = L::D, N = L::N;
@@ -852,6 +853,19 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
       aux = aux2;
       ep_step = es;
       ep_ret = ret;
+    }
+    if (kCritic && values_trunc && d == 2u) {  // truncated only: V of the post-step state
+      float o2[D];
+      L::obs_vals(s, aux, o2);
+      float v = wv[H];
+#pragma unroll
+      for (int j = 0; j < H; ++j) {
+        float acc = b1[j];
+#pragma unroll
+        for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o2[k], acc);
+        v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
+      }
+      if (live) st_cs(values_trunc + idx, v);
     }
     if (d) {  // auto-reset (R11)
       rc += 1;
@@ -1062,7 +1076,8 @@ __global__ void __launch_bounds__(256) k_rollout_continuous(const KArgs a, const
 template <int H, bool kCritic>
 __global__ void __launch_bounds__(128) k_rollout_gpolicy(const KArgs a, const int T, const uint64_t t0,
                                                         const float* __restrict__ weights,
-                                                        float* __restrict__ values, float* __restrict__ bootstrap) {
+                                                        float* __restrict__ values, float* __restrict__ bootstrap,
+                                                        float* __restrict__ values_trunc) {
   using L = Lane<Pendulum>;
   using St = Pendulum::St;
   constexpr int D = 3;
@@ -1136,6 +1151,14 @@ __global__ void __launch_bounds__(128) k_rollout_gpolicy(const KArgs a, const in
     const uint32_t d = ok ? (es >= a.max_steps ? 2u : 0u) : 0u;
     const float ret = ep_ret + r;
     const float rw = ok ? r : 0.0f;
+    if (kCritic && values_trunc && d == 2u) {  // truncated only: V of the post-step state
+      float sn2, cs2;
+      sincos_c(s2.th, sn2, cs2);
+      const float o2[3] = {cs2, sn2, s2.thd};
+      float m_unused, vt;
+      head(o2, m_unused, vt);
+      if (live) st_cs(values_trunc + idx, vt);
+    }
     if (d) L::init(key, eg, rc + 1, s2);
     s = ok ? s2 : s;
     rc += d ? 1u : 0u;
@@ -2141,21 +2164,21 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                  int hidden, float* values, float* bootstrap) {
+                                  int hidden, float* values, float* bootstrap, float* vtr) {
   const int b = l.block < 128 ? l.block : 128;                              // launch bounds 128
   const size_t smem = (size_t)(b / 32) * 3 * 16 * kWinStride * sizeof(uint32_t);  // per-warp 16-row windows
   const unsigned g = grid_for(a.E, b);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
-      case 64: k_rollout_policy<Env, 64, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 32: k_rollout_policy<Env, 32, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 64: k_rollout_policy<Env, 64, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
-      case 64: k_rollout_policy<Env, 64, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 32: k_rollout_policy<Env, 32, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 64: k_rollout_policy<Env, 64, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
       default: return cudaErrorInvalidValue;
     }
   }
@@ -2164,20 +2187,20 @@ static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64
 }
 
 static cudaError_t rollout_gpolicy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                   int hidden, float* values, float* bootstrap) {
+                                   int hidden, float* values, float* bootstrap, float* vtr) {
   const size_t smem = (size_t)4 * 3 * kContWinRows * kWinStride * sizeof(uint32_t);  // 4 warps' windows
   const unsigned g = grid_for(a.E, 128);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {
-      case 32: k_rollout_gpolicy<32, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
-      case 64: k_rollout_gpolicy<64, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap); break;
+      case 32: k_rollout_gpolicy<32, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 64: k_rollout_gpolicy<64, true><<<g, 128, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
     switch (hidden) {
-      case 32: k_rollout_gpolicy<32, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
-      case 64: k_rollout_gpolicy<64, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr); break;
+      case 32: k_rollout_gpolicy<32, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 64: k_rollout_gpolicy<64, false><<<g, 128, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
       default: return cudaErrorInvalidValue;
     }
   }
@@ -2186,13 +2209,13 @@ static cudaError_t rollout_gpolicy(const KArgs& a, const Launch& l, int T, uint6
 }
 
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
-                                  int hidden, uint64_t* launches, float* values, float* bootstrap) {
+                                  int hidden, uint64_t* launches, float* values, float* bootstrap, float* vtr) {
   cudaError_t err = cudaErrorInvalidValue;
   switch (l.kind) {
-    case kPendulum: err = rollout_gpolicy(a, l, T, t0, weights, hidden, values, bootstrap); break;
-    case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden, values, bootstrap); break;
-    case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden, values, bootstrap); break;
-    case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden, values, bootstrap); break;
+    case kPendulum: err = rollout_gpolicy(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
+    case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
+    case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
+    case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
     default: break;
   }
   *launches += 1;

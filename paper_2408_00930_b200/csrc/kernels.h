@@ -69,7 +69,7 @@ cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_
 // the critic's values [T, E] and bootstrap [E] (NEXT-N2)
 cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, uint64_t* launches, float* values = nullptr,
-                                  float* bootstrap = nullptr);
+                                  float* bootstrap = nullptr, float* values_trunc = nullptr);
 
 // NEXT-N2: generalised advantage estimation over the time-major store (gae.cu, R30)
 struct GaeArgs {

@@ -515,7 +515,7 @@ static void sum_stats(const long long* st, int n, ws_stats* out) {
 }
 
 static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t hidden, float* values,
-                            float* bootstrap) {
+                            float* bootstrap, float* values_trunc = nullptr) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
@@ -533,7 +533,8 @@ static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t 
     if (h->timing) mark_kernel(h, ws::kKRollout, 1);
     h->launches += 1;
   } else if (!e) {
-    e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches, values, bootstrap);
+    e = ws::launch_rollout_policy(kargs(h), launch_of(h), T, h->t, weights, hidden, &h->launches, values, bootstrap,
+                                  values_trunc);
   }
   if (e) return cuda_fail(h, e, "policy roll-out kernel");
   h->t += (uint64_t)T;
@@ -547,10 +548,12 @@ ws_status ws_rollout_policy(ws_env* h, int32_t T, const float* weights, int32_t 
 }
 
 ws_status ws_rollout_actor_critic(ws_env* h, int32_t T, const float* params, int32_t hidden, float* values,
-                                  float* bootstrap) {
+                                  float* bootstrap, float* values_trunc) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (!values || !bootstrap) return fail(h, WS_ERR_INVALID_ARGUMENT, "values and bootstrap are required");
-  return run_policy(h, T, params, hidden, values, bootstrap);
+  if (values_trunc && h->spec.kind == ws::kUser)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "values_trunc: built-in envs only");
+  return run_policy(h, T, params, hidden, values, bootstrap, values_trunc);
 }
 
 static ws_status run_gae(ws_env* h, const ws_gae_args* a, cudaStream_t s, const ws::Launch* l) {

@@ -235,7 +235,7 @@ class Env:
         self._keep = w  # alive until the stream has consumed it
 
     def rollout_actor_critic(self, T: int, params: torch.Tensor, hidden: int, values: torch.Tensor,
-                             bootstrap: torch.Tensor) -> None:
+                             bootstrap: torch.Tensor, values_trunc: Optional[torch.Tensor] = None) -> None:
         """NEXT-N2: the policy roll-out that also writes the critic's values [T, E] and the
         bootstrap values [E] (ws.h ws_rollout_actor_critic); params: R31 packed float32."""
         w = params.contiguous()
@@ -244,8 +244,11 @@ class Env:
                 raise WSError(_abi.INVALID_ARGUMENT, f"{name}: contiguous float32 on the handle's device")
         if values.numel() < T * self.n_envs or bootstrap.numel() < self.n_envs:
             raise WSError(_abi.INVALID_ARGUMENT, "values [T, E] / bootstrap [E]")
+        if values_trunc is not None and (values_trunc.dtype != torch.float32 or values_trunc.device != self.device
+                                         or values_trunc.numel() < T * self.n_envs):
+            raise WSError(_abi.INVALID_ARGUMENT, "values_trunc: float32 [T, E] on the handle's device")
         check(lib().ws_rollout_actor_critic(self._h, T, w.data_ptr(), hidden, values.data_ptr(),
-                                            bootstrap.data_ptr()), self._h)
+                                            bootstrap.data_ptr(), _ptr(values_trunc)), self._h)
         self._keep = w
 
     def gae_store(self, T: int, values: torch.Tensor, bootstrap: torch.Tensor, gamma: float, lam: float,

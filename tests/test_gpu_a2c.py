@@ -427,3 +427,42 @@ def test_pendulum_learns_with_gaussian_a2c(P):
     first, best = curve[0][2], max(c[2] for c in curve)
     print(f"pendulum A2C: mean return {first:.1f} -> best {best:.1f}")
     assert first < -900.0 and best > -600.0
+
+
+def test_truncation_bootstraps_from_post_step_value(P):
+    """S:185 "truncation ... flagged so the trainer bootstraps": with max_steps = 20 the
+    critic roll-out writes V(post-step state) at every truncated slot (the oracle recomputes
+    the post-step state with its pinned cartpole_step from the logged pre-step observation --
+    CartPole observes its state), and the A2C gradient uses it through GAE's v_trunc."""
+    import paper_2408_00930_b200 as WS
+    D, N, H, E, T = 4, 2, 64, 300, 60
+    params = W.a2c_params(D, H, N, seed=161)
+    g = WS.Env(E, 1, "cartpole", SEED, t_capacity=T, max_steps=20)
+    tr = P.A2C(g, H, params=torch.from_numpy(params), lr=1e-3)
+    tr.iteration(T)
+    g.synchronize()
+    o = O.Batch("cartpole", E, 1, SEED, t_capacity=T, max_steps=20)
+    assert o.rollout_policy(T, params[:D * H + H + H * N + N], H, n_threads=8) == 0
+    done = o.array("done")[:T]
+    assert np.array_equal(g.buffers()["done"].cpu().numpy()[:T], done)
+    obs, act = o.array("obs")[:T], o.array("act")[:T]
+    trunc = np.argwhere(done == 2)
+    assert len(trunc) > 100
+    post = np.stack([O.cartpole_step(obs[t, e, 0], int(act[t, e, 0]))[1] for t, e in trunc])
+    v_ref = OA.values(params, post, D, H, N)
+    v_gpu = tr._vtrunc.view(T, E).cpu().numpy()[trunc[:, 0], trunc[:, 1]]
+    h = OA.forward(params, post, D, H, N)[1]
+    wv = OA.unpack(params, D, H, N)[4]
+    assert np.all(np.abs(v_gpu - v_ref) <= 1e-5 * (10.0 + h @ np.abs(wv)))
+    # gradient with GAE bootstrapping from those terminal values
+    vt = np.zeros((T, E))
+    vt[trunc[:, 0], trunc[:, 1]] = v_ref
+    flat = obs.reshape(-1, D)
+    vals = OA.values(params, flat, D, H, N).reshape(T, E)
+    boot = OA.values(params, o.array("obs_live").reshape(-1, D), D, H, N)
+    adv, ret = O.gae(o.array("rew")[:T].reshape(T, E), done, vals, boot, 0.99, 0.95, v_trunc=vt, f64=True)
+    Ah = OA.normalize(adv)
+    ref = OA.grad(params, flat, act.reshape(-1), Ah, ret.ravel(), D, H, N, 0.5, 0.01)
+    scale = grad_scale(params, flat, act.reshape(-1), Ah, ret.ravel(), D, H, N, 0.5, 0.01, T * E)
+    got = tr.grad.cpu().numpy().astype(np.float64)
+    assert not (np.abs(got - ref) > 1e-4 * scale + 1e-10).any()
