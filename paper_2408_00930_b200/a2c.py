@@ -136,10 +136,11 @@ class A2C:
                  group: Optional[dist.ProcessGroup] = None, bootstrap_truncation: bool = True):
         info = env.info()
         self.gaussian = int(info.n_actions) == 0  # continuous actions: Gaussian head (R34 / R35)
-        if int(info.n_agents) != 1:
-            raise WSError(_abi.INVALID_ARGUMENT, "A2C: single-agent envs")
+        self.A = int(info.n_agents)  # multi-agent (tag): every agent is a row; rolled out by a torch policy
+        if self.A != 1 and int(info.n_actions) < 1:
+            raise WSError(_abi.INVALID_ARGUMENT, "A2C: multi-agent envs need discrete actions")
         self.env, self.H = env, hidden
-        self.D, self.E = int(info.obs_dim), int(info.n_envs)
+        self.D, self.E = int(info.obs_dim), int(info.n_envs) * self.A  # E counts agent columns (E * A)
         self.N = int(info.act_dim) if self.gaussian else int(info.n_actions)
         self.P = n_params(self.D, hidden, self.N, self.gaussian)
         if self.P == 0 or int(lib().ws_a2c_workspace_bytes(self.D, hidden, self.N)) == 0:
@@ -195,8 +196,10 @@ class A2C:
             ac_values(self.params, obs, D, H, N, out=self._values, stream=s)
             ac_values(self.params, buf["obs_live"].reshape(-1), D, H, N, out=self.bootstrap, stream=s)
         vtr = self._vtrunc.view(T, self.E, 1) if (values_ready and self.bootstrap_truncation) else None
-        adv, ret = env.gae_store(T, self._values.view(T, self.E, 1), self.bootstrap.view(self.E, 1),
-                                 hp["gamma"], hp["lam"], v_trunc=vtr)
+        if vtr is not None:
+            vtr = vtr.view(T, self.E // self.A, self.A)
+        adv, ret = env.gae_store(T, self._values.view(T, self.E // self.A, self.A),
+                                 self.bootstrap.view(self.E // self.A, self.A), hp["gamma"], hp["lam"], v_trunc=vtr)
         moments(adv.view(-1), self.ws, out=self.mom, stream=s)
         self._allreduce(self.mom)
         self._adv = adv  # alive until the stream consumed it
@@ -220,13 +223,34 @@ class A2C:
             obs, act, adv, ret, rows = self._advantages(T, values_ready)
             self._step(obs, act, adv, ret, rows, rows)
 
+    def torch_policy(self):
+        """The R29 policy of self.params as a torch function (for the single-step roll-out of
+        multi-agent envs, which have no fused policy kernel): probs = softmax(relu(o W1 + b1) W2 + b2)."""
+        D, H, N = self.D, self.H, self.N
+
+        def pol(obs):
+            p = self.params
+            W1 = p[:D * H].view(D, H)
+            b1 = p[D * H:D * H + H]
+            W2 = p[D * H + H:D * H + H + H * N].view(H, N)
+            b2 = p[D * H + H + H * N:D * H + H + H * N + N]
+            return torch.softmax(torch.relu(obs @ W1 + b1) @ W2 + b2, dim=-1)
+        return pol
+
     def iteration(self, T: int):
-        """Roll out T steps with the current policy (the kernel also writes the critic's values
-        from the hidden layer it already computes), then update (train)."""
+        """Roll out T steps with the current policy (single-agent: the kernel also writes the
+        critic's values from the hidden layer it already computes; multi-agent: the torch policy
+        through ws_sample / ws_step), then update (train)."""
         vals = self._value_buf(T * self.E)
-        self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap,
-                                      self._vtrunc if self.bootstrap_truncation else None)
-        self.update(T, values_ready=True)
+        if self.A == 1:
+            self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap,
+                                          self._vtrunc if self.bootstrap_truncation else None)
+            self.update(T, values_ready=True)
+        else:
+            from .policy import rollout_with
+            with torch.no_grad():
+                rollout_with(self.env, self.torch_policy(), T)
+            self.update(T, values_ready=False)
 
 
 class PPO(A2C):

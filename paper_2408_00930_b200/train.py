@@ -27,12 +27,13 @@ from .parallel import shard
 def train(env_name: str = "cartpole", n_envs: int = 10000, T: int = 32, iters: int = 1000, hidden: int = 64,
           lr: float = 3e-3, gamma: float = 0.99, lam: float = 0.95, c_v: float = 0.5, c_e: float = 0.01,
           max_norm: float = 0.5, seed: int = 0x24080930, target: float | None = None, log_every: int = 10,
-          out=None, algo: str = "a2c", epochs: int = 4, minibatches: int = 4, clip_eps: float = 0.2) -> list[tuple]:
+          out=None, algo: str = "a2c", epochs: int = 4, minibatches: int = 4, clip_eps: float = 0.2,
+          n_agents: int = 1) -> list[tuple]:
     """Returns the learning curve [(seconds, env_steps, mean_return, mean_length)]."""
     world = dist.get_world_size() if dist.is_available() and dist.is_initialized() else 1
     rank = dist.get_rank() if world > 1 else 0
     off, n = shard(n_envs, world, rank)
-    env = Env(n, 1, env_name, seed, env_offset=off, n_envs_global=n_envs, t_capacity=T)
+    env = Env(n, n_agents, env_name, seed, env_offset=off, n_envs_global=n_envs, t_capacity=T)
     kw = dict(lr=lr, gamma=gamma, lam=lam, c_v=c_v, c_e=c_e, max_norm=max_norm, seed=seed & 0xFFFF)
     if algo == "ppo":
         tr = PPO(env, hidden, epochs=epochs, minibatches=minibatches, clip_eps=clip_eps, **kw)
@@ -86,6 +87,7 @@ def main(argv=None):
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--minibatches", type=int, default=4)
     ap.add_argument("--clip", type=float, default=0.2)
+    ap.add_argument("--agents", type=int, default=1)
     a = ap.parse_args(argv)
     if "WORLD_SIZE" in os.environ and int(os.environ["WORLD_SIZE"]) > 1:
         local = int(os.environ.get("LOCAL_RANK", 0))
@@ -94,7 +96,7 @@ def main(argv=None):
     out = sys.stdout if a.csv == "-" else open(a.csv, "w", newline="")
     train(a.env, a.envs, a.T, a.iters, a.hidden, a.lr, a.gamma, a.lam, c_e=a.entropy, target=a.target,
           log_every=a.log_every, seed=a.seed, out=out, algo=a.algo, epochs=a.epochs, minibatches=a.minibatches,
-          clip_eps=a.clip)
+          clip_eps=a.clip, n_agents=a.agents)
     if out is not sys.stdout:
         out.close()
     if dist.is_initialized():

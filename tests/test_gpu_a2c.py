@@ -466,3 +466,35 @@ def test_truncation_bootstraps_from_post_step_value(P):
     scale = grad_scale(params, flat, act.reshape(-1), Ah, ret.ravel(), D, H, N, 0.5, 0.01, T * E)
     got = tr.grad.cpu().numpy().astype(np.float64)
     assert not (np.abs(got - ref) > 1e-4 * scale + 1e-10).any()
+
+
+def test_multi_agent_a2c_iteration_matches_oracle(P):
+    """Multi-agent A2C on tag (P:71 agents on threads; every agent is a row): a policy with a
+    zero output layer is exactly uniform in both torch and R29, so the single-step roll-out
+    equals the oracle's uniform-probability tag roll-out bit for bit; the critic, the GAE over
+    [T, E, A] with the per-replica done flag (R26) and the gradient then agree with the oracle."""
+    import paper_2408_00930_b200 as WS
+    D, N, H, E, A, T = 4, 5, 32, 6, 100, 40
+    params = W.a2c_params(D, H, N, seed=171)
+    params[D * H + H:D * H + H + H * N + N] = 0.0  # W2, b2 = 0: uniform policy
+    g = WS.Env(E, A, "tag", SEED, t_capacity=T)
+    tr = P.A2C(g, H, params=torch.from_numpy(params), lr=1e-3)
+    assert tr.A == A
+    tr.iteration(T)
+    g.synchronize()
+    o = O.Batch("tag", E, A, SEED, t_capacity=T)
+    assert o.rollout(T, np.full((E, A, N), 0.2, np.float32)) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done"):
+        assert np.array_equal(buf[k][:T], o.array(k)[:T]), k
+    obs = o.array("obs")[:T].reshape(-1, D)
+    act = o.array("act")[:T].reshape(-1)
+    vals = OA.values(params, obs, D, H, N).reshape(T, E, A)
+    boot = OA.values(params, o.array("obs_live").reshape(-1, D), D, H, N).reshape(E, A)
+    adv, ret = O.gae(o.array("rew")[:T], o.array("done")[:T], vals, boot, 0.99, 0.95, f64=True)
+    Ah = OA.normalize(adv)
+    ref = OA.grad(params, obs, act, Ah, ret.ravel(), D, H, N, 0.5, 0.01)
+    scale = grad_scale(params, obs, act, Ah, ret.ravel(), D, H, N, 0.5, 0.01, T * E * A)
+    got = tr.grad.cpu().numpy().astype(np.float64)
+    bad = np.abs(got - ref) > 1e-4 * scale + 1e-10
+    assert not bad.any(), (np.flatnonzero(bad)[:10], got[bad][:5], ref[bad][:5])
