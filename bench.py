@@ -150,11 +150,28 @@ def oracle_rollout(b, w, T, probs, cores):
     """One oracle roll-out of workload w (policy-driven for NEXT-N1 workloads; followed by
     GAE over the slots it wrote for NEXT-N2 workloads)."""
     pol = W.workload_policy(w)
-    if pol:
+    if pol and w.n_actions == 0:  # Gaussian policy (R34): the policy prefix W1..log_std
+        D, H, d = OBS_DIM[w.env], pol[0], w.act_dim
+        st = b.rollout_policy_gauss(T, pol[1][:D * H + H + H * d + 2 * d], H, n_threads=cores)
+    elif pol:
         st = b.rollout_policy(T, pol[1], pol[0], n_threads=cores)
     else:
         st = b.rollout(T, probs, n_threads=cores)
-    if w.params.get("a2c"):  # NEXT-N2: the oracle's A2C update on the slots just written
+    if w.params.get("a2c") and w.n_actions == 0:  # NEXT-N2 continuous (R35): the oracle's Gaussian update
+        import oracle as O
+        from oracle import a2c as OA
+        H, params = pol
+        D, d = OBS_DIM[w.env], w.act_dim
+        obs = b.array("obs")[:T].reshape(-1, D)
+        _, _, _, _, V = OA.forward_gauss(params, obs, D, H, d)
+        boot = OA.forward_gauss(params, b.array("obs_live").reshape(-1, D), D, H, d)[4]
+        adv, ret = O.gae(b.array("rew")[:T].reshape(T, w.n_envs), b.array("done")[:T], V.reshape(T, w.n_envs),
+                         boot, 0.99, 0.95, f64=True)
+        g = OA.grad_gauss(params, obs, b.array("act")[:T].reshape(-1, d), OA.normalize(adv), ret.ravel(), D, H, d,
+                          0.5, 0.01)
+        z = np.zeros(params.size)
+        OA.adam(params, OA.clip(g, 0.5), z, z, 1, 1e-4)
+    elif w.params.get("a2c"):  # NEXT-N2: the oracle's A2C update on the slots just written
         import oracle as O
         from oracle import a2c as OA
         H, params = pol
@@ -462,10 +479,11 @@ def main():
         # NEXT-N1: the MLP's fused multiply-adds per replica-step (D x H + H x n), against the
         # fp32 FMA peak from unit counts and clock: 148 SMs x 128 lanes x 2 flop x 1.965 GHz
         D_obs, Hh = OBS_DIM[w.env], pol[0]
-        flops = 2.0 * (D_obs * Hh + Hh * w.n_actions) * E * A * T
+        flops = 2.0 * (D_obs * Hh + Hh * max(w.n_actions, w.act_dim)) * E * A * T
         fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         tf = flops / (roll_ms / 1e3) / 1e12 if roll_ms > 0 else 0.0
-        roofline["kernel"] = f"k_rollout_policy<{w.env},{Hh}>"
+        roofline["kernel"] = (f"k_rollout_gpolicy<{Hh}> (Gaussian, Pendulum)" if w.n_actions == 0
+                              else f"k_rollout_policy<{w.env},{Hh}>")
         roofline["other_kernels"] = {}
         roofline["alu_view"] = {"achieved": round(tf, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",
                                 "frac": round(tf / fp32_peak, 4), "flops_per_launch": flops,

@@ -54,6 +54,9 @@ CONFIGS = {
     "C2O": Workload("C2O", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64, "a2c": True, "ppo": (4, 4)},
                     note="CartPole-v1 10K envs x 1000 steps + PPO update (4 epochs x 4 minibatches) of a 4-64-2 "
                          "actor-critic (NEXT-N2)"),
+    # NEXT-N2 continuous (R34 / R35): C3b's Pendulum shape with a Gaussian actor-critic iteration
+    "C3T": Workload("C3T", "pendulum", 100000, 1, 200, 0, 1, {"policy_hidden": 64, "a2c": True},
+                    note="Pendulum-v1 100K envs x 200 steps + A2C update of a 3-64-1 Gaussian actor-critic (NEXT-N2)"),
     # NEXT-N3: C2 through the copy-based baseline pipeline (per-step H2D of the
     # probabilities and D2H of the slot, synchronised every step) -- the "data transfer"
     # cost WarpSci removes
@@ -119,7 +122,9 @@ def workload_policy(w: Workload):
     H = w.params.get("policy_hidden")
     if not H:
         return None
-    D = {"cartpole": 4, "acrobot": 6, "dummy": 4}[w.env]
+    D = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3}[w.env]
+    if w.params.get("a2c") and w.n_actions == 0:  # Gaussian actor-critic (R35)
+        return H, a2c_params_gauss(D, H, w.act_dim, seed=SEED)
     if w.params.get("a2c"):  # actor-critic: the policy prefix followed by the value head
         return H, a2c_params(D, H, w.n_actions, seed=SEED, scale=1.0)
     return H, policy_weights(D, H, w.n_actions, seed=SEED, scale=2.0)
@@ -162,6 +167,16 @@ def a2c_params(D: int, H: int, N: int, seed: int = SEED, scale: float = 1.0) -> 
     rng = np.random.default_rng(seed + 1)
     head = np.concatenate([rng.standard_normal(H) * (scale / np.sqrt(H)), [10.0 * scale]])
     return np.concatenate([policy_weights(D, H, N, seed, scale), head]).astype(np.float32)
+
+
+def a2c_params_gauss(D: int, H: int, d: int, seed: int = SEED, log_std: float = -0.5) -> np.ndarray:
+    """NEXT-N2 continuous actor-critic parameters (R35): W1 | b1 | W2 [H][d] | b2 [d] |
+    log_std [d] | wv [H] | bv, float32 (Glorot-like normal draws)."""
+    rng = np.random.default_rng(seed + 3)
+    parts = [rng.standard_normal(D * H) / np.sqrt(D), rng.standard_normal(H) * 0.1,
+             rng.standard_normal(H * d) / np.sqrt(H), np.zeros(d), np.full(d, log_std),
+             rng.standard_normal(H) / np.sqrt(H), [-100.0]]
+    return np.concatenate(parts).astype(np.float32)
 
 
 def a2c_batch(rows: int, D: int, N: int, seed: int = SEED, invalid_frac: float = 0.0):
