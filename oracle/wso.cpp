@@ -1068,20 +1068,23 @@ int wso_policy_probs(const float* weights, int D, int H, int N, const float* obs
  * pre-step observation obs_live (single-agent discrete envs); otherwise as wso_rollout. */
 int wso_rollout_policy(void* h, int T, const float* weights, int H, int n_threads) {
   Batch* b = (Batch*)h;
-  if (T < 1 || !weights || H < 1 || b->A != 1 || b->n_actions < 1) return E_INVALID_ARGUMENT;
+  if (T < 1 || !weights || H < 1 || b->n_actions < 1) return E_INVALID_ARGUMENT;
   if (T > b->T_cap) return E_OUT_OF_RANGE;
   if (n_threads < 1) n_threads = 1;
   if (n_threads > b->E) n_threads = (int)b->E;
   const uint64_t t0 = b->t;
   const int D = b->obs_dim, N = b->n_actions;
   b->cursor = 0;
-  std::vector<float> probs((size_t)b->E * N);
+  const int A = b->A;  // multi-agent (tag): every agent evaluates the policy on its own row (R36)
+  std::vector<float> probs((size_t)b->E * A * N);
   std::vector<std::vector<double>> st(n_threads, std::vector<double>((size_t)T * 4, 0.0));
   std::vector<int> errs(n_threads, 0);
   auto worker = [&](int w) {
     int64_t e0 = b->E * w / n_threads, e1 = b->E * (w + 1) / n_threads;
     for (int c = 0; c < T; ++c) {
-      for (int64_t e = e0; e < e1; ++e) policy_probs(weights, D, H, N, &b->obs_live[(size_t)e * D], &probs[(size_t)e * N]);
+      for (int64_t e = e0; e < e1; ++e)
+        for (int ag = 0; ag < A; ++ag)
+          policy_probs(weights, D, H, N, &b->obs_live[((size_t)e * A + ag) * D], &probs[((size_t)e * A + ag) * N]);
       b->sample_range(c, t0 + c, probs.data(), N, nullptr, nullptr, e0, e1, &errs[w]);
       b->step_range(c, e0, e1, &st[w][(size_t)c * 4], &errs[w]);
     }

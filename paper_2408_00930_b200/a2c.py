@@ -238,11 +238,13 @@ class A2C:
         return pol
 
     def iteration(self, T: int):
-        """Roll out T steps with the current policy (single-agent: the kernel also writes the
-        critic's values from the hidden layer it already computes; multi-agent: the torch policy
-        through ws_sample / ws_step), then update (train)."""
+        """Roll out T steps with the current policy (the fused kernels also write the critic's
+        values from the hidden layer they already compute -- single-agent lanes, tag's agent
+        threads; other multi-agent cases: the torch policy through ws_sample / ws_step), then
+        update (train, S:419)."""
         vals = self._value_buf(T * self.E)
-        if self.A == 1:
+        if self.A == 1 or (self.env.env == "tag" and self.A <= 128 and not self.gaussian):
+            # fused roll-out with in-kernel policy + critic (tag: agent threads of the CTA kernel)
             self.env.rollout_actor_critic(T, self.params, self.H, vals, self.bootstrap,
                                           self._vtrunc if self.bootstrap_truncation else None)
             self.update(T, values_ready=True)

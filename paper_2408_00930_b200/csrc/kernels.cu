@@ -1685,13 +1685,70 @@ constexpr int kTagN = 5;
 __host__ __device__ inline int tag_red_offset(int G) { return 2 * G * G + ((2 * G * G) & 1); }  // in ints
 __host__ __device__ inline int tag_tab_offset(int G, int nwarps) { return tag_red_offset(G) + 6 * nwarps; }
 
+// NEXT-N1 for the multi-agent env: the R29 policy of one agent on its observation o[D]
+// (weights `sw` = W1 [D][H] | b1 | W2 [H][N] | b2 (| wv [H] | bv)), in R29's operation order:
+// the probabilities p_i = e_i / S with e_i = (float)exp((double)(l_i - m)), as the fp64-prefix
+// CDF of the R13 sampler; v = the R31 critic when kCritic.
+template <int D, int H, int N, bool kCritic>
+__device__ __forceinline__ void policy_cdf(const float* sw, const float (&o)[D], RowCDF<N>& cdf, float& v) {
+  const float* W1 = sw;
+  const float* b1 = W1 + D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + H * N;
+  const float* wv = b2 + N;
+  float hid[H];
+#pragma unroll
+  for (int j = 0; j < H; ++j) {
+    float acc = b1[j];
+#pragma unroll
+    for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
+    hid[j] = acc > 0.0f ? acc : 0.0f;
+  }
+  if (kCritic) {
+    v = wv[H];
+#pragma unroll
+    for (int j = 0; j < H; ++j) v = __fmaf_rn(wv[j], hid[j], v);
+  }
+  float lg[N];
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    float acc = b2[i];
+#pragma unroll
+    for (int j = 0; j < H; ++j) acc = __fmaf_rn(W2[j * N + i], hid[j], acc);
+    lg[i] = acc;
+  }
+  float m = lg[0];
+#pragma unroll
+  for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
+  float S = 0.0f;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    cdf.P[i] = (float)exp((double)fsub(lg[i], m));
+    S = fadd(S, cdf.P[i]);
+  }
+  double run = 0.0;
+  bool badp = false;
+#pragma unroll
+  for (int i = 0; i < N; ++i) {
+    cdf.P[i] = fdiv(cdf.P[i], S);
+    run += (double)cdf.P[i];
+    cdf.C[i] = run;
+    badp = badp || !(cdf.P[i] >= 0.0f) || !isfinite(cdf.P[i]);
+  }
+  cdf.bad = badp || !(run > 0.0) || !isfinite(run);
+}
+
 // kHoisted: roll-out with per-step-constant probabilities (thresholds hoisted, no per-step
 // CDF code in the kernel); otherwise the general kernel (per-step rows, ws_step modes).
-template <int kMaxThreads, int kMinBlocks, bool kHoisted>
+// kPolH > 0 (NEXT-N1, R29 / R36): every agent thread draws its action from the R29 policy
+// (hidden kPolH, weights in `given`, staged in shared memory after the observation table)
+// on its pre-step observation; kCritic also writes values [T, E, A] and bootstrap [E, A].
+template <int kMaxThreads, int kMinBlocks, bool kHoisted, int kPolH, bool kCritic>
 __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, const int mode, const int T, const uint64_t t0,
                                               const int slot0, const float* __restrict__ probs,
                                               const int64_t row_stride, const int64_t step_stride,
-                                              const void* __restrict__ given) {
+                                              const void* __restrict__ given, float* __restrict__ values,
+                                              float* __restrict__ bootstrap) {
   extern __shared__ int smem[];
   const int G = a.p0, NT = a.p1, A = a.A;
   const int nwarps = blockDim.x >> 5;
@@ -1711,6 +1768,11 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
   // observations are the G values x / (G - 1) (IEEE division, R22), tabulated once
   for (int i = ag; i < 2 * G * G; i += blockDim.x) smem[i] = 0;
   for (int i = ag; i < G; i += blockDim.x) obs_tab[i] = (float)i / (float)(G - 1);
+  constexpr int kPolHH = kPolH > 0 ? kPolH : 1;
+  constexpr int kNW = 4 * kPolHH + kPolHH + kPolHH * kTagN + kTagN + (kCritic ? kPolHH + 1 : 0);
+  float* sw = obs_tab + G;  // policy weights (kPolH > 0)
+  if (kPolH > 0)
+    for (int i = ag; i < kNW; i += blockDim.x) sw[i] = reinterpret_cast<const float*>(given)[i];
 
   int32_t x = 0, y = 0, active = 0;
   if (is_agent) {
@@ -1746,7 +1808,16 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
       if (c == 0 || (t & 3) == 0) w = block(key, t >> 2, eg, (uint32_t)ag, kAction);
       const uint32_t word = pick(w, (uint32_t)(t & 3));
       float lp;
-      if (kHoisted) {
+      if constexpr (kPolH > 0) {  // the agent's policy on its pre-step observation (R22 obs)
+        const float o[4] = {obs_tab[x], obs_tab[y], tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f};
+        RowCDF<kTagN> cdf;
+        float v = 0.0f;
+        policy_cdf<4, kPolHH, kTagN, kCritic>(sw, o, cdf, v);
+        bad_probs = cdf.bad;
+        act = search<kTagN>(cdf, u01(word));
+        lp = logp_of_normalised<kTagN>(cdf, act);
+        if (kCritic && is_agent) st_cs(values + idx, v);
+      } else if (kHoisted) {
         act = search_k<kTagN>(th, word >> 8, lp);
         bad_probs = th.bad;
       } else {
@@ -1861,6 +1932,13 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
     }
     // (the reduction buffer is next written after the next valid step's first barrier, which
     // every thread reaches only after reading it)
+  }
+  if (kCritic && is_agent) {  // bootstrap value of the observation after the last step
+    const float o[4] = {obs_tab[x], obs_tab[y], tagger ? 1.0f : 0.0f, active ? 1.0f : 0.0f};
+    RowCDF<kTagN> cdf;
+    float v = 0.0f;
+    policy_cdf<4, kPolHH, kTagN, kCritic>(sw, o, cdf, v);
+    bootstrap[e * A + ag] = v;
   }
   if (is_agent) {
     int32_t* ts = a.tstate + ((size_t)e * A + ag) * 3;
@@ -2010,8 +2088,9 @@ static void tag_launch(const KArgs& a, const Launch& l, int b, int mode, int T, 
 #define WS_TAG_MINB 7
 #endif
 #define WS_TAG_LAUNCH(MT, MB, H)                                                                        \
-  k_tag<MT, MB, H><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs, row_stride, \
-                                                                  step_stride, given)
+  k_tag<MT, MB, H, 0, false><<<(unsigned)a.E, b, tag_smem(a, b), l.stream>>>(a, mode, T, t0, slot0, probs,     \
+                                                                            row_stride, step_stride, given, \
+                                                                            nullptr, nullptr)
   const bool h = mode == kTagRollout && step_stride == 0;
   if (b <= 128) {  // 6 CTAs of 128 threads per SM (measured best for C4: 7 and 8 force spills / fewer registers)
     if (h) WS_TAG_LAUNCH(128, WS_TAG_MINB, true); else WS_TAG_LAUNCH(128, WS_TAG_MINB, false);
@@ -2021,6 +2100,24 @@ static void tag_launch(const KArgs& a, const Launch& l, int b, int mode, int T, 
     if (h) WS_TAG_LAUNCH(1024, 1, true); else WS_TAG_LAUNCH(1024, 1, false);
   }
 #undef WS_TAG_LAUNCH
+}
+
+// NEXT-N1 / R36: the tag roll-out with every agent's action from the in-kernel policy
+static cudaError_t tag_policy_launch(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
+                                     int hidden, float* values, float* bootstrap) {
+  const int b = tag_block(a);
+  if (b > 128) return cudaErrorInvalidValue;  // up to 128 agents per replica (launch bounds of the policy build)
+  const size_t smem = tag_smem(a, b) + (size_t)(4 * hidden + hidden + hidden * kTagN + kTagN + hidden + 1) * 4;
+#define WS_TAG_POL(HH, C)                                                                                   \
+  k_tag<128, 1, false, HH, C><<<(unsigned)a.E, b, smem, l.stream>>>(a, kTagRollout, T, t0, 0, nullptr, 0, 0, weights, \
+                                                                  values, bootstrap)
+  if (values) {
+    if (hidden == 32) WS_TAG_POL(32, true); else WS_TAG_POL(64, true);
+  } else {
+    if (hidden == 32) WS_TAG_POL(32, false); else WS_TAG_POL(64, false);
+  }
+#undef WS_TAG_POL
+  return cudaGetLastError();
 }
 
 // lane kernels carry one statistics window per warp in dynamic shared memory
@@ -2213,6 +2310,11 @@ cudaError_t launch_rollout_policy(const KArgs& a, const Launch& l, int T, uint64
   cudaError_t err = cudaErrorInvalidValue;
   switch (l.kind) {
     case kPendulum: err = rollout_gpolicy(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
+    case kTag:
+      l.m(kKRollout, 0);
+      err = tag_policy_launch(a, l, T, t0, weights, hidden, values, bootstrap);
+      l.m(kKRollout, 1);
+      break;
     case kCartPole: err = rollout_policy<CartPole>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
     case kAcrobot: err = rollout_policy<Acrobot>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;
     case kDummy: err = rollout_policy<Dummy>(a, l, T, t0, weights, hidden, values, bootstrap, vtr); break;

@@ -519,8 +519,10 @@ static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t 
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
-  if (h->A != 1 || (h->spec.n_actions < 1 && h->spec.kind != ws::kPendulum) || h->spec.kind == ws::kTag)
-    return fail(h, WS_ERR_INVALID_ARGUMENT, "policy roll-out: single-agent discrete envs or pendulum (Gaussian)");
+  if ((h->A != 1 && h->spec.kind != ws::kTag) || (h->spec.n_actions < 1 && h->spec.kind != ws::kPendulum) ||
+      (h->spec.kind == ws::kTag && h->A > 128))
+    return fail(h, WS_ERR_INVALID_ARGUMENT,
+                "policy roll-out: discrete envs (tag: <= 128 agents) or pendulum (Gaussian)");
   DeviceGuard g(h->device);
   ws_status st = ensure_store(h, T);
   if (st) return st;

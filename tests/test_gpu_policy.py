@@ -167,3 +167,37 @@ def test_torch_policy_rollout(P):
         lp_ref = torch.log(torch.gather(p_all, -1, act.unsqueeze(-1)).squeeze(-1))
     assert torch.allclose(C_["logp"][:T], lp_ref, atol=1e-5)
     assert 0.05 < (act == 0).float().mean().item() < 0.95
+
+
+@pytest.mark.parametrize("H,E,A,T", [(32, 20, 100, 60), (64, 7, 37, 80)])
+def test_tag_policy_rollout_parity(P, H, E, A, T):
+    """Multi-agent policy inference inside the CTA-per-replica tag kernel (P:65 / P:71:
+    every agent thread samples from the policy; R29, R36) against the oracle's per-agent
+    policy roll-out: bit-identical store (log-probs within 2 ulp, R18); with the critic,
+    values / bootstrap within the critic tolerance."""
+    w = W.policy_weights(4, H, 5, seed=181, scale=2.0)
+    g = P.Env(E, A, "tag", SEED, t_capacity=T)
+    g.rollout_policy(T, torch.from_numpy(w).cuda(), H)
+    assert g.status() == 0
+    o = O.Batch("tag", E, A, SEED, t_capacity=T)
+    assert o.rollout_policy(T, w, H, n_threads=4) == 0
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done", "obs_live", "reset_count"):
+        ref = o.array(k)[:T] if k in ("obs", "act", "rew", "done") else o.array(k)
+        got = buf[k][:T] if k in ("obs", "act", "rew", "done") else buf[k]
+        assert np.array_equal(got, ref), k
+    lg, lo = buf["logp"][:T].ravel(), o.array("logp")[:T].ravel()
+    assert np.all(np.abs(lg.view(np.int32).astype(np.int64) - lo.view(np.int32).astype(np.int64)) <= 2)
+    assert len(np.unique(buf["act"][:T])) >= 3  # the policy really varies the actions
+    # critic variant: same store, values of the logged observations
+    head = np.concatenate([np.random.default_rng(182).standard_normal(H) / np.sqrt(H), [0.5]]).astype(np.float32)
+    gc = P.Env(E, A, "tag", SEED, t_capacity=T)
+    vals, boot = torch.empty(T * E * A, device="cuda"), torch.empty(E * A, device="cuda")
+    gc.rollout_actor_critic(T, torch.from_numpy(np.concatenate([w, head])).cuda(), H, vals, boot)
+    assert np.array_equal(gc.buffers()["act"].cpu().numpy(), buf["act"])
+    obs = buf["obs"][:T].reshape(-1, 4).astype(np.float64)
+    W1 = w[:4 * H].reshape(4, H).astype(np.float64)
+    b1 = w[4 * H:4 * H + H].astype(np.float64)
+    h = np.maximum(obs @ W1 + b1, 0.0)
+    ref = h @ head[:H].astype(np.float64) + head[H]
+    assert np.all(np.abs(vals.cpu().numpy() - ref) <= 1e-5 * (1.0 + h @ np.abs(head[:H])))
