@@ -178,16 +178,18 @@ def oracle_rollout(b, w, T, probs, cores):
         D = OBS_DIM[w.env]
         N = w.n_actions
         obs = b.array("obs")[:T].reshape(-1, D)
-        vals = OA.values(params, obs, D, H, N).reshape(T, w.n_envs)
-        boot = OA.values(params, b.array("obs_live").reshape(-1, D), D, H, N)
-        adv, ret = O.gae(b.array("rew")[:T].reshape(T, w.n_envs), b.array("done")[:T], vals, boot, 0.99, 0.95,
-                         f64=True)
+        EA = w.n_envs * w.n_agents  # multi-agent (R36): every agent is a column
+        vals = OA.values(params, obs, D, H, N).reshape(T, w.n_envs, w.n_agents)
+        boot = OA.values(params, b.array("obs_live").reshape(-1, D), D, H, N).reshape(w.n_envs, w.n_agents)
+        adv, ret = O.gae(b.array("rew")[:T].reshape(T, w.n_envs, w.n_agents), b.array("done")[:T], vals, boot,
+                         0.99, 0.95, f64=True)
+        adv, ret = adv.reshape(T, EA), ret.reshape(T, EA)
         z = np.zeros(params.size)
         act = b.array("act")[:T].reshape(-1)
         ppo = w.params.get("ppo")
         if ppo:  # K epochs x M minibatches of the clipped surrogate (R33), whole-batch normalisation
             Ah, logp_old, p, m, v, k = OA.normalize(adv), b.array("logp")[:T].reshape(-1), params, z, z, 0
-            E = w.n_envs
+            E = EA
             for _ in range(ppo[0]):
                 for mb in range(ppo[1]):
                     r0, r1 = T * mb // ppo[1] * E, T * (mb + 1) // ppo[1] * E
@@ -483,6 +485,7 @@ def main():
         fp32_peak = 148 * 128 * 2 * 1.965e9 / 1e12
         tf = flops / (roll_ms / 1e3) / 1e12 if roll_ms > 0 else 0.0
         roofline["kernel"] = (f"k_rollout_gpolicy<{Hh}> (Gaussian, Pendulum)" if w.n_actions == 0
+                              else f"k_tag<policy {Hh}> (agent threads)" if w.env == "tag"
                               else f"k_rollout_policy<{w.env},{Hh}>")
         roofline["other_kernels"] = {}
         roofline["alu_view"] = {"achieved": round(tf, 3), "peak": round(fp32_peak, 1), "unit": "TFLOP/s",

@@ -7,7 +7,7 @@ nvidia-smi > gpurun_out/nvidia_smi.txt 2>&1
 python -c "import __graft_entry__ as g; g.build(); g.smoke()" > gpurun_out/smoke.log 2>&1; echo "smoke rc=$?"
 timeout 1500 python -m pytest tests -m gpu -x -q -s > gpurun_out/pytest_gpu.log 2>&1; echo "pytest rc=$?"
 tail -3 gpurun_out/pytest_gpu.log
-WORKLOADS="C1 C2 C3a C3b C4 C5 D0 C2P C2G C4G C2T C2O C3T C2X C2U" bash tools/all_workloads.sh
+WORKLOADS="C1 C2 C3a C3b C4 C5 D0 C2P C2G C4G C2T C2O C3T C4T C2X C2U" bash tools/all_workloads.sh
 timeout 600 python bench.py > gpurun_out/bench.json 2> gpurun_out/bench.err; echo "bench rc=$?"
 timeout 300 python -m paper_2408_00930_b200.train --envs 10000 --T 32 --iters 3000 --log-every 50 --csv gpurun_out/curve_cartpole.csv
 timeout 300 python -m paper_2408_00930_b200.train --env acrobot --envs 10000 --T 128 --iters 1500 --lr 1e-3 --log-every 50 --csv gpurun_out/curve_acrobot.csv

@@ -57,6 +57,9 @@ CONFIGS = {
     # NEXT-N2 continuous (R34 / R35): C3b's Pendulum shape with a Gaussian actor-critic iteration
     "C3T": Workload("C3T", "pendulum", 100000, 1, 200, 0, 1, {"policy_hidden": 64, "a2c": True},
                     note="Pendulum-v1 100K envs x 200 steps + A2C update of a 3-64-1 Gaussian actor-critic (NEXT-N2)"),
+    # NEXT-N2 multi-agent (R36): C4's tag shape with every agent's policy in the kernel + A2C
+    "C4T": Workload("C4T", "tag", 1000, 100, 200, 5, 1, {"grid": 20, "taggers": 10, "policy_hidden": 64, "a2c": True},
+                    note="tag 1K envs x 100 agents x 200 + multi-agent A2C update of a 4-64-5 actor-critic (NEXT-N2)"),
     # NEXT-N3: C2 through the copy-based baseline pipeline (per-step H2D of the
     # probabilities and D2H of the slot, synchronised every step) -- the "data transfer"
     # cost WarpSci removes
@@ -122,7 +125,7 @@ def workload_policy(w: Workload):
     H = w.params.get("policy_hidden")
     if not H:
         return None
-    D = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3}[w.env]
+    D = {"cartpole": 4, "acrobot": 6, "dummy": 4, "pendulum": 3, "tag": 4}[w.env]
     if w.params.get("a2c") and w.n_actions == 0:  # Gaussian actor-critic (R35)
         return H, a2c_params_gauss(D, H, w.act_dim, seed=SEED)
     if w.params.get("a2c"):  # actor-critic: the policy prefix followed by the value head
