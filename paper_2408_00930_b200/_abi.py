@@ -117,6 +117,7 @@ _SIGS = {
     "ws_register_env": (C.c_int, [C.POINTER(ws_env_def), C.c_char_p, C.c_size_t]),
     "ws_registered_env": (C.c_int32, [C.c_char_p]),
     "ws_set_env_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
+    "ws_set_time": (C.c_int, [C.c_void_p, C.c_uint64]),
     "ws_get_buffers": (C.c_int, [C.c_void_p, C.POINTER(ws_buffers)]),
     "ws_get_info": (C.c_int, [C.c_void_p, C.POINTER(ws_info)]),
     "ws_synchronize": (C.c_int, [C.c_void_p]),

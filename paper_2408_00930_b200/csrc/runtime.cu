@@ -302,6 +302,14 @@ ws_status ws_create(int64_t n_envs, int32_t n_agents, const char* env, uint64_t 
   return ws_create_ex(&c, out);
 }
 
+ws_status ws_set_time(ws_env* h, uint64_t t) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  h->t = t;
+  h->cursor = 0;
+  h->sampled_slot = -1;
+  return WS_OK;
+}
+
 ws_status ws_set_env_data(ws_env* h, const float* prm, const float* shared) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (h->spec.kind != ws::kUser) return fail(h, WS_ERR_INVALID_ARGUMENT, "ws_set_env_data: registered envs only");

@@ -180,3 +180,26 @@ def test_register_env_compiles_without_gpu():
         d.update(bad)
         assert L.ws_register_env(C.byref(_abi.ws_env_def(**d)), buf, 256) == _abi.INVALID_ARGUMENT, bad
     assert L.ws_set_env_data(None, None, None) == _abi.INVALID_ARGUMENT
+
+
+def test_param_checkpoint_round_trip_without_gpu(tmp_path):
+    """flat little-endian float32 with a header; bit-exact round trip, including
+    NaN payloads, -0 and subnormals; corrupted files are rejected."""
+    from paper_2408_00930_b200 import checkpoint as ck
+    p = torch.from_numpy(np.random.default_rng(1).standard_normal(515).astype(np.float32))
+    p[3] = float("nan")
+    p[4] = -0.0
+    p[5] = 1e-40
+    f = str(tmp_path / "p.wsac")
+    ck.save_params(f, p, 4, 64, 2, "softmax")
+    q, meta = ck.load_params(f)
+    assert meta == {"obs_dim": 4, "hidden": 64, "n_actions": 2, "head": "softmax"}
+    assert np.array_equal(q.numpy().view(np.uint32), p.numpy().view(np.uint32))
+    raw = open(f, "rb").read()
+    open(f, "wb").write(b"XXXX" + raw[4:])
+    with pytest.raises(ValueError):
+        ck.load_params(f)
+    open(f, "wb").write(raw[:-4])
+    with pytest.raises(ValueError):
+        ck.load_params(f)
+    assert P.lib().ws_set_time(None, 5) == _abi.INVALID_ARGUMENT
