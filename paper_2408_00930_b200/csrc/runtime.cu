@@ -10,6 +10,8 @@
 #include <string>
 #include <vector>
 
+#include <nvtx3/nvToolsExt.h>
+
 #include "../../include/ws.h"
 #include "common.cuh"
 #include "kernels.h"
@@ -48,6 +50,13 @@ bool lookup_env(const char* name, int A, int p0, EnvSpec* out) {
 bool surface_dim_supported(int D) {
   return D == 2 || D == 3 || D == 4 || D == 8 || D == 16 || D == 20 || D == 32;
 }
+
+// NVTX range per public call (SURVEY 5 tracing): header-only NVTX v3, a no-op unless a
+// profiler (nsys / ncu --nvtx) is attached
+struct NvtxRange {
+  explicit NvtxRange(const char* name) { nvtxRangePushA(name); }
+  ~NvtxRange() { nvtxRangePop(); }
+};
 
 struct DeviceGuard {
   int prev = -1;
@@ -407,6 +416,7 @@ ws_status ws_destroy(ws_env* h) {
 }
 
 ws_status ws_reset(ws_env* h) {
+  NvtxRange nvtx_("ws_reset");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
   cudaError_t e = cudaMemsetAsync(h->err, 0, sizeof(uint32_t), h->stream);
@@ -436,6 +446,7 @@ ws_status ws_rewind(ws_env* h) {
 }
 
 ws_status ws_sample(ws_env* h, const float* probs, int64_t row_stride) {
+  NvtxRange nvtx_("ws_sample");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (!probs || row_stride < 0) return fail(h, WS_ERR_INVALID_ARGUMENT, "probs must be a device pointer, row_stride >= 0");
   DeviceGuard g(h->device);
@@ -450,6 +461,7 @@ ws_status ws_sample(ws_env* h, const float* probs, int64_t row_stride) {
 }
 
 ws_status ws_step(ws_env* h, const void* actions) {
+  NvtxRange nvtx_("ws_step");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
   ws_status s = ensure_store(h, 1000);
@@ -467,6 +479,7 @@ ws_status ws_step(ws_env* h, const void* actions) {
 }
 
 ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_stride, int64_t step_stride) {
+  NvtxRange nvtx_("ws_rollout");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!probs || row_stride < 0 || step_stride < 0) return fail(h, WS_ERR_INVALID_ARGUMENT, "bad probs / strides");
@@ -524,6 +537,7 @@ static void sum_stats(const long long* st, int n, ws_stats* out) {
 
 static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t hidden, float* values,
                             float* bootstrap, float* values_trunc = nullptr) {
+  NvtxRange nvtx_("ws_rollout_policy");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
@@ -586,6 +600,7 @@ ws_status ws_gae(const ws_gae_args* args, void* stream) {
 
 ws_status ws_gae_store(ws_env* h, int32_t T, const float* values, const float* bootstrap, const float* v_trunc,
                        float gamma, float lambda, float* adv, float* ret) {
+  NvtxRange nvtx_("ws_gae_store");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1");
   if (!h->rew) return fail(h, WS_ERR_BAD_STATE, "ws_gae_store needs the store (t_capacity or a first ws_rollout)");
