@@ -90,9 +90,9 @@ def test_policy_argument_validation(P):
         g.rollout_policy(4, w, 48)  # hidden must be 32 or 64
     with pytest.raises(P.WSError):
         g.rollout_policy(5, w, 32)  # T beyond the store capacity
-    t = P.Env(2, 10, "tag", SEED, t_capacity=4)
+    t = P.Env(2, 200, "tag", SEED, t_capacity=4)
     with pytest.raises(P.WSError):
-        t.rollout_policy(4, w, 32)  # multi-agent env: not supported by the policy roll-out
+        t.rollout_policy(4, w, 32)  # tag policy roll-out: at most 128 agents per replica
     p = P.Env(4, 1, "surface", SEED, t_capacity=4, param0=20)
     with pytest.raises(P.WSError):
         p.rollout_policy(4, w, 32)  # continuous actions beyond Pendulum (R34): not supported
