@@ -16,6 +16,7 @@ from __future__ import annotations
 import ctypes as C
 from typing import Optional
 
+import numpy as np
 import torch
 import torch.distributed as dist
 
@@ -269,6 +270,7 @@ class PPO(A2C):
         if epochs < 1 or minibatches < 1:
             raise WSError(_abi.INVALID_ARGUMENT, "epochs, minibatches >= 1")
         self.epochs, self.minibatches, self.clip_eps = epochs, minibatches, clip_eps
+        self.ppo_seed = int(kw.get("seed", 0)) & 0xFFFFFFFF
 
     def update(self, T: int, values_ready: bool = False):
         if T < self.minibatches:
@@ -277,8 +279,12 @@ class PPO(A2C):
             obs, act, adv, ret, rows = self._advantages(T, values_ready)
             logp = self.env.buffers()["logp"][:T].reshape(rows)
             E, D, M = self.E, self.D, self.minibatches
-            for _ in range(self.epochs):
-                for m in range(M):
+            for ep in range(self.epochs):
+                # minibatch order shuffled per epoch from a dedicated stream ("minibatch
+                # shuffling from a dedicated RngStream"): Philox-free host permutation keyed by
+                # (update count, epoch), identical on every rank
+                order = np.random.Generator(np.random.PCG64([self.ppo_seed, self.step, ep])).permutation(M)
+                for m in order.tolist():
                     t0, t1 = T * m // M, T * (m + 1) // M
                     r0, r1 = t0 * E, t1 * E
                     na = self.N if self.gaussian else 1
