@@ -68,7 +68,7 @@ def lib():
             "wso_destroy": (None, [P]),
             "wso_set_capacity": (I, [P, I]),
             "wso_reset": (I, [P]),
-            "wso_register_user": (I, [C.c_char_p, C.c_char_p, I, I, I, I, I, I]),
+            "wso_register_user": (I, [C.c_char_p, C.c_char_p, I, I, I, I, I, I, I]),
             "wso_policy_gauss_rows": (I, [P, I, I, I, P, I64, P]),
             "wso_rollout_policy_gauss": (I, [P, I, P, I, I]),
             "wso_set_env_data": (I, [P, P, I64, P, I64]),
@@ -275,25 +275,30 @@ static inline float ws_max(float a, float b) { return a < b ? b : a; }
 static inline float ws_clip(float x, float lo, float hi) { return x < lo ? lo : (hi < x ? hi : x); }
 static inline float ws_abs(float x) { return std::fabs(x); }
 static inline float ws_floor(float x) { return std::floor(x); }
+static inline float ws_fmod(float x, float y) { return std::fmod(x, y); }
 #line 1 "user_env.c"
 """
 _USER_EPILOGUE = r"""
 extern "C" {
 void wsu_init(float* s, const float* u, const float* p, const float* sh) { ws_env_init(s, u, p, sh); }
 void wsu_obs(const float* s, float* o, const float* p, const float* sh) { ws_env_obs(s, o, p, sh); }
+#if WS_C > 0
+int wsu_step(float* s, const float* a, float* r, const float* p, const float* sh) { return ws_env_step(s, a, r, p, sh); }
+#else
 int wsu_step(float* s, int a, float* r, const float* p, const float* sh) { return ws_env_step(s, a, r, p, sh); }
+#endif
 }
 """
 _USER_ENVS = set()
 
 
 def register_user_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions: int, n_reset_draws: int,
-                      max_steps: int, n_params: int = 0) -> str:
+                      max_steps: int, n_params: int = 0, act_dim: int = 0) -> str:
     """Compile a user environment's C source with g++ (-O2 -ffp-contract=off) and register it
     with the oracle under `name`; Batch(name, ...) then simulates it.  Returns the .so path."""
     import hashlib
     defs = (f"#define WS_S {state_dim}\n#define WS_D {obs_dim}\n#define WS_N {n_actions}\n"
-            f"#define WS_R {n_reset_draws}\n#define WS_P {n_params}\n")
+            f"#define WS_R {n_reset_draws}\n#define WS_P {n_params}\n#define WS_C {act_dim}\n")
     text = defs + _USER_PRELUDE + source + "\n" + _USER_EPILOGUE
     key = hashlib.sha1(text.encode()).hexdigest()[:12]
     d = os.path.join(_HERE, "build_user")
@@ -307,7 +312,7 @@ def register_user_env(name: str, source: str, state_dim: int, obs_dim: int, n_ac
                         "-o", so + ".tmp", src], check=True)
         os.replace(so + ".tmp", so)
     st = lib().wso_register_user(name.encode(), so.encode(), state_dim, obs_dim, n_actions, n_reset_draws,
-                                 max_steps, n_params)
+                                 max_steps, n_params, act_dim)
     if st != OK:
         raise ValueError(f"wso_register_user failed ({st})")
     _USER_ENVS.add(name)

@@ -405,6 +405,8 @@ struct UserEnv {
   void (*init)(float*, const float*, const float*, const float*);
   void (*obs)(const float*, float*, const float*, const float*);
   int (*step)(float*, int, float*, const float*, const float*);
+  int act_dim;  // 0: discrete; > 0: continuous actions (step_c)
+  int (*step_c)(float*, const float*, float*, const float*, const float*);
 };
 std::map<std::string, UserEnv>& user_envs() {
   static std::map<std::string, UserEnv> m;
@@ -694,9 +696,16 @@ struct Batch {
           break;
         }
         case K_USER: {
-          int a = act_i[base];
-          bad = (a < 0 || a >= n_actions);
-          if (!bad) term = user->step(s, a, &r[0], prm_row(e), shared_ptr());
+          if (user->act_dim > 0) {  // continuous: a non-finite action is invalid (R19)
+            const float* ac = &act_f[base * user->act_dim];
+            bad = false;
+            for (int k = 0; k < user->act_dim; ++k) bad = bad || !std::isfinite(ac[k]);
+            if (!bad) term = user->step_c(s, ac, &r[0], prm_row(e), shared_ptr());
+          } else {
+            int a = act_i[base];
+            bad = (a < 0 || a >= n_actions);
+            if (!bad) term = user->step(s, a, &r[0], prm_row(e), shared_ptr());
+          }
           break;
         }
       }
@@ -895,7 +904,8 @@ void* wso_create(const char* env, int64_t E, int A, uint64_t seed, int64_t env_o
     case K_USER: {
       const UserEnv& u = user_envs()[env];
       b->user = &u;
-      b->obs_dim = u.obs_dim; b->n_actions = u.n_actions; b->act_dim = 1; b->state_dim = u.state_dim;
+      b->obs_dim = u.obs_dim; b->n_actions = u.n_actions; b->act_dim = u.act_dim > 0 ? u.act_dim : 1;
+      b->state_dim = u.state_dim;
       b->n_reset_draws = u.n_reset; b->T_max = u.max_steps;
       break;
     }
@@ -916,14 +926,18 @@ void* wso_create(const char* env, int64_t E, int A, uint64_t seed, int64_t env_o
 
 /* NEXT-N4: register the env compiled (by oracle/__init__.py) into so_path */
 int wso_register_user(const char* name, const char* so_path, int state_dim, int obs_dim, int n_actions, int n_reset,
-                      int max_steps, int n_params) {
+                      int max_steps, int n_params, int act_dim) {
   void* lib = dlopen(so_path, RTLD_NOW | RTLD_LOCAL);
   if (!lib) return E_INVALID_ARGUMENT;
   UserEnv u{state_dim, obs_dim, n_actions, n_reset, max_steps, n_params,
             reinterpret_cast<void (*)(float*, const float*, const float*, const float*)>(dlsym(lib, "wsu_init")),
             reinterpret_cast<void (*)(const float*, float*, const float*, const float*)>(dlsym(lib, "wsu_obs")),
-            reinterpret_cast<int (*)(float*, int, float*, const float*, const float*)>(dlsym(lib, "wsu_step"))};
-  if (!u.init || !u.obs || !u.step) return E_INVALID_ARGUMENT;
+            nullptr, act_dim, nullptr};
+  if (act_dim > 0)
+    u.step_c = reinterpret_cast<int (*)(float*, const float*, float*, const float*, const float*)>(dlsym(lib, "wsu_step"));
+  else
+    u.step = reinterpret_cast<int (*)(float*, int, float*, const float*, const float*)>(dlsym(lib, "wsu_step"));
+  if (!u.init || !u.obs || !(u.step || u.step_c)) return E_INVALID_ARGUMENT;
   user_envs()[name] = u;
   return E_OK;
 }

@@ -97,7 +97,7 @@ class ws_staged_report(C.Structure):
 class ws_env_def(C.Structure):
     _fields_ = [("name", C.c_char_p), ("source", C.c_char_p), ("state_dim", C.c_int32), ("obs_dim", C.c_int32),
                 ("n_actions", C.c_int32), ("n_reset_draws", C.c_int32), ("max_steps", C.c_int32),
-                ("n_params", C.c_int32)]
+                ("n_params", C.c_int32), ("act_dim", C.c_int32)]
 
 
 _SIGS = {

@@ -115,6 +115,7 @@ WS_FN float ws_max(float a, float b) { return a < b ? b : a; }
 WS_FN float ws_clip(float x, float lo, float hi) { return x < lo ? lo : (hi < x ? hi : x); }
 WS_FN float ws_abs(float x) { return fabsf(x); }
 WS_FN float ws_floor(float x) { return floorf(x); }
+WS_FN float ws_fmod(float x, float y) { return fmodf(x, y); }
 #line 1 "user_env.c"
 )WS";
 
@@ -145,6 +146,18 @@ WS_FN ws_u32 ws_draw(const WsUserArgs& a, ws_u32 eg, ws_u32 purpose, ws_u64 j) {
   return w[j & 3];
 }
 WS_FN float ws_u01(ws_u32 w) { return (float)(w >> 8) * (1.0f / 16777216.0f); }
+/* R14: Gaussian draw j of the GAUSS stream: Box-Muller on the word pair (2p, 2p+1),
+   p = (j & 3) >> 1, u1 in (0, 1], u2 in [0, 1), fp64, one rounding */
+WS_FN float ws_gauss(const WsUserArgs& a, ws_u32 eg, ws_u64 j) {
+  ws_u32 w[4];
+  ws_philox((ws_u32)(j >> 2), eg, 0u, 3u, a.k0, a.k1, w);
+  const int p = (int)((j & 3) >> 1);
+  const double u1 = (double)((w[2 * p] >> 8) + 1) * (1.0 / 16777216.0);
+  const double u2 = (double)(w[2 * p + 1] >> 8) * (1.0 / 16777216.0);
+  const double r = sqrt(-2.0 * log(u1));
+  const double ang = 2.0 * 3.14159265358979323846 * u2;
+  return (float)((j & 1) ? r * sin(ang) : r * cos(ang));
+}
 
 WS_FN void ws_init(const WsUserArgs& a, ws_u32 eg, ws_u32 rc, float* s, const float* prm) {
   float u[WS_R > 0 ? WS_R : 1];
@@ -255,7 +268,7 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
   ws_u32 rc = a.reset_count[e];
   float ep_ret = a.ep_ret[e];
   ws_u32 err = 0;
-  const bool hoist = kH == 0 && step_stride == 0;    /* same row every step: CDF and logs once */
+  const bool hoist = kH == 0 && step_stride == 0 && WS_C == 0;  /* same row every step: CDF and logs once */
   float p0[WS_N];
   WsRow row;
   if (hoist) {
@@ -278,7 +291,32 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
     const float u = ws_u01(w4[t & 3]);
     float lp;
     int act;
+#if WS_C > 0
+    /* continuous actions (R14): row = mean [WS_C] | log_std [WS_C] */
+    float cact[WS_C];
+    {
+      const float* row = probs + (ws_i64)c * step_stride + e * row_stride;
+      bool okr = true;
+      for (int k = 0; k < WS_C; ++k) okr = okr && isfinite(row[k]) && isfinite(row[WS_C + k]);
+      double lpd = 0.0;
+      for (int k = 0; k < WS_C; ++k) {
+        const float z = ws_gauss(a, eg, t * (ws_u64)WS_C + (ws_u64)k);
+        const float sd = (float)exp((double)row[WS_C + k]);
+        cact[k] = okr ? row[k] + sd * z : __int_as_float(0x7fc00000);
+        lpd = lpd + (((-0.5 * (double)z) * (double)z - (double)row[WS_C + k]) - 0.9189385332046727);
+        if (live) __stcs(reinterpret_cast<float*>(a.act) + idx * WS_C + k, cact[k]);
+      }
+      lp = okr ? (float)lpd : __int_as_float(0x7fc00000);
+      bool fin = true;
+      for (int k = 0; k < WS_C; ++k) fin = fin && isfinite(cact[k]);
+      act = fin ? 0 : -1;
+      if (live && !okr) err |= 2u;
+    }
+    if (true) {
+    } else if (kH > 0) {
+#else
     if (kH > 0) {
+#endif
       float lg[WS_N];
       for (int i = 0; i < WS_N; ++i) lg[i] = b2[i];
       float v = kCritic ? wv[kHH] : 0.0f;
@@ -304,7 +342,9 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
                   : ws_sample(probs + (ws_i64)c * step_stride + e * row_stride, u, &lp);
     }
     if (live) {
+#if WS_C == 0
       __stcs(a.act + idx, act);
+#endif
       if (a.write_logp) __stcs(a.logp + idx, lp);
     }
     float r = 0.0f;
@@ -312,9 +352,13 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
     float ret = 0.0f;
     ws_i32 es = 0;
     if (act < 0) {                                   /* R19: not advanced, rew 0, done 0 */
-      if (live) err |= 3u;
+      if (live) err |= (WS_C > 0 ? 1u : 3u);
     } else {
+#if WS_C > 0
+      const int term = ws_env_step(s, cact, &r, prm, a.shared);
+#else
       const int term = ws_env_step(s, act, &r, prm, a.shared);
+#endif
       es = ep_step + 1;
       d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
       ret = ep_ret + r;
@@ -376,6 +420,7 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
   ws_run<0, false>(a, T, t0, probs, row_stride, step_stride, 0, 0, 0);
 }
 
+#if WS_C == 0
 /* policy roll-outs: weights (R29, + R31 value head for the critic variants) staged in shared
    memory once per CTA */
 template <int kH, bool kCritic>
@@ -398,6 +443,7 @@ extern "C" __global__ void k_user_ac_32(const WsUserArgs a, int T, ws_u64 t0, co
 extern "C" __global__ void k_user_ac_64(const WsUserArgs a, int T, ws_u64 t0, const float* w, float* v, float* b) {
   ws_policy<64, true>(a, T, t0, w, v, b);
 }
+#endif
 )WS";
 
 // ------------------------------------------------------------------------------ registry
@@ -443,8 +489,9 @@ cudaError_t kernels_for(UserEnv* u, const UserEnv::Kernels** out) {
     const std::pair<cudaKernel_t*, const char*> names[] = {
         {&k.reset, "k_user_reset"},       {&k.rollout, "k_user_rollout"}, {&k.policy32, "k_user_policy_32"},
         {&k.policy64, "k_user_policy_64"}, {&k.ac32, "k_user_ac_32"},      {&k.ac64, "k_user_ac_64"}};
-    for (const auto& n : names)
-      if ((e = cudaLibraryGetKernel(n.first, k.lib, n.second))) return e;
+    const int n_req = u->def.act_dim > 0 ? 2 : 6;  // continuous envs carry no policy kernels
+    for (int i = 0; i < n_req; ++i)
+      if ((e = cudaLibraryGetKernel(names[i].first, k.lib, names[i].second))) return e;
     it = u->per_dev.emplace(dev, k).first;
   }
   *out = &it->second;
@@ -474,6 +521,7 @@ bool user_env_spec(const char* name, UserSpec* out) {
   out->state_dim = d.state_dim;
   out->max_steps = d.max_steps;
   out->n_params = d.n_params;
+  out->act_dim = d.act_dim;
   return true;
 }
 
@@ -520,8 +568,11 @@ extern "C" {
 
 ws_status ws_register_env(const ws_env_def* def, char* log, size_t log_size) {
   copy_log("", log, log_size);
+  const bool cont = def && def->act_dim != 0;
   if (!def || !def->name || !def->source || !*def->name || builtin(def->name) || def->state_dim < 1 ||
-      def->state_dim > 32 || def->obs_dim < 1 || def->obs_dim > 32 || def->n_actions < 2 || def->n_actions > 16 ||
+      def->state_dim > 32 || def->obs_dim < 1 || def->obs_dim > 32 ||
+      (cont ? (def->act_dim < 1 || def->act_dim > 8 || def->n_actions != 0)
+            : (def->n_actions < 2 || def->n_actions > 16)) ||
       def->n_reset_draws < 0 || def->n_reset_draws > 64 || def->max_steps < 1 || def->n_params < 0 ||
       def->n_params > 64) {
     copy_log("ws_register_env: name (not a built-in), source, state_dim 1..32, obs_dim 1..32, n_actions 2..16, "
@@ -547,9 +598,10 @@ ws_status ws_register_env(const ws_env_def* def, char* log, size_t log_size) {
   u->def.name = u->name.c_str();
   u->def.source = u->source.c_str();
   const std::string defs = "#define WS_S " + std::to_string(def->state_dim) + "\n#define WS_D " +
-                           std::to_string(def->obs_dim) + "\n#define WS_N " + std::to_string(def->n_actions) +
-                           "\n#define WS_R " + std::to_string(def->n_reset_draws) + "\n#define WS_P " +
-                           std::to_string(def->n_params) + "\n";
+                           std::to_string(def->obs_dim) + "\n#define WS_N " +
+                           std::to_string(def->act_dim > 0 ? 1 : def->n_actions) + "\n#define WS_R " +
+                           std::to_string(def->n_reset_draws) + "\n#define WS_P " + std::to_string(def->n_params) +
+                           "\n#define WS_C " + std::to_string(def->act_dim) + "\n";
   const std::string src = defs + kPrelude + u->source + "\n" + kEngine;
   nvrtcProgram prog;
   if (nv.create(&prog, src.c_str(), "ws_user_env.cu", 0, nullptr, nullptr) != NVRTC_SUCCESS) {

@@ -104,6 +104,7 @@ cudaError_t launch_peer_allreduce(const unsigned long long* local, int T, const 
 struct UserSpec {
   void* handle;  // registry entry
   int obs_dim, n_actions, state_dim, max_steps, n_params;
+  int act_dim;  // 0: discrete; > 0: continuous (n_actions 0)
 };
 struct UserLaunch {
   KArgs k;

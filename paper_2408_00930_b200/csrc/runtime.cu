@@ -40,7 +40,8 @@ bool lookup_env(const char* name, int A, int p0, EnvSpec* out) {
   if (n == "dummy") { *out = {ws::kDummy, 4, 2, 1, 0, 100}; return true; }
   ws::UserSpec u;
   if (ws::user_env_spec(name, &u)) {  // NEXT-N4: registered at run time (composer.cu)
-    *out = {ws::kUser, u.obs_dim, u.n_actions, 1, u.state_dim, u.max_steps, u.handle, u.n_params};
+    *out = {ws::kUser, u.obs_dim, u.n_actions, u.act_dim > 0 ? u.act_dim : 1, u.state_dim, u.max_steps, u.handle,
+            u.n_params};
     return true;
   }
   (void)A;

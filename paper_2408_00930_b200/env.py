@@ -341,7 +341,7 @@ class Env:
 
 
 def register_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions: int, n_reset_draws: int,
-                 max_steps: int, n_params: int = 0) -> str:
+                 max_steps: int, n_params: int = 0, act_dim: int = 0) -> str:
     """NEXT-N4: compile a C-source environment with NVRTC into the fused roll-out template
     (ws.h ws_register_env); afterwards Env(E, 1, name, ...) runs it.  Returns the NVRTC log;
     raises WSError (with the log) on a compile error.  Re-registering the same name with the
@@ -350,7 +350,7 @@ def register_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions
     if L.ws_registered_env(name.encode()):
         return ""
     d = _abi.ws_env_def(name.encode(), source.encode(), state_dim, obs_dim, n_actions, n_reset_draws, max_steps,
-                        n_params)
+                        n_params, act_dim)
     buf = C.create_string_buffer(1 << 16)
     st = L.ws_register_env(C.byref(d), buf, len(buf))
     log = buf.value.decode(errors="replace")

@@ -173,3 +173,32 @@ def test_noisy_pes_env_matches_oracle(P):
     st_g, st_o = g.stats_f64(T).cpu().numpy(), np.array(o.array("stats"))[:T]
     assert np.array_equal(st_g[:, [0, 2]], st_o[:, [0, 2]])
     np.testing.assert_allclose(st_g[:, [1, 3]], st_o[:, [1, 3]], rtol=1e-12, atol=E * 2.0 ** -32)
+
+
+def test_continuous_registered_env_equals_builtin(P):
+    """A continuous-action C-source env (act_dim 1): the NVRTC template's R14 Gaussian head and
+    the user's Pendulum reproduce the hand-written Pendulum kernels bit for bit (given rows and
+    per-step rows), and match the oracle's registered-env path."""
+    E, T = 700, 220
+    rows = W.gaussian_params(E, 1, 1, 0.3, -0.2)
+    for stride_rows in (rows, np.stack([W.gaussian_params(E, 1, 1, 0.1 * t, -0.3) for t in range(T)])):
+        step_stride = 0 if stride_rows.ndim == 3 else E * 2
+        tr = torch.from_numpy(np.ascontiguousarray(stride_rows)).cuda()
+        a = P.Env(E, 1, "pendulum", SEED, t_capacity=T)
+        b = P.Env(E, 1, "u_pendulum", SEED, t_capacity=T)
+        a.rollout(T, tr, row_stride=2, step_stride=step_stride)
+        b.rollout(T, tr, row_stride=2, step_stride=step_stride)
+        assert a.status() == 0 and b.status() == 0
+        A = {k: v.cpu().numpy() for k, v in a.buffers().items() if v is not None}
+        B = {k: v.cpu().numpy() for k, v in b.buffers().items() if v is not None}
+        for k in ("obs", "act", "rew", "done", "state", "obs_live", "reset_count"):
+            assert np.array_equal(A[k], B[k]), k
+        la, lb = A["logp"].ravel(), B["logp"].ravel()
+        assert np.all(np.abs(la.view(np.int32).astype(np.int64) - lb.view(np.int32).astype(np.int64)) <= 2)
+    o = O.Batch("u_pendulum", E, 1, SEED, t_capacity=T)
+    assert o.rollout(T, rows) == 0
+    g = P.Env(E, 1, "u_pendulum", SEED, t_capacity=T)
+    g.rollout(T, torch.from_numpy(rows).cuda())
+    buf = {k: v.cpu().numpy() for k, v in g.buffers().items() if v is not None}
+    for k in ("obs", "act", "rew", "done"):
+        assert np.array_equal(buf[k][:T], o.array(k)[:T]), k

@@ -104,3 +104,15 @@ def test_noisy_mueller_brown_surface():
     iy = np.clip(np.floor((y + np.float32(0.5)) * np.float32(32 / 2.5)).astype(int), 0, 31)
     np.testing.assert_allclose(o2.array("obs")[0, :, 0, 2] - o.array("obs")[0, :, 0, 2], grid[iy * 32 + ix],
                                rtol=1e-5, atol=1e-4)
+
+
+def test_user_pendulum_continuous_equals_builtin():
+    """A continuous-action registered env (act_dim 1, R14 Gaussian head): Pendulum written as
+    user C source reproduces the pinned built-in oracle Pendulum roll-out bit for bit."""
+    E, T = 48, 250
+    rows = W.gaussian_params(E, 1, 1, 0.3, -0.2)
+    a = O.Batch("pendulum", E, 1, SEED, t_capacity=T)
+    b = O.Batch("u_pendulum", E, 1, SEED, t_capacity=T)
+    assert a.rollout(T, rows) == 0 and b.rollout(T, rows) == 0
+    for k in ("obs", "act", "logp", "rew", "done", "stats", "state", "obs_live", "reset_count"):
+        assert np.array_equal(a.array(k), b.array(k), equal_nan=True), k

@@ -156,5 +156,35 @@ def mbgrid_data(E: int, seed: int = 0x24080930, noise: float = 5.0):
     return prm, grid
 
 
+PENDULUM = dict(state_dim=2, obs_dim=3, n_actions=0, n_reset_draws=2, max_steps=200, n_params=0, act_dim=1)
+PENDULUM_SRC = r"""
+/* gymnasium Pendulum-v1 in the built-in env's operation order: a continuous-action user env */
+WS_FN void ws_env_init(float *s, const float *u, const float *prm, const float *shared) {
+  s[0] = -(float)3.14159265358979323846 + (float)(2 * 3.14159265358979323846) * u[0];
+  s[1] = -1.0f + 2.0f * u[1];
+}
+WS_FN void ws_env_obs(const float *s, float *o, const float *prm, const float *shared) {
+  o[0] = ws_cos(s[0]);
+  o[1] = ws_sin(s[0]);
+  o[2] = s[1];
+}
+WS_FN int ws_env_step(float *s, const float *a, float *r, const float *prm, const float *shared) {
+  const float pi = (float)3.14159265358979323846, two_pi = (float)(2 * 3.14159265358979323846);
+  const float th = s[0], thdot = s[1];
+  const float u = ws_clip(a[0], -2.0f, 2.0f);
+  float an = ws_fmod(th + pi, two_pi);
+  if (an != 0.0f && an < 0.0f) an = an + two_pi;
+  an = an - pi;
+  const float costs = an * an + 0.1f * (thdot * thdot) + 0.001f * (u * u);
+  float newthdot = thdot + (3.0f * 10.0f / (2.0f * 1.0f) * ws_sin(th) + 3.0f / (1.0f * (1.0f * 1.0f)) * u) * 0.05f;
+  newthdot = ws_clip(newthdot, -8.0f, 8.0f);
+  s[0] = th + newthdot * 0.05f;
+  s[1] = newthdot;
+  *r = -costs;
+  return 0;
+}
+"""
+
 ENVS = {"u_cartpole": (CARTPOLE_SRC, CARTPOLE), "u_mountaincar": (MOUNTAINCAR_SRC, MOUNTAINCAR),
-        "u_pointmass": (POINTMASS_SRC, POINTMASS), "u_mbgrid": (MBGRID_SRC, MBGRID)}
+        "u_pointmass": (POINTMASS_SRC, POINTMASS), "u_mbgrid": (MBGRID_SRC, MBGRID),
+        "u_pendulum": (PENDULUM_SRC, PENDULUM)}
