@@ -276,6 +276,7 @@ static inline float ws_clip(float x, float lo, float hi) { return x < lo ? lo : 
 static inline float ws_abs(float x) { return std::fabs(x); }
 static inline float ws_floor(float x) { return std::floor(x); }
 static inline float ws_fmod(float x, float y) { return std::fmod(x, y); }
+static inline void ws_sincos(float x, float* s, float* c) { *s = (float)std::sin((double)x); *c = (float)std::cos((double)x); }
 #line 1 "user_env.c"
 """
 _USER_EPILOGUE = r"""

@@ -116,6 +116,13 @@ WS_FN float ws_clip(float x, float lo, float hi) { return x < lo ? lo : (hi < x 
 WS_FN float ws_abs(float x) { return fabsf(x); }
 WS_FN float ws_floor(float x) { return floorf(x); }
 WS_FN float ws_fmod(float x, float y) { return fmodf(x, y); }
+/* both with one fp64 range reduction, each rounded once (R3) */
+WS_FN void ws_sincos(float x, float *s, float *c) {
+  double sd, cd;
+  sincos((double)x, &sd, &cd);
+  *s = (float)sd;
+  *c = (float)cd;
+}
 #line 1 "user_env.c"
 )WS";
 

@@ -348,6 +348,9 @@ def register_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions
     same source is a no-op."""
     L = lib()
     if L.ws_registered_env(name.encode()):
+        if _REGISTERED.get(name, (source, state_dim, obs_dim, n_actions, act_dim)) != \
+                (source, state_dim, obs_dim, n_actions, act_dim):
+            raise WSError(_abi.INVALID_ARGUMENT, f"env {name!r} is already registered with a different definition")
         return ""
     d = _abi.ws_env_def(name.encode(), source.encode(), state_dim, obs_dim, n_actions, n_reset_draws, max_steps,
                         n_params, act_dim)
@@ -356,7 +359,11 @@ def register_env(name: str, source: str, state_dim: int, obs_dim: int, n_actions
     log = buf.value.decode(errors="replace")
     if st != _abi.OK:
         raise WSError(st, log)
+    _REGISTERED[name] = (source, state_dim, obs_dim, n_actions, act_dim)
     return log
+
+
+_REGISTERED: dict = {}
 
 
 def _numel(shape) -> int:

@@ -31,7 +31,8 @@ WS_FN int ws_env_step(float *s, int a, float *r, const float *prm, const float *
   const float theta_threshold = (float)(12 * 2 * 3.14159265358979323846 / 360);
   const float x = s[0], x_dot = s[1], theta = s[2], theta_dot = s[3];
   const float force = (a == 1) ? 10.0f : -10.0f;
-  const float costheta = ws_cos(theta), sintheta = ws_sin(theta);
+  float costheta, sintheta;
+  ws_sincos(theta, &sintheta, &costheta);
   const float temp = (force + polemass_length * (theta_dot * theta_dot) * sintheta) / total_mass;
   const float thetaacc = (9.8f * sintheta - costheta * temp) /
                          (0.5f * ((float)(4.0 / 3.0) - 0.1f * (costheta * costheta) / total_mass));
