@@ -118,6 +118,14 @@ _SIGS = {
     "ws_registered_env": (C.c_int32, [C.c_char_p]),
     "ws_set_env_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ws_set_time": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "ws_pgroup_create": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(ws_ipc_handle)]),
+    "ws_pgroup_attach": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),
+    "ws_pgroup_destroy": (C.c_int, [C.c_void_p]),
+    "ws_pgroup_status": (C.c_int, [C.c_void_p]),
+    "ws_pgroup_allreduce": (C.c_int, [C.c_void_p, C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
+    "ws_pgroup_allreduce_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32,
+                                           C.c_float, C.c_float, C.c_float, C.c_float, C.c_float, C.c_void_p,
+                                           C.c_void_p, C.c_void_p]),
     "ws_get_buffers": (C.c_int, [C.c_void_p, C.POINTER(ws_buffers)]),
     "ws_get_info": (C.c_int, [C.c_void_p, C.POINTER(ws_info)]),
     "ws_synchronize": (C.c_int, [C.c_void_p]),

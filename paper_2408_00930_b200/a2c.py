@@ -134,7 +134,8 @@ class A2C:
     def __init__(self, env: Env, hidden: int = 64, *, lr: float = 1e-3, gamma: float = 0.99, lam: float = 0.95,
                  c_v: float = 0.5, c_e: float = 0.01, max_norm: float = 0.5, beta1: float = 0.9,
                  beta2: float = 0.999, eps: float = 1e-8, seed: int = 0, params: Optional[torch.Tensor] = None,
-                 group: Optional[dist.ProcessGroup] = None, bootstrap_truncation: bool = True):
+                 group: Optional[dist.ProcessGroup] = None, bootstrap_truncation: bool = True,
+                 peer="auto"):
         info = env.info()
         self.gaussian = int(info.n_actions) == 0  # continuous actions: Gaussian head (R34 / R35)
         self.A = int(info.n_agents)  # multi-agent (tag): every agent is a row; rolled out by a torch policy
@@ -165,6 +166,23 @@ class A2C:
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.step = 0
         self._values = None
+        # peer=True (world > 1): moments and gradient reduced over CUDA-IPC peer memory, the
+        # gradient all-reduce fused with clip + Adam in one kernel (ws_pgroup_*), no NCCL
+        # ("auto": use it when CUDA IPC works on every rank, else torch.distributed / NCCL)
+        self._pg_mom = self._pg_grad = None
+        if peer and self.world > 1:
+            from .parallel import PeerGroup
+            try:
+                self._pg_mom = PeerGroup(2, group)
+                self._pg_grad = PeerGroup(self.P, group)
+                self._mom_sum = torch.zeros(2, dtype=torch.float64, device=dev)
+            except RuntimeError:
+                if peer != "auto":
+                    raise
+                for g in (self._pg_mom, self._pg_grad):
+                    if g is not None:
+                        g.close()
+                self._pg_mom = self._pg_grad = None
         # truncated episodes bootstrap from V(post-step state) written by the roll-out kernel
         # (GAE's v_trunc, R30); registered envs treat truncation as termination (R31)
         self.bootstrap_truncation = bootstrap_truncation and env.env in ("cartpole", "acrobot", "dummy",
@@ -202,7 +220,11 @@ class A2C:
         adv, ret = env.gae_store(T, self._values.view(T, self.E // self.A, self.A),
                                  self.bootstrap.view(self.E // self.A, self.A), hp["gamma"], hp["lam"], v_trunc=vtr)
         moments(adv.view(-1), self.ws, out=self.mom, stream=s)
-        self._allreduce(self.mom)
+        if self._pg_mom is not None:
+            self._pg_mom.allreduce(self.mom, self._mom_sum, stream=s)
+            self.mom.copy_(self._mom_sum)
+        else:
+            self._allreduce(self.mom)
         self._adv = adv  # alive until the stream consumed it
         return obs, act, adv.view(-1), ret.view(-1), rows
 
@@ -212,8 +234,13 @@ class A2C:
         a2c_grad(self.params, obs, act, adv, ret, self.mom, float(rows * self.world), self.D, self.H, self.N,
                  hp["c_v"], hp["c_e"], self.ws, grad=self.grad, loss=self.loss, stream=s, logp_old=logp_old,
                  clip_eps=clip_eps, norm_batch=float(norm_rows * self.world))
-        self._allreduce(self.grad)
         self.step += 1
+        if self._pg_grad is not None:  # fused peer-memory all-reduce + clip + Adam (one kernel)
+            self._pg_grad.allreduce_adam(self.grad, self.params, self.m, self.v, self.step, hp["lr"], hp["beta1"],
+                                         hp["beta2"], hp["eps"], hp["max_norm"], grad_out=self.grad,
+                                         grad_norm=self.grad_norm, stream=s)
+            return
+        self._allreduce(self.grad)
         adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
              hp["max_norm"], grad_norm=self.grad_norm, stream=s)
 

@@ -79,3 +79,62 @@ def summarize(stats: torch.Tensor) -> dict:
     n = s[0]
     return {"episodes": n, "mean_return": s[1] / n if n else float("nan"),
             "mean_length": s[2] / n if n else float("nan"), "sum_reward": s[3]}
+
+
+class PeerGroup:
+    """Collective: a libws peer group (ws.h "peer groups") of `n` values across the ranks of
+    `group` on their current devices -- fp64 sums over CUDA-IPC peer memory, optionally fused
+    with the clip + Adam step.  Raises RuntimeError (on every rank) if IPC is unavailable."""
+
+    def __init__(self, n: int, group: Optional[dist.ProcessGroup] = None):
+        import ctypes as C
+        from . import _abi
+        from ._abi import lib
+        self._C, self._abi, self._lib = C, _abi, lib()
+        world, rank = dist.get_world_size(group), dist.get_rank(group)
+        h = _abi.ws_ipc_handle()
+        g = C.c_void_p()
+        st = self._lib.ws_pgroup_create(world, n, C.byref(g), C.byref(h))
+        blobs = [None] * world
+        dist.all_gather_object(blobs, (bytes(h.bytes), st), group=group)
+        if any(s != 0 for _, s in blobs):
+            if g:
+                self._lib.ws_pgroup_destroy(g)
+            raise RuntimeError("peer group: cudaIpc export failed on some rank")
+        arr = (_abi.ws_ipc_handle * world)()
+        for r, (b, _) in enumerate(blobs):
+            C.memmove(arr[r].bytes, b, 64)
+        st = self._lib.ws_pgroup_attach(g, rank, arr)
+        oks = [None] * world
+        dist.all_gather_object(oks, st == 0, group=group)
+        if not all(oks):
+            self._lib.ws_pgroup_destroy(g)
+            raise RuntimeError("peer group: cudaIpcOpenMemHandle failed on some rank")
+        dist.barrier(group)
+        self._g, self.n, self.world, self.rank = g, n, world, rank
+
+    def allreduce(self, x: torch.Tensor, out: torch.Tensor, stream=None):
+        """out (fp64) = sum over ranks of x (fp32 or fp64), identical on every rank."""
+        s = self._C.c_void_p((stream or torch.cuda.current_stream(x.device)).cuda_stream)
+        st = self._lib.ws_pgroup_allreduce(self._g, x.data_ptr(), 1 if x.dtype == torch.float32 else 0,
+                                           out.data_ptr(), s)
+        if st != 0:
+            raise RuntimeError(f"ws_pgroup_allreduce: {st}")
+
+    def allreduce_adam(self, grad, params, m, v, step, lr, beta1, beta2, eps, max_norm, grad_out=None,
+                       grad_norm=None, stream=None):
+        s = self._C.c_void_p((stream or torch.cuda.current_stream(grad.device)).cuda_stream)
+        st = self._lib.ws_pgroup_allreduce_adam(
+            self._g, grad.data_ptr(), params.data_ptr(), m.data_ptr(), v.data_ptr(), step, lr, beta1, beta2, eps,
+            max_norm, None if grad_out is None else grad_out.data_ptr(),
+            None if grad_norm is None else grad_norm.data_ptr(), s)
+        if st != 0:
+            raise RuntimeError(f"ws_pgroup_allreduce_adam: {st}")
+
+    def status(self) -> int:
+        return int(self._lib.ws_pgroup_status(self._g))
+
+    def close(self):
+        if getattr(self, "_g", None):
+            self._lib.ws_pgroup_destroy(self._g)
+            self._g = None

@@ -20,20 +20,22 @@ from paper_2408_00930_b200.parallel import shard  # noqa: E402
 
 def main():
     out, E_g, T, iters = sys.argv[1], int(sys.argv[2]), int(sys.argv[3]), int(sys.argv[4])
+    peer = len(sys.argv) > 5 and sys.argv[5] == "peer"
     dist.init_process_group("gloo")
     rank, world = dist.get_rank(), dist.get_world_size()
     torch.cuda.set_device(0)
     off, n = shard(E_g, world, rank)
     env = Env(n, 1, "cartpole", W.SEED, env_offset=off, n_envs_global=E_g, t_capacity=T)
     params = torch.from_numpy(W.a2c_params(4, 64, 2, seed=71))
-    tr = A2C(env, 64, params=params, lr=1e-3)
+    tr = A2C(env, 64, params=params, lr=1e-3, peer=peer)  # peer=False: the torch.distributed path
+    assert (tr._pg_grad is not None) == peer
     grads = []
     for _ in range(iters):
         tr.iteration(T)
         torch.cuda.synchronize()
         grads.append(tr.grad.cpu().numpy().copy())
     np.savez(os.path.join(out, f"rank{rank}.npz"), grad0=grads[0], params=tr.params.cpu().numpy(),
-             mom=tr.mom.cpu().numpy())
+             mom=tr.mom.cpu().numpy(), peer_status=(tr._pg_grad.status() if peer else 0))
     dist.barrier()
     dist.destroy_process_group()
 
