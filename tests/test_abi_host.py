@@ -203,3 +203,18 @@ def test_param_checkpoint_round_trip_without_gpu(tmp_path):
     with pytest.raises(ValueError):
         ck.load_params(f)
     assert P.lib().ws_set_time(None, 5) == _abi.INVALID_ARGUMENT
+
+
+def test_peer_group_argument_validation_without_gpu():
+    """ws.h peer groups reject bad arguments before any CUDA call."""
+    L = P.lib()
+    h = _abi.ws_ipc_handle()
+    g = C.c_void_p()
+    for world, n in ((0, 10), (9, 10), (2, 0), (2, 70000)):
+        assert L.ws_pgroup_create(world, n, C.byref(g), C.byref(h)) == _abi.INVALID_ARGUMENT
+    assert L.ws_pgroup_attach(None, 0, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_pgroup_allreduce(None, None, 1, None, None) == _abi.INVALID_ARGUMENT
+    assert L.ws_pgroup_allreduce_adam(None, None, None, None, None, 1, 1e-3, 0.9, 0.999, 1e-8, 0.5, None, None,
+                                      None) == _abi.INVALID_ARGUMENT
+    assert L.ws_pgroup_status(None) == _abi.INVALID_ARGUMENT
+    assert L.ws_pgroup_destroy(None) == _abi.OK
