@@ -2109,7 +2109,7 @@ static cudaError_t tag_policy_launch(const KArgs& a, const Launch& l, int T, uin
   if (b > 128) return cudaErrorInvalidValue;  // up to 128 agents per replica (launch bounds of the policy build)
   const size_t smem = tag_smem(a, b) + (size_t)(4 * hidden + hidden + hidden * kTagN + kTagN + hidden + 1) * 4;
 #define WS_TAG_POL(HH, C)                                                                                   \
-  k_tag<128, 1, false, HH, C><<<(unsigned)a.E, b, smem, l.stream>>>(a, kTagRollout, T, t0, 0, nullptr, 0, 0, weights, \
+  k_tag<128, 4, false, HH, C><<<(unsigned)a.E, b, smem, l.stream>>>(a, kTagRollout, T, t0, 0, nullptr, 0, 0, weights, \
                                                                   values, bootstrap)
   if (values) {
     if (hidden == 32) WS_TAG_POL(32, true); else WS_TAG_POL(64, true);
