@@ -68,6 +68,7 @@ def parse():
     ap.add_argument("--warmup", type=int, default=5)
     ap.add_argument("--impl", default="ours", choices=["ours", "reference"])
     ap.add_argument("--workload", default="C2")
+    ap.add_argument("--csv", default=None, help="also append one row to this CSV (SURVEY 5 bench CSV)")
     ap.add_argument("--block", type=int, default=0)
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: no clocks / cpu baseline / e2e")
@@ -274,6 +275,23 @@ def run_reference(args, w):
                              "sample": f"{w.n_envs} replicas x {T_s} steps per step"},
             "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
+
+
+def write_csv_row(path, w, world, E_g, A, T, line):
+    """SURVEY 5 bench CSV: env,E,A,T,gpus,env_steps_per_s,agent_steps_per_s,kernel,achieved,unit,
+    roofline_frac,oracle_steps_per_s,oracle_cores (header written for a new file)."""
+    import csv
+    r = line["roofline"]
+    cb = line.get("cpu_baseline") or {}
+    row = [w.env, E_g, A, T, world, line["value"], line["value"] * A, r.get("kernel"), r.get("achieved"),
+           r.get("unit"), r.get("frac"), cb.get("value"), cb.get("cores")]
+    new = not os.path.exists(path)
+    with open(path, "a", newline="") as f:
+        wr = csv.writer(f)
+        if new:
+            wr.writerow(["env", "E", "A", "T", "gpus", "env_steps_per_s", "agent_steps_per_s", "kernel", "achieved",
+                         "unit", "roofline_frac", "oracle_steps_per_s", "oracle_cores"])
+        wr.writerow(row)
 
 
 def main():
@@ -607,6 +625,8 @@ def main():
         if not args.no_cpu_baseline and not args.ncu and world == 1:
             line["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(line), flush=True)
+        if args.csv:
+            write_csv_row(args.csv, w, world, E_g, A, T, line)
     env.close()
     if world > 1:
         dist.barrier()
