@@ -218,3 +218,21 @@ def test_peer_group_argument_validation_without_gpu():
                                       None) == _abi.INVALID_ARGUMENT
     assert L.ws_pgroup_status(None) == _abi.INVALID_ARGUMENT
     assert L.ws_pgroup_destroy(None) == _abi.OK
+
+
+def test_bench_csv_row(tmp_path):
+    """bench.py --csv (SURVEY 5 bench CSV): header once, one row per run."""
+    import importlib.util
+    import os
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    import wsinputs as W
+    line = {"value": 2.0e10, "roofline": {"kernel": "k", "achieved": 1.0, "unit": "GB/s", "frac": 0.5},
+            "cpu_baseline": {"value": 1.0e8, "cores": 16}}
+    f = str(tmp_path / "b.csv")
+    bench.write_csv_row(f, W.CONFIGS["C4"], 2, 2000, 100, 200, line)
+    bench.write_csv_row(f, W.CONFIGS["C4"], 2, 2000, 100, 200, line)
+    rows = open(f).read().strip().split("\n")
+    assert rows[0].startswith("env,E,A,T,gpus") and len(rows) == 3
+    assert rows[1].split(",")[:7] == ["tag", "2000", "100", "200", "2", "20000000000.0", "2000000000000.0"]
