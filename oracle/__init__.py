@@ -49,6 +49,7 @@ def lib():
             "wso_draw": (U32, [U64, U64, U32, U32, U64]),
             "wso_u01": (F, [U32]),
             "wso_gauss": (F, [U64, U64, U32, U64, I, I]),
+            "wso_box_muller": (F, [U32, U32, I]),
             "wso_sample_discrete": (I, [P, I, F, P, P, P]),
             "wso_sample_grid": (I64, [P, I, P]),
             "wso_sincos_f32": (None, [P, I64, P, P]),
@@ -110,6 +111,11 @@ def draw(seed: int, env_global: int, agent: int, purpose: int, j: int) -> int:
 
 def u01(w: int) -> float:
     return float(lib().wso_u01(w))
+
+
+def box_muller(wa: int, wb: int, odd: int) -> float:
+    """Box-Muller on the word pair (wa, wb): the cos (odd = 0) or sin (odd = 1) normal."""
+    return float(lib().wso_box_muller(wa, wb, odd))
 
 
 def gauss(seed: int, env_global: int, agent: int, t: int, d: int, k: int) -> float:

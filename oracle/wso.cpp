@@ -374,6 +374,18 @@ int sample_discrete(const float* p, int n, float u, int32_t* act, float* logp, i
   return 0;
 }
 
+/* Box-Muller on one word pair (reading Q14): u1 = ((wa >> 8) + 1) 2^-24 in (0, 1] (so the log is
+ * finite), u2 = (wb >> 8) 2^-24 in [0, 1); z = sqrt(-2 ln u1) cos(2 pi u2) for the even draw of the
+ * pair, sqrt(-2 ln u1) sin(2 pi u2) for the odd one; fp64, rounded once (reading Q3).
+ * Pinned by SURVEY App. A.8's worked value (tests/golden/box_muller.txt). */
+float box_muller(uint32_t wa, uint32_t wb, int odd) {
+  double u1 = (double)((wa >> 8) + 1) * (1.0 / 16777216.0);  // (0, 1]
+  double u2 = (double)(wb >> 8) * (1.0 / 16777216.0);        // [0, 1)
+  double r = std::sqrt(-2.0 * std::log(u1));
+  double ang = 2.0 * kPi * u2;
+  return (float)(odd ? r * std::sin(ang) : r * std::cos(ang));
+}
+
 /* Gaussian draw k of agent a at step t (reading Q14/Q15): j = t*d + k, Box-Muller on the
  * word pair (2p, 2p+1), p = (j & 3) >> 1; even j -> cos branch, odd j -> sin branch. */
 float gauss(uint64_t seed, uint64_t e_g, uint32_t agent, uint64_t t, int d, int k) {
@@ -383,11 +395,7 @@ float gauss(uint64_t seed, uint64_t e_g, uint32_t agent, uint64_t t, int d, int 
   uint32_t w[4];
   philox4x32_10(ctr, key, w);
   int p = (int)((j & 3) >> 1);
-  double u1 = (double)((w[2 * p] >> 8) + 1) * (1.0 / 16777216.0);  // (0, 1]
-  double u2 = (double)(w[2 * p + 1] >> 8) * (1.0 / 16777216.0);     // [0, 1)
-  double r = std::sqrt(-2.0 * std::log(u1));
-  double ang = 2.0 * kPi * u2;
-  return (float)((j & 1) ? r * std::sin(ang) : r * std::cos(ang));
+  return box_muller(w[2 * p], w[2 * p + 1], (int)(j & 1));
 }
 
 /* ------------------------------------------------------------------------------------
@@ -815,6 +823,7 @@ uint32_t wso_draw(uint64_t seed, uint64_t env_global, uint32_t agent, uint32_t p
   return draw(seed, env_global, agent, purpose, j);
 }
 float wso_u01(uint32_t w) { return u01(w); }
+float wso_box_muller(uint32_t wa, uint32_t wb, int odd) { return box_muller(wa, wb, odd); }
 float wso_gauss(uint64_t seed, uint64_t e_g, uint32_t agent, uint64_t t, int d, int k) {
   return gauss(seed, e_g, agent, t, d, k);
 }

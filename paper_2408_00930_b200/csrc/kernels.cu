@@ -701,6 +701,10 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
   R.aux_nxt = L::aux_of(R.nxt);
   R.stale = false;
 
+  // Fast path: one look-ahead reset refill per 8-step trip needs every episode that starts at a
+  // reset to last >= 8 steps -- proven for CartPole over the whole R11 reset box and all action
+  // sequences by interval arithmetic (tests/test_oracle_envs.py::
+  // test_cartpole_min_episode_proof_over_reset_box); truncation needs max_steps >= 8.
   const bool fast = L::kMinEpisode >= 8 && R.max_steps >= 8 && __all_sync(kFull, L::fast_ok(R.s));
   if (fast) R.template run<true>(); else R.template run<false>();
 

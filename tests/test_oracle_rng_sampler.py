@@ -188,3 +188,40 @@ def test_gaussian_logp_matches_library_density(oracle):
     want = stats.norm.logpdf(act, loc=prm[:, 0, 0], scale=np.exp(prm[:, 0, 1].astype(np.float64)))
     np.testing.assert_allclose(lp, want, rtol=2e-6, atol=2e-6)
     assert np.float32(-0.5 * math.log(2 * math.pi)) == np.float32(stats.norm.logpdf(0.0))
+
+
+def _golden_box_muller():
+    rows = []
+    with open(os.path.join(os.path.dirname(__file__), "golden", "box_muller.txt")) as f:
+        for line in f:
+            if line.strip() and not line.startswith("#"):
+                wa, wb, odd, z = line.split()
+                rows.append((int(wa, 16), int(wb, 16), int(odd), float(z)))
+    return rows
+
+
+def test_box_muller_worked_values(oracle):
+    """SURVEY App. A.8 worked value (Q14): the KAT words 6627e8d5, e169c58d give
+    z0 = 0.991137475 (cos branch) and z1 = -0.92466278 (sin branch).  A dropped +1 in u1,
+    swapped words or swapped cos / sin fail these rows; the w >> 8 = 0 row must stay finite."""
+    rows = _golden_box_muller()
+    assert len(rows) == 8
+    for wa, wb, odd, z in rows:
+        got = oracle.box_muller(wa, wb, odd)
+        assert math.isfinite(got)
+        assert abs(got - z) <= 2e-7 * max(1.0, abs(z)), (hex(wa), hex(wb), odd, got, z)
+
+
+def test_gauss_uses_the_q15_word_pair(oracle):
+    """gauss(seed, e, a, t, d, k): draw j = t d + k of the GAUSS stream (purpose 3) is the
+    Box-Muller of word pair p = (j & 3) >> 1 of Philox(ctr = (j >> 2, e, a, 3), seed), cos for
+    even j and sin for odd j (reading Q15).  Philox is the KAT / cuRAND-pinned oracle routine."""
+    seed = 0x0123456789ABCDEF
+    key = [seed & 0xFFFFFFFF, seed >> 32]
+    for (e, a, t, d) in [(0, 0, 0, 1), (7, 2, 5, 3), (123, 0, 41, 20), (5, 1, 1000, 2)]:
+        for k in range(d):
+            j = t * d + k
+            w = oracle.philox([j >> 2, e, a, 3], key)
+            p = (j & 3) >> 1
+            want = oracle.box_muller(int(w[2 * p]), int(w[2 * p + 1]), j & 1)
+            assert oracle.gauss(seed, e, a, t, d, k) == want
