@@ -73,8 +73,15 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--ncu", action="store_true", help="profiling mode: no clocks / cpu baseline / e2e")
     ap.add_argument("--dist-backend", default="nccl", help="process-group backend for N > 1 (gloo only for tests)")
-    ap.add_argument("--stats-reduce", default="p2p", choices=["p2p", "nccl"],
-                    help="N > 1: statistics all-reduce by libws's peer-memory kernel (default) or NCCL")
+    ap.add_argument("--stats-reduce", default="nccl", choices=["p2p", "nccl"],
+                    help="N > 1: statistics all-reduce by NCCL (default, north_star's design) or libws's "
+                         "peer-memory kernel (opt-in)")
+    ap.add_argument("--scaling", default="weak", choices=["weak", "strong"],
+                    help="weak: every rank runs the workload's full replica count (global = N x E); strong: the "
+                         "workload's E is the global count, split by parallel.shard.  At N > 1 the other mode is "
+                         "measured too and reported under `other_scaling`")
+    ap.add_argument("--sustain-s", type=float, default=1.0,
+                    help="after the K timed steps, a sustained pass of >= this many seconds (clock sampling, p10/p90)")
     ap.add_argument("--no-kernel-timing", action="store_true",
                     help="diagnostic: no per-kernel CUDA events in the timed region (roofline unavailable)")
     ap.add_argument("--same-device", action="store_true", help="all ranks on cuda:0 (multi-rank test on one GPU)")
@@ -209,33 +216,100 @@ def oracle_rollout(b, w, T, probs, cores):
     return st
 
 
-def cpu_baseline(w, budget_s: float = 10.0):
-    """The oracle as it stands (oracle/, never tuned for this), on this host's cores, on a
-    bounded sample of the same workload: consecutive whole-workload roll-outs (the bench's
-    steps) until ~budget_s of CPU work, or a prefix of one roll-out if one is longer."""
+def host_cpu() -> dict:
+    """CPU model and core counts of the host the oracle runs on (lscpu)."""
+    info = {"model": None, "sockets": None, "physical_cores": None, "logical_cpus": os.cpu_count(),
+            "affinity_cpus": len(os.sched_getaffinity(0))}
+    try:
+        out = subprocess.run(["lscpu"], capture_output=True, text=True, timeout=10).stdout
+        kv = {}
+        for line in out.splitlines():
+            if ":" in line:
+                k, v = line.split(":", 1)
+                kv[k.strip()] = v.strip()
+        info["model"] = kv.get("Model name")
+        sockets = int(kv.get("Socket(s)", "0") or 0)
+        cps = int(kv.get("Core(s) per socket", "0") or 0)
+        info["sockets"] = sockets or None
+        info["physical_cores"] = sockets * cps or None
+    except (OSError, ValueError, subprocess.SubprocessError):
+        pass
+    return info
+
+
+def _oracle_rate(w, budget_s: float, cores: int):
+    """Consecutive oracle roll-outs of workload w on `cores` threads for ~budget_s; returns
+    (env-steps/s, sample description, per-roll-out seconds)."""
     import oracle as O
-    cores = len(os.sched_getaffinity(0))
     probs = W.workload_probs(w)
-    register_user(w, oracle_side=True)
-    if w.params.get("gae"):
-        oracle_gae_inputs(w)
     b = O.Batch(w.env, w.n_envs, w.n_agents, W.SEED, t_capacity=w.T)
     t0 = time.perf_counter()
     oracle_rollout(b, w, min(10, w.T), probs, cores)
     probe = time.perf_counter() - t0
-    T_s = max(10, min(w.T, int(min(10, w.T) * budget_s / max(probe, 1e-6))))
-    steps, dt, n = 0, 0.0, 0
+    T_s = max(10, min(w.T, int(min(10, w.T) * budget_s / 3 / max(probe, 1e-6))))
+    steps, n, per = 0, 0, []
     t0 = time.perf_counter()
     while True:
+        t1 = time.perf_counter()
         oracle_rollout(b, w, T_s, probs, cores)
+        per.append(time.perf_counter() - t1)
         steps += w.n_envs * T_s
         n += 1
         dt = time.perf_counter() - t0
         if dt >= budget_s or n >= 1000:
             break
-    return {"value": steps / dt, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
-            "sample": f"{w.name} {w.env}: {n} x ({w.n_envs} replicas x {T_s} steps) = {steps} env-steps "
-                      f"in {dt:.1f} s on {cores} threads"}
+    return steps / dt, f"{n} x ({w.n_envs} replicas x {T_s} steps) = {steps} env-steps in {dt:.1f} s", per, \
+        w.n_envs * T_s
+
+
+def cpu_baseline(w, budget_s: float = 10.0, budget_w1_s: float = 6.0):
+    """The oracle as it stands (oracle/, never tuned for this), on this host's cores, on a
+    bounded sample of the same workload: consecutive roll-outs of every replica over a prefix
+    of T_s steps until ~budget_s of CPU work -- once with W = all host threads (the reported
+    value) and once with W = 1."""
+    cores = len(os.sched_getaffinity(0))
+    register_user(w, oracle_side=True)
+    if w.params.get("gae"):
+        oracle_gae_inputs(w)
+    v, sample, per, units = _oracle_rate(w, budget_s, cores)
+    v1, sample1, per1, units1 = _oracle_rate(w, budget_w1_s, 1)
+    pct = lambda xs, q: float(np.percentile(np.asarray(xs), q))
+    return {"value": v, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
+            "sample": f"{w.name} {w.env}: {sample} on {cores} threads",
+            "p10_p90": [units / pct(per, 90), units / pct(per, 10)],
+            "w1": {"value": v1, "cores": 1, "sample": sample1, "p10_p90": [units1 / pct(per1, 90), units1 / pct(per1, 10)]},
+            "host": host_cpu()}
+
+
+def shard_sizes(E_g: int, world: int) -> list:
+    """parallel.shard's contiguous balanced partition (restated: the reference arm must not
+    import the product package)."""
+    return [E_g * (r + 1) // world - E_g * r // world for r in range(world)]
+
+
+def layout(w, world: int, scaling: str):
+    """(E_global, [E per rank]) of workload w on `world` ranks."""
+    if scaling == "weak":
+        return w.n_envs * world, [w.n_envs] * world
+    return w.n_envs, shard_sizes(w.n_envs, world)
+
+
+def inputs_desc(w) -> str:
+    if W.workload_policy(w):
+        return f"in-kernel MLP policy (hidden {w.params['policy_hidden']}), seeded weights"
+    if w.n_actions:
+        return f"uniform 1/{w.n_actions} probabilities, resident in HBM, step_stride 0"
+    return "Gaussian head (mean, log_std) per replica, resident in HBM, step_stride 0"
+
+
+def make_config(w, world: int, scaling: str, reduce: str) -> dict:
+    """The `config` object -- identical for both arms (the driver compares them)."""
+    E_g, per = layout(w, world, scaling)
+    par = "1 GPU" if world == 1 else (
+        f"{world} GPUs: contiguous replica shards (parallel.shard) + one sum all-reduce of the [T,4] statistics per "
+        f"roll-out ({'NCCL' if reduce == 'nccl' else 'libws peer-memory kernel over CUDA IPC'})")
+    return {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs_global": E_g, "n_envs_per_rank": per,
+            "n_agents": w.n_agents, "T": w.T, "inputs": inputs_desc(w), "scaling": scaling, "parallelism": par}
 
 
 def run_reference(args, w):
@@ -267,12 +341,12 @@ def run_reference(args, w):
     value = w.n_envs * T_s * args.steps / tot
     line = {"metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": args.gpus, "steps": args.steps,
             "warmup": args.warmup, "ms_per_step": 1e3 * tot / args.steps, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "impl": "reference",
-            "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs": w.n_envs, "T": w.T,
-                       "sample_T_per_step": T_s, "device": f"host CPU, {cores} threads (oracle/)"},
+            "config": make_config(w, args.gpus, args.scaling, args.stats_reduce),
             "cpu_baseline": {"value": value, "unit": "env-steps/s", "cores": cores, "kind": "oracle",
-                             "sample": f"{w.n_envs} replicas x {T_s} steps per step"},
+                             "sample": f"{w.n_envs} replicas x {T_s} of the {w.T} steps per step, on {cores} host "
+                                       f"threads (oracle/); rank 0 only", "host": host_cpu()},
             "e2e": {"value": value, "unit": "env-steps/s", "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
     print(json.dumps(line), flush=True)
 
@@ -294,178 +368,150 @@ def write_csv_row(path, w, world, E_g, A, T, line):
         wr.writerow(row)
 
 
-def main():
-    args = parse()
-    w = W.CONFIGS[args.workload]
-    if args.impl == "reference":
-        return run_reference(args, w)
+L2_BYTES = 126 * 2 ** 20  # B200 L2 (B200_PROFILING.md)
 
-    import torch
-    import torch.distributed as dist
 
-    from paper_2408_00930_b200 import Env
-    from paper_2408_00930_b200.parallel import allreduce_stats
+def issue_table() -> dict:
+    """Per-workload ncu counters of the dominant kernel (profiles/ncu_inst.json, written from
+    `ncu --set full` captures): warp instructions executed per launch, issue-active %, DRAM bytes."""
+    try:
+        with open(os.path.join(ROOT, "profiles", "ncu_inst.json")) as f:
+            return json.load(f)
+    except (OSError, ValueError):
+        return {}
 
-    world, rank, local = dist_env()
-    if world != args.gpus and rank == 0:
-        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
-    local_dev = 0 if args.same_device else local
-    torch.cuda.set_device(local_dev)
-    dev = torch.device("cuda", local_dev)
-    if world > 1:
-        if args.dist_backend == "nccl":
-            dist.init_process_group("nccl", device_id=dev)
-        else:
-            dist.init_process_group(args.dist_backend)
 
-    # weak scaling: each rank owns a full C2-sized shard of a world*E global batch
-    E, A, T = w.n_envs, w.n_agents, w.T
-    E_g = E * world
-    offset = rank * E
-    params = (w.params.get("grid", w.params.get("dim", 0)), w.params.get("taggers", 0))
-    stream = torch.cuda.current_stream(dev)
-    register_user(w, oracle_side=False)
-    env = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
-              param0=params[0], param1=params[1], block_size=args.block)
-    probs_host = W.workload_probs(w)
-    probs = torch.from_numpy(probs_host).to(dev)
-    stats_view = env.buffers()["stats"][:T]
-    pol = W.workload_policy(w)  # NEXT-N1 workloads: actions from the in-kernel MLP policy
-    pol_w = torch.from_numpy(pol[1]).to(dev) if pol else None
-    gae = w.params.get("gae")   # NEXT-N2 workloads: GAE over the store after every roll-out
-    if gae:
-        g_vals, g_boot, _ = (torch.from_numpy(x).to(dev) if x is not None else None
-                             for x in W.gae_inputs(T, E, A, seed=W.SEED + rank))
-        g_out = (torch.empty((T, E, A), dtype=torch.float32, device=dev),
-                 torch.empty((T, E, A), dtype=torch.float32, device=dev))
+def pct(xs, q):
+    return float(np.percentile(np.asarray(xs, np.float64), q)) if len(xs) else None
 
-    trainer = None
-    if w.params.get("a2c"):  # NEXT-N2: every step is one A2C iteration (roll-out + update)
+
+class Run:
+    """One measured configuration (scaling mode) of workload w on this rank."""
+
+    def __init__(self, args, w, world, rank, dev, scaling):
+        import dataclasses
+        from paper_2408_00930_b200 import Env
+        self.args, self.world, self.rank, self.dev, self.scaling = args, world, rank, dev, scaling
+        self.E_g, per = layout(w, world, scaling)
+        self.E = per[rank]
+        self.offset = sum(per[:rank])
+        self.w = dataclasses.replace(w, n_envs=self.E)  # this rank's shard (inputs sized for it)
+        self.A, self.T = w.n_agents, w.T
+        self.params = (w.params.get("grid", w.params.get("dim", 0)), w.params.get("taggers", 0))
+        self.Env = Env
+        self.env = self.make_env()
+        self.stream = torch.cuda.current_stream(dev)
+        wl = self.w
+        self.probs_host = W.workload_probs(wl)
+        self.probs = torch.from_numpy(self.probs_host).to(dev)
+        self.stats_view = self.env.buffers()["stats"][:self.T]
+        self.pol = W.workload_policy(wl)
+        self.pol_w = torch.from_numpy(self.pol[1]).to(dev) if self.pol else None
+        self.gae = w.params.get("gae")
+        if self.gae:
+            self.g_vals, self.g_boot, _ = (torch.from_numpy(x).to(dev) if x is not None else None
+                                           for x in W.gae_inputs(self.T, self.E, self.A, seed=W.SEED + rank))
+            self.g_out = (torch.empty((self.T, self.E, self.A), dtype=torch.float32, device=dev),
+                          torch.empty((self.T, self.E, self.A), dtype=torch.float32, device=dev))
+        self.trainer = self.make_trainer(self.env) if w.params.get("a2c") else None
+        self.staged = w.params.get("staged")
+        self.staged_rep = {}
+        if self.staged:
+            self.st_probs = torch.from_numpy(self.probs_host).pin_memory()
+            self.st_dst = self.env.host_store(self.T)
+        self.p2p = False
+        if world > 1 and args.stats_reduce == "p2p":
+            from paper_2408_00930_b200.parallel import attach_peer_stats
+            self.p2p = attach_peer_stats(self.env)  # falls back to NCCL if CUDA IPC is unavailable on any rank
+
+    def make_env(self):
+        return self.Env(self.E, self.A, self.w.env, W.SEED, env_offset=self.offset, n_envs_global=self.E_g,
+                        t_capacity=self.T, param0=self.params[0], param1=self.params[1], block_size=self.args.block)
+
+    def make_trainer(self, env):
         from paper_2408_00930_b200.a2c import A2C, PPO
-        ppo = w.params.get("ppo")
-        trainer = (PPO(env, pol[0], params=pol_w, epochs=ppo[0], minibatches=ppo[1], lr=1e-4) if ppo else
-                   A2C(env, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5))
+        ppo = self.w.params.get("ppo")
+        pol = self.pol
+        return (PPO(env, pol[0], params=self.pol_w, epochs=ppo[0], minibatches=ppo[1], lr=1e-4) if ppo else
+                A2C(env, pol[0], params=self.pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01, max_norm=0.5))
 
-    staged = w.params.get("staged")  # NEXT-N3: copy-based baseline pipeline
-    staged_rep = {}
-    if staged:
-        st_probs = torch.from_numpy(probs_host).pin_memory()
-        st_dst = env.host_store(T)
-
-    def gpu_rollout(e_obj):
-        if staged and e_obj is env:
-            staged_rep.update(env.rollout_staged(T, st_probs, st_dst))
-        elif trainer is not None and e_obj is env:
-            trainer.iteration(T)
-        elif pol:
-            e_obj.rollout_policy(T, pol_w, pol[0])
+    def rollout(self):
+        env, T = self.env, self.T
+        if self.staged:
+            self.staged_rep.update(env.rollout_staged(T, self.st_probs, self.st_dst))
+        elif self.trainer is not None:
+            self.trainer.iteration(T)
+        elif self.pol:
+            env.rollout_policy(T, self.pol_w, self.pol[0])
         else:
-            e_obj.rollout(T, probs)
-        if gae:
-            e_obj.gae_store(T, g_vals, g_boot, gae[0], gae[1], out=g_out)
+            env.rollout(T, self.probs)
+        if self.gae:
+            env.gae_store(T, self.g_vals, self.g_boot, self.gae[0], self.gae[1], out=self.g_out)
 
-    p2p = False
-    if world > 1 and args.stats_reduce == "p2p":
-        from paper_2408_00930_b200.parallel import attach_peer_stats
-        p2p = attach_peer_stats(env)  # falls back to NCCL if CUDA IPC is unavailable on any rank
+    def step(self):
+        """One bench step: the whole hot path over the batch + (N > 1) the statistics all-reduce."""
+        self.rollout()
+        if self.world > 1 and not self.p2p:
+            from paper_2408_00930_b200.parallel import allreduce_stats
+            allreduce_stats(self.stats_view)
 
-    def merge_stats():
-        if not p2p:
-            allreduce_stats(stats_view)
-
-    def one_step():
-        gpu_rollout(env)
-        merge_stats()
-
-    for _ in range(max(args.warmup, 0)):
-        one_step()
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    if p2p:  # the peer-memory reduction must have worked on every rank, else fall back to NCCL
-        ok = torch.tensor([1 if env.status() == 0 else 0], dtype=torch.int32, device=dev)
-        dist.all_reduce(ok, op=dist.ReduceOp.MIN)
-        if int(ok.item()) == 0:
-            print("warning: peer-memory statistics reduction failed during warm-up; using NCCL", file=sys.stderr)
-            env.peer_detach()
-            env.reset()
-            p2p = False
-            for _ in range(max(args.warmup, 1)):
-                one_step()
-            torch.cuda.synchronize(dev)
+    def barrier(self):
+        torch.cuda.synchronize(self.dev)
+        if self.world > 1:
             dist.barrier()
 
-    clocks = Clocks(local_dev)
-    if not args.ncu:
-        clocks.start()
-        time.sleep(0.3)
-    # two CUDA events per step around the fused roll-out kernel only (libws ws_kernel_times):
-    # the dominant kernel is timed live with the least perturbation of the timed loop
-    env.enable_kernel_timing(0 if (args.no_kernel_timing or staged) else (3 if gae else 2))
-    env.kernel_times()
-    launches0 = env.info().launches
-    ev = [torch.cuda.Event(enable_timing=True) for _ in range(2)]
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    ev[0].record(stream)
-    for k in range(args.steps):
-        gpu_rollout(env)
-        merge_stats()
-    ev[1].record(stream)
-    torch.cuda.synchronize(dev)
-    if world > 1:
-        dist.barrier()
-    total_ms = ev[0].elapsed_time(ev[1])
-    st = env.status()  # sticky device errors (invalid rows, peer reduction timeout) fail the run
-    if st != 0:
-        raise RuntimeError(f"libws reported status {st} during the timed region")
-    launches = env.info().launches - launches0
-    if trainer is not None:  # handle-free kernels per step: moments + final, then (grad + final, Adam) per update
-        n_upd = (w.params["ppo"][0] * w.params["ppo"][1]) if w.params.get("ppo") else 1
-        launches += (2 + 3 * n_upd) * args.steps
-    ktimes = env.kernel_times()
-    env.enable_kernel_timing(False)
-    clk = clocks.stop() if not args.ncu else {}
+    def warm(self, n):
+        for _ in range(max(n, 0)):
+            self.step()
+        self.barrier()
+        if self.p2p:  # the peer-memory reduction must have worked on every rank, else fall back to NCCL
+            ok = torch.tensor([1 if self.env.status() == 0 else 0], dtype=torch.int32, device=self.dev)
+            dist.all_reduce(ok, op=dist.ReduceOp.MIN)
+            if int(ok.item()) == 0:
+                print("warning: peer-memory statistics reduction failed during warm-up; using NCCL", file=sys.stderr)
+                self.env.peer_detach()
+                self.env.reset()
+                self.p2p = False
+                for _ in range(max(n, 1)):
+                    self.step()
+                self.barrier()
 
-    # merged per-slot statistics of the last timed roll-out (all ranks, exact int64; R20)
-    from paper_2408_00930_b200.parallel import summarize
-    merged = summarize(stats_view.cpu())
+    def timed(self, K, flush):
+        """K steps timed with CUDA events on the handle's stream, one event per step boundary
+        (per-step times for p10 / p90).  flush: an L2 flush (a 256 MB write) before every step,
+        outside the events (stores smaller than L2)."""
+        ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1 if not flush else 2 * K)]
+        self.barrier()
+        if not flush:
+            ev[0].record(self.stream)
+            for k in range(K):
+                self.step()
+                ev[k + 1].record(self.stream)
+            self.barrier()
+            per = [ev[k].elapsed_time(ev[k + 1]) for k in range(K)]
+        else:
+            for k in range(K):
+                self.flush_buf.zero_()
+                ev[2 * k].record(self.stream)
+                self.step()
+                ev[2 * k + 1].record(self.stream)
+            self.barrier()
+            per = [ev[2 * k].elapsed_time(ev[2 * k + 1]) for k in range(K)]
+        return per
 
-    # diagnostic pass after the timed region (not part of `value`): every kernel and the whole
-    # ws_rollout call bracketed by events
-    n_diag = max(1, min(args.steps, 5))
-    env.enable_kernel_timing(1)
-    env.kernel_times()
-    dev_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_diag)]
-    for k in range(n_diag):
-        dev_ev[2 * k].record(stream)
-        gpu_rollout(env)
-        dev_ev[2 * k + 1].record(stream)
-    torch.cuda.synchronize(dev)
-    kern_ms = [dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)]
-    diag_times = env.kernel_times()
-    env.enable_kernel_timing(False)
-    upd_ms = None
-    if trainer is not None:  # the update alone (critic, GAE, moments, gradient, Adam)
-        for k in range(n_diag):
-            dev_ev[2 * k].record(stream)
-            trainer.update(T, values_ready=True)
-            dev_ev[2 * k + 1].record(stream)
-        torch.cuda.synchronize(dev)
-        upd_ms = sum(dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)) / n_diag
+    def max_over_ranks(self, x: float) -> float:
+        t = torch.tensor([x], dtype=torch.float64, device=self.dev)
+        if self.world > 1:
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        return float(t.item())
 
-    t = torch.tensor([total_ms], dtype=torch.float64, device=dev)
-    if world > 1:
-        dist.all_reduce(t, op=dist.ReduceOp.MAX)
-    max_ms = float(t.item())
-    value = E_g * T * args.steps / (max_ms / 1e3)
-    ms_per_step = max_ms / args.steps
+    def close(self):
+        self.env.close()
 
-    # Roofline of the dominant kernel (the fused roll-out kernel), timed live with CUDA
-    # events on the handle's stream over the timed region (ws_kernel_times).
-    peaks, peak_src = measured_peaks()
-    peak = float(peaks.get("hbm_gbs", 6650.0))
+
+def roofline_of(run, ktimes, diag_times, kern_ms, peak, peak_src, peaks, n_diag, upd_ms, w):
+    E, A, T = run.E, run.A, run.T
+    pol, gae, trainer, staged = run.pol, run.gae, run.trainer, run.staged
     n_roll, roll_ms = ktimes.get("rollout", (0, 0.0))
     n_plan, plan_ms = diag_times.get("plan", (0, 0.0))
     # tag samples inside its roll-out kernel: obs 16 + rew 4 + act 4 + logp 4 per agent-step, done 1 per env-step
@@ -476,12 +522,8 @@ def main():
         roll_bytes = int((4 * OBS_DIM[w.env] + 4 + 1 + 8) * E * A * T)
     achieved = roll_bytes / (roll_ms / 1e3) / 1e9 if roll_ms > 0 else 0.0
     call_ms = sum(kern_ms) / len(kern_ms)
-    all_bytes = int(roll_bytes + (PLAN_BYTES.get(w.env, 8) * E * A * T
-                                  if w.env not in ("tag",) and w.env not in USER_BYTES and not pol else 0))
-    # NEXT-N2: GAE reads rew + values and writes adv + returns (16 B per agent-step), reads
-    # the replica's done byte (1 B per replica-step) and the bootstrap row once
+    all_bytes = store_bytes(w, E)
     gae_bytes = 16 * E * A * T + E * T + 4 * E * A if gae else 0
-    all_bytes += gae_bytes
     roofline = {"bound": "hbm", "achieved": round(achieved, 1), "peak": peak, "unit": "GB/s",
                 "frac": round(achieved / peak, 4), "traffic": None,
                 "peak_source": f"{peak_src} hbm_gbs (copy, MEASURED_PEAKS.json)",
@@ -495,6 +537,27 @@ def main():
                 "ws_rollout_call": {"ms": round(call_ms, 4), "bytes": all_bytes,
                                     "achieved_GBps": round(all_bytes / (call_ms / 1e3) / 1e9, 1),
                                     "frac": round(all_bytes / (call_ms / 1e3) / 1e9 / peak, 4)}}
+    # issue view (report max(f_HBM, f_issue) and name the binding one): warp
+    # instructions the kernel executes per launch (ncu, profiles/ncu_inst.json, same workload and
+    # shape) / its live launch time, against 148 SMs x 4 schedulers x 1 warp-instruction / clock
+    tab = issue_table().get(w.name)
+    if tab and tab.get("E") == E and roll_ms > 0 and not pol and not staged:
+        clk = float(peaks.get("sm_max_mhz", 1965.0)) * 1e6
+        issue_peak = 148 * 4 * clk / 1e9  # G warp-instructions / s
+        ach_i = tab["inst_per_launch"] / (roll_ms / 1e3) / 1e9
+        roofline["issue_view"] = {"achieved": round(ach_i, 1), "peak": round(issue_peak, 1),
+                                  "unit": "G warp-inst/s", "frac": round(ach_i / issue_peak, 4),
+                                  "inst_per_launch": tab["inst_per_launch"],
+                                  "ncu_issue_active_pct": tab.get("issue_active_pct"),
+                                  "source": tab.get("source")}
+        if tab.get("dram_bytes") is not None:
+            roofline["traffic"] = tab["dram_bytes"]
+        if ach_i / issue_peak > roofline["frac"]:
+            hbm_view = {k: roofline[k] for k in ("achieved", "peak", "unit", "frac")}
+            roofline.update({"bound": "alu", "achieved": round(ach_i, 1), "peak": round(issue_peak, 1),
+                             "unit": "G warp-inst/s", "frac": round(ach_i / issue_peak, 4), "hbm_view": hbm_view,
+                             "peak_source": f"derived: 148 SMs x 4 SMSPs x 1 warp-instruction/clk x "
+                                            f"{clk / 1e6:.0f} MHz (MEASURED_PEAKS sm_max_mhz)"})
     if pol:
         # NEXT-N1: the MLP's fused multiply-adds per replica-step (D x H + H x n), against the
         # fp32 FMA peak from unit counts and clock: 148 SMs x 128 lanes x 2 flop x 1.965 GHz
@@ -514,16 +577,14 @@ def main():
             roofline.update({"bound": "alu", "achieved": round(tf, 3), "peak": round(fp32_peak, 1),
                              "unit": "TFLOP/s", "frac": round(tf / fp32_peak, 4), "hbm_view": hbm_view})
     if staged:
-        # the same kernels one step at a time (diagnostic pass timing of the step kernel) and
-        # the transfer split of the last timed step
         n_st, st_ms = diag_times.get("step", (0, 0.0))
         sb = ROLLOUT_BYTES.get(w.env, 0) * E * A
         ach = sb / (st_ms / 1e3) / 1e9 if st_ms > 0 else 0.0
         roofline.update({"kernel": f"k_step_lane<{w.env}> (single step)", "kernel_ms": round(st_ms, 5),
                          "launches_timed": n_st, "bytes_per_launch": sb, "achieved": round(ach, 1),
                          "frac": round(ach / peak, 4), "other_kernels": {}})
-        roofline["staged_pipeline"] = {k: (round(v, 4) if "ms" in k else v) for k, v in staged_rep.items()}
-        roofline["staged_pipeline"]["transfer_share"] = round(staged_rep["transfer_ms"] / staged_rep["total_ms"], 4)
+        roofline["staged_pipeline"] = {k: (round(v, 4) if "ms" in k else v) for k, v in run.staged_rep.items()}
+        roofline["staged_pipeline"]["transfer_share"] = round(run.staged_rep["transfer_ms"] / run.staged_rep["total_ms"], 4)
     if trainer is not None:
         roofline["a2c_update"] = {"ms": round(upd_ms, 4), "rows": E * A * T,
                                   "note": "gae + moments + gradient + clip/Adam (the critic comes from the roll-out kernel), diagnostic pass",
@@ -535,99 +596,257 @@ def main():
                                   "unit": "GB/s", "frac": round(g_ach / peak, 4), "kernel_ms": round(gae_ms, 4),
                                   "launches_timed": n_gae, "bytes_per_launch": gae_bytes,
                                   "bytes_per_agent_step": gae_bytes / (E * A * T)}
-    traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
-    if os.path.exists(traffic_file):
+    if roofline["traffic"] is None:
+        traffic_file = os.path.join(ROOT, "profiles", "traffic.json")
         try:
             tr = json.load(open(traffic_file)).get(w.name)
-            if tr:
+            if tr and run.world == 1:
                 roofline["traffic"] = tr
-        except Exception:
+        except (OSError, ValueError):
             pass
+    return roofline
 
-    line = None
-    if rank == 0:
-        e2e = None
-        if not args.ncu:
-            # end to end through the public API with HOST buffers: pinned probs H2D + stats D2H per step
-            henv = Env(E, A, w.env, W.SEED, env_offset=offset, n_envs_global=E_g, t_capacity=T,
-                       param0=params[0], param1=params[1], block_size=args.block)
-            if trainer is not None:  # NEXT-N2: one training iteration per step, loss + stats back to the host
-                from paper_2408_00930_b200.a2c import A2C, PPO
-                ppo = w.params.get("ppo")
-                htr = (PPO(henv, pol[0], params=pol_w, epochs=ppo[0], minibatches=ppo[1], lr=1e-4) if ppo else
-                       A2C(henv, pol[0], params=pol_w, lr=1e-4, gamma=0.99, lam=0.95, c_v=0.5, c_e=0.01,
-                           max_norm=0.5))
-                hl = torch.empty(3, dtype=torch.float64).pin_memory()
-                hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
 
-                def host_step():
-                    htr.iteration(T)
-                    hl.copy_(htr.loss, non_blocking=True)
-                    hs.copy_(henv.buffers()["stats"][:T], non_blocking=True)
-                    torch.cuda.synchronize(dev)
-                h2d = 0
-            elif staged:  # NEXT-N3: the staged pipeline is host-buffered by construction
-                hdst = henv.host_store(T)
+def store_bytes(w, E: int) -> int:
+    """Algorithmic bytes one step writes into (and reads from) the store on one rank."""
+    A, T = w.n_agents, w.T
+    if w.params.get("policy_hidden"):
+        b = (4 * OBS_DIM[w.env] + 4 + 1 + 8) * E * A * T
+    elif w.env == "tag":
+        b = (16 + 4 + 4 + 4) * E * A * T + E * T
+    elif w.env in USER_BYTES:
+        b = USER_BYTES[w.env] * E * A * T
+    else:
+        b = (ROLLOUT_BYTES.get(w.env, 0) + PLAN_BYTES.get(w.env, 8)) * E * A * T
+    if w.params.get("gae"):
+        b += 16 * E * A * T + E * T + 4 * E * A
+    return int(b)
 
-                def host_step():
-                    henv.rollout_staged(T, st_probs, hdst)
-                h2d = int(st_probs.numel() * 4 * T)
-            elif pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
-                hw = torch.from_numpy(pol[1]).pin_memory()
-                dw = torch.empty_like(hw, device=dev)
-                hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
 
-                def host_step():
-                    dw.copy_(hw, non_blocking=True)
-                    henv.rollout_policy(T, dw, pol[0])
-                    hs.copy_(henv.buffers()["stats"][:T], non_blocking=True)
-                    torch.cuda.synchronize(dev)
-                h2d = int(hw.numel() * 4)
+def e2e_pass(run, args, dev, world):
+    """End to end through the public API with HOST buffers, on every rank (the trainers'
+    collectives and the statistics all-reduce need all of them): per step the pinned-host
+    inputs go H2D and the step's result (statistics, loss) comes back D2H; host wall clock,
+    max over ranks."""
+    from paper_2408_00930_b200.parallel import allreduce_stats
+    w, T, E, A = run.w, run.T, run.E, run.A
+    henv = run.make_env()
+    hstats = henv.buffers()["stats"][:T]
+    trainer, staged, pol, gae = run.trainer, run.staged, run.pol, run.gae
+    if trainer is not None:  # NEXT-N2: one training iteration per step, loss + stats back to the host
+        htr = run.make_trainer(henv)
+        hl = torch.empty(3, dtype=torch.float64).pin_memory()
+        hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+
+        def host_step():
+            htr.iteration(T)
+            if world > 1:
+                allreduce_stats(hstats)
+            hl.copy_(htr.loss, non_blocking=True)
+            hs.copy_(hstats, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        h2d, d2h = 0, T * 4 * 8 + 24
+    elif staged:  # NEXT-N3: the staged pipeline is host-buffered by construction
+        hdst = henv.host_store(T)
+
+        def host_step():
+            henv.rollout_staged(T, run.st_probs, hdst)
+            if world > 1:
+                allreduce_stats(hstats)
+                torch.cuda.synchronize(dev)
+        h2d = int(run.st_probs.numel() * 4 * T)
+        d2h = int(sum(v.numel() * v.element_size() for v in hdst.values()))
+    elif pol:  # NEXT-N1: pinned host weights -> device each step, stats back to the host
+        hw = torch.from_numpy(pol[1]).pin_memory()
+        dw = torch.empty_like(hw, device=dev)
+        hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+
+        def host_step():
+            dw.copy_(hw, non_blocking=True)
+            henv.rollout_policy(T, dw, pol[0])
+            if world > 1:
+                allreduce_stats(hstats)
+            hs.copy_(hstats, non_blocking=True)
+            torch.cuda.synchronize(dev)
+        h2d, d2h = int(hw.numel() * 4), T * 4 * 8
+    else:
+        hp = torch.from_numpy(run.probs_host).pin_memory()
+        hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+
+        def host_step():
+            if world > 1:  # ws_rollout_host + the statistics all-reduce, then the merged slab to the host
+                henv.rollout_host(T, hp)
+                allreduce_stats(hstats)
+                hs.copy_(hstats, non_blocking=True)
+                torch.cuda.synchronize(dev)
             else:
-                hp = torch.from_numpy(probs_host).pin_memory()
+                henv.rollout_host(T, hp)
+            if gae:
+                henv.gae_store(T, run.g_vals, run.g_boot, gae[0], gae[1], out=run.g_out)
+                torch.cuda.synchronize(dev)
+        h2d, d2h = int(hp.numel() * 4), T * 4 * 8
+    for _ in range(max(args.warmup, 1)):
+        host_step()
+    run.barrier()
+    t0 = time.perf_counter()
+    for _ in range(args.steps):
+        host_step()
+    e2e_s = time.perf_counter() - t0
+    e2e_s = run.max_over_ranks(e2e_s)
+    henv.close()
+    return {"value": run.E_g * T * args.steps / e2e_s, "unit": "env-steps/s",
+            "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
+            "note": ("every rank, " if world > 1 else "") +
+                    ("ws_rollout_staged (per-step copies)" if staged else
+                     "A2C iteration, loss + stats to pinned host memory" if trainer is not None
+                     else "ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
+                    + (" + ws_gae_store" if gae else "") + (" + NCCL stats all-reduce" if world > 1 else "")
+                    + ", host wall clock" + (", max over ranks" if world > 1 else "")}
 
-                def host_step():
-                    henv.rollout_host(T, hp)
-                    if gae:
-                        henv.gae_store(T, g_vals, g_boot, gae[0], gae[1], out=g_out)
-                        torch.cuda.synchronize(dev)
-                h2d = int(hp.numel() * 4)
-            for _ in range(max(args.warmup, 1)):
-                host_step()
-            t0 = time.perf_counter()
-            for _ in range(args.steps):
-                host_step()
-            e2e_s = time.perf_counter() - t0
-            d2h = (int(sum(v.numel() * v.element_size() for v in hdst.values())) if staged
-                   else int(T * 4 * 8) + (24 if trainer is not None else 0))
-            e2e = {"value": E * T * args.steps / e2e_s, "unit": "env-steps/s",
-                   "h2d_bytes_per_step": h2d, "d2h_bytes_per_step": d2h,
-                   "note": "rank 0, " + ("ws_rollout_staged (per-step copies)" if staged else
-                                         "A2C iteration, loss + stats to pinned host memory" if trainer is not None
-                                         else "ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
-                           + (" + ws_gae_store" if gae else "")
-                           + ", host wall clock"}
-            henv.close()
+
+def main():
+    args = parse()
+    w = W.CONFIGS[args.workload]
+    if args.impl == "reference":
+        return run_reference(args, w)
+
+    global torch, dist
+    import torch
+    import torch.distributed as dist
+
+    world, rank, local = dist_env()
+    if world != args.gpus and rank == 0:
+        print(f"warning: --gpus {args.gpus} but WORLD_SIZE {world}", file=sys.stderr)
+    local_dev = 0 if args.same_device else local
+    torch.cuda.set_device(local_dev)
+    dev = torch.device("cuda", local_dev)
+    if world > 1:
+        if args.dist_backend == "nccl":
+            dist.init_process_group("nccl", device_id=dev)
+        else:
+            dist.init_process_group(args.dist_backend)
+    register_user(w, oracle_side=False)
+
+    run = Run(args, w, world, rank, dev, args.scaling)
+    E, A, T, E_g = run.E, run.A, run.T, run.E_g
+    sb = store_bytes(w, E)
+    flush = sb < 2 * L2_BYTES
+    if flush:
+        run.flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+    run.warm(args.warmup)
+
+    clocks = Clocks(local_dev)
+    if not args.ncu:
+        clocks.start()
+        time.sleep(0.3)
+    # two CUDA events per step around the fused roll-out kernel only (libws ws_kernel_times):
+    # the dominant kernel is timed live with the least perturbation of the timed loop
+    run.env.enable_kernel_timing(0 if (args.no_kernel_timing or run.staged) else (3 if run.gae else 2))
+    run.env.kernel_times()
+    launches0 = run.env.info().launches
+    per = run.timed(args.steps, flush)
+    total_ms = sum(per)
+    st = run.env.status()  # sticky device errors (invalid rows, peer reduction timeout) fail the run
+    if st != 0:
+        raise RuntimeError(f"libws reported status {st} during the timed region")
+    launches = run.env.info().launches - launches0
+    if run.trainer is not None:  # handle-free kernels per step: moments + final, then (grad + final, Adam) per update
+        n_upd = (w.params["ppo"][0] * w.params["ppo"][1]) if w.params.get("ppo") else 1
+        launches += (2 + 3 * n_upd) * args.steps
+    ktimes = run.env.kernel_times()
+    run.env.enable_kernel_timing(False)
+    max_ms = run.max_over_ranks(total_ms)
+    value = E_g * T * args.steps / (max_ms / 1e3)
+    ms_per_step = max_ms / args.steps
+
+    # sustained pass (>= --sustain-s seconds; not part of `value`): clocks under a long load and
+    # a stable p10 / p90 of the per-step time
+    sustained = None
+    if not args.ncu and args.sustain_s > 0:
+        n_sus = int(min(100000, max(args.steps, np.ceil(args.sustain_s * 1e3 / max(ms_per_step, 1e-3)))))
+        per_s = run.timed(n_sus, flush)
+        sus_ms = run.max_over_ranks(sum(per_s))
+        sustained = {"steps": n_sus, "seconds": round(sus_ms / 1e3, 3), "value": E_g * T * n_sus / (sus_ms / 1e3),
+                     "ms_per_step": sus_ms / n_sus, "p10_ms": pct(per_s, 10), "p50_ms": pct(per_s, 50),
+                     "p90_ms": pct(per_s, 90), "note": "rank-local per-step percentiles; value = max over ranks"}
+    clk = clocks.stop() if not args.ncu else {}
+
+    # merged per-slot statistics of the last timed roll-out (all ranks, exact int64; R20)
+    from paper_2408_00930_b200.parallel import summarize
+    merged = summarize(run.stats_view.cpu())
+
+    # diagnostic pass after the timed region (not part of `value`): every kernel and the whole
+    # ws_rollout call bracketed by events
+    n_diag = max(1, min(args.steps, 5))
+    run.env.enable_kernel_timing(1)
+    run.env.kernel_times()
+    dev_ev = [torch.cuda.Event(enable_timing=True) for _ in range(2 * n_diag)]
+    for k in range(n_diag):
+        dev_ev[2 * k].record(run.stream)
+        run.rollout()
+        dev_ev[2 * k + 1].record(run.stream)
+    torch.cuda.synchronize(dev)
+    kern_ms = [dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)]
+    diag_times = run.env.kernel_times()
+    run.env.enable_kernel_timing(False)
+    upd_ms = None
+    if run.trainer is not None:  # the update alone (critic, GAE, moments, gradient, Adam)
+        for k in range(n_diag):
+            dev_ev[2 * k].record(run.stream)
+            run.trainer.update(T, values_ready=True)
+            dev_ev[2 * k + 1].record(run.stream)
+        torch.cuda.synchronize(dev)
+        upd_ms = sum(dev_ev[2 * k].elapsed_time(dev_ev[2 * k + 1]) for k in range(n_diag)) / n_diag
+    if world > 1:
+        dist.barrier()
+
+    peaks, peak_src = measured_peaks()
+    peak = float(peaks.get("hbm_gbs", 6650.0))
+    roofline = roofline_of(run, ktimes, diag_times, kern_ms, peak, peak_src, peaks, n_diag, upd_ms, w)
+
+    e2e = e2e_pass(run, args, dev, world) if not args.ncu else None
+    p2p = run.p2p
+    run.close()
+
+    # N > 1: the other scaling mode too (strong = the workload's E split over the ranks,
+    # e.g. BJ:2's 10K CartPole total; weak = E per rank)
+    other = None
+    if world > 1 and not args.ncu:
+        mode = "strong" if args.scaling == "weak" else "weak"
+        r2 = Run(args, w, world, rank, dev, mode)
+        if flush or store_bytes(w, r2.E) < 2 * L2_BYTES:
+            r2.flush_buf = torch.empty(256 * 2 ** 20, dtype=torch.uint8, device=dev)
+        r2.warm(args.warmup)
+        per2 = r2.timed(args.steps, store_bytes(w, r2.E) < 2 * L2_BYTES)
+        m2 = r2.max_over_ranks(sum(per2))
+        other = {"scaling": mode, "n_envs_global": r2.E_g, "n_envs_per_rank": layout(w, world, mode)[1],
+                 "value": r2.E_g * T * args.steps / (m2 / 1e3), "ms_per_step": m2 / args.steps,
+                 "p10_ms": pct(per2, 10), "p90_ms": pct(per2, 90)}
+        r2.close()
+
+    if rank == 0:
+        l2 = (f"store {sb / 1e6:.1f} MB per step per GPU < 2 x L2 (126 MB): L2 flushed (256 MB write) before every "
+              f"timed step, outside the events" if flush else
+              f"store {sb / 1e6:.0f} MB per step per GPU > 2 x L2 (126 MB): no flush needed")
         line = {
             "metric": "env-steps/s", "value": value, "unit": "env-steps/s", "n_gpus": world,
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": f"{w.name}: {w.note}", "env": w.env, "n_envs_per_gpu": E, "n_envs_global": E_g,
-                       "n_agents": A, "T": T, "probs": "uniform, resident in HBM, step_stride 0",
-                       "parallelism": (f"env-shard x{world} + " + ("peer-memory (CUDA IPC, NVLink) stats all-reduce kernel"
-                                                                    if p2p else "NCCL stats all-reduce")) if world > 1 else "1 GPU",
-                       "l2": f"store {all_bytes / 1e6:.0f} MB written per step > 126 MB L2 (no flush needed)"},
+            "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": make_config(w, world, args.scaling, "p2p" if p2p else "nccl"),
+            "timing": {"p10_ms": pct(per, 10), "p50_ms": pct(per, 50), "p90_ms": pct(per, 90), "l2": l2,
+                       "per_step_events": True},
             "roofline": roofline, "gpu_launches": int(launches),
             "episode_stats_last_step": merged,
-            "clocks": clk, "e2e": e2e,
+            "clocks": clk, "e2e": e2e, "sustained": sustained,
             "paper_context": "A100 8.6M env-steps/s incl. training (P:39); not like-for-like",
         }
+        if other is not None:
+            line["other_scaling"] = other
         if not args.no_cpu_baseline and not args.ncu and world == 1:
             line["cpu_baseline"] = cpu_baseline(w)
         print(json.dumps(line), flush=True)
         if args.csv:
             write_csv_row(args.csv, w, world, E_g, A, T, line)
-    env.close()
     if world > 1:
         dist.barrier()
         dist.destroy_process_group()

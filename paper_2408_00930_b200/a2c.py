@@ -166,6 +166,13 @@ class A2C:
         self.world = dist.get_world_size(group) if dist.is_available() and dist.is_initialized() else 1
         self.step = 0
         self._values = None
+        # global agent columns (sum of every rank's E * A): shards may differ by one replica
+        # (parallel.shard), so the global batch is counted, not assumed to be E * world
+        self.E_global = self.E
+        if self.world > 1:
+            n = torch.tensor([self.E], dtype=torch.int64, device=dev if dist.get_backend(group) == "nccl" else "cpu")
+            dist.all_reduce(n, op=dist.ReduceOp.SUM, group=group)
+            self.E_global = int(n.item())
         # peer=True (world > 1): moments and gradient reduced over CUDA-IPC peer memory, the
         # gradient all-reduce fused with clip + Adam in one kernel (ws_pgroup_*), no NCCL
         # ("auto": use it when CUDA IPC works on every rank, else torch.distributed / NCCL)
@@ -228,12 +235,14 @@ class A2C:
         self._adv = adv  # alive until the stream consumed it
         return obs, act, adv.view(-1), ret.view(-1), rows
 
-    def _step(self, obs, act, adv, ret, rows, norm_rows, logp_old=None, clip_eps=0.2):
-        """One gradient (this shard's rows) -> all-reduce -> clip + Adam."""
+    def _step(self, obs, act, adv, ret, slots, norm_slots, logp_old=None, clip_eps=0.2):
+        """One gradient (this shard's rows of `slots` store slots) -> all-reduce -> clip + Adam.
+        The loss averages over the GLOBAL batch (slots x every rank's columns) and the advantages
+        are normalised with the global moments over norm_slots slots."""
         hp, s = self.hp, self.env.stream
-        a2c_grad(self.params, obs, act, adv, ret, self.mom, float(rows * self.world), self.D, self.H, self.N,
+        a2c_grad(self.params, obs, act, adv, ret, self.mom, float(slots * self.E_global), self.D, self.H, self.N,
                  hp["c_v"], hp["c_e"], self.ws, grad=self.grad, loss=self.loss, stream=s, logp_old=logp_old,
-                 clip_eps=clip_eps, norm_batch=float(norm_rows * self.world))
+                 clip_eps=clip_eps, norm_batch=float(norm_slots * self.E_global))
         self.step += 1
         if self._pg_grad is not None:  # fused peer-memory all-reduce + clip + Adam (one kernel)
             self._pg_grad.allreduce_adam(self.grad, self.params, self.m, self.v, self.step, hp["lr"], hp["beta1"],
@@ -249,7 +258,7 @@ class A2C:
         values_ready: the roll-out already wrote the critic (ws_rollout_actor_critic)."""
         with torch.cuda.stream(self.env.stream):
             obs, act, adv, ret, rows = self._advantages(T, values_ready)
-            self._step(obs, act, adv, ret, rows, rows)
+            self._step(obs, act, adv, ret, T, T)
 
     def torch_policy(self):
         """The R29 policy of self.params as a torch function (for the single-step roll-out of
@@ -315,5 +324,5 @@ class PPO(A2C):
                     t0, t1 = T * m // M, T * (m + 1) // M
                     r0, r1 = t0 * E, t1 * E
                     na = self.N if self.gaussian else 1
-                    self._step(obs[r0 * D:r1 * D], act[r0 * na:r1 * na], adv[r0:r1], ret[r0:r1], r1 - r0, rows,
+                    self._step(obs[r0 * D:r1 * D], act[r0 * na:r1 * na], adv[r0:r1], ret[r0:r1], t1 - t0, T,
                                logp_old=logp[r0:r1], clip_eps=self.clip_eps)

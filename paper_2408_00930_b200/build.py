@@ -53,14 +53,33 @@ def nvcc() -> str:
 
 def build(force: bool = False, verbose: bool = False, defines=(), out: str = LIB) -> str:
     """Compile libws.so.  `defines` / `out` are for profiling experiments only (e.g.
-    WS_EXP=...) -- the product library is always LIB built without extra defines."""
+    WS_EXP=...) -- the product library is always LIB built without extra defines.
+    Each translation unit compiles in its own nvcc process (in parallel; they share no device
+    symbols, so this equals one nvcc invocation over all sources), then one link step."""
     if out == LIB and not defines and not force and not needs_build():
         return LIB
+    from concurrent.futures import ThreadPoolExecutor
     os.makedirs(os.path.dirname(out), exist_ok=True)
+    objdir = os.path.join(os.path.dirname(out), "obj" + ("_" + "_".join(defines) if defines else ""))
+    os.makedirs(objdir, exist_ok=True)
+    flags = [f for f in NVCC_FLAGS if f != "-shared"]
+
+    def compile_one(src):
+        obj = os.path.join(objdir, os.path.basename(src)[:-3] + ".o")
+        hdrs = [p for p in deps() if not p.endswith(".cu")]
+        if not force and os.path.exists(obj) and all(os.path.getmtime(p) <= os.path.getmtime(obj)
+                                                     for p in hdrs + [src, __file__]):
+            return obj  # up to date
+        cmd = [nvcc()] + flags + (["-Xptxas", "-v"] if verbose else []) + \
+            [f"-D{d}" for d in defines] + ["-c", "-o", obj, src]
+        subprocess.run(cmd, check=True)
+        return obj
+
+    srcs = sources()
+    with ThreadPoolExecutor(max_workers=max(1, min(len(srcs), os.cpu_count() or 1))) as ex:
+        objs = list(ex.map(compile_one, srcs))
     tmp = out + ".tmp"
-    cmd = [nvcc()] + NVCC_FLAGS + (["-Xptxas", "-v"] if verbose else []) + \
-        [f"-D{d}" for d in defines] + ["-o", tmp] + sources()
-    subprocess.run(cmd, check=True)
+    subprocess.run([nvcc(), "-gencode", "arch=compute_100a,code=sm_100a", "-shared", "-o", tmp] + objs, check=True)
     os.replace(tmp, out)
     return out
 

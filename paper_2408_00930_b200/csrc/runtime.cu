@@ -479,6 +479,25 @@ ws_status ws_step(ws_env* h, const void* actions) {
   return WS_OK;
 }
 
+/* A8 across GPUs after any roll-out entry point (ws_rollout, the policy roll-outs, the staged
+ * pipeline): when peer statistics are attached, merge the [T, 4] slab in place over peer memory
+ * (k_peer_allreduce, no NCCL call).  No-op otherwise. */
+static ws_status peer_merge(ws_env* h, int32_t T) {
+  if (!h->peer_attached) return WS_OK;
+  ws::PeerArgs pa{};
+  for (int r = 0; r < h->peer_world; ++r)
+    pa.gather[r] = r == h->peer_rank ? h->peer_own : static_cast<unsigned long long*>(h->peer_open[r]);
+  pa.rank = h->peer_rank;
+  pa.world = h->peer_world;
+  pa.t_cap = h->peer_tcap;
+  cudaError_t e = ws::launch_peer_allreduce(h->stats, T, pa, h->peer_epoch, h->stats, h->err, h->peer_timeout_s,
+                                            h->stream);
+  if (e) return cuda_fail(h, e, "peer statistics reduction");
+  h->peer_epoch += 1;
+  h->launches += 1;
+  return WS_OK;
+}
+
 ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_stride, int64_t step_stride) {
   NvtxRange nvtx_("ws_rollout");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
@@ -499,18 +518,7 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
     e = ws::launch_rollout(kargs(h), launch_of(h), T, h->t, probs, row_stride, step_stride, &h->launches);
   }
   if (e) return cuda_fail(h, e, "rollout kernel");
-  if (h->peer_attached) {  // A8 across GPUs: merged statistics in place, no NCCL call
-    ws::PeerArgs pa{};
-    for (int r = 0; r < h->peer_world; ++r)
-      pa.gather[r] = r == h->peer_rank ? h->peer_own : static_cast<unsigned long long*>(h->peer_open[r]);
-    pa.rank = h->peer_rank;
-    pa.world = h->peer_world;
-    pa.t_cap = h->peer_tcap;
-    e = ws::launch_peer_allreduce(h->stats, T, pa, h->peer_epoch, h->stats, h->err, h->peer_timeout_s, h->stream);
-    if (e) return cuda_fail(h, e, "peer statistics reduction");
-    h->peer_epoch += 1;
-    h->launches += 1;
-  }
+  if ((s = peer_merge(h, T))) return s;
   h->t += (uint64_t)T;
   h->cursor = T;
   h->sampled_slot = -1;
@@ -562,6 +570,7 @@ static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t 
                                   values_trunc);
   }
   if (e) return cuda_fail(h, e, "policy roll-out kernel");
+  if ((st = peer_merge(h, T))) return st;
   h->t += (uint64_t)T;
   h->cursor = T;
   h->sampled_slot = -1;
@@ -708,6 +717,7 @@ ws_status ws_rollout_staged(ws_env* h, int32_t T, const float* host_probs, int64
   cudaEventDestroy(first);
   if (st) return st;
   if (e) return cuda_fail(h, e, "staged roll-out copy");
+  if ((st = peer_merge(h, T))) return st;
   if (out) {
     out->total_ms = total;
     out->transfer_ms = transfer;

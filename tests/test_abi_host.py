@@ -2,6 +2,7 @@
 declares, and its host-side argument validation (S:135-138) answers without a GPU;
 sharding arithmetic and the statistics merge of the multi-GPU path."""
 import ctypes as C
+import os
 
 import numpy as np
 import pytest
@@ -10,6 +11,7 @@ import torch
 import paper_2408_00930_b200 as P
 from paper_2408_00930_b200 import _abi
 from paper_2408_00930_b200.parallel import shard, summarize
+import wsinputs as W
 
 
 def test_library_exports_every_declared_symbol():
@@ -236,3 +238,43 @@ def test_bench_csv_row(tmp_path):
     rows = open(f).read().strip().split("\n")
     assert rows[0].startswith("env,E,A,T,gpus") and len(rows) == 3
     assert rows[1].split(",")[:7] == ["tag", "2000", "100", "200", "2", "20000000000.0", "2000000000000.0"]
+
+
+def _bench():
+    import importlib.util
+    spec = importlib.util.spec_from_file_location("bench_mod", os.path.join(os.path.dirname(__file__), "..", "bench.py"))
+    bench = importlib.util.module_from_spec(spec)
+    spec.loader.exec_module(bench)
+    return bench
+
+
+def test_bench_layout_strong_and_weak():
+    """bench.py --scaling: weak = the workload's E on every rank; strong = E split by
+    parallel.shard (contiguous, sizes differ by <= 1) -- e.g. C3a's 100K over 8 GPUs."""
+    from paper_2408_00930_b200.parallel import shard
+    bench = _bench()
+    w = W.CONFIGS["C3a"]
+    assert bench.layout(w, 8, "weak") == (800000, [100000] * 8)
+    E_g, per = bench.layout(w, 8, "strong")
+    assert E_g == 100000 and per == [12500] * 8
+    for E_g, world in [(37, 4), (10000, 3), (5, 8)]:
+        assert bench.shard_sizes(E_g, world) == [shard(E_g, world, r)[1] for r in range(world)]
+
+
+def test_bench_reference_arm_config_matches_ours():
+    """The reference arm (the oracle) prints the same `config` object as our arm for the same
+    flags, so the driver can pair the two lines (same_config)."""
+    import json
+    import subprocess
+    import sys
+    root = os.path.join(os.path.dirname(__file__), "..")
+    out = subprocess.run([sys.executable, "bench.py", "--impl", "reference", "--workload", "C1", "--steps", "2",
+                          "--warmup", "1"], cwd=root, capture_output=True, text=True, timeout=600)
+    assert out.returncode == 0, out.stderr[-2000:]
+    lines = [l for l in out.stdout.splitlines() if l.startswith("{")]
+    assert len(lines) == 1
+    d = json.loads(lines[0])
+    bench = _bench()
+    assert d["impl"] == "reference" and d["config"] == bench.make_config(W.CONFIGS["C1"], 1, "weak", "nccl")
+    assert d["cpu_baseline"]["cores"] >= 1 and d["e2e"]["h2d_bytes_per_step"] == 0
+    assert d["config"]["n_envs_per_rank"] == [64]

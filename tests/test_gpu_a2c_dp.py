@@ -26,10 +26,13 @@ def _port():
     return p
 
 
-def test_two_rank_a2c_equals_single_process(tmp_path):
+@pytest.mark.parametrize("E_g", [1000, 1001])
+def test_two_rank_a2c_equals_single_process(tmp_path, E_g):
+    """E_g = 1001: shards of 500 and 501 replicas -- the loss mean and the advantage
+    normalisation must still use the global batch (not rows x world)."""
     if not torch.cuda.is_available():
         pytest.skip("needs a GPU")
-    E_g, T, iters = 1000, 64, 3
+    T, iters = 64, 3
     cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", "--nproc-per-node=2",
            "--master-addr", "127.0.0.1", "--master-port", str(_port()),
            os.path.join(ROOT, "tests", "a2c_worker.py"), str(tmp_path), str(E_g), str(T), str(iters)]

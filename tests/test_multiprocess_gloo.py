@@ -1,4 +1,4 @@
-"""World-size-2 CPU coverage of the multi-GPU path with the
+"""World-size-2 and -4 CPU coverage of the multi-GPU path with the
 gloo backend: each rank owns a contiguous replica shard (parallel.shard) and the only
 exchange is the sum all-reduce of the per-slot statistics (parallel.allreduce_stats).  The
 per-rank roll-outs are computed by the oracle here (no GPU); the merged statistics must
@@ -48,10 +48,12 @@ def _worker(rank, world, port, env, out_dir):
     dist.destroy_process_group()
 
 
+@pytest.mark.parametrize("world", [2, 4])
 @pytest.mark.parametrize("env", ["cartpole", "tag"])
-def test_two_rank_stats_allreduce_matches_single_process(env, tmp_path):
+def test_multi_rank_stats_allreduce_matches_single_process(env, world, tmp_path):
+    """world 2 (shards 18 / 19) and world 4 (9 / 9 / 9 / 10): uneven contiguous shards of
+    E = 37."""
     import oracle as O
-    world = 2
     mp.start_processes(_worker, args=(world, _free_port(), env, str(tmp_path)), nprocs=world,
                        join=True, start_method="spawn")
     A = 10 if env == "tag" else 1

@@ -41,6 +41,12 @@ CONFIGS = {
     "C5": Workload("C5", "surface", 2000, 1, 200, 0, 20, {"dim": 20},
                    note="surface-20 2K envs x 200 (BJ:11)"),
     "D0": Workload("D0", "dummy", 1000000, 1, 100, 2, 1, note="store-write calibration"),
+    # saturation points of SURVEY 8(d).1's sweep (where the >= 60 % roofline target is assessed:
+    # enough replicas per GPU to fill every scheduler; same per-replica work as C2 / C3a)
+    "C2S": Workload("C2S", "cartpole", 640000, 1, 1000, 2, 1,
+                    note="CartPole-v1 640K envs x 1000 steps (saturation point, SURVEY 8(d).1 sweep)"),
+    "C3S": Workload("C3S", "acrobot", 400000, 1, 500, 3, 1,
+                    note="Acrobot-v1 400K envs x 500 steps (saturation point, SURVEY 8(d).1 sweep)"),
     # NEXT-N1: C2's shape with the actions drawn from an in-kernel MLP policy
     "C2P": Workload("C2P", "cartpole", 10000, 1, 1000, 2, 1, {"policy_hidden": 64},
                     note="CartPole-v1 10K envs x 1000 steps, in-kernel MLP policy 4-64-2 (NEXT-N1)"),
