@@ -759,6 +759,10 @@ def main():
     value = E_g * T * args.steps / (max_ms / 1e3)
     ms_per_step = max_ms / args.steps
 
+    # merged per-slot statistics of the last timed roll-out (all ranks, exact int64; R20)
+    from paper_2408_00930_b200.parallel import summarize
+    merged = summarize(run.stats_view.cpu())
+
     # sustained pass (>= --sustain-s seconds; not part of `value`): clocks under a long load and
     # a stable p10 / p90 of the per-step time
     sustained = None
@@ -770,10 +774,6 @@ def main():
                      "ms_per_step": sus_ms / n_sus, "p10_ms": pct(per_s, 10), "p50_ms": pct(per_s, 50),
                      "p90_ms": pct(per_s, 90), "note": "rank-local per-step percentiles; value = max over ranks"}
     clk = clocks.stop() if not args.ncu else {}
-
-    # merged per-slot statistics of the last timed roll-out (all ranks, exact int64; R20)
-    from paper_2408_00930_b200.parallel import summarize
-    merged = summarize(run.stats_view.cpu())
 
     # diagnostic pass after the timed region (not part of `value`): every kernel and the whole
     # ws_rollout call bracketed by events
