@@ -63,6 +63,7 @@ def lib():
             "wso_pendulum_step_f64": (I, [P, D, P, P]),
             "wso_mb_energy": (D, [D, D, P, P]),
             "wso_surface_energy": (F, [P, I]),
+            "wso_surface_spring": (D, [P, I]),
             "wso_surface_step": (I, [P, P, I, P, P, P]),
             "wso_tag_step": (I, [I, I, I, P, P, P, P, P, P]),
             "wso_create": (P, [C.c_char_p, I64, I, U64, I64, I64, I, I, I, P]),
@@ -226,6 +227,12 @@ def mb_energy(x, y):
     gx = np.zeros(1); gy = np.zeros(1)
     e = lib().wso_mb_energy(float(x), float(y), _p(gx), _p(gy))
     return e, gx[0], gy[0]
+
+
+def surface_spring(q) -> float:
+    """The fp64 spring sum of q_i^2 (i >= 2) in R23's pairwise order."""
+    qa = np.ascontiguousarray(q, np.float32)
+    return float(lib().wso_surface_spring(_p(qa), len(qa)))
 
 
 def surface_energy(q) -> float:

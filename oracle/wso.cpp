@@ -237,18 +237,28 @@ constexpr double MB_c[4] = {-10, -10, -6.5, 0.7};
 constexpr double MB_x0[4] = {1, 0, -0.5, -1};
 constexpr double MB_y0[4] = {0, 0.5, 1.5, 1};
 
+/* Pairwise (binary-tree) sum of w[0..n), n a power of two: sum(w, n) = sum(w, n/2) +
+ * sum(w + n/2, n/2) (reading R23: the fixed summation order of the energy's two sums). */
+double pairwise_sum(const double* w, int n) {
+  if (n == 1) return w[0];
+  return pairwise_sum(w, n / 2) + pairwise_sum(w + n / 2, n / 2);
+}
+
+/* Mueller-Brown potential: sum of the four terms t_k = A_k exp(a_k dx^2 + b_k dx dy +
+ * c_k dy^2), added as the pairwise tree (t0 + t1) + (t2 + t3) (R23).  The gradient (S:262,
+ * used by the pins only) is summed left to right. */
 double mb_energy(double x, double y, double* gx, double* gy) {
-  double E = 0, Gx = 0, Gy = 0;
+  double t[4], Gx = 0, Gy = 0;
   for (int k = 0; k < 4; ++k) {
     double dx = x - MB_x0[k], dy = y - MB_y0[k];
     double ex = MB_A[k] * std::exp(MB_a[k] * dx * dx + MB_b[k] * dx * dy + MB_c[k] * dy * dy);
-    E += ex;
+    t[k] = ex;
     Gx += ex * (2 * MB_a[k] * dx + MB_b[k] * dy);
     Gy += ex * (MB_b[k] * dx + 2 * MB_c[k] * dy);
   }
   if (gx) *gx = Gx;
   if (gy) *gy = Gy;
-  return E;
+  return pairwise_sum(t, 4);
 }
 
 struct SurfaceParams {
@@ -263,12 +273,20 @@ struct SurfaceParams {
   static float start(int i) { return i == 0 ? (float)start0 : (i == 1 ? (float)start1 : 0.0f); }
 };
 
-/* energy in fp64 from the fp32 state, rounded once (DESIGN R3) */
+/* spring sum of q_i^2, i = 2..D-1, as the pairwise tree over P = the smallest power of two
+ * >= max(D, 4) leaves w_i = q_i^2 (2 <= i < D), +0 otherwise (R23) */
+double surface_spring(const float* q, int D) {
+  int P = 4;
+  while (P < D) P *= 2;
+  std::vector<double> w(P, 0.0);
+  for (int i = 2; i < D; ++i) w[i] = (double)q[i] * (double)q[i];
+  return pairwise_sum(w.data(), P);
+}
+
+/* energy in fp64 from the fp32 state, rounded once (DESIGN R3, R23) */
 float surface_energy(const float* q, int D) {
   double E = mb_energy((double)q[0], (double)q[1], nullptr, nullptr);
-  double spring = 0;
-  for (int i = 2; i < D; ++i) spring += (double)q[i] * (double)q[i];
-  return (float)(E + 0.5 * SurfaceParams::kappa * spring);
+  return (float)(E + 0.5 * SurfaceParams::kappa * surface_spring(q, D));
 }
 
 int surface_step(const float* q, const float* a, int D, float* out, float* reward, int* terminated) {
@@ -874,6 +892,7 @@ int wso_pendulum_step_f64(const double* s, double u, double* out, double* r) {
 }
 double wso_mb_energy(double x, double y, double* gx, double* gy) { return mb_energy(x, y, gx, gy); }
 float wso_surface_energy(const float* q, int D) { return surface_energy(q, D); }
+double wso_surface_spring(const float* q, int D) { return surface_spring(q, D); }
 int wso_surface_step(const float* q, const float* a, int D, float* out, float* r, int* term) {
   return surface_step(q, a, D, out, r, term);
 }

@@ -156,6 +156,7 @@ _SIGS = {
     "ws_test_philox": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
     "ws_test_sample_grid": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_void_p]),
     "ws_test_unary": (C.c_int, [C.c_int32, C.c_float, C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p]),
+    "ws_test_surface_energy": (C.c_int, [C.c_void_p, C.c_int32, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ws_test_exhaustive": (C.c_int, [C.c_int32, C.c_int32, C.c_float, C.c_uint32, C.c_uint32,
                                      C.POINTER(C.c_uint64), C.c_void_p]),
 }

@@ -396,19 +396,19 @@ __device__ __forceinline__ unsigned long long* cta_stats_buf() {
 #endif
 constexpr int kPlanChunk = WS_PLAN_CHUNK;  // steps per plan thread (thresholds amortised over the chunk)
 
+// One warp's share of the plan: the 32 consecutive replicas starting at e - lane (lane =
+// threadIdx.x & 31), steps [c_begin, c_end) -- every lane of the warp must call it (the CDF of
+// the probability rows is a warp scan).
 template <int N, bool kStrided>
-__global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
-                                                      const float* __restrict__ probs, const int64_t row_stride,
-                                                      const int64_t step_stride) {
+__device__ __forceinline__ void plan_rows(const KArgs& a, const int T, const uint64_t t0, const float* __restrict__ probs,
+                                          const int64_t row_stride, const int64_t step_stride, const int64_t e,
+                                          const int c_begin, const int c_end) {
   const int lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t E = a.E;
   const bool live = e < E;
   const int64_t ec = live ? e : E - 1;  // tail lanes duplicate replica E-1 (identical stores)
   const uint32_t eg = (uint32_t)(a.offset + ec);
   const Key key{a.k0, a.k1};
-  const int c_begin = blockIdx.y * kPlanChunk;
-  const int c_end = min(T, c_begin + kPlanChunk);
   const bool wlogp = a.write_logp != 0;
   int32_t* const p_act = reinterpret_cast<int32_t*>(a.act) + ec;
   float* const p_logp = a.logp + ec;
@@ -493,6 +493,15 @@ __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int 
     }
   }
   if (live && any_bad) atomicOr(a.err, kErrProbs | kErrAction);
+}
+
+template <int N, bool kStrided>
+__global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
+                                                      const float* __restrict__ probs, const int64_t row_stride,
+                                                      const int64_t step_stride) {
+  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int c_begin = blockIdx.y * kPlanChunk;
+  plan_rows<N, kStrided>(a, T, t0, probs, row_stride, step_stride, e, c_begin, min(T, c_begin + kPlanChunk));
 }
 
 // =======================================================================================
@@ -656,10 +665,7 @@ struct DiscreteRunner {
 };
 
 template <class Env, bool kLat>
-// latency build: minBlocks 1 lets ptxas spend registers on a deeper schedule (C2 measured:
-// 174 registers, 0.180 ms vs 100 registers, 0.200 ms); throughput build: the env's budget
-__global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::kMinBlocksThr)
-    k_rollout_discrete(const KArgs a, const int T) {
+__device__ __forceinline__ void rollout_discrete_body(const KArgs& a, const int T) {
   using L = Lane<Env>;
   using Run = DiscreteRunner<Env, kLat>;
   constexpr int kWin = 3 * Run::kRows * kWinStride;  // window words per warp
@@ -715,6 +721,14 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
     a.ep_ret[e] = R.ep_ret;
     L::obs_store(a.obs_live + e * L::D, R.s, false);
   }
+}
+
+template <class Env, bool kLat>
+// latency build: minBlocks 1 lets ptxas spend registers on a deeper schedule (C2 measured:
+// 174 registers, 0.180 ms vs 100 registers, 0.200 ms); throughput build: the env's budget
+__global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::kMinBlocksThr)
+    k_rollout_discrete(const KArgs a, const int T) {
+  rollout_discrete_body<Env, kLat>(a, T);
 }
 
 // =======================================================================================
@@ -1216,12 +1230,15 @@ __device__ __forceinline__ double warp_tree_sum(double v) {
 // =======================================================================================
 // A7 for surface-D, segmented: each replica is a segment of L = ceil(D/4) lanes holding four
 // coordinates each, so a warp advances R = 32 / L replicas at once (D = 20: 5 lanes, 6
-// replicas).  The coordinate-parallel work (action clip, update, observation stores, reset
-// draws, goal-distance partials) stays on the lanes; the two order-sensitive fp64 sums of
-// the energy -- the four Mueller-Brown terms and the spring term over coordinates 2..D-1 --
-// are gathered through shared memory and added sequentially in coordinate order, exactly
-// as Surface<D>::energy and the oracle do (R23).  The goal distance only feeds a comparison,
-// so its partials are added per lane, then over the segment.
+// replicas).  Coordinate-parallel work (action clip, update, observation stores, reset draws,
+// squares) stays on the lanes; the energy's two fixed-order sums (R23: the Mueller-Brown terms
+// as (t0 + t1) + (t2 + t3), the spring sum as the pairwise tree over the padded coordinate
+// leaves) are assembled from register shuffles inside the segment: each lane's four leaves
+// form one 4-leaf subtree of the oracle's tree, the segment's lanes 0..3 each evaluate one
+// Mueller-Brown term (one fp64 exp per lane, in parallel), and every lane of the segment
+// gathers the L subtrees and the four terms and adds them in the tree order.  The goal
+// distance only feeds a comparison, so its lane partials are added in any fixed order.
+// Actions are prefetched four steps ahead (register ring).
 // =======================================================================================
 template <int D>
 struct SurfSeg {
@@ -1229,21 +1246,27 @@ struct SurfSeg {
   static constexpr int L = (D + C - 1) / C;  // lanes per replica
   static constexpr int R = 32 / L;           // replicas per warp
 };
-// per warp: qv [40][4] f32, sq [40][4] f64, mb [34][4] f64, gp [40] f64 -- lanes past the last
-// whole segment (D = 20: lanes 30, 31) work on a scratch segment R, so no branch diverges
-constexpr int kSegSlots = 40;
-constexpr int kSegWarpBytes = kSegSlots * 4 * 4 + kSegSlots * 4 * 8 + 34 * 4 * 8 + kSegSlots * 8;
+
+// pairwise tree over the segment's per-lane 4-leaf subtrees g[0 .. G) (G = the tree's leaves / 4;
+// subtrees >= L are padding, +0, skipped exactly as in spring_tree)
+template <int L, int LO, int N>
+__device__ __forceinline__ double group_tree(const double* g) {
+  if constexpr (N == 1) {
+    return LO < L ? g[LO] : 0.0;
+  } else if constexpr (LO + N / 2 >= L) {
+    return group_tree<L, LO, N / 2>(g);
+  } else {
+    return group_tree<L, LO, N / 2>(g) + group_tree<L, LO + N / 2, N / 2>(g);
+  }
+}
 
 template <int D>
 struct SurfSegWarp {
   using Env = Surface<D>;
   using G = SurfSeg<D>;
   static constexpr int C = G::C, L = G::L, R = G::R;
-  float* qv;   // [32][C] coordinates of the state being evaluated
-  double* sq;  // [32][C] squares (coordinates >= 2)
-  double* mb;  // [R][4] Mueller-Brown terms
-  double* gp;  // [32] goal-distance partials
-  int lane, seg, sl;
+  static constexpr int kGroups = spring_leaves(D) / C;  // 4-leaf subtrees of the spring tree
+  int lane, seg, sl, src;  // src: the segment's first lane
   bool used;
   double mc[6];  // Mueller-Brown coefficients (A, a, b, c, x0, y0) of term sl (L >= 4)
 
@@ -1252,54 +1275,49 @@ struct SurfSegWarp {
     for (int i = 0; i < 6; ++i) mc[i] = __ldg(&kMB[i][sl < 4 ? sl : 0]);
   }
   __device__ __forceinline__ bool valid(int i) const { return sl * C + i < D; }
-  // energy of the segment's state q (this lane's C coordinates); warp-collective
-  __device__ __forceinline__ float energy(const float (&q)[C]) {
-    __syncwarp();
+  __device__ __forceinline__ double shfl_d(double v, int from) const {
+    return __hiloint2double(__shfl_sync(kFull, __double2hiint(v), from), __shfl_sync(kFull, __double2loint(v), from));
+  }
+  // energy of the segment's state q (this lane's C coordinates); warp-collective; *spring_out
+  // (optional) receives the spring sum
+  __device__ __forceinline__ float energy(const float (&q)[C], double* spring_out = nullptr) const {
+    // spring: this lane's leaves 4 sl .. 4 sl + 3 (coordinates 0, 1 and >= D are +0 leaves)
+    double w[C];
 #pragma unroll
     for (int i = 0; i < C; ++i) {
       const int k = sl * C + i;
-      qv[lane * C + i] = q[i];
-      sq[lane * C + i] = (k >= 2 && k < D) ? (double)q[i] * (double)q[i] : 0.0;
+      w[i] = (k >= 2 && k < D) ? (double)q[i] * (double)q[i] : 0.0;
     }
-    __syncwarp();
-    const int base = seg * L * C;
-    const double x = (double)qv[base], y = (double)qv[base + 1];
-    if constexpr (L >= 4) {  // one term per lane, coefficients in registers
-      if (sl < 4) {
-        const double dx = x - mc[4], dy = y - mc[5];
-        mb[seg * 4 + sl] = mc[0] * exp(mc[1] * dx * dx + mc[2] * dx * dy + mc[3] * dy * dy);
-      }
+    const double g = (w[0] + w[1]) + (w[2] + w[3]);
+    // Mueller-Brown terms of (q0, q1), which live on the segment's first lane
+    const double x = (double)__shfl_sync(kFull, q[0], src), y = (double)__shfl_sync(kFull, q[1], src);
+    constexpr int kTermsPerLane = (4 + L - 1) / L;
+    double tv[kTermsPerLane];
+    if constexpr (L >= 4) {
+      const double dx = x - mc[4], dy = y - mc[5];
+      tv[0] = mc[0] * exp(mc[1] * dx * dx + mc[2] * dx * dy + mc[3] * dy * dy);
     } else {
 #pragma unroll
-      for (int m0 = 0; m0 < 4; m0 += L) {
-        const int m = m0 + sl;
-        if (m < 4) {
-          const double dx = x - __ldg(&kMB[4][m]), dy = y - __ldg(&kMB[5][m]);
-          mb[seg * 4 + m] = __ldg(&kMB[0][m]) * exp(__ldg(&kMB[1][m]) * dx * dx + __ldg(&kMB[2][m]) * dx * dy +
-                                                    __ldg(&kMB[3][m]) * dy * dy);
-        }
+      for (int r = 0; r < kTermsPerLane; ++r) {
+        const int m = min(r * L + sl, 3);
+        const double dx = x - __ldg(&kMB[4][m]), dy = y - __ldg(&kMB[5][m]);
+        tv[r] = __ldg(&kMB[0][m]) * exp(__ldg(&kMB[1][m]) * dx * dx + __ldg(&kMB[2][m]) * dx * dy +
+                                        __ldg(&kMB[3][m]) * dy * dy);
       }
     }
-    __syncwarp();
-    const double2 m01 = reinterpret_cast<const double2*>(mb + seg * 4)[0];
-    const double2 m23 = reinterpret_cast<const double2*>(mb + seg * 4)[1];
-    const double E = (((0.0 + m01.x) + m01.y) + m23.x) + m23.y;
-    // all squares are fetched first (16-byte loads), then added in coordinate order
-    const double2* sp = reinterpret_cast<const double2*>(sq + base);
-    double v[((D + 1) / 2) * 2];
+    double t[4];
 #pragma unroll
-    for (int k = 0; k < (D + 1) / 2; ++k) {
-      const double2 t = sp[k];
-      v[2 * k] = t.x;
-      v[2 * k + 1] = t.y;
-    }
-    double spring = 0.0;
+    for (int m = 0; m < 4; ++m) t[m] = shfl_d(tv[m / L], src + m % L);
+    double gs[L];
 #pragma unroll
-    for (int k = 2; k < D; ++k) spring += v[k];
+    for (int j = 0; j < L; ++j) gs[j] = shfl_d(g, src + j);
+    const double E = (t[0] + t[1]) + (t[2] + t[3]);
+    const double spring = group_tree<L, 0, kGroups>(gs);
+    if (spring_out) *spring_out = spring;
     return (float)(E + 0.5 * Env::kappa * spring);
   }
   // squared distance of the segment's state to the goal (fixed association; comparison only)
-  __device__ __forceinline__ double goal_d2(const float (&q)[C]) {
+  __device__ __forceinline__ double goal_d2(const float (&q)[C]) const {
     double p = 0.0;
 #pragma unroll
     for (int i = 0; i < C; ++i) {
@@ -1308,15 +1326,9 @@ struct SurfSegWarp {
         p += di * di;
       }
     }
-    __syncwarp();
-    gp[lane] = p;
-    __syncwarp();
-    double g[L];
-#pragma unroll
-    for (int j = 0; j < L; ++j) g[j] = gp[seg * L + j];
     double d2 = 0.0;
 #pragma unroll
-    for (int j = 0; j < L; ++j) d2 += g[j];
+    for (int j = 0; j < L; ++j) d2 += shfl_d(p, src + j);
     return d2;
   }
 };
@@ -1332,17 +1344,11 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
   const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + wib;  // global warp index
   if (wg * R >= E) return;  // whole warp past the last replica
   SW w;
-  {
-    char* wb = reinterpret_cast<char*>(ws_smem) + 256 * sizeof(unsigned long long) + wib * kSegWarpBytes;
-    w.qv = reinterpret_cast<float*>(wb);
-    w.sq = reinterpret_cast<double*>(wb + kSegSlots * C * 4);
-    w.mb = reinterpret_cast<double*>(wb + kSegSlots * C * 4 + kSegSlots * C * 8);
-    w.gp = reinterpret_cast<double*>(wb + kSegSlots * C * 4 + kSegSlots * C * 8 + 34 * 4 * 8);
-  }
   w.lane = lane;
   w.seg = lane / L;
   w.sl = lane % L;
   w.used = w.seg < R;  // lanes of the scratch segment R (if any) compute but never store
+  w.src = (w.used ? w.seg : R - 1) * L;  // scratch lanes read a real segment (values unused)
   w.load_coefficients();
   const int seg = w.used ? w.seg : R - 1, sl = w.sl;
   const int64_t e_raw = wg * R + seg;
@@ -1379,6 +1385,7 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
   const float* const p_act = reinterpret_cast<const float*>(a.act) + e * D + sl * C;
   float* const p_obs = a.obs + e * (D + 1) + sl * C;
   auto load_act = [&](int c, float (&v)[C]) {
+    if (c >= T) return;
     const float* p = p_act + (size_t)c * sE * D;
     if constexpr (D % 4 == 0) {
       const float4 t = __ldcg(reinterpret_cast<const float4*>(p));
@@ -1388,13 +1395,8 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       for (int i = 0; i < C; ++i) v[i] = w.valid(i) ? __ldcg(p + i) : 0.0f;
     }
   };
-  float an[C];
-  load_act(0, an);
-  for (int c = 0; c < T; ++c) {
-    float ak[C];
-#pragma unroll
-    for (int i = 0; i < C; ++i) ak[i] = an[i];
-    if (c + 1 < T) load_act(c + 1, an);
+  // one fused step at slot c with the (prefetched) action ak
+  auto one = [&](const int c, const float (&ak)[C]) {
     const size_t idx = (size_t)c * sE + (size_t)e;
     // pre-step observation (q, E(q))
     if (w.used) {
@@ -1468,7 +1470,26 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       if (d) Ecur = Er;
     }
     if ((c & 31) == 31 || c == T - 1) cta.push(lane, c >> 5, 0, c & 31, c & ~31, a.stats);
+  };
+  float a0[C] = {}, a1[C] = {}, a2[C] = {}, a3[C] = {};
+  load_act(0, a0);
+  load_act(1, a1);
+  load_act(2, a2);
+  load_act(3, a3);
+  int c = 0;
+  for (; c + 4 <= T; c += 4) {  // four steps per trip, each step's action loaded four steps ahead
+    one(c, a0);
+    load_act(c + 4, a0);
+    one(c + 1, a1);
+    load_act(c + 5, a1);
+    one(c + 2, a2);
+    load_act(c + 6, a2);
+    one(c + 3, a3);
+    load_act(c + 7, a3);
   }
+  if (c < T) one(c, a0);
+  if (c + 1 < T) one(c + 1, a1);
+  if (c + 2 < T) one(c + 2, a2);
   if (live) {
 #pragma unroll
     for (int i = 0; i < C; ++i) {
@@ -1485,6 +1506,38 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       a.ep_ret[e] = ep_ret;
       if (err) atomicOr(a.err, err);
     }
+  }
+}
+
+// test hook (ws_test_surface_energy): the segmented energy on arbitrary states, one warp per
+// R states
+template <int D>
+__global__ void __launch_bounds__(128) k_test_surface_energy(const float* q, int64_t n, float* energy, double* spring) {
+  using SW = SurfSegWarp<D>;
+  constexpr int C = SW::C, L = SW::L, R = SW::R;
+  const int lane = threadIdx.x & 31;
+  const int64_t wg = (int64_t)blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
+  if (wg * R >= n) return;
+  SW w;
+  w.lane = lane;
+  w.seg = lane / L;
+  w.sl = lane % L;
+  w.used = w.seg < R;
+  w.src = (w.used ? w.seg : R - 1) * L;
+  w.load_coefficients();
+  const int seg = w.used ? w.seg : R - 1;
+  const int64_t i = min(wg * R + seg, n - 1);
+  float v[C];
+#pragma unroll
+  for (int c = 0; c < C; ++c) {
+    const int k = w.sl * C + c;
+    v[c] = k < D ? q[i * D + k] : 0.0f;
+  }
+  double sp = 0.0;
+  const float en = w.energy(v, &sp);
+  if (w.used && w.sl == 0 && wg * R + seg < n) {
+    energy[i] = en;
+    spring[i] = sp;
   }
 }
 
@@ -2229,10 +2282,18 @@ static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint6
   const int wpb = l.block / 32;  // warps per CTA
   l.m(kKRollout, 0);
   {  // segments of ceil(D/4) lanes, 32 / ceil(D/4) replicas per warp
-    const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * kSegWarpBytes;
+    const size_t smem = 256 * sizeof(unsigned long long);  // CTA statistics only (energies via shuffles)
     k_rollout_surface_seg<D><<<grid_for(a.E, (int64_t)wpb * SurfSeg<D>::R), l.block, smem, l.stream>>>(a, T);
   }
   l.m(kKRollout, 1);
+  return cudaGetLastError();
+}
+
+cudaError_t launch_test_surface_energy(const float* q, int D, int64_t n, float* energy, double* spring,
+                                      cudaStream_t s) {
+#define M(DD) k_test_surface_energy<DD><<<grid_for(n, 4 * SurfSeg<DD>::R), 128, 0, s>>>(q, n, energy, spring)
+  WS_SURFACE_DISPATCH(D, M)
+#undef M
   return cudaGetLastError();
 }
 

@@ -61,6 +61,8 @@ cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* g
 cudaError_t launch_test_philox(const uint32_t* rows, int64_t n, uint32_t* out, cudaStream_t s);
 cudaError_t launch_test_sample_grid(const float* p, int n, int64_t* counts, cudaStream_t s);
 cudaError_t launch_test_unary(int fn, float p, const float* x, int64_t n, float* out, cudaStream_t s);
+cudaError_t launch_test_surface_energy(const float* q, int D, int64_t n, float* energy, double* spring,
+                                      cudaStream_t s);
 cudaError_t launch_test_exhaustive(int fa, int fb, float p, uint32_t lo, uint32_t hi, unsigned long long* mism,
                                    cudaStream_t s);
 

@@ -827,6 +827,15 @@ ws_status ws_test_unary(int32_t fn, float param, const float* x, int64_t n, floa
   return e ? WS_ERR_CUDA : WS_OK;
 }
 
+ws_status ws_test_surface_energy(const float* q, int32_t D, int64_t n, float* energy, double* spring, void* stream) {
+  if (!q || !energy || !spring || n < 0) return WS_ERR_INVALID_ARGUMENT;
+  if (D != 2 && D != 3 && D != 4 && D != 8 && D != 16 && D != 20 && D != 32) return WS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return WS_OK;
+  cudaError_t e = ws::launch_test_surface_energy(q, D, n, energy, spring, (cudaStream_t)stream);
+  if (!e) e = cudaStreamSynchronize((cudaStream_t)stream);
+  return e ? WS_ERR_CUDA : WS_OK;
+}
+
 ws_status ws_test_exhaustive(int32_t fn_a, int32_t fn_b, float param, uint32_t lo_bits, uint32_t hi_bits,
                              uint64_t* mismatches, void* stream) {
   if (!mismatches || fn_a < 0 || fn_a > 8 || fn_b < 0 || fn_b > 8 || hi_bits < lo_bits) return WS_ERR_INVALID_ARGUMENT;

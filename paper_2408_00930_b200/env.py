@@ -473,6 +473,17 @@ def ws_test_unary(fn: int, x: torch.Tensor, param: float = 0.0) -> torch.Tensor:
     return out
 
 
+def ws_test_surface_energy(q: torch.Tensor) -> tuple:
+    """(energy f32 [n], spring f64 [n]) of the device states q [n, D] by the segmented kernel's code."""
+    q = q.contiguous().float()
+    n, D = q.shape
+    en = torch.empty(n, dtype=torch.float32, device=q.device)
+    sp = torch.empty(n, dtype=torch.float64, device=q.device)
+    check(lib().ws_test_surface_energy(_ptr(q), D, n, _ptr(en), _ptr(sp),
+                                       C.c_void_p(torch.cuda.current_stream().cuda_stream)))
+    return en, sp
+
+
 def ws_test_exhaustive(fn_a: int, fn_b: int, lo_bits: int, hi_bits: int, param: float = 0.0) -> int:
     """Number of fp32 bit patterns in [lo_bits, hi_bits] where device functions differ."""
     m = C.c_uint64(0)

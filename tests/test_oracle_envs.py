@@ -7,6 +7,7 @@ tests/mechanics.py, a library ODE solver, published stationary points and the SP
 examples -- never against a re-typed copy of the oracle's own formulas.
 """
 import math
+import os
 from fractions import Fraction
 
 import numpy as np
@@ -392,3 +393,46 @@ def test_cartpole_min_episode_proof_over_reset_box():
     for k in range(8):
         _, st, _, term = O.cartpole_step(st, 0)
         assert term == (k == 7)
+
+
+def test_surface_spring_pairwise_order(oracle):
+    """R23: the spring sum is the pairwise tree over the padded leaves.  (i) Dyadic inputs
+    (every order exact) against the exact rational sum; (ii) the hand-derived order pins of
+    tests/golden/surface_spring_order.txt, where the tree equals the correctly rounded exact sum
+    and both sequential orders miss it by one ulp (a dropped, doubled or reordered term fails)."""
+    import math
+    from fractions import Fraction
+    rng = np.random.default_rng(8)
+    for D in (2, 3, 5, 8, 20, 32):
+        q = (rng.integers(-64, 65, D) / 64.0).astype(f32)
+        want = sum((Fraction(float(x)) ** 2 for x in q[2:]), Fraction(0))
+        assert oracle.surface_spring(q) == float(want)
+    with open(os.path.join(os.path.dirname(__file__), "golden", "surface_spring_order.txt")) as fh:
+        rows = [l.split() for l in fh if l.strip() and not l.startswith("#")]
+    assert len(rows) == 2
+    for r in rows:
+        D = int(r[0])
+        q = np.array([float(x) for x in r[1:1 + D]], f32)
+        S = float(r[-1])
+        assert S == math.fsum(float(x) * float(x) for x in q[2:])  # correctly rounded exact sum
+        seq = 0.0
+        for x in q[2:]:
+            seq += float(x) * float(x)
+        assert seq != S  # the left-to-right order would differ
+        assert oracle.surface_spring(q) == S
+
+
+def test_mueller_brown_pairwise_terms(oracle):
+    """R23: E_MB = (t0 + t1) + (t2 + t3).  At the published minimum A the four terms are
+    recomputed here from S:257's constants with Python's math.exp (glibc, the same libm as the
+    oracle) and the tree order must reproduce the oracle bit for bit, while the stationary-point
+    values (tests/golden/mueller_brown_stationary.txt) pin the terms themselves."""
+    import math
+    A = [-200, -100, -170, 15]; a = [-1, -1, -6.5, 0.7]; b = [0, 0, 11, 0.6]; c = [-10, -10, -6.5, 0.7]
+    x0 = [1, 0, -0.5, -1]; y0 = [0, 0.5, 1.5, 1]
+    for (x, y) in [(-0.558224, 1.441726), (0.623499, 0.028038), (-0.05, 0.47), (0.3, 0.9)]:
+        t = []
+        for k in range(4):
+            dx, dy = x - x0[k], y - y0[k]
+            t.append(A[k] * math.exp(a[k] * dx * dx + b[k] * dx * dy + c[k] * dy * dy))
+        assert oracle.mb_energy(x, y)[0] == (t[0] + t[1]) + (t[2] + t[3])
