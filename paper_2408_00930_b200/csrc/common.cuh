@@ -41,6 +41,35 @@ __device__ __forceinline__ U4 philox(uint32_t c0, uint32_t c1, uint32_t c2, uint
   return U4{c0, c1, c2, c3};
 }
 
+// Philox4x32-10 with the key schedule precomputed (ks[r] = key + r (0x9E3779B9, 0xBB67AE85)):
+// loops that draw many blocks under one key keep the 20 round keys in registers
+struct KeySchedule {
+  uint32_t k0[10], k1[10];
+};
+__device__ __forceinline__ KeySchedule key_schedule(uint32_t k0, uint32_t k1) {
+  KeySchedule ks;
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    ks.k0[r] = k0 + (uint32_t)r * 0x9E3779B9u;
+    ks.k1[r] = k1 + (uint32_t)r * 0xBB67AE85u;
+  }
+  return ks;
+}
+__device__ __forceinline__ U4 philox_ks(uint32_t c0, uint32_t c1, uint32_t c2, uint32_t c3, const KeySchedule& ks) {
+#pragma unroll
+  for (int r = 0; r < 10; ++r) {
+    const uint32_t hi0 = __umulhi(0xD2511F53u, c0), lo0 = 0xD2511F53u * c0;
+    const uint32_t hi1 = __umulhi(0xCD9E8D57u, c2), lo1 = 0xCD9E8D57u * c2;
+    const uint32_t n0 = hi1 ^ c1 ^ ks.k0[r];
+    const uint32_t n2 = hi0 ^ c3 ^ ks.k1[r];
+    c0 = n0;
+    c1 = lo1;
+    c2 = n2;
+    c3 = lo0;
+  }
+  return U4{c0, c1, c2, c3};
+}
+
 __device__ __forceinline__ uint32_t pick(const U4& v, uint32_t i) {
   return i == 0 ? v.x : (i == 1 ? v.y : (i == 2 ? v.z : v.w));
 }

@@ -445,8 +445,9 @@ __device__ __forceinline__ void plan_rows(const KArgs& a, const int T, const uin
   if ((t0 & 3) == 0) {
     // aligned: one Philox4x32 call per 4-slot group (ACTION draws j = t)
     const int g_end = c_end >> 2;  // full groups
+    const KeySchedule ks = key_schedule(key.k0, key.k1);
     for (int g = c_begin >> 2; g < g_end; ++g) {
-      const U4 w = block(key, (t0 >> 2) + (uint64_t)g, eg, 0, kAction);
+      const U4 w = philox_ks((uint32_t)((t0 >> 2) + (uint64_t)g), eg, 0, kAction, ks);
       const size_t base = (size_t)(4 * g) * sE;
       float lp0, lp1, lp2, lp3;
       const int a0 = sample(4 * g, w.x, lp0), a1 = sample(4 * g + 1, w.y, lp1);

@@ -133,30 +133,36 @@ __device__ __forceinline__ void make_thresholds(const RowCDF<N>& r, Thresholds<N
 #pragma unroll
   for (int i = 0; i < N; ++i) {
     if (r.P[i] > 0.0f) th.nzmask |= 1u << i;
-    uint32_t lo = 0, hi = 1u << 24;  // smallest k with !(k 2^-24 S < C_i)
+    // smallest k in [0, 2^24] with !(k 2^-24 S < C_i): the monotone predicate is evaluated at
+    // the estimate ceil(C_i / S 2^24) and the estimate stepped until it is the boundary --
+    // the same K as a bisection on the predicate, in a few evaluations instead of 24
+    auto below = [&](uint32_t k) { return (double)((float)k * (1.0f / 16777216.0f)) * S < r.C[i]; };
+    uint32_t k = 0;
     if (!r.bad) {
-      while (lo < hi) {
-        const uint32_t mid = (lo + hi) >> 1;
-        const double target = (double)((float)mid * (1.0f / 16777216.0f)) * S;
-        if (target < r.C[i]) lo = mid + 1; else hi = mid;
-      }
+      const double est = ceil(r.C[i] / S * 16777216.0);
+      k = est <= 0.0 ? 0u : (est >= 16777216.0 ? (1u << 24) : (uint32_t)est);
+      while (k < (1u << 24) && below(k)) ++k;
+      while (k > 0 && !below(k - 1)) --k;
     }
-    th.K[i] = lo;
+    th.K[i] = k;
     th.lp[i] = (r.P[i] > 0.0f && !r.bad) ? (float)(log((double)r.P[i]) - log(S)) : 0.0f;
   }
 }
 
+// Hoisted search = #{i < N-1 : K_i <= k}.  K is nondecreasing (C is, under the same monotone
+// predicate) and K_{last nonzero} = 2^24 > k (u S < S for u < 1), so the count is min{i : k < K_i};
+// that i has p_i > 0 (a zero-probability action has C_i = C_{i-1}, hence K_i = K_{i-1}, and
+// p_0 = 0 gives K_0 = 0), i.e. exactly R13's min{i : p_i > 0 and u S < C_i} -- the fallback is
+// never needed for a valid row.  (Exhaustively checked against the direct search by
+// ws_test_sample_grid.)
 template <int N>
 __device__ __forceinline__ int search_k(const Thresholds<N>& th, uint32_t k, float& lp) {
-  int a = -1;
+  int a = 0;
 #pragma unroll
-  for (int i = 0; i < N; ++i)
-    if (a < 0 && ((th.nzmask >> i) & 1u) && k < th.K[i]) a = i;
-  if (a < 0) a = th.fallback;
+  for (int i = 0; i < N - 1; ++i) a += k >= th.K[i] ? 1 : 0;
   lp = th.lp[0];
 #pragma unroll
-  for (int i = 1; i < N; ++i)
-    if (a == i) lp = th.lp[i];
+  for (int i = 1; i < N; ++i) lp = a == i ? th.lp[i] : lp;
   return a;
 }
 

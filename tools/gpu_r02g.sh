@@ -1,0 +1,3 @@
+timeout 900 python -m pytest tests/test_gpu_parity.py tests/test_gpu_kernels.py -x -q > gpurun_out/r02g_parity.log 2>&1; tail -2 gpurun_out/r02g_parity.log
+show() { tail -1 $1 | python -c "import json,sys; d=json.loads(sys.stdin.read()); r=d['roofline']; print('$2', round(d['ms_per_step'],4), round(d['sustained']['ms_per_step'],4), r['kernel_ms'], r['other_kernels'].get('plan',{}).get('ms'), r['ws_rollout_call'])"; }
+for w in C2 C2S C3a D0; do python bench.py --workload $w --no-cpu-baseline --sustain-s 0.3 > gpurun_out/r02g_$w.log 2>&1; show gpurun_out/r02g_$w.log $w; done
