@@ -69,6 +69,7 @@ struct Lane<CartPole> {
   __device__ static bool valid(int a) { return CartPole::valid(a); }
   // natural episodes last >= 8 steps (tests/test_oracle_envs.py::test_cartpole_min_episode_length)
   static constexpr int kMinEpisode = 8;
+  static constexpr bool kRolled = false;
   // two builds of the fused roll-out (section 5): latency (few warps: unconstrained registers for
   // the deepest schedule) and throughput (many warps: register budget for occupancy)
   static constexpr int kMaxThreads = 256;
@@ -125,6 +126,7 @@ struct Lane<Acrobot> {
   }
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
   static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
+  static constexpr bool kRolled = true;  // ~1000-instruction step: a rolled loop keeps the I-cache warm
   // throughput build: an 8-row statistics window and <= 80 registers give 6 resident CTAs of
   // 128 threads per SM (C3a 100K: one wave); latency build: 32 rows, unconstrained registers
   static constexpr int kMaxThreads = 128;
@@ -162,6 +164,7 @@ struct Lane<Dummy> {
   __device__ static void obs_vals(const St&, const Aux&, float (&o)[4]) { o[0] = o[1] = o[2] = o[3] = 0.0f; }
   __device__ static bool valid(int a) { return a == 0 || a == 1; }
   static constexpr int kMinEpisode = 1 << 30;  // episodes end by truncation only
+  static constexpr bool kRolled = false;
   static constexpr int kMaxThreads = 256;
   static constexpr int kWinRowsLat = 32, kWinRowsThr = 32, kMinBlocksThr = 0;  // 0: no register cap hint
   __device__ static bool fast_ok(const St&) { return true; }
@@ -641,8 +644,33 @@ struct DiscreteRunner {
     flush_after(4 * j + 7);
   }
 
+  // rolled loop for envs whose step is long (Acrobot: RK4 with 12 fp64 sincos): one step body
+  // in the instruction stream instead of eight, so the loop stays resident in the instruction
+  // cache; the same refill-per-4-steps and second-reset logic as the trips' slow path
+  __device__ __forceinline__ void run_rolled() {
+    const int ng = (T + 3) / 4;
+    uint32_t A = ld(0);
+#pragma unroll 1
+    for (int j = 0; j < ng; ++j) {
+      const uint32_t p = A;
+      A = ld(j + 1);
+      refill();
+      const int n = min(4, T - 4 * j);
+#pragma unroll 1
+      for (int k = 0; k < n; ++k) {
+        const int c = 4 * j + k;
+        step<false, false>(c, (size_t)c * sE, act_of(p, k));
+        flush_after(c);
+      }
+    }
+  }
+
   template <bool kFast>
   __device__ __forceinline__ void run() {
+    if constexpr (L::kRolled) {
+      run_rolled();
+      return;
+    }
     const int nfull = T >> 2;  // full 4-step blocks
     uint32_t A0 = ld(0), A1 = ld(1);
     int j = 0;
