@@ -79,6 +79,7 @@ def lib():
             "wso_rollout": (I, [P, I, P, I64, I64, P, P, I]),
             "wso_rollout_policy": (I, [P, I, P, I, I]),
             "wso_policy_probs": (I, [P, I, I, I, P, I64, P]),
+            "wso_policy_logits": (I, [P, I, I, I, P, I64, P]),
             "wso_gae_f32": (I, [I, I64, I, P, P, P, P, P, F, F, P, P]),
             "wso_gae_f64": (I, [I, I64, I, P, P, P, P, P, D, D, P, P]),
             "wso_synchronize": (I, [P]),
@@ -129,6 +130,15 @@ def sample_discrete(p, u: float):
     a = np.zeros(1, np.int32); lp = np.zeros(1, np.float32); amb = np.zeros(1, np.int32)
     st = lib().wso_sample_discrete(_p(pa), len(pa), np.float32(u), _p(a), _p(lp), _p(amb))
     return st, int(a[0]), float(lp[0]), bool(amb[0])
+
+
+def policy_logits(weights, D: int, H: int, N: int, obs) -> np.ndarray:
+    """Second-layer outputs (R29' quarter sums) of observations [n, D] -> [n, N]."""
+    weights = np.ascontiguousarray(weights, dtype=np.float32)
+    obs = np.ascontiguousarray(obs, dtype=np.float32).reshape(-1, D)
+    out = np.zeros((obs.shape[0], N), np.float32)
+    assert lib().wso_policy_logits(_p(weights), D, H, N, _p(obs), obs.shape[0], _p(out)) == 0
+    return out
 
 
 def policy_probs(weights, D: int, H: int, N: int, obs) -> np.ndarray:

@@ -447,27 +447,47 @@ const int ERRBIT_ACTION = 1, ERRBIT_PROBS = 2;
  * memory", "roll-outs, action inference, reset and training"): a two-layer MLP policy
  * obs[D] -> ReLU(W1^T obs + b1)[H] -> logits W2^T h + b2 [N] -> softmax -> probabilities.
  * Reading R29 (DESIGN): fp32 with fused multiply-adds in a fixed order -- h_j = b1_j, then
- * h_j = fma(W1[k][j], obs_k, h_j) for k = 0..D-1, h_j = h_j > 0 ? h_j : 0; l_i = b2_i, then
- * l_i = fma(W2[j][i], h_j, l_i) for j = 0..H-1; m = max_i l_i (first wins); e_i = (float)
+ * h_j = fma(W1[k][j], obs_k, h_j) for k = 0..D-1, h_j = h_j > 0 ? h_j : 0; every output i
+ * of the second layer (R29', DESIGN): the hidden units are split into four quarters
+ * Q_q = [q H/4, (q+1) H/4), P_q = 0, then P_q = fma(W2[j][i], h_j, P_q) for j in Q_q ascending,
+ * and l_i = b2_i + ((P_0 + P_1) + (P_2 + P_3)); m = max_i l_i (first wins); e_i = (float)
  * exp((double)(l_i - m)) (R3); S = e_0 + e_1 + ... in fp32; p_i = e_i / S.  Packed weights:
  * W1 [D][H] | b1 [H] | W2 [H][N] | b2 [N], row-major fp32.
  * ------------------------------------------------------------------------------------- */
-static void policy_probs(const float* w, int D, int H, int N, const float* obs, float* p) {
+/* R29' second-layer output: b + ((P_0 + P_1) + (P_2 + P_3)) over the four quarters of the
+ * hidden units (W2 column i with row stride `stride`) */
+static float quarter_dot(const float* W2col, int stride, const float* h, int H, float b) {
+  float P[4];
+  const int Hq = H / 4;
+  for (int q = 0; q < 4; ++q) {
+    float acc = 0.0f;
+    for (int j = q * Hq; j < (q + 1) * Hq; ++j) acc = std::fma(W2col[(size_t)j * stride], h[j], acc);
+    P[q] = acc;
+  }
+  return b + ((P[0] + P[1]) + (P[2] + P[3]));
+}
+
+static void policy_hidden(const float* w, int D, int H, const float* obs, float* h) {
   const float* W1 = w;
   const float* b1 = W1 + (size_t)D * H;
-  const float* W2 = b1 + H;
-  const float* b2 = W2 + (size_t)H * N;
-  std::vector<float> h((size_t)H), l((size_t)N);
   for (int j = 0; j < H; ++j) {
     float acc = b1[j];
     for (int k = 0; k < D; ++k) acc = std::fma(W1[(size_t)k * H + j], obs[k], acc);
     h[j] = acc > 0.0f ? acc : 0.0f;
   }
-  for (int i = 0; i < N; ++i) {
-    float acc = b2[i];
-    for (int j = 0; j < H; ++j) acc = std::fma(W2[(size_t)j * N + i], h[j], acc);
-    l[i] = acc;
-  }
+}
+
+static void policy_logits(const float* w, int D, int H, int N, const float* obs, float* l) {
+  const float* W2 = w + (size_t)D * H + H;
+  const float* b2 = W2 + (size_t)H * N;
+  std::vector<float> h((size_t)H);
+  policy_hidden(w, D, H, obs, h.data());
+  for (int i = 0; i < N; ++i) l[i] = quarter_dot(W2 + i, N, h.data(), H, b2[i]);
+}
+
+static void policy_probs(const float* w, int D, int H, int N, const float* obs, float* p) {
+  std::vector<float> l((size_t)N);
+  policy_logits(w, D, H, N, obs, l.data());
   float m = l[0];
   for (int i = 1; i < N; ++i) m = l[i] > m ? l[i] : m;
   float S = 0.0f;
@@ -1100,8 +1120,13 @@ int wso_gae_f64(int T, int64_t E, int A, const double* rew, const uint8_t* done,
 }
 
 /* NEXT-N1: probabilities of the MLP policy for n observations [n][D] -> out [n][N] */
+int wso_policy_logits(const float* weights, int D, int H, int N, const float* obs, int64_t n, float* out) {
+  if (!weights || !obs || !out || D < 1 || H < 4 || H % 4 || N < 1 || n < 0) return E_INVALID_ARGUMENT;
+  for (int64_t r = 0; r < n; ++r) policy_logits(weights, D, H, N, obs + r * D, out + r * N);
+  return 0;
+}
 int wso_policy_probs(const float* weights, int D, int H, int N, const float* obs, int64_t n, float* out) {
-  if (!weights || !obs || !out || D < 1 || H < 1 || N < 1) return E_INVALID_ARGUMENT;
+  if (!weights || !obs || !out || D < 1 || H < 4 || H % 4 || N < 1) return E_INVALID_ARGUMENT;
   for (int64_t r = 0; r < n; ++r) policy_probs(weights, D, H, N, obs + r * D, out + r * N);
   return E_OK;
 }
@@ -1110,7 +1135,7 @@ int wso_policy_probs(const float* weights, int D, int H, int N, const float* obs
  * pre-step observation obs_live (single-agent discrete envs); otherwise as wso_rollout. */
 int wso_rollout_policy(void* h, int T, const float* weights, int H, int n_threads) {
   Batch* b = (Batch*)h;
-  if (T < 1 || !weights || H < 1 || b->n_actions < 1) return E_INVALID_ARGUMENT;
+  if (T < 1 || !weights || H < 4 || H % 4 || b->n_actions < 1) return E_INVALID_ARGUMENT;  // R29' quarters
   if (T > b->T_cap) return E_OUT_OF_RANGE;
   if (n_threads < 1) n_threads = 1;
   if (n_threads > b->E) n_threads = (int)b->E;
@@ -1152,8 +1177,9 @@ int wso_rollout_policy(void* h, int T, const float* weights, int H, int n_thread
 }
 
 /* NEXT-N1 for continuous actions (reading R34): a Gaussian policy -- the R29 network with d
- * linear outputs as the mean (mean_i = b2_i, then fma(W2[j][i], h_j, mean_i) for j = 0..H-1)
- * and a learned, state-independent log standard deviation vector; packed weights
+ * linear outputs as the mean (mean_i = b2_i + ((P_0 + P_1) + (P_2 + P_3)), the R29' quarter
+ * sums of fma(W2[j][i], h_j, .)) and a learned, state-independent log standard deviation vector;
+ * packed weights
  * W1 [D][H] | b1 [H] | W2 [H][d] | b2 [d] | log_std [d].  Each step the replica's head row
  * (mean | log_std) is sampled by the R14 Gaussian head exactly as a given row would be. */
 static void policy_gauss_row(const float* w, int D, int H, int d, const float* obs, float* row) {
@@ -1162,16 +1188,11 @@ static void policy_gauss_row(const float* w, int D, int H, int d, const float* o
   const float* W2 = b1 + H;
   const float* b2 = W2 + (size_t)H * d;
   const float* log_std = b2 + d;
+  (void)b1;
   std::vector<float> h((size_t)H);
-  for (int j = 0; j < H; ++j) {
-    float acc = b1[j];
-    for (int k = 0; k < D; ++k) acc = std::fma(W1[(size_t)k * H + j], obs[k], acc);
-    h[j] = acc > 0.0f ? acc : 0.0f;
-  }
+  policy_hidden(w, D, H, obs, h.data());
   for (int i = 0; i < d; ++i) {
-    float acc = b2[i];
-    for (int j = 0; j < H; ++j) acc = std::fma(W2[(size_t)j * d + i], h[j], acc);
-    row[i] = acc;
+    row[i] = quarter_dot(W2 + i, d, h.data(), H, b2[i]);
     row[d + i] = log_std[i];
   }
 }
@@ -1183,7 +1204,7 @@ int wso_policy_gauss_rows(const float* weights, int D, int H, int d, const float
 
 int wso_rollout_policy_gauss(void* h, int T, const float* weights, int H, int n_threads) {
   Batch* b = (Batch*)h;
-  if (T < 1 || !weights || H < 1 || b->A != 1 || b->n_actions != 0) return E_INVALID_ARGUMENT;
+  if (T < 1 || !weights || H < 4 || H % 4 || b->A != 1 || b->n_actions != 0) return E_INVALID_ARGUMENT;
   if (T > b->T_cap) return E_OUT_OF_RANGE;
   if (n_threads < 1) n_threads = 1;
   if (n_threads > b->E) n_threads = (int)b->E;

@@ -283,6 +283,7 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
     ws_row_init(p0, row);
   }
   const int kHH = kH > 0 ? kH : 1;
+  const int kHQ = kHH >= 4 ? kHH / 4 : 1;  /* R29' quarter size */
   const float* W1 = sw;                       /* [D][H] */
   const float* b1 = W1 + WS_D * kHH;          /* [H] */
   const float* W2 = b1 + kHH;                 /* [H][N] */
@@ -324,16 +325,23 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
 #else
     if (kH > 0) {
 #endif
-      float lg[WS_N];
-      for (int i = 0; i < WS_N; ++i) lg[i] = b2[i];
-      float v = kCritic ? wv[kHH] : 0.0f;
+      /* R29': second layer as four quarter chains P_q from +0, l = b2 + ((P0 + P1) + (P2 + P3)) */
+      float lg[WS_N], Pq[4][WS_N], Pv[4];
+      for (int qq = 0; qq < 4; ++qq) {
+        Pv[qq] = 0.0f;
+        for (int i = 0; i < WS_N; ++i) Pq[qq][i] = 0.0f;
+      }
       for (int j = 0; j < kHH; ++j) {
         float acc = b1[j];
         for (int k = 0; k < WS_D; ++k) acc = __fmaf_rn(W1[k * kHH + j], o[k], acc);
         const float hj = acc > 0.0f ? acc : 0.0f;
-        for (int i = 0; i < WS_N; ++i) lg[i] = __fmaf_rn(W2[j * WS_N + i], hj, lg[i]);
-        if (kCritic) v = __fmaf_rn(wv[j], hj, v);
+        const int qq = j / kHQ;
+        for (int i = 0; i < WS_N; ++i) Pq[qq][i] = __fmaf_rn(W2[j * WS_N + i], hj, Pq[qq][i]);
+        if (kCritic) Pv[qq] = __fmaf_rn(wv[j], hj, Pv[qq]);
       }
+      for (int i = 0; i < WS_N; ++i)
+        lg[i] = __fadd_rn(b2[i], __fadd_rn(__fadd_rn(Pq[0][i], Pq[1][i]), __fadd_rn(Pq[2][i], Pq[3][i])));
+      const float v = kCritic ? __fadd_rn(wv[kHH], __fadd_rn(__fadd_rn(Pv[0], Pv[1]), __fadd_rn(Pv[2], Pv[3]))) : 0.0f;
       if (kCritic && live) __stcs(values + idx, v);
       float m = lg[0];
       for (int i = 1; i < WS_N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -403,14 +411,14 @@ WS_FN void ws_run(const WsUserArgs& a, int T, ws_u64 t0, const float* probs, ws_
       }
     }
   }
-  if (kCritic) {  /* bootstrap value of the observation after the last step */
-    float v = wv[kHH];
+  if (kCritic) {  /* bootstrap value of the observation after the last step (R29' quarters) */
+    float Pv[4] = {0.0f, 0.0f, 0.0f, 0.0f};
     for (int j = 0; j < kHH; ++j) {
       float acc = b1[j];
       for (int k = 0; k < WS_D; ++k) acc = __fmaf_rn(W1[k * kHH + j], o[k], acc);
-      v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
+      Pv[j / kHQ] = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, Pv[j / kHQ]);
     }
-    if (live) bootstrap[e] = v;
+    if (live) bootstrap[e] = __fadd_rn(wv[kHH], __fadd_rn(__fadd_rn(Pv[0], Pv[1]), __fadd_rn(Pv[2], Pv[3])));
   }
   if (live) {
     for (int i = 0; i < WS_S; ++i) a.state[e * WS_S + i] = s[i];

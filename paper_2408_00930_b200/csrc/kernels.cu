@@ -760,20 +760,110 @@ __global__ void __launch_bounds__(Lane<Env>::kMaxThreads, kLat ? 1 : Lane<Env>::
   rollout_discrete_body<Env, kLat>(a, T);
 }
 
+// R29' second-layer output evaluated in one lane: b + ((P_0 + P_1) + (P_2 + P_3)), P_q the fma
+// chain from +0 over the q-th quarter of the hidden units (column w with row stride `stride`)
+template <int H>
+__device__ __forceinline__ float quarter_dot(const float* w, int stride, const float (&h)[H], float b) {
+  constexpr int HQ = H / 4;
+  float P[4];
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    float acc = 0.0f;
+#pragma unroll
+    for (int u = 0; u < HQ; ++u) acc = __fmaf_rn(w[(q * HQ + u) * stride], h[q * HQ + u], acc);
+    P[q] = acc;
+  }
+  return fadd(b, fadd(fadd(P[0], P[1]), fadd(P[2], P[3])));
+}
+
 // =======================================================================================
 // NEXT-N1: fused roll-out with in-kernel policy inference ("operating an agent that
 // samples actions", "roll-outs, action inference, reset and training" on one GPU
-// store).  Each lane runs its replica's two-layer MLP on the pre-step observation
-// (weights in shared memory, fp32 FMAs in the fixed order of reading R29), softmax (R3
-// exponentials), the R13 inverse-CDF draw from the ACTION stream (R15), then the dynamics,
-// reward / done, auto-reset and all stores of k_rollout_discrete.  Actions now depend on
-// the state, so there is no plan kernel.  The network is tiny (D x H + H x N MACs per
-// replica-step) and per-replica, so it runs on the FMA pipe rather than the tensor cores.
+// store).  A QUAD of four lanes runs each replica: lane q of the quad evaluates the q-th
+// quarter of the hidden units (reading R29': h_j in the R29 order, the second layer as four
+// quarter chains P_q combined by ((P_0 + P_1) + (P_2 + P_3)) -- two xor-shuffle levels, which
+// every lane of the quad ends with bit-identically because fp32 addition is commutative), so a
+// warp advances 8 replicas and C2P's 10K replicas fill 1252 warps (~2 per scheduler) instead of
+// 313.  The softmax (R3 exponentials), the R13 draw from the ACTION stream (R15), the dynamics,
+// reward / done and auto-reset run redundantly in the four lanes (identical values); the
+// quad's lane 0 stores.  Weights sit in shared memory as per-unit records (W1 column, b1, W2
+// row, wv), interleaved by quarter so the quad's four LDS.128 hit distinct banks.  The
+// network is tiny and per-replica, so it runs on the FMA pipe rather than the tensor cores.
 // =======================================================================================
 // kCritic (NEXT-N2, R31): the weights carry a value head wv [H] | bv after b2 and the kernel
 // also writes values[t][e] = V(obs[t]) (the pre-step observation of slot t) and, after the
-// last step, bootstrap[e] = V(obs_live): v = bv, then v = fma(wv_j, h_j, v) for j = 0..H-1,
-// from the hidden layer the policy already computed (no second pass over the store).
+// last step, bootstrap[e] = V(obs_live), V = bv + the R29' quarter sums of fma(wv_j, h_j, .).
+template <int D, int N, int H, bool kCritic>
+struct QuadMLP {
+  static constexpr int HQ = H / 4;
+  static constexpr int kRec = ((D + 1 + N + (kCritic ? 1 : 0)) + 3) / 4 * 4;  // floats per unit record
+  static constexpr int kWords = H * kRec + N + 1;                               // records | b2 | bv
+  const float* rec;  // this lane's quarter: record of unit u at rec + u * 4 * kRec
+  const float* b2;
+  float bv;
+  // smem image: unit j = q HQ + u -> record (u * 4 + q)
+  __device__ static void load(float* s, const float* w, int tid, int nthr) {
+    const float* W1 = w;
+    const float* b1 = W1 + D * H;
+    const float* W2 = b1 + H;
+    const float* b2g = W2 + H * N;
+    const float* wv = b2g + N;
+    for (int i = tid; i < kWords; i += nthr) {
+      float v = 0.0f;
+      if (i < H * kRec) {
+        const int r = i / kRec, f = i - r * kRec;
+        const int u = r >> 2, q = r & 3, j = q * HQ + u;
+        if (f < D) v = W1[f * H + j];
+        else if (f == D) v = b1[j];
+        else if (f < D + 1 + N) v = W2[j * N + (f - D - 1)];
+        else if (kCritic && f == D + 1 + N) v = wv[j];
+      } else if (i < H * kRec + N) {
+        v = b2g[i - H * kRec];
+      } else {
+        v = kCritic ? wv[H] : 0.0f;
+      }
+      s[i] = v;
+    }
+  }
+  __device__ void bind(const float* s, int q) {
+    rec = s + q * kRec;
+    b2 = s + H * kRec;
+    bv = s[H * kRec + N];
+  }
+  // quad-collective: logits (and V) of observation o
+  __device__ __forceinline__ void eval(const float (&o)[D], float (&lg)[N], float& v) const {
+    float P[N], Pv = 0.0f;
+#pragma unroll
+    for (int i = 0; i < N; ++i) P[i] = 0.0f;
+#pragma unroll
+    for (int u = 0; u < HQ; ++u) {
+      const float* r = rec + u * 4 * kRec;
+      float w[kRec];
+#pragma unroll
+      for (int f = 0; f < kRec; f += 4) {
+        const float4 t = *reinterpret_cast<const float4*>(r + f);
+        w[f] = t.x; w[f + 1] = t.y; w[f + 2] = t.z; w[f + 3] = t.w;
+      }
+      float acc = w[D];
+#pragma unroll
+      for (int k = 0; k < D; ++k) acc = __fmaf_rn(w[k], o[k], acc);
+      const float hj = acc > 0.0f ? acc : 0.0f;
+#pragma unroll
+      for (int i = 0; i < N; ++i) P[i] = __fmaf_rn(w[D + 1 + i], hj, P[i]);
+      if (kCritic) Pv = __fmaf_rn(w[D + 1 + N], hj, Pv);
+    }
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float t = fadd(P[i], __shfl_xor_sync(kFull, P[i], 1));  // P_q + P_{q^1}
+      lg[i] = fadd(b2[i], fadd(t, __shfl_xor_sync(kFull, t, 2)));    // b2 + ((P0+P1) + (P2+P3))
+    }
+    if (kCritic) {
+      const float t = fadd(Pv, __shfl_xor_sync(kFull, Pv, 1));
+      v = fadd(bv, fadd(t, __shfl_xor_sync(kFull, t, 2)));
+    }
+  }
+};
+
 template <class Env, int H, bool kCritic>
 __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int T, const uint64_t t0,
                                                        const float* __restrict__ weights,
@@ -782,24 +872,21 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
   using L = Lane<Env>;
   using St = typename L::St;
   constexpr int D = L::D, N = L::N;
-  constexpr int NW = D * H + H + H * N + N + (kCritic ? H + 1 : 0);
+  using M = QuadMLP<D, N, H, kCritic>;
   constexpr int kRows = 16;
-  __shared__ __align__(16) float sw[NW];
+  __shared__ __align__(16) float sw[M::kWords];
   extern __shared__ __align__(16) uint32_t ws_smem[];
-  for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = weights[i];
+  M::load(sw, weights, threadIdx.x, blockDim.x);
   __syncthreads();
-  const float* W1 = sw;
-  const float* b1 = W1 + D * H;
-  const float* W2 = b1 + H;
-  const float* b2 = W2 + H * N;
-  const float* wv = b2 + N;  // kCritic only
-  const int lane = threadIdx.x & 31;
-  const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int lane = threadIdx.x & 31, q = lane & 3;
+  M mlp;
+  mlp.bind(sw, q);
+  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2;  // replica of this quad
   const int64_t E = a.E;
-  if (e - lane >= E) return;  // whole warp past the last replica
+  if (e - (lane >> 2) >= E) return;  // whole warp past the last replica
   const bool live = e < E;
-  const int64_t ec = live ? e : E - 1;  // tail lanes shadow replica E-1 (identical stores)
-  const int nlive = (int)min((int64_t)32, E - (e - lane));
+  const bool writer = live && q == 0;   // the quad's lane 0 stores
+  const int64_t ec = live ? e : E - 1;  // tail quads shadow replica E-1 (identical values)
   const uint32_t eg = (uint32_t)(a.offset + ec);
   const Key key{a.k0, a.k1};
   const size_t sE = (size_t)E;
@@ -813,36 +900,18 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
   float ep_ret = a.ep_ret[ec];
   uint32_t err = 0;
   U4 w4{0, 0, 0, 0};
+  int32_t* const p_act = reinterpret_cast<int32_t*>(a.act);
   for (int c = 0; c < T; ++c) {
     const uint64_t t = t0 + (uint64_t)c;
     if (c == 0 || (t & 3) == 0) w4 = block(key, t >> 2, eg, 0, kAction);
     const size_t idx = (size_t)c * sE + (size_t)ec;
-    L::obs_store_aux(a.obs + idx * L::D, s, aux, true);
-    // ---- inference: h = relu(W1^T o + b1), l = W2^T h + b2, p = softmax(l)
+    if (writer) L::obs_store_aux(a.obs + idx * L::D, s, aux, true);
+    // ---- inference: h = relu(W1^T o + b1) (this lane's quarter), logits / V by the quad
     float o[D];
     L::obs_vals(s, aux, o);
-    float hid[H];
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-      float acc = b1[j];
-#pragma unroll
-      for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
-      hid[j] = acc > 0.0f ? acc : 0.0f;
-    }
-    if constexpr (kCritic) {
-      float v = wv[H];
-#pragma unroll
-      for (int j = 0; j < H; ++j) v = __fmaf_rn(wv[j], hid[j], v);
-      if (live) st_cs(values + idx, v);
-    }
-    float lg[N];
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      float acc = b2[i];
-#pragma unroll
-      for (int j = 0; j < H; ++j) acc = __fmaf_rn(W2[j * N + i], hid[j], acc);
-      lg[i] = acc;
-    }
+    float lg[N], vv = 0.0f;
+    mlp.eval(o, lg, vv);
+    if (kCritic && writer) st_cs(values + idx, vv);
     float m = lg[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -880,10 +949,12 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     if (cdf.bad) {
       act = -1;
       lp = __int_as_float(0x7fc00000);
-      if (live) err |= kErrProbs | kErrAction;
+      if (writer) err |= kErrProbs | kErrAction;
     }
-    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
-    if (a.write_logp) st_cs(a.logp + idx, lp);
+    if (writer) {
+      st_cs(p_act + idx, act);
+      if (a.write_logp) st_cs(a.logp + idx, lp);
+    }
     // ---- A3-A5
     const bool bad = act < 0;
     St s2 = s;
@@ -901,18 +972,11 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
       ep_step = es;
       ep_ret = ret;
     }
-    if (kCritic && values_trunc && d == 2u) {  // truncated only: V of the post-step state
-      float o2[D];
+    if (kCritic && values_trunc && __any_sync(kFull, d == 2u)) {  // truncated only: V of the post-step state
+      float o2[D], lg2[N], v2 = 0.0f;
       L::obs_vals(s, aux, o2);
-      float v = wv[H];
-#pragma unroll
-      for (int j = 0; j < H; ++j) {
-        float acc = b1[j];
-#pragma unroll
-        for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o2[k], acc);
-        v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
-      }
-      if (live) st_cs(values_trunc + idx, v);
+      mlp.eval(o2, lg2, v2);
+      if (writer && d == 2u) st_cs(values_trunc + idx, v2);
     }
     if (d) {  // auto-reset (R11)
       rc += 1;
@@ -921,26 +985,21 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
       ep_step = 0;
       ep_ret = 0.0f;
     }
-    st_cs(a.rew + idx, rw);
-    st_cs_u8(a.done + idx, (uint8_t)d);
-    win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
-    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
-      win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, nlive);
+    if (writer) {
+      st_cs(a.rew + idx, rw);
+      st_cs_u8(a.done + idx, (uint8_t)d);
+    }
+    win.put(c & (kRows - 1), lane, (writer && d) ? (uint32_t)es : 0u, (writer && d) ? ret : 0.0f,
+            writer ? rw : 0.0f);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1) win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats);
   }
   if constexpr (kCritic) {  // bootstrap value of the observation after the last step
-    float o[D];
+    float o[D], lg[N], v = 0.0f;
     L::obs_vals(s, aux, o);
-    float v = wv[H];
-#pragma unroll
-    for (int j = 0; j < H; ++j) {
-      float acc = b1[j];
-#pragma unroll
-      for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
-      v = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, v);
-    }
-    if (live) bootstrap[e] = v;
+    mlp.eval(o, lg, v);
+    if (writer) bootstrap[e] = v;
   }
-  if (live) {
+  if (writer) {
     L::save(a.state + e * L::S, s);
     a.ep_step[e] = ep_step;
     a.reset_count[e] = rc;
@@ -1157,18 +1216,17 @@ __global__ void __launch_bounds__(128) k_rollout_gpolicy(const KArgs a, const in
   uint32_t rc = a.reset_count[ec];
   float ep_ret = a.ep_ret[ec];
   uint32_t err = 0;
-  auto head = [&](const float (&o)[3], float& mean, float& v) {
-    mean = b2[0];
-    v = kCritic ? wv[H] : 0.0f;
+  auto head = [&](const float (&o)[3], float& mean, float& v) {  // R29' quarter sums (in-lane)
+    float hid[H];
 #pragma unroll
     for (int j = 0; j < H; ++j) {
       float acc = b1[j];
 #pragma unroll
       for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
-      const float hj = acc > 0.0f ? acc : 0.0f;
-      mean = __fmaf_rn(W2[j], hj, mean);
-      if (kCritic) v = __fmaf_rn(wv[j], hj, v);
+      hid[j] = acc > 0.0f ? acc : 0.0f;
     }
+    mean = quarter_dot<H>(W2, 1, hid, b2[0]);
+    v = kCritic ? quarter_dot<H>(wv, 1, hid, wv[H]) : 0.0f;
   };
   for (int c = 0; c < T; ++c) {
     const uint64_t t = t0 + (uint64_t)c;
@@ -1772,7 +1830,7 @@ __host__ __device__ inline int tag_red_offset(int G) { return 2 * G * G + ((2 * 
 __host__ __device__ inline int tag_tab_offset(int G, int nwarps) { return tag_red_offset(G) + 6 * nwarps; }
 
 // NEXT-N1 for the multi-agent env: the R29 policy of one agent on its observation o[D]
-// (weights `sw` = W1 [D][H] | b1 | W2 [H][N] | b2 (| wv [H] | bv)), in R29's operation order:
+// (weights `sw` = W1 [D][H] | b1 | W2 [H][N] | b2 (| wv [H] | bv)), in R29 / R29's operation order:
 // the probabilities p_i = e_i / S with e_i = (float)exp((double)(l_i - m)), as the fp64-prefix
 // CDF of the R13 sampler; v = the R31 critic when kCritic.
 template <int D, int H, int N, bool kCritic>
@@ -1790,19 +1848,10 @@ __device__ __forceinline__ void policy_cdf(const float* sw, const float (&o)[D],
     for (int k = 0; k < D; ++k) acc = __fmaf_rn(W1[k * H + j], o[k], acc);
     hid[j] = acc > 0.0f ? acc : 0.0f;
   }
-  if (kCritic) {
-    v = wv[H];
+  if (kCritic) v = quarter_dot<H>(wv, 1, hid, wv[H]);
+  float lg[N];  // R29' quarter sums
 #pragma unroll
-    for (int j = 0; j < H; ++j) v = __fmaf_rn(wv[j], hid[j], v);
-  }
-  float lg[N];
-#pragma unroll
-  for (int i = 0; i < N; ++i) {
-    float acc = b2[i];
-#pragma unroll
-    for (int j = 0; j < H; ++j) acc = __fmaf_rn(W2[j * N + i], hid[j], acc);
-    lg[i] = acc;
-  }
+  for (int i = 0; i < N; ++i) lg[i] = quarter_dot<H>(W2 + i, N, hid, b2[i]);
   float m = lg[0];
 #pragma unroll
   for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -2356,9 +2405,9 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, float* values, float* bootstrap, float* vtr) {
-  const int b = l.block < 128 ? l.block : 128;                              // launch bounds 128
+  const int b = 128;                                                        // 32 replicas (quads) per CTA
   const size_t smem = (size_t)(b / 32) * 3 * 16 * kWinStride * sizeof(uint32_t);  // per-warp 16-row windows
-  const unsigned g = grid_for(a.E, b);
+  const unsigned g = grid_for(a.E, b / 4);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {

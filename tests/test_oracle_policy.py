@@ -40,10 +40,10 @@ def test_policy_exact_on_dyadic_inputs():
     """Weights, biases and observations that are small multiples of 1/16: every product and
     partial sum is exact in fp32, so the logits equal the exact rational values and the
     probabilities follow from the softmax reading alone."""
-    D, H, N = 4, 3, 2
-    W1 = np.array([[1, -2, 0.5], [0.25, 1, -1], [0, 0.5, 2], [-1, 0.75, 1]], np.float32)
-    b1 = np.array([0.5, -0.25, 0], np.float32)
-    W2 = np.array([[1, -1], [0.5, 0.5], [-0.25, 1]], np.float32)
+    D, H, N = 4, 4, 2  # (R29': H a multiple of 4 -- the fourth hidden unit is a zero column)
+    W1 = np.array([[1, -2, 0.5, 0], [0.25, 1, -1, 0], [0, 0.5, 2, 0], [-1, 0.75, 1, 0]], np.float32)
+    b1 = np.array([0.5, -0.25, 0, 0], np.float32)
+    W2 = np.array([[1, -1], [0.5, 0.5], [-0.25, 1], [0, 0]], np.float32)
     b2 = np.array([0, 0], np.float32)
     w = np.concatenate([W1.ravel(), b1, W2.ravel(), b2]).astype(np.float32)
     obs = np.array([[0.5, -1, 0.25, 2]], np.float32)
@@ -58,7 +58,7 @@ def test_policy_exact_on_dyadic_inputs():
 
 
 def test_policy_softmax_closed_forms():
-    D, H, N = 2, 2, 4
+    D, H, N = 2, 4, 4
     w = np.zeros(D * H + H + H * N + N, np.float32)
     p = O.policy_probs(w, D, H, N, np.ones((3, D), np.float32))
     assert np.array_equal(p, np.full((3, N), 0.25, np.float32))  # equal logits: exactly uniform
@@ -149,3 +149,28 @@ def test_gauss_policy_logp_is_density_at_logged_observation():
     act = o.array("act")[:T].reshape(-1)
     ref = norm.logpdf(act.astype(np.float64), rows[:, 0].astype(np.float64), np.exp(np.float64(-0.2)))
     np.testing.assert_allclose(o.array("logp")[:T].reshape(-1), ref, rtol=1e-5, atol=1e-5)
+
+
+def test_policy_second_layer_quarter_order(oracle):
+    """R29': l_i = b2_i + ((P_0 + P_1) + (P_2 + P_3)) over the four quarters of the hidden units,
+    pinned by the hand-derived case of tests/golden/policy_quarter_order.txt (the former single
+    sequential chain gives 2^24 there, a dropped or reordered quarter another value)."""
+    import os
+    with open(os.path.join(os.path.dirname(__file__), "golden", "policy_quarter_order.txt")) as fh:
+        rows = [l for l in fh if l.strip() and not l.startswith("#")]
+    assert len(rows) == 1
+    head, rest = rows[0].split("|")
+    D, H, N = (int(x) for x in head.split())
+    b1_s, out_s = rest.split("->")
+    b1 = np.array([float(x) for x in b1_s.split()], np.float32)
+    want = np.array([float(x) for x in out_s.split()], np.float32)
+    W1 = np.zeros((D, H), np.float32)
+    W2 = np.zeros((H, N), np.float32)
+    W2[:, 0] = 1.0
+    b2 = np.array([0.0, 0.5], np.float32)
+    w = np.concatenate([W1.ravel(), b1, W2.ravel(), b2]).astype(np.float32)
+    got = oracle.policy_logits(w, D, H, N, np.zeros((1, D), np.float32))[0]
+    assert np.array_equal(got, want), (got, want)
+    # probabilities follow from these logits: p_1 = exp(0.5 - (2^24 + 8)) underflows to 0
+    p = oracle.policy_probs(w, D, H, N, np.zeros((1, D), np.float32))[0]
+    assert p[0] == 1.0 and p[1] == 0.0
