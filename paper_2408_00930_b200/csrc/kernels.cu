@@ -778,140 +778,167 @@ __device__ __forceinline__ float quarter_dot(const float* w, int stride, const f
 
 // =======================================================================================
 // NEXT-N1: fused roll-out with in-kernel policy inference ("operating an agent that
-// samples actions", "roll-outs, action inference, reset and training" on one GPU
-// store).  A QUAD of four lanes runs each replica: lane q of the quad evaluates the q-th
-// quarter of the hidden units (reading R29': h_j in the R29 order, the second layer as four
-// quarter chains P_q combined by ((P_0 + P_1) + (P_2 + P_3)) -- two xor-shuffle levels, which
-// every lane of the quad ends with bit-identically because fp32 addition is commutative), so a
-// warp advances 8 replicas and C2P's 10K replicas fill 1252 warps (~2 per scheduler) instead of
-// 313.  The softmax (R3 exponentials), the R13 draw from the ACTION stream (R15), the dynamics,
-// reward / done and auto-reset run redundantly in the four lanes (identical values); the
-// quad's lane 0 stores.  Weights sit in shared memory as per-unit records (W1 column, b1, W2
-// row, wv), interleaved by quarter so the quad's four LDS.128 hit distinct banks.  The
-// network is tiny and per-replica, so it runs on the FMA pipe rather than the tensor cores.
-// =======================================================================================
-// kCritic (NEXT-N2, R31): the weights carry a value head wv [H] | bv after b2 and the kernel
-// also writes values[t][e] = V(obs[t]) (the pre-step observation of slot t) and, after the
-// last step, bootstrap[e] = V(obs_live), V = bv + the R29' quarter sums of fma(wv_j, h_j, .).
-template <int D, int N, int H, bool kCritic>
-struct QuadMLP {
-  static constexpr int HQ = H / 4;
-  static constexpr int kRec = ((D + 1 + N + (kCritic ? 1 : 0)) + 3) / 4 * 4;  // floats per unit record
-  static constexpr int kWords = H * kRec + N + 1;                               // records | b2 | bv
-  const float* rec;  // this lane's quarter: record of unit u at rec + u * 4 * kRec
-  const float* b2;
-  float bv;
-  // smem image: unit j = q HQ + u -> record (u * 4 + q)
-  __device__ static void load(float* s, const float* w, int tid, int nthr) {
-    const float* W1 = w;
-    const float* b1 = W1 + D * H;
-    const float* W2 = b1 + H;
-    const float* b2g = W2 + H * N;
-    const float* wv = b2g + N;
-    for (int i = tid; i < kWords; i += nthr) {
-      float v = 0.0f;
-      if (i < H * kRec) {
-        const int r = i / kRec, f = i - r * kRec;
-        const int u = r >> 2, q = r & 3, j = q * HQ + u;
-        if (f < D) v = W1[f * H + j];
-        else if (f == D) v = b1[j];
-        else if (f < D + 1 + N) v = W2[j * N + (f - D - 1)];
-        else if (kCritic && f == D + 1 + N) v = wv[j];
-      } else if (i < H * kRec + N) {
-        v = b2g[i - H * kRec];
-      } else {
-        v = kCritic ? wv[H] : 0.0f;
-      }
-      s[i] = v;
-    }
-  }
-  __device__ void bind(const float* s, int q) {
-    rec = s + q * kRec;
-    b2 = s + H * kRec;
-    bv = s[H * kRec + N];
-  }
-  // quad-collective: logits (and V) of observation o
-  __device__ __forceinline__ void eval(const float (&o)[D], float (&lg)[N], float& v) const {
-    float P[N], Pv = 0.0f;
-#pragma unroll
-    for (int i = 0; i < N; ++i) P[i] = 0.0f;
-#pragma unroll
-    for (int u = 0; u < HQ; ++u) {
-      const float* r = rec + u * 4 * kRec;
-      float w[kRec];
-#pragma unroll
-      for (int f = 0; f < kRec; f += 4) {
-        const float4 t = *reinterpret_cast<const float4*>(r + f);
-        w[f] = t.x; w[f + 1] = t.y; w[f + 2] = t.z; w[f + 3] = t.w;
-      }
-      float acc = w[D];
-#pragma unroll
-      for (int k = 0; k < D; ++k) acc = __fmaf_rn(w[k], o[k], acc);
-      const float hj = acc > 0.0f ? acc : 0.0f;
-#pragma unroll
-      for (int i = 0; i < N; ++i) P[i] = __fmaf_rn(w[D + 1 + i], hj, P[i]);
-      if (kCritic) Pv = __fmaf_rn(w[D + 1 + N], hj, Pv);
-    }
-#pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const float t = fadd(P[i], __shfl_xor_sync(kFull, P[i], 1));  // P_q + P_{q^1}
-      lg[i] = fadd(b2[i], fadd(t, __shfl_xor_sync(kFull, t, 2)));    // b2 + ((P0+P1) + (P2+P3))
-    }
-    if (kCritic) {
-      const float t = fadd(Pv, __shfl_xor_sync(kFull, Pv, 1));
-      v = fadd(bv, fadd(t, __shfl_xor_sync(kFull, t, 2)));
-    }
-  }
+// samples actions", "roll-outs, action inference, reset and training" on one GPU store),
+// warp-specialised.  A CTA of five warps serves NG groups of 32 replicas (NG = 1 in production;
+// NG = 2 pipelines two groups and measured slower).  Warp 0 is
+// the ENV warp (lane = one replica of each group): it owns the states, publishes each group's
+// pre-step observations to shared memory, and once the group's inference round is back it
+// combines the four quarter partials (R29': b2 + ((P_0 + P_1) + (P_2 + P_3))), draws the
+// action and steps the dynamics.  Warps 1..4 are INFERENCE warps: warp 1 + q evaluates hidden
+// quarter q of the 32 replicas of the round (lane = replica; weights broadcast from shared
+// memory) and publishes its partials.  Each group's rounds are handed over by its own pair of
+// named barriers (obs ready / partials ready); with NG = 2 the groups are pipelined (while the
+// inference warps evaluate group A the env warp finishes group B).  The env warp's step uses
+// the env's fast path when every lane satisfies its invariant.  Auto-reset uses a look-ahead state init(e, rc + 1) kept in registers and refilled
+// after the next round is published (off the critical path).  The critic's values_trunc (rare)
+// and bootstrap values are evaluated in the env warp itself (R29' quarter sums in-lane).
+template <int D, int N>
+struct PolicyWsSmem {
+  float obs[2][D][32];            // [group]
+  float part[2][4][N + 1][32];    // [group][quarter]
 };
 
-template <class Env, int H, bool kCritic>
-__global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int T, const uint64_t t0,
-                                                       const float* __restrict__ weights,
-                                                       float* __restrict__ values, float* __restrict__ bootstrap,
-                                                       float* __restrict__ values_trunc) {
+template <class Env, int H, bool kCritic, int NG>
+__global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const int T, const uint64_t t0,
+                                                          const float* __restrict__ weights,
+                                                          float* __restrict__ values, float* __restrict__ bootstrap,
+                                                          float* __restrict__ values_trunc) {
   using L = Lane<Env>;
   using St = typename L::St;
-  constexpr int D = L::D, N = L::N;
-  using M = QuadMLP<D, N, H, kCritic>;
+  constexpr int D = L::D, N = L::N, HQ = H / 4;
+  constexpr int NW = D * H + H + H * N + N + (kCritic ? H + 1 : 0);
   constexpr int kRows = 16;
-  __shared__ __align__(16) float sw[M::kWords];
-  extern __shared__ __align__(16) uint32_t ws_smem[];
-  M::load(sw, weights, threadIdx.x, blockDim.x);
+  __shared__ __align__(16) float sw[NW];
+  __shared__ __align__(16) PolicyWsSmem<D, N> x;
+  extern __shared__ __align__(16) uint32_t ws_smem[];  // the env warp's two statistics windows
+  for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = weights[i];
   __syncthreads();
-  const int lane = threadIdx.x & 31, q = lane & 3;
-  M mlp;
-  mlp.bind(sw, q);
-  const int64_t e = ((int64_t)blockIdx.x * blockDim.x + threadIdx.x) >> 2;  // replica of this quad
+  const float* W1 = sw;
+  const float* b1 = W1 + D * H;
+  const float* W2 = b1 + H;
+  const float* b2 = W2 + H * N;
+  const float* wv = b2 + N;  // kCritic only
+  const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t E = a.E;
-  if (e - (lane >> 2) >= E) return;  // whole warp past the last replica
-  const bool live = e < E;
-  const bool writer = live && q == 0;   // the quad's lane 0 stores
-  const int64_t ec = live ? e : E - 1;  // tail quads shadow replica E-1 (identical values)
-  const uint32_t eg = (uint32_t)(a.offset + ec);
+
+  if (warp > 0) {  // ------------------------------------------------ inference warp, quarter q
+    const int q = warp - 1;
+    auto evaluate = [&](int g) {
+      float o[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) o[d] = x.obs[g][d][lane];
+      float P[N], Pv = 0.0f;
+#pragma unroll
+      for (int i = 0; i < N; ++i) P[i] = 0.0f;
+#pragma unroll
+      for (int u = 0; u < HQ; ++u) {
+        const int j = q * HQ + u;
+        float acc = b1[j];
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc = __fmaf_rn(W1[d * H + j], o[d], acc);
+        const float hj = acc > 0.0f ? acc : 0.0f;
+#pragma unroll
+        for (int i = 0; i < N; ++i) P[i] = __fmaf_rn(W2[j * N + i], hj, P[i]);
+        if (kCritic) Pv = __fmaf_rn(wv[j], hj, Pv);
+      }
+#pragma unroll
+      for (int i = 0; i < N; ++i) x.part[g][q][i][lane] = P[i];
+      if (kCritic) x.part[g][q][N][lane] = Pv;
+    };
+    for (int t = 0; t < T; ++t) {
+      asm volatile("bar.sync 1, 160;" ::: "memory");  // group A's observation of step t
+      evaluate(0);
+      asm volatile("bar.arrive 2, 160;" ::: "memory");
+      if (NG == 2) {
+        asm volatile("bar.sync 3, 160;" ::: "memory");  // group B's
+        evaluate(1);
+        asm volatile("bar.arrive 4, 160;" ::: "memory");
+      }
+    }
+    return;
+  }
+
+  // ------------------------------------------------------------------------------ env warp
   const Key key{a.k0, a.k1};
   const size_t sE = (size_t)E;
-  StatsWindow win;
-  win.init(ws_smem + (threadIdx.x >> 5) * (3 * kRows * kWinStride), kRows);
-  St s;
-  L::load(a.state + ec * L::S, s);
-  typename L::Aux aux = L::aux_of(s);
-  int32_t ep_step = a.ep_step[ec];
-  uint32_t rc = a.reset_count[ec];
-  float ep_ret = a.ep_ret[ec];
+  struct Grp {
+    int64_t e, ec;
+    bool live;
+    uint32_t eg;
+    St s, nxt;
+    typename L::Aux aux;
+    int32_t ep_step;
+    uint32_t rc;
+    float ep_ret;
+    U4 w4;
+    StatsWindow win;
+    int nlive;
+  } G[NG];
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    Grp& r = G[g];
+    const int64_t first = (int64_t)blockIdx.x * (32 * NG) + 32 * g;
+    r.e = first + lane;
+    r.live = r.e < E;
+    r.ec = r.live ? r.e : E - 1;  // tail lanes (and a group past E) shadow replica E-1
+    r.nlive = (int)max((int64_t)0, min((int64_t)32, E - first));
+    r.eg = (uint32_t)(a.offset + r.ec);
+    L::load(a.state + r.ec * L::S, r.s);
+    r.aux = L::aux_of(r.s);
+    r.ep_step = a.ep_step[r.ec];
+    r.rc = a.reset_count[r.ec];
+    r.ep_ret = a.ep_ret[r.ec];
+    L::init(key, r.eg, r.rc + 1, r.nxt);
+    r.w4 = U4{0, 0, 0, 0};
+    r.win.init(ws_smem + g * (3 * kRows * kWinStride), kRows);
+  }
   uint32_t err = 0;
-  U4 w4{0, 0, 0, 0};
-  int32_t* const p_act = reinterpret_cast<int32_t*>(a.act);
-  for (int c = 0; c < T; ++c) {
-    const uint64_t t = t0 + (uint64_t)c;
-    if (c == 0 || (t & 3) == 0) w4 = block(key, t >> 2, eg, 0, kAction);
-    const size_t idx = (size_t)c * sE + (size_t)ec;
-    if (writer) L::obs_store_aux(a.obs + idx * L::D, s, aux, true);
-    // ---- inference: h = relu(W1^T o + b1) (this lane's quarter), logits / V by the quad
+  auto publish = [&](int g) {
     float o[D];
-    L::obs_vals(s, aux, o);
+    L::obs_vals(G[g].s, G[g].aux, o);
+#pragma unroll
+    for (int d = 0; d < D; ++d) x.obs[g][d][lane] = o[d];
+    if (g == 0) asm volatile("bar.arrive 1, 160;" ::: "memory");
+    else asm volatile("bar.arrive 3, 160;" ::: "memory");
+  };
+  // in-lane R29' evaluation (values_trunc / bootstrap)
+  auto value_of = [&](const St& st, const typename L::Aux& ax) {
+    float o[D], P[4];
+    L::obs_vals(st, ax, o);
+#pragma unroll
+    for (int q = 0; q < 4; ++q) {
+      float acc_q = 0.0f;
+#pragma unroll 4
+      for (int u = 0; u < HQ; ++u) {
+        const int j = q * HQ + u;
+        float acc = b1[j];
+#pragma unroll
+        for (int d = 0; d < D; ++d) acc = __fmaf_rn(W1[d * H + j], o[d], acc);
+        acc_q = __fmaf_rn(wv[j], acc > 0.0f ? acc : 0.0f, acc_q);
+      }
+      P[q] = acc_q;
+    }
+    return fadd(wv[H], fadd(fadd(P[0], P[1]), fadd(P[2], P[3])));
+  };
+  // finish step c of group g: partials -> logits -> draw -> dynamics -> stores / statistics;
+  // returns whether any lane reset (its look-ahead state is refilled after the next publish)
+  auto finish = [&](int g, int c) -> bool {
+    Grp& r = G[g];
+    const uint64_t t = t0 + (uint64_t)c;
+    if (c == 0 || (t & 3) == 0) r.w4 = block(key, t >> 2, r.eg, 0, kAction);
+    const size_t idx = (size_t)c * sE + (size_t)r.ec;
     float lg[N], vv = 0.0f;
-    mlp.eval(o, lg, vv);
-    if (kCritic && writer) st_cs(values + idx, vv);
+#pragma unroll
+    for (int i = 0; i < N; ++i) {
+      const float* pp = &x.part[g][0][i][lane];
+      lg[i] = fadd(b2[i], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
+    }
+    if (kCritic) {
+      const float* pp = &x.part[g][0][N][lane];
+      vv = fadd(wv[H], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
+      if (r.live) st_cs(values + idx, vv);
+    }
+    L::obs_store_aux(a.obs + idx * L::D, r.s, r.aux, true);
     float m = lg[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -919,7 +946,6 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     float S = 0.0f;
     if constexpr (N == 2) {
       // exp(l_max - m) = exp(0) = 1 exactly: one fp64 exponential per step instead of two
-      // (bit-identical to the loop below, including non-finite logits -> NaN -> invalid row)
       const bool k0 = !(lg[1] > lg[0]);  // m == lg[0]
       const float eo = (float)exp((double)fsub(k0 ? lg[1] : lg[0], m));
       const float em = isfinite(m) ? 1.0f : __int_as_float(0x7fc00000);
@@ -944,69 +970,87 @@ __global__ void __launch_bounds__(128) k_rollout_policy(const KArgs a, const int
     }
     cdf.bad = badp || !(run > 0.0) || !isfinite(run);
     // ---- A2 draw (R13) from the ACTION stream
-    int act = search<N>(cdf, u01(pick(w4, (uint32_t)(t & 3))));
+    int act = search<N>(cdf, u01(pick(r.w4, (uint32_t)(t & 3))));
     float lp = logp_of_normalised<N>(cdf, act);
     if (cdf.bad) {
       act = -1;
       lp = __int_as_float(0x7fc00000);
-      if (writer) err |= kErrProbs | kErrAction;
+      if (r.live) err |= kErrProbs | kErrAction;
     }
-    if (writer) {
-      st_cs(p_act + idx, act);
-      if (a.write_logp) st_cs(a.logp + idx, lp);
-    }
+    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
+    if (a.write_logp) st_cs(a.logp + idx, lp);
     // ---- A3-A5
     const bool bad = act < 0;
-    St s2 = s;
-    typename L::Aux aux2 = aux;
-    float r;
+    St s2 = r.s;
+    typename L::Aux aux2 = r.aux;
+    float rr;
     bool term;
-    L::template step_aux<false>(s2, aux2, bad ? 0 : act, r, term);
-    const int32_t es = ep_step + 1;
+    // the env's fast step when every lane satisfies its invariant (CartPole: guard-free
+    // divisions and the Taylor sincos, bit-identical; section 5), else the generic step
+    if (L::kMinEpisode >= 8 && __all_sync(kFull, L::fast_ok(r.s)))
+      L::template step_aux<true>(s2, aux2, bad ? 0 : act, rr, term);
+    else
+      L::template step_aux<false>(s2, aux2, bad ? 0 : act, rr, term);
+    const int32_t es = r.ep_step + 1;
     const uint32_t d = bad ? 0u : ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u));
-    const float rw = bad ? 0.0f : r;
-    const float ret = ep_ret + r;
+    const float rw = bad ? 0.0f : rr;
+    const float ret = r.ep_ret + rr;
     if (!bad) {
-      s = s2;
-      aux = aux2;
-      ep_step = es;
-      ep_ret = ret;
+      r.s = s2;
+      r.aux = aux2;
+      r.ep_step = es;
+      r.ep_ret = ret;
     }
     if (kCritic && values_trunc && __any_sync(kFull, d == 2u)) {  // truncated only: V of the post-step state
-      float o2[D], lg2[N], v2 = 0.0f;
-      L::obs_vals(s, aux, o2);
-      mlp.eval(o2, lg2, v2);
-      if (writer && d == 2u) st_cs(values_trunc + idx, v2);
+      const float v2 = value_of(r.s, r.aux);
+      if (r.live && d == 2u) st_cs(values_trunc + idx, v2);
     }
-    if (d) {  // auto-reset (R11)
-      rc += 1;
-      L::init(key, eg, rc, s);
-      aux = L::aux_of(s);
-      ep_step = 0;
-      ep_ret = 0.0f;
+    if (d) {  // auto-reset (R11) from the look-ahead state init(e, rc + 1)
+      r.rc += 1;
+      r.s = r.nxt;
+      r.aux = L::aux_of(r.s);
+      r.ep_step = 0;
+      r.ep_ret = 0.0f;
     }
-    if (writer) {
-      st_cs(a.rew + idx, rw);
-      st_cs_u8(a.done + idx, (uint8_t)d);
+    st_cs(a.rew + idx, rw);
+    st_cs_u8(a.done + idx, (uint8_t)d);
+    r.win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
+      r.win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, r.nlive);
+    return __any_sync(kFull, d != 0);
+  };
+  auto refill = [&](int g, bool any) {
+    if (any) L::init(key, G[g].eg, G[g].rc + 1, G[g].nxt);  // (lanes without a reset recompute the same state)
+  };
+  publish(0);
+  for (int c = 0; c < T; ++c) {
+    if constexpr (NG == 2) publish(NG - 1);
+    asm volatile("bar.sync 2, 160;" ::: "memory");  // group A's partials of step c
+    const bool ra = finish(0, c);
+    if (c + 1 < T) publish(0);
+    refill(0, ra);
+    if constexpr (NG == 2) {
+      asm volatile("bar.sync 4, 160;" ::: "memory");  // group B's partials of step c
+      const bool rb = finish(NG - 1, c);
+      refill(NG - 1, rb);
     }
-    win.put(c & (kRows - 1), lane, (writer && d) ? (uint32_t)es : 0u, (writer && d) ? ret : 0.0f,
-            writer ? rw : 0.0f);
-    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1) win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats);
   }
-  if constexpr (kCritic) {  // bootstrap value of the observation after the last step
-    float o[D], lg[N], v = 0.0f;
-    L::obs_vals(s, aux, o);
-    mlp.eval(o, lg, v);
-    if (writer) bootstrap[e] = v;
+#pragma unroll
+  for (int g = 0; g < NG; ++g) {
+    Grp& r = G[g];
+    if constexpr (kCritic) {  // bootstrap value of the observation after the last step
+      const float v = value_of(r.s, r.aux);
+      if (r.live) bootstrap[r.e] = v;
+    }
+    if (r.live) {
+      L::save(a.state + r.e * L::S, r.s);
+      a.ep_step[r.e] = r.ep_step;
+      a.reset_count[r.e] = r.rc;
+      a.ep_ret[r.e] = r.ep_ret;
+      L::obs_store(a.obs_live + r.e * L::D, r.s, false);
+    }
   }
-  if (writer) {
-    L::save(a.state + e * L::S, s);
-    a.ep_step[e] = ep_step;
-    a.reset_count[e] = rc;
-    a.ep_ret[e] = ep_ret;
-    L::obs_store(a.obs_live + e * L::D, s, false);
-    if (err) atomicOr(a.err, err);
-  }
+  if (err) atomicOr(a.err, err);
 }
 
 // =======================================================================================
@@ -2405,20 +2449,22 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, float* values, float* bootstrap, float* vtr) {
-  const int b = 128;                                                        // 32 replicas (quads) per CTA
-  const size_t smem = (size_t)(b / 32) * 3 * 16 * kWinStride * sizeof(uint32_t);  // per-warp 16-row windows
-  const unsigned g = grid_for(a.E, b / 4);
+  // warp-specialised: one env warp + four inference warps per 32 replicas; the env warp's
+  // 16-row statistics window is the dynamic shared memory
+  constexpr int NG = 1;  // replica groups per CTA (2: pipelined groups -- measured slower)
+  const size_t smem = (size_t)NG * 3 * 16 * kWinStride * sizeof(uint32_t);
+  const unsigned g = grid_for(a.E, 32 * NG);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
-      case 64: k_rollout_policy<Env, 64, true><<<g, b, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 32: k_rollout_policy_ws<Env, 32, true, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 64: k_rollout_policy_ws<Env, 64, true, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
     switch (hidden) {
-      case 32: k_rollout_policy<Env, 32, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
-      case 64: k_rollout_policy<Env, 64, false><<<g, b, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 32: k_rollout_policy_ws<Env, 32, false, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 64: k_rollout_policy_ws<Env, 64, false, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
       default: return cudaErrorInvalidValue;
     }
   }
