@@ -147,6 +147,7 @@ _SIGS = {
                                C.c_void_p]),
     "ws_a2c_moments": (C.c_int, [C.c_void_p, C.c_int64, C.c_void_p, C.c_void_p, C.c_void_p]),
     "ws_a2c_grad": (C.c_int, [C.POINTER(ws_a2c_args), C.c_void_p]),
+    "ws_clamp": (C.c_int, [C.c_void_p, C.c_int32, C.c_float, C.c_float, C.c_void_p]),
     "ws_adam": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p, C.c_void_p, C.c_int32, C.c_int32, C.c_float,
                           C.c_float, C.c_float, C.c_float, C.c_float, C.c_void_p, C.c_void_p]),
     "ws_peer_export": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),

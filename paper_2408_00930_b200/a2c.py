@@ -248,10 +248,14 @@ class A2C:
             self._pg_grad.allreduce_adam(self.grad, self.params, self.m, self.v, self.step, hp["lr"], hp["beta1"],
                                          hp["beta2"], hp["eps"], hp["max_norm"], grad_out=self.grad,
                                          grad_norm=self.grad_norm, stream=s)
-            return
-        self._allreduce(self.grad)
-        adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
-             hp["max_norm"], grad_norm=self.grad_norm, stream=s)
+        else:
+            self._allreduce(self.grad)
+            adam(self.params, self.grad, self.m, self.v, self.step, hp["lr"], hp["beta1"], hp["beta2"], hp["eps"],
+                 hp["max_norm"], grad_norm=self.grad_norm, stream=s)
+        if self.gaussian:  # SPEC policy invariant: log_std in [-5, 2] (ws_clamp on the log_std slice)
+            o = self.D * self.H + self.H + self.H * self.N + self.N
+            ls = self.params[o:o + self.N]
+            check(lib().ws_clamp(ls.data_ptr(), self.N, -5.0, 2.0, C.c_void_p(s.cuda_stream)))
 
     def update(self, T: int, values_ready: bool = False):
         """One A2C update on store slots [0, T) (already rolled out with self.params).

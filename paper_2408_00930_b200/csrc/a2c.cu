@@ -636,6 +636,18 @@ ws_status ws_a2c_grad(const ws_a2c_args* a, void* stream) {
   return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
 }
 
+__global__ void k_clamp(float* __restrict__ x, int n, float lo, float hi) {
+  const int i = blockIdx.x * blockDim.x + threadIdx.x;
+  if (i < n) x[i] = fminf(fmaxf(x[i], lo), hi);
+}
+
+ws_status ws_clamp(float* x, int32_t n, float lo, float hi, void* stream) {
+  if (!x || n < 0 || !(lo <= hi)) return WS_ERR_INVALID_ARGUMENT;
+  if (n == 0) return WS_OK;
+  k_clamp<<<(n + 127) / 128, 128, 0, static_cast<cudaStream_t>(stream)>>>(x, n, lo, hi);
+  return cudaGetLastError() ? WS_ERR_CUDA : WS_OK;
+}
+
 ws_status ws_adam(float* params, const float* grad, float* m, float* v, int32_t n, int32_t step, float lr,
                   float beta1, float beta2, float eps, float max_norm, float* grad_norm, void* stream) {
   if (!params || !grad || !m || !v || n < 1 || n > 65536 || step < 1 || !(lr >= 0.0f) || !(beta1 >= 0.0f && beta1 < 1.0f) ||

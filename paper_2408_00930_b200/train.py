@@ -1,7 +1,8 @@
 """NEXT-N2: the training loop (SPEC train S:418-421; A2C or PPO; P:86 / P:95 convergence claims, Fig 2(b)):
 alternate fused roll-outs with in-kernel inference and on-device A2C updates until a budget
-of iterations or a target mean episodic return, emitting the learning curve
-(wall-clock seconds, env steps, mean episodic return, mean episode length) as CSV.  No data
+of iterations or a target mean episodic return, emitting the learning curve as CSV with the
+SPEC columns wall_clock_s, env_steps, mean_episodic_reward, mean_episodic_length, policy_loss,
+value_loss, entropy (the last update's loss terms) and the episode count.  No data
 leaves the GPU between the phases; the statistics of each iteration (exact fixed-point
 per-slot sums, R20) are read back once per `log_every` iterations.
 
@@ -43,7 +44,8 @@ def train(env_name: str = "cartpole", n_envs: int = 10000, T: int = 32, iters: i
     curve = []
     writer = csv.writer(out) if out is not None and rank == 0 else None
     if writer:
-        writer.writerow(["seconds", "env_steps", "mean_return", "mean_length", "episodes"])
+        writer.writerow(["wall_clock_s", "env_steps", "mean_episodic_reward", "mean_episodic_length", "policy_loss",
+                         "value_loss", "entropy", "episodes"])
     torch.cuda.synchronize(env.device)
     t0 = time.perf_counter()
     st_view = env.buffers()["stats"]
@@ -62,7 +64,9 @@ def train(env_name: str = "cartpole", n_envs: int = 10000, T: int = 32, iters: i
             row = (time.perf_counter() - t0, (it + 1) * T * n_envs, mean_ret, mean_len, ep)
             curve.append(row[:4])
             if writer:
-                writer.writerow([f"{row[0]:.4f}", row[1], f"{row[2]:.3f}", f"{row[3]:.3f}", row[4]])
+                pl, vl, ent = tr.loss.tolist()  # the last update's policy / value / entropy terms
+                writer.writerow([f"{row[0]:.4f}", row[1], f"{row[2]:.3f}", f"{row[3]:.3f}", f"{pl:.6g}",
+                                 f"{vl:.6g}", f"{ent:.6g}", row[4]])
             if target is not None and ep and mean_ret >= target:
                 break
     return curve
@@ -83,7 +87,7 @@ def main(argv=None):
     ap.add_argument("--log-every", type=int, default=10)
     ap.add_argument("--csv", default="-")
     ap.add_argument("--seed", type=lambda x: int(x, 0), default=0x24080930)
-    ap.add_argument("--algo", choices=["a2c", "ppo"], default="a2c")
+    ap.add_argument("--algo", choices=["a2c", "ppo"], default="ppo")  # SPEC: PPO is the default trainer
     ap.add_argument("--epochs", type=int, default=4)
     ap.add_argument("--minibatches", type=int, default=4)
     ap.add_argument("--clip", type=float, default=0.2)
