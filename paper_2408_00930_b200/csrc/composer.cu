@@ -103,9 +103,39 @@ const char* kPrelude = R"WS(
 typedef unsigned int ws_u32; typedef unsigned long long ws_u64; typedef long long ws_i64;
 typedef unsigned char ws_u8; typedef int ws_i32;
 #define WS_FN __device__ __forceinline__
-/* transcendental contract (DESIGN R3): fp64 evaluation, one rounding to fp32 */
-WS_FN float ws_sin(float x) { return (float)sin((double)x); }
-WS_FN float ws_cos(float x) { return (float)cos((double)x); }
+/* transcendental contract (DESIGN R3): fp64 evaluation, one rounding to fp32.  sin / cos use
+   the library's branch-free fp64 evaluation (Cody-Waite reduction by pi/2 with the fdlibm
+   three-part constant, Taylor polynomials through r^17 / r^18 on |r| <= pi/4 -- pinned against
+   the host libm by the device tests); |x| >= 2^20 falls back to libdevice */
+WS_FN void ws_sincos64(double x, double* s, double* c) {
+  const double kd = fma(x, 6.36619772367581382433e-01, 6755399441055744.0);
+  const double k = kd - 6755399441055744.0;
+  const int q = __double2loint(kd);
+  double r = fma(-k, 1.57079632673412561417e+00, x);
+  r = fma(-k, 6.07710050630396597660e-11, r);
+  r = fma(-k, 2.02226624871116645580e-21, r);
+  r = fma(-k, 8.47842766036889956997e-32, r);
+  const double z = r * r, z2 = z * z, z4 = z2 * z2;
+  const double s_a = fma(z, 1.0 / 120.0, -1.0 / 6.0);
+  const double s_b = fma(z, 1.0 / 362880.0, -1.0 / 5040.0);
+  const double s_c = fma(z, 1.0 / 6227020800.0, -1.0 / 39916800.0);
+  const double s_d = fma(z, 1.0 / 355687428096000.0, -1.0 / 1307674368000.0);
+  const double ps = fma(z4, fma(z2, s_d, s_c), fma(z2, s_b, s_a));
+  const double c_a = fma(z, 1.0 / 24.0, -0.5);
+  const double c_b = fma(z, 1.0 / 40320.0, -1.0 / 720.0);
+  const double c_c = fma(z, 1.0 / 479001600.0, -1.0 / 3628800.0);
+  const double c_d = fma(z, 1.0 / 20922789888000.0, -1.0 / 87178291200.0);
+  const double pc = fma(z4, fma(z4, -1.0 / 6402373705728000.0, fma(z2, c_d, c_c)), fma(z2, c_b, c_a));
+  const double sr = fma(r * z, ps, r);
+  const double cr = fma(z, pc, 1.0);
+  const double s0 = (q & 1) ? cr : sr;
+  const double c0 = (q & 1) ? sr : cr;
+  *s = (q & 2) ? -s0 : s0;
+  *c = ((q + 1) & 2) ? -c0 : c0;
+  if (!(fabs(x) < 1048576.0)) sincos(x, s, c);
+}
+WS_FN float ws_sin(float x) { double s, c; ws_sincos64((double)x, &s, &c); return (float)s; }
+WS_FN float ws_cos(float x) { double s, c; ws_sincos64((double)x, &s, &c); return (float)c; }
 WS_FN float ws_exp(float x) { return (float)exp((double)x); }
 WS_FN float ws_log(float x) { return (float)log((double)x); }
 WS_FN float ws_tanh(float x) { return (float)tanh((double)x); }
@@ -119,7 +149,7 @@ WS_FN float ws_fmod(float x, float y) { return fmodf(x, y); }
 /* both with one fp64 range reduction, each rounded once (R3) */
 WS_FN void ws_sincos(float x, float *s, float *c) {
   double sd, cd;
-  sincos((double)x, &sd, &cd);
+  ws_sincos64((double)x, &sd, &cd);
   *s = (float)sd;
   *c = (float)cd;
 }
@@ -436,6 +466,109 @@ extern "C" __global__ void k_user_rollout(const WsUserArgs a, int T, ws_u64 t0, 
 }
 
 #if WS_C == 0
+/* Roll-out with GIVEN constant probabilities (step stride 0): the library's plan kernel has
+   already drawn every action (R28: act / logp slabs and the packed plan, four 8-bit actions per
+   word, 0xFF = invalid row), so the loop only runs the user's dynamics -- the hand-written lane
+   kernel's structure: actions prefetched one 4-step group ahead, the reset state init(e, rc + 1)
+   kept ready in registers and selected on done (refilled once per group; a second reset inside a
+   group recomputes it, warp-uniformly), per-warp statistics window in shared memory reduced every
+   16 slots to exact fixed point (one atomic per field, slot and warp; R20). */
+#define WS_WR 16
+extern "C" __global__ void __launch_bounds__(128) k_user_rollout_plan(const WsUserArgs a, int T, const ws_u32* plan) {
+  __shared__ float win[4][3][WS_WR][33];  /* per warp: [len | ret | rew][slot row][lane] */
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  const ws_i64 e0 = (ws_i64)blockIdx.x * blockDim.x + threadIdx.x;
+  if (e0 - lane >= a.E) return;                         /* whole warp past the end */
+  const bool live = e0 < a.E;
+  const ws_i64 e = live ? e0 : a.E - 1;                 /* tail lanes shadow E-1 (identical stores) */
+  const ws_u32 eg = (ws_u32)(a.offset + e);
+  const float* prm = a.prm ? a.prm + e * (WS_P > 0 ? WS_P : 1) : 0;
+  float s[WS_S], nx[WS_S], o[WS_D];
+  for (int i = 0; i < WS_S; ++i) s[i] = a.state[e * WS_S + i];
+  for (int i = 0; i < WS_D; ++i) o[i] = a.obs_live[e * WS_D + i];
+  ws_i32 ep_step = a.ep_step[e];
+  ws_u32 rc = a.reset_count[e];
+  float ep_ret = a.ep_ret[e];
+  ws_u32 err = 0;
+  bool stale = true;
+  const int ng = (T + 3) / 4;
+  ws_u32 pk_next = plan[e];
+  for (int j = 0; j < ng; ++j) {
+    const ws_u32 pk = pk_next;
+    if (j + 1 < ng) pk_next = plan[(ws_i64)(j + 1) * a.E + e];
+    if (__any_sync(0xffffffffu, stale)) { ws_init(a, eg, rc + 1u, nx, prm); stale = false; }
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int c = 4 * j + k;
+      if (c >= T) break;
+      const ws_i64 idx = (ws_i64)c * a.E + e;
+#if WS_D % 4 == 0                                    /* R12, vector stores: a warp writes whole lines */
+      for (int i = 0; i < WS_D; i += 4) __stcs(reinterpret_cast<float4*>(a.obs + idx * WS_D + i), make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]));
+#elif WS_D % 2 == 0
+      for (int i = 0; i < WS_D; i += 2) __stcs(reinterpret_cast<float2*>(a.obs + idx * WS_D + i), make_float2(o[i], o[i + 1]));
+#else
+      for (int i = 0; i < WS_D; ++i) __stcs(a.obs + idx * WS_D + i, o[i]);
+#endif
+      const int act = (int)(signed char)(unsigned char)(pk >> (8 * k));
+      float r = 0.0f;
+      ws_u32 d = 0u;
+      float ret = 0.0f;
+      ws_i32 es = 0;
+      if (act < 0) {                                 /* R19: not advanced, rew 0, done 0 */
+        if (live) err |= 3u;
+      } else {
+        const int term = ws_env_step(s, act, &r, prm, a.shared);
+        es = ep_step + 1;
+        d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
+        ret = ep_ret + r;
+        ep_step = d ? 0 : es;
+        ep_ret = d ? 0.0f : ret;
+      }
+      if (__any_sync(0xffffffffu, d != 0u && stale)) {  /* second reset inside this group */
+        if (d != 0u && stale) ws_init(a, eg, rc + 1u, nx, prm);
+      }
+      if (d) {                                       /* auto-reset (R11) from the look-ahead state */
+        rc += 1u;
+        for (int i = 0; i < WS_S; ++i) s[i] = nx[i];
+        stale = true;
+      }
+      ws_env_obs(s, o, prm, a.shared);
+      __stcs(a.rew + idx, r);
+      a.done[idx] = (ws_u8)d;
+      const int row = c & (WS_WR - 1);
+      win[wp][0][row][lane] = (live && d) ? __int_as_float(es) : 0.0f;
+      win[wp][1][row][lane] = (live && d) ? ret : 0.0f;
+      win[wp][2][row][lane] = live ? r : 0.0f;
+      if (row == WS_WR - 1 || c == T - 1) {          /* lane i reduces slot row i (R20, exact) */
+        __syncwarp();
+        if (lane <= row) {
+          ws_u64 nd = 0, ln = 0;
+          ws_i64 rt = 0, rs = 0;
+          for (int q = 0; q < 32; ++q) {
+            const int l = __float_as_int(win[wp][0][lane][q]);
+            nd += l != 0 ? 1u : 0u;
+            ln += (ws_u64)l;
+            rt += ws_fx(win[wp][1][lane][q]);
+            rs += ws_fx(win[wp][2][lane][q]);
+          }
+          ws_u64* st = a.stats + (ws_i64)(c - row + lane) * 4;
+          if (nd) { atomicAdd(st + 0, nd); atomicAdd(st + 1, (ws_u64)rt); atomicAdd(st + 2, ln); }
+          if (rs) atomicAdd(st + 3, (ws_u64)rs);
+        }
+        __syncwarp();
+      }
+    }
+  }
+  if (live) {
+    for (int i = 0; i < WS_S; ++i) a.state[e * WS_S + i] = s[i];
+    for (int i = 0; i < WS_D; ++i) a.obs_live[e * WS_D + i] = o[i];
+    a.ep_step[e] = ep_step;
+    a.reset_count[e] = rc;
+    a.ep_ret[e] = ep_ret;
+    if (err) atomicOr(a.err, err);
+  }
+}
+
 /* policy roll-outs: weights (R29, + R31 value head for the critic variants) staged in shared
    memory once per CTA */
 template <int kH, bool kCritic>
@@ -468,7 +601,7 @@ struct UserEnv {
   std::vector<char> cubin;
   struct Kernels {
     cudaLibrary_t lib;
-    cudaKernel_t reset, rollout, policy32, policy64, ac32, ac64;
+    cudaKernel_t reset, rollout, policy32, policy64, ac32, ac64, rollout_plan;
   };
   std::map<int, Kernels> per_dev;
 };
@@ -503,8 +636,9 @@ cudaError_t kernels_for(UserEnv* u, const UserEnv::Kernels** out) {
     if ((e = cudaLibraryLoadData(&k.lib, u->cubin.data(), nullptr, nullptr, 0, nullptr, nullptr, 0))) return e;
     const std::pair<cudaKernel_t*, const char*> names[] = {
         {&k.reset, "k_user_reset"},       {&k.rollout, "k_user_rollout"}, {&k.policy32, "k_user_policy_32"},
-        {&k.policy64, "k_user_policy_64"}, {&k.ac32, "k_user_ac_32"},      {&k.ac64, "k_user_ac_64"}};
-    const int n_req = u->def.act_dim > 0 ? 2 : 6;  // continuous envs carry no policy kernels
+        {&k.policy64, "k_user_policy_64"}, {&k.ac32, "k_user_ac_32"},      {&k.ac64, "k_user_ac_64"},
+        {&k.rollout_plan, "k_user_rollout_plan"}};
+    const int n_req = u->def.act_dim > 0 ? 2 : 7;  // continuous envs carry no policy / plan kernels
     for (int i = 0; i < n_req; ++i)
       if ((e = cudaLibraryGetKernel(names[i].first, k.lib, names[i].second))) return e;
     it = u->per_dev.emplace(dev, k).first;
@@ -556,8 +690,18 @@ cudaError_t launch_user_rollout(const UserLaunch& l, int T, uint64_t t0, const f
   cudaError_t e = kernels_for(static_cast<UserEnv*>(l.handle), &k);
   if (e) return e;
   UserArgs a = user_args(l);
-  void* args[] = {&a, &T, &t0, &probs, &row_stride, &step_stride};
   const unsigned grid = (unsigned)((l.k.E + 127) / 128);
+  const UserEnv* u = static_cast<const UserEnv*>(l.handle);
+  if (step_stride == 0 && u->def.act_dim == 0 && u->def.n_actions <= 8 && l.k.plan) {
+    // constant probabilities: the library's plan kernel draws every action up front (R28), the
+    // composed kernel runs only the dynamics
+    if ((e = launch_plan(l.k, u->def.n_actions, T, t0, probs, row_stride, l.stream))) return e;
+    const uint32_t* plan = l.k.plan;
+    void* args[] = {&a, &T, &plan};
+    return cudaLaunchKernel(reinterpret_cast<const void*>(k->rollout_plan), dim3(grid), dim3(128), args, 0,
+                            l.stream);
+  }
+  void* args[] = {&a, &T, &t0, &probs, &row_stride, &step_stride};
   return cudaLaunchKernel(reinterpret_cast<const void*>(k->rollout), dim3(grid), dim3(128), args, 0, l.stream);
 }
 

@@ -2332,6 +2332,21 @@ cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches) {
   return cudaGetLastError();
 }
 
+// the plan kernel alone, for the runtime-composed (NVRTC) roll-out of a registered discrete env
+// with constant probabilities (NEXT-N4): act / logp slabs and the packed plan, n_actions 2..8
+cudaError_t launch_plan(const KArgs& a, int n_actions, int T, uint64_t t0, const float* probs, int64_t row_stride,
+                        cudaStream_t s) {
+  const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kPlanChunk - 1) / kPlanChunk));
+  switch (n_actions) {
+#define WS_PLAN_N(NN) \
+  case NN: k_plan_discrete<NN, false><<<grid, 128, 0, s>>>(a, T, t0, probs, row_stride, 0); break;
+    WS_PLAN_N(2) WS_PLAN_N(3) WS_PLAN_N(4) WS_PLAN_N(5) WS_PLAN_N(6) WS_PLAN_N(7) WS_PLAN_N(8)
+#undef WS_PLAN_N
+    default: return cudaErrorInvalidValue;
+  }
+  return cudaGetLastError();
+}
+
 template <class Env>
 static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
                                     int64_t row_stride, int64_t step_stride, uint64_t* launches) {

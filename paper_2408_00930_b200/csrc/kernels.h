@@ -55,6 +55,8 @@ struct Launch {
 cudaError_t launch_reset(const KArgs& a, const Launch& l, uint64_t* launches);
 cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* probs,
                            int64_t row_stride, int64_t step_stride, uint64_t* launches);
+cudaError_t launch_plan(const KArgs& a, int n_actions, int T, uint64_t t0, const float* probs, int64_t row_stride,
+                        cudaStream_t s);
 cudaError_t launch_sample(const KArgs& a, const Launch& l, int slot, uint64_t t, const float* probs,
                           int64_t row_stride, uint64_t* launches);
 cudaError_t launch_step(const KArgs& a, const Launch& l, int slot, const void* given, uint64_t* launches);
