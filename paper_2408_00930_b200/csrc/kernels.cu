@@ -502,7 +502,11 @@ __device__ __forceinline__ void plan_rows(const KArgs& a, const int T, const uin
 template <int N, bool kStrided>
 __global__ void __launch_bounds__(128) k_plan_discrete(const KArgs a, const int T, const uint64_t t0,
                                                       const float* __restrict__ probs, const int64_t row_stride,
-                                                      const int64_t step_stride) {
+                                                      const int64_t step_stride, const int zero_stats) {
+  // zero_stats: this launch also clears the roll-out's [T, 4] statistics slab (the roll-out kernel
+  // runs after it on the same stream) -- one launch fewer than a separate memset
+  if (zero_stats && blockIdx.x == 0 && blockIdx.y == 0)
+    for (int i = threadIdx.x; i < 4 * T; i += blockDim.x) a.stats[i] = 0ull;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int c_begin = blockIdx.y * kPlanChunk;
   plan_rows<N, kStrided>(a, T, t0, probs, row_stride, step_stride, e, c_begin, min(T, c_begin + kPlanChunk));
@@ -1489,6 +1493,9 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
   const uint32_t eg = (uint32_t)(a.offset + e);
   const Key key{a.k0, a.k1};
   const size_t sE = (size_t)E;
+  constexpr int kRows = 16;  // statistics window depth (slots per flush)
+  StatsWindow win;           // per-warp window: leaders' (length, return, reward) per slot
+  win.init(ws_smem + 2 * 256 + wib * (3 * kRows * kWinStride), kRows);
   CtaStats cta;
   {
     const int64_t first_w = (int64_t)blockIdx.x * (blockDim.x >> 5);
@@ -1561,24 +1568,17 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       const int32_t es = ep_step + 1;
       d = (term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u);
       const float ret = ep_ret + r;
-      if (leader && d) {  // episode ends: rare except at the (synchronous) truncation step
-        unsigned long long* ac = cta.acc(c >> 5) + (c & 31) * 4;
-        atomicAdd(ac + kStEpisodes, 1ull);
-        atomicAdd(ac + kStLength, (unsigned long long)es);
-        atomicAdd(ac + kStReturn, (unsigned long long)to_fx(ret));
-      }
+      win.put(c & (kRows - 1), lane, (leader && d) ? (uint32_t)es : 0u, (leader && d) ? ret : 0.0f, 0.0f);
       ep_step = d ? 0 : es;
       ep_ret = d ? 0.0f : ret;
 #pragma unroll
       for (int i = 0; i < C; ++i) q[i] = qn[i];
       Ecur = En;
-    } else if (leader) {
-      err |= kErrAction;
+    } else {
+      win.put(c & (kRows - 1), lane, 0u, 0.0f, 0.0f);
+      if (leader) err |= kErrAction;
     }
-    {  // slot reward sum over the warp's replicas: exact 64-bit sum by four 16-bit REDUXes
-      const unsigned long long sr = warp_sum_u64(leader ? (unsigned long long)to_fx(r) : 0ull);
-      if (lane == 0 && sr) atomicAdd(cta.acc(c >> 5) + (c & 31) * 4 + kStReward, sr);
-    }
+    win.rew[(c & (kRows - 1)) * kWinStride + lane] = leader ? r : 0.0f;  // slot reward (R20 at flush)
     if (leader) {
       st_cs(a.rew + idx, r);
       st_cs_u8(a.done + idx, (uint8_t)d);
@@ -1600,7 +1600,12 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       const float Er = w.energy(q);
       if (d) Ecur = Er;
     }
-    if ((c & 31) == 31 || c == T - 1) cta.push(lane, c >> 5, 0, c & 31, c & ~31, a.stats);
+    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1) {  // window -> CTA accumulator -> global atomics
+      const int wdx = c / kRows;
+      win.cta_acc = cta.acc(wdx);
+      win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, 32);
+      cta.push(lane, wdx, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats);
+    }
   };
   float a0[C] = {}, a1[C] = {}, a2[C] = {}, a3[C] = {};
   load_act(0, a0);
@@ -2339,7 +2344,7 @@ cudaError_t launch_plan(const KArgs& a, int n_actions, int T, uint64_t t0, const
   const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kPlanChunk - 1) / kPlanChunk));
   switch (n_actions) {
 #define WS_PLAN_N(NN) \
-  case NN: k_plan_discrete<NN, false><<<grid, 128, 0, s>>>(a, T, t0, probs, row_stride, 0); break;
+  case NN: k_plan_discrete<NN, false><<<grid, 128, 0, s>>>(a, T, t0, probs, row_stride, 0, 0); break;
     WS_PLAN_N(2) WS_PLAN_N(3) WS_PLAN_N(4) WS_PLAN_N(5) WS_PLAN_N(6) WS_PLAN_N(7) WS_PLAN_N(8)
 #undef WS_PLAN_N
     default: return cudaErrorInvalidValue;
@@ -2354,9 +2359,9 @@ static cudaError_t rollout_discrete(const KArgs& a, const Launch& l, int T, uint
   const dim3 grid(grid_for(a.E, 128), (unsigned)((T + kPlanChunk - 1) / kPlanChunk));
   l.m(kKPlan, 0);
   if (step_stride == 0)
-    k_plan_discrete<N, false><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+    k_plan_discrete<N, false><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride, 1);
   else
-    k_plan_discrete<N, true><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride);
+    k_plan_discrete<N, true><<<grid, 128, 0, l.stream>>>(a, T, t0, probs, row_stride, step_stride, 1);
   l.m(kKPlan, 1);
   *launches += 1;
   const cudaError_t err = cudaGetLastError();
@@ -2419,7 +2424,8 @@ static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint6
   const int wpb = l.block / 32;  // warps per CTA
   l.m(kKRollout, 0);
   {  // segments of ceil(D/4) lanes, 32 / ceil(D/4) replicas per warp
-    const size_t smem = 256 * sizeof(unsigned long long);  // CTA statistics only (energies via shuffles)
+    // CTA statistics accumulator + one 16-slot statistics window per warp (energies via shuffles)
+    const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * 3 * 16 * kWinStride * sizeof(uint32_t);
     k_rollout_surface_seg<D><<<grid_for(a.E, (int64_t)wpb * SurfSeg<D>::R), l.block, smem, l.stream>>>(a, T);
   }
   l.m(kKRollout, 1);

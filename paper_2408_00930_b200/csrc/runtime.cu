@@ -507,7 +507,10 @@ ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_strid
   ws_status s = ensure_store(h, T);
   if (s) return s;
   if (T > h->T_cap) return fail(h, WS_ERR_OUT_OF_RANGE, "T exceeds the store capacity (S:79)");
-  cudaError_t e = cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
+  // the discrete lane envs' plan kernel clears the statistics slab itself
+  const bool plan_zeroes = h->spec.kind == ws::kCartPole || h->spec.kind == ws::kAcrobot || h->spec.kind == ws::kDummy;
+  cudaError_t e = plan_zeroes ? cudaSuccess
+                              : cudaMemsetAsync(h->stats, 0, (size_t)T * 4 * sizeof(unsigned long long), h->stream);
   if (!e && h->spec.kind == ws::kUser) {  // NEXT-N4: NVRTC-compiled fused roll-out
     if (h->timing) mark_kernel(h, ws::kKRollout, 0);
     e = ws::launch_user_rollout(ws::UserLaunch{kargs(h), h->spec.user, h->user_prm, h->user_shared, h->stream}, T,
