@@ -127,10 +127,13 @@ struct Lane<Acrobot> {
   __device__ static bool valid(int a) { return Acrobot::valid(a); }
   static constexpr int kMinEpisode = 1;  // no proven bound: keep the per-step reset check
   static constexpr bool kRolled = true;  // ~1000-instruction step: a rolled loop keeps the I-cache warm
-  // throughput build: an 8-row statistics window and <= 80 registers give 6 resident CTAs of
-  // 128 threads per SM (C3a 100K: one wave); latency build: 32 rows, unconstrained registers
+  // throughput build: an 8-row statistics window and <= 96 registers (5 resident CTAs of 128
+  // threads per SM, no spills); latency build: 32 rows, unconstrained registers
   static constexpr int kMaxThreads = 128;
-  static constexpr int kWinRowsLat = 32, kWinRowsThr = 8, kMinBlocksThr = 6;
+#ifndef WS_ACRO_MINB
+#define WS_ACRO_MINB 5  // 96 registers, no spills (6: 80 with spills; C3a 3.00 -> 2.94 ms, C3S 10.2 -> 9.9 ms)
+#endif
+  static constexpr int kWinRowsLat = 32, kWinRowsThr = 8, kMinBlocksThr = WS_ACRO_MINB;
   __device__ static bool fast_ok(const St&) { return true; }
 };
 
