@@ -170,6 +170,43 @@ __device__ __forceinline__ float cos_c(float x) {
   return (float)cd;
 }
 
+// exp64: branch-free fp64 e^x (no slow-path branch, so independent evaluations interleave;
+// libdevice's exp(double) has one).  x is clamped to [-746, 710] (e^x is 0 / inf beyond in
+// fp64; NaN propagates); k = round(x log2 e) by the 2^52 + 2^51 trick, r = x - k ln2 with the
+// fdlibm two-part ln2 (k ln2_hi exact), e^r = 1 + r (1 + r (1/2 + r T(r))) with T the Taylor
+// tail 1/3! .. r^10/13! (truncation < 2^-57 relative on |r| <= ln2 / 2) in Estrin form and the
+// last three steps in Horner form (final rounding error ~0.5-0.8 ulp), then 2^k applied as two
+// exact power-of-two factors (one rounding, gradual underflow).  The R3 contract rounds what
+// is built from it to fp32 once; pinned against the host libm through the surface-energy and
+// surface roll-out parity tests (tests/test_gpu_kernels.py, tests/test_gpu_parity.py).  (In the
+// policy kernels' softmax it measured 5 % slower than libdevice's exp, so they keep the latter.)
+__constant__ double kExp[15] = {
+    1.44269504088896338700e+00,  // 0  log2 e
+    6.93147180369123816490e-01,  // 1  ln2 hi (fdlibm)
+    1.90821492927058770002e-10,  // 2  ln2 lo
+    6755399441055744.0,          // 3  2^52 + 2^51
+    1.0 / 6.0, 1.0 / 24.0, 1.0 / 120.0, 1.0 / 720.0, 1.0 / 5040.0, 1.0 / 40320.0, 1.0 / 362880.0,
+    1.0 / 3628800.0, 1.0 / 39916800.0, 1.0 / 479001600.0, 1.0 / 6227020800.0};  // 4..14: 1/3! .. 1/13!
+
+__device__ __forceinline__ double exp64(const double x0) {
+  const double x = fmin(fmax(x0, -746.0), 710.0);
+  const double kd = fma(x, kExp[0], kExp[3]);
+  const double k = kd - kExp[3];
+  const int ki = __double2loint(kd);
+  double r = fma(-k, kExp[1], x);
+  r = fma(-k, kExp[2], r);
+  const double r2 = r * r, r4 = r2 * r2, r8 = r4 * r4;
+  const double t01 = fma(r, kExp[5], kExp[4]), t23 = fma(r, kExp[7], kExp[6]);
+  const double t45 = fma(r, kExp[9], kExp[8]), t67 = fma(r, kExp[11], kExp[10]);
+  const double t89 = fma(r, kExp[13], kExp[12]);
+  const double u0 = fma(r2, t23, t01), u1 = fma(r2, t67, t45), u2 = fma(r2, kExp[14], t89);
+  const double T = fma(r8, u2, fma(r4, u1, u0));
+  const double p = fma(r, fma(r, fma(r, T, 0.5), 1.0), 1.0);
+  const int k1 = ki >> 1, k2 = ki - k1;  // 2^k = 2^k1 2^k2, each a normal double
+  const double y = (p * __hiloint2double((k1 + 1023) << 20, 0)) * __hiloint2double((k2 + 1023) << 20, 0);
+  return x0 == x0 ? y : x0;
+}
+
 // IEEE fp32 arithmetic without contraction: the library is built with --fmad=false, and
 // these make the intended rounding explicit where it matters.
 __device__ __forceinline__ float fmul(float a, float b) { return __fmul_rn(a, b); }

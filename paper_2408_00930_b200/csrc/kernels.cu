@@ -1433,14 +1433,14 @@ struct SurfSegWarp {
     double tv[kTermsPerLane];
     if constexpr (L >= 4) {
       const double dx = x - mc[4], dy = y - mc[5];
-      tv[0] = mc[0] * exp(mc[1] * dx * dx + mc[2] * dx * dy + mc[3] * dy * dy);
+      tv[0] = mc[0] * exp64(mc[1] * dx * dx + mc[2] * dx * dy + mc[3] * dy * dy);
     } else {
 #pragma unroll
       for (int r = 0; r < kTermsPerLane; ++r) {
         const int m = min(r * L + sl, 3);
         const double dx = x - __ldg(&kMB[4][m]), dy = y - __ldg(&kMB[5][m]);
-        tv[r] = __ldg(&kMB[0][m]) * exp(__ldg(&kMB[1][m]) * dx * dx + __ldg(&kMB[2][m]) * dx * dy +
-                                        __ldg(&kMB[3][m]) * dy * dy);
+        tv[r] = __ldg(&kMB[0][m]) * exp64(__ldg(&kMB[1][m]) * dx * dx + __ldg(&kMB[2][m]) * dx * dy +
+                                          __ldg(&kMB[3][m]) * dy * dy);
       }
     }
     double t[4];
@@ -1610,25 +1610,128 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       cta.push(lane, wdx, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats);
     }
   };
+  // Fast 4-step trip (round 2).  The only loop-carried dependence of a step without a reset is
+  // the clip-and-add state update; the energy (fp64 exp + shuffles, ~1300 cycles in one()) and the
+  // goal test only feed the reward, the stores and the done flag.  So when no replica of the warp
+  // can finish inside the trip -- every action finite, no truncation, and every post-step state
+  // provably outside the goal ball -- the trip computes the four states first, then the four
+  // energies as independent chains, then the rewards and stores: the same values in the same
+  // order as four one() calls.  The goal proof: d2 is a sum of non-negative fp64 terms, so with
+  // monotone rounding it is >= any lane's partial sum; one lane partial >= r_goal^2 rules the
+  // goal out (R23's d2 < r_goal^2).  Otherwise (and for the rare trips with a done flag or an
+  // invalid action) the trip returns false before changing anything and one() runs four times.
+  auto fast4 = [&](const int c, const float (&A0)[C], const float (&A1)[C], const float (&A2)[C],
+                   const float (&A3)[C]) -> bool {
+    const float* act[4] = {A0, A1, A2, A3};
+    bool bad = ep_step + 4 >= a.max_steps;  // a truncation inside the trip
+#pragma unroll
+    for (int k = 0; k < 4; ++k)
+#pragma unroll
+      for (int i = 0; i < C; ++i) bad = bad || (w.valid(i) && !isfinite(act[k][i]));
+    float qs[4][C];
+    bool near = false;
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      float p = 0.0f;
+#pragma unroll
+      for (int i = 0; i < C; ++i) {
+        const float prev = k == 0 ? q[i] : qs[k - 1][i];
+        const float ai = fminf(fmaxf(act[k][i], -Env::delta), Env::delta);
+        qs[k][i] = w.valid(i) ? fminf(fmaxf(prev + ai, lo[i]), hi[i]) : 0.0f;
+        if (w.valid(i)) {
+          const float di = qs[k][i] - (float)Env::goal(sl * C + i);
+          p = p + di * di;
+        }
+      }
+      // the segment may be inside the goal ball only if none of its lanes rules it out.  The
+      // lane partial is evaluated in fp32: against the fp64 partial its error is < 1e-6
+      // relative + 1e-7 absolute (four terms, |goal| < 2), so p > r_goal^2 + 1e-4 proves the
+      // fp64 partial > r_goal^2 as well
+      const unsigned far = __ballot_sync(kFull, p > (float)(Env::r_goal * Env::r_goal) + 1e-4f);
+      near = near || ((far >> (seg * L)) & ((1u << L) - 1u)) == 0u;
+    }
+    if (__any_sync(kFull, w.used && (bad || near))) return false;
+    float En[4];
+#pragma unroll
+    for (int k = 0; k < 4; ++k) En[k] = w.energy(qs[k]);
+#pragma unroll
+    for (int k = 0; k < 4; ++k) {
+      const int ck = c + k;
+      const float Epre = k == 0 ? Ecur : En[k - 1];
+      if (w.used) {
+        float* po = p_obs + (size_t)ck * sE * (D + 1);
+#pragma unroll
+        for (int i = 0; i < C; ++i)
+          if (w.valid(i)) st_cs(po + i, k == 0 ? q[i] : qs[k - 1][i]);
+        if (sl == L - 1) st_cs(po + (D - sl * C), Epre);
+      }
+      const float r = -(Env::w_E * (En[k] - Epre)) - Env::c_step;
+      ep_step = ep_step + 1;
+      ep_ret = ep_ret + r;
+      win.put(ck & (kRows - 1), lane, 0u, 0.0f, 0.0f);
+      win.rew[(ck & (kRows - 1)) * kWinStride + lane] = leader ? r : 0.0f;
+      if (leader) {
+        const size_t idx = (size_t)ck * sE + (size_t)e;
+        st_cs(a.rew + idx, r);
+        st_cs_u8(a.done + idx, (uint8_t)0);
+      }
+    }
+#pragma unroll
+    for (int i = 0; i < C; ++i) q[i] = qs[3][i];
+    Ecur = En[3];
+    const int cl = c + 3;
+    if ((cl & (kRows - 1)) == kRows - 1 || cl == T - 1) {
+      const int wdx = cl / kRows;
+      win.cta_acc = cta.acc(wdx);
+      win.flush(lane, 0, cl & (kRows - 1), cl & ~(kRows - 1), a.stats, 32);
+      cta.push(lane, wdx, 0, cl & (kRows - 1), cl & ~(kRows - 1), a.stats);
+    }
+    return true;
+  };
+  auto trip = [&](const int c, const float (&A0)[C], const float (&A1)[C], const float (&A2)[C],
+                  const float (&A3)[C]) {
+    if (!fast4(c, A0, A1, A2, A3)) {
+      one(c, A0);
+      one(c + 1, A1);
+      one(c + 2, A2);
+      one(c + 3, A3);
+    }
+  };
+  // two action register sets used in turn (no copies: a copy placed by the compiler right after
+  // the loads stalls on them): the next trip's actions load while this trip runs
   float a0[C] = {}, a1[C] = {}, a2[C] = {}, a3[C] = {};
+  float b0[C] = {}, b1[C] = {}, b2[C] = {}, b3[C] = {};
   load_act(0, a0);
   load_act(1, a1);
   load_act(2, a2);
   load_act(3, a3);
   int c = 0;
-  for (; c + 4 <= T; c += 4) {  // four steps per trip, each step's action loaded four steps ahead
-    one(c, a0);
-    load_act(c + 4, a0);
-    one(c + 1, a1);
-    load_act(c + 5, a1);
-    one(c + 2, a2);
-    load_act(c + 6, a2);
-    one(c + 3, a3);
-    load_act(c + 7, a3);
+  for (; c + 8 <= T; c += 8) {
+    load_act(c + 4, b0);
+    load_act(c + 5, b1);
+    load_act(c + 6, b2);
+    load_act(c + 7, b3);
+    trip(c, a0, a1, a2, a3);
+    load_act(c + 8, a0);
+    load_act(c + 9, a1);
+    load_act(c + 10, a2);
+    load_act(c + 11, a3);
+    trip(c + 4, b0, b1, b2, b3);
   }
-  if (c < T) one(c, a0);
-  if (c + 1 < T) one(c + 1, a1);
-  if (c + 2 < T) one(c + 2, a2);
+  if (c + 4 <= T) {  // one more full trip on set a; the tail's actions go to set b
+    load_act(c + 4, b0);
+    load_act(c + 5, b1);
+    load_act(c + 6, b2);
+    trip(c, a0, a1, a2, a3);
+    c += 4;
+    if (c < T) one(c, b0);
+    if (c + 1 < T) one(c + 1, b1);
+    if (c + 2 < T) one(c + 2, b2);
+  } else {
+    if (c < T) one(c, a0);
+    if (c + 1 < T) one(c + 1, a1);
+    if (c + 2 < T) one(c + 2, a2);
+  }
   if (live) {
 #pragma unroll
     for (int i = 0; i < C; ++i) {

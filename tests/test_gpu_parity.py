@@ -266,6 +266,37 @@ def test_env_parity(P, env, E, A, T, params):
     compare(buf, o, amb, env, T)
 
 
+@pytest.mark.parametrize("D", [20, 8, 3])
+def test_surface_goal_reached(P, D):
+    """Per-step Gaussian heads that steer replicas into the goal ball: step 0 cancels each
+    replica's reset offsets in q_2.. (read from the oracle's initial state), then q0 / q1 drift
+    from minimum B toward minimum A (the goal) with tiny noise, so first episodes end at the goal
+    (bonus reward, done bit 0), restart and later truncate; every third replica only diffuses and
+    one replica's head is non-finite.  The segmented kernel's fast 4-step trips must hand every
+    trip that may touch the goal ball (or a truncation / invalid action) to the exact per-step
+    path -- element for element as the oracle."""
+    E, T, ms = 300, {20: 203, 8: 197, 3: 200}[D], 150  # T % 8 = 3, 5, 0: every tail path of the trip loop
+    o = O.Batch("surface", E, 1, SEED, t_capacity=T, p0=D, max_steps=ms)
+    q0 = np.array(o.array("state")).reshape(E, D)
+    probs = np.zeros((T, E, 1, 2 * D), np.float32)
+    probs[..., D:] = np.log(1e-6)
+    probs[:, :, 0, 0] = -0.05 * 1.181 / 1.414
+    probs[:, :, 0, 1] = 0.05
+    if D > 2:
+        probs[0, :, 0, 2:D] = -q0[:, 2:]
+    probs[:, ::3, 0, :2] = 0.0  # every third replica only diffuses: truncated at max_steps
+    probs[:, 7, 0, 0] = np.nan  # an invalid head: replica 7 never advances (sticky error)
+    g = P.Env(E, 1, "surface", SEED, t_capacity=T, param0=D, max_steps=ms)
+    g.rollout(T, torch.from_numpy(probs).cuda(), row_stride=2 * D, step_stride=E * 2 * D)
+    amb = np.zeros((T, E, 1), np.uint8)
+    assert o.rollout(T, probs, row_stride=2 * D, step_stride=E * 2 * D, ambiguous=amb, n_threads=8) == 0
+    assert g.status() == o.synchronize() != 0
+    buf = {k: (v.cpu().numpy() if v is not None else None) for k, v in g.buffers().items()}
+    compare(buf, o, amb, "surface", T)
+    assert int((buf["done"][:T] & 1).sum()) > E // 2  # goal terminations happened
+    assert int((buf["done"][:T] & 2).sum()) > E // 4  # and truncations
+
+
 @pytest.mark.parametrize("cfg,windows", [("C3a", [(0, 128), (49_936, 128), (99_872, 128)]),
                                          ("C3b", [(0, 128), (77_000, 128)]),
                                          ("C4", [(0, 8), (992, 8)]),
