@@ -1067,7 +1067,8 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
 // range of GAUSS draws j = t*d + k, one Philox4x32 call per 4 draws and one fp64
 // Box-Muller per pair, and writes act = mean + exp(log_std) z and logp (R14) into the store.
 // =======================================================================================
-constexpr int kGaussChunk = 32;  // steps per thread
+constexpr int kGaussChunk = 32;  // steps per thread (k_plan_gauss_warp: = the warp size, lane = step)
+static_assert(kGaussChunk == 32, "k_plan_gauss_warp maps the chunk's steps onto the lanes");
 
 template <int DIM, bool kStrided>
 __global__ void __launch_bounds__(128) k_plan_gauss(const KArgs a, const int T, const uint64_t t0,
@@ -1814,26 +1815,55 @@ __global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const in
   __shared__ float zbuf[4][kGaussChunk * DIM];
   float* const zb = zbuf[(threadIdx.x >> 5) & 3];
   const uint64_t J0 = (t0 + (uint64_t)c_begin) * (uint64_t)DIM, J1 = (t0 + (uint64_t)c_end) * (uint64_t)DIM;
-  for (uint64_t pr = (J0 >> 1) + (uint64_t)lane; pr < ((J1 + 1) >> 1); pr += 32) {
-    const U4 w = block(key, pr >> 1, eg, 0, kGauss);
-    float ze, zo;
-    gauss_pair(w, (int)(pr & 1), ze, zo);
-    const int64_t i0 = (int64_t)(2 * pr) - (int64_t)J0;
-    if (i0 >= 0) zb[i0] = ze;
-    if (i0 + 1 < (int64_t)(J1 - J0)) zb[i0 + 1] = zo;
+  // one Philox block (two pairs, four normals) per lane and iteration: no block computed twice
+  for (uint64_t b = (J0 >> 2) + (uint64_t)lane; b < ((J1 + 3) >> 2); b += 32) {
+    const U4 w = block(key, b, eg, 0, kGauss);
+    const int64_t i0 = (int64_t)(4 * b) - (int64_t)J0;
+    const int64_t n = (int64_t)(J1 - J0);
+#pragma unroll
+    for (int p = 0; p < 2; ++p) {
+      const int64_t i = i0 + 2 * p;
+      if (i + 1 >= 0 && i < n) {  // the pair has a draw inside [J0, J1)
+        float ze, zo;
+        gauss_pair(w, p, ze, zo);
+        if (i >= 0) zb[i] = ze;
+        if (i + 1 < n) zb[i + 1] = zo;
+      }
+    }
   }
   __syncwarp();
   float* const p_act = reinterpret_cast<float*>(a.act) + e * DIM + kk;
   bool any_bad = false;
-  for (int c = c_begin; c < c_end; ++c) {
-    if (kStrided) load_head(probs + (int64_t)c * step_stride);
-    const float z = zb[(c - c_begin) * DIM + kk];
-    const double term = act_lane ? (((-0.5 * (double)z) * (double)z - (double)ls) - kHalfLog2Pi) : 0.0;
-    const double lp = warp_tree_sum(term);
-    const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
-    if (act_lane) st_cs(p_act + (size_t)c * (size_t)a.E * DIM, ok ? mean + sd * z : __int_as_float(0x7fc00000));
-    if (lane == 0 && a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : __int_as_float(0x7fc00000));
-    any_bad |= !ok;
+  if constexpr (!kStrided) {
+    // one head for the whole chunk: lanes = coordinates for the act rows, then lanes = steps for
+    // the log-densities, lp = -(sum_k z_k^2) / 2 - sum_k (log sd_k + log(2 pi) / 2) in fp64 (R14;
+    // the association is free: one fp32 rounding follows, R18 <= 2 ulp) -- no per-step warp
+    // reduction
+    for (int c = c_begin; c < c_end; ++c) {
+      const float z = zb[(c - c_begin) * DIM + kk];
+      if (act_lane) st_cs(p_act + (size_t)c * (size_t)a.E * DIM, ok ? mean + sd * z : __int_as_float(0x7fc00000));
+    }
+    const double cst = warp_tree_sum(act_lane ? (double)ls + kHalfLog2Pi : 0.0);
+    const int c = c_begin + lane;
+    if (a.write_logp && c < c_end) {
+      double s2 = 0.0;
+      const float* zr = zb + lane * DIM;
+#pragma unroll
+      for (int k = 0; k < DIM; ++k) s2 = fma((double)zr[k], (double)zr[k], s2);
+      st_cs(a.logp + (size_t)c * (size_t)a.E + (size_t)e, ok ? (float)(-0.5 * s2 - cst) : __int_as_float(0x7fc00000));
+    }
+    any_bad = !ok;
+  } else {
+    for (int c = c_begin; c < c_end; ++c) {
+      load_head(probs + (int64_t)c * step_stride);
+      const float z = zb[(c - c_begin) * DIM + kk];
+      const double term = act_lane ? (((-0.5 * (double)z) * (double)z - (double)ls) - kHalfLog2Pi) : 0.0;
+      const double lp = warp_tree_sum(term);
+      const size_t idx = (size_t)c * (size_t)a.E + (size_t)e;
+      if (act_lane) st_cs(p_act + (size_t)c * (size_t)a.E * DIM, ok ? mean + sd * z : __int_as_float(0x7fc00000));
+      if (lane == 0 && a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : __int_as_float(0x7fc00000));
+      any_bad |= !ok;
+    }
   }
   if (lane == 0 && any_bad) atomicOr(a.err, kErrProbs);
 }
