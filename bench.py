@@ -476,13 +476,20 @@ class Run:
                     self.step()
                 self.barrier()
 
-    def timed(self, K, flush):
-        """K steps timed with CUDA events on the handle's stream, one event per step boundary
-        (per-step times for p10 / p90).  flush: an L2 flush (a 256 MB write) before every step,
-        outside the events (stores smaller than L2)."""
+    def timed(self, K, flush, per_step=False):
+        """K steps timed with CUDA events on the handle's stream: two events around the K steps
+        (per_step: one event per step boundary, per-step times for p10 / p90).  flush: an L2
+        flush (a 256 MB write) before every step, outside the events (stores smaller than L2)."""
         ev = [torch.cuda.Event(enable_timing=True) for _ in range(K + 1 if not flush else 2 * K)]
         self.barrier()
-        if not flush:
+        if not flush and not per_step:  # two events: an event between steps costs the loop ~3 us
+            ev[0].record(self.stream)
+            for k in range(K):
+                self.step()
+            ev[1].record(self.stream)
+            self.barrier()
+            per = [ev[0].elapsed_time(ev[1]) / K] * K
+        elif not flush:
             ev[0].record(self.stream)
             for k in range(K):
                 self.step()
@@ -739,9 +746,12 @@ def main():
     if not args.ncu:
         clocks.start()
         time.sleep(0.3)
-    # two CUDA events per step around the fused roll-out kernel only (libws ws_kernel_times):
-    # the dominant kernel is timed live with the least perturbation of the timed loop
-    run.env.enable_kernel_timing(0 if (args.no_kernel_timing or run.staged) else (3 if run.gae else 2))
+    # two CUDA events around the fused roll-out kernel only (libws ws_kernel_times), on every
+    # fourth launch of a >= 8-step timed loop: the dominant kernel is timed live with the least
+    # perturbation of the timed loop (an event pair between kernels costs it ~6 us per step)
+    kt_period = 4 if args.steps >= 8 else 1
+    run.env.enable_kernel_timing(0 if (args.no_kernel_timing or run.staged) else (3 if run.gae else 2),
+                                 period=kt_period)
     run.env.kernel_times()
     launches0 = run.env.info().launches
     per = run.timed(args.steps, flush)
@@ -768,7 +778,7 @@ def main():
     sustained = None
     if not args.ncu and args.sustain_s > 0:
         n_sus = int(min(100000, max(args.steps, np.ceil(args.sustain_s * 1e3 / max(ms_per_step, 1e-3)))))
-        per_s = run.timed(n_sus, flush)
+        per_s = run.timed(n_sus, flush, per_step=True)
         sus_ms = run.max_over_ranks(sum(per_s))
         sustained = {"steps": n_sus, "seconds": round(sus_ms / 1e3, 3), "value": E_g * T * n_sus / (sus_ms / 1e3),
                      "ms_per_step": sus_ms / n_sus, "p10_ms": pct(per_s, 10), "p50_ms": pct(per_s, 50),
@@ -833,8 +843,11 @@ def main():
             "steps": args.steps, "warmup": args.warmup, "ms_per_step": ms_per_step, "higher_is_better": True,
             "scaling": args.scaling, "vs_baseline": None, "dtype": "f32", "data": "synthetic",
             "config": make_config(w, world, args.scaling, "p2p" if p2p else "nccl"),
-            "timing": {"p10_ms": pct(per, 10), "p50_ms": pct(per, 50), "p90_ms": pct(per, 90), "l2": l2,
-                       "per_step_events": True},
+            "timing": ({"p10_ms": pct(per, 10), "p50_ms": pct(per, 50), "p90_ms": pct(per, 90), "l2": l2,
+                        "per_step_events": True} if flush else
+                       {"l2": l2, "per_step_events": False,
+                        "note": "two events around the K steps (per-step p10 / p50 / p90: `sustained`); the "
+                                "roll-out kernel bracketed on every %d-th step" % kt_period}),
             "roofline": roofline, "gpu_launches": int(launches),
             "episode_stats_last_step": merged,
             "clocks": clk, "e2e": e2e, "sustained": sustained,

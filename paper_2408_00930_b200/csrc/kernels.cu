@@ -927,25 +927,36 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
     }
     return fadd(wv[H], fadd(fadd(P[0], P[1]), fadd(P[2], P[3])));
   };
-  // finish step c of group g: partials -> logits -> draw -> dynamics -> stores / statistics;
-  // returns whether any lane reset (its look-ahead state is refilled after the next publish)
-  auto finish = [&](int g, int c) -> bool {
+  // Step c of group g in two parts.  finish_a is the recurrence: partials -> logits -> draw ->
+  // dynamics -> auto-reset (returns whether any lane reset; its look-ahead state is refilled
+  // after the next publish).  finish_b is everything that only feeds the store -- the fp64 log
+  // of the log-probability, the act / logp / obs / value / rew / done stores and the statistics
+  // window -- and runs after the next observation is published, i.e. while the inference warps
+  // evaluate step c + 1 (the same values; only the program order changes).
+  struct Pend {
+    St s_pre;
+    typename L::Aux aux_pre;
+    float pa, vv, rw, ret;
+    double cN;
+    int act;
+    int32_t es;
+    uint32_t d;
+  };
+  auto finish_a = [&](int g, int c, Pend& p) -> bool {
     Grp& r = G[g];
     const uint64_t t = t0 + (uint64_t)c;
     if (c == 0 || (t & 3) == 0) r.w4 = block(key, t >> 2, r.eg, 0, kAction);
-    const size_t idx = (size_t)c * sE + (size_t)r.ec;
-    float lg[N], vv = 0.0f;
+    float lg[N];
 #pragma unroll
     for (int i = 0; i < N; ++i) {
       const float* pp = &x.part[g][0][i][lane];
       lg[i] = fadd(b2[i], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
     }
+    p.vv = 0.0f;
     if (kCritic) {
       const float* pp = &x.part[g][0][N][lane];
-      vv = fadd(wv[H], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
-      if (r.live) st_cs(values + idx, vv);
+      p.vv = fadd(wv[H], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
     }
-    L::obs_store_aux(a.obs + idx * L::D, r.s, r.aux, true);
     float m = lg[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -978,14 +989,18 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
     cdf.bad = badp || !(run > 0.0) || !isfinite(run);
     // ---- A2 draw (R13) from the ACTION stream
     int act = search<N>(cdf, u01(pick(r.w4, (uint32_t)(t & 3))));
-    float lp = logp_of_normalised<N>(cdf, act);
+    p.pa = cdf.P[0];
+#pragma unroll
+    for (int i = 1; i < N; ++i)
+      if (act == i) p.pa = cdf.P[i];
+    p.cN = cdf.C[N - 1];
     if (cdf.bad) {
       act = -1;
-      lp = __int_as_float(0x7fc00000);
       if (r.live) err |= kErrProbs | kErrAction;
     }
-    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
-    if (a.write_logp) st_cs(a.logp + idx, lp);
+    p.act = act;
+    p.s_pre = r.s;
+    p.aux_pre = r.aux;
     // ---- A3-A5
     const bool bad = act < 0;
     St s2 = r.s;
@@ -1000,17 +1015,19 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
       L::template step_aux<false>(s2, aux2, bad ? 0 : act, rr, term);
     const int32_t es = r.ep_step + 1;
     const uint32_t d = bad ? 0u : ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u));
-    const float rw = bad ? 0.0f : rr;
-    const float ret = r.ep_ret + rr;
+    p.rw = bad ? 0.0f : rr;
+    p.ret = r.ep_ret + rr;
+    p.es = es;
+    p.d = d;
     if (!bad) {
       r.s = s2;
       r.aux = aux2;
       r.ep_step = es;
-      r.ep_ret = ret;
+      r.ep_ret = p.ret;
     }
     if (kCritic && values_trunc && __any_sync(kFull, d == 2u)) {  // truncated only: V of the post-step state
       const float v2 = value_of(r.s, r.aux);
-      if (r.live && d == 2u) st_cs(values_trunc + idx, v2);
+      if (r.live && d == 2u) st_cs(values_trunc + (size_t)c * sE + (size_t)r.ec, v2);
     }
     if (d) {  // auto-reset (R11) from the look-ahead state init(e, rc + 1)
       r.rc += 1;
@@ -1019,26 +1036,43 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
       r.ep_step = 0;
       r.ep_ret = 0.0f;
     }
-    st_cs(a.rew + idx, rw);
-    st_cs_u8(a.done + idx, (uint8_t)d);
-    r.win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+    return __any_sync(kFull, d != 0);
+  };
+  auto finish_b = [&](int g, int c, const Pend& p) {
+    Grp& r = G[g];
+    const size_t idx = (size_t)c * sE + (size_t)r.ec;
+    if (kCritic && r.live) st_cs(values + idx, p.vv);
+    L::obs_store_aux(a.obs + idx * L::D, p.s_pre, p.aux_pre, true);
+    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, p.act);
+    if (a.write_logp) {
+      // logp_of_normalised: log p_a - log(sum of the normalised row), fp64 (R13 / R18)
+      const double dd = p.cN - 1.0;
+      const double lC = fabs(dd) < 1e-6 ? dd * (1.0 - dd * (0.5 - dd * (1.0 / 3.0))) : log(p.cN);
+      const float lp = p.act < 0 ? __int_as_float(0x7fc00000) : (float)(log((double)p.pa) - lC);
+      st_cs(a.logp + idx, lp);
+    }
+    st_cs(a.rew + idx, p.rw);
+    st_cs_u8(a.done + idx, (uint8_t)p.d);
+    r.win.put(c & (kRows - 1), lane, p.d ? (uint32_t)p.es : 0u, p.d ? p.ret : 0.0f, p.rw);
     if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
       r.win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, r.nlive);
-    return __any_sync(kFull, d != 0);
   };
   auto refill = [&](int g, bool any) {
     if (any) L::init(key, G[g].eg, G[g].rc + 1, G[g].nxt);  // (lanes without a reset recompute the same state)
   };
   publish(0);
   for (int c = 0; c < T; ++c) {
+    Pend pa, pb;
     if constexpr (NG == 2) publish(NG - 1);
     asm volatile("bar.sync 2, 160;" ::: "memory");  // group A's partials of step c
-    const bool ra = finish(0, c);
+    const bool ra = finish_a(0, c, pa);
     if (c + 1 < T) publish(0);
+    finish_b(0, c, pa);
     refill(0, ra);
     if constexpr (NG == 2) {
       asm volatile("bar.sync 4, 160;" ::: "memory");  // group B's partials of step c
-      const bool rb = finish(NG - 1, c);
+      const bool rb = finish_a(NG - 1, c, pb);
+      finish_b(NG - 1, c, pb);
       refill(NG - 1, rb);
     }
   }

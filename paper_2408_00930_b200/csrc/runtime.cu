@@ -118,8 +118,11 @@ struct ws_env {
   struct Ring {
     std::vector<cudaEvent_t> b, e;
     int n = 0, open = 0;
+    uint64_t calls = 0;  // launches seen (the sampling period picks every period-th)
+    bool skip = false;   // the open launch is not sampled
   };
   bool timing = false;
+  int timing_period = 1;  // events on every period-th launch of a timed class
   uint32_t timed_mask = 0;  // kernels (bit = KernelId) that get events
   // cross-GPU statistics reduction over peer memory (ws_peer_export / ws_peer_attach)
   unsigned long long* peer_own = nullptr;  // this rank's gather buffer (cudaMalloc, IPC-exported)
@@ -218,8 +221,9 @@ void mark_kernel(void* ctx, int kernel, int phase) {
   ws_env::Ring& r = h->rings[kernel];
   const int i = r.n % kTimingCap;
   if (phase == 0) {
-    cudaEventRecord(r.b[i], h->stream);
-  } else {
+    r.skip = (r.calls++ % (uint64_t)h->timing_period) != 0;
+    if (!r.skip) cudaEventRecord(r.b[i], h->stream);
+  } else if (!r.skip) {
     cudaEventRecord(r.e[i], h->stream);
     r.n += 1;
   }
@@ -911,7 +915,7 @@ ws_status ws_peer_detach(ws_env* h) {
 ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
   DeviceGuard g(h->device);
-  if (enable && h->rings[0].b.empty()) {
+  if ((enable & 0xFF) && h->rings[0].b.empty()) {
     for (auto& r : h->rings) {
       r.b.resize(kTimingCap);
       r.e.resize(kTimingCap);
@@ -922,11 +926,17 @@ ws_status ws_enable_kernel_timing(ws_env* h, int32_t enable) {
       }
     }
   }
-  for (auto& r : h->rings) r.n = 0;
-  h->timing = enable != 0;
-  h->timed_mask = enable == 2   ? (1u << ws::kKRollout)
-                 : enable == 3 ? (1u << ws::kKRollout) | (1u << ws::kKGae)
-                               : 0xFFFFFFFFu;
+  for (auto& r : h->rings) {
+    r.n = 0;
+    r.calls = 0;
+    r.skip = false;
+  }
+  const int mode = enable & 0xFF, period = (enable >> 8) & 0xFF;
+  h->timing = mode != 0;
+  h->timing_period = period > 1 ? period : 1;
+  h->timed_mask = mode == 2   ? (1u << ws::kKRollout)
+                 : mode == 3 ? (1u << ws::kKRollout) | (1u << ws::kKGae)
+                             : 0xFFFFFFFFu;
   return WS_OK;
 }
 

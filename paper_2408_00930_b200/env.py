@@ -219,11 +219,14 @@ class Env:
         check(lib().ws_read_stats(self._h, t0, info.cursor if t1 is None else t1, C.byref(out)), self._h)
         return out
 
-    def enable_kernel_timing(self, enable=True):
+    def enable_kernel_timing(self, enable=True, period: int = 1):
         """True / 1: events around every kernel; 2: around the fused roll-out kernel only;
-        False / 0: off (ws.h ws_enable_kernel_timing)."""
+        3: roll-out and GAE; False / 0: off; period P > 1: only every P-th launch of a timed
+        class is bracketed (ws.h ws_enable_kernel_timing)."""
         mode = 0 if enable is False else (1 if enable is True else int(enable))
-        check(lib().ws_enable_kernel_timing(self._h, mode), self._h)
+        if not 1 <= int(period) <= 255:
+            raise ValueError("period must be in [1, 255]")
+        check(lib().ws_enable_kernel_timing(self._h, mode | (int(period) << 8 if period > 1 else 0)), self._h)
 
     def rollout_policy(self, T: int, weights: torch.Tensor, hidden: int) -> None:
         """NEXT-N1: T fused steps whose actions are drawn from an in-kernel MLP policy
