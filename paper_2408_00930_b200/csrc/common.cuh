@@ -5,8 +5,17 @@
 // Citation keys: P:n PAPER.md, S:n SPEC.md, BJ:5 north_star, Rk = DESIGN.md reading k.
 #pragma once
 
+#ifdef __CUDACC_RTC__  // also compiled into the env composer's NVRTC programs (composer.cu)
+typedef unsigned char uint8_t;
+typedef unsigned short uint16_t;
+typedef unsigned int uint32_t;
+typedef int int32_t;
+typedef unsigned long long uint64_t;
+typedef long long int64_t;
+#else
 #include <cstdint>
 #include <cuda_runtime.h>
+#endif
 
 namespace ws {
 

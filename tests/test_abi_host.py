@@ -182,6 +182,11 @@ def test_register_env_compiles_without_gpu():
         d.update(bad)
         assert L.ws_register_env(C.byref(_abi.ws_env_def(**d)), buf, 256) == _abi.INVALID_ARGUMENT, bad
     assert L.ws_set_env_data(None, None, None) == _abi.INVALID_ARGUMENT
+    # every shipped user env (discrete, continuous, per-replica parameters) compiles against the
+    # library's own device headers (common.cuh / sampler.cuh are NVRTC headers of the program)
+    for name, (src, dims) in U.ENVS.items():
+        P.register_env("h_" + name, src, **dims)
+        assert L.ws_registered_env(("h_" + name).encode()) == 1
 
 
 def test_param_checkpoint_round_trip_without_gpu(tmp_path):
