@@ -1907,9 +1907,10 @@ __global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const in
 // =======================================================================================
 // ws_sample, discrete rows (any A): warp-cooperative scan + search, one row per lane.
 template <int N>
-__global__ void __launch_bounds__(256) k_sample_discrete(const KArgs a, const int slot, const uint64_t t,
+__global__ void __launch_bounds__(256) k_sample_discrete(const KArgs a, const int slot, const uint64_t t_host,
                                                         const float* __restrict__ probs,
                                                         const int64_t row_stride) {
+  const uint64_t t = a.t_dev ? *a.t_dev : t_host;
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;  // e*A + agent
   const int lane = threadIdx.x & 31;
   const int64_t n_rows = a.E * (int64_t)a.A;
@@ -1932,9 +1933,10 @@ __global__ void __launch_bounds__(256) k_sample_discrete(const KArgs a, const in
 }
 
 template <int DIM>
-__global__ void __launch_bounds__(256) k_sample_continuous(const KArgs a, const int slot, const uint64_t t,
+__global__ void __launch_bounds__(256) k_sample_continuous(const KArgs a, const int slot, const uint64_t t_host,
                                                           const float* __restrict__ probs,
                                                           const int64_t row_stride) {
+  const uint64_t t = a.t_dev ? *a.t_dev : t_host;
   const int64_t row = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
   const int64_t n_rows = a.E * (int64_t)a.A;
   if (row >= n_rows) return;
@@ -1963,6 +1965,7 @@ __global__ void __launch_bounds__(256) k_step_lane(const KArgs a, const int slot
   using St = typename L::St;
   const int lane = threadIdx.x & 31;
   const int64_t e = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  if (a.t_dev && e == 0) *a.t_dev += 1;  // device clock: nothing in this kernel reads it
   if (e - lane >= a.E) return;  // whole warp past the last replica
   const bool live = e < a.E;
   const int64_t ec = live ? e : a.E - 1;
@@ -2104,6 +2107,7 @@ __global__ void __launch_bounds__(kMaxThreads, kMinBlocks) k_tag(const KArgs a, 
                                               const void* __restrict__ given, float* __restrict__ values,
                                               float* __restrict__ bootstrap) {
   extern __shared__ int smem[];
+  if (a.t_dev && mode != kTagRollout && blockIdx.x == 0 && threadIdx.x == 0) *a.t_dev += 1;  // device clock
   const int G = a.p0, NT = a.p1, A = a.A;
   const int nwarps = blockDim.x >> 5;
   int* taggers_on = smem;

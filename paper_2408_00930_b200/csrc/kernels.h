@@ -35,6 +35,10 @@ struct KArgs {
   int32_t write_logp;
   int32_t p0, p1;     // env params (tag G / taggers; surface D)
   uint32_t k0, k1;    // Philox key
+  // device step counter (ws_enable_device_clock) or null: the single-step sampler reads its
+  // ACTION draw index t from here and every single step advances it, so captured CUDA graphs of
+  // sample / step sequences replay with fresh draws (NEXT-N1 policy graphs)
+  uint64_t* t_dev;
 };
 
 // kernel classes for the optional per-kernel timing (ws_enable_kernel_timing)

@@ -132,6 +132,9 @@ struct ws_env {
   uint64_t peer_epoch = 0;
   double peer_timeout_s = 30.0;
   Ring rings[ws::kKCount];
+  // device step counter (ws_enable_device_clock): authoritative while dev_clock is set
+  uint64_t* t_dev = nullptr;
+  bool dev_clock = false;
 };
 
 namespace {
@@ -210,6 +213,7 @@ ws::KArgs kargs(const ws_env* h) {
   a.p1 = h->p1;
   a.k0 = (uint32_t)h->seed;
   a.k1 = (uint32_t)(h->seed >> 32);
+  a.t_dev = h->dev_clock ? h->t_dev : nullptr;
   return a;
 }
 
@@ -318,6 +322,13 @@ ws_status ws_create(int64_t n_envs, int32_t n_agents, const char* env, uint64_t 
 
 ws_status ws_set_time(ws_env* h, uint64_t t) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (h->dev_clock) {
+    DeviceGuard g(h->device);
+    cudaError_t e;
+    if ((e = cudaMemcpyAsync(h->t_dev, &t, sizeof(t), cudaMemcpyHostToDevice, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+      return cuda_fail(h, e, "ws_set_time device clock");
+  }
   h->t = t;
   h->cursor = 0;
   h->sampled_slot = -1;
@@ -440,6 +451,33 @@ ws_status ws_reset(ws_env* h) {
   h->t = 0;
   h->cursor = 0;
   h->sampled_slot = -1;
+  if (h->dev_clock && (e = cudaMemsetAsync(h->t_dev, 0, sizeof(uint64_t), h->stream)))
+    return cuda_fail(h, e, "ws_reset device clock");
+  return WS_OK;
+}
+
+ws_status ws_enable_device_clock(ws_env* h, int32_t enable) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  DeviceGuard g(h->device);
+  cudaError_t e;
+  if (enable && !h->dev_clock) {
+    if (!h->t_dev) {
+      h->t_dev = (uint64_t*)dev_alloc(h, sizeof(uint64_t), &e);
+      if (e) return cuda_fail(h, e, "alloc device clock");
+    }
+    const uint64_t t = h->t;
+    if ((e = cudaMemcpyAsync(h->t_dev, &t, sizeof(t), cudaMemcpyHostToDevice, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+      return cuda_fail(h, e, "ws_enable_device_clock");
+    h->dev_clock = true;
+  } else if (!enable && h->dev_clock) {
+    uint64_t t = 0;
+    if ((e = cudaMemcpyAsync(&t, h->t_dev, sizeof(t), cudaMemcpyDeviceToHost, h->stream)) ||
+        (e = cudaStreamSynchronize(h->stream)))
+      return cuda_fail(h, e, "ws_enable_device_clock");
+    h->t = t;
+    h->dev_clock = false;
+  }
   return WS_OK;
 }
 
@@ -505,6 +543,8 @@ static ws_status peer_merge(ws_env* h, int32_t T) {
 ws_status ws_rollout(ws_env* h, int32_t T, const float* probs, int64_t row_stride, int64_t step_stride) {
   NvtxRange nvtx_("ws_rollout");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (h->dev_clock)
+    return fail(h, WS_ERR_BAD_STATE, "device clock on (ws_enable_device_clock): fused roll-outs take the host step index");
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!probs || row_stride < 0 || step_stride < 0) return fail(h, WS_ERR_INVALID_ARGUMENT, "bad probs / strides");
   DeviceGuard g(h->device);
@@ -555,6 +595,8 @@ static ws_status run_policy(ws_env* h, int32_t T, const float* weights, int32_t 
                             float* bootstrap, float* values_trunc = nullptr) {
   NvtxRange nvtx_("ws_rollout_policy");
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (h->dev_clock)
+    return fail(h, WS_ERR_BAD_STATE, "device clock on (ws_enable_device_clock): fused roll-outs take the host step index");
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1 (S:166)");
   if (!weights || (hidden != 32 && hidden != 64)) return fail(h, WS_ERR_INVALID_ARGUMENT, "weights / hidden (32 or 64)");
   if ((h->A != 1 && h->spec.kind != ws::kTag) || (h->spec.n_actions < 1 && h->spec.kind != ws::kPendulum) ||
@@ -656,6 +698,8 @@ ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t
 ws_status ws_rollout_staged(ws_env* h, int32_t T, const float* host_probs, int64_t n_probs, int64_t row_stride,
                             int64_t step_stride, const ws_host_store* dst, ws_staged_report* out) {
   if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (h->dev_clock)
+    return fail(h, WS_ERR_BAD_STATE, "device clock on (ws_enable_device_clock): fused roll-outs take the host step index");
   if (T < 1) return fail(h, WS_ERR_INVALID_ARGUMENT, "T must be >= 1");
   if (!host_probs || n_probs < 1 || row_stride < 0 || step_stride < 0 || !dst)
     return fail(h, WS_ERR_INVALID_ARGUMENT, "host_probs / n_probs / strides / dst");
@@ -779,6 +823,13 @@ ws_status ws_get_info(const ws_env* h, ws_info* out) {
   out->env_offset = h->offset;
   out->n_envs_global = h->E_global;
   out->t = h->t;
+  if (h->dev_clock) {  // the device clock is authoritative
+    DeviceGuard g(h->device);
+    uint64_t t = 0;
+    if (cudaMemcpyAsync(&t, h->t_dev, sizeof(t), cudaMemcpyDeviceToHost, h->stream) == cudaSuccess &&
+        cudaStreamSynchronize(h->stream) == cudaSuccess)
+      out->t = t;
+  }
   out->launches = h->launches;
   out->probs_width = h->spec.n_actions ? h->spec.n_actions : 2 * h->spec.act_dim;
   return WS_OK;

@@ -209,6 +209,11 @@ class Env:
     def synchronize(self):
         check(lib().ws_synchronize(self._h), self._h)
 
+    def enable_device_clock(self, enable: bool = True):
+        """ws.h ws_enable_device_clock: the step index lives on the device (CUDA-graph capture of
+        sample / step sequences, policy.PolicyGraph)."""
+        check(lib().ws_enable_device_clock(self._h, 1 if enable else 0), self._h)
+
     def status(self) -> int:
         """ws_synchronize without raising: returns the ws_status."""
         return lib().ws_synchronize(self._h)

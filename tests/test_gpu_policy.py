@@ -169,6 +169,44 @@ def test_torch_policy_rollout(P):
     assert 0.05 < (act == 0).float().mean().item() < 0.95
 
 
+@pytest.mark.parametrize("env,A", [("cartpole", 1), ("tag", 20)])
+def test_policy_graph_replays_equal_eager_rollouts(P, env, A):
+    """policy.PolicyGraph (SURVEY 8(f) N1 "captured in a CUDA Graph"): the T-step loop of a
+    torch policy captured once and replayed three times writes, after every replay, exactly
+    the store, live state and statistics of three eager rollout_with calls (the device clock
+    advances the ACTION draw index per step, R15); fused roll-outs are refused while the graph
+    holds the clock, and closing it hands the step index (3 T) back to the host."""
+    from paper_2408_00930_b200.policy import PolicyGraph, rollout_with
+    E, T = 96, 40
+    D, n = (4, 2) if env == "cartpole" else (4, 5)
+    g = torch.Generator(device="cpu").manual_seed(7)
+    Wt = (torch.randn(D, n, generator=g) * 2.0).cuda()
+    b = torch.randn(n, generator=g).cuda()
+    pol = lambda obs: torch.softmax((obs[..., :, None] * Wt).sum(-2) + b, dim=-1)  # noqa: E731  (no cuBLAS)
+    sa, sb = torch.cuda.Stream(), torch.cuda.Stream()
+    a = P.Env(E, A, env, SEED, t_capacity=T, stream=sa)
+    e = P.Env(E, A, env, SEED, t_capacity=T, stream=sb)
+    keys = ("obs", "act", "logp", "rew", "done", "state", "tstate", "obs_live", "reset_count", "ep_step", "stats")
+    pg = PolicyGraph(a, pol, T)
+    with pytest.raises(P.WSError):
+        a.rollout(T, torch.full((E, A, n), 1.0 / n, device="cuda"))
+    for k in range(3):
+        pg.rollout()
+        with torch.cuda.stream(sb):
+            rollout_with(e, pol, T)
+        torch.cuda.synchronize()
+        A_ = {q: v.cpu().numpy() for q, v in a.buffers().items() if v is not None}
+        B_ = {q: v.cpu().numpy() for q, v in e.buffers().items() if v is not None}
+        for q in keys:
+            if q in A_:
+                assert np.array_equal(A_[q], B_[q], equal_nan=True), (env, k, q)
+    assert a.info().t == 3 * T
+    pg.close()
+    assert a.info().t == 3 * T and e.info().t == 3 * T
+    a.rollout(T, torch.full((E, A, n), 1.0 / n, device="cuda"))  # the host owns the clock again
+    assert a.status() == 0
+
+
 @pytest.mark.parametrize("H,E,A,T", [(32, 20, 100, 60), (64, 7, 37, 80)])
 def test_tag_policy_rollout_parity(P, H, E, A, T):
     """Multi-agent policy inference inside the CTA-per-replica tag kernel (P:65 / P:71:
