@@ -786,27 +786,39 @@ __device__ __forceinline__ float quarter_dot(const float* w, int stride, const f
 // =======================================================================================
 // NEXT-N1: fused roll-out with in-kernel policy inference ("operating an agent that
 // samples actions", "roll-outs, action inference, reset and training" on one GPU store),
-// warp-specialised.  A CTA of five warps serves NG groups of 32 replicas (NG = 1 in production;
-// NG = 2 pipelines two groups and measured slower).  Warp 0 is
-// the ENV warp (lane = one replica of each group): it owns the states, publishes each group's
-// pre-step observations to shared memory, and once the group's inference round is back it
-// combines the four quarter partials (R29': b2 + ((P_0 + P_1) + (P_2 + P_3))), draws the
-// action and steps the dynamics.  Warps 1..4 are INFERENCE warps: warp 1 + q evaluates hidden
-// quarter q of the 32 replicas of the round (lane = replica; weights broadcast from shared
-// memory) and publishes its partials.  Each group's rounds are handed over by its own pair of
-// named barriers (obs ready / partials ready); with NG = 2 the groups are pipelined (while the
-// inference warps evaluate group A the env warp finishes group B).  The env warp's step uses
-// the env's fast path when every lane satisfies its invariant.  Auto-reset uses a look-ahead state init(e, rc + 1) kept in registers and refilled
-// after the next round is published (off the critical path).  The critic's values_trunc (rare)
-// and bootstrap values are evaluated in the env warp itself (R29' quarter sums in-lane).
+// warp-specialised: a CTA of six warps serves 32 replicas (lane = replica).  Warp 0 is the ENV
+// warp: it owns the states, publishes the pre-step observations to shared memory, and once
+// the inference round is back it combines the four quarter partials (R29': b2 + ((P_0 + P_1) +
+// (P_2 + P_3))), draws the action, steps the dynamics (the env's fast path when every lane
+// satisfies its invariant) and publishes the next observation.  Warps 1..4 are INFERENCE warps:
+// warp 1 + q evaluates hidden quarter q (weights broadcast from shared memory).  Warp 5 is the
+// STORE warp: the log-probability (fp64 log), the stores and the statistics of each step, from
+// a hand-off record, beside the env warp's next step.  Auto-reset uses a look-ahead state
+// init(e, rc + 1) kept in registers and refilled after the record is handed over.  The critic's
+// values_trunc (rare) and bootstrap values are evaluated in the env warp (R29' quarter sums
+// in-lane).  (Round 2 history: one lane per replica 1.67 ms; env + 4 inference warps 1.18 ms;
+// two pipelined replica groups per env warp 2.45 ms, not adopted.)
 template <int D, int N>
 struct PolicyWsSmem {
-  float obs[2][D][32];            // [group]
-  float part[2][4][N + 1][32];    // [group][quarter]
+  float obs[D][32];            // the env warp's published observations
+  float part[4][N + 1][32];    // [quarter] partial logits (+ critic) of the inference warps
+  // the step handed from the env warp to the store warp (lane-indexed, conflict-free)
+  float po[D][32];             // pre-step observation
+  float pa[32], pvv[32], prw[32], pret[32];
+  double pcN[32];
+  int pact[32], pes[32];
+  uint32_t pd[32];
 };
 
-template <class Env, int H, bool kCritic, int NG>
-__global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const int T, const uint64_t t0,
+// Warp-specialised policy roll-out, 32 replicas per CTA of six warps.  ENV warp (0): the
+// recurrence -- partial logits -> softmax -> R13 draw -> dynamics -> auto-reset -> next observation
+// published.  INFERENCE warps (1..4): warp 1+q evaluates R29''s hidden quarter q.  STORE warp (5):
+// everything that only feeds the store -- the fp64 log of the log-probability, the act / logp /
+// obs / value / rew / done stores and the statistics window -- from a per-step hand-off record in
+// shared memory, so it runs beside the env warp's next step.  Named barriers: 1 obs ready,
+// 2 partials ready (env + inference warps), 5 record written, 6 record read (env + store warp).
+template <class Env, int H, bool kCritic>
+__global__ void __launch_bounds__(192) k_rollout_policy_ws(const KArgs a, const int T, const uint64_t t0,
                                                           const float* __restrict__ weights,
                                                           float* __restrict__ values, float* __restrict__ bootstrap,
                                                           float* __restrict__ values_trunc) {
@@ -817,7 +829,7 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
   constexpr int kRows = 16;
   __shared__ __align__(16) float sw[NW];
   __shared__ __align__(16) PolicyWsSmem<D, N> x;
-  extern __shared__ __align__(16) uint32_t ws_smem[];  // the env warp's two statistics windows
+  extern __shared__ __align__(16) uint32_t ws_smem[];  // the store warp's statistics window
   for (int i = threadIdx.x; i < NW; i += blockDim.x) sw[i] = weights[i];
   __syncthreads();
   const float* W1 = sw;
@@ -827,13 +839,19 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
   const float* wv = b2 + N;  // kCritic only
   const int lane = threadIdx.x & 31, warp = threadIdx.x >> 5;
   const int64_t E = a.E;
+  const size_t sE = (size_t)E;
+  // the CTA's 32 replicas (tail lanes shadow replica E-1)
+  const int64_t e_lane = (int64_t)blockIdx.x * 32 + lane;
+  const bool live = e_lane < E;
+  const int64_t ec = live ? e_lane : E - 1;
 
-  if (warp > 0) {  // ------------------------------------------------ inference warp, quarter q
+  if (warp >= 1 && warp <= 4) {  // ------------------------------------- inference warp, quarter q
     const int q = warp - 1;
-    auto evaluate = [&](int g) {
+    for (int t = 0; t < T; ++t) {
+      asm volatile("bar.sync 1, 160;" ::: "memory");  // the observation of step t
       float o[D];
 #pragma unroll
-      for (int d = 0; d < D; ++d) o[d] = x.obs[g][d][lane];
+      for (int d = 0; d < D; ++d) o[d] = x.obs[d][lane];
       float P[N], Pv = 0.0f;
 #pragma unroll
       for (int i = 0; i < N; ++i) P[i] = 0.0f;
@@ -849,64 +867,74 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
         if (kCritic) Pv = __fmaf_rn(wv[j], hj, Pv);
       }
 #pragma unroll
-      for (int i = 0; i < N; ++i) x.part[g][q][i][lane] = P[i];
-      if (kCritic) x.part[g][q][N][lane] = Pv;
-    };
-    for (int t = 0; t < T; ++t) {
-      asm volatile("bar.sync 1, 160;" ::: "memory");  // group A's observation of step t
-      evaluate(0);
+      for (int i = 0; i < N; ++i) x.part[q][i][lane] = P[i];
+      if (kCritic) x.part[q][N][lane] = Pv;
       asm volatile("bar.arrive 2, 160;" ::: "memory");
-      if (NG == 2) {
-        asm volatile("bar.sync 3, 160;" ::: "memory");  // group B's
-        evaluate(1);
-        asm volatile("bar.arrive 4, 160;" ::: "memory");
+    }
+    return;
+  }
+
+  if (warp == 5) {  // -------------------------------------------------------------- store warp
+    StatsWindow win;
+    win.init(ws_smem, kRows);
+    const int nlive = (int)max((int64_t)0, min((int64_t)32, E - (int64_t)blockIdx.x * 32));
+    for (int c = 0; c < T; ++c) {
+      asm volatile("bar.sync 5, 64;" ::: "memory");  // the record of step c
+      float o[D];
+#pragma unroll
+      for (int d = 0; d < D; ++d) o[d] = x.po[d][lane];
+      const float pa = x.pa[lane], vv = x.pvv[lane], rw = x.prw[lane], ret = x.pret[lane];
+      const double cN = x.pcN[lane];
+      const int act = x.pact[lane], es = x.pes[lane];
+      const uint32_t d = x.pd[lane];
+      asm volatile("bar.arrive 6, 64;" ::: "memory");  // the record may be overwritten
+      const size_t idx = (size_t)c * sE + (size_t)ec;
+      if (kCritic && live) st_cs(values + idx, vv);
+      float* po = a.obs + idx * D;
+      if constexpr (D % 4 == 0) {
+#pragma unroll
+        for (int i = 0; i < D; i += 4) st_cs(reinterpret_cast<float4*>(po + i), make_float4(o[i], o[i + 1], o[i + 2], o[i + 3]));
+      } else if constexpr (D % 2 == 0) {
+#pragma unroll
+        for (int i = 0; i < D; i += 2) st_cs(reinterpret_cast<float2*>(po + i), make_float2(o[i], o[i + 1]));
+      } else {
+#pragma unroll
+        for (int i = 0; i < D; ++i) st_cs(po + i, o[i]);
       }
+      st_cs(reinterpret_cast<int32_t*>(a.act) + idx, act);
+      if (a.write_logp) {
+        // logp_of_normalised: log p_a - log(sum of the normalised row), fp64 (R13 / R18)
+        const double dd = cN - 1.0;
+        const double lC = fabs(dd) < 1e-6 ? dd * (1.0 - dd * (0.5 - dd * (1.0 / 3.0))) : log(cN);
+        st_cs(a.logp + idx, act < 0 ? __int_as_float(0x7fc00000) : (float)(log((double)pa) - lC));
+      }
+      st_cs(a.rew + idx, rw);
+      st_cs_u8(a.done + idx, (uint8_t)d);
+      win.put(c & (kRows - 1), lane, d ? (uint32_t)es : 0u, d ? ret : 0.0f, rw);
+      if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
+        win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, nlive);
     }
     return;
   }
 
   // ------------------------------------------------------------------------------ env warp
   const Key key{a.k0, a.k1};
-  const size_t sE = (size_t)E;
-  struct Grp {
-    int64_t e, ec;
-    bool live;
-    uint32_t eg;
-    St s, nxt;
-    typename L::Aux aux;
-    int32_t ep_step;
-    uint32_t rc;
-    float ep_ret;
-    U4 w4;
-    StatsWindow win;
-    int nlive;
-  } G[NG];
-#pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    Grp& r = G[g];
-    const int64_t first = (int64_t)blockIdx.x * (32 * NG) + 32 * g;
-    r.e = first + lane;
-    r.live = r.e < E;
-    r.ec = r.live ? r.e : E - 1;  // tail lanes (and a group past E) shadow replica E-1
-    r.nlive = (int)max((int64_t)0, min((int64_t)32, E - first));
-    r.eg = (uint32_t)(a.offset + r.ec);
-    L::load(a.state + r.ec * L::S, r.s);
-    r.aux = L::aux_of(r.s);
-    r.ep_step = a.ep_step[r.ec];
-    r.rc = a.reset_count[r.ec];
-    r.ep_ret = a.ep_ret[r.ec];
-    L::init(key, r.eg, r.rc + 1, r.nxt);
-    r.w4 = U4{0, 0, 0, 0};
-    r.win.init(ws_smem + g * (3 * kRows * kWinStride), kRows);
-  }
+  const uint32_t eg = (uint32_t)(a.offset + ec);
+  St s, nxt;
+  L::load(a.state + ec * L::S, s);
+  typename L::Aux aux = L::aux_of(s);
+  int32_t ep_step = a.ep_step[ec];
+  uint32_t rc = a.reset_count[ec];
+  float ep_ret = a.ep_ret[ec];
+  L::init(key, eg, rc + 1, nxt);
+  U4 w4{0, 0, 0, 0};
   uint32_t err = 0;
-  auto publish = [&](int g) {
+  auto publish = [&]() {
     float o[D];
-    L::obs_vals(G[g].s, G[g].aux, o);
+    L::obs_vals(s, aux, o);
 #pragma unroll
-    for (int d = 0; d < D; ++d) x.obs[g][d][lane] = o[d];
-    if (g == 0) asm volatile("bar.arrive 1, 160;" ::: "memory");
-    else asm volatile("bar.arrive 3, 160;" ::: "memory");
+    for (int d = 0; d < D; ++d) x.obs[d][lane] = o[d];
+    asm volatile("bar.arrive 1, 160;" ::: "memory");
   };
   // in-lane R29' evaluation (values_trunc / bootstrap)
   auto value_of = [&](const St& st, const typename L::Aux& ax) {
@@ -927,36 +955,17 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
     }
     return fadd(wv[H], fadd(fadd(P[0], P[1]), fadd(P[2], P[3])));
   };
-  // Step c of group g in two parts.  finish_a is the recurrence: partials -> logits -> draw ->
-  // dynamics -> auto-reset (returns whether any lane reset; its look-ahead state is refilled
-  // after the next publish).  finish_b is everything that only feeds the store -- the fp64 log
-  // of the log-probability, the act / logp / obs / value / rew / done stores and the statistics
-  // window -- and runs after the next observation is published, i.e. while the inference warps
-  // evaluate step c + 1 (the same values; only the program order changes).
-  struct Pend {
-    St s_pre;
-    typename L::Aux aux_pre;
-    float pa, vv, rw, ret;
-    double cN;
-    int act;
-    int32_t es;
-    uint32_t d;
-  };
-  auto finish_a = [&](int g, int c, Pend& p) -> bool {
-    Grp& r = G[g];
+  publish();
+  for (int c = 0; c < T; ++c) {
+    asm volatile("bar.sync 2, 160;" ::: "memory");  // the partials of step c
     const uint64_t t = t0 + (uint64_t)c;
-    if (c == 0 || (t & 3) == 0) r.w4 = block(key, t >> 2, r.eg, 0, kAction);
-    float lg[N];
+    if (c == 0 || (t & 3) == 0) w4 = block(key, t >> 2, eg, 0, kAction);
+    float lg[N], vv = 0.0f;
 #pragma unroll
-    for (int i = 0; i < N; ++i) {
-      const float* pp = &x.part[g][0][i][lane];
-      lg[i] = fadd(b2[i], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
-    }
-    p.vv = 0.0f;
-    if (kCritic) {
-      const float* pp = &x.part[g][0][N][lane];
-      p.vv = fadd(wv[H], fadd(fadd(pp[0], pp[(N + 1) * 32]), fadd(pp[2 * (N + 1) * 32], pp[3 * (N + 1) * 32])));
-    }
+    for (int i = 0; i < N; ++i)
+      lg[i] = fadd(b2[i], fadd(fadd(x.part[0][i][lane], x.part[1][i][lane]), fadd(x.part[2][i][lane], x.part[3][i][lane])));
+    if (kCritic)
+      vv = fadd(wv[H], fadd(fadd(x.part[0][N][lane], x.part[1][N][lane]), fadd(x.part[2][N][lane], x.part[3][N][lane])));
     float m = lg[0];
 #pragma unroll
     for (int i = 1; i < N; ++i) m = lg[i] > m ? lg[i] : m;
@@ -988,108 +997,77 @@ __global__ void __launch_bounds__(160) k_rollout_policy_ws(const KArgs a, const 
     }
     cdf.bad = badp || !(run > 0.0) || !isfinite(run);
     // ---- A2 draw (R13) from the ACTION stream
-    int act = search<N>(cdf, u01(pick(r.w4, (uint32_t)(t & 3))));
-    p.pa = cdf.P[0];
+    int act = search<N>(cdf, u01(pick(w4, (uint32_t)(t & 3))));
+    float pa = cdf.P[0];
 #pragma unroll
     for (int i = 1; i < N; ++i)
-      if (act == i) p.pa = cdf.P[i];
-    p.cN = cdf.C[N - 1];
+      if (act == i) pa = cdf.P[i];
     if (cdf.bad) {
       act = -1;
-      if (r.live) err |= kErrProbs | kErrAction;
+      if (live) err |= kErrProbs | kErrAction;
     }
-    p.act = act;
-    p.s_pre = r.s;
-    p.aux_pre = r.aux;
+    float opre[D];
+    L::obs_vals(s, aux, opre);
     // ---- A3-A5
     const bool bad = act < 0;
-    St s2 = r.s;
-    typename L::Aux aux2 = r.aux;
+    St s2 = s;
+    typename L::Aux aux2 = aux;
     float rr;
     bool term;
     // the env's fast step when every lane satisfies its invariant (CartPole: guard-free
     // divisions and the Taylor sincos, bit-identical; section 5), else the generic step
-    if (L::kMinEpisode >= 8 && __all_sync(kFull, L::fast_ok(r.s)))
+    if (L::kMinEpisode >= 8 && __all_sync(kFull, L::fast_ok(s)))
       L::template step_aux<true>(s2, aux2, bad ? 0 : act, rr, term);
     else
       L::template step_aux<false>(s2, aux2, bad ? 0 : act, rr, term);
-    const int32_t es = r.ep_step + 1;
+    const int32_t es = ep_step + 1;
     const uint32_t d = bad ? 0u : ((term ? 1u : 0u) | (es >= a.max_steps ? 2u : 0u));
-    p.rw = bad ? 0.0f : rr;
-    p.ret = r.ep_ret + rr;
-    p.es = es;
-    p.d = d;
+    const float rw = bad ? 0.0f : rr;
+    const float ret = ep_ret + rr;
     if (!bad) {
-      r.s = s2;
-      r.aux = aux2;
-      r.ep_step = es;
-      r.ep_ret = p.ret;
+      s = s2;
+      aux = aux2;
+      ep_step = es;
+      ep_ret = ret;
     }
     if (kCritic && values_trunc && __any_sync(kFull, d == 2u)) {  // truncated only: V of the post-step state
-      const float v2 = value_of(r.s, r.aux);
-      if (r.live && d == 2u) st_cs(values_trunc + (size_t)c * sE + (size_t)r.ec, v2);
+      const float v2 = value_of(s, aux);
+      if (live && d == 2u) st_cs(values_trunc + (size_t)c * sE + (size_t)ec, v2);
     }
     if (d) {  // auto-reset (R11) from the look-ahead state init(e, rc + 1)
-      r.rc += 1;
-      r.s = r.nxt;
-      r.aux = L::aux_of(r.s);
-      r.ep_step = 0;
-      r.ep_ret = 0.0f;
+      rc += 1;
+      s = nxt;
+      aux = L::aux_of(s);
+      ep_step = 0;
+      ep_ret = 0.0f;
     }
-    return __any_sync(kFull, d != 0);
-  };
-  auto finish_b = [&](int g, int c, const Pend& p) {
-    Grp& r = G[g];
-    const size_t idx = (size_t)c * sE + (size_t)r.ec;
-    if (kCritic && r.live) st_cs(values + idx, p.vv);
-    L::obs_store_aux(a.obs + idx * L::D, p.s_pre, p.aux_pre, true);
-    st_cs(reinterpret_cast<int32_t*>(a.act) + idx, p.act);
-    if (a.write_logp) {
-      // logp_of_normalised: log p_a - log(sum of the normalised row), fp64 (R13 / R18)
-      const double dd = p.cN - 1.0;
-      const double lC = fabs(dd) < 1e-6 ? dd * (1.0 - dd * (0.5 - dd * (1.0 / 3.0))) : log(p.cN);
-      const float lp = p.act < 0 ? __int_as_float(0x7fc00000) : (float)(log((double)p.pa) - lC);
-      st_cs(a.logp + idx, lp);
-    }
-    st_cs(a.rew + idx, p.rw);
-    st_cs_u8(a.done + idx, (uint8_t)p.d);
-    r.win.put(c & (kRows - 1), lane, p.d ? (uint32_t)p.es : 0u, p.d ? p.ret : 0.0f, p.rw);
-    if ((c & (kRows - 1)) == kRows - 1 || c == T - 1)
-      r.win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, r.nlive);
-  };
-  auto refill = [&](int g, bool any) {
-    if (any) L::init(key, G[g].eg, G[g].rc + 1, G[g].nxt);  // (lanes without a reset recompute the same state)
-  };
-  publish(0);
-  for (int c = 0; c < T; ++c) {
-    Pend pa, pb;
-    if constexpr (NG == 2) publish(NG - 1);
-    asm volatile("bar.sync 2, 160;" ::: "memory");  // group A's partials of step c
-    const bool ra = finish_a(0, c, pa);
-    if (c + 1 < T) publish(0);
-    finish_b(0, c, pa);
-    refill(0, ra);
-    if constexpr (NG == 2) {
-      asm volatile("bar.sync 4, 160;" ::: "memory");  // group B's partials of step c
-      const bool rb = finish_a(NG - 1, c, pb);
-      finish_b(NG - 1, c, pb);
-      refill(NG - 1, rb);
-    }
-  }
+    if (c + 1 < T) publish();  // the inference warps start step c + 1
+    // hand the store-only work of step c to the store warp
+    if (c > 0) asm volatile("bar.sync 6, 64;" ::: "memory");  // it has read step c - 1's record
 #pragma unroll
-  for (int g = 0; g < NG; ++g) {
-    Grp& r = G[g];
-    if constexpr (kCritic) {  // bootstrap value of the observation after the last step
-      const float v = value_of(r.s, r.aux);
-      if (r.live) bootstrap[r.e] = v;
-    }
-    if (r.live) {
-      L::save(a.state + r.e * L::S, r.s);
-      a.ep_step[r.e] = r.ep_step;
-      a.reset_count[r.e] = r.rc;
-      a.ep_ret[r.e] = r.ep_ret;
-      L::obs_store(a.obs_live + r.e * L::D, r.s, false);
-    }
+    for (int i = 0; i < D; ++i) x.po[i][lane] = opre[i];
+    x.pa[lane] = pa;
+    x.pvv[lane] = vv;
+    x.prw[lane] = rw;
+    x.pret[lane] = ret;
+    x.pcN[lane] = cdf.C[N - 1];
+    x.pact[lane] = act;
+    x.pes[lane] = es;
+    x.pd[lane] = d;
+    asm volatile("bar.arrive 5, 64;" ::: "memory");
+    if (__any_sync(kFull, d != 0)) L::init(key, eg, rc + 1, nxt);  // (lanes without a reset recompute the same state)
+  }
+  asm volatile("bar.sync 6, 64;" ::: "memory");  // the store warp has read the last record
+  if constexpr (kCritic) {  // bootstrap value of the observation after the last step
+    const float v = value_of(s, aux);
+    if (live) bootstrap[e_lane] = v;
+  }
+  if (live) {
+    L::save(a.state + e_lane * L::S, s);
+    a.ep_step[e_lane] = ep_step;
+    a.reset_count[e_lane] = rc;
+    a.ep_ret[e_lane] = ep_ret;
+    L::obs_store(a.obs_live + e_lane * L::D, s, false);
   }
   if (err) atomicOr(a.err, err);
 }
@@ -2644,22 +2622,21 @@ cudaError_t launch_rollout(const KArgs& a, const Launch& l, int T, uint64_t t0, 
 template <class Env>
 static cudaError_t rollout_policy(const KArgs& a, const Launch& l, int T, uint64_t t0, const float* weights,
                                   int hidden, float* values, float* bootstrap, float* vtr) {
-  // warp-specialised: one env warp + four inference warps per 32 replicas; the env warp's
-  // 16-row statistics window is the dynamic shared memory
-  constexpr int NG = 1;  // replica groups per CTA (2: pipelined groups -- measured slower)
-  const size_t smem = (size_t)NG * 3 * 16 * kWinStride * sizeof(uint32_t);
-  const unsigned g = grid_for(a.E, 32 * NG);
+  // warp-specialised: one env warp + four inference warps + one store warp per 32 replicas; the
+  // store warp's 16-row statistics window is the dynamic shared memory
+  const size_t smem = (size_t)3 * 16 * kWinStride * sizeof(uint32_t);
+  const unsigned g = grid_for(a.E, 32);
   l.m(kKRollout, 0);
   if (values) {
     switch (hidden) {
-      case 32: k_rollout_policy_ws<Env, 32, true, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
-      case 64: k_rollout_policy_ws<Env, 64, true, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 32: k_rollout_policy_ws<Env, 32, true><<<g, 192, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
+      case 64: k_rollout_policy_ws<Env, 64, true><<<g, 192, smem, l.stream>>>(a, T, t0, weights, values, bootstrap, vtr); break;
       default: return cudaErrorInvalidValue;
     }
   } else {
     switch (hidden) {
-      case 32: k_rollout_policy_ws<Env, 32, false, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
-      case 64: k_rollout_policy_ws<Env, 64, false, NG><<<g, 160, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 32: k_rollout_policy_ws<Env, 32, false><<<g, 192, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
+      case 64: k_rollout_policy_ws<Env, 64, false><<<g, 192, smem, l.stream>>>(a, T, t0, weights, nullptr, nullptr, nullptr); break;
       default: return cudaErrorInvalidValue;
     }
   }
