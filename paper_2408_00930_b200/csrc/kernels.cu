@@ -988,9 +988,22 @@ __global__ void __launch_bounds__(192) k_rollout_policy_ws(const KArgs a, const 
     }
     double run = 0.0;
     bool badp = false;
+    if constexpr (N == 2) {
+      // p_i = e_i / S without the FCHK guard: one e_i is 1 and the other eo in [0, 1], so S lies
+      // in [1, 2] (or is NaN, a bad row either way) and div_normal equals IEEE division for the
+      // numerators 1 and eo >= 2^-100; below that, S = fl(1 + eo) = 1 and eo / S = eo exactly
+      const bool k0 = !(lg[1] > lg[0]);
+      const float eo = k0 ? cdf.P[1] : cdf.P[0], em = k0 ? cdf.P[0] : cdf.P[1];
+      const float qm = isfinite(em) ? div_normal(1.0f, S) : fdiv(em, S);
+      const float qo = eo < 0x1.0p-100f ? eo : div_normal(eo, S);
+      cdf.P[0] = k0 ? qm : qo;
+      cdf.P[1] = k0 ? qo : qm;
+    } else {
+#pragma unroll
+      for (int i = 0; i < N; ++i) cdf.P[i] = fdiv(cdf.P[i], S);
+    }
 #pragma unroll
     for (int i = 0; i < N; ++i) {
-      cdf.P[i] = fdiv(cdf.P[i], S);
       run += (double)cdf.P[i];
       cdf.C[i] = run;
       badp = badp || !(cdf.P[i] >= 0.0f) || !isfinite(cdf.P[i]);

@@ -1,0 +1,5 @@
+mkdir -p gpurun_out/r02ae
+timeout 900 python -m pytest tests/test_gpu_kernels.py tests/test_gpu_policy.py tests/test_gpu_a2c.py -x -q > gpurun_out/r02ae/pytest.log 2>&1; echo "pytest exit $?" >> gpurun_out/r02ae/pytest.log
+for w in C2P C2T; do
+  timeout 300 python bench.py --workload $w --no-cpu-baseline --sustain-s 0.3 > gpurun_out/r02ae/bench_$w.log 2>&1
+done
