@@ -41,7 +41,25 @@ c = P.Env(50, 1, "cartpole", W.SEED, t_capacity=T)
 c.rollout(T, torch.from_numpy(W.uniform_probs(50, 1, 2)).cuda())
 tr = a2c.A2C(P.Env(64, 1, "cartpole", W.SEED, t_capacity=T), H, lr=1e-3)
 tr.iteration(T)
+# round 2, last session: the policy kernel's store warp (named barriers 5 / 6) is exercised above;
+# the surface kernel's fast 4-step trips with goal terminations (per-step steering heads), the
+# Gaussian plan (one Philox block per lane, lane = step log-densities), and a CUDA-graph-captured
+# torch-policy roll-out on the device clock (sample / step kernels reading / advancing t_dev)
+D = 20
+g0 = P.Env(40, 1, "surface", W.SEED, t_capacity=T, param0=D, max_steps=30)
+hd = np.zeros((T, 40, 1, 2 * D), np.float32)
+hd[..., D:] = np.log(1e-6)
+hd[:, :, 0, 0], hd[:, :, 0, 1] = -0.05 * 1.181 / 1.414, 0.05
+g0.rollout(T, torch.from_numpy(hd).cuda(), row_stride=2 * D, step_stride=40 * 2 * D)
+from paper_2408_00930_b200.policy import PolicyGraph  # noqa: E402
+st = torch.cuda.Stream()
+pg_env = P.Env(33, 1, "cartpole", W.SEED, t_capacity=T, stream=st)
+Wt = torch.randn(4, 2, device="cuda")
+pg = PolicyGraph(pg_env, lambda o: torch.softmax((o[..., :, None] * Wt).sum(-2), -1), T)
+pg.rollout()
+pg.rollout()
+pg.close()
 torch.cuda.synchronize()
-for x in (e, ac, u, s, c):
+for x in (e, ac, u, s, c, g0, pg_env):
     assert x.status() == 0, x.status()
 print("racecheck_r02: done")
