@@ -1646,18 +1646,17 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
   // monotone rounding it is >= any lane's partial sum; one lane partial >= r_goal^2 rules the
   // goal out (R23's d2 < r_goal^2).  Otherwise (and for the rare trips with a done flag or an
   // invalid action) the trip returns false before changing anything and one() runs four times.
-  auto fast4 = [&](const int c, const float (&A0)[C], const float (&A1)[C], const float (&A2)[C],
-                   const float (&A3)[C]) -> bool {
-    const float* act[4] = {A0, A1, A2, A3};
-    bool bad = ep_step + 4 >= a.max_steps;  // a truncation inside the trip
+  auto fastK = [&](auto Kc, const int c, const auto& act) -> bool {  // act: float[K][C]
+    constexpr int K = decltype(Kc)::value;
+    bool bad = ep_step + K >= a.max_steps;  // a truncation inside the trip
 #pragma unroll
-    for (int k = 0; k < 4; ++k)
+    for (int k = 0; k < K; ++k)
 #pragma unroll
       for (int i = 0; i < C; ++i) bad = bad || (w.valid(i) && !isfinite(act[k][i]));
-    float qs[4][C];
+    float qs[K][C];
     bool near = false;
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < K; ++k) {
       float p = 0.0f;
 #pragma unroll
       for (int i = 0; i < C; ++i) {
@@ -1677,11 +1676,11 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       near = near || ((far >> (seg * L)) & ((1u << L) - 1u)) == 0u;
     }
     if (__any_sync(kFull, w.used && (bad || near))) return false;
-    float En[4];
+    float En[K];
 #pragma unroll
-    for (int k = 0; k < 4; ++k) En[k] = w.energy(qs[k]);
+    for (int k = 0; k < K; ++k) En[k] = w.energy(qs[k]);
 #pragma unroll
-    for (int k = 0; k < 4; ++k) {
+    for (int k = 0; k < K; ++k) {
       const int ck = c + k;
       const float Epre = k == 0 ? Ecur : En[k - 1];
       if (w.used) {
@@ -1703,9 +1702,9 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       }
     }
 #pragma unroll
-    for (int i = 0; i < C; ++i) q[i] = qs[3][i];
-    Ecur = En[3];
-    const int cl = c + 3;
+    for (int i = 0; i < C; ++i) q[i] = qs[K - 1][i];
+    Ecur = En[K - 1];
+    const int cl = c + K - 1;  // K <= kRows: at most one window ends inside the trip, at its last step
     if ((cl & (kRows - 1)) == kRows - 1 || cl == T - 1) {
       const int wdx = cl / kRows;
       win.cta_acc = cta.acc(wdx);
@@ -1714,49 +1713,89 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
     }
     return true;
   };
-  auto trip = [&](const int c, const float (&A0)[C], const float (&A1)[C], const float (&A2)[C],
-                  const float (&A3)[C]) {
-    if (!fast4(c, A0, A1, A2, A3)) {
-      one(c, A0);
-      one(c + 1, A1);
-      one(c + 2, A2);
-      one(c + 3, A3);
+  if constexpr (D % 4 == 0) {
+    // 8-step trips (eight energies in flight).  The actions stream through a per-warp cp.async
+    // ring in shared memory ([2 trips][8 steps][32 lanes] float4 after the statistics windows):
+    // trip j + 2's group is issued once trip j's actions are in registers, so a trip's loads
+    // have a whole trip to land and take no registers while in flight.
+    float4* const ring = reinterpret_cast<float4*>(ws_smem + 2 * 256 + (blockDim.x >> 5) * (3 * kRows * kWinStride)) +
+                         wib * (2 * 8 * 32);
+    auto issue = [&](int j) {  // steps 8j .. 8j+7 into buffer j & 1 (an empty group past the end)
+      float4* dst = ring + (j & 1) * 256 + lane;
+#pragma unroll
+      for (int k = 0; k < 8; ++k) {
+        const int ck = 8 * j + k;
+        if (ck < T) {
+          const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + k * 32);
+          asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(p_act + (size_t)ck * sE * D) : "memory");
+        }
+      }
+      asm volatile("cp.async.commit_group;" ::: "memory");
+    };
+    const int ntrip = (T + 7) / 8;
+    issue(0);
+    issue(1);
+    for (int j = 0; j < ntrip; ++j) {
+      asm volatile("cp.async.wait_group 1;" ::: "memory");  // trip j's group has landed (each lane reads its own)
+      const int c = 8 * j, n = min(8, T - c);
+      const float4* src = ring + (j & 1) * 256 + lane;
+      bool done_fast = false;
+      if (n == 8) {
+        float A[8][C];
+#pragma unroll
+        for (int k = 0; k < 8; ++k) {
+          const float4 t = src[k * 32];
+          A[k][0] = t.x; A[k][1] = t.y; A[k][2] = t.z; A[k][3] = t.w;
+        }
+        done_fast = fastK(std::integral_constant<int, 8>{}, c, A);
+      }
+      if (!done_fast) {
+#pragma unroll 1
+        for (int k = 0; k < n; ++k) {
+          const float4 t = src[k * 32];
+          const float v[C] = {t.x, t.y, t.z, t.w};
+          one(c + k, v);
+        }
+      }
+      issue(j + 2);  // into buffer j & 1, whose values have been consumed
     }
-  };
-  // two action register sets used in turn (no copies: a copy placed by the compiler right after
-  // the loads stalls on them): the next trip's actions load while this trip runs
-  float a0[C] = {}, a1[C] = {}, a2[C] = {}, a3[C] = {};
-  float b0[C] = {}, b1[C] = {}, b2[C] = {}, b3[C] = {};
-  load_act(0, a0);
-  load_act(1, a1);
-  load_act(2, a2);
-  load_act(3, a3);
-  int c = 0;
-  for (; c + 8 <= T; c += 8) {
-    load_act(c + 4, b0);
-    load_act(c + 5, b1);
-    load_act(c + 6, b2);
-    load_act(c + 7, b3);
-    trip(c, a0, a1, a2, a3);
-    load_act(c + 8, a0);
-    load_act(c + 9, a1);
-    load_act(c + 10, a2);
-    load_act(c + 11, a3);
-    trip(c + 4, b0, b1, b2, b3);
-  }
-  if (c + 4 <= T) {  // one more full trip on set a; the tail's actions go to set b
-    load_act(c + 4, b0);
-    load_act(c + 5, b1);
-    load_act(c + 6, b2);
-    trip(c, a0, a1, a2, a3);
-    c += 4;
-    if (c < T) one(c, b0);
-    if (c + 1 < T) one(c + 1, b1);
-    if (c + 2 < T) one(c + 2, b2);
+    asm volatile("cp.async.wait_group 0;" ::: "memory");
   } else {
-    if (c < T) one(c, a0);
-    if (c + 1 < T) one(c + 1, a1);
-    if (c + 2 < T) one(c + 2, a2);
+    auto trip = [&](const int c, const float (&A)[4][C]) {
+      if (!fastK(std::integral_constant<int, 4>{}, c, A)) {
+        one(c, A[0]);
+        one(c + 1, A[1]);
+        one(c + 2, A[2]);
+        one(c + 3, A[3]);
+      }
+    };
+    // two action register sets used in turn (no copies: a copy placed by the compiler right after
+    // the loads stalls on them): the next trip's actions load while this trip runs
+    float a4[4][C] = {}, b4[4][C] = {};
+#pragma unroll
+    for (int k = 0; k < 4; ++k) load_act(k, a4[k]);
+    int c = 0;
+    for (; c + 8 <= T; c += 8) {
+#pragma unroll
+      for (int k = 0; k < 4; ++k) load_act(c + 4 + k, b4[k]);
+      trip(c, a4);
+#pragma unroll
+      for (int k = 0; k < 4; ++k) load_act(c + 8 + k, a4[k]);
+      trip(c + 4, b4);
+    }
+    if (c + 4 <= T) {  // one more full trip on set a; the tail's actions go to set b
+#pragma unroll
+      for (int k = 0; k < 3; ++k) load_act(c + 4 + k, b4[k]);
+      trip(c, a4);
+      c += 4;
+      if (c < T) one(c, b4[0]);
+      if (c + 1 < T) one(c + 1, b4[1]);
+      if (c + 2 < T) one(c + 2, b4[2]);
+    } else {
+      if (c < T) one(c, a4[0]);
+      if (c + 1 < T) one(c + 1, a4[1]);
+      if (c + 2 < T) one(c + 2, a4[2]);
+    }
   }
   if (live) {
 #pragma unroll
@@ -2590,7 +2629,14 @@ static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint6
   l.m(kKRollout, 0);
   {  // segments of ceil(D/4) lanes, 32 / ceil(D/4) replicas per warp
     // CTA statistics accumulator + one 16-slot statistics window per warp (energies via shuffles)
-    const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * 3 * 16 * kWinStride * sizeof(uint32_t);
+    // (+ D % 4 == 0: the per-warp cp.async action ring, 2 x 8 x 32 float4)
+    const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * 3 * 16 * kWinStride * sizeof(uint32_t) +
+                        (D % 4 == 0 ? (size_t)wpb * 2 * 8 * 32 * sizeof(float4) : 0);
+    if (smem > 48 * 1024) {
+      const cudaError_t e = cudaFuncSetAttribute(k_rollout_surface_seg<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
+                                                 (int)smem);
+      if (e != cudaSuccess) return e;
+    }
     k_rollout_surface_seg<D><<<grid_for(a.E, (int64_t)wpb * SurfSeg<D>::R), l.block, smem, l.stream>>>(a, T);
   }
   l.m(kKRollout, 1);

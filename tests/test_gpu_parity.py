@@ -266,7 +266,7 @@ def test_env_parity(P, env, E, A, T, params):
     compare(buf, o, amb, env, T)
 
 
-@pytest.mark.parametrize("D", [20, 8, 3])
+@pytest.mark.parametrize("D", [20, 16, 8, 3])
 def test_surface_goal_reached(P, D):
     """Per-step Gaussian heads that steer replicas into the goal ball: step 0 cancels each
     replica's reset offsets in q_2.. (read from the oracle's initial state), then q0 / q1 drift
@@ -275,7 +275,7 @@ def test_surface_goal_reached(P, D):
     one replica's head is non-finite.  The segmented kernel's fast 4-step trips must hand every
     trip that may touch the goal ball (or a truncation / invalid action) to the exact per-step
     path -- element for element as the oracle."""
-    E, T, ms = 300, {20: 203, 8: 197, 3: 200}[D], 150  # T % 8 = 3, 5, 0: every tail path of the trip loop
+    E, T, ms = 300, {20: 203, 8: 197, 3: 200, 16: 196}[D], 150  # T % 8 = 3, 5, 0, 4: every tail path of the trip loops
     o = O.Batch("surface", E, 1, SEED, t_capacity=T, p0=D, max_steps=ms)
     q0 = np.array(o.array("state")).reshape(E, D)
     probs = np.zeros((T, E, 1, 2 * D), np.float32)
