@@ -285,6 +285,9 @@ constexpr int kWinWords = 3 * 32 * kWinStride;  // per warp (13.5 KiB)
 #define WS_CONT_WIN_ROWS 16
 #endif
 constexpr int kContWinRows = WS_CONT_WIN_ROWS;  // window depth of k_rollout_continuous
+#ifndef WS_SURF_TRIP
+#define WS_SURF_TRIP 8  // surface-D fast-trip length (D % 4 == 0); <= the 16-row statistics window
+#endif
 
 struct StatsWindow {
   uint32_t* len;
@@ -1718,13 +1721,14 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
     // ring in shared memory ([2 trips][8 steps][32 lanes] float4 after the statistics windows):
     // trip j + 2's group is issued once trip j's actions are in registers, so a trip's loads
     // have a whole trip to land and take no registers while in flight.
+    constexpr int KT = WS_SURF_TRIP;  // steps per trip
     float4* const ring = reinterpret_cast<float4*>(ws_smem + 2 * 256 + (blockDim.x >> 5) * (3 * kRows * kWinStride)) +
-                         wib * (2 * 8 * 32);
-    auto issue = [&](int j) {  // steps 8j .. 8j+7 into buffer j & 1 (an empty group past the end)
-      float4* dst = ring + (j & 1) * 256 + lane;
+                         wib * (2 * KT * 32);
+    auto issue = [&](int j) {  // steps KT j .. KT j + KT - 1 into buffer j & 1 (an empty group past the end)
+      float4* dst = ring + (j & 1) * (KT * 32) + lane;
 #pragma unroll
-      for (int k = 0; k < 8; ++k) {
-        const int ck = 8 * j + k;
+      for (int k = 0; k < KT; ++k) {
+        const int ck = KT * j + k;
         if (ck < T) {
           const uint32_t sa = (uint32_t)__cvta_generic_to_shared(dst + k * 32);
           asm volatile("cp.async.cg.shared.global [%0], [%1], 16;" ::"r"(sa), "l"(p_act + (size_t)ck * sE * D) : "memory");
@@ -1732,22 +1736,22 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       }
       asm volatile("cp.async.commit_group;" ::: "memory");
     };
-    const int ntrip = (T + 7) / 8;
+    const int ntrip = (T + KT - 1) / KT;
     issue(0);
     issue(1);
     for (int j = 0; j < ntrip; ++j) {
       asm volatile("cp.async.wait_group 1;" ::: "memory");  // trip j's group has landed (each lane reads its own)
-      const int c = 8 * j, n = min(8, T - c);
-      const float4* src = ring + (j & 1) * 256 + lane;
+      const int c = KT * j, n = min(KT, T - c);
+      const float4* src = ring + (j & 1) * (KT * 32) + lane;
       bool done_fast = false;
-      if (n == 8) {
-        float A[8][C];
+      if (n == KT) {
+        float A[KT][C];
 #pragma unroll
-        for (int k = 0; k < 8; ++k) {
+        for (int k = 0; k < KT; ++k) {
           const float4 t = src[k * 32];
           A[k][0] = t.x; A[k][1] = t.y; A[k][2] = t.z; A[k][3] = t.w;
         }
-        done_fast = fastK(std::integral_constant<int, 8>{}, c, A);
+        done_fast = fastK(std::integral_constant<int, KT>{}, c, A);
       }
       if (!done_fast) {
 #pragma unroll 1
@@ -2631,7 +2635,7 @@ static cudaError_t rollout_surface(const KArgs& a, const Launch& l, int T, uint6
     // CTA statistics accumulator + one 16-slot statistics window per warp (energies via shuffles)
     // (+ D % 4 == 0: the per-warp cp.async action ring, 2 x 8 x 32 float4)
     const size_t smem = 256 * sizeof(unsigned long long) + (size_t)wpb * 3 * 16 * kWinStride * sizeof(uint32_t) +
-                        (D % 4 == 0 ? (size_t)wpb * 2 * 8 * 32 * sizeof(float4) : 0);
+                        (D % 4 == 0 ? (size_t)wpb * 2 * WS_SURF_TRIP * 32 * sizeof(float4) : 0);
     if (smem > 48 * 1024) {
       const cudaError_t e = cudaFuncSetAttribute(k_rollout_surface_seg<D>, cudaFuncAttributeMaxDynamicSharedMemorySize,
                                                  (int)smem);
