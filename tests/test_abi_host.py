@@ -79,6 +79,8 @@ def test_null_handle_and_status_strings():
     assert L.ws_peer_export(None, 2, None) == _abi.INVALID_ARGUMENT
     assert L.ws_peer_attach(None, 0, 2, None) == _abi.INVALID_ARGUMENT
     assert L.ws_peer_detach(None) == _abi.INVALID_ARGUMENT
+    assert L.ws_enable_device_clock(None, 1) == _abi.INVALID_ARGUMENT
+    assert L.ws_enable_kernel_timing(None, 2 | (4 << 8)) == _abi.INVALID_ARGUMENT
 
 
 @pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-GPU failure mode")
