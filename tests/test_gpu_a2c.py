@@ -287,6 +287,53 @@ def test_acrobot_solved_by_training_loop(P):
     assert ret >= -100.0 and curve[0][2] < -400.0
 
 
+def test_ppo_grad_at_the_clip_edges(P):
+    """R33's clip boundary, the rows test_ppo_grad_matches_oracle moves away: six rows whose
+    behaviour log-prob puts rho exactly on an edge in fp64 (three at 1 - eps, three at 1 + eps,
+    advantages of both signs).  fp32 (GPU) and fp64 (oracle) may decide such a row either way, so
+    the GPU gradient must equal the oracle gradient for SOME choice of the six rows' branches
+    (2^6 candidates, each row's two contributions differ by far more than the tolerance), and
+    the rows away from the edges must follow the oracle's choice exactly."""
+    import itertools
+    D, H, N, rows = 4, 64, 2, 600
+    params = W.a2c_params(D, H, N, seed=111)
+    obs, act, adv, ret = W.a2c_batch(rows, D, N, seed=112)
+    act = np.clip(act, 0, N - 1).astype(np.int32)
+    p_new = OA.forward(params, obs, D, H, N)[3][np.arange(rows), act]
+    pert = params + np.random.default_rng(113).standard_normal(params.size).astype(np.float32) * 0.3
+    p_old = OA.forward(pert, obs, D, H, N)[3][np.arange(rows), act]
+    rho = p_new / p_old
+    for edge in (0.8, 1.2):  # the bulk stays clear of the edges
+        near = np.abs(rho - edge) < 1e-3
+        p_old[near] = p_new[near] / (edge + 2e-3)
+    logp_old = np.log(p_old).astype(np.float32)
+    edge_rows = np.array([5, 50, 100, 150, 200, 250])
+    for k, r in enumerate(edge_rows):
+        e = 0.8 if k < 3 else 1.2
+        logp_old[r] = np.float32(np.log(p_new[r]) - np.log(e))
+        adv[r] = np.float32((1.0 if k % 2 == 0 else -1.0) * (1.0 + 0.5 * k))
+    ws = P.workspace(D, H, N, "cuda")
+    tadv = cuda(adv)
+    mom = P.moments(tadv, ws)
+    g, _ = P.a2c_grad(cuda(params), cuda(obs).view(-1), cuda(act), tadv, cuda(ret), mom, float(rows), D, H, N,
+                      0.5, 0.01, ws, logp_old=cuda(logp_old), clip_eps=0.2)
+    g = g.cpu().numpy().astype(np.float64)
+    Ah = OA.normalize(adv)
+    logp64 = np.log(p_new)
+    rho64 = np.exp(logp64 - logp_old.astype(np.float64))
+    assert np.all(np.abs(rho64[edge_rows] - np.repeat([0.8, 1.2], 3)) < 1e-6)
+    active = rho64 * Ah <= np.clip(rho64, 0.8, 1.2) * Ah
+    scale = grad_scale(params, obs, act, Ah * np.maximum(rho64, 1.0), ret, D, H, N, 0.5, 0.01, rows)
+    hits = 0
+    for choice in itertools.product([False, True], repeat=len(edge_rows)):
+        act_mask = active.copy()
+        act_mask[edge_rows] = choice
+        ref = OA.grad(params, obs, act, np.where(act_mask, rho64 * Ah, 0.0), ret, D, H, N, 0.5, 0.01)
+        if np.all(np.abs(g - ref) <= 2e-5 * scale + 1e-12):
+            hits += 1
+    assert hits == 1, hits  # exactly one branch assignment of the edge rows reproduces the GPU
+
+
 @pytest.mark.parametrize("D,H,N,rows", [(4, 64, 2, 3000), (6, 32, 3, 1000)])
 def test_ppo_grad_matches_oracle(P, D, H, N, rows):
     """ws_a2c_grad with behaviour log-probs (PPO, R33) against oracle/a2c.py ppo_grad; the
