@@ -415,18 +415,48 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
         hv[0] = hs[r * S::kHrow + lane];
       }
       const float dv = ogv[D + N];
+      if constexpr (KP == 2) {
+        // the lane's two units in packed fp32 pairs (FMUL2 / FFMA2 / FADD2: each element rounded
+        // exactly like the scalar FMUL / FFMA / FADD, half the instructions)
+        const float2 dvv = make_float2(dv, dv);
+        float2 dh = __fmul2_rn(make_float2(wvk[0], wvk[1]), dvv);
 #pragma unroll
-      for (int q = 0; q < KP; ++q) {
-        float dh = wvk[q] * dv;
+        for (int j = 0; j < N; ++j)
+          dh = __ffma2_rn(make_float2(w2k[0][j], w2k[1][j]), make_float2(ogv[D + j], ogv[D + j]), dh);
+        const float2 dz = make_float2(hv[0] > 0.0f ? dh.x : 0.0f, hv[1] > 0.0f ? dh.y : 0.0f);
 #pragma unroll
-        for (int j = 0; j < N; ++j) dh = fmaf(w2k[q][j], ogv[D + j], dh);
-        const float dz = hv[q] > 0.0f ? dh : 0.0f;
+        for (int d = 0; d < D; ++d) {
+          const float2 t = __ffma2_rn(make_float2(ogv[d], ogv[d]), dz, make_float2(aW1[0][d], aW1[1][d]));
+          aW1[0][d] = t.x;
+          aW1[1][d] = t.y;
+        }
+        const float2 b = __fadd2_rn(make_float2(ab1[0], ab1[1]), dz);
+        ab1[0] = b.x;
+        ab1[1] = b.y;
+        const float2 hh = make_float2(hv[0], hv[1]);
 #pragma unroll
-        for (int d = 0; d < D; ++d) aW1[q][d] = fmaf(ogv[d], dz, aW1[q][d]);
-        ab1[q] += dz;
+        for (int j = 0; j < N; ++j) {
+          const float2 t = __ffma2_rn(hh, make_float2(ogv[D + j], ogv[D + j]), make_float2(aW2[0][j], aW2[1][j]));
+          aW2[0][j] = t.x;
+          aW2[1][j] = t.y;
+        }
+        const float2 v = __ffma2_rn(hh, dvv, make_float2(awv[0], awv[1]));
+        awv[0] = v.x;
+        awv[1] = v.y;
+      } else {
 #pragma unroll
-        for (int j = 0; j < N; ++j) aW2[q][j] = fmaf(hv[q], ogv[D + j], aW2[q][j]);
-        awv[q] = fmaf(hv[q], dv, awv[q]);
+        for (int q = 0; q < KP; ++q) {
+          float dh = wvk[q] * dv;
+#pragma unroll
+          for (int j = 0; j < N; ++j) dh = fmaf(w2k[q][j], ogv[D + j], dh);
+          const float dz = hv[q] > 0.0f ? dh : 0.0f;
+#pragma unroll
+          for (int d = 0; d < D; ++d) aW1[q][d] = fmaf(ogv[d], dz, aW1[q][d]);
+          ab1[q] += dz;
+#pragma unroll
+          for (int j = 0; j < N; ++j) aW2[q][j] = fmaf(hv[q], ogv[D + j], aW2[q][j]);
+          awv[q] = fmaf(hv[q], dv, awv[q]);
+        }
       }
     }
   }
