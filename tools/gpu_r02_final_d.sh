@@ -1,0 +1,10 @@
+# round-2 final evidence, part D: every bench line on the final code
+mkdir -p gpurun_out/r02_final
+python bench.py > gpurun_out/r02_final/bench_default.log 2>&1; tail -1 gpurun_out/r02_final/bench_default.log > gpurun_out/r02_final/bench_default.jsonl
+python bench.py --impl reference > gpurun_out/r02_final/bench_reference.log 2>&1; tail -1 gpurun_out/r02_final/bench_reference.log > gpurun_out/r02_final/bench_reference.jsonl
+rm -f gpurun_out/r02_final/workloads.jsonl
+for w in C1 C2S C3a C3S C3b C4 C5 D0 C2P C2G C4G C2T C2O C3T C4T C2X C2U; do
+  timeout 600 python bench.py --workload $w --no-cpu-baseline --sustain-s 0.5 > gpurun_out/r02_final/bench_$w.log 2>&1
+  tail -1 gpurun_out/r02_final/bench_$w.log >> gpurun_out/r02_final/workloads.jsonl
+done
+timeout 600 python -m pytest tests/test_gpu_a2c.py -q -k "solved or learns" -s > gpurun_out/r02_final/learning.log 2>&1
