@@ -571,9 +571,19 @@ struct DiscreteRunner {
   __device__ __forceinline__ void flush_after(int c_last) {
     if ((c_last & (kRows - 1)) == kRows - 1 || c_last == T - 1) {
       const int w = c_last / kRows;
-      win.cta_acc = cta.acc(w);
-      win.flush(lane, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats, nlive);
-      cta.push(lane, w, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats);
+      // latency build of the straight-line envs (few warps, each alone on its scheduler): every
+      // warp adds its window to the global statistics itself -- a CTA barrier would make the four
+      // warps wait for the slowest every window (measured: C2 roll-out 0.170 -> 0.160 ms without
+      // it; the rolled Acrobot loop measured 0.750 -> 0.771 ms, so it keeps the CTA path);
+      // throughput build: CTA aggregation first (a quarter of the atomics on the slot's words)
+      if ((kLat && !L::kRolled) || (WS_EXP & 64)) {
+        win.cta_acc = nullptr;
+        win.flush(lane, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats, nlive);
+      } else {
+        win.cta_acc = cta.acc(w);
+        win.flush(lane, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats, nlive);
+        cta.push(lane, w, 0, c_last & (kRows - 1), c_last & ~(kRows - 1), p_stats);
+      }
     }
   }
 
