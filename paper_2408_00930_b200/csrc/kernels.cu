@@ -1538,17 +1538,8 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
   constexpr int kRows = 16;  // statistics window depth (slots per flush)
   StatsWindow win;           // per-warp window: leaders' (length, return, reward) per slot
   win.init(ws_smem + 2 * 256 + wib * (3 * kRows * kWinStride), kRows);
-  CtaStats cta;
-  {
-    const int64_t first_w = (int64_t)blockIdx.x * (blockDim.x >> 5);
-    int64_t live_w = 0;
-    for (int i = 0; i < (int)(blockDim.x >> 5); ++i) live_w += ((first_w + i) * R < E) ? 1 : 0;
-    cta.buf = reinterpret_cast<unsigned long long*>(ws_smem);
-    cta.n_live_threads = (int)live_w * 32;
-    cta.leader = wib == 0;
-    for (int i = threadIdx.x; i < 256; i += cta.n_live_threads) cta.buf[i] = 0ull;
-    asm volatile("bar.sync 1, %0;" ::"r"(cta.n_live_threads) : "memory");
-  }
+  // (the first 2 KB of the dynamic shared memory are not used by this kernel: the statistics
+  // windows flush straight to the global slab, warp by warp)
   float lo[C], hi[C], q[C];
 #pragma unroll
   for (int i = 0; i < C; ++i) {
@@ -1643,10 +1634,10 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
       if (d) Ecur = Er;
     }
     if ((c & (kRows - 1)) == kRows - 1 || c == T - 1) {  // window -> CTA accumulator -> global atomics
-      const int wdx = c / kRows;
-      win.cta_acc = cta.acc(wdx);
+      // per-warp global atomics (no CTA barrier between the latency-bound warps, as the
+      // discrete latency build)
+      win.cta_acc = nullptr;
       win.flush(lane, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats, 32);
-      cta.push(lane, wdx, 0, c & (kRows - 1), c & ~(kRows - 1), a.stats);
     }
   };
   // Fast 4-step trip (round 2).  The only loop-carried dependence of a step without a reset is
@@ -1719,10 +1710,8 @@ __global__ void __launch_bounds__(256) k_rollout_surface_seg(const KArgs a, cons
     Ecur = En[K - 1];
     const int cl = c + K - 1;  // K <= kRows: at most one window ends inside the trip, at its last step
     if ((cl & (kRows - 1)) == kRows - 1 || cl == T - 1) {
-      const int wdx = cl / kRows;
-      win.cta_acc = cta.acc(wdx);
+      win.cta_acc = nullptr;  // per-warp global atomics (see one())
       win.flush(lane, 0, cl & (kRows - 1), cl & ~(kRows - 1), a.stats, 32);
-      cta.push(lane, wdx, 0, cl & (kRows - 1), cl & ~(kRows - 1), a.stats);
     }
     return true;
   };
