@@ -52,12 +52,19 @@ struct GaeDev {
 };
 
 // one row of the recursion for column c (shared by both kernels: identical arithmetic)
+// Branch-free (round 2): the three cases are evaluated and selected, so the only dependence
+// between rows is the FMUL + FADD of the last line; the v_trunc load is predicated.  Each case
+// keeps its own operation order (the values are those of the branching form).
 __device__ __forceinline__ float gae_row(const GaeDev& g, float gl, float r, float v, uint32_t d, float v_next,
                                          float a_next, int64_t i) {
-  if ((d & 1u) || ((d & 2u) && g.v_trunc == nullptr)) return __fsub_rn(r, v);
-  if (d & 2u) return __fsub_rn(__fadd_rn(r, __fmul_rn(g.gamma, __ldg(g.v_trunc + i))), v);
+  const bool trunc = (d & 2u) != 0u, has_vt = g.v_trunc != nullptr;
+  const bool stop = (d & 1u) || (trunc && !has_vt);
+  const float vt = (trunc && has_vt) ? __ldg(g.v_trunc + i) : 0.0f;
+  const float a_stop = __fsub_rn(r, v);
+  const float a_trunc = __fsub_rn(__fadd_rn(r, __fmul_rn(g.gamma, vt)), v);
   const float delta = __fsub_rn(__fadd_rn(r, __fmul_rn(g.gamma, v_next)), v);
-  return __fadd_rn(delta, __fmul_rn(gl, a_next));
+  const float a_run = __fadd_rn(delta, __fmul_rn(gl, a_next));
+  return stop ? a_stop : (trunc ? a_trunc : a_run);
 }
 
 __device__ __forceinline__ void st_cs(float* p, float x) {
