@@ -169,14 +169,15 @@ __global__ void __launch_bounds__(W) k_gae_tma(const __grid_constant__ CUtensorM
       for (int i = 0; i < TC; ++i) dn_next[i] = (nrow0 >= 0) ? __ldg(g.done + (int64_t)(nrow0 + i) * g.E + e) : 0;
     }
     mbar_wait(&sm.full[s], (uint32_t)((q / S) & 1));
+    if (row0 + TC <= g.T) {
+      // full tile (every tile but a ragged last one): no row bounds checks, the element offset
+      // stepped down by one row (C elements) per row instead of recomputed
+      int64_t idx = (int64_t)(row0 + TC - 1) * g.C + c;
 #pragma unroll
-    for (int i = TC - 1; i >= 0; --i) {
-      const int t = row0 + i;
-      if (t < g.T) {
+      for (int i = TC - 1; i >= 0; --i) {
         const float r = sm.r[s][i][j];
         const float v = sm.v[s][i][j];
         const uint32_t d = kDoneTma ? sm.d[s][i][j] : dn[i];
-        const int64_t idx = (int64_t)t * g.C + c;
         const float a = gae_row(g, gl, r, v, d, v_next, a_next, idx);
         if (live) {
           st_cs(g.adv + idx, a);
@@ -184,6 +185,25 @@ __global__ void __launch_bounds__(W) k_gae_tma(const __grid_constant__ CUtensorM
         }
         a_next = a;
         v_next = v;
+        idx -= g.C;
+      }
+    } else {
+#pragma unroll
+      for (int i = TC - 1; i >= 0; --i) {
+        const int t = row0 + i;
+        if (t < g.T) {
+          const float r = sm.r[s][i][j];
+          const float v = sm.v[s][i][j];
+          const uint32_t d = kDoneTma ? sm.d[s][i][j] : dn[i];
+          const int64_t idx = (int64_t)t * g.C + c;
+          const float a = gae_row(g, gl, r, v, d, v_next, a_next, idx);
+          if (live) {
+            st_cs(g.adv + idx, a);
+            st_cs(g.ret + idx, __fadd_rn(a, v));
+          }
+          a_next = a;
+          v_next = v;
+        }
       }
     }
     if (!kDoneTma) {
