@@ -86,6 +86,29 @@ __device__ __forceinline__ void load_records(float* wrec, const float* params) {
   }
 }
 
+// The gradient kernel's records, interleaved by unit pairs (round 2): field f of unit k at
+// [(k / 2) * 2 kLen + 2 f + (k & 1)], so one LDS.128 yields two fields of both units of a pair
+// -- the operands of the packed (FFMA2) forward pass.
+template <int D, int N>
+__device__ __forceinline__ int rec_pair_index(int k, int f) {
+  return (k >> 1) * (2 * Rec<D, N>::kLen) + 2 * f + (k & 1);
+}
+template <int D, int H, int N, int G = 0>
+__device__ __forceinline__ void load_records_paired(float* wrec, const float* params) {
+  using RC = Rec<D, N>;
+  const Layout L = layout(D, H, N, G);
+  for (int i = threadIdx.x; i < H * RC::kLen; i += blockDim.x) {
+    const int rem = i % (2 * RC::kLen);
+    const int k = 2 * (i / (2 * RC::kLen)) + (rem & 1), f = rem >> 1;
+    float x = 0.0f;
+    if (f < D) x = __ldg(params + L.oW1 + f * H + k);
+    else if (f == RC::kB1) x = __ldg(params + L.ob1 + k);
+    else if (f == RC::kWv) x = __ldg(params + L.owv + k);
+    else if (f < RC::kW2 + N) x = __ldg(params + L.oW2 + k * N + (f - RC::kW2));
+    wrec[i] = x;
+  }
+}
+
 // ------------------------------------------------------------------------------ values
 template <int D, int H, int N>
 __global__ void __launch_bounds__(256) k_ac_values(const float* __restrict__ params, const float* __restrict__ obs,
@@ -202,7 +225,7 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
   float* wrec = sm + S::kW;
   float* hs = sm + S::kHs;
   float* ogs = sm + S::kOgs;
-  load_records<D, H, N, G>(wrec, g.params);
+  load_records_paired<D, H, N, G>(wrec, g.params);
   if (threadIdx.x < N) sm[S::kB2 + threadIdx.x] = __ldg(g.params + L.ob2 + threadIdx.x);
   if (threadIdx.x == N) sm[S::kB2 + N] = __ldg(g.params + L.obv);
   if (G && threadIdx.x < N) sm[S::kB2 + 4 + threadIdx.x] = __ldg(g.params + L.ols + threadIdx.x);
@@ -237,10 +260,10 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
   float w2k[KP][N], wvk[KP];
 #pragma unroll
   for (int q = 0; q < KP; ++q) {
-    const float* rk = wrec + (KP * lane + q) * S::kRec;
-    wvk[q] = rk[RC::kWv];
+    const int k = KP * lane + q;
+    wvk[q] = wrec[rec_pair_index<D, N>(k, RC::kWv)];
 #pragma unroll
-    for (int j = 0; j < N; ++j) w2k[q][j] = rk[RC::kW2 + j];
+    for (int j = 0; j < N; ++j) w2k[q][j] = wrec[rec_pair_index<D, N>(k, RC::kW2 + j)];
   }
 
   const int64_t n_tiles = (g.rows + kTile - 1) / kTile;
@@ -270,32 +293,37 @@ __global__ void __launch_bounds__(kTile, 4) k_a2c_grad(const GradDev g) {
         l1[j] = 0.0f;
       }
       float4* hrow = reinterpret_cast<float4*>(hs + s * S::kHrow);
+      // units in pairs (2m, 2m + 1) as packed fp32 pairs: the even unit accumulates into l0 / v0,
+      // the odd one into l1 / v1, exactly the scalar code's chains (FFMA2 rounds each element as
+      // FFMA does)
 #pragma unroll 2
       for (int kc = 0; kc < H; kc += 4) {
         float h[4];
 #pragma unroll
-        for (int i = 0; i < 4; ++i) {
-          const int k = kc + i;
-          float w[RC::kLen];
-          const float4* rk = reinterpret_cast<const float4*>(wrec + k * S::kRec);
+        for (int pp = 0; pp < 2; ++pp) {
+          const float4* rk = reinterpret_cast<const float4*>(wrec + ((kc >> 1) + pp) * (2 * RC::kLen));
+          float2 w[RC::kLen];  // field f of the pair
 #pragma unroll
-          for (int c = 0; c < RC::kLen / 4; ++c) {
+          for (int c = 0; c < RC::kLen / 2; ++c) {
             const float4 t = rk[c];
-            w[4 * c] = t.x; w[4 * c + 1] = t.y; w[4 * c + 2] = t.z; w[4 * c + 3] = t.w;
+            w[2 * c] = make_float2(t.x, t.y);
+            w[2 * c + 1] = make_float2(t.z, t.w);
           }
-          float z = w[RC::kB1];
+          float2 z = w[RC::kB1];
 #pragma unroll
-          for (int d = 0; d < D; ++d) z = fmaf(w[d], o[d], z);
-          h[i] = fmaxf(z, 0.0f);
-          if (i & 1) {
+          for (int d = 0; d < D; ++d) z = __ffma2_rn(w[d], make_float2(o[d], o[d]), z);
+          const float2 hh = make_float2(fmaxf(z.x, 0.0f), fmaxf(z.y, 0.0f));
+          h[2 * pp] = hh.x;
+          h[2 * pp + 1] = hh.y;
 #pragma unroll
-            for (int j = 0; j < N; ++j) l1[j] = fmaf(w[RC::kW2 + j], h[i], l1[j]);
-            v1 = fmaf(w[RC::kWv], h[i], v1);
-          } else {
-#pragma unroll
-            for (int j = 0; j < N; ++j) l0[j] = fmaf(w[RC::kW2 + j], h[i], l0[j]);
-            v0 = fmaf(w[RC::kWv], h[i], v0);
+          for (int j = 0; j < N; ++j) {
+            const float2 lj = __ffma2_rn(w[RC::kW2 + j], hh, make_float2(l0[j], l1[j]));
+            l0[j] = lj.x;
+            l1[j] = lj.y;
           }
+          const float2 vv = __ffma2_rn(w[RC::kWv], hh, make_float2(v0, v1));
+          v0 = vv.x;
+          v1 = vv.y;
         }
         hrow[kc >> 2] = make_float4(h[0], h[1], h[2], h[3]);
       }
