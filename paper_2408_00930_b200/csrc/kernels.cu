@@ -1879,10 +1879,22 @@ __global__ void __launch_bounds__(128) k_plan_gauss_warp(const KArgs a, const in
   // The chunk's GAUSS draws J0 .. J1-1 are Box-Muller pairs (2p, 2p+1): the warp's 32 lanes
   // each take one pair at a time (one fp64 log / sqrt / sincos per pair, no lane computing a
   // pair twice) and stage the normals in shared memory; the coordinate lanes then read them.
-  __shared__ float zbuf[4][kGaussChunk * DIM];
+  __shared__ __align__(16) float zbuf[4][kGaussChunk * DIM];
   float* const zb = zbuf[(threadIdx.x >> 5) & 3];
   const uint64_t J0 = (t0 + (uint64_t)c_begin) * (uint64_t)DIM, J1 = (t0 + (uint64_t)c_end) * (uint64_t)DIM;
   // one Philox block (two pairs, four normals) per lane and iteration: no block computed twice
+  const int nJ = (int)(J1 - J0);
+  if ((J0 & 3) == 0 && (nJ & 3) == 0) {
+    // aligned chunk (every chunk when D % 4 == 0): whole blocks, 32-bit indices, one 16-byte store
+    const uint64_t b0 = J0 >> 2;
+    for (int kb = lane; kb < (nJ >> 2); kb += 32) {
+      const U4 w = block(key, b0 + (uint64_t)kb, eg, 0, kGauss);
+      float z0, z1, z2, z3;
+      gauss_pair(w, 0, z0, z1);
+      gauss_pair(w, 1, z2, z3);
+      *reinterpret_cast<float4*>(zb + 4 * kb) = make_float4(z0, z1, z2, z3);
+    }
+  } else
   for (uint64_t b = (J0 >> 2) + (uint64_t)lane; b < ((J1 + 3) >> 2); b += 32) {
     const U4 w = block(key, b, eg, 0, kGauss);
     const int64_t i0 = (int64_t)(4 * b) - (int64_t)J0;
