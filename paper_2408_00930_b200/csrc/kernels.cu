@@ -1137,7 +1137,29 @@ __global__ void __launch_bounds__(128) k_plan_gauss(const KArgs a, const int T, 
   uint64_t cur_blk = ~0ull, cur_pair = ~0ull;
   U4 w{0, 0, 0, 0};
   float ze = 0.0f, zo = 0.0f;
-  for (int c = c_begin; c < c_end; ++c) {
+  int c = c_begin;
+  if constexpr (DIM == 1 && !kStrided) {
+    // one action per step: when the chunk starts on a Philox block, four steps per block in
+    // straight-line code (the same draws, values and stores as the general loop below)
+    if (((t0 + (uint64_t)c_begin) & 3) == 0) {
+      const float nan = __int_as_float(0x7fc00000);
+      for (; c + 4 <= c_end; c += 4) {
+        const U4 b = block(key, (t0 + (uint64_t)c) >> 2, eg, 0, kGauss);
+        float zz[4];
+        gauss_pair(b, 0, zz[0], zz[1]);
+        gauss_pair(b, 1, zz[2], zz[3]);
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const size_t idx = (size_t)(c + k) * (size_t)E + (size_t)e;
+          st_cs(p_act + idx, ok ? mean[0] + sd[0] * zz[k] : nan);
+          const double lp = 0.0 + (((-0.5 * (double)zz[k]) * (double)zz[k] - (double)log_std[0]) - kHalfLog2Pi);
+          if (a.write_logp) st_cs(a.logp + idx, ok ? (float)lp : nan);
+        }
+      }
+      any_bad = !ok;
+    }
+  }
+  for (; c < c_end; ++c) {
     if (kStrided) load_head(probs + (int64_t)c * step_stride);
     const uint64_t j0 = (t0 + (uint64_t)c) * (uint64_t)DIM;
     float z[DIM];
