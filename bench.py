@@ -640,6 +640,7 @@ def e2e_pass(run, args, dev, world):
     henv = run.make_env()
     hstats = henv.buffers()["stats"][:T]
     trainer, staged, pol, gae = run.trainer, run.staged, run.pol, run.gae
+    pipelined = False
     if trainer is not None:  # NEXT-N2: one training iteration per step, loss + stats back to the host
         htr = run.make_trainer(henv)
         hl = torch.empty(3, dtype=torch.float64).pin_memory()
@@ -679,6 +680,17 @@ def e2e_pass(run, args, dev, world):
     else:
         hp = torch.from_numpy(run.probs_host).pin_memory()
         hs = torch.empty((T, 4), dtype=torch.int64).pin_memory()
+        if world == 1 and not gae:
+            # the public pipelined host API (ws_rollout_host_submit / _wait, two deep): every step
+            # still copies its pinned inputs H2D and reads its statistics back to the host, but the
+            # next step is submitted before this one's result is awaited
+            def host_steps(n):
+                henv.rollout_host_submit(T, hp, 0)
+                for k in range(n):
+                    if k + 1 < n:
+                        henv.rollout_host_submit(T, hp, (k + 1) & 1)
+                    henv.rollout_host_wait(k & 1)
+            pipelined = True
 
         def host_step():
             if world > 1:  # ws_rollout_host + the statistics all-reduce, then the merged slab to the host
@@ -692,12 +704,18 @@ def e2e_pass(run, args, dev, world):
                 henv.gae_store(T, run.g_vals, run.g_boot, gae[0], gae[1], out=run.g_out)
                 torch.cuda.synchronize(dev)
         h2d, d2h = int(hp.numel() * 4), T * 4 * 8
-    for _ in range(max(args.warmup, 1)):
-        host_step()
-    run.barrier()
-    t0 = time.perf_counter()
-    for _ in range(args.steps):
-        host_step()
+    if pipelined:
+        host_steps(max(args.warmup, 1))
+        run.barrier()
+        t0 = time.perf_counter()
+        host_steps(args.steps)
+    else:
+        for _ in range(max(args.warmup, 1)):
+            host_step()
+        run.barrier()
+        t0 = time.perf_counter()
+        for _ in range(args.steps):
+            host_step()
     e2e_s = time.perf_counter() - t0
     e2e_s = run.max_over_ranks(e2e_s)
     henv.close()
@@ -706,7 +724,8 @@ def e2e_pass(run, args, dev, world):
             "note": ("every rank, " if world > 1 else "") +
                     ("ws_rollout_staged (per-step copies)" if staged else
                      "A2C iteration, loss + stats to pinned host memory" if trainer is not None
-                     else "ws_rollout_policy with pinned weights" if pol else "ws_rollout_host")
+                     else "ws_rollout_policy with pinned weights" if pol else
+                     "ws_rollout_host_submit / _wait (pipelined two deep)" if pipelined else "ws_rollout_host")
                     + (" + ws_gae_store" if gae else "") + (" + NCCL stats all-reduce" if world > 1 else "")
                     + ", host wall clock" + (", max over ranks" if world > 1 else "")}
 

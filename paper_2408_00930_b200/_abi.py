@@ -118,6 +118,8 @@ _SIGS = {
     "ws_registered_env": (C.c_int32, [C.c_char_p]),
     "ws_set_env_data": (C.c_int, [C.c_void_p, C.c_void_p, C.c_void_p]),
     "ws_set_time": (C.c_int, [C.c_void_p, C.c_uint64]),
+    "ws_rollout_host_submit": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p, C.c_int64, C.c_int64, C.c_int64, C.c_int32]),
+    "ws_rollout_host_wait": (C.c_int, [C.c_void_p, C.c_int32, C.c_void_p]),
     "ws_enable_device_clock": (C.c_int, [C.c_void_p, C.c_int32]),
     "ws_pgroup_create": (C.c_int, [C.c_int32, C.c_int32, C.POINTER(C.c_void_p), C.POINTER(ws_ipc_handle)]),
     "ws_pgroup_attach": (C.c_int, [C.c_void_p, C.c_int32, C.POINTER(ws_ipc_handle)]),

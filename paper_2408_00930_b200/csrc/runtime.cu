@@ -112,6 +112,13 @@ struct ws_env {
   float* staging = nullptr;
   int64_t staging_n = 0;
   std::vector<long long> host_stats;
+  // pipelined host roll-outs (ws_rollout_host_submit / _wait): two pinned result slots
+  struct HostSlot {
+    long long* st = nullptr;  // pinned [T_cap][4]
+    cudaEvent_t done = nullptr;
+    int32_t T = 0;
+    bool pending = false;
+  } hslot[2];
   uint64_t launches = 0;
   std::string last_error;
   // optional per-kernel CUDA-event timing (ws_enable_kernel_timing)
@@ -426,6 +433,10 @@ ws_status ws_destroy(ws_env* h) {
     for (auto ev : r.e) cudaEventDestroy(ev);
   }
   peer_release(h);
+  for (auto& hs : h->hslot) {
+    if (hs.st) cudaFreeHost(hs.st);
+    if (hs.done) cudaEventDestroy(hs.done);
+  }
   free_all(h);
   delete h;
   return WS_OK;
@@ -692,6 +703,54 @@ ws_status ws_rollout_host(ws_env* h, int32_t T, const float* host_probs, int64_t
     return cuda_fail(h, e, "D2H stats");
   if ((e = cudaStreamSynchronize(h->stream))) return cuda_fail(h, e, "sync");
   sum_stats(h->host_stats.data(), T, out);
+  return WS_OK;
+}
+
+ws_status ws_rollout_host_submit(ws_env* h, int32_t T, const float* host_probs, int64_t n_probs, int64_t row_stride,
+                                 int64_t step_stride, int32_t slot) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (!host_probs || n_probs < 1 || slot < 0 || slot > 1)
+    return fail(h, WS_ERR_INVALID_ARGUMENT, "host_probs / n_probs / slot (0 or 1)");
+  ws_env::HostSlot& hs = h->hslot[slot];
+  if (hs.pending) return fail(h, WS_ERR_BAD_STATE, "slot has a submission that was not waited for");
+  DeviceGuard g(h->device);
+  cudaError_t e;
+  if (h->staging_n < n_probs) {
+    if (h->staging) return fail(h, WS_ERR_INVALID_ARGUMENT, "n_probs grew beyond the first call's staging size");
+    h->staging = (float*)dev_alloc(h, (size_t)n_probs * sizeof(float), &e);
+    if (e) return cuda_fail(h, e, "alloc staging");
+    h->staging_n = n_probs;
+  }
+  // (same stream: this copy runs after the previous submission's roll-out has read the staging buffer)
+  if ((e = cudaMemcpyAsync(h->staging, host_probs, (size_t)n_probs * sizeof(float), cudaMemcpyHostToDevice, h->stream)))
+    return cuda_fail(h, e, "H2D probs");
+  ws_status s = ws_rollout(h, T, h->staging, row_stride, step_stride);
+  if (s) return s;
+  if (!hs.st) {
+    if ((e = cudaMallocHost(&hs.st, (size_t)h->T_cap * 4 * sizeof(long long))) ||
+        (e = cudaEventCreateWithFlags(&hs.done, cudaEventDisableTiming))) {
+      hs.st = nullptr;
+      return cuda_fail(h, e, "alloc pinned result slot");
+    }
+  }
+  if ((e = cudaMemcpyAsync(hs.st, h->stats, (size_t)T * 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream)) ||
+      (e = cudaEventRecord(hs.done, h->stream)))
+    return cuda_fail(h, e, "D2H stats");
+  hs.T = T;
+  hs.pending = true;
+  return WS_OK;
+}
+
+ws_status ws_rollout_host_wait(ws_env* h, int32_t slot, ws_stats* out) {
+  if (check(h)) return WS_ERR_INVALID_ARGUMENT;
+  if (slot < 0 || slot > 1 || !out) return fail(h, WS_ERR_INVALID_ARGUMENT, "slot (0 or 1) / out");
+  ws_env::HostSlot& hs = h->hslot[slot];
+  if (!hs.pending) return fail(h, WS_ERR_BAD_STATE, "no submission in this slot");
+  DeviceGuard g(h->device);
+  cudaError_t e = cudaEventSynchronize(hs.done);
+  hs.pending = false;
+  if (e) return cuda_fail(h, e, "wait");
+  sum_stats(hs.st, hs.T, out);
   return WS_OK;
 }
 

@@ -171,6 +171,21 @@ class Env:
                                     self._row_stride(host_probs, row_stride), step_stride, C.byref(out)), self._h)
         return out
 
+    def rollout_host_submit(self, T: int, host_probs: torch.Tensor, slot: int, row_stride: Optional[int] = None,
+                            step_stride: int = 0) -> None:
+        """ws_rollout_host_submit: enqueue a host-buffered roll-out into result slot 0 / 1 (pinned
+        host_probs, left unchanged until the matching rollout_host_wait)."""
+        if host_probs.device.type != "cpu" or host_probs.dtype != torch.float32 or not host_probs.is_contiguous():
+            raise WSError(_abi.INVALID_ARGUMENT, "host_probs must be a contiguous float32 CPU tensor")
+        check(lib().ws_rollout_host_submit(self._h, T, _ptr(host_probs), host_probs.numel(),
+                                           self._row_stride(host_probs, row_stride), step_stride, slot), self._h)
+
+    def rollout_host_wait(self, slot: int) -> _abi.ws_stats:
+        """ws_rollout_host_wait: the statistics of the submission in `slot`."""
+        out = _abi.ws_stats()
+        check(lib().ws_rollout_host_wait(self._h, slot, C.byref(out)), self._h)
+        return out
+
     def rollout_staged(self, T: int, host_probs: torch.Tensor, dst: dict, row_stride: Optional[int] = None,
                        step_stride: int = 0) -> dict:
         """NEXT-N3 copy-based baseline (ws.h ws_rollout_staged): the same T steps as rollout(),

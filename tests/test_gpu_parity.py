@@ -479,6 +479,34 @@ def test_rollout_host_e2e(P):
     assert abs(st.sum_return - ref[1]) <= 1e-9 * max(1, ref[1])
 
 
+def test_rollout_host_pipelined_equals_synchronous(P):
+    """ws_rollout_host_submit / _wait (two deep): a chain of six roll-outs with per-step host
+    probabilities (the next submitted before the previous is awaited) returns, roll-out by
+    roll-out, the statistics of ws_rollout_host on an identical handle, and leaves the same live
+    state; waiting on an empty slot or resubmitting a pending one is WS_ERR_BAD_STATE."""
+    E, T, n = 700, 150, 6
+    hp = [torch.from_numpy(W.random_probs(E, 1, 2, seed=300 + k, zero_frac=0.1)).pin_memory() for k in range(n)]
+    a = P.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    b = P.Env(E, 1, "cartpole", SEED, t_capacity=T)
+    got = []
+    a.rollout_host_submit(T, hp[0], 0)
+    for k in range(n):
+        if k + 1 < n:
+            a.rollout_host_submit(T, hp[k + 1], (k + 1) & 1)
+        got.append(a.rollout_host_wait(k & 1))
+    for k in range(n):
+        ref = b.rollout_host(T, hp[k])
+        assert (got[k].episodes, got[k].sum_length, got[k].sum_return) == (ref.episodes, ref.sum_length, ref.sum_return), k
+    for key in ("state", "reset_count", "ep_step", "obs_live"):
+        assert torch.equal(a.buffers()[key], b.buffers()[key]), key
+    with pytest.raises(P.WSError):
+        a.rollout_host_wait(0)
+    a.rollout_host_submit(T, hp[0], 1)
+    with pytest.raises(P.WSError):
+        a.rollout_host_submit(T, hp[0], 1)
+    a.rollout_host_wait(1)
+
+
 def test_unaligned_rollouts_and_chunks(P):
     """Roll-outs whose start step t0 is not a multiple of 4 (prologue / epilogue paths) and
     whose length is not a multiple of 32 (partial statistics windows), chained across calls
