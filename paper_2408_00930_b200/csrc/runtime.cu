@@ -116,9 +116,14 @@ struct ws_env {
   struct HostSlot {
     long long* st = nullptr;  // pinned [T_cap][4]
     cudaEvent_t done = nullptr;
+    float* staging = nullptr;  // device copy of this slot's probabilities
+    cudaEvent_t copied = nullptr, consumed = nullptr;
+    bool used = false;
     int32_t T = 0;
     bool pending = false;
   } hslot[2];
+  int64_t hslot_n = 0;                // probabilities per slot staging buffer
+  cudaStream_t copy_stream = nullptr;  // H2D of the next submission, beside the running roll-out
   uint64_t launches = 0;
   std::string last_error;
   // optional per-kernel CUDA-event timing (ws_enable_kernel_timing)
@@ -436,7 +441,10 @@ ws_status ws_destroy(ws_env* h) {
   for (auto& hs : h->hslot) {
     if (hs.st) cudaFreeHost(hs.st);
     if (hs.done) cudaEventDestroy(hs.done);
+    if (hs.copied) cudaEventDestroy(hs.copied);
+    if (hs.consumed) cudaEventDestroy(hs.consumed);
   }
+  if (h->copy_stream) cudaStreamDestroy(h->copy_stream);
   free_all(h);
   delete h;
   return WS_OK;
@@ -715,23 +723,36 @@ ws_status ws_rollout_host_submit(ws_env* h, int32_t T, const float* host_probs, 
   if (hs.pending) return fail(h, WS_ERR_BAD_STATE, "slot has a submission that was not waited for");
   DeviceGuard g(h->device);
   cudaError_t e;
-  if (h->staging_n < n_probs) {
-    if (h->staging) return fail(h, WS_ERR_INVALID_ARGUMENT, "n_probs grew beyond the first call's staging size");
-    h->staging = (float*)dev_alloc(h, (size_t)n_probs * sizeof(float), &e);
-    if (e) return cuda_fail(h, e, "alloc staging");
-    h->staging_n = n_probs;
+  if (!h->copy_stream) {
+    if ((e = cudaStreamCreateWithFlags(&h->copy_stream, cudaStreamNonBlocking))) return cuda_fail(h, e, "copy stream");
+    for (auto& x : h->hslot)
+      if ((e = cudaEventCreateWithFlags(&x.copied, cudaEventDisableTiming)) ||
+          (e = cudaEventCreateWithFlags(&x.consumed, cudaEventDisableTiming)) ||
+          (e = cudaEventCreateWithFlags(&x.done, cudaEventDisableTiming)))
+        return cuda_fail(h, e, "pipeline events");
   }
-  // (same stream: this copy runs after the previous submission's roll-out has read the staging buffer)
-  if ((e = cudaMemcpyAsync(h->staging, host_probs, (size_t)n_probs * sizeof(float), cudaMemcpyHostToDevice, h->stream)))
-    return cuda_fail(h, e, "H2D probs");
-  ws_status s = ws_rollout(h, T, h->staging, row_stride, step_stride);
-  if (s) return s;
-  if (!hs.st) {
-    if ((e = cudaMallocHost(&hs.st, (size_t)h->T_cap * 4 * sizeof(long long))) ||
-        (e = cudaEventCreateWithFlags(&hs.done, cudaEventDisableTiming))) {
-      hs.st = nullptr;
-      return cuda_fail(h, e, "alloc pinned result slot");
+  if (h->hslot_n < n_probs) {
+    if (h->hslot_n) return fail(h, WS_ERR_INVALID_ARGUMENT, "n_probs grew beyond the first submission's size");
+    for (auto& x : h->hslot) {
+      x.staging = (float*)dev_alloc(h, (size_t)n_probs * sizeof(float), &e);
+      if (e) return cuda_fail(h, e, "alloc staging");
     }
+    h->hslot_n = n_probs;
+  }
+  // H2D of this slot's probabilities on the copy stream, after the roll-out that last read the
+  // slot's staging buffer (two submissions ago) -- it overlaps the roll-out now running
+  if (hs.used && (e = cudaStreamWaitEvent(h->copy_stream, hs.consumed, 0))) return cuda_fail(h, e, "wait consumed");
+  if ((e = cudaMemcpyAsync(hs.staging, host_probs, (size_t)n_probs * sizeof(float), cudaMemcpyHostToDevice,
+                           h->copy_stream)) ||
+      (e = cudaEventRecord(hs.copied, h->copy_stream)) || (e = cudaStreamWaitEvent(h->stream, hs.copied, 0)))
+    return cuda_fail(h, e, "H2D probs");
+  ws_status s = ws_rollout(h, T, hs.staging, row_stride, step_stride);
+  if (s) return s;
+  if ((e = cudaEventRecord(hs.consumed, h->stream))) return cuda_fail(h, e, "record consumed");
+  hs.used = true;
+  if (!hs.st && (e = cudaMallocHost(&hs.st, (size_t)h->T_cap * 4 * sizeof(long long)))) {
+    hs.st = nullptr;
+    return cuda_fail(h, e, "alloc pinned result slot");
   }
   if ((e = cudaMemcpyAsync(hs.st, h->stats, (size_t)T * 4 * sizeof(long long), cudaMemcpyDeviceToHost, h->stream)) ||
       (e = cudaEventRecord(hs.done, h->stream)))
