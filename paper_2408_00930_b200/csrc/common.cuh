@@ -159,6 +159,35 @@ __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
   if (kChecked && !(fabs(x) < 1048576.0)) sincos(x, &s, &c);
 }
 
+#ifdef __CUDACC_RTC__
+// sincos_small (NVRTC programs of the env composer only): the R3 sin / cos of an fp32 angle with
+// |x| <= 0.25 without range reduction -- the Taylor series through x^13 / x^14 (truncation < 3e-21)
+// in Estrin form, rounded once; the same series and evaluation order as the built-in CartPole's
+// sincos_poly (envs.cuh), which keeps its own copy so that the library's constant-bank layout
+// (and with it the roll-out kernels' schedule) is unchanged.  Pinned against the host libm on
+// 40 M angles through CartPole (tests/test_gpu_kernels.py) and through the composer's
+// bit-exact CartPole tests (tests/test_gpu_user_env.py).
+__constant__ double kSinSmall[6] = {1.0 / 6227020800.0, -1.0 / 39916800.0, 1.0 / 362880.0, -1.0 / 5040.0,
+                                    1.0 / 120.0, -1.0 / 6.0};
+__constant__ double kCosSmall[8] = {-1.0 / 87178291200.0, 1.0 / 479001600.0, -1.0 / 3628800.0, 1.0 / 40320.0,
+                                    -1.0 / 720.0, 1.0 / 24.0, -0.5, 1.0};
+__device__ __forceinline__ void sincos_small(float th, float& s, float& c) {
+  const double x = (double)th, z = x * x, z2 = z * z;
+  const double ps_hi = fma(z, kSinSmall[0], kSinSmall[1]);   // c13 z + c11
+  const double ps_mid = fma(z, kSinSmall[2], kSinSmall[3]);  // c9 z + c7
+  const double ps_lo = fma(z, kSinSmall[4], kSinSmall[5]);   // c5 z + c3
+  const double ps = fma(z2, fma(z2, ps_hi, ps_mid), ps_lo);
+  const double c_l = fma(z, kCosSmall[6], kCosSmall[7]);     // c2 z + 1
+  const double c_a = fma(z, kCosSmall[4], kCosSmall[5]);     // c6 z + c4
+  const double c_b = fma(z, kCosSmall[2], kCosSmall[3]);     // c10 z + c8
+  const double c_c = fma(z, kCosSmall[0], kCosSmall[1]);     // c14 z + c12
+  const double z4 = z2 * z2;
+  const double cA = fma(z2, c_a, c_l), cB = fma(z2, c_c, c_b);
+  s = (float)fma(x * z, ps, x);
+  c = (float)fma(z4, cB, cA);
+}
+#endif
+
 template <bool kChecked = true>
 __device__ __forceinline__ void sincos_c(float x, float& s, float& c) {
   double sd, cd;
