@@ -105,26 +105,28 @@ __device__ __forceinline__ float u01(uint32_t w) { return (float)(w >> 8) * (1.0
 //
 // sincos64: branch-free fp64 sin and cos for |x| < 2^20 -- Cody-Waite reduction by pi/2
 // with the fdlibm three-part constant (products exact inside the FMAs), quadrant from the
-// 2^52+2^51 rounding trick, Taylor polynomials through r^17 / r^18 on |r| <= pi/4 (truncation
-// < 1e-19) in Estrin form.  Larger |x| (never reached by the dynamics) use libdevice.
+// 2^52+2^51 rounding trick, near-minimax polynomials of degree 13 / 14 on |r| <= pi/4 in Estrin
+// form (Chebyshev interpolation in z = r^2, coefficients from tools/fit_sincos.py; max relative
+// error of the rounded-coefficient polynomials 2.0e-17 / 5.8e-19, i.e. below 0.2 ulp, against
+// 6.4e-18 / 1.3e-18 for the Taylor series through r^17 / r^18 they replace at four fewer DFMAs).
+// Larger |x| (never reached by the dynamics) use libdevice.
 // Pinned against the host libm by tests/test_gpu_kernels.py.
 // ---------------------------------------------------------------------------------------
 // fp64 constants in constant memory: DFMA / DMUL read them through the constant cache
 // instead of re-materialising each 64-bit immediate with two UMOVs per use
-__constant__ double kTrig[24] = {
+__constant__ double kTrig[19] = {
     6.36619772367581382433e-01,  // 0  2/pi
     1.57079632673412561417e+00,  // 1  pi/2, three-part Cody-Waite split (fdlibm)
     6.07710050630396597660e-11,  // 2
     2.02226624871116645580e-21,  // 3
     8.47842766036889956997e-32,  // 4
     6755399441055744.0,          // 5  2^52 + 2^51
-    // sin: s3 .. s17
-    -1.0 / 6.0, 1.0 / 120.0, -1.0 / 5040.0, 1.0 / 362880.0, -1.0 / 39916800.0, 1.0 / 6227020800.0,
-    -1.0 / 1307674368000.0, 1.0 / 355687428096000.0,
-    // cos: c2 .. c18
-    -0.5, 1.0 / 24.0, -1.0 / 720.0, 1.0 / 40320.0, -1.0 / 3628800.0, 1.0 / 479001600.0,
-    -1.0 / 87178291200.0, 1.0 / 20922789888000.0, -1.0 / 6402373705728000.0,
-    0.0};
+    // sin r = r + r^3 P(r^2): P coefficients of z^0 .. z^5
+    -0x1.5555555555555p-3, 0x1.1111111110bb2p-7, -0x1.a01a019e83aaep-13, 0x1.71de37968a100p-19,
+    -0x1.ae600b02b6262p-26, 0x1.5e0b19f8b1451p-33,
+    // cos r = 1 + r^2 Q(r^2): Q coefficients of z^0 .. z^6
+    -0x1.0000000000000p-1, 0x1.5555555555551p-5, -0x1.6c16c16c15d79p-10, 0x1.a01a019de131fp-16,
+    -0x1.27e4f8e4a2e74p-22, 0x1.1eea7f259b344p-29, -0x1.8ff9d439a204ap-37};
 
 // kChecked: |x| >= 2^20 (never reached by the environments' dynamics) falls back to
 // libdevice; callers whose arguments are provably bounded pass false.
@@ -138,18 +140,15 @@ __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
   r = fma(-k, kTrig[3], r);
   r = fma(-k, kTrig[4], r);
   const double z = r * r, z2 = z * z, z4 = z2 * z2;
-  // sin r = r + r^3 (s3 + s5 z + ... + s17 z^7), Estrin
+  // sin r = r + r^3 P(z), cos r = 1 + z Q(z), Estrin
   const double s_a = fma(z, kTrig[7], kTrig[6]);
   const double s_b = fma(z, kTrig[9], kTrig[8]);
   const double s_c = fma(z, kTrig[11], kTrig[10]);
-  const double s_d = fma(z, kTrig[13], kTrig[12]);
-  const double ps = fma(z4, fma(z2, s_d, s_c), fma(z2, s_b, s_a));
-  // cos r = 1 + z (c2 + c4 z + ... + c18 z^8)
-  const double c_a = fma(z, kTrig[15], kTrig[14]);
-  const double c_b = fma(z, kTrig[17], kTrig[16]);
-  const double c_c = fma(z, kTrig[19], kTrig[18]);
-  const double c_d = fma(z, kTrig[21], kTrig[20]);
-  const double pc = fma(z4, fma(z4, kTrig[22], fma(z2, c_d, c_c)), fma(z2, c_b, c_a));
+  const double ps = fma(z4, s_c, fma(z2, s_b, s_a));
+  const double c_a = fma(z, kTrig[13], kTrig[12]);
+  const double c_b = fma(z, kTrig[15], kTrig[14]);
+  const double c_c = fma(z, kTrig[17], kTrig[16]);
+  const double pc = fma(z4, fma(z2, kTrig[18], c_c), fma(z2, c_b, c_a));
   const double sr = fma(r * z, ps, r);
   const double cr = fma(z, pc, 1.0);
   const double s0 = (q & 1) ? cr : sr;
@@ -162,9 +161,9 @@ __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
 #ifdef __CUDACC_RTC__
 // sincos_small (NVRTC programs of the env composer only): the R3 sin / cos of an fp32 angle with
 // |x| <= 0.25 without range reduction -- the Taylor series through x^13 / x^14 (truncation < 3e-21)
-// in Estrin form, rounded once; the same series and evaluation order as the built-in CartPole's
-// sincos_poly (envs.cuh), which keeps its own copy so that the library's constant-bank layout
-// (and with it the roll-out kernels' schedule) is unchanged.  Pinned against the host libm on
+// in Estrin form, rounded once (the built-in CartPole's sincos_poly uses near-minimax polynomials
+// of degree 11 / 10 with the same accuracy; here they measured 3 % slower on C2U, so the composer
+// keeps the series).  Pinned against the host libm on
 // 40 M angles through CartPole (tests/test_gpu_kernels.py) and through the composer's
 // bit-exact CartPole tests (tests/test_gpu_user_env.py).
 __constant__ double kSinSmall[6] = {1.0 / 6227020800.0, -1.0 / 39916800.0, 1.0 / 362880.0, -1.0 / 5040.0,
