@@ -103,8 +103,9 @@ __device__ __forceinline__ float u01(uint32_t w) { return (float)(w >> 8) * (1.0
 // R3 transcendental contract: evaluate in fp64 and round once to fp32 -- the same value
 // (up to a 2^-28-rare double-rounding coincidence) as (float)libm((double)x) on the host.
 //
-// sincos64: branch-free fp64 sin and cos for |x| < 2^20 -- Cody-Waite reduction by pi/2
-// with the fdlibm three-part constant (products exact inside the FMAs), quadrant from the
+// sincos64: branch-free fp64 sin and cos for |x| < 2^20 -- Cody-Waite reduction by pi/2 in
+// three FMAs (x - k p1 exact, k p2 exact; the split's residual, 1e-37 k, is < 2e-25 relative to the
+// smallest |r| an fp32 argument below 2^20 produces: 4.19e-9 at x = 252.8982, k = 161), quadrant from the
 // 2^52+2^51 rounding trick, near-minimax polynomials of degree 13 / 14 on |r| <= pi/4 in Estrin
 // form (Chebyshev interpolation in z = r^2, coefficients from tools/fit_sincos.py; max relative
 // error of the rounded-coefficient polynomials 2.0e-17 / 5.8e-19, i.e. below 0.2 ulp, against
@@ -114,13 +115,12 @@ __device__ __forceinline__ float u01(uint32_t w) { return (float)(w >> 8) * (1.0
 // ---------------------------------------------------------------------------------------
 // fp64 constants in constant memory: DFMA / DMUL read them through the constant cache
 // instead of re-materialising each 64-bit immediate with two UMOVs per use
-__constant__ double kTrig[19] = {
+__constant__ double kTrig[18] = {
     6.36619772367581382433e-01,  // 0  2/pi
-    1.57079632673412561417e+00,  // 1  pi/2, three-part Cody-Waite split (fdlibm)
-    6.07710050630396597660e-11,  // 2
-    2.02226624871116645580e-21,  // 3
-    8.47842766036889956997e-32,  // 4
-    6755399441055744.0,          // 5  2^52 + 2^51
+    1.57079632673412561417e+00,  // 1  p1 (fdlibm pio2_1, 33 bits)   pi/2 = p1 + p2 + p2t
+    6.07710050630396597660e-11,  // 2  p2 (pio2_2, 33 bits)
+    2.02226624879595063154e-21,  // 3  p2t (pio2_2t, the rounded rest; residual 1.0e-37)
+    6755399441055744.0,          // 4  2^52 + 2^51
     // sin r = r + r^3 P(r^2): P coefficients of z^0 .. z^5
     -0x1.5555555555555p-3, 0x1.1111111110bb2p-7, -0x1.a01a019e83aaep-13, 0x1.71de37968a100p-19,
     -0x1.ae600b02b6262p-26, 0x1.5e0b19f8b1451p-33,
@@ -132,23 +132,22 @@ __constant__ double kTrig[19] = {
 // libdevice; callers whose arguments are provably bounded pass false.
 template <bool kChecked = true>
 __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
-  const double kd = fma(x, kTrig[0], kTrig[5]);
-  const double k = kd - kTrig[5];
+  const double kd = fma(x, kTrig[0], kTrig[4]);
+  const double k = kd - kTrig[4];
   const int q = __double2loint(kd);
   double r = fma(-k, kTrig[1], x);
   r = fma(-k, kTrig[2], r);
   r = fma(-k, kTrig[3], r);
-  r = fma(-k, kTrig[4], r);
   const double z = r * r, z2 = z * z, z4 = z2 * z2;
   // sin r = r + r^3 P(z), cos r = 1 + z Q(z), Estrin
-  const double s_a = fma(z, kTrig[7], kTrig[6]);
-  const double s_b = fma(z, kTrig[9], kTrig[8]);
-  const double s_c = fma(z, kTrig[11], kTrig[10]);
+  const double s_a = fma(z, kTrig[6], kTrig[5]);
+  const double s_b = fma(z, kTrig[8], kTrig[7]);
+  const double s_c = fma(z, kTrig[10], kTrig[9]);
   const double ps = fma(z4, s_c, fma(z2, s_b, s_a));
-  const double c_a = fma(z, kTrig[13], kTrig[12]);
-  const double c_b = fma(z, kTrig[15], kTrig[14]);
-  const double c_c = fma(z, kTrig[17], kTrig[16]);
-  const double pc = fma(z4, fma(z2, kTrig[18], c_c), fma(z2, c_b, c_a));
+  const double c_a = fma(z, kTrig[12], kTrig[11]);
+  const double c_b = fma(z, kTrig[14], kTrig[13]);
+  const double c_c = fma(z, kTrig[16], kTrig[15]);
+  const double pc = fma(z4, fma(z2, kTrig[17], c_c), fma(z2, c_b, c_a));
   const double sr = fma(r * z, ps, r);
   const double cr = fma(z, pc, 1.0);
   const double s0 = (q & 1) ? cr : sr;

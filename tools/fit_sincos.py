@@ -71,14 +71,13 @@ def emulate(x, ps_c, pc_c):
         return float(F(a) * F(b))
 
     t = [6.36619772367581382433e-01, 1.57079632673412561417e+00, 6.07710050630396597660e-11,
-         2.02226624871116645580e-21, 8.47842766036889956997e-32, 6755399441055744.0]
-    kd = fma(x, t[0], t[5])
-    k = kd - t[5]
-    q = int(kd - t[5]) & 3
+         2.02226624879595063154e-21, 6755399441055744.0]
+    kd = fma(x, t[0], t[4])
+    k = kd - t[4]
+    q = int(k) & 3
     r = fma(-k, t[1], x)
     r = fma(-k, t[2], r)
     r = fma(-k, t[3], r)
-    r = fma(-k, t[4], r)
     z = mul(r, r)
     z2 = mul(z, z)
     z4 = mul(z2, z2)
