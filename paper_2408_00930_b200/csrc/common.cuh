@@ -128,13 +128,12 @@ __constant__ double kTrig[18] = {
     -0x1.0000000000000p-1, 0x1.5555555555551p-5, -0x1.6c16c16c15d79p-10, 0x1.a01a019de131fp-16,
     -0x1.27e4f8e4a2e74p-22, 0x1.1eea7f259b344p-29, -0x1.8ff9d439a204ap-37};
 
-// kChecked: |x| >= 2^20 (never reached by the environments' dynamics) falls back to
-// libdevice; callers whose arguments are provably bounded pass false.
-template <bool kChecked = true>
-__device__ __forceinline__ void sincos64(double x, double& s, double& c) {
+// sincos64_core: the reduced-argument polynomials sr = sin r, cr = cos r and the quadrant q of x
+// (valid for |x| < 2^20); sincos64 / sincos_c assemble the result from them.
+__device__ __forceinline__ void sincos64_core(double x, double& sr, double& cr, int& q) {
   const double kd = fma(x, kTrig[0], kTrig[4]);
   const double k = kd - kTrig[4];
-  const int q = __double2loint(kd);
+  q = __double2loint(kd);
   double r = fma(-k, kTrig[1], x);
   r = fma(-k, kTrig[2], r);
   r = fma(-k, kTrig[3], r);
@@ -148,8 +147,17 @@ __device__ __forceinline__ void sincos64(double x, double& s, double& c) {
   const double c_b = fma(z, kTrig[14], kTrig[13]);
   const double c_c = fma(z, kTrig[16], kTrig[15]);
   const double pc = fma(z4, fma(z2, kTrig[17], c_c), fma(z2, c_b, c_a));
-  const double sr = fma(r * z, ps, r);
-  const double cr = fma(z, pc, 1.0);
+  sr = fma(r * z, ps, r);
+  cr = fma(z, pc, 1.0);
+}
+
+// kChecked: |x| >= 2^20 (never reached by the environments' dynamics) falls back to
+// libdevice; callers whose arguments are provably bounded pass false.
+template <bool kChecked = true>
+__device__ __forceinline__ void sincos64(double x, double& s, double& c) {
+  double sr, cr;
+  int q;
+  sincos64_core(x, sr, cr, q);
   const double s0 = (q & 1) ? cr : sr;
   const double c0 = (q & 1) ? sr : cr;
   s = (q & 2) ? -s0 : s0;
@@ -186,12 +194,25 @@ __device__ __forceinline__ void sincos_small(float th, float& s, float& c) {
 }
 #endif
 
+// both rounded to fp32 first, then the quadrant's swap (one FSEL each) and sign (one LOP3 on the
+// fp32 bit pattern each): rounding to nearest commutes with both, so the results are those of
+// (float) of sincos64's, with half the select work of the fp64 assembly
 template <bool kChecked = true>
 __device__ __forceinline__ void sincos_c(float x, float& s, float& c) {
-  double sd, cd;
-  sincos64<kChecked>((double)x, sd, cd);
-  s = (float)sd;
-  c = (float)cd;
+  double sr, cr;
+  int q;
+  sincos64_core((double)x, sr, cr, q);
+  const float sf = (float)sr, cf = (float)cr;
+  const float s0 = (q & 1) ? cf : sf;
+  const float c0 = (q & 1) ? sf : cf;
+  s = __int_as_float(__float_as_int(s0) ^ ((q & 2) << 30));
+  c = __int_as_float(__float_as_int(c0) ^ (((q + 1) & 2) << 30));
+  if (kChecked && !(fabsf(x) < 1048576.0f)) {
+    double sd, cd;
+    sincos((double)x, &sd, &cd);
+    s = (float)sd;
+    c = (float)cd;
+  }
 }
 template <bool kChecked = true>
 __device__ __forceinline__ float sin_c(float x) {
