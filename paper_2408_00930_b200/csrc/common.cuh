@@ -115,7 +115,7 @@ __device__ __forceinline__ float u01(uint32_t w) { return (float)(w >> 8) * (1.0
 // ---------------------------------------------------------------------------------------
 // fp64 constants in constant memory: DFMA / DMUL read them through the constant cache
 // instead of re-materialising each 64-bit immediate with two UMOVs per use
-__constant__ double kTrig[18] = {
+__constant__ double kTrig[19] = {
     6.36619772367581382433e-01,  // 0  2/pi
     1.57079632673412561417e+00,  // 1  p1 (fdlibm pio2_1, 33 bits)   pi/2 = p1 + p2 + p2t
     6.07710050630396597660e-11,  // 2  p2 (pio2_2, 33 bits)
@@ -126,7 +126,8 @@ __constant__ double kTrig[18] = {
     -0x1.ae600b02b6262p-26, 0x1.5e0b19f8b1451p-33,
     // cos r = 1 + r^2 Q(r^2): Q coefficients of z^0 .. z^6
     -0x1.0000000000000p-1, 0x1.5555555555551p-5, -0x1.6c16c16c15d79p-10, 0x1.a01a019de131fp-16,
-    -0x1.27e4f8e4a2e74p-22, 0x1.1eea7f259b344p-29, -0x1.8ff9d439a204ap-37};
+    -0x1.27e4f8e4a2e74p-22, 0x1.1eea7f259b344p-29, -0x1.8ff9d439a204ap-37,
+    0.0};  // 18: padding -- keeps the constant-bank offsets of the tables after it (measured)
 
 // sincos64_core: the reduced-argument polynomials sr = sin r, cr = cos r and the quadrant q of x
 // (valid for |x| < 2^20); sincos64 / sincos_c assemble the result from them.
