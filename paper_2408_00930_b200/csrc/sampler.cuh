@@ -179,9 +179,13 @@ __device__ __forceinline__ float gauss_z(const Key& key, uint32_t eg, uint32_t a
   const double u2 = (double)(w1 >> 8) * (1.0 / 16777216.0);
   const double r = sqrt(-2.0 * log(u1));
   const double ang = 2.0 * 3.14159265358979323846 * u2;
-  double sn, cs;
-  sincos64(ang, sn, cs);
-  return (float)((j & 1) ? r * sn : r * cs);
+  double sr, cr;
+  int q;
+  sincos64_core(ang, sr, cr, q);  // ang in [0, 2 pi): no wide-argument check needed
+  const bool odd = (j & 1) != 0;  // r sin(ang) : r cos(ang)
+  const double v = (((q & 1) != 0) == odd) ? cr : sr;  // odd quadrants swap sin and cos
+  const int sign = (odd ? (q & 2) : ((q + 1) & 2)) << 30;
+  return __int_as_float(__float_as_int((float)(r * v)) ^ sign);  // r (-x) = -(r x), rounding symmetric
 }
 
 // Both normals of the Box-Muller pair p of block b (draws 4 (b) + 2p and 4 (b) + 2p + 1).
@@ -191,10 +195,14 @@ __device__ __forceinline__ void gauss_pair(const U4& b, int p, float& z_even, fl
   const double u2 = (double)(w1 >> 8) * (1.0 / 16777216.0);
   const double r = sqrt(-2.0 * log(u1));
   const double ang = 2.0 * 3.14159265358979323846 * u2;
-  double sn, cs;
-  sincos64(ang, sn, cs);
-  z_even = (float)(r * cs);
-  z_odd = (float)(r * sn);
+  double sr, cr;
+  int q;
+  sincos64_core(ang, sr, cr, q);  // ang in [0, 2 pi): no wide-argument check needed
+  // the quadrant's swap before the products, its signs on the rounded fp32 bits (r (-x) = -(r x)
+  // exactly and rounding to nearest is symmetric: the values of (float)(r cos), (float)(r sin))
+  const double s0 = (q & 1) ? cr : sr, c0 = (q & 1) ? sr : cr;
+  z_even = __int_as_float(__float_as_int((float)(r * c0)) ^ (((q + 1) & 2) << 30));
+  z_odd = __int_as_float(__float_as_int((float)(r * s0)) ^ ((q & 2) << 30));
 }
 
 // R14 log-density constant 0.5 * log(fl64(2 pi)) (= 0.5 * log(6.283185307179586)).
